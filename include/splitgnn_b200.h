@@ -1,0 +1,270 @@
+/*
+ * splitgnn-b200 — C ABI of the B200-native split-parallel GNN training step.
+ *
+ * The reference (arXiv 2303.13775 desk-scale package, /root/reference) is a
+ * pure-Python/NumPy library with no FFI; every entry point below REPLACES the
+ * NumPy body of the reference function cited beside it, and is bound from the
+ * Python mirror package `paper_2303_13775_b200` through ctypes (see
+ * INTEGRATION.md for the binding a maintainer adds on the reference side).
+ *
+ * Conventions
+ *   - plain C types only: device pointers are `void*`/typed pointers into
+ *     caller-owned (PyTorch-allocated) CUDA memory, sizes are int64_t;
+ *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*)
+ *     and never synchronises the host;
+ *   - return 0 on success, SG_ERR_ARG (1) for a bad argument, SG_ERR_CUDA (2)
+ *     for a CUDA error; sg_last_error() returns the message;
+ *   - data-dependent errors found on the device (e.g. a sampled vertex outside
+ *     the partition map, scheduler.py:175-178) are reported through
+ *     SgMeta.err, which the host reads with the per-iteration count D2H.
+ */
+#ifndef SPLITGNN_B200_H
+#define SPLITGNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SG_OK 0
+#define SG_ERR_ARG 1
+#define SG_ERR_CUDA 2
+
+#define SG_MAXL 8  /* max GNN layers */
+#define SG_MAXG 16 /* max devices (split parts) */
+
+#define SG_ERR_MISSING_VERTEX 1 /* SgMeta.err bit: scheduler.py:177-178 */
+
+/* Per-iteration split descriptor written by sg_split_run into device memory.
+ * Counts / offsets of the reference's LocalSplit + ShufflePlan
+ * (scheduler.py:24-122). Index conventions: [l] layer 0..L, [l-1] for edge
+ * layers 1..L, [s][o] = holder s -> owner o. */
+typedef struct SgMeta {
+  int32_t L, g, err, dst_grouped;
+  int64_t nV[SG_MAXL + 1];   /* |V^l| */
+  int64_t nE[SG_MAXL];       /* |E^l| at [l-1] */
+  int64_t voff[SG_MAXL + 2]; /* offsets of V^l in the concatenated vertex array */
+  int64_t eoff[SG_MAXL + 1]; /* offsets of E^l at [l-1] */
+  int32_t n_own[SG_MAXL + 1][SG_MAXG];        /* len(owned_gids[l]) per device */
+  int32_t own_off[SG_MAXL + 1][SG_MAXG + 1];  /* exclusive prefix over devices */
+  int32_t n_edge[SG_MAXL][SG_MAXG];           /* per-device edges of layer l at [l-1] */
+  int32_t edge_off[SG_MAXL][SG_MAXG + 1];
+  int32_t n_load[SG_MAXG]; /* len(load_gids) */
+  int32_t load_off[SG_MAXG + 1];
+  int32_t n_uniq[SG_MAXL + 1];               /* distinct reference vertices at l */
+  int32_t n_ref[SG_MAXL + 1][SG_MAXG];       /* len(ref_gids[l]) per holder */
+  int32_t ref_off[SG_MAXL + 1][SG_MAXG + 1]; /* == first pair slot of holder */
+  int32_t cnt[SG_MAXL + 1][SG_MAXG][SG_MAXG];      /* PlanEntry.count (l,s,o) */
+  int32_t pair_off[SG_MAXL + 1][SG_MAXG][SG_MAXG]; /* s-major slot of entry (l,s,o) */
+  int32_t recv_off[SG_MAXL + 1][SG_MAXG + 1];      /* owner o's receive base (o-major) */
+  int32_t recv_in[SG_MAXL + 1][SG_MAXG][SG_MAXG];  /* offset of sender s inside o's block */
+  int32_t npairs[SG_MAXL + 1];                     /* ShufflePlan.pair_count(l) */
+} SgMeta;
+
+/* Byte offsets (inside one caller-allocated workspace) of every split array.
+ * Produced by sg_split_layout from the sample sizes; mirrored in Python. */
+typedef struct SgSplitLayout {
+  int64_t total_bytes;
+  int32_t L, g;
+  int64_t n_vertices;   /* len(PartitionMap.assignment) */
+  int64_t nV[SG_MAXL + 1];
+  int64_t nE[SG_MAXL];
+  int64_t voff[SG_MAXL + 2];
+  int64_t eoff[SG_MAXL + 1];
+  int64_t pbase[SG_MAXL + 2]; /* per-layer base of pair-indexed arrays */
+  int64_t nVtot, nEtot, nPtot;
+  int64_t bm_words;           /* bitmap words per layer (padded) */
+  int64_t pos_tiles, edge_tiles, pair_tiles;
+  /* byte offsets */
+  int64_t o_meta;
+  int64_t o_keys, o_rank, o_grouped;      /* positions multisplit: nVtot + nV0 */
+  int64_t o_ekey, o_egrouped, o_lsrc, o_ldst; /* edges: nEtot */
+  int64_t o_pmask;                        /* u32 per position */
+  int64_t o_bitmap, o_wpre, o_ctot;       /* gid-order ranking (layers 1..L) */
+  int64_t o_uorder;                       /* positions of reference vertices in gid order */
+  int64_t o_refrank;                      /* g * nVtot */
+  int64_t o_contrib;                      /* g * nVtot, -1 = no contribution */
+  int64_t o_pairs, o_pair_hidx, o_sendpos, o_xfer, o_recv_row; /* nPtot each */
+  int64_t o_selfrow;                      /* nVtot, aligned with o_grouped */
+  int64_t o_rowbeg, o_rowend;             /* per-layer local row space: nVtot + nPtot */
+  int64_t o_tiles_pos, o_tiles_edge, o_tiles_pair; /* multisplit tile tables */
+  int64_t o_tilebase_pos, o_tilebase_edge, o_tilebase_pair;
+  int64_t rbase[SG_MAXL + 2]; /* per-layer base of row-space arrays */
+} SgSplitLayout;
+
+/* ---------------------------------------------------------------- library */
+const char* sg_last_error(void);
+const char* sg_version(void);
+unsigned long long sg_launch_count(void); /* kernels launched by this library */
+int sg_device_sm_count(void);
+void sg_struct_sizes(int64_t* out /* [sizeof(SgMeta), sizeof(SgSplitLayout)] */);
+
+/* ---------------------------------------------------------------- splitter
+ * Replaces split_minibatch (scheduler.py:164-254) including _group_by
+ * (:157-161), the cache-filtered load set (:193-203), reference-vertex
+ * ordering by gid (:228-238) and the ShufflePlan entries (:244-252). Computes
+ * the split of ALL g devices from the replicated sample (each rank of a
+ * multi-GPU job runs it on its own copy and keeps its own slice).
+ *
+ * V: int32 concatenated layer vertices (V^0..V^L), esrc/edst: int32
+ * concatenated per-layer edge positions (E^1..E^L). asn: uint8 device of each
+ * global vertex (PartitionMap.assignment, partition.py:20-52). cache_bits:
+ * nullable bitmap of CacheState.global_mask (partition.py:70-75). dst_grouped:
+ * 1 if every layer's edges list each destination's in-edges contiguously
+ * (true for sample_minibatch output, sampling.py:148-169). */
+int sg_split_layout(int32_t L, int32_t g, const int64_t* nV, const int64_t* nE,
+                    int64_t n_vertices, SgSplitLayout* out);
+int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V,
+                 const int32_t* esrc, const int32_t* edst, const uint8_t* asn,
+                 const uint32_t* cache_bits, int32_t dst_grouped, void* stream);
+
+/* Stable LSD radix sort of (key,value) pairs (keys < 2^key_bits), used to
+ * build CSR-by-source for the transpose SpMM (engine.py:263-273) and
+ * CSR-by-destination for unordered samples. n is read from *n_dev (<= n_max).
+ * Workspace from sg_sort_ws_bytes. */
+int64_t sg_sort_ws_bytes(int64_t n_max);
+int sg_sort_pairs(void* ws, int64_t n_max, const int32_t* n_dev, uint32_t* keys,
+                  int32_t* vals, int32_t key_bits, void* stream);
+
+/* Build CSR-by-source of the edges of device d at layers [lmin, L]. Keys are
+ * global rows at l-1 (row_base[l] + own_off[l-1][d] + lsrc); on return
+ * srcbeg/srcend (indexed by that key space) bound runs of `perm` (values are
+ * global edge slots in the split's grouped edge array). */
+int sg_src_csr(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+               int32_t lmin, void* sort_ws, int64_t n_max, int32_t* n_dev,
+               uint32_t* keys, int32_t* perm, int32_t* srcbeg, int32_t* srcend,
+               int64_t n_rows_total, void* stream);
+/* Same for destinations (only needed when the sample is not dst-grouped):
+ * writes rowbeg/rowend of the split workspace, with a permutation array. */
+int sg_dst_csr(void* split_ws, const SgSplitLayout* lay, int32_t d,
+               void* sort_ws, int64_t n_max, int32_t* n_dev, uint32_t* keys,
+               int32_t* perm, void* stream);
+
+/* ---------------------------------------------------------------- feature cache
+ * Replaces SplitExecutor._load_inputs (engine.py:160-167): layer-0 rows of
+ * device d resolve to rows of the GPU-resident partitioned feature cache
+ * (cache_slot[gid] >= 0) or of the miss staging area appended after it
+ * (miss_base + rank in load_gids). */
+int sg_layer0_rows(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                   const int32_t* V, const int32_t* cache_slot, int32_t miss_base,
+                   int32_t* src_row0, void* stream);
+int sg_gather_rows(const float* table, const int32_t* rows, int64_t n_rows, int32_t width,
+                   float* out, void* stream);
+/* Synthetic U[0,1) features (hash of (seed, row, col)), written on the device. */
+int sg_fill_uniform(float* out, int64_t rows, int32_t width, uint64_t seed,
+                    int64_t row0, void* stream);
+
+/* ---------------------------------------------------------------- GraphSAGE
+ * Forward local aggregation (engine.py:180-195, segment_sum/count
+ * models.py:150-175): per local destination row, the sum of h_prev rows over
+ * its in-edges and the edge count. Owned rows go to sums[own_off+q], counts;
+ * reference rows are PACKED into the layer's pair-slot send buffer (width
+ * send_stride >= w+1: sums then count) — the push-to-owner payload. h_prev
+ * rows are addressed through `src_row` when non-null (layer 0: feature cache
+ * indirection), else by global owned row. */
+int sg_sage_agg_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                    const float* h_prev, const int32_t* src_row, int32_t w,
+                    float* sums, float* counts, float* sendbuf, int32_t send_stride,
+                    int64_t max_rows, void* stream);
+/* As sg_sage_agg_fwd for samples whose edges are not grouped by destination:
+ * rowbeg/rowend index `dperm` (from sg_dst_csr). */
+int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                         const float* h_prev, const int32_t* src_row, int32_t w, float* sums,
+                         float* counts, float* sendbuf, int32_t send_stride,
+                         const int32_t* dperm, int64_t max_rows, void* stream);
+/* Owner combine + update (engine.py:197-226): adds the holders' partial
+ * (sum,count) rows from recvbuf in ascending sender order, mean = S/N,
+ * pre = h_self@W_self + mean@W_neigh + b, h = relu(pre) unless final.
+ * Writes mean (n_own x w), counts (combined), h (n_own x dout). */
+int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                   const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                   const float* sums, float* counts, const float* recvbuf, int32_t recv_stride,
+                   const float* w_self, const float* w_neigh, const float* bias,
+                   int32_t final_layer, float* mean, float* h, int64_t max_rows, void* stream);
+/* Backward row pass (engine.py:228-254): d_pre = d_h*[h>0] (or d_h if final);
+ * per-block partial sums of h_self^T d_pre, mean^T d_pre and sum(d_pre)
+ * (reduced later by sg_reduce_partials, deterministic order); optionally
+ * d_self = d_pre W_self^T and d_sums = (d_pre W_neigh^T)/counts. */
+int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                     const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                     const float* d_h, const float* h, int32_t final_layer,
+                     const float* mean, const float* counts,
+                     const float* w_self, const float* w_neigh,
+                     float* partial, int32_t nblocks, float* d_self, float* d_sums,
+                     int64_t max_rows, void* stream);
+/* Transpose SpMM (engine.py:263-273): for each owned row u at l-1,
+ * d_prev[u] = [u is the self row of v] d_self[v] + sum over out-edges of
+ * d_sums_all[dst], where reference destinations read the owners' returned
+ * gradients from bwd_recv[sendpos[...]] (push-from-owner payload). */
+int sg_sage_scatter_bwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                        int32_t w, const float* d_self, const float* d_sums,
+                        const float* bwd_recv, int32_t recv_stride,
+                        const int32_t* perm, const int32_t* srcbeg, const int32_t* srcend,
+                        int64_t key_base, float* d_prev, int64_t max_rows, void* stream);
+
+/* ---------------------------------------------------------------- exchange
+ * Pack / transport helpers for the push-to-owner / push-from-owner rounds
+ * (engine.py:125-156, scatter_shuffle_forward :591-630). Layer-l pair slots
+ * are holder-major (the holders' send buffers back to back); receive slots
+ * are owner-major (xfer maps slot -> receive slot). */
+int sg_xfer_to_owner(const void* split_ws, const SgSplitLayout* lay, int32_t l,
+                     const float* sendbuf, float* recvbuf, int32_t stride, void* stream);
+int sg_xfer_from_owner(const void* split_ws, const SgSplitLayout* lay, int32_t l,
+                       const float* sendbuf_recv_layout, float* recvbuf_pair_layout,
+                       int32_t stride, void* stream);
+/* Owner-side pack of owned rows for push-from-owner: out[recv slot] = rows[recv_row]. */
+int sg_pack_from_owner(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                       const float* rows, int32_t w, float* out, int32_t stride,
+                       int64_t max_slots, void* stream);
+/* Holder-side unpack of a push-from-owner payload into ref-aligned rows. */
+int sg_unpack_refs(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                   const float* recv_pair_layout, int32_t stride, int32_t w, float* out,
+                   int64_t max_rows, void* stream);
+
+/* ---------------------------------------------------------------- loss / optimizer
+ * classifier_loss (models.py:287-302) fused: logits, summed softmax-CE,
+ * d_h = (softmax-onehot) W^T, per-block partials of W-grad, b-grad and loss. */
+int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                const int32_t* V, const int32_t* labels, const float* h, int32_t hid,
+                int32_t ncls, const float* w_cls, const float* b_cls, float* d_h,
+                float* partial, int32_t nblocks, int64_t max_rows, void* stream);
+/* Deterministic reduction of per-block partials: out[k] = sum_b partial[b*n+k]
+ * (ascending b). jobs: n_jobs triples (partial_ptr, nblocks, n, out_ptr) in a
+ * device array of int64 [4*n_jobs]. */
+int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n, void* stream);
+/* allreduce_and_step (engine.py:633-647): grads = sum over devices in device
+ * order (n_dev flat buffers), then p -= lr/num_targets * grads. */
+int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_ptrs, int32_t n_dev,
+               int64_t n, float scale, void* stream);
+
+/* ---------------------------------------------------------------- host-side native code
+ * Synthetic block-planted Chung-Lu power-law graph as an
+ * in-CSR (graph.py:23-128 layout: col = sources of each destination, sorted
+ * within a row). Multithreaded; deterministic in (n, m, blocks, p_local,
+ * gamma, seed) whatever the thread count. Caller allocates n+1 / m. */
+int sg_gen_powerlaw(int64_t n, int64_t m, int32_t blocks, double p_local, double gamma,
+                    uint64_t seed, int32_t threads, int64_t* row_offsets, int32_t* col_indices);
+/* Uniform labels in [0, num_classes) (hash of (seed, v)). */
+int sg_gen_labels(int64_t n, int32_t num_classes, uint64_t seed, int32_t* out);
+/* Host twin of sg_fill_uniform (bit-identical values) for rows row_ids (or
+ * row0.. when row_ids is null). */
+int sg_fill_uniform_host(float* out, int64_t rows, int32_t width, uint64_t seed, int64_t row0,
+                         const int64_t* row_ids);
+/* Native k-hop neighbour sampler with sample_minibatch semantics
+ * (sampling.py:105-177): self-edge first, up to fanout distinct in-neighbours
+ * by partial Fisher-Yates, duplicates and the vertex itself dropped, new
+ * vertices appended in first-seen order; ValueError cases (:128-136) return
+ * SG_ERR_ARG with the reference's message. Counter-based RNG keyed by
+ * (seed, layer, position, draw) so results do not depend on threads. */
+void* sg_sampler_create(int64_t n, const int64_t* row_offsets, const int32_t* col_indices);
+void sg_sampler_destroy(void* h);
+int sg_sampler_run(void* h, const int64_t* targets, int64_t n_targets, const int32_t* fanouts,
+                   int32_t L, uint64_t seed, int32_t threads, int64_t* nV_out /* L+1 */,
+                   int64_t* nE_out /* L */);
+int sg_sampler_fetch(void* h, int32_t* V /* sum nV */, int32_t* esrc, int32_t* edst);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPLITGNN_B200_H */

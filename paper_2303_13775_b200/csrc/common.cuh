@@ -1,0 +1,73 @@
+// Shared definitions for the splitgnn-b200 CUDA library (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "../../include/splitgnn_b200.h"
+
+namespace sg {
+
+extern std::atomic<unsigned long long> g_launches;
+void set_error(const std::string& msg);
+
+#define SG_LAUNCHED() (::sg::g_launches.fetch_add(1, std::memory_order_relaxed))
+
+#define SG_CHECK_LAUNCH(name)                                                  \
+  do {                                                                         \
+    cudaError_t e__ = cudaGetLastError();                                      \
+    if (e__ != cudaSuccess) {                                                  \
+      ::sg::set_error(std::string(name) + ": " + cudaGetErrorString(e__));     \
+      return SG_ERR_CUDA;                                                      \
+    }                                                                          \
+    SG_LAUNCHED();                                                             \
+  } while (0)
+
+#define SG_CUDA(call)                                                          \
+  do {                                                                         \
+    cudaError_t e__ = (call);                                                  \
+    if (e__ != cudaSuccess) {                                                  \
+      ::sg::set_error(std::string(#call) + ": " + cudaGetErrorString(e__));    \
+      return SG_ERR_CUDA;                                                      \
+    }                                                                          \
+  } while (0)
+
+#define SG_REQUIRE(cond, msg)                                                  \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      ::sg::set_error(msg);                                                    \
+      return SG_ERR_ARG;                                                       \
+    }                                                                          \
+  } while (0)
+
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+inline int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+inline int clamp_grid(long long want, int cap) {
+  if (want < 1) return 1;
+  return want > cap ? cap : (int)want;
+}
+
+// Device-side: find d in [0, g) with off[d] <= x < off[d+1] (off non-decreasing).
+__device__ __forceinline__ int find_bucket(const int32_t* off, int g, int x) {
+  int lo = 0, hi = g - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace sg

@@ -1,0 +1,95 @@
+// GPU-resident partitioned feature cache (replaces _load_inputs,
+// engine.py:160-167, and the host loads of transfer_manifest,
+// scheduler.py:324-347).
+//
+// Each device's cache shard holds its own partition's rows (CacheState keeps
+// cached vertices inside the owner partition, partition.py:85-91), so every
+// layer-0 row a device aggregates is a local hit or one of its own misses.
+// Instead of materialising h0 = features[owned_gids[0]], layer 1 reads the
+// shard through a row-index indirection (src_row0), fused into the
+// aggregation's loads.
+#include "common.cuh"
+#include "rng.h"
+
+namespace sg {
+namespace {
+
+__global__ void k_layer0_rows(const SgMeta* __restrict__ meta, int d,
+                              const int32_t* __restrict__ grouped, const int32_t* __restrict__ rank,
+                              const int32_t* __restrict__ V, const int32_t* __restrict__ cache_slot,
+                              int32_t miss_base, int64_t nVtot, int miss_global,
+                              int32_t* __restrict__ src_row0) {
+  const int n = meta->n_own[0][d];
+  const int own0 = meta->own_off[0][d];
+  const int lbase = miss_global ? meta->load_off[d] : 0;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int p = grouped[own0 + q];
+    const int32_t gid = V[p];
+    int32_t slot = cache_slot ? cache_slot[gid] : gid;
+    if (slot < 0) slot = miss_base + lbase + rank[nVtot + p];
+    src_row0[own0 + q] = slot;
+  }
+}
+
+__global__ void k_gather_rows(const float* __restrict__ table, const int32_t* __restrict__ rows,
+                              int64_t n, int w, float* __restrict__ out) {
+  const int64_t total = n * w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / w;
+    const int c = (int)(i - r * w);
+    out[i] = table[(int64_t)rows[r] * w + c];
+  }
+}
+
+__global__ void k_fill_uniform(float* __restrict__ out, int64_t rows, int w, uint64_t seed,
+                               int64_t row0) {
+  const int64_t total = rows * w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / w;
+    const int c = (int)(i - r * w);
+    out[i] = sg_uniform24(seed, (uint64_t)(row0 + r), (uint64_t)c);
+  }
+}
+
+}  // namespace
+
+extern "C" int sg_layer0_rows(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                              const int32_t* V, const int32_t* cache_slot, int32_t miss_base,
+                              int32_t* src_row0, void* stream) {
+  SG_REQUIRE(split_ws && lay, "layer0_rows: null workspace");
+  const char* base = (const char*)split_ws;
+  const SgSplitLayout& y = *lay;
+  SG_REQUIRE(d >= 0 && d < y.g, "layer0_rows: bad device");
+  if (y.nV[0] <= 0) return SG_OK;
+  // miss_base < 0 encodes "per-device staging" (dist mode): staging index is
+  // the rank inside this device's load list; otherwise the global load index.
+  const int miss_global = miss_base >= 0 ? 1 : 0;
+  const int32_t mb = miss_base >= 0 ? miss_base : -miss_base - 1;
+  k_layer0_rows<<<clamp_grid(div_up(y.nV[0], 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
+      (const SgMeta*)(base + y.o_meta), d, (const int32_t*)(base + y.o_grouped),
+      (const int32_t*)(base + y.o_rank), V, cache_slot, mb, y.nVtot, miss_global, src_row0);
+  SG_CHECK_LAUNCH("k_layer0_rows");
+  return SG_OK;
+}
+
+extern "C" int sg_gather_rows(const float* table, const int32_t* rows, int64_t n_rows,
+                              int32_t width, float* out, void* stream) {
+  if (n_rows <= 0 || width <= 0) return SG_OK;
+  k_gather_rows<<<clamp_grid(div_up(n_rows * width, 256), kSMs * 8), 256, 0,
+                  (cudaStream_t)stream>>>(table, rows, n_rows, width, out);
+  SG_CHECK_LAUNCH("k_gather_rows");
+  return SG_OK;
+}
+
+extern "C" int sg_fill_uniform(float* out, int64_t rows, int32_t width, uint64_t seed,
+                               int64_t row0, void* stream) {
+  if (rows <= 0 || width <= 0) return SG_OK;
+  k_fill_uniform<<<clamp_grid(div_up(rows * width, 256), kSMs * 16), 256, 0,
+                   (cudaStream_t)stream>>>(out, rows, width, seed, row0);
+  SG_CHECK_LAUNCH("k_fill_uniform");
+  return SG_OK;
+}
+
+}  // namespace sg

@@ -1,0 +1,221 @@
+// Classifier loss, deterministic gradient reduction and the SGD step.
+//
+//   sg_cls_loss        classifier_loss (models.py:287-302) for the owned target
+//                      rows of one device: logits, summed softmax-CE, d_h and
+//                      per-block partials of dW_cls, db_cls and the loss.
+//   sg_reduce_partials per-block partials -> gradients in ascending block
+//                      order (replaces float atomics: run-to-run bit-identical)
+//   sg_sum_sgd         allreduce_and_step (engine.py:633-647): device-order sum
+//                      then p -= lr/num_targets * g (ModelParams.sgd_step,
+//                      models.py:95-99).
+#include <cstring>
+
+#include "common.cuh"
+
+namespace sg {
+namespace {
+
+constexpr int LTR = 32;  // rows per tile
+constexpr int LMAXACC = 24;
+
+struct LossArgs {
+  int L, d, hid, ncls;
+  int64_t voff_L;
+  const int32_t* V;
+  const int32_t* grouped;
+  const int32_t* labels;
+  const float* h;
+  const float* w;  // [hid][ncls]
+  const float* b;
+  float* d_h;
+  float* partial;
+};
+
+__global__ void __launch_bounds__(256) k_cls_loss(const SgMeta* __restrict__ meta, LossArgs a) {
+  extern __shared__ float smem[];
+  const int hid = a.hid, C = a.ncls, cp = C + 1;
+  float* w_s = smem;                // [hid][C]
+  float* h_s = w_s + hid * C;       // [LTR][hid]
+  float* lg_s = h_s + LTR * hid;    // [LTR][C+1]  logits, then d_logits
+  int* y_s = (int*)(lg_s + LTR * cp);
+  float* loss_s = (float*)(y_s + LTR);
+  for (int i = threadIdx.x; i < hid * C; i += blockDim.x) w_s[i] = a.w[i];
+  const int n = meta->n_own[a.L][a.d];
+  const int own0 = meta->own_off[a.L][a.d];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwc = hid * C;
+  float aw[LMAXACC];
+#pragma unroll
+  for (int k = 0; k < LMAXACC; ++k) aw[k] = 0.f;
+  float ab = 0.f, al = 0.f;
+  const int ntiles = (n + LTR - 1) / LTR;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < LTR * hid; idx += blockDim.x) {
+      const int rr = idx / hid, j = idx - rr * hid;
+      const int q = tile * LTR + rr;
+      h_s[idx] = q < n ? a.h[(int64_t)(own0 + q) * hid + j] : 0.f;
+    }
+    if (threadIdx.x < LTR) {
+      const int q = tile * LTR + threadIdx.x;
+      int y = -1;
+      if (q < n) {
+        const int p = a.grouped[a.voff_L + own0 + q];
+        y = a.labels[a.V[a.voff_L + p]];
+      }
+      y_s[threadIdx.x] = y;
+      loss_s[threadIdx.x] = 0.f;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < LTR * C; idx += blockDim.x) {
+      const int rr = idx / C, c = idx - rr * C;
+      float acc = a.b[c];
+      for (int j = 0; j < hid; ++j) acc = fmaf(h_s[rr * hid + j], w_s[j * C + c], acc);
+      lg_s[rr * cp + c] = acc;
+    }
+    __syncthreads();
+    for (int rr = warp; rr < LTR; rr += 8) {
+      const int y = y_s[rr];
+      if (y < 0) {
+        for (int c = lane; c < C; c += 32) lg_s[rr * cp + c] = 0.f;
+        continue;
+      }
+      float m = -INFINITY;
+      for (int c = lane; c < C; c += 32) m = fmaxf(m, lg_s[rr * cp + c]);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float s = 0.f;
+      for (int c = lane; c < C; c += 32) s += expf(lg_s[rr * cp + c] - m);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const float ly = lg_s[rr * cp + y];
+      __syncwarp();
+      const float inv = 1.0f / s;
+      for (int c = lane; c < C; c += 32) {
+        float p = expf(lg_s[rr * cp + c] - m) * inv;
+        if (c == y) p -= 1.0f;
+        lg_s[rr * cp + c] = p;
+      }
+      if (lane == 0) loss_s[rr] = (m + logf(s)) - ly;
+    }
+    __syncthreads();
+    // d_h = d_logits @ W^T
+    for (int idx = threadIdx.x; idx < LTR * hid; idx += blockDim.x) {
+      const int rr = idx / hid, j = idx - rr * hid;
+      const int q = tile * LTR + rr;
+      if (q >= n) continue;
+      float acc = 0.f;
+      for (int c = 0; c < C; ++c) acc = fmaf(lg_s[rr * cp + c], w_s[j * C + c], acc);
+      a.d_h[(int64_t)(own0 + q) * hid + j] = acc;
+    }
+#pragma unroll
+    for (int k = 0; k < LMAXACC; ++k) {
+      const int idx = threadIdx.x + 256 * k;
+      if (idx < nwc) {
+        const int j = idx / C, c = idx - j * C;
+        float s = aw[k];
+        for (int rr = 0; rr < LTR; ++rr) s = fmaf(h_s[rr * hid + j], lg_s[rr * cp + c], s);
+        aw[k] = s;
+      }
+    }
+    if (threadIdx.x < C)
+      for (int rr = 0; rr < LTR; ++rr) ab += lg_s[rr * cp + threadIdx.x];
+    if (threadIdx.x == 0)
+      for (int rr = 0; rr < LTR; ++rr) al += loss_s[rr];
+  }
+  const int64_t ntot = (int64_t)nwc + C + 1;
+  float* out = a.partial + (int64_t)blockIdx.x * ntot;
+#pragma unroll
+  for (int k = 0; k < LMAXACC; ++k) {
+    const int idx = threadIdx.x + 256 * k;
+    if (idx < nwc) out[idx] = aw[k];
+  }
+  if (threadIdx.x < C) out[nwc + threadIdx.x] = ab;
+  if (threadIdx.x == 0) out[nwc + C] = al;
+}
+
+__global__ void k_reduce_partials(const int64_t* __restrict__ jobs) {
+  const int jb = blockIdx.y;
+  const float* p = (const float*)jobs[4 * jb + 0];
+  const int nb = (int)jobs[4 * jb + 1];
+  const int64_t n = jobs[4 * jb + 2];
+  float* out = (float*)jobs[4 * jb + 3];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < nb; ++b) s += p[(int64_t)b * n + k];
+    out[k] = s;
+  }
+}
+
+__global__ void k_sum_sgd(float* __restrict__ params, float* __restrict__ gout,
+                          const int64_t* __restrict__ gptrs, int ndev, int64_t n, float scale) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    float s = ((const float*)gptrs[0])[k];
+    for (int d = 1; d < ndev; ++d) s += ((const float*)gptrs[d])[k];
+    if (gout) gout[k] = s;
+    params[k] -= scale * s;
+  }
+}
+
+}  // namespace
+
+extern "C" int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                           const int32_t* V, const int32_t* labels, const float* h, int32_t hid,
+                           int32_t ncls, const float* w_cls, const float* b_cls, float* d_h,
+                           float* partial, int32_t nblocks, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "cls_loss: null workspace");
+  const char* base = (const char*)split_ws;
+  const SgSplitLayout& y = *lay;
+  SG_REQUIRE(d >= 0 && d < y.g, "cls_loss: bad device");
+  SG_REQUIRE(hid >= 1 && ncls >= 1 && (int64_t)hid * ncls <= 256 * LMAXACC,
+             "cls_loss: hidden*classes > 6144 unsupported");
+  SG_REQUIRE(nblocks >= 1, "cls_loss: nblocks >= 1");
+  (void)max_rows;
+  LossArgs a;
+  memset(&a, 0, sizeof(a));
+  a.L = y.L;
+  a.d = d;
+  a.hid = hid;
+  a.ncls = ncls;
+  a.voff_L = y.voff[y.L];
+  a.V = V;
+  a.grouped = (const int32_t*)(base + y.o_grouped);
+  a.labels = labels;
+  a.h = h;
+  a.w = w_cls;
+  a.b = b_cls;
+  a.d_h = d_h;
+  a.partial = partial;
+  const size_t smem = sizeof(float) * ((size_t)hid * ncls + (size_t)LTR * hid +
+                                       (size_t)LTR * (ncls + 1) + 2 * LTR);
+  SG_REQUIRE(smem <= 227 * 1024, "cls_loss: too large for shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (smem > 48 * 1024)
+    SG_CUDA(cudaFuncSetAttribute(k_cls_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_cls_loss<<<nblocks, 256, smem, st>>>((const SgMeta*)(base + y.o_meta), a);
+  SG_CHECK_LAUNCH("k_cls_loss");
+  return SG_OK;
+}
+
+extern "C" int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n,
+                                  void* stream) {
+  if (n_jobs <= 0 || max_n <= 0) return SG_OK;
+  dim3 grid(clamp_grid(div_up(max_n, 256), kSMs), n_jobs);
+  k_reduce_partials<<<grid, 256, 0, (cudaStream_t)stream>>>(jobs);
+  SG_CHECK_LAUNCH("k_reduce_partials");
+  return SG_OK;
+}
+
+extern "C" int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_ptrs,
+                          int32_t n_dev, int64_t n, float scale, void* stream) {
+  SG_REQUIRE(params && grad_ptrs && n_dev >= 1, "sum_sgd: bad arguments");
+  if (n <= 0) return SG_OK;
+  k_sum_sgd<<<clamp_grid(div_up(n, 256), kSMs * 4), 256, 0, (cudaStream_t)stream>>>(
+      params, grads_out, grad_ptrs, n_dev, n, scale);
+  SG_CHECK_LAUNCH("k_sum_sgd");
+  return SG_OK;
+}
+
+}  // namespace sg

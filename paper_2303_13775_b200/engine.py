@@ -1,0 +1,611 @@
+"""Cooperative split-parallel forward/backward on B200 (engine.py of the reference).
+
+SplitStep is the device-resident hot path: for every local device it launches
+the sm_100a kernels layer by layer, with the push-to-owner / push-from-owner
+rounds handed to a transport (one copy kernel when all devices share this
+GPU, NCCL all-to-all-v when each device is its own process/GPU). No host
+synchronisation happens inside a step except the transports' use of the
+count descriptor, which is fetched once per iteration.
+
+The reference-facing API keeps the reference's names and signatures:
+SplitExecutor (engine.py:95-588), PhaseRunner (:58-79),
+scatter_shuffle_forward (:591-630), allreduce_and_step (:633-647) and
+Trainer / train_model (:655-870).
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+
+from paper_2303_13775_b200 import _lib
+from paper_2303_13775_b200.exchange import LocalTransport
+from paper_2303_13775_b200.features import FeatureStore
+from paper_2303_13775_b200.metrics import EpochMetrics, IterationMetrics, account_transfer
+from paper_2303_13775_b200.models import DeviceParams, ModelParams, init_params
+from paper_2303_13775_b200.partition import CacheState, PartitionMap
+from paper_2303_13775_b200.sampling import epoch_batches, sample_minibatch
+from paper_2303_13775_b200.scheduler import DeviceSplit, split_minibatch
+
+DEBUG_CHECK_FINITE = False
+NB_PARTIAL = 2 * 148  # blocks of the deterministic partial reductions
+
+
+def _r4(x):
+    return (int(x) + 3) // 4 * 4
+
+
+def _f32(n, *shape, device):
+    return torch.empty((max(int(n), 1),) + tuple(shape), dtype=torch.float32, device=device)
+
+
+class SplitStep:
+    """One iteration's forward + backward for `devices` of a DeviceSplit."""
+
+    def __init__(self, dparams: DeviceParams, dsplit: DeviceSplit, feats: FeatureStore,
+                 labels_dev, devices=None, transport=None, exact=True, record_events=False):
+        self.p = dparams
+        self.ds = dsplit
+        self.f = feats
+        self.labels = labels_dev
+        self.g, self.L = dsplit.g, dsplit.L
+        self.devices = list(range(self.g)) if devices is None else list(devices)
+        self.transport = transport or LocalTransport()
+        self.meta = dsplit.host_meta() if exact else None
+        self.dev = dsplit.device
+        self.kind = dparams.kind
+        if self.kind != "graphsage":
+            from paper_2303_13775_b200 import gat  # noqa: F401  (GAT path)
+        self.h = [None] * (self.L + 1)
+        self.keep = [None] * (self.L + 1)
+        self.grads = None
+        self.events = {} if record_events else None
+        self.wire_bytes = 0
+        self.host_bytes = 0
+
+    # -- size bounds (exact when the count descriptor was fetched) ------------
+    def n_own(self, l, d):
+        return int(self.meta.n_own[l][d]) if self.meta is not None else self.ds.nV[l]
+
+    def n_rows(self, l, d):
+        if self.meta is not None:
+            return int(self.meta.n_own[l][d] + self.meta.n_ref[l][d])
+        return self.ds.nV[l] + self.ds.pair_bound(l)
+
+    def n_recv(self, l, d):
+        if self.meta is not None:
+            return int(self.meta.recv_off[l][d + 1] - self.meta.recv_off[l][d])
+        return self.ds.pair_bound(l)
+
+    def _ev(self, name):
+        if self.events is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.events.setdefault(name, []).append(e)
+        return e
+
+    # -- forward ----------------------------------------------------------------
+    def layer0(self):
+        ds, st = self.ds, _lib.stream_ptr()
+        self.src_row0 = torch.empty(max(ds.nV[0], 1), dtype=torch.int32, device=self.dev)
+        if self.meta is not None and int(self.meta.load_off[self.g]) > 0:
+            self.host_bytes += self.f.stage_misses(ds, self.meta)
+        for d in self.devices:
+            _lib.call("sg_layer0_rows", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(ds.V),
+                      _lib.ptr(self.f.cache_slot), int(self.f.n_cached), _lib.ptr(self.src_row0), st)
+
+    def _dst_perm(self):
+        """CSR-by-destination for samples whose edges are not grouped by dst."""
+        if self.ds.dst_grouped:
+            return None
+        if getattr(self, "_dperm", None) is None:
+            ds, st = self.ds, _lib.stream_ptr()
+            n_max = max(int(ds.lay.nEtot), 1)
+            self._dperm = {}
+            for d in self.devices:
+                ws = torch.empty(int(_lib.load().sg_sort_ws_bytes(n_max)), dtype=torch.uint8, device=self.dev)
+                keys = torch.empty(n_max, dtype=torch.int32, device=self.dev)
+                perm = torch.empty(n_max, dtype=torch.int32, device=self.dev)
+                ndev = torch.empty(1, dtype=torch.int32, device=self.dev)
+                _lib.call("sg_dst_csr", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(ws), n_max, _lib.ptr(ndev),
+                          _lib.ptr(keys), _lib.ptr(perm), st)
+                self._dperm[d] = (perm, ws, keys, ndev)
+        return self._dperm
+
+    def forward(self):
+        if self.kind != "graphsage":
+            from paper_2303_13775_b200.gat import gat_forward
+            return gat_forward(self)
+        ds, p, st = self.ds, self.p, _lib.stream_ptr()
+        self.layer0()
+        dperm = self._dst_perm()
+        self.h[0] = self.f.table
+        for l in range(1, self.L + 1):
+            w, dout = p.layer_dims(l - 1)
+            final = int(l == self.L)
+            h_prev, src_row = (self.f.table, self.src_row0) if l == 1 else (self.h[l - 1], None)
+            nV = ds.nV[l]
+            sums = _f32(nV, w, device=self.dev)
+            counts = _f32(nV, device=self.dev)
+            SW = _r4(w + 1)
+            P = ds.pair_bound(l)
+            send = _f32(P, SW, device=self.dev)
+            recv = _f32(P, SW, device=self.dev)
+            self._ev(f"agg{l}_start")
+            for d in self.devices:
+                if dperm is None:
+                    _lib.call("sg_sage_agg_fwd", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
+                              _lib.ptr(src_row), w, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
+                              SW, self.n_rows(l, d), st)
+                else:
+                    _lib.call("sg_sage_agg_fwd_perm", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
+                              _lib.ptr(src_row), w, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
+                              SW, _lib.ptr(dperm[d][0]), self.n_rows(l, d), st)
+            self._ev(f"agg{l}_end")
+            if self.g > 1 and P > 0:
+                self.transport.to_owner(ds, l, send, recv, SW)
+                if self.meta is not None:
+                    self.wire_bytes += int(self.meta.npairs[l]) * SW * 4
+            mean = _f32(nV, w, device=self.dev)
+            h = _f32(nV, dout, device=self.dev)
+            for d in self.devices:
+                _lib.call("sg_sage_update", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
+                          _lib.ptr(src_row), w, dout, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(recv),
+                          SW, _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
+                          _lib.ptr(p.view(f"layer{l-1}.bias")), final, _lib.ptr(mean), _lib.ptr(h),
+                          self.n_own(l, d), st)
+            self.h[l] = h
+            self.keep[l] = dict(mean=mean, counts=counts)
+            if DEBUG_CHECK_FINITE and not torch.isfinite(h[:nV]).all():
+                raise FloatingPointError(f"non-finite values in graphsage layer {l} output")
+
+    # -- loss + backward -----------------------------------------------------------
+    def _src_csr(self, lmin):
+        ds, st = self.ds, _lib.stream_ptr()
+        n_max = max(int(ds.lay.nEtot - ds.lay.eoff[lmin - 1]), 1)
+        rows = max(sum(ds.nV[l - 1] for l in range(lmin, self.L + 1)), 1)
+        out = {}
+        for d in self.devices:
+            ws = torch.empty(int(_lib.load().sg_sort_ws_bytes(n_max)), dtype=torch.uint8, device=self.dev)
+            keys = torch.empty(n_max, dtype=torch.int32, device=self.dev)
+            perm = torch.empty(n_max, dtype=torch.int32, device=self.dev)
+            ndev = torch.empty(1, dtype=torch.int32, device=self.dev)
+            beg = torch.empty(rows, dtype=torch.int32, device=self.dev)
+            end = torch.empty(rows, dtype=torch.int32, device=self.dev)
+            _lib.call("sg_src_csr", _lib.ptr(ds.ws), ds.lay, d, lmin, _lib.ptr(ws), n_max, _lib.ptr(ndev),
+                      _lib.ptr(keys), _lib.ptr(perm), _lib.ptr(beg), _lib.ptr(end), rows, st)
+            out[d] = (perm, beg, end, ws, keys, ndev)
+        kb, acc = {}, 0
+        for l in range(lmin, self.L + 1):
+            kb[l] = acc
+            acc += ds.nV[l - 1]
+        return out, kb
+
+    def loss(self):
+        ds, p, st = self.ds, self.p, _lib.stream_ptr()
+        L = self.L
+        hid, C = p.hidden, p.num_classes
+        self.grads = {d: torch.zeros(p.n + 1, dtype=torch.float32, device=self.dev) for d in self.devices}
+        self.jobs = []
+        self.d_h = _f32(ds.nV[L], hid, device=self.dev)
+        ncls = hid * C + C + 1
+        self._partials = []
+        for d in self.devices:
+            part = _f32(NB_PARTIAL * ncls, device=self.dev)
+            _lib.call("sg_cls_loss", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(ds.V), _lib.ptr(self.labels),
+                      _lib.ptr(self.h[L]), hid, C, _lib.ptr(p.view("cls.w")), _lib.ptr(p.view("cls.b")),
+                      _lib.ptr(self.d_h), _lib.ptr(part), NB_PARTIAL, self.n_own(L, d), st)
+            self.jobs.append((part, NB_PARTIAL, ncls, self.grads[d], p.offset("cls.w")))
+            self._partials.append(part)
+
+    def backward(self):
+        if self.kind != "graphsage":
+            from paper_2303_13775_b200.gat import gat_backward
+            self.loss()
+            gat_backward(self)
+            self.reduce()
+            return
+        ds, p, st = self.ds, self.p, _lib.stream_ptr()
+        self.loss()
+        csr, kb = self._src_csr(2) if self.L >= 2 else ({}, {})
+        d_h = self.d_h
+        for l in range(self.L, 0, -1):
+            w, dout = p.layer_dims(l - 1)
+            final = int(l == self.L)
+            need_prev = l > 1  # d(loss)/d(features) is never used
+            h_prev, src_row = (self.f.table, self.src_row0) if l == 1 else (self.h[l - 1], None)
+            nV = ds.nV[l]
+            d_self = _f32(nV, w, device=self.dev) if need_prev else None
+            d_sums = _f32(nV, w, device=self.dev) if need_prev else None
+            npart = 2 * w * dout + dout
+            for d in self.devices:
+                part = _f32(NB_PARTIAL * npart, device=self.dev)
+                _lib.call("sg_sage_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
+                          _lib.ptr(src_row), w, dout, _lib.ptr(d_h), _lib.ptr(self.h[l]), final,
+                          _lib.ptr(self.keep[l]["mean"]), _lib.ptr(self.keep[l]["counts"]),
+                          _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
+                          _lib.ptr(part), NB_PARTIAL, _lib.ptr(d_self), _lib.ptr(d_sums),
+                          self.n_own(l, d), st)
+                self.jobs.append((part, NB_PARTIAL, npart, self.grads[d], p.offset(f"layer{l-1}.w_self")))
+                self._partials.append(part)
+            if not need_prev:
+                break
+            SWb = _r4(w)
+            P = ds.pair_bound(l)
+            bsend = _f32(P, SWb, device=self.dev)
+            brecv = _f32(P, SWb, device=self.dev)
+            if self.g > 1 and P > 0:
+                for d in self.devices:
+                    _lib.call("sg_pack_from_owner", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(d_sums), w,
+                              _lib.ptr(bsend), SWb, self.n_recv(l, d), st)
+                self.transport.from_owner(ds, l, bsend, brecv, SWb)
+                if self.meta is not None:
+                    self.wire_bytes += int(self.meta.npairs[l]) * SWb * 4
+            d_prev = _f32(ds.nV[l - 1], w, device=self.dev)
+            for d in self.devices:
+                perm, beg, end = csr[d][:3]
+                _lib.call("sg_sage_scatter_bwd", _lib.ptr(ds.ws), ds.lay, l, d, w, _lib.ptr(d_self),
+                          _lib.ptr(d_sums), _lib.ptr(brecv), SWb, _lib.ptr(perm), _lib.ptr(beg),
+                          _lib.ptr(end), kb[l], _lib.ptr(d_prev), self.n_own(l - 1, d), st)
+            d_h = d_prev
+        self.reduce()
+
+    def reduce(self):
+        """Per-block partials -> per-device flat gradients (+ loss slot)."""
+        jobs = []
+        max_n = 1
+        for part, nb, n, gbuf, off in self.jobs:
+            jobs += [part.data_ptr(), nb, n, gbuf.data_ptr() + 4 * off]
+            max_n = max(max_n, n)
+        host = torch.tensor(jobs, dtype=torch.int64).pin_memory()
+        self._jobs_dev = host.to(self.dev, non_blocking=True)
+        self._jobs_host = host
+        _lib.call("sg_reduce_partials", _lib.ptr(self._jobs_dev), len(self.jobs), max_n,
+                  _lib.stream_ptr())
+
+    def loss_sum_dev(self):
+        return sum(self.grads[d][self.p.n] for d in self.devices)
+
+    def run(self):
+        self.forward()
+        self.backward()
+        return self
+
+
+class PhaseRunner:
+    """Signature-compatible with the reference (engine.py:58-79). Device work
+    is stream-ordered, so phases need no threads; `workers` is accepted and
+    results are identical for any value."""
+
+    def __init__(self, num_devices, workers=1):
+        self.num_devices = num_devices
+        self.workers = max(1, int(workers))
+
+    def each(self, fn):
+        for d in range(self.num_devices):
+            fn(d)
+
+    def close(self):
+        pass
+
+
+# ---- reference-compatible executor --------------------------------------------
+
+_FEATS = {}
+_LABELS = {}
+
+
+def _feature_store(features, cache, device):
+    if isinstance(features, FeatureStore):
+        return features
+    key = (id(features), id(cache))
+    hit = _FEATS.get(key)
+    if hit is not None and hit[0] is features:
+        return hit[1]
+    fs = FeatureStore.from_host(np.asarray(features), cache, device=device)
+    _FEATS.clear()
+    _FEATS[key] = (features, fs)
+    return fs
+
+
+def _labels_dev(labels, device):
+    if isinstance(labels, torch.Tensor):
+        return labels.to(device=device, dtype=torch.int32)
+    hit = _LABELS.get(id(labels))
+    if hit is not None and hit[0] is labels:
+        return hit[1]
+    t = torch.from_numpy(np.asarray(labels, dtype=np.int32)).to(device)
+    _LABELS.clear()
+    _LABELS[id(labels)] = (labels, t)
+    return t
+
+
+class GradDict(dict):
+    """dict name -> float64 ndarray (reference type) that also carries the
+    device-resident fp32 flat gradient for allreduce_and_step."""
+
+    device_flat = None
+
+
+class _StateView:
+    def __init__(self, split):
+        self.split = split
+        self.h = []
+        self.layer = []
+        self.loss_sum = 0.0
+
+
+class SplitExecutor:
+    """engine.py:95-588: SplitExecutor(params, splits, plan, features, labels,
+    runner, record).run() -> (loss_sum, per-device gradient dicts)."""
+
+    def __init__(self, params, splits, plan, features, labels, runner=None, record=None):
+        ds = getattr(splits, "device_split", None) or getattr(plan, "device_split", None)
+        if ds is None:
+            raise TypeError("splits/plan must come from paper_2303_13775_b200.split_minibatch "
+                            "(they carry the device-resident split)")
+        if not isinstance(params, ModelParams):
+            params = ModelParams.from_reference(params)
+        self.params = params
+        self.splits = splits
+        self.plan = plan
+        self.ds = ds
+        self.record = record
+        self.runner = runner
+        self.g = ds.g
+        self.L = params.num_layers
+        self.dparams = DeviceParams.from_host(params, ds.device)
+        self.feats = _feature_store(features, ds.cache, ds.device)
+        self.labels = _labels_dev(labels, ds.device)
+        self.step = SplitStep(self.dparams, ds, self.feats, self.labels)
+        self._states = None
+
+    def forward(self):
+        self.step.forward()
+        self._states = None
+
+    def backward(self):
+        self.step.backward()
+
+    def _meter(self):
+        if self.record is None:
+            return
+        for l in range(1, self.L + 1):
+            d_in, d_out = self.params.layer_dims(l - 1)
+            width = (2 * d_in + 1) if self.params.kind == "graphsage" else (2 * d_out + 8)
+            account_transfer(self.record, "peer", self.ds.pair_count(l) * width * 8)
+        self.record.wire_bytes += self.step.wire_bytes
+
+    def run(self):
+        self.forward()
+        self.backward()
+        self._meter()
+        loss = float(self.step.loss_sum_dev().item())
+        out = []
+        for d in range(self.g):
+            gd = GradDict(self.dparams.grads_to_dict(self.step.grads[d]))
+            gd.device_flat = self.step.grads[d]
+            out.append(gd)
+        for d, st in enumerate(self.states):
+            st.loss_sum = float(self.step.grads[d][self.dparams.n].item())
+        return loss, out
+
+    @property
+    def states(self):
+        """Per-device owned-row activations (reference DeviceState.h / .layer),
+        materialised on demand from the device."""
+        if self._states is None:
+            self._states = _materialise_states(self)
+        return self._states
+
+
+def _materialise_states(ex):
+    ds, st = ex.ds, ex.step
+    m = ds.host_meta()
+    states = []
+    table = ex.feats.table
+    for d in range(ds.g):
+        sv = _StateView(ex.splits[d] if d < len(ex.splits) else None)
+        b0, n0 = int(m.own_off[0][d]), int(m.n_own[0][d])
+        F = table.shape[1]
+        h0 = torch.empty((max(n0, 1), F), dtype=torch.float32, device=ds.device)
+        _lib.call("sg_gather_rows", _lib.ptr(table), _lib.ptr(st.src_row0[b0:]), n0, F, _lib.ptr(h0),
+                  _lib.stream_ptr())
+        sv.h.append(h0[:n0].double().cpu().numpy())
+        sv.layer.append(None)
+        for l in range(1, ds.L + 1):
+            b, n = int(m.own_off[l][d]), int(m.n_own[l][d])
+            sv.h.append(st.h[l][b:b + n].double().cpu().numpy())
+            keep = {}
+            for k, v in (st.keep[l] or {}).items():
+                if k in ("alpha", "pre_e", "w_e"):
+                    eb = int(ds.lay.eoff[l - 1]) + int(m.edge_off[l - 1][d])
+                    keep[k] = v[eb:eb + int(m.n_edge[l - 1][d])].double().cpu().numpy()
+                else:
+                    keep[k] = v[b:b + n].double().cpu().numpy()
+            sv.layer.append(keep)
+        states.append(sv)
+    return states
+
+
+def scatter_shuffle_forward(splits, plan, l, owned_rows, runner=None, record=None):
+    """engine.py:591-630: fill every device's reference rows at layer l from
+    the owners' rows (one push-from-owner round on the GPU)."""
+    ds = getattr(splits, "device_split", None) or getattr(plan, "device_split", None)
+    if ds is None:
+        raise TypeError("splits must come from paper_2303_13775_b200.split_minibatch")
+    m = ds.host_meta()
+    width = 0
+    for r in owned_rows:
+        if np.ndim(r) == 2:
+            width = int(np.shape(r)[1])
+            break
+    if record is not None:
+        account_transfer(record, "peer", int(m.npairs[l]) * width * 8)
+    nV = ds.nV[l]
+    rows = torch.zeros((max(nV, 1), max(width, 1)), dtype=torch.float32, device=ds.device)
+    for d, r in enumerate(owned_rows):
+        n = int(m.n_own[l][d])
+        if n and width:
+            b = int(m.own_off[l][d])
+            rows[b:b + n] = torch.as_tensor(np.asarray(r, dtype=np.float32), device=ds.device)
+    out = []
+    P = ds.pair_bound(l)
+    if ds.g > 1 and P > 0 and width:
+        stride = width
+        bsend = _f32(P, stride, device=ds.device)
+        brecv = _f32(P, stride, device=ds.device)
+        st = _lib.stream_ptr()
+        for d in range(ds.g):
+            _lib.call("sg_pack_from_owner", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(rows), width,
+                      _lib.ptr(bsend), stride, int(m.recv_off[l][d + 1] - m.recv_off[l][d]), st)
+        LocalTransport().from_owner(ds, l, bsend, brecv, stride)
+        refs = _f32(P, width, device=ds.device)
+        for d in range(ds.g):
+            _lib.call("sg_unpack_refs", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(brecv), stride, width,
+                      _lib.ptr(refs), int(m.n_ref[l][d]), st)
+        host = refs.double().cpu().numpy()
+    for d in range(ds.g):
+        n = int(m.n_ref[l][d])
+        if n == 0 or width == 0:
+            out.append(np.zeros((n, width)))
+        else:
+            b = int(m.ref_off[l][d])
+            out.append(host[b:b + n].copy())
+    return out
+
+
+def allreduce_and_step(params, per_device_grads, lr, num_targets):
+    """engine.py:633-647: device-order gradient sum + SGD, on the GPU.
+    Mutates `params` (host ModelParams, reference semantics) and returns the
+    summed gradients."""
+    if isinstance(params, DeviceParams):
+        dp = params
+        host_params = None
+    else:
+        host_params = params if isinstance(params, ModelParams) else ModelParams.from_reference(params)
+        dp = DeviceParams.from_host(host_params)
+    flats = []
+    for gd in per_device_grads:
+        f = getattr(gd, "device_flat", None)
+        if f is None:
+            t = np.concatenate([np.asarray(gd[k], dtype=np.float32).reshape(-1) for k in dp.names])
+            f = torch.from_numpy(t).to(dp.flat.device)
+        flats.append(f)
+    ptrs = torch.tensor([f.data_ptr() for f in flats], dtype=torch.int64).to(dp.flat.device)
+    total = torch.empty(dp.n, dtype=torch.float32, device=dp.flat.device)
+    _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), _lib.ptr(total), _lib.ptr(ptrs), len(flats), dp.n,
+              float(lr) / float(num_targets), _lib.stream_ptr())
+    summed = dp.grads_to_dict(total)
+    if host_params is not None:
+        new = dp.to_host().tensors()
+        for k, v in host_params.tensors().items():
+            v[...] = new[k]
+        if params is not host_params:  # reference object: write back in place
+            _write_back_reference(params, new)
+    return summed
+
+
+def _write_back_reference(params, new):
+    for i, layer in enumerate(params.layers):
+        for k in vars(layer):
+            key = f"layer{i}.{k}"
+            if key in new:
+                getattr(layer, k)[...] = new[key]
+    params.w_cls[...] = new["cls.w"]
+    params.b_cls[...] = new["cls.b"]
+
+
+# ---- training driver (engine.py:655-870) -----------------------------------------
+
+class Trainer:
+    """Drives sample -> split -> cooperative step -> all-reduce + SGD, with the
+    model parameters resident on the GPU for the whole epoch."""
+
+    def __init__(self, graph, pm: PartitionMap, cache: CacheState | None, labels, features=None,
+                 device="cuda"):
+        feats = features if features is not None else graph.features
+        if feats is None:
+            raise ValueError("graph has no features attached")
+        self.graph = graph
+        self.pm = pm
+        self.cache = cache
+        self.labels = np.asarray(labels, dtype=np.int64)
+        self.num_devices = pm.num_devices
+        self.device = torch.device(device)
+        self.feats = feats if isinstance(feats, FeatureStore) else FeatureStore.from_host(feats, cache, device=device)
+        self.labels_dev = _labels_dev(self.labels, self.device)
+
+    def split_step(self, sample, dparams, record=None):
+        ds = DeviceSplit.from_sample(sample, self.pm, self.cache, self.device)
+        step = SplitStep(dparams, ds, self.feats, self.labels_dev)
+        step.run()
+        return step, ds
+
+    def run_epoch(self, mode, params, *, seed, epoch, fanouts, batch_size, lr, workers=1,
+                  train_set=None):
+        if mode not in ("single", "split", "data_parallel"):
+            raise ValueError(f"unknown mode {mode!r}")
+        if mode != "split":
+            raise NotImplementedError(f"mode {mode!r} is outside the B200 hot path (SURVEY §8(f))")
+        g = self.num_devices
+        if train_set is None:
+            train_set = np.arange(self.graph.num_vertices, dtype=np.int64)
+        ss = np.random.SeedSequence([seed, epoch])
+        batches = epoch_batches(train_set, batch_size, np.random.default_rng(ss.spawn(1)[0]))
+        host_params = params if isinstance(params, ModelParams) else ModelParams.from_reference(params)
+        dp = DeviceParams.from_host(host_params, self.device)
+        metrics = EpochMetrics(epoch=epoch, mode=mode, num_devices=g)
+        for it, targets in enumerate(batches):
+            brng = np.random.default_rng(ss.spawn(1)[0])
+            rec = IterationMetrics(iteration=it, mode=mode, num_devices=g)
+            t0 = time.perf_counter()
+            sample = sample_minibatch(self.graph, targets, fanouts, brng)
+            t1 = time.perf_counter()
+            rec.sample_ms = (t1 - t0) * 1e3
+            ds = DeviceSplit.from_sample(sample, self.pm, self.cache, self.device)
+            m = ds.host_meta()
+            t2 = time.perf_counter()
+            rec.split_ms = (t2 - t1) * 1e3
+            account_transfer(rec, "host", int(m.load_off[g]) * self.graph_feat_dim() * 8)
+            step = SplitStep(dp, ds, self.feats, self.labels_dev)
+            step.run()
+            ptrs = torch.tensor([step.grads[d].data_ptr() for d in range(g)], dtype=torch.int64).to(self.device)
+            _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs), g, dp.n,
+                      float(lr) / len(targets), _lib.stream_ptr())
+            loss = sum(float(step.grads[d][dp.n].item()) for d in range(g))
+            for l in range(1, ds.L + 1):
+                d_in, d_out = dp.layer_dims(l - 1)
+                width = (2 * d_in + 1) if dp.kind == "graphsage" else (2 * d_out + 8)
+                account_transfer(rec, "peer", int(m.npairs[l]) * width * 8)
+            rec.wire_bytes = step.wire_bytes
+            rec.edges_per_device = np.array([sum(int(m.n_edge[l][d]) for l in range(ds.L)) for d in range(g)],
+                                            dtype=np.int64)
+            t3 = time.perf_counter()
+            rec.train_ms = (t3 - t2) * 1e3
+            rec.loss = loss / len(targets)
+            metrics.iterations.append(rec)
+        new = dp.to_host().tensors()
+        for k, v in host_params.tensors().items():
+            v[...] = new[k]
+        if params is not host_params:
+            _write_back_reference(params, new)
+        return metrics
+
+    def graph_feat_dim(self):
+        return int(self.feats.feat_dim)
+
+
+def train_model(graph, pm, cache, labels, *, model_kind, num_layers, hidden, fanouts, batch_size,
+                lr, epochs, seed, mode="split", workers=1, train_set=None, num_classes=None):
+    """engine.py:829-870."""
+    if num_classes is None:
+        num_classes = int(np.max(labels)) + 1 if len(labels) else 1
+    trainer = Trainer(graph, pm, cache, labels)
+    params = init_params(model_kind, trainer.graph_feat_dim(), hidden, num_classes, num_layers, seed=seed)
+    records = [trainer.run_epoch(mode, params, seed=seed, epoch=e, fanouts=fanouts, batch_size=batch_size,
+                                 lr=lr, workers=workers, train_set=train_set) for e in range(epochs)]
+    return records, params

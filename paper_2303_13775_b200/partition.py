@@ -1,0 +1,129 @@
+"""Partition map and per-device feature-cache selection.
+
+Mirrors splitgnn.partition's data types (partition.py:20-91) and the cache
+policy build_cache (:358-377). The offline multilevel partitioner itself is
+out of scope for the B200 hot path; range_partition
+gives the contiguous-id map the benchmark configs use.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def max_part_size(n: int, g: int, eps: float) -> int:
+    """Largest allowed per-device vertex count (partition.py:94-99)."""
+    if n == 0:
+        return 0
+    return max(math.ceil(n / g), math.ceil((1.0 + eps) * n / g - 1e-7))
+
+
+@dataclass
+class PartitionMap:
+    assignment: np.ndarray
+    num_devices: int
+    balance_eps: float = 0.05
+
+    def __post_init__(self):
+        self.assignment = np.ascontiguousarray(self.assignment, dtype=np.int64)
+        if self.num_devices < 1:
+            raise ValueError("num_devices must be >= 1")
+        if self.balance_eps < 0:
+            raise ValueError("balance_eps must be >= 0")
+        a = self.assignment
+        if len(a) and (a.min() < 0 or a.max() >= self.num_devices):
+            raise ValueError("device id out of range in assignment")
+        cap = max_part_size(len(a), self.num_devices, self.balance_eps)
+        counts = self.counts()
+        if counts.max(initial=0) > cap:
+            raise ValueError(f"partition violates balance: max part {counts.max()} > cap {cap}")
+        self._dev_u8 = None
+
+    def counts(self):
+        return np.bincount(self.assignment, minlength=self.num_devices)
+
+    def device_vertices(self, d):
+        return np.flatnonzero(self.assignment == d)
+
+    def device_u8(self, device="cuda"):
+        """uint8 copy of the map resident on the GPU (cached)."""
+        import torch
+        if self._dev_u8 is None or str(self._dev_u8.device) != str(torch.device(device)):
+            if self.num_devices > 16:
+                raise ValueError("the B200 splitter supports at most 16 devices")
+            self._dev_u8 = torch.from_numpy(self.assignment.astype(np.uint8)).to(device)
+        return self._dev_u8
+
+
+def range_partition(n: int, g: int) -> PartitionMap:
+    """Contiguous-id map P(v) = floor(v*g/n) (block-aligned)."""
+    return PartitionMap((np.arange(n, dtype=np.int64) * g) // max(n, 1), g, 1.0)
+
+
+@dataclass
+class CacheState:
+    """Per-device cached vertex ids, each inside its own partition
+    (partition.py:55-91)."""
+
+    cached: list
+    capacity_fraction: float
+
+    def __post_init__(self):
+        self.cached = [np.ascontiguousarray(c, dtype=np.int64) for c in self.cached]
+        self._bits = None
+
+    @property
+    def num_devices(self):
+        return len(self.cached)
+
+    def global_mask(self, n):
+        mask = np.zeros(n, dtype=bool)
+        for ids in self.cached:
+            mask[ids] = True
+        return mask
+
+    def device_bits(self, n, device="cuda"):
+        """Global cache mask as a uint32 bitmap on the GPU (cached)."""
+        import torch
+        if self._bits is None:
+            words = (n + 31) // 32
+            mask = np.zeros(words * 32, dtype=bool)
+            mask[:n] = self.global_mask(n)
+            packed = np.packbits(mask, bitorder="little")
+            self._bits = torch.from_numpy(packed.view(np.uint32).copy()).to(device)
+        return self._bits
+
+    def validate(self, pm, n):
+        cap = math.ceil(self.capacity_fraction * n - 1e-9)
+        for d, ids in enumerate(self.cached):
+            if len(ids) > cap:
+                raise ValueError(f"device {d} caches {len(ids)} > capacity {cap}")
+            if len(ids) and np.any(pm.assignment[ids] != d):
+                raise ValueError(f"device {d} caches vertices outside its partition")
+
+
+def build_cache(graph, pm: PartitionMap, capacity_fraction: float) -> CacheState:
+    """Highest in+out degree vertices of each partition, ties by lower id
+    (partition.py:358-377)."""
+    if not (0.0 <= capacity_fraction <= 1.0):
+        raise ValueError("capacity_fraction must be in [0, 1]")
+    n = graph.num_vertices
+    cap = math.ceil(capacity_fraction * n - 1e-9)
+    degree = graph.in_degrees() + graph.out_degrees()
+    cached = []
+    for d in range(pm.num_devices):
+        ids = pm.device_vertices(d)
+        order = np.lexsort((ids, -degree[ids]))
+        cached.append(np.sort(ids[order][:cap]))
+    return CacheState(cached, capacity_fraction)
+
+
+def full_cache(pm: PartitionMap) -> CacheState:
+    """Every partition fully cached on its device (zero host bytes,
+    test_acceptance.py:161-172)."""
+    n = len(pm.assignment)
+    frac = (pm.counts().max() / n) if n else 0.0
+    return CacheState([pm.device_vertices(d) for d in range(pm.num_devices)], float(frac))

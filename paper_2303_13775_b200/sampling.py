@@ -1,0 +1,172 @@
+"""Mini-batch samples and the native k-hop sampler.
+
+MiniBatchSample mirrors splitgnn.sampling.MiniBatchSample (sampling.py:18-102):
+layer_vertices[l] global ids of V^l (l = 0..L, V^l a positional prefix of
+V^(l-1)), layer_edges[l-1] = (src_pos in V^(l-1), dst_pos in V^l).
+sample_minibatch has the reference semantics (sampling.py:118-177) but runs in
+native threaded C++ with a counter-based RNG; parity with the reference is
+established on EXPORTED samples (same sample -> same split and same step).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2303_13775_b200 import _lib
+
+
+@dataclass
+class MiniBatchSample:
+    num_layers: int
+    layer_vertices: list
+    layer_edges: list
+    dst_grouped: bool | None = field(default=None, compare=False)
+
+    @property
+    def targets(self):
+        return self.layer_vertices[self.num_layers]
+
+    def vertices(self, l):
+        return self.layer_vertices[l]
+
+    def edges(self, l):
+        return self.layer_edges[l - 1]
+
+    def num_edges(self, l):
+        return len(self.layer_edges[l - 1][0])
+
+    @property
+    def total_edges(self):
+        return int(sum(len(s) for s, _ in self.layer_edges))
+
+    def sizes(self):
+        nV = [len(v) for v in self.layer_vertices]
+        nE = [len(s) for s, _ in self.layer_edges]
+        return nV, nE
+
+    def is_dst_grouped(self) -> bool:
+        """True when each destination's in-edges are contiguous in every layer
+        (always the case for sampler output: edges are emitted per destination)."""
+        if self.dst_grouped is None:
+            ok = True
+            for _, dst in self.layer_edges:
+                dst = np.asarray(dst)
+                if len(dst) > 1:
+                    starts = np.flatnonzero(np.r_[True, dst[1:] != dst[:-1]])
+                    if len(np.unique(dst[starts])) != len(starts):
+                        ok = False
+                        break
+            self.dst_grouped = ok
+        return bool(self.dst_grouped)
+
+    def packed(self):
+        """(V, esrc, edst) int32 concatenations used by the device splitter."""
+        V = np.concatenate([np.asarray(v, dtype=np.int32) for v in self.layer_vertices])
+        src = np.concatenate([np.asarray(s, dtype=np.int32) for s, _ in self.layer_edges])
+        dst = np.concatenate([np.asarray(d, dtype=np.int32) for _, d in self.layer_edges])
+        return V, src, dst
+
+    def validate(self, num_vertices=None):
+        """sampling.py:68-90."""
+        L = self.num_layers
+        assert len(self.layer_vertices) == L + 1 and len(self.layer_edges) == L
+        for ids in self.layer_vertices:
+            ids = np.asarray(ids)
+            assert len(np.unique(ids)) == len(ids), "duplicate vertex in a layer"
+            if num_vertices is not None and len(ids):
+                assert ids.min() >= 0 and ids.max() < num_vertices
+        for l in range(1, L + 1):
+            lo, hi = np.asarray(self.layer_vertices[l - 1]), np.asarray(self.layer_vertices[l])
+            assert np.array_equal(lo[: len(hi)], hi), "V^(l) must prefix V^(l-1)"
+            src, dst = (np.asarray(a, dtype=np.int64) for a in self.edges(l))
+            assert len(src) == len(dst)
+            if len(src):
+                assert src.min() >= 0 and src.max() < len(lo)
+                assert dst.min() >= 0 and dst.max() < len(hi)
+            key = src * len(hi) + dst
+            assert len(np.unique(key)) == len(key), "duplicate edge in a layer"
+            diag = np.arange(len(hi), dtype=np.int64) * (len(hi) + 1)
+            assert np.isin(diag, key).all(), "missing self-edge"
+
+
+def as_sample(obj) -> MiniBatchSample:
+    """Accept a reference splitgnn MiniBatchSample (duck-typed) or ours."""
+    if isinstance(obj, MiniBatchSample):
+        return obj
+    return MiniBatchSample(int(obj.num_layers), list(obj.layer_vertices), list(obj.layer_edges))
+
+
+class NativeSampler:
+    """Reusable native sampler bound to one graph (keeps O(n) scratch)."""
+
+    def __init__(self, graph, threads=0):
+        self.graph = graph
+        self.threads = int(threads)
+        self._h = _lib.load().sg_sampler_create(int(graph.num_vertices),
+                                                _lib.ptr(graph.row_offsets),
+                                                _lib.ptr(graph.col_indices))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().sg_sampler_destroy(h)
+            self._h = None
+
+    def sample(self, targets, fanouts, seed) -> MiniBatchSample:
+        lib = _lib.load()
+        targets = np.ascontiguousarray(np.asarray(targets, dtype=np.int64))
+        fan = np.ascontiguousarray(np.asarray(list(fanouts), dtype=np.int32))
+        L = len(fan)
+        if L == 0:
+            raise ValueError("fanouts must be non-empty")
+        nV = np.zeros(L + 1, dtype=np.int64)
+        nE = np.zeros(max(L, 1), dtype=np.int64)
+        _lib.check(lib.sg_sampler_run(self._h, _lib.ptr(targets), len(targets), _lib.ptr(fan), L,
+                                      int(seed) & (2**64 - 1), self.threads, _lib.ptr(nV),
+                                      _lib.ptr(nE)), "sample_minibatch")
+        V = np.empty(int(nV.sum()), dtype=np.int32)
+        es = np.empty(int(nE[:L].sum()), dtype=np.int32)
+        ed = np.empty(int(nE[:L].sum()), dtype=np.int32)
+        _lib.check(lib.sg_sampler_fetch(self._h, _lib.ptr(V), _lib.ptr(es), _lib.ptr(ed)),
+                   "sampler_fetch")
+        vo = np.r_[0, np.cumsum(nV)]
+        eo = np.r_[0, np.cumsum(nE[:L])]
+        lv = [V[vo[l]:vo[l + 1]] for l in range(L + 1)]
+        le = [(es[eo[l]:eo[l + 1]], ed[eo[l]:eo[l + 1]]) for l in range(L)]
+        return MiniBatchSample(L, lv, le, dst_grouped=True)
+
+
+_SAMPLERS = {}
+
+
+def sample_minibatch(graph, targets, fanouts, rng) -> MiniBatchSample:
+    """k-hop in-neighbourhood sample (sampling.py:118-177). `rng` is a numpy
+    Generator (one 63-bit draw seeds the native counter-based stream) or an int
+    seed."""
+    targets = np.asarray(targets, dtype=np.int64)
+    if targets.size == 0:
+        raise ValueError("targets must be non-empty")
+    if len(np.unique(targets)) != len(targets):
+        raise ValueError("targets must be distinct")
+    if targets.min() < 0 or targets.max() >= graph.num_vertices:
+        raise ValueError("target id out of range")
+    if not list(fanouts):
+        raise ValueError("fanouts must be non-empty")
+    seed = int(rng) if isinstance(rng, (int, np.integer)) else int(rng.integers(0, 2**63 - 1))
+    key = id(graph)
+    s = _SAMPLERS.get(key)
+    if s is None or s.graph is not graph:
+        s = NativeSampler(graph)
+        _SAMPLERS.clear()
+        _SAMPLERS[key] = s
+    return s.sample(targets, fanouts, seed)
+
+
+def epoch_batches(train_set, batch_size, rng) -> list:
+    """Shuffle and chunk (sampling.py:199-204)."""
+    if batch_size < 1:
+        raise ValueError("batch_size must be >= 1")
+    perm = rng.permutation(np.asarray(train_set, dtype=np.int64))
+    return [perm[i:i + batch_size] for i in range(0, len(perm), batch_size)]

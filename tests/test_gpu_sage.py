@@ -1,0 +1,165 @@
+"""GraphSAGE split-parallel step on the GPU vs the reference (golden) and the
+oracle: activations and gradients within rel 1e-4 (fp32 vs float64), loss
+curve within 1e-3 over 50 steps (BASELINE.json north_star tolerances)."""
+
+import numpy as np
+import pytest
+
+from golden_io import unpack_dict, unpack_sample, unpack_splits
+from helpers import cached_lists, load_golden, random_partition_case, rel_err
+from oracle.coop_oracle import CoopRun, reduce_and_sgd
+from oracle.model_oracle import glorot_params, single_device_run
+from oracle.split_oracle import split_sample
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4          # activations / gradients (fp32 path vs float64 reference)
+LOSS_TOL = 1e-3     # loss curve over 50 steps
+
+
+def _run_fixture(name):
+    import paper_2303_13775_b200 as sg
+    z = load_golden(name)
+    V, E = unpack_sample(z)
+    pm = sg.PartitionMap(z["assignment"], int(z["g"]), 100.0)
+    cl = cached_lists(z)
+    cache = sg.CacheState(cl, 1.0) if cl is not None else None
+    splits, plan = sg.split_minibatch(sg.MiniBatchSample(len(E), V, E), pm, cache)
+    P = unpack_dict(z, "P")
+    L = len(E)
+    kind = str(z["kind"])
+    if kind == "graphsage":
+        layers = [sg.SageLayer(P[f"layer{i}.w_self"], P[f"layer{i}.w_neigh"], P[f"layer{i}.bias"])
+                  for i in range(L)]
+    else:
+        layers = [sg.GatLayer(P[f"layer{i}.w"], P[f"layer{i}.a_src"], P[f"layer{i}.a_dst"])
+                  for i in range(L)]
+    params = sg.ModelParams(kind, layers, P["cls.w"], P["cls.b"])
+    rec = sg.IterationMetrics(iteration=0, mode="split", num_devices=int(z["g"]))
+    ex = sg.SplitExecutor(params, splits, plan, z["features"], z["labels"], sg.PhaseRunner(int(z["g"])), rec)
+    loss, grads = ex.run()
+    return z, ex, loss, grads, rec
+
+
+SAGE_FIXTURES = ["exec_graphsage_0", "exec_graphsage_1", "exec_graphsage_2", "exec_graphsage_3",
+                 "edge_single_cross", "edge_idle_device_graphsage", "workload3_graphsage"]
+
+
+@pytest.mark.parametrize("name", SAGE_FIXTURES)
+def test_sage_matches_reference_golden(name):
+    z, ex, loss, grads, rec = _run_fixture(name)
+    assert abs(loss - float(z["loss_split"])) <= TOL * max(1.0, abs(float(z["loss_split"])))
+    for d in range(int(z["g"])):
+        want = unpack_dict(z, f"G{d}")
+        for k in want:
+            assert rel_err(grads[d][k], want[k]) < TOL, (d, k, rel_err(grads[d][k], want[k]))
+        for l in range(len(ex.states[d].h)):
+            assert rel_err(ex.states[d].h[l], z[f"h_{d}_{l}"]) < TOL, (d, l)
+    assert rec.peer_bytes == int(z["peer_bytes"])  # reference metering formula
+
+
+@pytest.mark.parametrize("g", [1, 2, 4, 8])
+def test_sage_matches_oracle_random(g):
+    import paper_2303_13775_b200 as sg
+    graph, pm, sample, cache = random_partition_case(11 + g, n=5000, m=60000, g=g, batch=128,
+                                                     fanouts=(6, 5, 4), cache_frac=0.2)
+    F = 24
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=3)
+    labels = sg.synthetic_labels(graph.num_vertices, 7, seed=4)
+    params = sg.init_params("graphsage", F, 16, 7, 3, seed=5)
+    splits, plan = sg.split_minibatch(sample, pm, cache)
+    ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+    loss, grads = ex.run()
+    ws, wp = split_sample(sample.layer_vertices, sample.layer_edges, pm.assignment, g, cache.cached)
+    ref = CoopRun(glorot_params("graphsage", F, 16, 7, 3, seed=5), ws, wp, feats.astype(np.float64), labels)
+    rloss, rgrads = ref.run()
+    assert abs(loss - rloss) <= TOL * abs(rloss)
+    for d in range(g):
+        for k in rgrads[d]:
+            assert rel_err(grads[d][k], rgrads[d][k]) < TOL, (d, k)
+        for l in range(4):
+            assert rel_err(ex.states[d].h[l], ref.h[d][l]) < TOL, (d, l)
+
+
+def test_sage_unordered_edges_match():
+    import paper_2303_13775_b200 as sg
+    graph, pm, sample, _ = random_partition_case(21, g=3)
+    rng = np.random.default_rng(1)
+    edges = [tuple(np.asarray(a)[p] for a in e) for e, p in
+             ((e, rng.permutation(len(e[0]))) for e in sample.layer_edges)]
+    sample2 = sg.MiniBatchSample(sample.num_layers, sample.layer_vertices, edges)
+    F = 8
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=1)
+    labels = sg.synthetic_labels(graph.num_vertices, 3, seed=2)
+    params = sg.init_params("graphsage", F, 4, 3, 2, seed=3)
+    s2, p2 = sg.split_minibatch(sample2, pm)
+    loss2, g2 = sg.SplitExecutor(params, s2, p2, feats, labels).run()
+    lr, gr = single_device_run(sample.layer_vertices, sample.layer_edges,
+                               glorot_params("graphsage", F, 4, 3, 2, seed=3), feats.astype(np.float64), labels)
+    assert abs(loss2 - lr) <= TOL * abs(lr)
+    tot = {k: sum(gd[k] for gd in g2) for k in gr}
+    for k in gr:
+        assert rel_err(tot[k], gr[k]) < TOL, k
+
+
+def test_sage_loss_curve_50_steps():
+    import paper_2303_13775_b200 as sg
+    z = load_golden("losscurve_graphsage")
+    P0 = unpack_dict(z, "P0")
+    params = sg.ModelParams("graphsage", [sg.SageLayer(P0[f"layer{i}.w_self"].copy(), P0[f"layer{i}.w_neigh"].copy(),
+                                                       P0[f"layer{i}.bias"].copy()) for i in range(2)],
+                            P0["cls.w"].copy(), P0["cls.b"].copy())
+    pm = sg.PartitionMap(z["assignment"], int(z["g"]), 100.0)
+    cache = sg.CacheState(cached_lists(z), 1.0)
+    losses = []
+    for it in range(int(z["steps"])):
+        sub = {k[len(f"it{it}_"):]: z[k] for k in z.files if k.startswith(f"it{it}_")}
+        V, E = unpack_sample(sub)
+        splits, plan = sg.split_minibatch(sg.MiniBatchSample(len(E), V, E), pm, cache)
+        loss, grads = sg.SplitExecutor(params, splits, plan, z["features"], z["labels"]).run()
+        sg.allreduce_and_step(params, grads, float(z["lr"]), len(V[-1]))
+        losses.append(loss / len(V[-1]))
+    diff = np.abs(np.asarray(losses) - z["losses"])
+    assert diff.max() < LOSS_TOL, diff.max()
+    final = unpack_dict(z, "Pfinal")
+    for k, v in params.tensors().items():
+        assert rel_err(v, final[k]) < 1e-3, k
+
+
+def test_sage_c1_shape_parity():
+    """C1 (100K nodes / 1M edges, F=64, batch 512, fanout [10,10], 2 parts)."""
+    import paper_2303_13775_b200 as sg
+    graph = sg.generate_powerlaw(100_000, 1_000_000, seed=0)
+    pm = sg.range_partition(graph.num_vertices, 2)
+    cache = sg.full_cache(pm)
+    feats = sg.synthetic_features(graph.num_vertices, 64, seed=1)
+    labels = sg.synthetic_labels(graph.num_vertices, 8, seed=2)
+    rng = np.random.default_rng(0)
+    sample = sg.sample_minibatch(graph, rng.choice(graph.num_vertices, 512, replace=False), [10, 10], rng)
+    params = sg.init_params("graphsage", 64, 16, 8, 2, seed=0)
+    splits, plan = sg.split_minibatch(sample, pm, cache)
+    ex = sg.SplitExecutor(params, splits, plan, sg.FeatureStore.from_host(feats, cache), labels)
+    loss, grads = ex.run()
+    ws, wp = split_sample(sample.layer_vertices, sample.layer_edges, pm.assignment, 2, cache.cached)
+    ref = CoopRun(glorot_params("graphsage", 64, 16, 8, 2, seed=0), ws, wp, feats.astype(np.float64), labels)
+    rloss, rgrads = ref.run()
+    assert abs(loss - rloss) <= TOL * abs(rloss)
+    for d in range(2):
+        for k in rgrads[d]:
+            assert rel_err(grads[d][k], rgrads[d][k]) < TOL, (d, k)
+
+
+def test_sage_step_is_deterministic():
+    import paper_2303_13775_b200 as sg
+    graph, pm, sample, cache = random_partition_case(31, g=4, cache_frac=0.5)
+    feats = sg.synthetic_features(graph.num_vertices, 16, seed=1)
+    labels = sg.synthetic_labels(graph.num_vertices, 5, seed=2)
+    params = sg.init_params("graphsage", 16, 16, 5, 2, seed=3)
+    outs = []
+    for _ in range(2):
+        splits, plan = sg.split_minibatch(sample, pm, cache)
+        outs.append(sg.SplitExecutor(params, splits, plan, feats, labels).run())
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), k
