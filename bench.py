@@ -1,0 +1,379 @@
+"""Benchmark: split-parallel GraphSAGE training step on an ogbn-products-shaped
+synthetic power-law graph (BASELINE.json configs[1], "C2").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One process per GPU (torchrun for N>1): split parts g = N, rank r owns part r
+(range partition, fully cached feature shard), NCCL all-to-all-v for the
+push-to-owner / push-from-owner rounds and an NCCL all-reduce of gradients.
+A step = split + layer-0 gather + 3-layer forward + loss + backward + gradient
+reduction + SGD for one 1024-target mini-batch (samples are produced ahead by
+the native sampler, as in the paper's methodology).
+Metric: aggregated edges/s = sum_l |E^l| per sample / step time (engine.py:799-800).
+
+--impl reference times the reference CPU algorithm (oracle/ NumPy port) on
+this host, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# ogbn-products shape
+N_NODES = 2_449_029
+N_EDGES = 61_859_140
+FEAT = 100
+CLASSES = 47
+HIDDEN = 16
+FANOUTS = [15, 10, 5]
+BATCH = 1024
+TRAIN_FRAC = 0.0803
+LR = 0.1
+GRAPH_SEED, FEAT_SEED, LABEL_SEED, TRAIN_SEED, RUN_SEED = 0, 1, 2, 3, 0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline)")
+    return ap.parse_args()
+
+
+def build_workload(threads):
+    import paper_2303_13775_b200 as sg
+    t = time.time()
+    graph = sg.generate_powerlaw(N_NODES, N_EDGES, blocks=64, p_local=0.92, gamma=2.1,
+                                 seed=GRAPH_SEED, threads=threads)
+    labels = sg.synthetic_labels(N_NODES, CLASSES, LABEL_SEED)
+    perm = np.random.default_rng(TRAIN_SEED).permutation(N_NODES)
+    train = np.sort(perm[: int(np.ceil(TRAIN_FRAC * N_NODES))])
+    return graph, labels, train, time.time() - t
+
+
+def make_samples(graph, train, k, batch, threads):
+    import paper_2303_13775_b200 as sg
+    sampler = sg.NativeSampler(graph, threads=threads)
+    ss = np.random.SeedSequence([RUN_SEED, 0])
+    batches = sg.epoch_batches(train, batch, np.random.default_rng(ss.spawn(1)[0]))
+    out = []
+    for i in range(k):
+        tg = batches[i % len(batches)]
+        seed = int(np.random.default_rng(ss.spawn(1)[0]).integers(0, 2**63 - 1))
+        out.append(sampler.sample(tg, FANOUTS, seed))
+    return out, len(batches)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def sage_fwd_bytes(E, R, w):
+    """SURVEY §8(d) SpMM-forward algorithmic bytes (per-edge source-row model)."""
+    return 4 * w * E + 4 * E + 4 * (R + 1) + 4 * (w + 1) * R
+
+
+def cpu_baseline(graph, labels, samples, pm_assign, g, n_iter=2):
+    """Reference algorithm (oracle NumPy port) on this host, 1 thread, on the
+    first n_iter samples of the same workload: split + forward + backward +
+    all-reduce/SGD, float64."""
+    from threadpoolctl import threadpool_limits
+
+    import paper_2303_13775_b200 as sg
+    from oracle.coop_oracle import CoopRun, reduce_and_sgd
+    from oracle.model_oracle import glorot_params
+    from oracle.split_oracle import split_sample
+    params = glorot_params("graphsage", FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED)
+    edges = 0
+    t_total = 0.0
+    with threadpool_limits(limits=1):
+        for smp in samples[:n_iter]:
+            # compact the gids the sample touches (sorted, so gid order is kept)
+            V = [np.asarray(v, dtype=np.int64) for v in smp.layer_vertices]
+            uniq = np.unique(V[0])
+            Vc = [np.searchsorted(uniq, v) for v in V]
+            Ec = [(np.asarray(s, np.int64), np.asarray(d, np.int64)) for s, d in smp.layer_edges]
+            X = sg.synthetic_features(0, FEAT, FEAT_SEED, row_ids=uniq).astype(np.float64)
+            asn = pm_assign[uniq]
+            lab = np.asarray(labels, dtype=np.int64)[uniq]
+            t0 = time.perf_counter()
+            splits, plan = split_sample(Vc, Ec, asn, g, None)
+            run = CoopRun(params, splits, plan, X, lab)
+            _, grads = run.run()
+            reduce_and_sgd(params, grads, LR, len(V[-1]))
+            t_total += time.perf_counter() - t0
+            edges += smp.total_edges
+    return edges / t_total, t_total, n_iter, edges
+
+
+def run_reference_arm(args, rank, world):
+    import torch  # noqa: F401
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    graph, labels, train, _ = build_workload(threads)
+    samples, _ = make_samples(graph, train, args.warmup + args.steps, args.batch, threads)
+    g = args.gpus
+    pm_assign = (np.arange(N_NODES, dtype=np.int64) * g) // N_NODES
+    cpu_baseline(graph, labels, samples[: args.warmup], pm_assign, g, n_iter=args.warmup)
+    rate, secs, n_it, edges = cpu_baseline(graph, labels, samples[args.warmup:], pm_assign, g,
+                                           n_iter=args.steps)
+    line = {
+        "impl": "reference", "metric": "aggregated_edges_per_s", "value": rate, "unit": "edges/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / n_it, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 GraphSAGE-3L mean, products-shape synthetic (2.45M/61.9M, F=100), "
+                               f"batch {args.batch}, fanout {FANOUTS}, g={g}", "model": "graphsage-3l-h16",
+                   "global_batch": args.batch},
+        "cpu_baseline": {"value": rate, "unit": "edges/s", "cores": 1, "kind": "port",
+                         "sample": f"{n_it} C2 iterations (batch {args.batch}), oracle NumPy port of "
+                                   "split_minibatch+SplitExecutor+allreduce_and_step, float64, 1 thread"},
+        "e2e": {"value": rate, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import _lib
+    from paper_2303_13775_b200.engine import SplitStep
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    g = world
+    threads = max(1, (os.cpu_count() or 1) // max(1, world))
+    graph, labels, train, gen_s = build_workload(threads)
+    pm = sg.range_partition(N_NODES, g)
+    part_rows = pm.device_vertices(rank)
+    feats = sg.FeatureStore.synthetic(N_NODES, FEAT, FEAT_SEED,
+                                      row_ids=None if g == 1 else part_rows, device=dev)
+    cache = sg.full_cache(pm)
+    labels_dev = torch.from_numpy(labels).to(dev)
+    n_steps = args.warmup + args.steps
+    samples, iters_per_epoch = make_samples(graph, train, n_steps, args.batch, threads)
+    params = sg.init_params("graphsage", FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED)
+    dp = sg.DeviceParams.from_host(params, dev)
+    transport = sg.NcclTransport(rank, world) if g > 1 else sg.LocalTransport()
+    # device-resident inputs
+    dev_samples = []
+    for s in samples:
+        V, es, ed = s.packed()
+        dev_samples.append((torch.from_numpy(V).to(dev), torch.from_numpy(es).to(dev),
+                            torch.from_numpy(ed).to(dev), s.sizes()))
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    exact = g > 1
+
+    def one_step(i, host=False, record_events=False):
+        if host:
+            ds = sg.DeviceSplit.from_sample(samples[i], pm, cache, dev)
+        else:
+            V, es, ed, (nV, nE) = dev_samples[i]
+            ds = sg.DeviceSplit(V, es, ed, nV, nE, pm, cache, True, dev)
+        step = SplitStep(dp, ds, feats, labels_dev, devices=[rank], transport=transport,
+                         exact=exact, record_events=record_events)
+        step.run()
+        gbuf = step.grads[rank]
+        if g > 1:
+            dist.all_reduce(gbuf)
+        ptrs_h = np.asarray([gbuf.data_ptr()], dtype=np.int64)
+        _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs_h), 1, dp.n,
+                  LR / len(samples[i].targets), _lib.stream_ptr())
+        return step, gbuf, None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        one_step(i)
+    barrier()
+
+    # ---- device-resident timing: per-step CUDA events, L2 flushed between steps
+    agg_ms, step_ms, keep = [], [], []
+    l0 = _lib.launch_count()
+    clocks = ClockSampler(local)
+    with clocks:
+        barrier()
+        t_wall = time.perf_counter()
+        for i in range(args.warmup, n_steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step, gbuf, pd = one_step(i, record_events=True)
+            e1.record()
+            keep.append((e0, e1, step, gbuf, pd))
+        barrier()
+        t_wall = time.perf_counter() - t_wall
+    launches = _lib.launch_count() - l0
+    for e0, e1, step, _, _ in keep:
+        step_ms.append(e0.elapsed_time(e1))
+        a0, a1 = step.events["agg1_start"][0], step.events["agg1_end"][0]
+        agg_ms.append(a0.elapsed_time(a1))
+    my_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([my_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        my_ms = float(t.item())
+    edges = sum(samples[i].total_edges for i in range(args.warmup, n_steps))
+    value = edges / (my_ms / 1e3)
+
+    # ---- end to end through the public API: host sample -> H2D -> step -> D2H loss
+    h2d = 0
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    losses = []
+    for i in range(args.warmup, n_steps):
+        step, gbuf, _ = one_step(i, host=True)
+        losses.append(float(gbuf[dp.n].item()) / len(samples[i].targets))
+        V, es, ed = samples[i].packed()
+        h2d += V.nbytes + es.nbytes + ed.nbytes
+    e1.record()
+    barrier()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = edges / (e2e_ms / 1e3)
+
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            peak_src = "measured"
+        except Exception:
+            peak_src = "fallback"
+        hbm = float(peaks.get("hbm_gbs", 6650.0))
+        s0 = samples[args.warmup]
+        nV, nE = s0.sizes()
+        # dominant kernel: layer-1 SpMM (agg) of this rank's split
+        E1 = np.mean([samples[i].sizes()[1][0] for i in range(args.warmup, n_steps)]) / g
+        R1 = np.mean([samples[i].sizes()[0][1] for i in range(args.warmup, n_steps)]) / g
+        alg = sage_fwd_bytes(E1, R1, FEAT)
+        agg_avg = float(np.mean(agg_ms))
+        achieved = alg / (agg_avg / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "agg1_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        base = None
+        if not args.no_cpu_baseline and not args.profile:
+            rate, secs, n_it, _ = cpu_baseline(graph, labels, samples[args.warmup:], pm.assignment, g, 2)
+            base = {"value": rate, "unit": "edges/s", "cores": 1, "kind": "port",
+                    "sample": f"{n_it} C2 iterations (batch {args.batch}) through the oracle NumPy port of "
+                              f"split_minibatch+SplitExecutor+allreduce_and_step, float64, 1 thread, {secs:.1f}s"}
+        line = {
+            "metric": "aggregated_edges_per_s", "value": value, "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": my_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "C2 GraphSAGE-3L mean, products-shape synthetic power-law "
+                                   "(2.45M nodes / 61.9M edges, F=100, 47 classes), batch "
+                                   f"{args.batch}, fanout {FANOUTS}, hidden 16, split parts g={g}, "
+                                   "range partition, full feature cache",
+                       "model": "graphsage-3l-h16", "global_batch": args.batch, "seq_len": None,
+                       "parallelism": f"split{g}", "l2": "flushed between timed steps (256 MB write, "
+                                                          "outside the per-step events)",
+                       "epoch_iterations": iters_per_epoch,
+                       "epoch_time_s": iters_per_epoch * my_ms / args.steps / 1e3,
+                       "edges_per_step": edges / args.steps, "graph_gen_s": round(gen_s, 1),
+                       "sample_sizes_first": {"V": nV, "E": nE}},
+            "roofline": {"bound": "hbm", "kernel": "k_sage_agg<4,32,1> layer 1 (F=100)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg, "avg_launch_ms": agg_avg,
+                         "share_of_step": agg_avg / (my_ms / args.steps)},
+            "e2e": {"value": e2e, "unit": "edges/s", "h2d_bytes_per_step": h2d // args.steps,
+                    "d2h_bytes_per_step": 4 + (0 if g == 1 else 0), "ms_per_step": e2e_ms / args.steps},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "wall_s_timed": t_wall,
+            "loss_last": losses[-1] if losses else None,
+        }
+        if base is not None:
+            line["cpu_baseline"] = base
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -230,11 +230,12 @@ int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32_t d,
                 int32_t ncls, const float* w_cls, const float* b_cls, float* d_h,
                 float* partial, int32_t nblocks, int64_t max_rows, void* stream);
 /* Deterministic reduction of per-block partials: out[k] = sum_b partial[b*n+k]
- * (ascending b). jobs: n_jobs triples (partial_ptr, nblocks, n, out_ptr) in a
- * device array of int64 [4*n_jobs]. */
+ * (ascending b). jobs: HOST array of n_jobs quadruples (partial device ptr,
+ * nblocks, n, out device ptr), passed to the kernel by value. */
 int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n, void* stream);
 /* allreduce_and_step (engine.py:633-647): grads = sum over devices in device
- * order (n_dev flat buffers), then p -= lr/num_targets * grads. */
+ * order (grad_ptrs: HOST array of n_dev device pointers to flat buffers), then
+ * p -= lr/num_targets * grads; grads_out (nullable) receives the sum. */
 int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_ptrs, int32_t n_dev,
                int64_t n, float scale, void* stream);
 

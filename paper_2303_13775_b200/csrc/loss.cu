@@ -8,6 +8,7 @@
 //   sg_sum_sgd         allreduce_and_step (engine.py:633-647): device-order sum
 //                      then p -= lr/num_targets * g (ModelParams.sgd_step,
 //                      models.py:95-99).
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -134,12 +135,20 @@ __global__ void __launch_bounds__(256) k_cls_loss(const SgMeta* __restrict__ met
   if (threadIdx.x == 0) out[nwc + C] = al;
 }
 
-__global__ void k_reduce_partials(const int64_t* __restrict__ jobs) {
+constexpr int MAXJOBS = 48;
+struct Jobs {
+  int64_t v[4 * MAXJOBS];
+};
+struct DevPtrs {
+  int64_t v[SG_MAXG];
+};
+
+__global__ void k_reduce_partials(Jobs jobs) {
   const int jb = blockIdx.y;
-  const float* p = (const float*)jobs[4 * jb + 0];
-  const int nb = (int)jobs[4 * jb + 1];
-  const int64_t n = jobs[4 * jb + 2];
-  float* out = (float*)jobs[4 * jb + 3];
+  const float* p = (const float*)jobs.v[4 * jb + 0];
+  const int nb = (int)jobs.v[4 * jb + 1];
+  const int64_t n = jobs.v[4 * jb + 2];
+  float* out = (float*)jobs.v[4 * jb + 3];
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -148,12 +157,12 @@ __global__ void k_reduce_partials(const int64_t* __restrict__ jobs) {
   }
 }
 
-__global__ void k_sum_sgd(float* __restrict__ params, float* __restrict__ gout,
-                          const int64_t* __restrict__ gptrs, int ndev, int64_t n, float scale) {
+__global__ void k_sum_sgd(float* __restrict__ params, float* __restrict__ gout, DevPtrs gptrs,
+                          int ndev, int64_t n, float scale) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
-    float s = ((const float*)gptrs[0])[k];
-    for (int d = 1; d < ndev; ++d) s += ((const float*)gptrs[d])[k];
+    float s = ((const float*)gptrs.v[0])[k];
+    for (int d = 1; d < ndev; ++d) s += ((const float*)gptrs.v[d])[k];
     if (gout) gout[k] = s;
     params[k] -= scale * s;
   }
@@ -202,18 +211,28 @@ extern "C" int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32
 extern "C" int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n,
                                   void* stream) {
   if (n_jobs <= 0 || max_n <= 0) return SG_OK;
-  dim3 grid(clamp_grid(div_up(max_n, 256), kSMs), n_jobs);
-  k_reduce_partials<<<grid, 256, 0, (cudaStream_t)stream>>>(jobs);
-  SG_CHECK_LAUNCH("k_reduce_partials");
+  SG_REQUIRE(jobs != nullptr, "reduce_partials: null job table");
+  for (int j0 = 0; j0 < n_jobs; j0 += MAXJOBS) {
+    const int nj = std::min(MAXJOBS, n_jobs - j0);
+    Jobs jb;
+    memset(&jb, 0, sizeof(jb));
+    memcpy(jb.v, jobs + 4 * j0, sizeof(int64_t) * 4 * nj);
+    dim3 grid(clamp_grid(div_up(max_n, 256), kSMs), nj);
+    k_reduce_partials<<<grid, 256, 0, (cudaStream_t)stream>>>(jb);
+    SG_CHECK_LAUNCH("k_reduce_partials");
+  }
   return SG_OK;
 }
 
 extern "C" int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_ptrs,
                           int32_t n_dev, int64_t n, float scale, void* stream) {
-  SG_REQUIRE(params && grad_ptrs && n_dev >= 1, "sum_sgd: bad arguments");
+  SG_REQUIRE(params && grad_ptrs && n_dev >= 1 && n_dev <= SG_MAXG, "sum_sgd: bad arguments");
   if (n <= 0) return SG_OK;
+  DevPtrs gp;
+  memset(&gp, 0, sizeof(gp));
+  for (int d = 0; d < n_dev; ++d) gp.v[d] = grad_ptrs[d];
   k_sum_sgd<<<clamp_grid(div_up(n, 256), kSMs * 4), 256, 0, (cudaStream_t)stream>>>(
-      params, grads_out, grad_ptrs, n_dev, n, scale);
+      params, grads_out, gp, n_dev, n, scale);
   SG_CHECK_LAUNCH("k_sum_sgd");
   return SG_OK;
 }

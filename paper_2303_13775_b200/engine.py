@@ -260,11 +260,8 @@ class SplitStep:
         for part, nb, n, gbuf, off in self.jobs:
             jobs += [part.data_ptr(), nb, n, gbuf.data_ptr() + 4 * off]
             max_n = max(max_n, n)
-        host = torch.tensor(jobs, dtype=torch.int64).pin_memory()
-        self._jobs_dev = host.to(self.dev, non_blocking=True)
-        self._jobs_host = host
-        _lib.call("sg_reduce_partials", _lib.ptr(self._jobs_dev), len(self.jobs), max_n,
-                  _lib.stream_ptr())
+        table = np.asarray(jobs, dtype=np.int64)
+        _lib.call("sg_reduce_partials", _lib.ptr(table), len(self.jobs), max_n, _lib.stream_ptr())
 
     def loss_sum_dev(self):
         return sum(self.grads[d][self.p.n] for d in self.devices)
@@ -495,7 +492,7 @@ def allreduce_and_step(params, per_device_grads, lr, num_targets):
             t = np.concatenate([np.asarray(gd[k], dtype=np.float32).reshape(-1) for k in dp.names])
             f = torch.from_numpy(t).to(dp.flat.device)
         flats.append(f)
-    ptrs = torch.tensor([f.data_ptr() for f in flats], dtype=torch.int64).to(dp.flat.device)
+    ptrs = np.asarray([f.data_ptr() for f in flats], dtype=np.int64)
     total = torch.empty(dp.n, dtype=torch.float32, device=dp.flat.device)
     _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), _lib.ptr(total), _lib.ptr(ptrs), len(flats), dp.n,
               float(lr) / float(num_targets), _lib.stream_ptr())
@@ -573,7 +570,7 @@ class Trainer:
             account_transfer(rec, "host", int(m.load_off[g]) * self.graph_feat_dim() * 8)
             step = SplitStep(dp, ds, self.feats, self.labels_dev)
             step.run()
-            ptrs = torch.tensor([step.grads[d].data_ptr() for d in range(g)], dtype=torch.int64).to(self.device)
+            ptrs = np.asarray([step.grads[d].data_ptr() for d in range(g)], dtype=np.int64)
             _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs), g, dp.n,
                       float(lr) / len(targets), _lib.stream_ptr())
             loss = sum(float(step.grads[d][dp.n].item()) for d in range(g))
