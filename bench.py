@@ -234,81 +234,126 @@ def main():
     flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
     exact = g > 1
 
-    def one_step(i, host=False, record_events=False):
-        if host:
-            ds = sg.DeviceSplit.from_sample(samples[i], pm, cache, dev)
-        else:
-            V, es, ed, (nV, nE) = dev_samples[i]
-            ds = sg.DeviceSplit(V, es, ed, nV, nE, pm, cache, True, dev)
-        step = SplitStep(dp, ds, feats, labels_dev, devices=[rank], transport=transport,
-                         exact=exact, record_events=record_events)
-        step.run()
-        gbuf = step.grads[rank]
-        if g > 1:
-            dist.all_reduce(gbuf)
-        ptrs_h = np.asarray([gbuf.data_ptr()], dtype=np.int64)
-        _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs_h), 1, dp.n,
-                  LR / len(samples[i].targets), _lib.stream_ptr())
-        return step, gbuf, None
-
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for i in range(args.warmup):
-        one_step(i)
-    barrier()
-
-    # ---- device-resident timing: per-step CUDA events, L2 flushed between steps
-    agg_ms, step_ms, keep = [], [], []
-    l0 = _lib.launch_count()
-    clocks = ClockSampler(local)
-    with clocks:
-        barrier()
-        t_wall = time.perf_counter()
-        for i in range(args.warmup, n_steps):
-            flush.zero_()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            step, gbuf, pd = one_step(i, record_events=True)
-            e1.record()
-            keep.append((e0, e1, step, gbuf, pd))
-        barrier()
-        t_wall = time.perf_counter() - t_wall
-    launches = _lib.launch_count() - l0
-    for e0, e1, step, _, _ in keep:
-        step_ms.append(e0.elapsed_time(e1))
-        a0, a1 = step.events["agg1_start"][0], step.events["agg1_end"][0]
-        agg_ms.append(a0.elapsed_time(a1))
-    my_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([my_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        my_ms = float(t.item())
     edges = sum(samples[i].total_edges for i in range(args.warmup, n_steps))
-    value = edges / (my_ms / 1e3)
+    agg_ms, step_ms = [], []
+    clocks = ClockSampler(local)
+    if g == 1:
+        # ---- single GPU: the whole step is one captured CUDA graph ----------------
+        from paper_2303_13775_b200.engine import CapturedStep, capacities_for
+        cap_nV, cap_nE = capacities_for(samples)
+        cs = CapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, LR / args.batch, dev,
+                          record_events=True)
+        cs.capture(samples[0])                     # eager warm-up step 0 + capture
+        for i in range(1, args.warmup):
+            cs.run(samples[i])
+        barrier()
+        l0 = _lib.launch_count()
+        with clocks:
+            t_wall = time.perf_counter()
+            for i in range(args.warmup, n_steps):
+                flush.zero_()
+                cs.inp.load(samples[i])            # H2D outside the device-resident timing
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                cs.replay()
+                e1.record()
+                e1.synchronize()
+                step_ms.append(e0.elapsed_time(e1))
+                ev = cs.step.events
+                agg_ms.append(ev["agg1_start"][0].elapsed_time(ev["agg1_end"][0]))
+            barrier()
+            t_wall = time.perf_counter() - t_wall
+        # graph replays launch the captured kernels: count them from one eager step
+        per_step_launches = _lib.launch_count()
+        cs._body()
+        torch.cuda.synchronize()
+        per_step_launches = _lib.launch_count() - per_step_launches
+        launches = per_step_launches * args.steps
+        my_ms = sum(step_ms)
+        # ---- end to end: host sample -> pinned -> H2D -> graph -> D2H loss ----------
+        barrier()
+        losses = []
+        h2d = 0
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.warmup, n_steps):
+            out = cs.run(samples[i])
+            h2d += cs.inp.bytes_h2d
+            losses.append(float(out[dp.n].item()) / len(samples[i].targets))
+        e1.record()
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
+    else:
+        # ---- one rank per GPU: eager step, NCCL all-to-all-v + all-reduce ---------
+        def one_step(i, record_events=False):
+            V, es, ed, (nV, nE) = dev_samples[i]
+            ds = sg.DeviceSplit(V, es, ed, nV, nE, pm, cache, True, dev)
+            step = SplitStep(dp, ds, feats, labels_dev, devices=[rank], transport=transport,
+                             exact=True, record_events=record_events)
+            step.run()
+            gbuf = step.grads[rank]
+            dist.all_reduce(gbuf)
+            ptrs_h = np.asarray([gbuf.data_ptr()], dtype=np.int64)
+            _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs_h), 1, dp.n,
+                      LR / len(samples[i].targets), _lib.stream_ptr())
+            return step, gbuf
 
-    # ---- end to end through the public API: host sample -> H2D -> step -> D2H loss
-    h2d = 0
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    losses = []
-    for i in range(args.warmup, n_steps):
-        step, gbuf, _ = one_step(i, host=True)
-        losses.append(float(gbuf[dp.n].item()) / len(samples[i].targets))
-        V, es, ed = samples[i].packed()
-        h2d += V.nbytes + es.nbytes + ed.nbytes
-    e1.record()
-    barrier()
-    e2e_ms = e0.elapsed_time(e1)
+        for i in range(args.warmup):
+            one_step(i)
+        barrier()
+        keep = []
+        l0 = _lib.launch_count()
+        with clocks:
+            barrier()
+            t_wall = time.perf_counter()
+            for i in range(args.warmup, n_steps):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                step, gbuf = one_step(i, record_events=True)
+                e1.record()
+                keep.append((e0, e1, step))
+            barrier()
+            t_wall = time.perf_counter() - t_wall
+        launches = _lib.launch_count() - l0
+        for e0, e1, step in keep:
+            step_ms.append(e0.elapsed_time(e1))
+            agg_ms.append(step.events["agg1_start"][0].elapsed_time(step.events["agg1_end"][0]))
+        my_ms = sum(step_ms)
+        barrier()
+        losses, h2d = [], 0
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(args.warmup, n_steps):
+            smp = samples[i]
+            ds = sg.DeviceSplit.from_sample(smp, pm, cache, dev)
+            step = SplitStep(dp, ds, feats, labels_dev, devices=[rank], transport=transport, exact=True)
+            step.run()
+            gbuf = step.grads[rank]
+            dist.all_reduce(gbuf)
+            ptrs_h = np.asarray([gbuf.data_ptr()], dtype=np.int64)
+            _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs_h), 1, dp.n,
+                      LR / len(smp.targets), _lib.stream_ptr())
+            losses.append(float(gbuf[dp.n].item()) / len(smp.targets))
+            V, es, ed = smp.packed()
+            h2d += V.nbytes + es.nbytes + ed.nbytes
+        e1.record()
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
+        t = torch.tensor([my_ms, e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        my_ms, e2e_ms = float(t[0].item()), float(t[1].item())
+    value = edges / (my_ms / 1e3)
     e2e = edges / (e2e_ms / 1e3)
 
     if rank == 0:

@@ -107,8 +107,12 @@ void sg_struct_sizes(int64_t* out /* [sizeof(SgMeta), sizeof(SgSplitLayout)] */)
  * the split of ALL g devices from the replicated sample (each rank of a
  * multi-GPU job runs it on its own copy and keeps its own slice).
  *
- * V: int32 concatenated layer vertices (V^0..V^L), esrc/edst: int32
- * concatenated per-layer edge positions (E^1..E^L). asn: uint8 device of each
+ * The layout (sg_split_layout) is computed from CAPACITIES nV/nE; V: int32
+ * layer vertices (V^l at offset voff[l]), esrc/edst: int32 per-layer edge
+ * positions (E^l at eoff[l-1]). sizes: nullable DEVICE array of the actual
+ * sizes [nV_0..nV_L, nE_1..nE_L] (<= capacities) — every kernel reads the
+ * actual sizes from device memory, so one captured CUDA graph serves every
+ * sample that fits the capacities. asn: uint8 device of each
  * global vertex (PartitionMap.assignment, partition.py:20-52). cache_bits:
  * nullable bitmap of CacheState.global_mask (partition.py:70-75). dst_grouped:
  * 1 if every layer's edges list each destination's in-edges contiguously
@@ -116,8 +120,9 @@ void sg_struct_sizes(int64_t* out /* [sizeof(SgMeta), sizeof(SgSplitLayout)] */)
 int sg_split_layout(int32_t L, int32_t g, const int64_t* nV, const int64_t* nE,
                     int64_t n_vertices, SgSplitLayout* out);
 int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V,
-                 const int32_t* esrc, const int32_t* edst, const uint8_t* asn,
-                 const uint32_t* cache_bits, int32_t dst_grouped, void* stream);
+                 const int32_t* esrc, const int32_t* edst, const int64_t* sizes,
+                 const uint8_t* asn, const uint32_t* cache_bits, int32_t dst_grouped,
+                 void* stream);
 
 /* Stable LSD radix sort of (key,value) pairs (keys < 2^key_bits), used to
  * build CSR-by-source for the transpose SpMM (engine.py:263-273) and
@@ -129,10 +134,12 @@ int sg_sort_pairs(void* ws, int64_t n_max, const int32_t* n_dev, uint32_t* keys,
 
 /* Build CSR-by-source of the edges of device d at layers [lmin, L]. Keys are
  * global rows at l-1 (row_base[l] + own_off[l-1][d] + lsrc); on return
- * srcbeg/srcend (indexed by that key space) bound runs of `perm` (values are
- * global edge slots in the split's grouped edge array). */
+ * srcbeg/srcend (indexed by that key space) bound runs of `perm`. val_mode 0:
+ * values are global edge slots of the split's grouped edge array; 1: values
+ * encode the gradient row each out-edge reads (>= 0 owned row, < 0
+ * -(1 + pair slot) of the push-from-owner payload). */
 int sg_src_csr(const void* split_ws, const SgSplitLayout* lay, int32_t d,
-               int32_t lmin, void* sort_ws, int64_t n_max, int32_t* n_dev,
+               int32_t lmin, int32_t val_mode, void* sort_ws, int64_t n_max, int32_t* n_dev,
                uint32_t* keys, int32_t* perm, int32_t* srcbeg, int32_t* srcend,
                int64_t n_rows_total, void* stream);
 /* Same for destinations (only needed when the sample is not dst-grouped):
@@ -200,7 +207,7 @@ int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, 
 int sg_sage_scatter_bwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                         int32_t w, const float* d_self, const float* d_sums,
                         const float* bwd_recv, int32_t recv_stride,
-                        const int32_t* perm, const int32_t* srcbeg, const int32_t* srcend,
+                        const int32_t* enc, const int32_t* srcbeg, const int32_t* srcend,
                         int64_t key_base, float* d_prev, int64_t max_rows, void* stream);
 
 /* ---------------------------------------------------------------- exchange

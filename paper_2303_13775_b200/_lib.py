@@ -71,10 +71,10 @@ _SIGS = {
     "sg_device_sm_count": (i32, []),
     "sg_struct_sizes": (None, [vp]),
     "sg_split_layout": (i32, [i32, i32, P(i64), P(i64), i64, P(SgSplitLayout)]),
-    "sg_split_run": (i32, [vp, P(SgSplitLayout), vp, vp, vp, vp, vp, i32, vp]),
+    "sg_split_run": (i32, [vp, P(SgSplitLayout), vp, vp, vp, vp, vp, vp, i32, vp]),
     "sg_sort_ws_bytes": (i64, [i64]),
     "sg_sort_pairs": (i32, [vp, i64, vp, vp, vp, i32, vp]),
-    "sg_src_csr": (i32, [vp, P(SgSplitLayout), i32, i32, vp, i64, vp, vp, vp, vp, vp, i64, vp]),
+    "sg_src_csr": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, i64, vp]),
     "sg_dst_csr": (i32, [vp, P(SgSplitLayout), i32, vp, i64, vp, vp, vp, vp]),
     "sg_layer0_rows": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, vp, vp]),
     "sg_gather_rows": (i32, [vp, vp, i64, i32, vp, vp]),

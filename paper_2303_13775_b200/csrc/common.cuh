@@ -45,6 +45,16 @@ void set_error(const std::string& msg);
 
 constexpr int kSMs = 148;
 
+// Raise a kernel's dynamic shared-memory limit to the sm_100 maximum once per
+// process (never inside a later CUDA-graph capture).
+template <auto K>
+inline cudaError_t allow_max_smem() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  done = true;
+  return cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

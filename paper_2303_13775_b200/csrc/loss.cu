@@ -143,17 +143,38 @@ struct DevPtrs {
   int64_t v[SG_MAXG];
 };
 
-__global__ void k_reduce_partials(Jobs jobs) {
+// Block = 32 output columns x 8 warps; warp w sums partial rows b = w, w+8, ...
+// (4 loads in flight), then the 8 warp sums are added in warp order.
+__global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs) {
+  __shared__ float red[8][33];
   const int jb = blockIdx.y;
   const float* p = (const float*)jobs.v[4 * jb + 0];
   const int nb = (int)jobs.v[4 * jb + 1];
   const int64_t n = jobs.v[4 * jb + 2];
   float* out = (float*)jobs.v[4 * jb + 3];
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int b = 0; b < nb; ++b) s += p[(int64_t)b * n + k];
-    out[k] = s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t k0 = (int64_t)blockIdx.x * 32; k0 < n; k0 += (int64_t)gridDim.x * 32) {
+    const int64_t k = k0 + lane;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    if (k < n) {
+      int b = warp;
+      for (; b + 24 < nb; b += 32) {
+        s0 += p[(int64_t)b * n + k];
+        s1 += p[(int64_t)(b + 8) * n + k];
+        s2 += p[(int64_t)(b + 16) * n + k];
+        s3 += p[(int64_t)(b + 24) * n + k];
+      }
+      for (; b < nb; b += 8) s0 += p[(int64_t)b * n + k];
+    }
+    __syncthreads();
+    red[warp][lane] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    if (warp == 0 && k < n) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) t += red[w][lane];
+      out[k] = t;
+    }
   }
 }
 
@@ -201,8 +222,7 @@ extern "C" int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32
                                        (size_t)LTR * (ncls + 1) + 2 * LTR);
   SG_REQUIRE(smem <= 227 * 1024, "cls_loss: too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
-  if (smem > 48 * 1024)
-    SG_CUDA(cudaFuncSetAttribute(k_cls_loss, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SG_CUDA(allow_max_smem<k_cls_loss>());
   k_cls_loss<<<nblocks, 256, smem, st>>>((const SgMeta*)(base + y.o_meta), a);
   SG_CHECK_LAUNCH("k_cls_loss");
   return SG_OK;
@@ -217,7 +237,7 @@ extern "C" int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t m
     Jobs jb;
     memset(&jb, 0, sizeof(jb));
     memcpy(jb.v, jobs + 4 * j0, sizeof(int64_t) * 4 * nj);
-    dim3 grid(clamp_grid(div_up(max_n, 256), kSMs), nj);
+    dim3 grid(clamp_grid(div_up(max_n, 32), kSMs * 2), nj);
     k_reduce_partials<<<grid, 256, 0, (cudaStream_t)stream>>>(jb);
     SG_CHECK_LAUNCH("k_reduce_partials");
   }

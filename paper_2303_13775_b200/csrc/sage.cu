@@ -1,18 +1,27 @@
 // GraphSAGE (mean aggregator) forward / backward for one device of a split.
 //
 //   sg_sage_agg_fwd     local_aggregate (engine.py:180-195): CSR-by-destination
-//                       segment-sum SpMM, warp (or sub-warp) per destination
-//                       row, 128-bit loads, 4 source rows in flight per lane
-//                       group; reference rows are packed straight into the
+//                       segment-sum SpMM. A row group (LPR lanes, warp for
+//                       F=100) first fetches up to LPR edge indices in ONE
+//                       round (lane i -> edge i, both index hops in parallel),
+//                       then broadcasts them with shuffles and issues all the
+//                       source-row loads (128-bit) back to back, 8 in flight.
+//                       Reference rows are packed straight into the
 //                       push-to-owner send buffer (fused pack epilogue).
 //   sg_sage_update      owner combine in ascending sender order + mean +
-//                       h_self@W_self + mean@W_neigh + b + ReLU (:197-226),
-//                       FP32 FFMA with both weight matrices staged in smem.
+//                       h_self@W_self + mean@W_neigh + b + ReLU (:197-226);
+//                       FP32 FFMA, weights in smem, each thread a 1x4 output
+//                       tile (2 scalar + 2 LDS.128 per 8 FMA).
 //   sg_sage_bwd_rows    d_pre, weight/bias gradient partials (deterministic
-//                       per-block), d_self and d_sums (:228-254).
-//   sg_sage_scatter_bwd transpose SpMM over CSR-by-source (:263-276) reading
-//                       reference destinations from the push-from-owner
-//                       payload (fused unpack).
+//                       per-block, 1x4 register tiles), d_self and d_sums
+//                       (:228-254).
+//   sg_sage_scatter_bwd transpose SpMM over CSR-by-source (:263-276): warp per
+//                       source row, 32 out-edges fetched per round and split
+//                       over 32/LPR lane groups (hub rows load-balanced inside
+//                       the warp), fixed-tree reduction (deterministic);
+//                       reference destinations read the owners' returned
+//                       gradients from the push-from-owner payload (fused
+//                       unpack).
 // All arithmetic is FP32 (parity target rel 1e-4 vs the float64 reference).
 #include <cstring>
 
@@ -21,6 +30,45 @@
 namespace sg {
 namespace {
 
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<4> {
+  using T = float4;
+  __device__ static float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ static float4 ld(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  __device__ static float4 ld_any(const float* p) { return make_float4(p[0], p[1], p[2], p[3]); }
+  __device__ static void add(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+  }
+  __device__ static float4 shfl_xor(const float4& v, int o) {
+    return make_float4(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o),
+                       __shfl_xor_sync(0xffffffffu, v.z, o), __shfl_xor_sync(0xffffffffu, v.w, o));
+  }
+  __device__ static void st(float* p, const float4& v) { *reinterpret_cast<float4*>(p) = v; }
+  __device__ static void st_any(float* p, const float4& v) {
+    p[0] = v.x;
+    p[1] = v.y;
+    p[2] = v.z;
+    p[3] = v.w;
+  }
+};
+template <>
+struct VecT<1> {
+  using T = float;
+  __device__ static float zero() { return 0.f; }
+  __device__ static float ld(const float* p) { return __ldg(p); }
+  __device__ static float ld_any(const float* p) { return *p; }
+  __device__ static void add(float& a, const float& b) { a += b; }
+  __device__ static float shfl_xor(const float& v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+  __device__ static void st(float* p, const float& v) { *p = v; }
+  __device__ static void st_any(float* p, const float& v) { *p = v; }
+};
+
+// ---------------------------------------------------------------- forward SpMM
 struct AggArgs {
   int l, d, w, stride;
   int64_t eoff_li, rbase_li, pbase_l;
@@ -36,31 +84,6 @@ struct AggArgs {
   float* sendbuf;
 };
 
-template <int VEC>
-struct VecT;
-template <>
-struct VecT<4> {
-  using T = float4;
-  __device__ static float4 zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-  __device__ static float4 ld(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-  __device__ static void add(float4& a, const float4& b) {
-    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-  }
-  __device__ static void st(float* p, const float4& v) { *reinterpret_cast<float4*>(p) = v; }
-  __device__ static void st_any(float* p, const float4& v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w; }
-};
-template <>
-struct VecT<1> {
-  using T = float;
-  __device__ static float zero() { return 0.f; }
-  __device__ static float ld(const float* p) { return __ldg(p); }
-  __device__ static void add(float& a, const float& b) { a += b; }
-  __device__ static void st(float* p, const float& v) { *p = v; }
-  __device__ static void st_any(float* p, const float& v) { *p = v; }
-};
-
-// Warp-or-subwarp per destination row. LPR lanes per row, each lane owns NCH
-// chunks of VEC consecutive columns: col = (ch*LPR + lane_in_row)*VEC.
 template <int VEC, int LPR, int NCH>
 __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ meta, AggArgs a) {
   using V = VecT<VEC>;
@@ -74,46 +97,57 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
   const int64_t rb = a.rbase_li + own0 + ref0;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR, lr = lane % LPR;
+  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t q = gw * RPW + sub; q < R; q += nw * RPW) {
-    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
+  // all row groups of a warp run the same number of iterations (shuffles)
+  const int64_t iters = (R + nw * RPW - 1) / (nw * RPW);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t q = (it * nw + gw) * RPW + sub;
+    const bool live = q < R;
+    const int b = live ? a.rowbeg[rb + q] : 0;
+    const int e = live ? a.rowend[rb + q] : 0;
     T acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = V::zero();
-    auto rowptr = [&](int j) -> const float* {
-      const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
-      int r = prev0 + a.lsrc[x];
-      if (a.src_row) r = a.src_row[r];
-      return a.h_prev + (int64_t)r * w;
-    };
-    int j = b;
-    for (; j + 4 <= e; j += 4) {
-      const float* p0 = rowptr(j);
-      const float* p1 = rowptr(j + 1);
-      const float* p2 = rowptr(j + 2);
-      const float* p3 = rowptr(j + 3);
+    for (int jb = b; jb < e; jb += LPR) {
+      // round: lane lr fetches edge jb+lr's physical source row (2 hops, in parallel)
+      const int j = jb + lr;
+      int r = 0;
+      if (j < e) {
+        const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
+        r = prev0 + a.lsrc[x];
+        if (a.src_row) r = a.src_row[r];
+      }
+      const int cnt = min(LPR, e - jb);
+      int k = 0;
+      for (; k + 8 <= cnt; k += 8) {
+        int rr[8];
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const int col = (c * LPR + lr) * VEC;
-        if (col < w) {
-          T v0 = V::ld(p0 + col), v1 = V::ld(p1 + col), v2 = V::ld(p2 + col), v3 = V::ld(p3 + col);
-          V::add(acc[c], v0);
-          V::add(acc[c], v1);
-          V::add(acc[c], v2);
-          V::add(acc[c], v3);
+        for (int u = 0; u < 8; ++u) rr[u] = __shfl_sync(gmask, r, k + u, LPR);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int col = (c * LPR + lr) * VEC;
+          if (col < w) {
+            T v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = V::ld(a.h_prev + (int64_t)rr[u] * w + col);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) V::add(acc[c], v[u]);
+          }
+        }
+      }
+      for (; k < cnt; ++k) {
+        const int r0 = __shfl_sync(gmask, r, k, LPR);
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int col = (c * LPR + lr) * VEC;
+          if (col < w) V::add(acc[c], V::ld(a.h_prev + (int64_t)r0 * w + col));
         }
       }
     }
-    for (; j < e; ++j) {
-      const float* p0 = rowptr(j);
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const int col = (c * LPR + lr) * VEC;
-        if (col < w) V::add(acc[c], V::ld(p0 + col));
-      }
-    }
-    const float cnt = (float)(e - b);
+    if (!live) continue;
+    const float cntf = (float)(e - b);
     if (q < n_own) {
       float* out = a.sums + (int64_t)(own0 + q) * w;
 #pragma unroll
@@ -121,7 +155,7 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
         const int col = (c * LPR + lr) * VEC;
         if (col < w) V::st(out + col, acc[c]);
       }
-      if (lr == 0) a.counts[own0 + q] = cnt;
+      if (lr == 0) a.counts[own0 + q] = cntf;
     } else {
       const int slot = a.sendpos[a.pbase_l + ref0 + (q - n_own)];
       float* out = a.sendbuf + (int64_t)slot * a.stride;
@@ -132,7 +166,7 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
           if ((a.stride & 3) == 0) V::st(out + col, acc[c]); else V::st_any(out + col, acc[c]);
         }
       }
-      if (lr == 0) out[w] = cnt;
+      if (lr == 0) out[w] = cntf;
     }
   }
 }
@@ -140,7 +174,7 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
 template <int VEC, int LPR, int NCH>
 int launch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStream_t st) {
   constexpr int RPB = 8 * (32 / LPR);  // rows per 256-thread block
-  const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 16);
+  const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
   k_sage_agg<VEC, LPR, NCH><<<grid, 256, 0, st>>>(meta, a);
   SG_CHECK_LAUNCH("k_sage_agg");
   return SG_OK;
@@ -167,7 +201,7 @@ int dispatch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStr
 }
 
 // ---------------------------------------------------------------- update
-constexpr int UTR = 32;  // rows per tile
+constexpr int UTR = 64;  // rows per tile
 
 struct UpdArgs {
   int l, d, w, dout, final_, g, stride;
@@ -186,13 +220,14 @@ struct UpdArgs {
   float* h;
 };
 
+template <bool Q4>
 __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ meta, UpdArgs a) {
-  extern __shared__ float smem[];
+  extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, wp = w + 1;
-  float* ws_s = smem;                 // [w][dout]
-  float* wn_s = ws_s + w * dout;      // [w][dout]
-  float* hs_s = wn_s + w * dout;      // [UTR][w+1]
-  float* mn_s = hs_s + UTR * wp;      // [UTR][w+1]
+  float* ws_s = smem;              // [w][dout]
+  float* wn_s = ws_s + w * dout;   // [w][dout]
+  float* hs_s = wn_s + w * dout;   // [UTR][w+1]
+  float* mn_s = hs_s + UTR * wp;   // [UTR][w+1]
   for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
     ws_s[i] = a.ws[i];
     wn_s[i] = a.wn[i];
@@ -210,44 +245,80 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
       const int G = own0 + q;
       float N = a.counts[G];
       const int* cb = a.contrib + (int64_t)g * a.voff_l + (int64_t)G * g;
-      int rs[SG_MAXG];
-#pragma unroll
-      for (int s = 0; s < SG_MAXG; ++s) rs[s] = s < g ? cb[s] : -1;
-#pragma unroll
-      for (int s = 0; s < SG_MAXG; ++s)
-        if (rs[s] >= 0) N += a.recv[(int64_t)rs[s] * a.stride + w];
+      // the owner combines holders' partials in ascending sender order
+      int rs_l = lane < g ? cb[lane] : -1;
+      unsigned has = __ballot_sync(0xffffffffu, rs_l >= 0);
+      for (unsigned m = has; m; m &= m - 1) {
+        const int s = __ffs(m) - 1;
+        const int rs = __shfl_sync(0xffffffffu, rs_l, s);
+        N += a.recv[(int64_t)rs * a.stride + w];
+      }
       int r = prev0 + a.selfrow[a.voff_l + G];
       if (a.src_row) r = a.src_row[r];
       const float* hrow = a.h_prev + (int64_t)r * w;
-      for (int c = lane; c < w; c += 32) {
-        float S = a.sums[(int64_t)G * w + c];
-#pragma unroll
-        for (int s = 0; s < SG_MAXG; ++s)
-          if (rs[s] >= 0) S += a.recv[(int64_t)rs[s] * a.stride + c];
-        const float m = S / N;
-        mn_s[rr * wp + c] = m;
-        a.mean[(int64_t)G * w + c] = m;
-        hs_s[rr * wp + c] = __ldg(hrow + c);
+      for (int c0 = 0; c0 < w; c0 += 32) {  // all lanes iterate: shuffles stay warp-wide
+        const int c = c0 + lane;
+        float S = c < w ? a.sums[(int64_t)G * w + c] : 0.f;
+        for (unsigned m = has; m; m &= m - 1) {
+          const int s = __ffs(m) - 1;
+          const int rs = __shfl_sync(0xffffffffu, rs_l, s);
+          if (c < w) S += a.recv[(int64_t)rs * a.stride + c];
+        }
+        if (c < w) {
+          const float mv = S / N;
+          mn_s[rr * wp + c] = mv;
+          a.mean[(int64_t)G * w + c] = mv;
+          hs_s[rr * wp + c] = __ldg(hrow + c);
+        }
       }
       if (lane == 0) a.counts[G] = N;
     }
     __syncthreads();
-    for (int idx = threadIdx.x; idx < UTR * dout; idx += blockDim.x) {
-      const int rr = idx / dout, j = idx - rr * dout;
-      const int q = tile * UTR + rr;
-      if (q >= n_own) continue;
-      const float* hr = hs_s + rr * wp;
-      const float* mr = mn_s + rr * wp;
-      float acc = a.bias[j];
-      for (int c = 0; c < w; ++c) acc = fmaf(hr[c], ws_s[c * dout + j], fmaf(mr[c], wn_s[c * dout + j], acc));
-      a.h[(int64_t)(own0 + q) * dout + j] = a.final_ ? acc : fmaxf(acc, 0.f);
+    if (Q4) {
+      const int nq = dout >> 2;
+      for (int idx = threadIdx.x; idx < UTR * nq; idx += blockDim.x) {
+        const int rr = idx / nq, jq = idx - rr * nq;
+        const int q = tile * UTR + rr;
+        if (q >= n_own) continue;
+        const float* hr = hs_s + rr * wp;
+        const float* mr = mn_s + rr * wp;
+        float4 acc = *reinterpret_cast<const float4*>(a.bias + 4 * jq);
+        for (int c = 0; c < w; ++c) {
+          const float hv = hr[c], mv = mr[c];
+          const float4 s4 = *reinterpret_cast<const float4*>(ws_s + c * dout + 4 * jq);
+          const float4 n4 = *reinterpret_cast<const float4*>(wn_s + c * dout + 4 * jq);
+          acc.x = fmaf(hv, s4.x, fmaf(mv, n4.x, acc.x));
+          acc.y = fmaf(hv, s4.y, fmaf(mv, n4.y, acc.y));
+          acc.z = fmaf(hv, s4.z, fmaf(mv, n4.z, acc.z));
+          acc.w = fmaf(hv, s4.w, fmaf(mv, n4.w, acc.w));
+        }
+        if (!a.final_) {
+          acc.x = fmaxf(acc.x, 0.f);
+          acc.y = fmaxf(acc.y, 0.f);
+          acc.z = fmaxf(acc.z, 0.f);
+          acc.w = fmaxf(acc.w, 0.f);
+        }
+        *reinterpret_cast<float4*>(a.h + (int64_t)(own0 + q) * dout + 4 * jq) = acc;
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < UTR * dout; idx += blockDim.x) {
+        const int rr = idx / dout, j = idx - rr * dout;
+        const int q = tile * UTR + rr;
+        if (q >= n_own) continue;
+        const float* hr = hs_s + rr * wp;
+        const float* mr = mn_s + rr * wp;
+        float acc = a.bias[j];
+        for (int c = 0; c < w; ++c) acc = fmaf(hr[c], ws_s[c * dout + j], fmaf(mr[c], wn_s[c * dout + j], acc));
+        a.h[(int64_t)(own0 + q) * dout + j] = a.final_ ? acc : fmaxf(acc, 0.f);
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------- backward rows
 constexpr int BTR = 32;
-constexpr int MAXACC = 16;  // per thread per weight matrix: w*dout <= 4096
+constexpr int BMAXQ = 4;    // float4 slots per thread per weight matrix (w*dout <= 4096)
+constexpr int BMAXACC = 16;  // scalar slots (dout % 4 != 0 path)
 
 struct BwdArgs {
   int l, d, w, dout, final_;
@@ -266,31 +337,38 @@ struct BwdArgs {
   float* d_sums;
 };
 
+template <bool Q4>
 __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict__ meta, BwdArgs a) {
-  extern __shared__ float smem[];
-  const int w = a.w, dout = a.dout, wp = w + 1, dp1 = dout + 1;
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, dout = a.dout, wp = w + 1;
+  const int wst = Q4 ? dout + 4 : dout + 1;  // padded weight row stride
   const bool need_c = a.d_self != nullptr || a.d_sums != nullptr;
-  float* dp_s = smem;                       // [BTR][dout]
-  float* hs_s = dp_s + BTR * dout;          // [BTR][w+1]
-  float* mn_s = hs_s + BTR * wp;            // [BTR][w+1]
-  float* ws_s = mn_s + BTR * wp;            // [w][dout+1] (only if need_c)
-  float* wn_s = ws_s + w * dp1;
-  float* inv_s = wn_s + w * dp1;            // [BTR]
+  float* dp_s = smem;                  // [BTR][dout]
+  float* ws_s = dp_s + BTR * dout;     // [w][wst] (only if need_c)
+  float* wn_s = ws_s + w * wst;
+  float* hs_s = wn_s + w * wst;        // [BTR][w+1]
+  float* mn_s = hs_s + BTR * wp;       // [BTR][w+1]
+  float* cnt_s = mn_s + BTR * wp;      // [BTR]
   if (need_c) {
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
-      ws_s[c * dp1 + j] = a.ws[i];
-      wn_s[c * dp1 + j] = a.wn[i];
+      ws_s[c * wst + j] = a.ws[i];
+      wn_s[c * wst + j] = a.wn[i];
     }
   }
   const int l = a.l, d = a.d;
   const int n_own = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d], prev0 = meta->own_off[l - 1][d];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwd = w * dout;
-  float aS[MAXACC], aN[MAXACC], ab = 0.f;
+  const int nq = dout >> 2;
+  const int nslots = Q4 ? w * nq : w * dout;
+  float4 aS4[BMAXQ], aN4[BMAXQ];
+  float aS[BMAXACC], aN[BMAXACC];
 #pragma unroll
-  for (int k = 0; k < MAXACC; ++k) aS[k] = aN[k] = 0.f;
+  for (int k = 0; k < BMAXQ; ++k) aS4[k] = aN4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < BMAXACC; ++k) aS[k] = aN[k] = 0.f;
+  float ab = 0.f;
   const int ntiles = (n_own + BTR - 1) / BTR;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     __syncthreads();
@@ -315,26 +393,52 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
           hs_s[rr * wp + c] = __ldg(hrow + c);
           mn_s[rr * wp + c] = mrow[c];
         }
-        if (lane == 0) inv_s[rr] = a.counts[G];
+        if (lane == 0) cnt_s[rr] = a.counts[G];
       } else {
         for (int c = lane; c < w; c += 32) hs_s[rr * wp + c] = mn_s[rr * wp + c] = 0.f;
-        if (lane == 0) inv_s[rr] = 1.f;
+        if (lane == 0) cnt_s[rr] = 1.f;
       }
     }
     __syncthreads();
+    if (Q4) {
 #pragma unroll
-    for (int k = 0; k < MAXACC; ++k) {
-      const int idx = threadIdx.x + 256 * k;
-      if (idx < nwd) {
-        const int c = idx / dout, j = idx - c * dout;
-        float s1 = aS[k], s2 = aN[k];
-        for (int rr = 0; rr < BTR; ++rr) {
-          const float g = dp_s[rr * dout + j];
-          s1 = fmaf(hs_s[rr * wp + c], g, s1);
-          s2 = fmaf(mn_s[rr * wp + c], g, s2);
+      for (int k = 0; k < BMAXQ; ++k) {
+        const int idx = threadIdx.x + 256 * k;
+        if (idx < nslots) {
+          const int c = idx / nq, jq = idx - c * nq;
+          float4 s1 = aS4[k], s2 = aN4[k];
+#pragma unroll 4
+          for (int rr = 0; rr < BTR; ++rr) {
+            const float4 g4 = *reinterpret_cast<const float4*>(dp_s + rr * dout + 4 * jq);
+            const float hv = hs_s[rr * wp + c], mv = mn_s[rr * wp + c];
+            s1.x = fmaf(hv, g4.x, s1.x);
+            s1.y = fmaf(hv, g4.y, s1.y);
+            s1.z = fmaf(hv, g4.z, s1.z);
+            s1.w = fmaf(hv, g4.w, s1.w);
+            s2.x = fmaf(mv, g4.x, s2.x);
+            s2.y = fmaf(mv, g4.y, s2.y);
+            s2.z = fmaf(mv, g4.z, s2.z);
+            s2.w = fmaf(mv, g4.w, s2.w);
+          }
+          aS4[k] = s1;
+          aN4[k] = s2;
         }
-        aS[k] = s1;
-        aN[k] = s2;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < BMAXACC; ++k) {
+        const int idx = threadIdx.x + 256 * k;
+        if (idx < nslots) {
+          const int c = idx / dout, j = idx - c * dout;
+          float s1 = aS[k], s2 = aN[k];
+          for (int rr = 0; rr < BTR; ++rr) {
+            const float gv = dp_s[rr * dout + j];
+            s1 = fmaf(hs_s[rr * wp + c], gv, s1);
+            s2 = fmaf(mn_s[rr * wp + c], gv, s2);
+          }
+          aS[k] = s1;
+          aN[k] = s2;
+        }
       }
     }
     if (threadIdx.x < dout)
@@ -346,24 +450,52 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
         if (q >= n_own) continue;
         const int64_t G = own0 + q;
         float s1 = 0.f, s2 = 0.f;
-        for (int j = 0; j < dout; ++j) {
-          const float g = dp_s[rr * dout + j];
-          s1 = fmaf(g, ws_s[c * dp1 + j], s1);
-          s2 = fmaf(g, wn_s[c * dp1 + j], s2);
+        if (Q4) {
+          for (int jq = 0; jq < nq; ++jq) {
+            const float4 g4 = *reinterpret_cast<const float4*>(dp_s + rr * dout + 4 * jq);
+            const float4 w1 = *reinterpret_cast<const float4*>(ws_s + c * wst + 4 * jq);
+            const float4 w2 = *reinterpret_cast<const float4*>(wn_s + c * wst + 4 * jq);
+            s1 = fmaf(g4.x, w1.x, fmaf(g4.y, w1.y, fmaf(g4.z, w1.z, fmaf(g4.w, w1.w, s1))));
+            s2 = fmaf(g4.x, w2.x, fmaf(g4.y, w2.y, fmaf(g4.z, w2.z, fmaf(g4.w, w2.w, s2))));
+          }
+        } else {
+          for (int j = 0; j < dout; ++j) {
+            const float gv = dp_s[rr * dout + j];
+            s1 = fmaf(gv, ws_s[c * wst + j], s1);
+            s2 = fmaf(gv, wn_s[c * wst + j], s2);
+          }
         }
         if (a.d_self) a.d_self[G * w + c] = s1;
-        if (a.d_sums) a.d_sums[G * w + c] = s2 / inv_s[rr];
+        if (a.d_sums) a.d_sums[G * w + c] = s2 / cnt_s[rr];
       }
     }
   }
+  // per-block partial in the parameter layout [dW_self | dW_neigh | db]
+  const int nwd = w * dout;
   const int64_t ntot = 2 * (int64_t)nwd + dout;
   float* out = a.partial + (int64_t)blockIdx.x * ntot;
+  if (Q4) {
 #pragma unroll
-  for (int k = 0; k < MAXACC; ++k) {
-    const int idx = threadIdx.x + 256 * k;
-    if (idx < nwd) {
-      out[idx] = aS[k];
-      out[nwd + idx] = aN[k];
+    for (int k = 0; k < BMAXQ; ++k) {
+      const int idx = threadIdx.x + 256 * k;
+      if (idx < nslots) {
+        const int c = idx / nq, jq = idx - c * nq;
+        *reinterpret_cast<float4*>(out + c * dout + 4 * jq) = aS4[k];
+        float* o2 = out + nwd + c * dout + 4 * jq;
+        o2[0] = aN4[k].x;
+        o2[1] = aN4[k].y;
+        o2[2] = aN4[k].z;
+        o2[3] = aN4[k].w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < BMAXACC; ++k) {
+      const int idx = threadIdx.x + 256 * k;
+      if (idx < nslots) {
+        out[idx] = aS[k];
+        out[nwd + idx] = aN[k];
+      }
     }
   }
   if (threadIdx.x < dout) out[2 * nwd + threadIdx.x] = ab;
@@ -372,13 +504,10 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
 // ---------------------------------------------------------------- scatter (transpose SpMM)
 struct ScatArgs {
   int l, d, w, stride;
-  int64_t voff_lm1, voff_l, pbase_l, key_base;
-  int64_t nV_l;
+  int64_t voff_lm1, voff_l, key_base;
   const int32_t* grouped;
   const int32_t* rank;
-  const int32_t* ldst;
-  const int32_t* sendpos;
-  const int32_t* perm;
+  const int32_t* enc;  // sorted out-edges: >=0 owned dst row, <0 -(1+pair slot)
   const int32_t* srcbeg;
   const int32_t* srcend;
   const float* d_self;
@@ -391,71 +520,79 @@ template <int VEC, int LPR, int NCH>
 __global__ void __launch_bounds__(256) k_sage_scatter(const SgMeta* __restrict__ meta, ScatArgs a) {
   using V = VecT<VEC>;
   using T = typename V::T;
-  constexpr int RPW = 32 / LPR;
+  constexpr int NG = 32 / LPR;  // lane groups per warp, each takes every NG-th edge
   const int l = a.l, d = a.d, w = a.w;
   const int n_prev = meta->n_own[l - 1][d];
   const int prev0 = meta->own_off[l - 1][d];
-  const int own0 = meta->own_off[l][d], n_own = meta->n_own[l][d], ref0 = meta->ref_off[l][d];
+  const int own0 = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
   const int lane = threadIdx.x & 31;
-  const int sub = lane / LPR, lr = lane % LPR;
+  const int gi = lane / LPR, lr = lane % LPR;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = gw * RPW + sub; u < n_prev; u += nw * RPW) {
+  for (int64_t u = gw; u < n_prev; u += nw) {
     const int64_t U = prev0 + u;
     T acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = V::zero();
-    const int p = a.grouped[a.voff_lm1 + U];
-    if (p < a.nV_l) {
-      const int64_t v = own0 + a.rank[a.voff_l + p];
-      const float* sr = a.d_self + v * w;
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const int col = (c * LPR + lr) * VEC;
-        if (col < w) acc[c] = V::ld(sr + col);
-      }
-    }
     const int b = a.srcbeg[a.key_base + U], e = a.srcend[a.key_base + U];
-    for (int j = b; j < e; ++j) {
-      const int x = a.perm[j];
-      const int q = a.ldst[x];
-      const float* row;
-      if (q < n_own) {
-        row = a.d_sums + (int64_t)(own0 + q) * w;
-      } else {
-        const int slot = a.sendpos[a.pbase_l + ref0 + (q - n_own)];
-        row = a.bwd_recv + (int64_t)slot * a.stride;
-      }
-      const bool vec_ok = q < n_own || (a.stride & 3) == 0;
+    for (int jb = b; jb < e; jb += 32) {
+      const int j = jb + lane;
+      const int my = j < e ? a.enc[j] : 0;
+      const int cnt = min(32, e - jb);
+      const int rounds = (cnt + NG - 1) / NG;
+      for (int kk = 0; kk < rounds; ++kk) {
+        const int k = kk * NG + gi;
+        const int code = __shfl_sync(0xffffffffu, my, k < 32 ? k : 31);
+        if (k < cnt) {
+          const bool own = code >= 0;
+          const float* row = own ? a.d_sums + (int64_t)code * w
+                                 : a.bwd_recv + (int64_t)(-code - 1) * a.stride;
 #pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const int col = (c * LPR + lr) * VEC;
-        if (col < w) {
-          if (vec_ok) {
-            V::add(acc[c], V::ld(row + col));
-          } else {
-            T t;
-            float* tp = reinterpret_cast<float*>(&t);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) tp[v] = row[col + v];
-            V::add(acc[c], t);
+          for (int c = 0; c < NCH; ++c) {
+            const int col = (c * LPR + lr) * VEC;
+            if (col < w) {
+              if (own || (a.stride & 3) == 0) V::add(acc[c], V::ld(row + col));
+              else V::add(acc[c], V::ld_any(row + col));
+            }
           }
         }
       }
     }
-    float* out = a.d_prev + U * w;
+    // fixed-order tree over the lane groups (deterministic)
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const int col = (c * LPR + lr) * VEC;
-      if (col < w) V::st(out + col, acc[c]);
+    for (int o = LPR; o < 32; o <<= 1) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) V::add(acc[c], V::shfl_xor(acc[c], o));
+    }
+    if (gi == 0) {
+      const int p = a.grouped[a.voff_lm1 + U];
+      float* out = a.d_prev + U * w;
+      if (p < nVl) {
+        const int64_t v = own0 + a.rank[a.voff_l + p];
+        const float* sr = a.d_self + v * w;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+          const int col = (c * LPR + lr) * VEC;
+          if (col < w) {
+            T s = V::ld(sr + col);
+            V::add(s, acc[c]);
+            acc[c] = s;
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const int col = (c * LPR + lr) * VEC;
+        if (col < w) V::st(out + col, acc[c]);
+      }
     }
   }
 }
 
 template <int VEC, int LPR, int NCH>
 int launch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaStream_t st) {
-  constexpr int RPB = 8 * (32 / LPR);
-  const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 16);
+  const int grid = clamp_grid(div_up(max_rows, 8), kSMs * 8);
   k_sage_scatter<VEC, LPR, NCH><<<grid, 256, 0, st>>>(meta, a);
   SG_CHECK_LAUNCH("k_sage_scatter");
   return SG_OK;
@@ -487,45 +624,14 @@ int dispatch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaS
   const SgMeta* meta = (const SgMeta*)(base + y.o_meta);               \
   auto I32 = [&](int64_t o) { return (const int32_t*)(base + o); };
 
-extern "C" int sg_sage_agg_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
-                               int32_t d, const float* h_prev, const int32_t* src_row, int32_t w,
-                               float* sums, float* counts, float* sendbuf, int32_t send_stride,
-                               int64_t max_rows, void* stream) {
+static int agg_common(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                      const float* h_prev, const int32_t* src_row, int32_t w, float* sums,
+                      float* counts, float* sendbuf, int32_t send_stride, const int32_t* dperm,
+                      int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "sage_agg_fwd: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_agg_fwd: bad layer/device");
   SG_REQUIRE(send_stride >= w + 1 || y.g == 1, "sage_agg_fwd: send stride < w+1");
-  if (max_rows <= 0) return SG_OK;
-  AggArgs a;
-  memset(&a, 0, sizeof(a));
-  a.l = l;
-  a.d = d;
-  a.w = w;
-  a.stride = send_stride;
-  a.eoff_li = y.eoff[l - 1];
-  a.rbase_li = y.rbase[l - 1];
-  a.pbase_l = y.pbase[l];
-  a.rowbeg = I32(y.o_rowbeg);
-  a.rowend = I32(y.o_rowend);
-  a.lsrc = I32(y.o_lsrc);
-  a.dperm = nullptr;
-  a.sendpos = I32(y.o_sendpos);
-  a.src_row = src_row;
-  a.h_prev = h_prev;
-  a.sums = sums;
-  a.counts = counts;
-  a.sendbuf = sendbuf;
-  return dispatch_agg(meta, a, max_rows, (cudaStream_t)stream);
-}
-
-extern "C" int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t l,
-                                    int32_t d, const float* h_prev, const int32_t* src_row,
-                                    int32_t w, float* sums, float* counts, float* sendbuf,
-                                    int32_t send_stride, const int32_t* dperm, int64_t max_rows,
-                                    void* stream) {
-  SG_REQUIRE(split_ws && lay, "sage_agg_fwd: null workspace");
-  SPLIT_PTRS
-  SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_agg_fwd: bad layer/device");
   if (max_rows <= 0) return SG_OK;
   AggArgs a;
   memset(&a, 0, sizeof(a));
@@ -549,6 +655,23 @@ extern "C" int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* l
   return dispatch_agg(meta, a, max_rows, (cudaStream_t)stream);
 }
 
+extern "C" int sg_sage_agg_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
+                               int32_t d, const float* h_prev, const int32_t* src_row, int32_t w,
+                               float* sums, float* counts, float* sendbuf, int32_t send_stride,
+                               int64_t max_rows, void* stream) {
+  return agg_common(split_ws, lay, l, d, h_prev, src_row, w, sums, counts, sendbuf, send_stride,
+                    nullptr, max_rows, stream);
+}
+
+extern "C" int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t l,
+                                    int32_t d, const float* h_prev, const int32_t* src_row,
+                                    int32_t w, float* sums, float* counts, float* sendbuf,
+                                    int32_t send_stride, const int32_t* dperm, int64_t max_rows,
+                                    void* stream) {
+  return agg_common(split_ws, lay, l, d, h_prev, src_row, w, sums, counts, sendbuf, send_stride,
+                    dperm, max_rows, stream);
+}
+
 extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l,
                               int32_t d, const float* h_prev, const int32_t* src_row, int32_t w,
                               int32_t dout, const float* sums, float* counts,
@@ -559,6 +682,7 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_update: bad layer/device");
   SG_REQUIRE(dout >= 1 && dout <= 256, "sage_update: dout out of range");
+  SG_REQUIRE(y.g <= 32, "sage_update: g > 32");
   if (max_rows <= 0) return SG_OK;
   UpdArgs a;
   memset(&a, 0, sizeof(a));
@@ -585,11 +709,14 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
   const size_t smem = sizeof(float) * (2 * (size_t)w * dout + 2 * (size_t)UTR * (w + 1));
   SG_REQUIRE(smem <= 227 * 1024, "sage_update: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
-  if (smem > 48 * 1024)
-    SG_CUDA(cudaFuncSetAttribute(k_sage_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  const int grid = clamp_grid(div_up(max_rows, UTR), kSMs * 4);
-  k_sage_update<<<grid, 256, smem, st>>>(meta, a);
+  const int grid = clamp_grid(div_up(max_rows, UTR), kSMs * 3);
+  if (dout % 4 == 0) {
+    SG_CUDA(allow_max_smem<k_sage_update<true>>());
+    k_sage_update<true><<<grid, 256, smem, st>>>(meta, a);
+  } else {
+    SG_CUDA(allow_max_smem<k_sage_update<false>>());
+    k_sage_update<false><<<grid, 256, smem, st>>>(meta, a);
+  }
   SG_CHECK_LAUNCH("k_sage_update");
   return SG_OK;
 }
@@ -605,7 +732,9 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_bwd_rows: bad layer/device");
   SG_REQUIRE(dout >= 1 && dout <= 32, "sage_bwd_rows: dout must be <= 32");
-  SG_REQUIRE((int64_t)w * dout <= 256 * MAXACC, "sage_bwd_rows: w*dout > 4096 unsupported");
+  const bool q4 = dout % 4 == 0;
+  SG_REQUIRE(q4 ? (int64_t)w * (dout / 4) <= 256 * BMAXQ : (int64_t)w * dout <= 256 * BMAXACC,
+             "sage_bwd_rows: w*dout > 4096 unsupported");
   SG_REQUIRE(nblocks >= 1, "sage_bwd_rows: nblocks >= 1");
   (void)max_rows;
   BwdArgs a;
@@ -628,14 +757,18 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   a.partial = partial;
   a.d_self = d_self;
   a.d_sums = d_sums;
-  const size_t smem =
-      sizeof(float) * ((size_t)BTR * dout + 2 * (size_t)BTR * (w + 1) + 2 * (size_t)w * (dout + 1) + BTR);
+  const int wst = q4 ? dout + 4 : dout + 1;
+  const size_t smem = sizeof(float) * ((size_t)BTR * dout + 2 * (size_t)w * wst +
+                                       2 * (size_t)BTR * (w + 1) + BTR);
   SG_REQUIRE(smem <= 227 * 1024, "sage_bwd_rows: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
-  if (smem > 48 * 1024)
-    SG_CUDA(cudaFuncSetAttribute(k_sage_bwd_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  k_sage_bwd_rows<<<nblocks, 256, smem, st>>>(meta, a);
+  if (q4) {
+    SG_CUDA(allow_max_smem<k_sage_bwd_rows<true>>());
+    k_sage_bwd_rows<true><<<nblocks, 256, smem, st>>>(meta, a);
+  } else {
+    SG_CUDA(allow_max_smem<k_sage_bwd_rows<false>>());
+    k_sage_bwd_rows<false><<<nblocks, 256, smem, st>>>(meta, a);
+  }
   SG_CHECK_LAUNCH("k_sage_bwd_rows");
   return SG_OK;
 }
@@ -643,7 +776,7 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
 extern "C" int sg_sage_scatter_bwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
                                    int32_t d, int32_t w, const float* d_self, const float* d_sums,
                                    const float* bwd_recv, int32_t recv_stride,
-                                   const int32_t* perm, const int32_t* srcbeg,
+                                   const int32_t* enc, const int32_t* srcbeg,
                                    const int32_t* srcend, int64_t key_base, float* d_prev,
                                    int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "sage_scatter_bwd: null workspace");
@@ -658,14 +791,10 @@ extern "C" int sg_sage_scatter_bwd(const void* split_ws, const SgSplitLayout* la
   a.stride = recv_stride;
   a.voff_lm1 = y.voff[l - 1];
   a.voff_l = y.voff[l];
-  a.pbase_l = y.pbase[l];
   a.key_base = key_base;
-  a.nV_l = y.nV[l];
   a.grouped = I32(y.o_grouped);
   a.rank = I32(y.o_rank);
-  a.ldst = I32(y.o_ldst);
-  a.sendpos = I32(y.o_sendpos);
-  a.perm = perm;
+  a.enc = enc;
   a.srcbeg = srcbeg;
   a.srcend = srcend;
   a.d_self = d_self;

@@ -16,7 +16,7 @@ namespace sg {
 namespace {
 
 constexpr int RS_THREADS = 256;
-constexpr int RS_ROUNDS = 16;
+constexpr int RS_ROUNDS = 4;
 constexpr int RS_T = RS_THREADS * RS_ROUNDS;  // 4096 elements per tile
 constexpr int RADIX = 256;
 
@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint32_t* __restr
   const unsigned lt = lanemask_lt();
   uint32_t key[RS_ROUNDS];
   int rnk[RS_ROUNDS];
+  (void)ntiles;
 #pragma unroll
   for (int j = 0; j < RS_ROUNDS; ++j) {
     const int64_t i = base + j * 32 + lane;
@@ -138,13 +139,17 @@ __global__ void k_copy_pairs(const uint32_t* __restrict__ ks, const int32_t* __r
 
 struct KeyBase {
   int64_t v[SG_MAXL];
+  int64_t pbase[SG_MAXL + 2];
 };
 
 // Edges of device d, layers [lmin, L], as (row key, edge slot). mode 0: key =
 // global source row at l-1 (+ per-layer base); mode 1: key = destination row
 // in the split's per-layer row space (owned rows then reference rows).
+// val_mode 0: value = global edge slot; 1: value = encoded destination row of
+// the backward gradient (>= 0: owned row own_off+q, < 0: -(1 + pair slot)).
 __global__ void k_edge_row_keys(const SgMeta* __restrict__ meta, const int32_t* __restrict__ lidx,
-                                int d, int lmin, int mode, KeyBase kb,
+                                const int32_t* __restrict__ ldst, const int32_t* __restrict__ sendpos,
+                                int d, int lmin, int mode, int val_mode, KeyBase kb,
                                 uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
                                 int32_t* __restrict__ n_dev) {
   const int L = meta->L;
@@ -168,7 +173,15 @@ __global__ void k_edge_row_keys(const SgMeta* __restrict__ meta, const int32_t* 
         ? meta->own_off[li][d]
         : (int64_t)meta->own_off[li + 1][d] + meta->ref_off[li + 1][d];
     keys[f] = (uint32_t)(kb.v[li] + row + lidx[x]);
-    vals[f] = (int32_t)x;
+    if (val_mode == 0) {
+      vals[f] = (int32_t)x;
+    } else {
+      const int l = li + 1;
+      const int q = ldst[x];
+      const int no = meta->n_own[l][d];
+      vals[f] = q < no ? meta->own_off[l][d] + q
+                       : -1 - sendpos[kb.pbase[l] + meta->ref_off[l][d] + (q - no)];
+    }
   }
 }
 
@@ -228,9 +241,9 @@ extern "C" int sg_sort_pairs(void* ws, int64_t n_max, const int32_t* n_dev, uint
 }
 
 extern "C" int sg_src_csr(const void* split_ws, const SgSplitLayout* lay, int32_t d,
-                          int32_t lmin, void* sort_ws, int64_t n_max, int32_t* n_dev,
-                          uint32_t* keys, int32_t* perm, int32_t* srcbeg, int32_t* srcend,
-                          int64_t n_rows_total, void* stream) {
+                          int32_t lmin, int32_t val_mode, void* sort_ws, int64_t n_max,
+                          int32_t* n_dev, uint32_t* keys, int32_t* perm, int32_t* srcbeg,
+                          int32_t* srcend, int64_t n_rows_total, void* stream) {
   SG_REQUIRE(split_ws && lay, "src_csr: null workspace");
   const SgSplitLayout& y = *lay;
   SG_REQUIRE(lmin >= 1 && lmin <= y.L, "src_csr: lmin out of range");
@@ -251,8 +264,10 @@ extern "C" int sg_src_csr(const void* split_ws, const SgSplitLayout* lay, int32_
   SG_CUDA(cudaMemsetAsync(srcbeg, 0, 4 * acc, st));
   SG_CUDA(cudaMemsetAsync(srcend, 0, 4 * acc, st));
   const int64_t e_span = y.eoff[y.L] - y.eoff[lmin - 1];
+  for (int l = 0; l <= y.L + 1; ++l) kb.pbase[l] = y.pbase[l];
   k_edge_row_keys<<<clamp_grid(div_up(e_span, 256), kSMs * 8), 256, 0, st>>>(
-      meta, (const int32_t*)(base + y.o_lsrc), d, lmin, 0, kb, keys, perm, n_dev);
+      meta, (const int32_t*)(base + y.o_lsrc), (const int32_t*)(base + y.o_ldst),
+      (const int32_t*)(base + y.o_sendpos), d, lmin, 0, val_mode, kb, keys, perm, n_dev);
   SG_CHECK_LAUNCH("k_edge_row_keys(src)");
   int rc = sg_sort_pairs(sort_ws, n_max, n_dev, keys, perm, bits, stream);
   if (rc) return rc;
@@ -276,7 +291,7 @@ extern "C" int sg_dst_csr(void* split_ws, const SgSplitLayout* lay, int32_t d, v
   int bits = 0;
   while ((int64_t(1) << bits) < y.rbase[y.L]) ++bits;
   k_edge_row_keys<<<clamp_grid(div_up(y.nEtot, 256), kSMs * 8), 256, 0, st>>>(
-      meta, (const int32_t*)(base + y.o_ldst), d, 1, 1, kb, keys, perm, n_dev);
+      meta, (const int32_t*)(base + y.o_ldst), nullptr, nullptr, d, 1, 1, 0, kb, keys, perm, n_dev);
   SG_CHECK_LAUNCH("k_edge_row_keys(dst)");
   int rc = sg_sort_pairs(sort_ws, n_max, n_dev, keys, perm, bits, stream);
   if (rc) return rc;

@@ -42,9 +42,17 @@ constexpr int MAXKQ = SG_MAXG * SG_MAXG + SG_MAXG;
 struct SegDesc {
   int nseg;
   int nkeys;
+  int mode;  // 0: position segments (lengths meta->nV[s], load segment nV[0]); 1: edges (nE[s])
   int64_t beg[MAXSEG + 1];
   int64_t tile_beg[MAXSEG + 1];
 };
+
+__device__ __forceinline__ int64_t seg_end(const SegDesc& sd, const SgMeta* meta, int s) {
+  int64_t len;
+  if (sd.mode == 0) len = (s <= meta->L) ? meta->nV[s] : meta->nV[0];
+  else len = meta->nE[s];
+  return sd.beg[s] + len;
+}
 
 struct MetaHeader {
   int32_t L, g, dst_grouped, pad;
@@ -67,7 +75,9 @@ __device__ __forceinline__ int layer_of(const int64_t* off, int nl, int64_t i) {
   return l;
 }
 
-__global__ void k_meta_init(MetaHeader h, SgMeta* meta) {
+// Header (capacity offsets) + ACTUAL sizes (device array nV[0..L], nE[0..L-1],
+// or the capacities when sizes == nullptr) -> SgMeta with zero counts.
+__global__ void k_meta_init(MetaHeader h, const int64_t* __restrict__ sizes, SgMeta* meta) {
   int32_t* w = reinterpret_cast<int32_t*>(meta);
   const int nwords = sizeof(SgMeta) / 4;
   for (int i = threadIdx.x; i < nwords; i += blockDim.x) w[i] = 0;
@@ -76,20 +86,30 @@ __global__ void k_meta_init(MetaHeader h, SgMeta* meta) {
     meta->L = h.L;
     meta->g = h.g;
     meta->dst_grouped = h.dst_grouped;
-    for (int l = 0; l <= SG_MAXL; ++l) meta->nV[l] = h.nV[l];
-    for (int l = 0; l < SG_MAXL; ++l) meta->nE[l] = h.nE[l];
+    for (int l = 0; l <= SG_MAXL; ++l) {
+      int64_t v = h.nV[l];
+      if (sizes && l <= h.L) v = min(v, sizes[l]);
+      meta->nV[l] = v;
+    }
+    for (int l = 0; l < SG_MAXL; ++l) {
+      int64_t v = h.nE[l];
+      if (sizes && l < h.L) v = min(v, sizes[h.L + 1 + l]);
+      meta->nE[l] = v;
+    }
     for (int l = 0; l < SG_MAXL + 2; ++l) meta->voff[l] = h.voff[l];
     for (int l = 0; l < SG_MAXL + 1; ++l) meta->eoff[l] = h.eoff[l];
   }
 }
 
 // dev of every position; layer-0 load key appended after nVtot.
-__global__ void k_owner_keys(const int32_t* __restrict__ V, int64_t nVtot, int64_t nV0,
-                             const uint8_t* __restrict__ asn, int64_t n_asn,
+__global__ void k_owner_keys(const int32_t* __restrict__ V, MetaHeader h, int64_t nVtot,
+                             int64_t nV0, const uint8_t* __restrict__ asn, int64_t n_asn,
                              const uint32_t* __restrict__ cache_bits, int g,
                              uint8_t* __restrict__ keys, SgMeta* meta) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nVtot;
        i += (int64_t)gridDim.x * blockDim.x) {
+    const int l = layer_of(h.voff, h.L + 1, i);
+    if (i - h.voff[l] >= meta->nV[l]) continue;  // capacity padding
     int32_t gid = V[i];
     uint8_t dv = 0;
     if (gid < 0 || gid >= n_asn) {
@@ -109,12 +129,13 @@ __global__ void k_owner_keys(const int32_t* __restrict__ V, int64_t nVtot, int64
 // ---- generic stable multisplit (counting sort by small key, per segment) ----
 
 __global__ void __launch_bounds__(MS_THREADS) ms_count(const uint8_t* __restrict__ keys, SegDesc sd,
+                                                       const SgMeta* __restrict__ meta,
                                                        int32_t* __restrict__ tilecnt) {
   __shared__ int cnt[MAXKEY];
   const int64_t t = blockIdx.x;
   const int s = seg_of_tile(sd, t);
   const int64_t base = sd.beg[s] + (t - sd.tile_beg[s]) * MS_T;
-  const int64_t end = min(base + MS_T, sd.beg[s + 1]);
+  const int64_t end = min(base + MS_T, seg_end(sd, meta, s));
   if (threadIdx.x < sd.nkeys) cnt[threadIdx.x] = 0;
   __syncthreads();
   for (int64_t i = base + threadIdx.x; i < end; i += MS_THREADS) atomicAdd(&cnt[keys[i]], 1);
@@ -175,6 +196,7 @@ __global__ void ms_scan(SegDesc sd, const int32_t* __restrict__ tilecnt,
 }
 
 __global__ void __launch_bounds__(MS_THREADS) ms_scatter(const uint8_t* __restrict__ keys, SegDesc sd,
+                                                         const SgMeta* __restrict__ meta,
                                                          const int32_t* __restrict__ tilebase,
                                                          const int32_t* __restrict__ keyoff,
                                                          int32_t* __restrict__ rank_out,
@@ -185,7 +207,7 @@ __global__ void __launch_bounds__(MS_THREADS) ms_scatter(const uint8_t* __restri
   const int s = seg_of_tile(sd, t);
   const int64_t sbeg = sd.beg[s];
   const int64_t base = sbeg + (t - sd.tile_beg[s]) * MS_T;
-  const int64_t end = min(base + MS_T, sd.beg[s + 1]);
+  const int64_t end = min(base + MS_T, seg_end(sd, meta, s));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = sd.nkeys;
   for (int k = lane; k < nk; k += 32) wcnt[warp][k] = 0;
@@ -230,12 +252,14 @@ __global__ void __launch_bounds__(MS_THREADS) ms_scatter(const uint8_t* __restri
 
 // ---- edges: source-device key + pair masks ----
 __global__ void k_edge_keys(const int32_t* __restrict__ esrc, const int32_t* __restrict__ edst,
-                            MetaHeader h, const uint8_t* __restrict__ keys,
-                            uint8_t* __restrict__ ekey, uint32_t* __restrict__ pmask) {
+                            MetaHeader h, const SgMeta* __restrict__ meta,
+                            const uint8_t* __restrict__ keys, uint8_t* __restrict__ ekey,
+                            uint32_t* __restrict__ pmask) {
   const int64_t n = h.eoff[h.L];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int li = layer_of(h.eoff, h.L, e);  // edge layer l = li + 1
+    if (e - h.eoff[li] >= meta->nE[li]) continue;  // capacity padding
     const int32_t src = esrc[e], dst = edst[e];
     const uint8_t sd = keys[h.voff[li] + src];
     const uint8_t dd = keys[h.voff[li + 1] + dst];
@@ -525,6 +549,7 @@ __global__ void k_local_edges(const int32_t* __restrict__ esrc, const int32_t* _
       const int l = li + 1;
       const int64_t eo = h.eoff[li];
       const int i = (int)(x - eo);
+      if (i >= meta->nE[li]) continue;  // capacity padding
       const int d = find_bucket(meta->edge_off[li], g, i);
       const int e = egrouped[eo + i];
       const int32_t src = esrc[eo + e], dst = edst[eo + e];
@@ -544,6 +569,7 @@ __global__ void k_local_edges(const int32_t* __restrict__ esrc, const int32_t* _
     } else {
       const int64_t y = x - nE + h.voff[1];
       const int l = layer_of(h.voff, h.L + 1, y);
+      if (y - h.voff[l] >= meta->nV[l]) continue;  // capacity padding
       const int32_t p = grouped[y];
       out.selfrow[y] = rank[h.voff[l - 1] + p];
     }
@@ -657,8 +683,9 @@ extern "C" int sg_split_layout(int32_t L, int32_t g, const int64_t* nV, const in
 }
 
 extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V,
-                            const int32_t* esrc, const int32_t* edst, const uint8_t* asn,
-                            const uint32_t* cache_bits, int32_t dst_grouped, void* stream) {
+                            const int32_t* esrc, const int32_t* edst, const int64_t* sizes,
+                            const uint8_t* asn, const uint32_t* cache_bits, int32_t dst_grouped,
+                            void* stream) {
   SG_REQUIRE(ws && lay, "split: null workspace");
   const SgSplitLayout& y = *lay;
   const int L = y.L, g = y.g;
@@ -690,13 +717,13 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
     SG_CUDA(cudaMemsetAsync(base + y.o_rowend, 0, 4 * rows_total, st));
   }
 
-  k_meta_init<<<1, 256, 0, st>>>(h, meta);
+  k_meta_init<<<1, 256, 0, st>>>(h, sizes, meta);
   SG_CHECK_LAUNCH("k_meta_init");
 
   const int64_t nVtot = y.nVtot, nV0 = y.nV[0];
   if (nVtot > 0) {
     k_owner_keys<<<clamp_grid(div_up(nVtot, 256), kSMs * 8), 256, 0, st>>>(
-        V, nVtot, nV0, asn, y.n_vertices, cache_bits, g, P8(y.o_keys), meta);
+        V, h, nVtot, nV0, asn, y.n_vertices, cache_bits, g, P8(y.o_keys), meta);
     SG_CHECK_LAUNCH("k_owner_keys");
   }
 
@@ -705,6 +732,7 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   memset(&sp, 0, sizeof(sp));
   sp.nseg = L + 2;
   sp.nkeys = g + 1;
+  sp.mode = 0;
   {
     int64_t t = 0;
     for (int s = 0; s <= L; ++s) {
@@ -721,13 +749,13 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   int32_t* tb_pos = P32(y.o_tilebase_pos);
   int32_t* keyoff_pos = tb_pos + y.pos_tiles * (g + 1);
   if (y.pos_tiles > 0) {
-    ms_count<<<(int)y.pos_tiles, MS_THREADS, 0, st>>>(P8(y.o_keys), sp, P32(y.o_tiles_pos));
+    ms_count<<<(int)y.pos_tiles, MS_THREADS, 0, st>>>(P8(y.o_keys), sp, meta, P32(y.o_tiles_pos));
     SG_CHECK_LAUNCH("ms_count(pos)");
   }
   ms_scan<<<sp.nseg, 1024, 0, st>>>(sp, P32(y.o_tiles_pos), tb_pos, keyoff_pos, 0, meta);
   SG_CHECK_LAUNCH("ms_scan(pos)");
   if (y.pos_tiles > 0) {
-    ms_scatter<<<(int)y.pos_tiles, MS_THREADS, 0, st>>>(P8(y.o_keys), sp, tb_pos, keyoff_pos,
+    ms_scatter<<<(int)y.pos_tiles, MS_THREADS, 0, st>>>(P8(y.o_keys), sp, meta, tb_pos, keyoff_pos,
                                                         P32(y.o_rank), P32(y.o_grouped));
     SG_CHECK_LAUNCH("ms_scatter(pos)");
   }
@@ -736,13 +764,14 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   const int64_t nEtot = y.nEtot;
   if (nEtot > 0) {
     k_edge_keys<<<clamp_grid(div_up(nEtot, 256), kSMs * 8), 256, 0, st>>>(
-        esrc, edst, h, P8(y.o_keys), P8(y.o_ekey), U32(y.o_pmask));
+        esrc, edst, h, meta, P8(y.o_keys), P8(y.o_ekey), U32(y.o_pmask));
     SG_CHECK_LAUNCH("k_edge_keys");
   }
   SegDesc se;
   memset(&se, 0, sizeof(se));
   se.nseg = L;
   se.nkeys = g;
+  se.mode = 1;
   {
     int64_t t = 0;
     for (int s = 0; s < L; ++s) {
@@ -756,13 +785,13 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   int32_t* tb_edge = P32(y.o_tilebase_edge);
   int32_t* keyoff_edge = tb_edge + y.edge_tiles * g;
   if (y.edge_tiles > 0) {
-    ms_count<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, P32(y.o_tiles_edge));
+    ms_count<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, meta, P32(y.o_tiles_edge));
     SG_CHECK_LAUNCH("ms_count(edge)");
   }
   ms_scan<<<se.nseg, 1024, 0, st>>>(se, P32(y.o_tiles_edge), tb_edge, keyoff_edge, 1, meta);
   SG_CHECK_LAUNCH("ms_scan(edge)");
   if (y.edge_tiles > 0) {
-    ms_scatter<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, tb_edge, keyoff_edge,
+    ms_scatter<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, meta, tb_edge, keyoff_edge,
                                                          nullptr, P32(y.o_egrouped));
     SG_CHECK_LAUNCH("ms_scatter(edge)");
   }

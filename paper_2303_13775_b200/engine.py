@@ -30,7 +30,11 @@ from paper_2303_13775_b200.sampling import epoch_batches, sample_minibatch
 from paper_2303_13775_b200.scheduler import DeviceSplit, split_minibatch
 
 DEBUG_CHECK_FINITE = False
-NB_PARTIAL = 2 * 148  # blocks of the deterministic partial reductions
+NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions
+
+
+def _nblocks(rows, tile=32):
+    return int(max(1, min(NB_PARTIAL, (int(rows) + tile - 1) // tile)))
 
 
 def _r4(x):
@@ -163,7 +167,7 @@ class SplitStep:
                 raise FloatingPointError(f"non-finite values in graphsage layer {l} output")
 
     # -- loss + backward -----------------------------------------------------------
-    def _src_csr(self, lmin):
+    def _src_csr(self, lmin, val_mode=1):
         ds, st = self.ds, _lib.stream_ptr()
         n_max = max(int(ds.lay.nEtot - ds.lay.eoff[lmin - 1]), 1)
         rows = max(sum(ds.nV[l - 1] for l in range(lmin, self.L + 1)), 1)
@@ -175,8 +179,8 @@ class SplitStep:
             ndev = torch.empty(1, dtype=torch.int32, device=self.dev)
             beg = torch.empty(rows, dtype=torch.int32, device=self.dev)
             end = torch.empty(rows, dtype=torch.int32, device=self.dev)
-            _lib.call("sg_src_csr", _lib.ptr(ds.ws), ds.lay, d, lmin, _lib.ptr(ws), n_max, _lib.ptr(ndev),
-                      _lib.ptr(keys), _lib.ptr(perm), _lib.ptr(beg), _lib.ptr(end), rows, st)
+            _lib.call("sg_src_csr", _lib.ptr(ds.ws), ds.lay, d, lmin, val_mode, _lib.ptr(ws), n_max,
+                      _lib.ptr(ndev), _lib.ptr(keys), _lib.ptr(perm), _lib.ptr(beg), _lib.ptr(end), rows, st)
             out[d] = (perm, beg, end, ws, keys, ndev)
         kb, acc = {}, 0
         for l in range(lmin, self.L + 1):
@@ -194,11 +198,12 @@ class SplitStep:
         ncls = hid * C + C + 1
         self._partials = []
         for d in self.devices:
-            part = _f32(NB_PARTIAL * ncls, device=self.dev)
+            nb = _nblocks(self.n_own(L, d))
+            part = _f32(nb * ncls, device=self.dev)
             _lib.call("sg_cls_loss", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(ds.V), _lib.ptr(self.labels),
                       _lib.ptr(self.h[L]), hid, C, _lib.ptr(p.view("cls.w")), _lib.ptr(p.view("cls.b")),
-                      _lib.ptr(self.d_h), _lib.ptr(part), NB_PARTIAL, self.n_own(L, d), st)
-            self.jobs.append((part, NB_PARTIAL, ncls, self.grads[d], p.offset("cls.w")))
+                      _lib.ptr(self.d_h), _lib.ptr(part), nb, self.n_own(L, d), st)
+            self.jobs.append((part, nb, ncls, self.grads[d], p.offset("cls.w")))
             self._partials.append(part)
 
     def backward(self):
@@ -222,14 +227,15 @@ class SplitStep:
             d_sums = _f32(nV, w, device=self.dev) if need_prev else None
             npart = 2 * w * dout + dout
             for d in self.devices:
-                part = _f32(NB_PARTIAL * npart, device=self.dev)
+                nb = _nblocks(self.n_own(l, d))
+                part = _f32(nb * npart, device=self.dev)
                 _lib.call("sg_sage_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
                           _lib.ptr(src_row), w, dout, _lib.ptr(d_h), _lib.ptr(self.h[l]), final,
                           _lib.ptr(self.keep[l]["mean"]), _lib.ptr(self.keep[l]["counts"]),
                           _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
-                          _lib.ptr(part), NB_PARTIAL, _lib.ptr(d_self), _lib.ptr(d_sums),
+                          _lib.ptr(part), nb, _lib.ptr(d_self), _lib.ptr(d_sums),
                           self.n_own(l, d), st)
-                self.jobs.append((part, NB_PARTIAL, npart, self.grads[d], p.offset(f"layer{l-1}.w_self")))
+                self.jobs.append((part, nb, npart, self.grads[d], p.offset(f"layer{l-1}.w_self")))
                 self._partials.append(part)
             if not need_prev:
                 break
@@ -606,3 +612,123 @@ def train_model(graph, pm, cache, labels, *, model_kind, num_layers, hidden, fan
     records = [trainer.run_epoch(mode, params, seed=seed, epoch=e, fanouts=fanouts, batch_size=batch_size,
                                  lr=lr, workers=workers, train_set=train_set) for e in range(epochs)]
     return records, params
+
+
+# ---- CUDA-graph captured step ------------------------------------------------------
+
+class StaticSample:
+    """Fixed-capacity device buffers holding one sample (CUDA-graph inputs).
+
+    Layer l's vertices live at the capacity offset voff[l]; the actual sizes
+    go to a small device array the kernels read, so one captured graph serves
+    every sample that fits the capacities."""
+
+    def __init__(self, cap_nV, cap_nE, device):
+        self.cap_nV = [int(x) for x in cap_nV]
+        self.cap_nE = [int(x) for x in cap_nE]
+        self.L = len(self.cap_nE)
+        self.voff = np.r_[0, np.cumsum(self.cap_nV)].astype(np.int64)
+        self.eoff = np.r_[0, np.cumsum(self.cap_nE)].astype(np.int64)
+        dev = torch.device(device)
+        self.V = torch.zeros(int(self.voff[-1]), dtype=torch.int32, device=dev)
+        self.es = torch.zeros(max(int(self.eoff[-1]), 1), dtype=torch.int32, device=dev)
+        self.ed = torch.zeros(max(int(self.eoff[-1]), 1), dtype=torch.int32, device=dev)
+        self.sizes = torch.zeros(2 * self.L + 1, dtype=torch.int64, device=dev)
+        self.hV = torch.zeros(self.V.shape, dtype=torch.int32).pin_memory()
+        self.hes = torch.zeros(self.es.shape, dtype=torch.int32).pin_memory()
+        self.hed = torch.zeros(self.ed.shape, dtype=torch.int32).pin_memory()
+        self.hsizes = torch.zeros(self.sizes.shape, dtype=torch.int64).pin_memory()
+        self.bytes_h2d = 0
+
+    def fits(self, sample):
+        nV, nE = sample.sizes()
+        return all(a <= b for a, b in zip(nV, self.cap_nV)) and all(a <= b for a, b in zip(nE, self.cap_nE))
+
+    def load(self, sample):
+        """Stage the sample into pinned memory and copy it to the device
+        buffers (async, on the current stream)."""
+        if not self.fits(sample):
+            raise ValueError("sample exceeds the captured capacities")
+        if not sample.is_dst_grouped():
+            raise ValueError("captured steps need destination-grouped samples")
+        hV, hes, hed = self.hV.numpy(), self.hes.numpy(), self.hed.numpy()
+        nV, nE = sample.sizes()
+        for l, v in enumerate(sample.layer_vertices):
+            hV[self.voff[l]:self.voff[l] + nV[l]] = v
+        for l, (s, d) in enumerate(sample.layer_edges):
+            hes[self.eoff[l]:self.eoff[l] + nE[l]] = s
+            hed[self.eoff[l]:self.eoff[l] + nE[l]] = d
+        self.hsizes.numpy()[:] = list(nV) + list(nE)
+        # only the used prefix of each buffer crosses PCIe
+        nv_used = int(self.voff[self.L] + nV[self.L])
+        ne_used = int(self.eoff[self.L - 1] + nE[self.L - 1])
+        self.V[:nv_used].copy_(self.hV[:nv_used], non_blocking=True)
+        self.es[:ne_used].copy_(self.hes[:ne_used], non_blocking=True)
+        self.ed[:ne_used].copy_(self.hed[:ne_used], non_blocking=True)
+        self.sizes.copy_(self.hsizes, non_blocking=True)
+        self.bytes_h2d = 4 * nv_used + 8 * ne_used + 8 * self.sizes.numel()
+        return self.bytes_h2d
+
+
+def capacities_for(samples, slack=1.0):
+    """Per-layer capacities covering `samples` (optionally with slack)."""
+    L = samples[0].num_layers
+    nV = [max(s.sizes()[0][l] for s in samples) for l in range(L + 1)]
+    nE = [max(s.sizes()[1][l] for s in samples) for l in range(L)]
+    return [int(np.ceil(x * slack)) for x in nV], [int(np.ceil(x * slack)) for x in nE]
+
+
+class CapturedStep:
+    """The whole split-parallel training step of the single-GPU (g = 1) case
+    captured once as a CUDA graph: split -> layer-0 rows -> forward -> loss ->
+    backward -> gradient reduction -> SGD, replayed per sample with only the
+    sample's H2D copy in front. Kernels read every size from device memory."""
+
+    def __init__(self, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale,
+                 device="cuda", record_events=False):
+        if pm.num_devices != 1:
+            raise ValueError("CapturedStep covers the single-GPU split (g = 1)")
+        self.p = dparams
+        self.pm, self.cache, self.f, self.labels = pm, cache, feats, labels_dev
+        self.dev = torch.device(device)
+        self.inp = StaticSample(cap_nV, cap_nE, self.dev)
+        self.scale = float(lr_scale)
+        self.record_events = record_events
+        self.graph = None
+
+    def _body(self):
+        inp = self.inp
+        ds = DeviceSplit(inp.V, inp.es, inp.ed, inp.cap_nV, inp.cap_nE, self.pm, self.cache, True,
+                         self.dev, sizes=inp.sizes)
+        step = SplitStep(self.p, ds, self.f, self.labels, exact=False, record_events=self.record_events)
+        step.run()
+        gbuf = step.grads[0]
+        ptrs = np.asarray([gbuf.data_ptr()], dtype=np.int64)
+        _lib.call("sg_sum_sgd", _lib.ptr(self.p.flat), None, _lib.ptr(ptrs), 1, self.p.n,
+                  self.scale, _lib.stream_ptr())
+        self.ds, self.step = ds, step
+        return gbuf
+
+    def capture(self, warm_sample):
+        """Eager warm-up on the static buffers, then capture. The warm-up
+        applies real SGD updates (it is a training step); callers that need
+        untouched parameters restore them afterwards."""
+        self.inp.load(warm_sample)
+        self._body()
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = self._body()
+        torch.cuda.synchronize()
+        return self
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+    def run(self, sample):
+        self.inp.load(sample)
+        return self.replay()
+
+    def loss_sum(self):
+        return self.out[self.p.n]

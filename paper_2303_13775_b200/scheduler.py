@@ -133,7 +133,10 @@ class DeviceSplit:
     receive slots (recv_off, owner-major)."""
 
     def __init__(self, V, esrc, edst, nV, nE, pm: PartitionMap, cache: CacheState | None,
-                 dst_grouped: bool, device=None, host_V=None):
+                 dst_grouped: bool, device=None, host_V=None, sizes=None):
+        """nV / nE are the CAPACITIES the layout is built for; `sizes` (device
+        int64 [nV_0..nV_L, nE_1..nE_L]) gives the actual sizes (default: the
+        capacities). V / esrc / edst hold layer l at the capacity offsets."""
         lib = _lib.load()
         self.device = torch.device(device or "cuda")
         self.pm = pm
@@ -153,8 +156,9 @@ class DeviceSplit:
         self.V, self.esrc, self.edst = V, esrc, edst
         self.host_V = host_V
         bits = cache.device_bits(len(pm.assignment), self.device) if cache is not None else None
+        self.sizes = sizes
         _lib.check(lib.sg_split_run(_lib.ptr(self.ws), C.byref(lay), _lib.ptr(V), _lib.ptr(esrc),
-                                    _lib.ptr(edst), _lib.ptr(pm.device_u8(self.device)),
+                                    _lib.ptr(edst), _lib.ptr(sizes), _lib.ptr(pm.device_u8(self.device)),
                                     _lib.ptr(bits), int(self.dst_grouped), _lib.stream_ptr()),
                    "split_run")
         self._meta = None
@@ -219,7 +223,7 @@ class DeviceSplit:
         V = self.host_V if self.host_V is not None else self.V.cpu().numpy()
         V = np.asarray(V, dtype=np.int64)
         vo, eo = self.voff, self.eoff
-        Vl = [V[vo[l]:vo[l + 1]] for l in range(L + 1)]
+        Vl = [V[vo[l]:vo[l] + int(m.nV[l])] for l in range(L + 1)]
         grouped = arr(lay.o_grouped, nVtot + self.nV[0])
         rank = arr(lay.o_rank, nVtot + self.nV[0])
         lsrc = arr(lay.o_lsrc, lay.nEtot)

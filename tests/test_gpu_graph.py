@@ -1,0 +1,50 @@
+"""The CUDA-graph captured step (capacity layouts, sizes read from device
+memory) trains exactly like the eager step and the oracle."""
+
+import numpy as np
+import pytest
+
+from helpers import rel_err
+from oracle.coop_oracle import CoopRun, reduce_and_sgd
+from oracle.model_oracle import glorot_params
+from oracle.split_oracle import split_sample
+
+pytestmark = pytest.mark.gpu
+
+
+def test_captured_step_matches_oracle_over_steps():
+    import torch
+
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200.engine import CapturedStep, capacities_for
+    graph = sg.generate_powerlaw(20000, 200000, blocks=16, p_local=0.8, seed=9)
+    pm = sg.range_partition(graph.num_vertices, 1)
+    cache = sg.full_cache(pm)
+    F, C, B = 32, 6, 96
+    feats = sg.FeatureStore.synthetic(graph.num_vertices, F, seed=1)
+    hostX = sg.synthetic_features(graph.num_vertices, F, seed=1).astype(np.float64)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
+    rng = np.random.default_rng(3)
+    samples = [sg.sample_minibatch(graph, rng.choice(graph.num_vertices, B, replace=False), [8, 6, 4], rng)
+               for _ in range(6)]
+    cap_nV, cap_nE = capacities_for(samples, slack=1.1)
+    params = sg.init_params("graphsage", F, 16, C, 3, seed=4)
+    dp = sg.DeviceParams.from_host(params)
+    lab = torch.from_numpy(labels).cuda()
+    cs = CapturedStep(dp, pm, cache, feats, lab, cap_nV, cap_nE, 0.1 / B)
+    cs.capture(samples[0])  # applies step 0 eagerly
+    ref = glorot_params("graphsage", F, 16, C, 3, seed=4)
+    losses = []
+    for i, smp in enumerate(samples):
+        if i > 0:
+            cs.run(smp)
+        losses.append(float(cs.out[dp.n].item()) if i > 0 else None)
+        ws, wp = split_sample(smp.layer_vertices, smp.layer_edges, pm.assignment, 1, cache.cached)
+        run = CoopRun(ref, ws, wp, hostX, labels)
+        rl, rg = run.run()
+        reduce_and_sgd(ref, rg, 0.1, B)
+        if i > 0:
+            assert abs(losses[-1] - rl) <= 1e-4 * abs(rl), (i, losses[-1], rl)
+    got = dp.to_host().tensors()
+    for k in ref:
+        assert rel_err(got[k], ref[k]) < 1e-4, k
