@@ -86,7 +86,10 @@ class SplitStep:
     def _ev(self, name):
         if self.events is None:
             return None
-        e = torch.cuda.Event(enable_timing=True)
+        try:  # external=True: a real event-record node when captured in a CUDA graph
+            e = torch.cuda.Event(enable_timing=True, external=True)
+        except TypeError:
+            e = torch.cuda.Event(enable_timing=True)
         e.record()
         self.events.setdefault(name, []).append(e)
         return e

@@ -51,10 +51,13 @@ class PartitionMap:
     def device_u8(self, device="cuda"):
         """uint8 copy of the map resident on the GPU (cached)."""
         import torch
-        if self._dev_u8 is None or str(self._dev_u8.device) != str(torch.device(device)):
+        dev = torch.device(device)
+        if dev.type == "cuda" and dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        if self._dev_u8 is None or self._dev_u8.device != dev:
             if self.num_devices > 16:
                 raise ValueError("the B200 splitter supports at most 16 devices")
-            self._dev_u8 = torch.from_numpy(self.assignment.astype(np.uint8)).to(device)
+            self._dev_u8 = torch.from_numpy(self.assignment.astype(np.uint8)).to(dev)
         return self._dev_u8
 
 
