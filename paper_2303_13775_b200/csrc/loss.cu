@@ -16,7 +16,7 @@
 namespace sg {
 namespace {
 
-constexpr int LTR = 32;  // rows per tile
+constexpr int LTR = 8;  // rows per tile (small: the batch is only ~1K rows)
 constexpr int LMAXACC = 24;
 
 struct LossArgs {
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k_cls_loss(const SgMeta* __restrict__ met
       lg_s[rr * cp + c] = acc;
     }
     __syncthreads();
-    for (int rr = warp; rr < LTR; rr += 8) {
+    for (int rr = warp; rr < LTR; rr += 8) {  // one warp per row
       const int y = y_s[rr];
       if (y < 0) {
         for (int c = lane; c < C; c += 32) lg_s[rr * cp + c] = 0.f;

@@ -84,11 +84,16 @@ struct AggArgs {
   float* sendbuf;
 };
 
-template <int VEC, int LPR, int NCH>
+// A row "team" of RL = LPR*EG lanes: LPR lanes cover the row width (VEC floats
+// each), EG edge groups take every EG-th in-edge, then a fixed xor-tree adds
+// the groups (deterministic). Each round the team fetches RL edge indices at
+// once (both index hops in parallel), then issues the row loads back to back.
+template <int VEC, int LPR, int EG, int NCH>
 __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ meta, AggArgs a) {
   using V = VecT<VEC>;
   using T = typename V::T;
-  constexpr int RPW = 32 / LPR;
+  constexpr int RL = LPR * EG;
+  constexpr int RPW = 32 / RL;
   const int l = a.l, d = a.d, w = a.w;
   const int n_own = meta->n_own[l][d];
   const int R = n_own + meta->n_ref[l][d];
@@ -96,57 +101,75 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
   const int prev0 = meta->own_off[l - 1][d];
   const int64_t rb = a.rbase_li + own0 + ref0;
   const int lane = threadIdx.x & 31;
-  const int sub = lane / LPR, lr = lane % LPR;
-  const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+  const int team = lane / RL, tl = lane % RL;
+  const int eg = tl / LPR, lr = tl % LPR;
+  const unsigned tmask = (RL == 32) ? 0xffffffffu : (((1u << RL) - 1u) << (team * RL));
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // all row groups of a warp run the same number of iterations (shuffles)
-  const int64_t iters = (R + nw * RPW - 1) / (nw * RPW);
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t q = (it * nw + gw) * RPW + sub;
-    const bool live = q < R;
-    const int b = live ? a.rowbeg[rb + q] : 0;
-    const int e = live ? a.rowend[rb + q] : 0;
+  for (int64_t q = gw * RPW + team; q < R; q += nw * RPW) {
+    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
     T acc[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) acc[c] = V::zero();
-    for (int jb = b; jb < e; jb += LPR) {
-      // round: lane lr fetches edge jb+lr's physical source row (2 hops, in parallel)
-      const int j = jb + lr;
+    for (int jb = b; jb < e; jb += RL) {
+      const int j = jb + tl;
       int r = 0;
       if (j < e) {
         const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
         r = prev0 + a.lsrc[x];
         if (a.src_row) r = a.src_row[r];
       }
-      const int cnt = min(LPR, e - jb);
-      int k = 0;
-      for (; k + 8 <= cnt; k += 8) {
-        int rr[8];
+      const int cnt = min(RL, e - jb);
+      const int rounds = (cnt + EG - 1) / EG;
+      int kk = 0;
+      for (; kk + 4 <= rounds; kk += 4) {
+        int rr[4];
+        bool ok[4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) rr[u] = __shfl_sync(gmask, r, k + u, LPR);
+        for (int u = 0; u < 4; ++u) {
+          const int k = (kk + u) * EG + eg;
+          rr[u] = __shfl_sync(tmask, r, k < RL ? k : RL - 1, RL);
+          ok[u] = k < cnt;
+        }
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           const int col = (c * LPR + lr) * VEC;
           if (col < w) {
-            T v[8];
+            T v[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = V::ld(a.h_prev + (int64_t)rr[u] * w + col);
+            for (int u = 0; u < 4; ++u) v[u] = ok[u] ? V::ld(a.h_prev + (int64_t)rr[u] * w + col) : V::zero();
 #pragma unroll
-            for (int u = 0; u < 8; ++u) V::add(acc[c], v[u]);
+            for (int u = 0; u < 4; ++u) V::add(acc[c], v[u]);
           }
         }
       }
-      for (; k < cnt; ++k) {
-        const int r0 = __shfl_sync(gmask, r, k, LPR);
+      for (; kk < rounds; ++kk) {
+        const int k = kk * EG + eg;
+        const int r0 = __shfl_sync(tmask, r, k < RL ? k : RL - 1, RL);
+        if (k < cnt) {
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-          const int col = (c * LPR + lr) * VEC;
-          if (col < w) V::add(acc[c], V::ld(a.h_prev + (int64_t)r0 * w + col));
+          for (int c = 0; c < NCH; ++c) {
+            const int col = (c * LPR + lr) * VEC;
+            if (col < w) V::add(acc[c], V::ld(a.h_prev + (int64_t)r0 * w + col));
+          }
         }
       }
     }
-    if (!live) continue;
+#pragma unroll
+    for (int o = LPR; o < RL; o <<= 1) {
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        if constexpr (VEC == 4) {
+          acc[c].x += __shfl_xor_sync(tmask, acc[c].x, o, RL);
+          acc[c].y += __shfl_xor_sync(tmask, acc[c].y, o, RL);
+          acc[c].z += __shfl_xor_sync(tmask, acc[c].z, o, RL);
+          acc[c].w += __shfl_xor_sync(tmask, acc[c].w, o, RL);
+        } else {
+          acc[c] += __shfl_xor_sync(tmask, acc[c], o, RL);
+        }
+      }
+    }
+    if (eg != 0) continue;
     const float cntf = (float)(e - b);
     if (q < n_own) {
       float* out = a.sums + (int64_t)(own0 + q) * w;
@@ -171,11 +194,11 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
   }
 }
 
-template <int VEC, int LPR, int NCH>
+template <int VEC, int LPR, int EG, int NCH>
 int launch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStream_t st) {
-  constexpr int RPB = 8 * (32 / LPR);  // rows per 256-thread block
+  constexpr int RPB = 8 * (32 / (LPR * EG));  // rows per 256-thread block
   const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
-  k_sage_agg<VEC, LPR, NCH><<<grid, 256, 0, st>>>(meta, a);
+  k_sage_agg<VEC, LPR, EG, NCH><<<grid, 256, 0, st>>>(meta, a);
   SG_CHECK_LAUNCH("k_sage_agg");
   return SG_OK;
 }
@@ -184,17 +207,17 @@ int launch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStrea
 int dispatch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStream_t st) {
   const int w = a.w;
   if (w % 4 == 0) {
-    if (w <= 16) return launch_agg<4, 4, 1>(meta, a, max_rows, st);
-    if (w <= 32) return launch_agg<4, 8, 1>(meta, a, max_rows, st);
-    if (w <= 64) return launch_agg<4, 16, 1>(meta, a, max_rows, st);
-    if (w <= 128) return launch_agg<4, 32, 1>(meta, a, max_rows, st);
-    if (w <= 256) return launch_agg<4, 32, 2>(meta, a, max_rows, st);
-    if (w <= 512) return launch_agg<4, 32, 4>(meta, a, max_rows, st);
+    if (w <= 16) return launch_agg<4, 4, 4, 1>(meta, a, max_rows, st);
+    if (w <= 32) return launch_agg<4, 8, 4, 1>(meta, a, max_rows, st);
+    if (w <= 64) return launch_agg<4, 16, 2, 1>(meta, a, max_rows, st);
+    if (w <= 128) return launch_agg<4, 32, 1, 1>(meta, a, max_rows, st);
+    if (w <= 256) return launch_agg<4, 32, 1, 2>(meta, a, max_rows, st);
+    if (w <= 512) return launch_agg<4, 32, 1, 4>(meta, a, max_rows, st);
   } else {
-    if (w <= 8) return launch_agg<1, 8, 1>(meta, a, max_rows, st);
-    if (w <= 32) return launch_agg<1, 32, 1>(meta, a, max_rows, st);
-    if (w <= 128) return launch_agg<1, 32, 4>(meta, a, max_rows, st);
-    if (w <= 512) return launch_agg<1, 32, 16>(meta, a, max_rows, st);
+    if (w <= 8) return launch_agg<1, 8, 4, 1>(meta, a, max_rows, st);
+    if (w <= 32) return launch_agg<1, 32, 1, 1>(meta, a, max_rows, st);
+    if (w <= 128) return launch_agg<1, 32, 1, 4>(meta, a, max_rows, st);
+    if (w <= 512) return launch_agg<1, 32, 1, 16>(meta, a, max_rows, st);
   }
   set_error("sage_agg_fwd: width > 512 unsupported");
   return SG_ERR_ARG;
@@ -228,6 +251,9 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
   float* wn_s = ws_s + w * dout;   // [w][dout]
   float* hs_s = wn_s + w * dout;   // [UTR][w+1]
   float* mn_s = hs_s + UTR * wp;   // [UTR][w+1]
+  float* n_s = mn_s + UTR * wp;    // [UTR]
+  int* prow_s = (int*)(n_s + UTR); // [UTR]
+  int* cs_s = prow_s + UTR;        // [UTR][g]
   for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
     ws_s[i] = a.ws[i];
     wn_s[i] = a.wn[i];
@@ -235,43 +261,47 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
   const int l = a.l, d = a.d, g = a.g;
   const int n_own = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d], prev0 = meta->own_off[l - 1][d];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = (n_own + UTR - 1) / UTR;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     __syncthreads();
-    for (int rr = warp; rr < UTR; rr += 8) {
+    // A1: one thread per row resolves the row's indices (all rows in parallel)
+    if (threadIdx.x < UTR) {
+      const int rr = threadIdx.x;
       const int q = tile * UTR + rr;
-      if (q >= n_own) continue;
-      const int G = own0 + q;
-      float N = a.counts[G];
-      const int* cb = a.contrib + (int64_t)g * a.voff_l + (int64_t)G * g;
-      // the owner combines holders' partials in ascending sender order
-      int rs_l = lane < g ? cb[lane] : -1;
-      unsigned has = __ballot_sync(0xffffffffu, rs_l >= 0);
-      for (unsigned m = has; m; m &= m - 1) {
-        const int s = __ffs(m) - 1;
-        const int rs = __shfl_sync(0xffffffffu, rs_l, s);
-        N += a.recv[(int64_t)rs * a.stride + w];
-      }
-      int r = prev0 + a.selfrow[a.voff_l + G];
-      if (a.src_row) r = a.src_row[r];
-      const float* hrow = a.h_prev + (int64_t)r * w;
-      for (int c0 = 0; c0 < w; c0 += 32) {  // all lanes iterate: shuffles stay warp-wide
-        const int c = c0 + lane;
-        float S = c < w ? a.sums[(int64_t)G * w + c] : 0.f;
-        for (unsigned m = has; m; m &= m - 1) {
-          const int s = __ffs(m) - 1;
-          const int rs = __shfl_sync(0xffffffffu, rs_l, s);
-          if (c < w) S += a.recv[(int64_t)rs * a.stride + c];
+      if (q < n_own) {
+        const int G = own0 + q;
+        float N = a.counts[G];
+        const int* cb = a.contrib + (int64_t)g * a.voff_l + (int64_t)G * g;
+        for (int s = 0; s < g; ++s) {  // ascending sender order (engine.py:130-138)
+          const int rs = cb[s];
+          cs_s[rr * g + s] = rs;
+          if (rs >= 0) N += a.recv[(int64_t)rs * a.stride + w];
         }
-        if (c < w) {
-          const float mv = S / N;
-          mn_s[rr * wp + c] = mv;
-          a.mean[(int64_t)G * w + c] = mv;
-          hs_s[rr * wp + c] = __ldg(hrow + c);
-        }
+        int r = prev0 + a.selfrow[a.voff_l + G];
+        if (a.src_row) r = a.src_row[r];
+        prow_s[rr] = r;
+        n_s[rr] = N;
+        a.counts[G] = N;
       }
-      if (lane == 0) a.counts[G] = N;
+    }
+    __syncthreads();
+    // A2: coalesced tile loads (many independent loads in flight per thread)
+    {
+      const int nrow = min(UTR, n_own - tile * UTR);
+#pragma unroll 4
+      for (int idx = threadIdx.x; idx < nrow * w; idx += blockDim.x) {
+        const int rr = idx / w, c = idx - rr * w;
+        const int64_t G = own0 + tile * UTR + rr;
+        float S = a.sums[G * w + c];
+        for (int s = 0; s < g; ++s) {
+          const int rs = cs_s[rr * g + s];
+          if (rs >= 0) S += a.recv[(int64_t)rs * a.stride + c];
+        }
+        const float mv = S / n_s[rr];
+        mn_s[rr * wp + c] = mv;
+        a.mean[G * w + c] = mv;
+        hs_s[rr * wp + c] = __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c);
+      }
     }
     __syncthreads();
     if (Q4) {
@@ -349,6 +379,7 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
   float* hs_s = wn_s + w * wst;        // [BTR][w+1]
   float* mn_s = hs_s + BTR * wp;       // [BTR][w+1]
   float* cnt_s = mn_s + BTR * wp;      // [BTR]
+  int* prow_s = (int*)(cnt_s + BTR);   // [BTR]
   if (need_c) {
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
@@ -359,7 +390,6 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
   const int l = a.l, d = a.d;
   const int n_own = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d], prev0 = meta->own_off[l - 1][d];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nq = dout >> 2;
   const int nslots = Q4 ? w * nq : w * dout;
   float4 aS4[BMAXQ], aN4[BMAXQ];
@@ -372,32 +402,43 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
   const int ntiles = (n_own + BTR - 1) / BTR;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     __syncthreads();
-    for (int rr = warp; rr < BTR; rr += 8) {
+    if (threadIdx.x < BTR) {
+      const int rr = threadIdx.x;
       const int q = tile * BTR + rr;
-      const bool valid = q < n_own;
-      const int G = own0 + q;
-      for (int j = lane; j < dout; j += 32) {
-        float v = 0.f;
-        if (valid) {
-          v = a.d_h[(int64_t)G * dout + j];
-          if (!a.final_ && !(a.h[(int64_t)G * dout + j] > 0.f)) v = 0.f;
-        }
-        dp_s[rr * dout + j] = v;
-      }
-      if (valid) {
+      if (q < n_own) {
+        const int G = own0 + q;
         int r = prev0 + a.selfrow[a.voff_l + G];
         if (a.src_row) r = a.src_row[r];
-        const float* hrow = a.h_prev + (int64_t)r * w;
-        const float* mrow = a.mean + (int64_t)G * w;
-        for (int c = lane; c < w; c += 32) {
-          hs_s[rr * wp + c] = __ldg(hrow + c);
-          mn_s[rr * wp + c] = mrow[c];
-        }
-        if (lane == 0) cnt_s[rr] = a.counts[G];
+        prow_s[rr] = r;
+        cnt_s[rr] = a.counts[G];
       } else {
-        for (int c = lane; c < w; c += 32) hs_s[rr * wp + c] = mn_s[rr * wp + c] = 0.f;
-        if (lane == 0) cnt_s[rr] = 1.f;
+        prow_s[rr] = -1;
+        cnt_s[rr] = 1.f;
       }
+    }
+    for (int idx = threadIdx.x; idx < BTR * dout; idx += blockDim.x) {
+      const int rr = idx / dout, j = idx - rr * dout;
+      const int q = tile * BTR + rr;
+      float v = 0.f;
+      if (q < n_own) {
+        const int64_t G = own0 + q;
+        v = a.d_h[G * dout + j];
+        if (!a.final_ && !(a.h[G * dout + j] > 0.f)) v = 0.f;
+      }
+      dp_s[idx] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < BTR * w; idx += blockDim.x) {
+      const int rr = idx / w, c = idx - rr * w;
+      const int pr = prow_s[rr];
+      float hv = 0.f, mv = 0.f;
+      if (pr >= 0) {
+        hv = __ldg(a.h_prev + (int64_t)pr * w + c);
+        mv = a.mean[(int64_t)(own0 + tile * BTR + rr) * w + c];
+      }
+      hs_s[rr * wp + c] = hv;
+      mn_s[rr * wp + c] = mv;
     }
     __syncthreads();
     if (Q4) {
@@ -706,7 +747,8 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
   a.bias = bias;
   a.mean = mean;
   a.h = h;
-  const size_t smem = sizeof(float) * (2 * (size_t)w * dout + 2 * (size_t)UTR * (w + 1));
+  const size_t smem = sizeof(float) * (2 * (size_t)w * dout + 2 * (size_t)UTR * (w + 1) +
+                                       (size_t)UTR * (2 + y.g));
   SG_REQUIRE(smem <= 227 * 1024, "sage_update: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = clamp_grid(div_up(max_rows, UTR), kSMs * 3);
@@ -759,7 +801,7 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   a.d_sums = d_sums;
   const int wst = q4 ? dout + 4 : dout + 1;
   const size_t smem = sizeof(float) * ((size_t)BTR * dout + 2 * (size_t)w * wst +
-                                       2 * (size_t)BTR * (w + 1) + BTR);
+                                       2 * (size_t)BTR * (w + 1) + 2 * BTR);
   SG_REQUIRE(smem <= 227 * 1024, "sage_bwd_rows: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   if (q4) {

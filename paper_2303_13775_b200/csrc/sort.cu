@@ -35,39 +35,37 @@ __global__ void __launch_bounds__(RS_THREADS) rs_hist(const uint32_t* __restrict
   hist[threadIdx.x * ntiles + t] = cnt[threadIdx.x];
 }
 
-// Exclusive scan of hist[256 * ntiles] (digit-major) in one block.
-__global__ void __launch_bounds__(1024) rs_scan(int32_t* __restrict__ hist, int total) {
-  __shared__ int wsum[32];
-  const int per = (total + 1023) / 1024;
-  const int b = threadIdx.x * per;
-  int s = 0;
-  for (int i = b; i < min(b + per, total); ++i) s += hist[i];
+// One block per digit: exclusive scan of that digit's tile counts (in place)
+// and the digit total. The scatter kernel scans the 256 totals itself.
+__global__ void __launch_bounds__(256) rs_scan(int32_t* __restrict__ hist, int ntiles,
+                                               int32_t* __restrict__ dtot) {
+  __shared__ int wsum[8];
+  __shared__ int carry;
+  const int dg = blockIdx.x;
+  int32_t* h = hist + (int64_t)dg * ntiles;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int inc = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += y;
-  }
-  if (lane == 31) wsum[warp] = inc;
+  if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  if (warp == 0) {
-    int v = wsum[lane];
-    int iv = v;
+  for (int b0 = 0; b0 < ntiles; b0 += 256) {
+    const int i = b0 + threadIdx.x;
+    const int v = i < ntiles ? h[i] : 0;
+    int inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, iv, o);
-      if (lane >= o) iv += y;
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
     }
-    wsum[lane] = iv - v;
+    if (lane == 31) wsum[warp] = inc;
+    __syncthreads();
+    int wp = 0;
+    for (int w = 0; w < warp; ++w) wp += wsum[w];
+    const int base = carry;
+    if (i < ntiles) h[i] = base + wp + inc - v;
+    __syncthreads();
+    if (threadIdx.x == 255) carry = base + wp + inc;
+    __syncthreads();
   }
-  __syncthreads();
-  int run = wsum[warp] + inc - s;
-  for (int i = b; i < min(b + per, total); ++i) {
-    int v = hist[i];
-    hist[i] = run;
-    run += v;
-  }
+  if (threadIdx.x == 0) dtot[dg] = carry;
 }
 
 __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint32_t* __restrict__ kin,
@@ -75,9 +73,11 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint32_t* __restr
                                                          const int32_t* __restrict__ n_dev,
                                                          int shift, int ntiles,
                                                          const int32_t* __restrict__ hist,
+                                                         const int32_t* __restrict__ dtot,
                                                          uint32_t* __restrict__ kout,
                                                          int32_t* __restrict__ vout) {
   __shared__ int wcnt[RS_THREADS / 32][RADIX];
+  __shared__ int dsum[8];
   const int t = blockIdx.x;
   const int n = *n_dev;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -103,10 +103,22 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint32_t* __restr
     rnk[j] = prior + r;
   }
   __syncthreads();
-  // exclusive prefix over warps per digit (thread = digit), plus tile base
+  // digit base = exclusive scan of the 256 digit totals (thread = digit),
+  // plus this tile's prefix inside the digit, plus the warps before
   {
     const int dg = threadIdx.x;
-    int run = hist[dg * ntiles + t];
+    const int v = dtot[dg];
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) dsum[warp] = inc;
+    __syncthreads();
+    int wp = 0;
+    for (int w = 0; w < warp; ++w) wp += dsum[w];
+    int run = wp + inc - v + hist[dg * ntiles + t];
 #pragma unroll
     for (int w = 0; w < RS_THREADS / 32; ++w) {
       int v = wcnt[w][dg];
@@ -202,7 +214,7 @@ static int64_t a256(int64_t x) { return (x + 255) & ~int64_t(255); }
 
 extern "C" int64_t sg_sort_ws_bytes(int64_t n_max) {
   const int64_t ntiles = (n_max + RS_T - 1) / RS_T;
-  return a256(4 * n_max) * 2 + a256(4 * RADIX * (ntiles > 0 ? ntiles : 1));
+  return a256(4 * n_max) * 2 + a256(4 * RADIX * (ntiles > 0 ? ntiles : 1)) + a256(4 * RADIX);
 }
 
 extern "C" int sg_sort_pairs(void* ws, int64_t n_max, const int32_t* n_dev, uint32_t* keys,
@@ -216,6 +228,7 @@ extern "C" int sg_sort_pairs(void* ws, int64_t n_max, const int32_t* n_dev, uint
   uint32_t* k2 = (uint32_t*)b;
   int32_t* v2 = (int32_t*)(b + a256(4 * n_max));
   int32_t* hist = (int32_t*)(b + 2 * a256(4 * n_max));
+  int32_t* dtot = (int32_t*)(b + 2 * a256(4 * n_max) + a256(4 * RADIX * ntiles));
   const int passes = (key_bits + 7) / 8;
   uint32_t* ka = keys;
   int32_t* va = vals;
@@ -225,9 +238,9 @@ extern "C" int sg_sort_pairs(void* ws, int64_t n_max, const int32_t* n_dev, uint
     const int shift = 8 * p;
     rs_hist<<<ntiles, RS_THREADS, 0, st>>>(ka, n_dev, shift, ntiles, hist);
     SG_CHECK_LAUNCH("rs_hist");
-    rs_scan<<<1, 1024, 0, st>>>(hist, RADIX * ntiles);
+    rs_scan<<<RADIX, 256, 0, st>>>(hist, ntiles, dtot);
     SG_CHECK_LAUNCH("rs_scan");
-    rs_scatter<<<ntiles, RS_THREADS, 0, st>>>(ka, va, n_dev, shift, ntiles, hist, kb, vb);
+    rs_scatter<<<ntiles, RS_THREADS, 0, st>>>(ka, va, n_dev, shift, ntiles, hist, dtot, kb, vb);
     SG_CHECK_LAUNCH("rs_scatter");
     std::swap(ka, kb);
     std::swap(va, vb);

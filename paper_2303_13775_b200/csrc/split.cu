@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(MS_THREADS) ms_scatter(const uint8_t* __restri
 __global__ void k_edge_keys(const int32_t* __restrict__ esrc, const int32_t* __restrict__ edst,
                             MetaHeader h, const SgMeta* __restrict__ meta,
                             const uint8_t* __restrict__ keys, uint8_t* __restrict__ ekey,
-                            uint32_t* __restrict__ pmask) {
+                            uint32_t* __restrict__ pmask, int32_t* __restrict__ egrouped_identity) {
   const int64_t n = h.eoff[h.L];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -265,6 +265,17 @@ __global__ void k_edge_keys(const int32_t* __restrict__ esrc, const int32_t* __r
     const uint8_t dd = keys[h.voff[li + 1] + dst];
     ekey[e] = sd;
     if (sd != dd) atomicOr(&pmask[h.voff[li + 1] + dst], 1u << sd);
+    if (egrouped_identity) egrouped_identity[e] = (int32_t)(e - h.eoff[li]);
+  }
+}
+
+// g == 1: one device owns every edge, grouping is the identity.
+__global__ void k_single_edge_meta(SgMeta* meta) {
+  const int li = threadIdx.x;
+  if (li < meta->L) {
+    meta->n_edge[li][0] = (int32_t)meta->nE[li];
+    meta->edge_off[li][0] = 0;
+    meta->edge_off[li][1] = (int32_t)meta->nE[li];
   }
 }
 
@@ -764,7 +775,8 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   const int64_t nEtot = y.nEtot;
   if (nEtot > 0) {
     k_edge_keys<<<clamp_grid(div_up(nEtot, 256), kSMs * 8), 256, 0, st>>>(
-        esrc, edst, h, meta, P8(y.o_keys), P8(y.o_ekey), U32(y.o_pmask));
+        esrc, edst, h, meta, P8(y.o_keys), P8(y.o_ekey), U32(y.o_pmask),
+        g == 1 ? P32(y.o_egrouped) : nullptr);
     SG_CHECK_LAUNCH("k_edge_keys");
   }
   SegDesc se;
@@ -784,13 +796,18 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   }
   int32_t* tb_edge = P32(y.o_tilebase_edge);
   int32_t* keyoff_edge = tb_edge + y.edge_tiles * g;
-  if (y.edge_tiles > 0) {
+  if (g == 1) {
+    k_single_edge_meta<<<1, 32, 0, st>>>(meta);
+    SG_CHECK_LAUNCH("k_single_edge_meta");
+  } else if (y.edge_tiles > 0) {
     ms_count<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, meta, P32(y.o_tiles_edge));
     SG_CHECK_LAUNCH("ms_count(edge)");
   }
-  ms_scan<<<se.nseg, 1024, 0, st>>>(se, P32(y.o_tiles_edge), tb_edge, keyoff_edge, 1, meta);
-  SG_CHECK_LAUNCH("ms_scan(edge)");
-  if (y.edge_tiles > 0) {
+  if (g > 1) {
+    ms_scan<<<se.nseg, 1024, 0, st>>>(se, P32(y.o_tiles_edge), tb_edge, keyoff_edge, 1, meta);
+    SG_CHECK_LAUNCH("ms_scan(edge)");
+  }
+  if (g > 1 && y.edge_tiles > 0) {
     ms_scatter<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, meta, tb_edge, keyoff_edge,
                                                          nullptr, P32(y.o_egrouped));
     SG_CHECK_LAUNCH("ms_scatter(edge)");

@@ -195,7 +195,8 @@ class SplitStep:
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
         L = self.L
         hid, C = p.hidden, p.num_classes
-        self.grads = {d: torch.zeros(p.n + 1, dtype=torch.float32, device=self.dev) for d in self.devices}
+        # every parameter block (and the loss slot) is written by a reduction job
+        self.grads = {d: torch.empty(p.n + 1, dtype=torch.float32, device=self.dev) for d in self.devices}
         self.jobs = []
         self.d_h = _f32(ds.nV[L], hid, device=self.dev)
         ncls = hid * C + C + 1
