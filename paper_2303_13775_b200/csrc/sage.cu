@@ -224,7 +224,7 @@ int dispatch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStr
 }
 
 // ---------------------------------------------------------------- update
-constexpr int UTR = 64;  // rows per tile
+constexpr int UTR = 32;  // rows per tile
 
 struct UpdArgs {
   int l, d, w, dout, final_, g, stride;
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
         int r = prev0 + a.selfrow[a.voff_l + G];
         if (a.src_row) r = a.src_row[r];
         prow_s[rr] = r;
-        n_s[rr] = N;
+        n_s[rr] = 1.0f / N;  // one division per row; the tile multiplies
         a.counts[G] = N;
       }
     }
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
           const int rs = cs_s[rr * g + s];
           if (rs >= 0) S += a.recv[(int64_t)rs * a.stride + c];
         }
-        const float mv = S / n_s[rr];
+        const float mv = S * n_s[rr];
         mn_s[rr * wp + c] = mv;
         a.mean[G * w + c] = mv;
         hs_s[rr * wp + c] = __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c);
@@ -312,16 +312,24 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
         if (q >= n_own) continue;
         const float* hr = hs_s + rr * wp;
         const float* mr = mn_s + rr * wp;
-        float4 acc = *reinterpret_cast<const float4*>(a.bias + 4 * jq);
+        // two independent accumulator sets (self / neighbour), 4-way unrolled
+        float4 as = *reinterpret_cast<const float4*>(a.bias + 4 * jq);
+        float4 an = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
         for (int c = 0; c < w; ++c) {
           const float hv = hr[c], mv = mr[c];
           const float4 s4 = *reinterpret_cast<const float4*>(ws_s + c * dout + 4 * jq);
           const float4 n4 = *reinterpret_cast<const float4*>(wn_s + c * dout + 4 * jq);
-          acc.x = fmaf(hv, s4.x, fmaf(mv, n4.x, acc.x));
-          acc.y = fmaf(hv, s4.y, fmaf(mv, n4.y, acc.y));
-          acc.z = fmaf(hv, s4.z, fmaf(mv, n4.z, acc.z));
-          acc.w = fmaf(hv, s4.w, fmaf(mv, n4.w, acc.w));
+          as.x = fmaf(hv, s4.x, as.x);
+          as.y = fmaf(hv, s4.y, as.y);
+          as.z = fmaf(hv, s4.z, as.z);
+          as.w = fmaf(hv, s4.w, as.w);
+          an.x = fmaf(mv, n4.x, an.x);
+          an.y = fmaf(mv, n4.y, an.y);
+          an.z = fmaf(mv, n4.z, an.z);
+          an.w = fmaf(mv, n4.w, an.w);
         }
+        float4 acc = make_float4(as.x + an.x, as.y + an.y, as.z + an.z, as.w + an.w);
         if (!a.final_) {
           acc.x = fmaxf(acc.x, 0.f);
           acc.y = fmaxf(acc.y, 0.f);
@@ -410,7 +418,7 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
         int r = prev0 + a.selfrow[a.voff_l + G];
         if (a.src_row) r = a.src_row[r];
         prow_s[rr] = r;
-        cnt_s[rr] = a.counts[G];
+        cnt_s[rr] = 1.0f / a.counts[G];
       } else {
         prow_s[rr] = -1;
         cnt_s[rr] = 1.f;
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
         if (idx < nslots) {
           const int c = idx / nq, jq = idx - c * nq;
           float4 s1 = aS4[k], s2 = aN4[k];
-#pragma unroll 4
+#pragma unroll 8
           for (int rr = 0; rr < BTR; ++rr) {
             const float4 g4 = *reinterpret_cast<const float4*>(dp_s + rr * dout + 4 * jq);
             const float hv = hs_s[rr * wp + c], mv = mn_s[rr * wp + c];
@@ -507,7 +515,7 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
           }
         }
         if (a.d_self) a.d_self[G * w + c] = s1;
-        if (a.d_sums) a.d_sums[G * w + c] = s2 / cnt_s[rr];
+        if (a.d_sums) a.d_sums[G * w + c] = s2 * cnt_s[rr];
       }
     }
   }
