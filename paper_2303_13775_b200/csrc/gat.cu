@@ -1,0 +1,905 @@
+// GAT (single head; multi-head = heads stacked by the host) forward/backward for
+// one device of a split — replaces _gat_forward / _gat_backward
+// (engine.py:280-552) and the layer math of models.py:217-261.
+//
+// The reference runs 10 barrier exchange rounds per layer (test_engine.py:
+// 376-384). Here they are 5, with identical mathematics:
+//   forward   from_owner t (w 1)            t_v = z_v.a_dst for reference dsts
+//             to_owner (U, m, s) (w d+2)     ONLINE-SOFTMAX partials: local max
+//                                            m, s = sum e^(e-m), U = sum e^(e-m) z_u;
+//                                            the owner merges with rescaling
+//             from_owner (m, den) (w 2)      global stabiliser + denominator, so
+//                                            every holder materialises alpha
+//   backward  from_owner (d_num, c) (w d+1)  c_v = d_num_v . num_v; the softmax
+//                                            backward identity
+//                                            d_e = alpha_e (d_num_v.z_u - c_v)
+//                                            replaces the dd to/from rounds
+//             to_owner dt (w 1)
+//   (SURVEY §7 hard part 5; verified there to 1e-15 in float64.)
+//
+// Kernels (per layer l, device d):
+//   k_gat_project   z = h_prev W, s = z.a_src, t = z_self.a_dst (tile GEMV, FP32)
+//   k_gat_agg       per destination row: e = leaky(s_u + t_v), online softmax
+//                   (m, s, U) over its in-edges (team per row, EG edge groups
+//                   merged by a fixed xor tree); pre_e stored per edge; ref rows
+//                   packed into the push-to-owner buffer
+//   k_gat_combine   owner merge of local + holders' (m, s, U) in ascending
+//                   sender order -> m, den, num, h
+//   k_gat_alpha     alpha_e = exp(e - m_v) / den_v per local edge
+//   k_gat_bwd_rows  d_num, c
+//   k_gat_bwd_dst   per destination row: d_alpha, d_pre_e (stored), dt partial
+//   k_gat_bwd_src   per source row (CSR-by-source): d_z = sum alpha d_num +
+//                   ds a_src (+ dt a_dst on self rows), ds
+//   k_gat_bwd_param per-block partials of [dW | da_src | da_dst] and d_h_prev
+#include <cstring>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace sg {
+namespace {
+
+__device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? x : slope * x; }
+
+// ---------------------------------------------------------------- projection
+constexpr int PTR = 32;
+
+struct ProjArgs {
+  int l, d, w, dout;
+  int64_t voff_lm1, voff_l;
+  const float* h_prev;
+  const int32_t* src_row;
+  const int32_t* grouped;
+  const int32_t* rank;
+  const float* W;
+  const float* a_src;
+  const float* a_dst;
+  float* z;
+  float* s;
+  float* t;
+};
+
+template <bool Q4>
+__global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ meta, ProjArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, dout = a.dout, wp = w + 1, dp = dout + 1;
+  float* W_s = smem;               // [w][dout]
+  float* h_s = W_s + w * dout;     // [PTR][w+1]
+  float* z_s = h_s + PTR * wp;     // [PTR][dout+1]
+  int* prow_s = (int*)(z_s + PTR * dp);
+  for (int i = threadIdx.x; i < w * dout; i += blockDim.x) W_s[i] = a.W[i];
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d];
+  const int ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int ntiles = (n + PTR - 1) / PTR;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();
+    if (threadIdx.x < PTR) {
+      const int q = tile * PTR + threadIdx.x;
+      int r = -1;
+      if (q < n) {
+        r = own0 + q;
+        if (a.src_row) r = a.src_row[r];
+      }
+      prow_s[threadIdx.x] = r;
+    }
+    __syncthreads();
+    const int nrow = min(PTR, n - tile * PTR);
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < nrow * w; idx += blockDim.x) {
+      const int rr = idx / w, c = idx - rr * w;
+      h_s[rr * wp + c] = __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c);
+    }
+    __syncthreads();
+    if (Q4) {
+      const int nq = dout >> 2;
+      for (int idx = threadIdx.x; idx < nrow * nq; idx += blockDim.x) {
+        const int rr = idx / nq, jq = idx - rr * nq;
+        const float* hr = h_s + rr * wp;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int c = 0; c < w; ++c) {
+          const float hv = hr[c];
+          const float4 w4 = *reinterpret_cast<const float4*>(W_s + c * dout + 4 * jq);
+          acc.x = fmaf(hv, w4.x, acc.x);
+          acc.y = fmaf(hv, w4.y, acc.y);
+          acc.z = fmaf(hv, w4.z, acc.z);
+          acc.w = fmaf(hv, w4.w, acc.w);
+        }
+        *reinterpret_cast<float4*>(a.z + (int64_t)(own0 + tile * PTR + rr) * dout + 4 * jq) = acc;
+        float* zr = z_s + rr * dp + 4 * jq;
+        zr[0] = acc.x;
+        zr[1] = acc.y;
+        zr[2] = acc.z;
+        zr[3] = acc.w;
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < nrow * dout; idx += blockDim.x) {
+        const int rr = idx / dout, j = idx - rr * dout;
+        const float* hr = h_s + rr * wp;
+        float acc = 0.f;
+        for (int c = 0; c < w; ++c) acc = fmaf(hr[c], W_s[c * dout + j], acc);
+        a.z[(int64_t)(own0 + tile * PTR + rr) * dout + j] = acc;
+        z_s[rr * dp + j] = acc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < nrow) {
+      const int rr = threadIdx.x;
+      const int G = own0 + tile * PTR + rr;
+      float sv = 0.f;
+      for (int j = 0; j < dout; ++j) sv = fmaf(z_s[rr * dp + j], a.a_src[j], sv);
+      a.s[G] = sv;
+      const int p = a.grouped[a.voff_lm1 + G];
+      if (p < nVl) {  // self row of owned v at layer l
+        float tv = 0.f;
+        for (int j = 0; j < dout; ++j) tv = fmaf(z_s[rr * dp + j], a.a_dst[j], tv);
+        a.t[ownl + a.rank[a.voff_l + p]] = tv;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- online-softmax aggregation
+struct AggArgs {
+  int l, d, dout, stride;
+  float slope;
+  int64_t eoff_li, rbase_li, pbase_l;
+  const int32_t* rowbeg;
+  const int32_t* rowend;
+  const int32_t* lsrc;
+  const int32_t* dperm;
+  const int32_t* sendpos;
+  const float* z;
+  const float* s;
+  const float* t;
+  const float* t_recv;  // pair layout, stride 1
+  float* pre_e;
+  float* loc_m;
+  float* loc_s;
+  float* loc_U;
+  float* sendbuf;  // [U | m | s]
+};
+
+template <int VEC>
+struct V4;
+template <>
+struct V4<4> {
+  using T = float4;
+  __device__ static T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ static T ld(const float* p) { return *reinterpret_cast<const float4*>(p); }
+  __device__ static T ld_any(const float* p) { return make_float4(p[0], p[1], p[2], p[3]); }
+  __device__ static void st(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
+  __device__ static void st_any(float* p, T v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w; }
+  __device__ static T axpby(float a, T x, float b, T y) {  // a*x + b*y
+    return make_float4(fmaf(a, x.x, b * y.x), fmaf(a, x.y, b * y.y), fmaf(a, x.z, b * y.z), fmaf(a, x.w, b * y.w));
+  }
+  __device__ static void fma_(T& acc, float a, T x) {
+    acc.x = fmaf(a, x.x, acc.x); acc.y = fmaf(a, x.y, acc.y); acc.z = fmaf(a, x.z, acc.z); acc.w = fmaf(a, x.w, acc.w);
+  }
+  __device__ static T scale(T x, float a) { return make_float4(x.x * a, x.y * a, x.z * a, x.w * a); }
+  __device__ static float dot(T x, T y) { return fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, x.w * y.w))); }
+  __device__ static T shfl_xor(unsigned m, T v, int o, int w) {
+    return make_float4(__shfl_xor_sync(m, v.x, o, w), __shfl_xor_sync(m, v.y, o, w),
+                       __shfl_xor_sync(m, v.z, o, w), __shfl_xor_sync(m, v.w, o, w));
+  }
+  __device__ static void add(T& a, T b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+};
+template <>
+struct V4<1> {
+  using T = float;
+  __device__ static T zero() { return 0.f; }
+  __device__ static T ld(const float* p) { return *p; }
+  __device__ static T ld_any(const float* p) { return *p; }
+  __device__ static void st(float* p, T v) { *p = v; }
+  __device__ static void st_any(float* p, T v) { *p = v; }
+  __device__ static T axpby(float a, T x, float b, T y) { return fmaf(a, x, b * y); }
+  __device__ static void fma_(T& acc, float a, T x) { acc = fmaf(a, x, acc); }
+  __device__ static T scale(T x, float a) { return x * a; }
+  __device__ static float dot(T x, T y) { return x * y; }
+  __device__ static T shfl_xor(unsigned m, T v, int o, int w) { return __shfl_xor_sync(m, v, o, w); }
+  __device__ static void add(T& a, T b) { a += b; }
+};
+
+// Team of RL = LPR*EG lanes per destination row; LPR lanes span dout (VEC each).
+template <int VEC, int LPR, int EG>
+__global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta, AggArgs a) {
+  using V = V4<VEC>;
+  using T = typename V::T;
+  constexpr int RL = LPR * EG;
+  constexpr int RPW = 32 / RL;
+  const int l = a.l, d = a.d, dout = a.dout;
+  const int n_own = meta->n_own[l][d];
+  const int R = n_own + meta->n_ref[l][d];
+  const int own0 = meta->own_off[l][d], ref0 = meta->ref_off[l][d];
+  const int prev0 = meta->own_off[l - 1][d];
+  const int64_t rb = a.rbase_li + own0 + ref0;
+  const int lane = threadIdx.x & 31;
+  const int team = lane / RL, tl = lane % RL, eg = tl / LPR, lr = tl % LPR;
+  const unsigned tmask = (RL == 32) ? 0xffffffffu : (((1u << RL) - 1u) << (team * RL));
+  const int col = lr * VEC;
+  const bool colok = col < dout;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = gw * RPW + team; q < R; q += nw * RPW) {
+    const bool own = q < n_own;
+    const int slot = own ? 0 : a.sendpos[a.pbase_l + ref0 + (q - n_own)];
+    const float tq = own ? a.t[own0 + q] : a.t_recv[slot];
+    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
+    float m = -INFINITY, ssum = 0.f;
+    T U = V::zero();
+    for (int j = b + eg; j < e; j += EG) {
+      const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
+      const int u = prev0 + a.lsrc[x];
+      const float pre = a.s[u] + tq;
+      const float ev = leaky(pre, a.slope);
+      if (lr == 0) a.pre_e[x] = pre;
+      const T zu = colok ? V::ld(a.z + (int64_t)u * dout + col) : V::zero();
+      if (ev > m) {
+        const float sc = expf(m - ev);  // 0 on the first edge (m = -inf)
+        ssum = fmaf(ssum, sc, 1.f);
+        U = V::axpby(1.f, zu, sc, U);
+        m = ev;
+      } else {
+        const float wv = expf(ev - m);
+        ssum += wv;
+        V::fma_(U, wv, zu);
+      }
+    }
+    // merge the EG edge groups with a fixed xor tree
+#pragma unroll
+    for (int o = LPR; o < RL; o <<= 1) {
+      const float m2 = __shfl_xor_sync(tmask, m, o, RL);
+      const float s2 = __shfl_xor_sync(tmask, ssum, o, RL);
+      const T U2 = V::shfl_xor(tmask, U, o, RL);
+      const float mm = fmaxf(m, m2);
+      const float f1 = (m == -INFINITY) ? 0.f : expf(m - mm);
+      const float f2 = (m2 == -INFINITY) ? 0.f : expf(m2 - mm);
+      ssum = ssum * f1 + s2 * f2;
+      U = V::axpby(f1, U, f2, U2);
+      m = mm;
+    }
+    if (eg != 0) continue;
+    if (own) {
+      const int G = own0 + q;
+      if (colok) V::st(a.loc_U + (int64_t)G * dout + col, U);
+      if (lr == 0) {
+        a.loc_m[G] = m;
+        a.loc_s[G] = ssum;
+      }
+    } else {
+      float* out = a.sendbuf + (int64_t)slot * a.stride;
+      if (colok) {
+        if ((a.stride & 3) == 0 && VEC == 4) V::st(out + col, U); else V::st_any(out + col, U);
+      }
+      if (lr == 0) {
+        out[dout] = m;
+        out[dout + 1] = ssum;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- owner combine
+struct CombArgs {
+  int l, d, dout, g, stride, final_;
+  int64_t voff_l;
+  const int32_t* contrib;
+  const float* loc_m;
+  const float* loc_s;
+  const float* loc_U;
+  const float* recv;  // [U | m | s] rows, receive layout
+  float* md;          // [m, den] per owned row
+  float* num;
+  float* h;
+};
+
+__global__ void k_gat_combine(const SgMeta* __restrict__ meta, CombArgs a) {
+  const int l = a.l, d = a.d, dout = a.dout, g = a.g;
+  const int n = meta->n_own[l][d];
+  const int own0 = meta->own_off[l][d];
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * dout;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(idx / dout), j = (int)(idx - (int64_t)q * dout);
+    const int64_t G = own0 + q;
+    const int* cb = a.contrib + (int64_t)g * a.voff_l + G * g;
+    float m = a.loc_m[G];
+    for (int s = 0; s < g; ++s) {
+      const int rs = cb[s];
+      if (rs >= 0) m = fmaxf(m, a.recv[(int64_t)rs * a.stride + dout]);
+    }
+    float f = expf(a.loc_m[G] - m);
+    float den = a.loc_s[G] * f;
+    float U = a.loc_U[G * dout + j] * f;
+    for (int s = 0; s < g; ++s) {  // ascending sender order
+      const int rs = cb[s];
+      if (rs >= 0) {
+        const float* r = a.recv + (int64_t)rs * a.stride;
+        const float fs = expf(r[dout] - m);
+        den = fmaf(r[dout + 1], fs, den);
+        U = fmaf(r[j], fs, U);
+      }
+    }
+    const float nv = U / den;
+    a.num[G * dout + j] = nv;
+    a.h[G * dout + j] = a.final_ ? nv : fmaxf(nv, 0.f);
+    if (j == 0) {
+      a.md[2 * G] = m;
+      a.md[2 * G + 1] = den;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- alpha per edge
+struct AlphaArgs {
+  int l, d;
+  float slope;
+  int64_t eoff_li, pbase_l;
+  const int32_t* ldst;
+  const int32_t* sendpos;
+  const float* pre_e;
+  const float* md;        // owned rows
+  const float* md_recv;   // pair layout, stride 2
+  float* alpha;
+};
+
+__global__ void k_gat_alpha(const SgMeta* __restrict__ meta, AlphaArgs a) {
+  const int l = a.l, d = a.d, li = l - 1;
+  const int b = meta->edge_off[li][d], e = meta->edge_off[li][d + 1];
+  const int n_own = meta->n_own[l][d];
+  const int own0 = meta->own_off[l][d], ref0 = meta->ref_off[l][d];
+  for (int i = b + blockIdx.x * blockDim.x + threadIdx.x; i < e; i += gridDim.x * blockDim.x) {
+    const int64_t x = a.eoff_li + i;
+    const int q = a.ldst[x];
+    const float* mdp = q < n_own ? a.md + 2 * (int64_t)(own0 + q)
+                                 : a.md_recv + 2 * (int64_t)a.sendpos[a.pbase_l + ref0 + (q - n_own)];
+    a.alpha[x] = expf(leaky(a.pre_e[x], a.slope) - mdp[0]) / mdp[1];
+  }
+}
+
+// ---------------------------------------------------------------- backward
+struct BRowsArgs {
+  int l, d, dout, final_;
+  const float* d_h;
+  const float* num;
+  float* dnc;  // [d_num | c] per owned row (stride dout+1)
+};
+
+__global__ void k_gat_bwd_rows(const SgMeta* __restrict__ meta, BRowsArgs a) {
+  const int l = a.l, d = a.d, dout = a.dout;
+  const int n = meta->n_own[l][d];
+  const int own0 = meta->own_off[l][d];
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    const int64_t G = own0 + q;
+    float c = 0.f;
+    for (int j = 0; j < dout; ++j) {
+      const float nv = a.num[G * dout + j];
+      float dn = a.d_h[G * dout + j];
+      if (!a.final_ && !(nv > 0.f)) dn = 0.f;
+      a.dnc[G * (dout + 1) + j] = dn;
+      c = fmaf(dn, nv, c);
+    }
+    a.dnc[G * (dout + 1) + dout] = c;
+  }
+}
+
+struct BDstArgs {
+  int l, d, dout, stride;
+  float slope;
+  int64_t eoff_li, rbase_li, pbase_l;
+  const int32_t* rowbeg;
+  const int32_t* rowend;
+  const int32_t* lsrc;
+  const int32_t* dperm;
+  const int32_t* sendpos;
+  const float* z;
+  const float* alpha;
+  const float* pre_e;
+  const float* dnc;       // owned rows, stride dout+1
+  const float* dnc_recv;  // pair layout, stride `stride`
+  float* d_pre;
+  float* dt_loc;
+  float* sendbuf;  // dt per pair slot (stride 1)
+};
+
+template <int VEC, int LPR, int EG>
+__global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ meta, BDstArgs a) {
+  using V = V4<VEC>;
+  using T = typename V::T;
+  constexpr int RL = LPR * EG;
+  constexpr int RPW = 32 / RL;
+  const int l = a.l, d = a.d, dout = a.dout;
+  const int n_own = meta->n_own[l][d];
+  const int R = n_own + meta->n_ref[l][d];
+  const int own0 = meta->own_off[l][d], ref0 = meta->ref_off[l][d];
+  const int prev0 = meta->own_off[l - 1][d];
+  const int64_t rb = a.rbase_li + own0 + ref0;
+  const int lane = threadIdx.x & 31;
+  const int team = lane / RL, tl = lane % RL, eg = tl / LPR, lr = tl % LPR;
+  const unsigned tmask = (RL == 32) ? 0xffffffffu : (((1u << RL) - 1u) << (team * RL));
+  const int col = lr * VEC;
+  const bool colok = col < dout;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = gw * RPW + team; q < R; q += nw * RPW) {
+    const bool own = q < n_own;
+    const int slot = own ? 0 : a.sendpos[a.pbase_l + ref0 + (q - n_own)];
+    const float* dn_row = own ? a.dnc + (int64_t)(own0 + q) * (dout + 1) : a.dnc_recv + (int64_t)slot * a.stride;
+    // rows of stride dout+1 are not 16B aligned: element-wise loads
+    const T dn = colok ? V::ld_any(dn_row + col) : V::zero();
+    const float c = dn_row[dout];
+    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
+    float dt = 0.f;
+    const int rounds = (e - b + EG - 1) / EG;
+    for (int kk = 0; kk < rounds; ++kk) {
+      const int j = b + kk * EG + eg;
+      const bool ok = j < e;
+      int64_t x = 0;
+      float part = 0.f;
+      if (ok) {
+        x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
+        const int u = prev0 + a.lsrc[x];
+        if (colok) part = V::dot(dn, V::ld(a.z + (int64_t)u * dout + col));
+      }
+      // d_alpha = d_num . z_u : reduce over the LPR lanes of this edge group
+#pragma unroll
+      for (int o = 1; o < LPR; o <<= 1) part += __shfl_xor_sync(tmask, part, o, RL);
+      if (ok) {
+        const float de = a.alpha[x] * (part - c);
+        const float dp = de * (a.pre_e[x] > 0.f ? 1.f : a.slope);
+        if (lr == 0) a.d_pre[x] = dp;
+        dt += dp;
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < RL; o <<= 1) dt += __shfl_xor_sync(tmask, dt, o, RL);
+    if (tl != 0) continue;
+    if (own) a.dt_loc[own0 + q] = dt;
+    else a.sendbuf[slot] = dt;
+  }
+}
+
+struct BSrcArgs {
+  int l, d, dout, g, stride;
+  int64_t voff_lm1, voff_l, pbase_l, key_base;
+  const int32_t* grouped;
+  const int32_t* rank;
+  const int32_t* contrib;
+  const int32_t* ldst;
+  const int32_t* sendpos;
+  const int32_t* perm;  // edge slots sorted by source row
+  const int32_t* srcbeg;
+  const int32_t* srcend;
+  const float* alpha;
+  const float* d_pre;
+  const float* dnc;
+  const float* dnc_recv;
+  int dnc_stride;
+  const float* dt_loc;
+  const float* dt_recv;  // receive layout, stride 1
+  const float* a_src;
+  const float* a_dst;
+  float* d_z;
+  float* ds;
+  float* dt_tot;
+};
+
+// warp per source row; NG = 32/LPR lane groups split the out-edges
+template <int VEC, int LPR>
+__global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ meta, BSrcArgs a) {
+  using V = V4<VEC>;
+  using T = typename V::T;
+  constexpr int NG = 32 / LPR;
+  const int l = a.l, d = a.d, dout = a.dout;
+  const int n_prev = meta->n_own[l - 1][d];
+  const int prev0 = meta->own_off[l - 1][d];
+  const int own0 = meta->own_off[l][d], n_own = meta->n_own[l][d], ref0 = meta->ref_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int lane = threadIdx.x & 31;
+  const int gi = lane / LPR, lr = lane % LPR;
+  const int col = lr * VEC;
+  const bool colok = col < dout;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = gw; u < n_prev; u += nw) {
+    const int64_t U = prev0 + u;
+    T acc = V::zero();
+    float dsv = 0.f;
+    const int b = a.srcbeg[a.key_base + U], e = a.srcend[a.key_base + U];
+    for (int jb = b; jb < e; jb += 32) {
+      const int j = jb + lane;
+      const int my = j < e ? a.perm[j] : 0;
+      const int cnt = min(32, e - jb);
+      const int rounds = (cnt + NG - 1) / NG;
+      for (int kk = 0; kk < rounds; ++kk) {
+        const int k = kk * NG + gi;
+        const int x = __shfl_sync(0xffffffffu, my, k < 32 ? k : 31);
+        if (k < cnt) {
+          const int q = a.ldst[x];
+          const float* dn_row = q < n_own
+              ? a.dnc + (int64_t)(own0 + q) * (dout + 1)
+              : a.dnc_recv + (int64_t)a.sendpos[a.pbase_l + ref0 + (q - n_own)] * a.dnc_stride;
+          const float al = a.alpha[x];
+          if (colok) V::fma_(acc, al, V::ld_any(dn_row + col));
+          if (lr == 0) dsv += a.d_pre[x];
+        }
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) {
+      V::add(acc, V::shfl_xor(0xffffffffu, acc, o, 32));
+      dsv += __shfl_xor_sync(0xffffffffu, dsv, o);
+    }
+    dsv = __shfl_sync(0xffffffffu, dsv, 0);  // lane 0 holds the full sum
+    if (gi != 0) continue;
+    // d_z += ds * a_src
+    if (colok) V::fma_(acc, dsv, V::ld_any(a.a_src + col));
+    const int p = a.grouped[a.voff_lm1 + U];
+    if (p < nVl) {  // self row of owned v: d_z += dt_v * a_dst (owner combines holders' dt)
+      const int64_t v = own0 + a.rank[a.voff_l + p];
+      float dt = a.dt_loc[v];
+      const int* cb = a.contrib + (int64_t)a.g * a.voff_l + v * a.g;
+      for (int s = 0; s < a.g; ++s) {
+        const int rs = cb[s];
+        if (rs >= 0) dt += a.dt_recv[rs];
+      }
+      if (colok) V::fma_(acc, dt, V::ld_any(a.a_dst + col));
+      if (lr == 0) a.dt_tot[v] = dt;
+    }
+    if (colok) V::st(a.d_z + U * dout + col, acc);  // dout % VEC == 0: aligned
+    if (lr == 0) a.ds[U] = dsv;
+  }
+}
+
+// per-block partials of [dW | da_src | da_dst] over source rows; d_h_prev
+constexpr int QTR = 32;
+constexpr int QMAXQ = 8;  // float4 slots: w*dout/4 <= 2048
+
+struct BParamArgs {
+  int l, d, w, dout;
+  int64_t voff_lm1, voff_l;
+  const float* h_prev;
+  const int32_t* src_row;
+  const int32_t* grouped;
+  const int32_t* rank;
+  const float* z;
+  const float* d_z;
+  const float* ds;
+  const float* dt_tot;
+  const float* W;
+  float* partial;
+  float* d_prev;
+};
+
+__global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict__ meta, BParamArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, dout = a.dout, wp = w + 1, wst = dout + 4;
+  float* dz_s = smem;               // [QTR][dout]
+  float* W_s = dz_s + QTR * dout;   // [w][dout+4] (for d_prev)
+  float* h_s = W_s + w * wst;       // [QTR][w+1]
+  float* z_s = h_s + QTR * wp;      // [QTR][dout]
+  float* ds_s = z_s + QTR * dout;   // [QTR]
+  float* dt_s = ds_s + QTR;         // [QTR] (0 when not a self row)
+  int* prow_s = (int*)(dt_s + QTR);
+  if (a.d_prev)
+    for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
+      const int c = i / dout, j = i - c * dout;
+      W_s[c * wst + j] = a.W[i];
+    }
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d];
+  const int ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int nslots = w * dout;  // scalar slots: idx -> (c, j)
+  float acc[QMAXQ * 4];
+#pragma unroll
+  for (int k = 0; k < QMAXQ * 4; ++k) acc[k] = 0.f;
+  float as = 0.f, ad = 0.f;
+  const int ntiles = (n + QTR - 1) / QTR;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();
+    const int nrow = min(QTR, n - tile * QTR);
+    if (threadIdx.x < QTR) {
+      const int rr = threadIdx.x;
+      if (rr < nrow) {
+        const int G = own0 + tile * QTR + rr;
+        int r = G;
+        if (a.src_row) r = a.src_row[r];
+        prow_s[rr] = r;
+        ds_s[rr] = a.ds[G];
+        const int p = a.grouped[a.voff_lm1 + G];
+        dt_s[rr] = p < nVl ? a.dt_tot[ownl + a.rank[a.voff_l + p]] : 0.f;
+      } else {
+        prow_s[rr] = -1;
+        ds_s[rr] = 0.f;
+        dt_s[rr] = 0.f;
+      }
+    }
+    for (int idx = threadIdx.x; idx < QTR * dout; idx += blockDim.x) {
+      const int rr = idx / dout;
+      const bool v = rr < nrow;
+      const int64_t G = own0 + tile * QTR + rr;
+      dz_s[idx] = v ? a.d_z[G * dout + (idx - rr * dout)] : 0.f;
+      z_s[idx] = v ? a.z[G * dout + (idx - rr * dout)] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < QTR * w; idx += blockDim.x) {
+      const int rr = idx / w, c = idx - rr * w;
+      h_s[rr * wp + c] = prow_s[rr] >= 0 ? __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < QMAXQ * 4; ++k) {
+      const int idx = threadIdx.x + 256 * k;
+      if (idx < nslots) {
+        const int c = idx / dout, j = idx - c * dout;
+        float sacc = acc[k];
+#pragma unroll 8
+        for (int rr = 0; rr < QTR; ++rr) sacc = fmaf(h_s[rr * wp + c], dz_s[rr * dout + j], sacc);
+        acc[k] = sacc;
+      }
+    }
+    if (threadIdx.x < dout) {
+      const int j = threadIdx.x;
+      for (int rr = 0; rr < QTR; ++rr) {
+        as = fmaf(z_s[rr * dout + j], ds_s[rr], as);
+        ad = fmaf(z_s[rr * dout + j], dt_s[rr], ad);
+      }
+    }
+    if (a.d_prev) {
+      for (int idx = threadIdx.x; idx < nrow * w; idx += blockDim.x) {
+        const int rr = idx / w, c = idx - rr * w;
+        float sacc = 0.f;
+        for (int j = 0; j < dout; ++j) sacc = fmaf(dz_s[rr * dout + j], W_s[c * wst + j], sacc);
+        a.d_prev[(int64_t)(own0 + tile * QTR + rr) * w + c] = sacc;
+      }
+    }
+  }
+  const int64_t ntot = (int64_t)nslots + 2 * dout;
+  float* out = a.partial + (int64_t)blockIdx.x * ntot;
+#pragma unroll
+  for (int k = 0; k < QMAXQ * 4; ++k) {
+    const int idx = threadIdx.x + 256 * k;
+    if (idx < nslots) out[idx] = acc[k];
+  }
+  if (threadIdx.x < dout) {
+    out[nslots + threadIdx.x] = as;
+    out[nslots + dout + threadIdx.x] = ad;
+  }
+}
+
+// ---------------------------------------------------------------- dispatch helpers
+#define GAT_TEAM_DISPATCH(KERNEL, DOUT, GRIDROWS, ST, ...)                                 \
+  do {                                                                                    \
+    const int dd_ = (DOUT);                                                               \
+    auto go_ = [&](auto vec_, auto lpr_, auto eg_) {                                      \
+      constexpr int VEC_ = decltype(vec_)::value, LPR_ = decltype(lpr_)::value,           \
+                    EG_ = decltype(eg_)::value;                                           \
+      constexpr int RPB_ = 8 * (32 / (LPR_ * EG_));                                       \
+      const int grid_ = clamp_grid(div_up((GRIDROWS), RPB_), kSMs * 8);                   \
+      KERNEL<VEC_, LPR_, EG_><<<grid_, 256, 0, ST>>>(__VA_ARGS__);                        \
+    };                                                                                    \
+    using I1 = std::integral_constant<int, 1>;                                            \
+    using I2 = std::integral_constant<int, 2>;                                            \
+    using I4 = std::integral_constant<int, 4>;                                            \
+    using I8 = std::integral_constant<int, 8>;                                            \
+    using I16 = std::integral_constant<int, 16>;                                          \
+    using I32 = std::integral_constant<int, 32>;                                          \
+    if (dd_ % 4 == 0 && dd_ <= 4) go_(I4(), I1(), I8());                                  \
+    else if (dd_ % 4 == 0 && dd_ <= 8) go_(I4(), I2(), I8());                             \
+    else if (dd_ % 4 == 0 && dd_ <= 16) go_(I4(), I4(), I4());                            \
+    else if (dd_ % 4 == 0 && dd_ <= 32) go_(I4(), I8(), I2());                            \
+    else if (dd_ % 4 == 0 && dd_ <= 64) go_(I4(), I16(), I2());                           \
+    else if (dd_ % 4 == 0 && dd_ <= 128) go_(I4(), I32(), I1());                          \
+    else if (dd_ <= 4) go_(I1(), I4(), I4());                                             \
+    else if (dd_ <= 8) go_(I1(), I8(), I2());                                             \
+    else if (dd_ <= 16) go_(I1(), I16(), I2());                                           \
+    else if (dd_ <= 32) go_(I1(), I32(), I1());                                           \
+    else {                                                                                \
+      set_error("gat: hidden width unsupported (<=128 with %4==0, else <=32)");           \
+      return SG_ERR_ARG;                                                                  \
+    }                                                                                     \
+  } while (0)
+
+}  // namespace
+
+#define SPLIT_PTRS                                                     \
+  const char* base = (const char*)split_ws;                           \
+  const SgSplitLayout& y = *lay;                                       \
+  const SgMeta* meta = (const SgMeta*)(base + y.o_meta);               \
+  auto I32p = [&](int64_t o) { return (const int32_t*)(base + o); };
+
+extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                              const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                              const float* W, const float* a_src, const float* a_dst, float* z,
+                              float* s, float* t, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_project: null workspace");
+  SPLIT_PTRS
+  SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_project: bad layer/device");
+  if (max_rows <= 0) return SG_OK;
+  ProjArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.w = w; a.dout = dout;
+  a.voff_lm1 = y.voff[l - 1];
+  a.voff_l = y.voff[l];
+  a.h_prev = h_prev; a.src_row = src_row;
+  a.grouped = I32p(y.o_grouped);
+  a.rank = I32p(y.o_rank);
+  a.W = W; a.a_src = a_src; a.a_dst = a_dst;
+  a.z = z; a.s = s; a.t = t;
+  const size_t smem = sizeof(float) * ((size_t)w * dout + (size_t)PTR * (w + 1) + (size_t)PTR * (dout + 1) + PTR);
+  SG_REQUIRE(smem <= 227 * 1024, "gat_project: width too large for shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = clamp_grid(div_up(max_rows, PTR), kSMs * 4);
+  if (dout % 4 == 0) {
+    SG_CUDA(allow_max_smem<k_gat_project<true>>());
+    k_gat_project<true><<<grid, 256, smem, st>>>(meta, a);
+  } else {
+    SG_CUDA(allow_max_smem<k_gat_project<false>>());
+    k_gat_project<false><<<grid, 256, smem, st>>>(meta, a);
+  }
+  SG_CHECK_LAUNCH("k_gat_project");
+  return SG_OK;
+}
+
+extern "C" int sg_gat_agg(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                          int32_t dout, float slope, const float* z, const float* s, const float* t,
+                          const float* t_recv, const int32_t* dperm, float* pre_e, float* loc_m,
+                          float* loc_s, float* loc_U, float* sendbuf, int32_t send_stride,
+                          int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_agg: null workspace");
+  SPLIT_PTRS
+  SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_agg: bad layer/device");
+  SG_REQUIRE(send_stride >= dout + 2 || y.g == 1, "gat_agg: send stride < dout+2");
+  if (max_rows <= 0) return SG_OK;
+  AggArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.dout = dout; a.stride = send_stride; a.slope = slope;
+  a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.pbase_l = y.pbase[l];
+  a.rowbeg = I32p(y.o_rowbeg); a.rowend = I32p(y.o_rowend); a.lsrc = I32p(y.o_lsrc);
+  a.dperm = dperm; a.sendpos = I32p(y.o_sendpos);
+  a.z = z; a.s = s; a.t = t; a.t_recv = t_recv;
+  a.pre_e = pre_e; a.loc_m = loc_m; a.loc_s = loc_s; a.loc_U = loc_U; a.sendbuf = sendbuf;
+  cudaStream_t st = (cudaStream_t)stream;
+  GAT_TEAM_DISPATCH(k_gat_agg, dout, max_rows, st, meta, a);
+  SG_CHECK_LAUNCH("k_gat_agg");
+  return SG_OK;
+}
+
+extern "C" int sg_gat_combine(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                              int32_t dout, const float* loc_m, const float* loc_s,
+                              const float* loc_U, const float* recv, int32_t recv_stride,
+                              int32_t final_layer, float* md, float* num, float* h,
+                              int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_combine: null workspace");
+  SPLIT_PTRS
+  SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_combine: bad layer/device");
+  if (max_rows <= 0) return SG_OK;
+  CombArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.dout = dout; a.g = y.g; a.stride = recv_stride; a.final_ = final_layer;
+  a.voff_l = y.voff[l]; a.contrib = I32p(y.o_contrib);
+  a.loc_m = loc_m; a.loc_s = loc_s; a.loc_U = loc_U; a.recv = recv; a.md = md; a.num = num; a.h = h;
+  k_gat_combine<<<clamp_grid(div_up(max_rows * dout, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  SG_CHECK_LAUNCH("k_gat_combine");
+  return SG_OK;
+}
+
+extern "C" int sg_gat_alpha(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                            float slope, const float* pre_e, const float* md, const float* md_recv,
+                            float* alpha, int64_t max_edges, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_alpha: null workspace");
+  SPLIT_PTRS
+  SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_alpha: bad layer/device");
+  if (max_edges <= 0) return SG_OK;
+  AlphaArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.slope = slope; a.eoff_li = y.eoff[l - 1]; a.pbase_l = y.pbase[l];
+  a.ldst = I32p(y.o_ldst); a.sendpos = I32p(y.o_sendpos);
+  a.pre_e = pre_e; a.md = md; a.md_recv = md_recv; a.alpha = alpha;
+  k_gat_alpha<<<clamp_grid(div_up(max_edges, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  SG_CHECK_LAUNCH("k_gat_alpha");
+  return SG_OK;
+}
+
+extern "C" int sg_gat_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                               int32_t dout, const float* d_h, const float* num, int32_t final_layer,
+                               float* dnc, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_bwd_rows: null workspace");
+  SPLIT_PTRS
+  if (max_rows <= 0) return SG_OK;
+  BRowsArgs a{l, d, dout, final_layer, d_h, num, dnc};
+  k_gat_bwd_rows<<<clamp_grid(div_up(max_rows, 256), kSMs * 4), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  SG_CHECK_LAUNCH("k_gat_bwd_rows");
+  return SG_OK;
+}
+
+extern "C" int sg_gat_bwd_dst(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                              int32_t dout, float slope, const float* z, const float* alpha,
+                              const float* pre_e, const float* dnc, const float* dnc_recv,
+                              int32_t recv_stride, const int32_t* dperm, float* d_pre,
+                              float* dt_loc, float* sendbuf, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_bwd_dst: null workspace");
+  SPLIT_PTRS
+  if (max_rows <= 0) return SG_OK;
+  BDstArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.dout = dout; a.stride = recv_stride; a.slope = slope;
+  a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.pbase_l = y.pbase[l];
+  a.rowbeg = I32p(y.o_rowbeg); a.rowend = I32p(y.o_rowend); a.lsrc = I32p(y.o_lsrc);
+  a.dperm = dperm; a.sendpos = I32p(y.o_sendpos);
+  a.z = z; a.alpha = alpha; a.pre_e = pre_e; a.dnc = dnc; a.dnc_recv = dnc_recv;
+  a.d_pre = d_pre; a.dt_loc = dt_loc; a.sendbuf = sendbuf;
+  cudaStream_t st = (cudaStream_t)stream;
+  GAT_TEAM_DISPATCH(k_gat_bwd_dst, dout, max_rows, st, meta, a);
+  SG_CHECK_LAUNCH("k_gat_bwd_dst");
+  return SG_OK;
+}
+
+extern "C" int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                              int32_t dout, const int32_t* perm, const int32_t* srcbeg,
+                              const int32_t* srcend, int64_t key_base, const float* alpha,
+                              const float* d_pre, const float* dnc, const float* dnc_recv,
+                              int32_t dnc_stride, const float* dt_loc, const float* dt_recv,
+                              const float* a_src, const float* a_dst, float* d_z, float* ds,
+                              float* dt_tot, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_bwd_src: null workspace");
+  SPLIT_PTRS
+  if (max_rows <= 0) return SG_OK;
+  BSrcArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.dout = dout; a.g = y.g;
+  a.voff_lm1 = y.voff[l - 1]; a.voff_l = y.voff[l]; a.pbase_l = y.pbase[l]; a.key_base = key_base;
+  a.grouped = I32p(y.o_grouped); a.rank = I32p(y.o_rank); a.contrib = I32p(y.o_contrib);
+  a.ldst = I32p(y.o_ldst); a.sendpos = I32p(y.o_sendpos);
+  a.perm = perm; a.srcbeg = srcbeg; a.srcend = srcend;
+  a.alpha = alpha; a.d_pre = d_pre; a.dnc = dnc; a.dnc_recv = dnc_recv; a.dnc_stride = dnc_stride;
+  a.dt_loc = dt_loc; a.dt_recv = dt_recv; a.a_src = a_src; a.a_dst = a_dst;
+  a.d_z = d_z; a.ds = ds; a.dt_tot = dt_tot;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = clamp_grid(div_up(max_rows, 8), kSMs * 8);
+  if (dout % 4 == 0 && dout <= 16) k_gat_bwd_src<4, 4><<<grid, 256, 0, st>>>(meta, a);
+  else if (dout % 4 == 0 && dout <= 32) k_gat_bwd_src<4, 8><<<grid, 256, 0, st>>>(meta, a);
+  else if (dout % 4 == 0 && dout <= 64) k_gat_bwd_src<4, 16><<<grid, 256, 0, st>>>(meta, a);
+  else if (dout % 4 == 0 && dout <= 128) k_gat_bwd_src<4, 32><<<grid, 256, 0, st>>>(meta, a);
+  else if (dout <= 8) k_gat_bwd_src<1, 8><<<grid, 256, 0, st>>>(meta, a);
+  else if (dout <= 32) k_gat_bwd_src<1, 32><<<grid, 256, 0, st>>>(meta, a);
+  else {
+    set_error("gat_bwd_src: hidden width unsupported");
+    return SG_ERR_ARG;
+  }
+  SG_CHECK_LAUNCH("k_gat_bwd_src");
+  return SG_OK;
+}
+
+extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                                const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                                const float* z, const float* d_z, const float* ds,
+                                const float* dt_tot, const float* W, float* partial, int32_t nblocks,
+                                float* d_prev, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "gat_bwd_param: null workspace");
+  SPLIT_PTRS
+  SG_REQUIRE((int64_t)w * dout <= 256 * QMAXQ * 4, "gat_bwd_param: w*dout > 8192 unsupported");
+  SG_REQUIRE(nblocks >= 1, "gat_bwd_param: nblocks >= 1");
+  (void)max_rows;
+  BParamArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.w = w; a.dout = dout;
+  a.voff_lm1 = y.voff[l - 1]; a.voff_l = y.voff[l];
+  a.h_prev = h_prev; a.src_row = src_row; a.grouped = I32p(y.o_grouped); a.rank = I32p(y.o_rank);
+  a.z = z; a.d_z = d_z; a.ds = ds; a.dt_tot = dt_tot; a.W = W; a.partial = partial; a.d_prev = d_prev;
+  const size_t smem = sizeof(float) * (2 * (size_t)QTR * dout + (size_t)w * (dout + 4) +
+                                       (size_t)QTR * (w + 1) + 3 * QTR);
+  SG_REQUIRE(smem <= 227 * 1024, "gat_bwd_param: width too large for shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+  SG_CUDA(allow_max_smem<k_gat_bwd_param>());
+  k_gat_bwd_param<<<nblocks, 256, smem, st>>>(meta, a);
+  SG_CHECK_LAUNCH("k_gat_bwd_param");
+  return SG_OK;
+}
+
+}  // namespace sg

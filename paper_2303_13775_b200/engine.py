@@ -431,6 +431,9 @@ def _materialise_states(ex):
                 if k in ("alpha", "pre_e", "w_e"):
                     eb = int(ds.lay.eoff[l - 1]) + int(m.edge_off[l - 1][d])
                     keep[k] = v[eb:eb + int(m.n_edge[l - 1][d])].double().cpu().numpy()
+                elif k in ("z", "s"):  # rows at layer l-1
+                    b1, n1 = int(m.own_off[l - 1][d]), int(m.n_own[l - 1][d])
+                    keep[k] = v[b1:b1 + n1].double().cpu().numpy()
                 else:
                     keep[k] = v[b:b + n].double().cpu().numpy()
             sv.layer.append(keep)

@@ -1,0 +1,155 @@
+"""GAT layers of the split step (engine.py:280-552) on the sm_100a kernels.
+
+Five exchange rounds per layer instead of the reference's ten (gat.cu header):
+forward  from_owner t, to_owner (U, m, s), from_owner (m, den);
+backward from_owner (d_num, c), to_owner dt.
+The peer-bytes metering of the API keeps the reference's formula; the bytes
+actually moved are reported separately as wire bytes.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from paper_2303_13775_b200 import _lib
+
+
+def _f32(n, *shape, device):
+    return torch.empty((max(int(n), 1),) + tuple(shape), dtype=torch.float32, device=device)
+
+
+def _r4(x):
+    return (int(x) + 3) // 4 * 4
+
+
+def _from_owner(step, l, rows, width):
+    """Owner rows (global owned index) -> holders' pair-layout rows."""
+    ds = step.ds
+    P = ds.pair_bound(l)
+    out = _f32(P, width, device=step.dev)
+    if step.g > 1 and P > 0:
+        send = _f32(P, width, device=step.dev)
+        st = _lib.stream_ptr()
+        for d in step.devices:
+            _lib.call("sg_pack_from_owner", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(rows), width,
+                      _lib.ptr(send), width, step.n_recv(l, d), st)
+        step.transport.from_owner(ds, l, send, out, width)
+        if step.meta is not None:
+            step.wire_bytes += int(step.meta.npairs[l]) * width * 4
+    return out
+
+
+def gat_forward(step):
+    ds, p = step.ds, step.p
+    st = _lib.stream_ptr()
+    slope = float(p.leaky_slope)
+    step.layer0()
+    dperm = step._dst_perm()
+    dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
+    nEtot = int(ds.lay.nEtot)
+    step.h[0] = step.f.table
+    for l in range(1, step.L + 1):
+        w, dout = p.layer_dims(l - 1)
+        final = int(l == step.L)
+        h_prev, src_row = (step.f.table, step.src_row0) if l == 1 else (step.h[l - 1], None)
+        nVp, nV, P = ds.nV[l - 1], ds.nV[l], ds.pair_bound(l)
+        W, a_s, a_d = (p.view(f"layer{l-1}.{k}") for k in ("w", "a_src", "a_dst"))
+        z = _f32(nVp, dout, device=step.dev)
+        s = _f32(nVp, device=step.dev)
+        t = _f32(nV, device=step.dev)
+        for d in step.devices:
+            _lib.call("sg_gat_project", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
+                      w, dout, _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(z), _lib.ptr(s),
+                      _lib.ptr(t), step.n_own(l - 1, d), st)
+        t_recv = _from_owner(step, l, t, 1)
+        SW = _r4(dout + 2)
+        send = _f32(P, SW, device=step.dev)
+        recv = _f32(P, SW, device=step.dev)
+        pre_e = _f32(nEtot, device=step.dev)
+        loc_m = _f32(nV, device=step.dev)
+        loc_s = _f32(nV, device=step.dev)
+        loc_U = _f32(nV, dout, device=step.dev)
+        step._ev(f"agg{l}_start")
+        for d in step.devices:
+            _lib.call("sg_gat_agg", _lib.ptr(ds.ws), ds.lay, l, d, dout, slope, _lib.ptr(z), _lib.ptr(s),
+                      _lib.ptr(t), _lib.ptr(t_recv), dp_ptr(d), _lib.ptr(pre_e), _lib.ptr(loc_m),
+                      _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(send), SW, step.n_rows(l, d), st)
+        step._ev(f"agg{l}_end")
+        if step.g > 1 and P > 0:
+            step.transport.to_owner(ds, l, send, recv, SW)
+            if step.meta is not None:
+                step.wire_bytes += int(step.meta.npairs[l]) * SW * 4
+        md = _f32(nV, 2, device=step.dev)
+        num = _f32(nV, dout, device=step.dev)
+        h = _f32(nV, dout, device=step.dev)
+        for d in step.devices:
+            _lib.call("sg_gat_combine", _lib.ptr(ds.ws), ds.lay, l, d, dout, _lib.ptr(loc_m), _lib.ptr(loc_s),
+                      _lib.ptr(loc_U), _lib.ptr(recv), SW, final, _lib.ptr(md), _lib.ptr(num), _lib.ptr(h),
+                      step.n_own(l, d), st)
+        md_recv = _from_owner(step, l, md, 2)
+        alpha = _f32(nEtot, device=step.dev)
+        for d in step.devices:
+            ne = int(step.meta.n_edge[l - 1][d]) if step.meta is not None else ds.nE[l - 1]
+            _lib.call("sg_gat_alpha", _lib.ptr(ds.ws), ds.lay, l, d, slope, _lib.ptr(pre_e), _lib.ptr(md),
+                      _lib.ptr(md_recv), _lib.ptr(alpha), ne, st)
+        step.h[l] = h
+        step.keep[l] = dict(z=z, s=s, num=num, md=md, alpha=alpha, pre_e=pre_e)
+
+
+def gat_backward(step):
+    ds, p = step.ds, step.p
+    st = _lib.stream_ptr()
+    slope = float(p.leaky_slope)
+    dperm = step._dst_perm()
+    dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
+    nEtot = int(ds.lay.nEtot)
+    csr, kb = step._src_csr(1, val_mode=0)
+    d_h = step.d_h
+    from paper_2303_13775_b200.engine import _nblocks
+    for l in range(step.L, 0, -1):
+        w, dout = p.layer_dims(l - 1)
+        final = int(l == step.L)
+        keep = step.keep[l]
+        h_prev, src_row = (step.f.table, step.src_row0) if l == 1 else (step.h[l - 1], None)
+        nVp, nV, P = ds.nV[l - 1], ds.nV[l], ds.pair_bound(l)
+        W, a_s, a_d = (p.view(f"layer{l-1}.{k}") for k in ("w", "a_src", "a_dst"))
+        DS = dout + 1
+        dnc = _f32(nV, DS, device=step.dev)
+        for d in step.devices:
+            _lib.call("sg_gat_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, dout, _lib.ptr(d_h),
+                      _lib.ptr(keep["num"]), final, _lib.ptr(dnc), step.n_own(l, d), st)
+        dnc_recv = _from_owner(step, l, dnc, DS)
+        d_pre = _f32(nEtot, device=step.dev)
+        dt_loc = _f32(nV, device=step.dev)
+        dt_send = _f32(P, device=step.dev)
+        dt_recv = _f32(P, device=step.dev)
+        for d in step.devices:
+            _lib.call("sg_gat_bwd_dst", _lib.ptr(ds.ws), ds.lay, l, d, dout, slope, _lib.ptr(keep["z"]),
+                      _lib.ptr(keep["alpha"]), _lib.ptr(keep["pre_e"]), _lib.ptr(dnc), _lib.ptr(dnc_recv),
+                      DS, dp_ptr(d), _lib.ptr(d_pre), _lib.ptr(dt_loc), _lib.ptr(dt_send),
+                      step.n_rows(l, d), st)
+        if step.g > 1 and P > 0:
+            step.transport.to_owner(ds, l, dt_send, dt_recv, 1)
+            if step.meta is not None:
+                step.wire_bytes += int(step.meta.npairs[l]) * 4
+        d_z = _f32(nVp, dout, device=step.dev)
+        dsb = _f32(nVp, device=step.dev)
+        dt_tot = _f32(nV, device=step.dev)
+        for d in step.devices:
+            perm, beg, end = csr[d][:3]
+            _lib.call("sg_gat_bwd_src", _lib.ptr(ds.ws), ds.lay, l, d, dout, _lib.ptr(perm), _lib.ptr(beg),
+                      _lib.ptr(end), kb[l], _lib.ptr(keep["alpha"]), _lib.ptr(d_pre), _lib.ptr(dnc),
+                      _lib.ptr(dnc_recv), DS, _lib.ptr(dt_loc), _lib.ptr(dt_recv), _lib.ptr(a_s), _lib.ptr(a_d),
+                      _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), step.n_own(l - 1, d), st)
+        need_prev = l > 1
+        d_prev = _f32(nVp, w, device=step.dev) if need_prev else None
+        npart = w * dout + 2 * dout
+        for d in step.devices:
+            nb = _nblocks(step.n_own(l - 1, d))
+            part = _f32(nb * npart, device=step.dev)
+            _lib.call("sg_gat_bwd_param", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
+                      w, dout, _lib.ptr(keep["z"]), _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), _lib.ptr(W),
+                      _lib.ptr(part), nb, _lib.ptr(d_prev), step.n_own(l - 1, d), st)
+            step.jobs.append((part, nb, npart, step.grads[d], p.offset(f"layer{l-1}.w")))
+            step._partials.append(part)
+        d_h = d_prev
