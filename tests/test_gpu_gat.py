@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from golden_io import unpack_dict, unpack_sample
-from helpers import cached_lists, load_golden, random_partition_case, rel_err
+from helpers import assert_grads_close, cached_lists, load_golden, random_partition_case, rel_err
 from oracle.coop_oracle import CoopRun
 from oracle.model_oracle import glorot_params
 from oracle.split_oracle import split_sample
@@ -24,9 +24,7 @@ def test_gat_matches_reference_golden(name):
     assert abs(loss - float(z["loss_split"])) <= TOL * max(1.0, abs(float(z["loss_split"])))
     L = int(z["L"])
     for d in range(int(z["g"])):
-        want = unpack_dict(z, f"G{d}")
-        for k in want:
-            assert rel_err(grads[d][k], want[k]) < TOL, (d, k, rel_err(grads[d][k], want[k]))
+        assert_grads_close(grads[d], unpack_dict(z, f"G{d}"), TOL, d)
         for l in range(L + 1):
             assert rel_err(ex.states[d].h[l], z[f"h_{d}_{l}"]) < TOL, (d, l)
         for l in range(1, L + 1):
@@ -51,8 +49,7 @@ def test_gat_matches_oracle_random(g):
     rloss, rgrads = ref.run()
     assert abs(loss - rloss) <= TOL * abs(rloss)
     for d in range(g):
-        for k in rgrads[d]:
-            assert rel_err(grads[d][k], rgrads[d][k]) < TOL, (d, k, rel_err(grads[d][k], rgrads[d][k]))
+        assert_grads_close(grads[d], rgrads[d], TOL, d)
         for l in range(1, 4):
             assert rel_err(ex.states[d].h[l], ref.h[d][l]) < TOL, (d, l)
             assert rel_err(ex.states[d].layer[l]["alpha"], ref.keep[d][l]["alpha"]) < TOL, (d, l)

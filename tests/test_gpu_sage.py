@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 from golden_io import unpack_dict, unpack_sample, unpack_splits
-from helpers import cached_lists, load_golden, random_partition_case, rel_err
+from helpers import assert_grads_close, cached_lists, load_golden, random_partition_case, rel_err
 from oracle.coop_oracle import CoopRun, reduce_and_sgd
 from oracle.model_oracle import glorot_params, single_device_run
 from oracle.split_oracle import split_sample
@@ -50,9 +50,7 @@ def test_sage_matches_reference_golden(name):
     z, ex, loss, grads, rec = _run_fixture(name)
     assert abs(loss - float(z["loss_split"])) <= TOL * max(1.0, abs(float(z["loss_split"])))
     for d in range(int(z["g"])):
-        want = unpack_dict(z, f"G{d}")
-        for k in want:
-            assert rel_err(grads[d][k], want[k]) < TOL, (d, k, rel_err(grads[d][k], want[k]))
+        assert_grads_close(grads[d], unpack_dict(z, f"G{d}"), TOL, d)
         for l in range(len(ex.states[d].h)):
             assert rel_err(ex.states[d].h[l], z[f"h_{d}_{l}"]) < TOL, (d, l)
     assert rec.peer_bytes == int(z["peer_bytes"])  # reference metering formula
@@ -75,8 +73,7 @@ def test_sage_matches_oracle_random(g):
     rloss, rgrads = ref.run()
     assert abs(loss - rloss) <= TOL * abs(rloss)
     for d in range(g):
-        for k in rgrads[d]:
-            assert rel_err(grads[d][k], rgrads[d][k]) < TOL, (d, k)
+        assert_grads_close(grads[d], rgrads[d], TOL, d)
         for l in range(4):
             assert rel_err(ex.states[d].h[l], ref.h[d][l]) < TOL, (d, l)
 
@@ -145,8 +142,7 @@ def test_sage_c1_shape_parity():
     rloss, rgrads = ref.run()
     assert abs(loss - rloss) <= TOL * abs(rloss)
     for d in range(2):
-        for k in rgrads[d]:
-            assert rel_err(grads[d][k], rgrads[d][k]) < TOL, (d, k)
+        assert_grads_close(grads[d], rgrads[d], TOL, d)
 
 
 def test_sage_step_is_deterministic():
