@@ -739,3 +739,36 @@ class CapturedStep:
 
     def loss_sum(self):
         return self.out[self.p.n]
+
+
+# ---- one process per GPU ------------------------------------------------------------
+
+class RankSplitTrainer:
+    """Split-parallel training where this process is device `rank` of a
+    `world`-GPU split (torchrun, one process per GPU). Every rank runs the
+    splitter on the replicated sample, computes only its own part, exchanges
+    partial aggregates with its peers over the transport (NCCL all-to-all-v)
+    and all-reduces the flat gradient before the SGD step."""
+
+    def __init__(self, params, pm, cache, feats, labels, rank, world, transport, device="cuda"):
+        self.pm, self.cache = pm, cache
+        self.rank, self.world = int(rank), int(world)
+        self.dev = torch.device(device)
+        host = params if isinstance(params, ModelParams) else ModelParams.from_reference(params)
+        self.dp = params if isinstance(params, DeviceParams) else DeviceParams.from_host(host, self.dev)
+        self.feats = feats
+        self.labels = labels if isinstance(labels, torch.Tensor) else _labels_dev(labels, self.dev)
+        self.transport = transport
+
+    def step(self, sample, lr, record_events=False, dsplit=None):
+        ds = dsplit if dsplit is not None else DeviceSplit.from_sample(sample, self.pm, self.cache, self.dev)
+        st = SplitStep(self.dp, ds, self.feats, self.labels, devices=[self.rank],
+                       transport=self.transport, exact=True, record_events=record_events)
+        st.run()
+        gbuf = st.grads[self.rank]
+        self.transport.all_reduce(gbuf)          # sum over ranks (includes the loss slot)
+        ptrs = np.asarray([gbuf.data_ptr()], dtype=np.int64)
+        _lib.call("sg_sum_sgd", _lib.ptr(self.dp.flat), None, _lib.ptr(ptrs), 1, self.dp.n,
+                  float(lr) / len(sample.targets), _lib.stream_ptr())
+        self.last = st
+        return gbuf

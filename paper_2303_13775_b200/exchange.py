@@ -17,6 +17,9 @@ from paper_2303_13775_b200 import _lib
 class LocalTransport:
     kind = "local"
 
+    def all_reduce(self, t):
+        pass  # all devices' gradients are summed by sg_sum_sgd in device order
+
     def to_owner(self, dsplit, l, send, recv, stride):
         _lib.call("sg_xfer_to_owner", _lib.ptr(dsplit.ws), dsplit.lay, l, _lib.ptr(send),
                   _lib.ptr(recv), int(stride), _lib.stream_ptr())
@@ -28,15 +31,38 @@ class LocalTransport:
 
 
 class NcclTransport:
-    """Rank-local exchange over torch.distributed (NCCL on GPUs; gloo works
-    for CPU tests of the descriptor logic)."""
+    """Rank-local exchange over torch.distributed: NCCL all-to-all-v on GPUs.
+
+    stage_on_host=True copies the payload through host memory and uses the
+    process group's CPU collective (gloo); it exists so the rank-local code
+    path can be exercised by several processes sharing one GPU in tests."""
 
     kind = "nccl"
 
-    def __init__(self, rank, world_size, group=None):
+    def __init__(self, rank, world_size, group=None, stage_on_host=False):
         self.rank = int(rank)
         self.world = int(world_size)
         self.group = group
+        self.stage = bool(stage_on_host)
+
+    def _a2a(self, out, inp, out_splits, in_splits):
+        import torch.distributed as dist
+        if not self.stage:
+            dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+            return
+        o = out.cpu()
+        dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits, group=self.group)
+        out.copy_(o)
+
+    def all_reduce(self, t):
+        """Sum a flat gradient buffer over ranks (NCCL allreduce)."""
+        import torch.distributed as dist
+        if not self.stage:
+            dist.all_reduce(t, group=self.group)
+            return
+        c = t.cpu()
+        dist.all_reduce(c, group=self.group)
+        t.copy_(c)
 
     def _splits(self, meta, l):
         r, g = self.rank, self.world
@@ -45,24 +71,19 @@ class NcclTransport:
         return send_rows, recv_rows
 
     def to_owner(self, dsplit, l, send, recv, stride):
-        import torch.distributed as dist
         m = dsplit.host_meta()
         r = self.rank
         send_rows, recv_rows = self._splits(m, l)
         s0, s1 = int(m.ref_off[l][r]), int(m.ref_off[l][r + 1])
         r0, r1 = int(m.recv_off[l][r]), int(m.recv_off[l][r + 1])
-        dist.all_to_all_single(recv[r0:r1].reshape(-1), send[s0:s1].reshape(-1),
-                               [c * stride for c in recv_rows], [c * stride for c in send_rows],
-                               group=self.group)
+        self._a2a(recv[r0:r1].reshape(-1), send[s0:s1].reshape(-1),
+                  [c * stride for c in recv_rows], [c * stride for c in send_rows])
 
     def from_owner(self, dsplit, l, send_recv_layout, recv_pair_layout, stride):
-        import torch.distributed as dist
         m = dsplit.host_meta()
         r = self.rank
         send_rows, recv_rows = self._splits(m, l)   # reversed roles
         s0, s1 = int(m.recv_off[l][r]), int(m.recv_off[l][r + 1])
         r0, r1 = int(m.ref_off[l][r]), int(m.ref_off[l][r + 1])
-        dist.all_to_all_single(recv_pair_layout[r0:r1].reshape(-1),
-                               send_recv_layout[s0:s1].reshape(-1),
-                               [c * stride for c in send_rows], [c * stride for c in recv_rows],
-                               group=self.group)
+        self._a2a(recv_pair_layout[r0:r1].reshape(-1), send_recv_layout[s0:s1].reshape(-1),
+                  [c * stride for c in send_rows], [c * stride for c in recv_rows])

@@ -1,0 +1,160 @@
+"""CPU tests of the native library's host side: the C ABI loads and exports
+every entry point include/splitgnn_b200.h declares, struct layouts agree,
+and the host-native sampler / generator keep the reference semantics
+(sampling.py:105-177). No GPU compute is called here."""
+
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "splitgnn_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2303_13775_b200 import _lib
+    lib = _lib.load()
+    syms = _declared_symbols()
+    assert len(syms) > 30
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    # the ctypes binding covers every declared entry point
+    assert not (set(syms) - set(_lib.EXPORTED)), sorted(set(syms) - set(_lib.EXPORTED))
+
+
+def test_struct_sizes_match_abi():
+    from paper_2303_13775_b200 import _lib
+    sizes = np.zeros(2, dtype=np.int64)
+    _lib.load().sg_struct_sizes(sizes.ctypes.data)
+    assert sizes.tolist() == [C.sizeof(_lib.SgMeta), C.sizeof(_lib.SgSplitLayout)]
+
+
+def test_split_layout_is_aligned_and_bounded():
+    from paper_2303_13775_b200 import _lib
+    lay = _lib.SgSplitLayout()
+    nV = (C.c_int64 * 4)(5000, 900, 200, 64)
+    nE = (C.c_int64 * 3)(8000, 1500, 300)
+    _lib.check(_lib.load().sg_split_layout(3, 4, nV, nE, 100000, C.byref(lay)))
+    offs = [getattr(lay, n) for n, _ in _lib.SgSplitLayout._fields_ if n.startswith("o_")]
+    assert all(o % 256 == 0 for o in offs)
+    assert max(offs) < lay.total_bytes
+    assert lay.nPtot == min(1500, 3 * 200) + min(300, 3 * 64) + min(8000, 3 * 900)
+    with pytest.raises(ValueError):
+        _lib.check(_lib.load().sg_split_layout(3, 17, nV, nE, 100000, C.byref(lay)))
+
+
+def _graph():
+    import paper_2303_13775_b200 as sg
+    return sg.generate_powerlaw(20000, 200000, blocks=16, p_local=0.8, seed=5, threads=4)
+
+
+def test_generator_deterministic_across_threads():
+    import paper_2303_13775_b200 as sg
+    a = sg.generate_powerlaw(5000, 40000, seed=3, threads=1)
+    b = sg.generate_powerlaw(5000, 40000, seed=3, threads=7)
+    assert np.array_equal(a.row_offsets, b.row_offsets)
+    assert np.array_equal(a.col_indices, b.col_indices)
+    assert a.num_edges == 40000
+    # power law: a hub far above the mean in-degree
+    assert a.in_degrees().max() > 20 * a.in_degrees().mean()
+
+
+def test_sampler_reference_semantics():
+    import paper_2303_13775_b200 as sg
+    g = _graph()
+    rng = np.random.default_rng(0)
+    targets = rng.choice(g.num_vertices, 300, replace=False)
+    s = sg.NativeSampler(g, threads=4).sample(targets, [7, 5, 3], seed=11)
+    s.validate(g.num_vertices)  # prefix property, unique edges, self-edges (sampling.py:68-90)
+    fan = [7, 5, 3]
+    for l in range(1, 4):
+        src, dst = (np.asarray(a) for a in s.edges(l))
+        V_lo, V_hi = np.asarray(s.vertices(l - 1)), np.asarray(s.vertices(l))
+        # destinations in order, each starting with its self-edge
+        assert np.all(np.diff(dst) >= 0)
+        first = np.r_[True, dst[1:] != dst[:-1]]
+        assert np.array_equal(src[first], dst[first])
+        deg = np.bincount(dst, minlength=len(V_hi))
+        indeg = g.in_degrees()[V_hi]
+        assert np.all(deg <= 1 + fan[l - 1])
+        assert np.all(deg <= 1 + indeg)
+        # every sampled neighbour is a real in-neighbour
+        for i in rng.choice(len(src), 50):
+            u, v = V_lo[src[i]], V_hi[dst[i]]
+            if u != v:
+                nb = g.col_indices[g.row_offsets[v]:g.row_offsets[v + 1]]
+                assert u in nb
+        # vertices with deg <= fanout take every distinct neighbour
+        small = np.flatnonzero((indeg > 0) & (indeg <= fan[l - 1]))[:20]
+        for i in small:
+            v = V_hi[i]
+            nb = set(g.col_indices[g.row_offsets[v]:g.row_offsets[v + 1]].tolist()) - {int(v)}
+            assert deg[i] - 1 == len(nb)
+
+
+def test_sampler_deterministic_and_thread_independent():
+    import paper_2303_13775_b200 as sg
+    g = _graph()
+    t = np.arange(0, 20000, 37)
+    a = sg.NativeSampler(g, threads=1).sample(t, [6, 4], seed=3)
+    b = sg.NativeSampler(g, threads=8).sample(t, [6, 4], seed=3)
+    c = sg.NativeSampler(g, threads=8).sample(t, [6, 4], seed=4)
+    for x, y in zip(a.layer_vertices, b.layer_vertices):
+        assert np.array_equal(x, y)
+    for (xs, xd), (ys, yd) in zip(a.layer_edges, b.layer_edges):
+        assert np.array_equal(xs, ys) and np.array_equal(xd, yd)
+    assert not all(np.array_equal(x, y) for x, y in zip(a.layer_vertices, c.layer_vertices))
+
+
+def test_sampler_errors_match_reference_messages():  # sampling.py:128-136
+    import paper_2303_13775_b200 as sg
+    g = _graph()
+    rng = np.random.default_rng(0)
+    with pytest.raises(ValueError, match="non-empty"):
+        sg.sample_minibatch(g, [], [2], rng)
+    with pytest.raises(ValueError, match="distinct"):
+        sg.sample_minibatch(g, [1, 1], [2], rng)
+    with pytest.raises(ValueError, match="out of range"):
+        sg.sample_minibatch(g, [g.num_vertices], [2], rng)
+    with pytest.raises(ValueError, match="fanouts"):
+        sg.sample_minibatch(g, [1], [], rng)
+
+
+def test_sampler_zero_fanout_and_path_graph():  # test_sampling.py:20-43
+    import paper_2303_13775_b200 as sg
+    # path 0 -> 1 -> 2 -> 3 (in-CSR: in-neighbour of v is v-1)
+    g = sg.from_edges(4, [0, 1, 2], [1, 2, 3])
+    s = sg.sample_minibatch(g, [3], [1, 1], np.random.default_rng(0))
+    assert [v.tolist() for v in s.layer_vertices] == [[3, 2, 1], [3, 2], [3]]
+    z = sg.sample_minibatch(g, [3, 1], [0], np.random.default_rng(0))
+    assert z.layer_vertices[0].tolist() == [3, 1]
+    assert np.asarray(z.edges(1)[0]).tolist() == [0, 1]
+
+
+def test_synthetic_features_host_values():
+    import paper_2303_13775_b200 as sg
+    a = sg.synthetic_features(10, 7, seed=3)
+    b = sg.synthetic_features(0, 7, seed=3, row_ids=np.array([4, 9]))
+    assert np.array_equal(a[[4, 9]], b)
+    assert a.dtype == np.float32 and a.min() >= 0 and a.max() < 1
+    # 24-bit values: exact in fp32 and fp64
+    assert np.array_equal((a * 2**24).astype(np.float64), np.round(a.astype(np.float64) * 2**24))
+
+
+def test_init_params_matches_oracle_draws():
+    import paper_2303_13775_b200 as sg
+    from oracle.model_oracle import glorot_params
+    for kind in ("graphsage", "gat"):
+        p = sg.init_params(kind, 12, 8, 5, 3, seed=9).tensors()
+        q = glorot_params(kind, 12, 8, 5, 3, seed=9)
+        assert list(p) == list(q)
+        for k in p:
+            assert np.array_equal(p[k], q[k])
