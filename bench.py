@@ -241,13 +241,14 @@ def main():
 
     edges = sum(samples[i].total_edges for i in range(args.warmup, n_steps))
     agg_ms, step_ms = [], []
+    phases = {}
     clocks = ClockSampler(local)
     if g == 1:
         # ---- single GPU: the whole step is one captured CUDA graph ----------------
         from paper_2303_13775_b200.engine import CapturedStep, capacities_for
         cap_nV, cap_nE = capacities_for(samples)
         cs = CapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, LR / args.batch, dev,
-                          record_events=True)
+                          record_events="agg")
         cs.capture(samples[0])                     # eager warm-up step 0 + capture
         agg_in_graph = True
         for i in range(1, args.warmup):
@@ -273,6 +274,17 @@ def main():
                     agg_in_graph = False
             barrier()
             t_wall = time.perf_counter() - t_wall
+        # diagnostic (untimed): a second capture with an event around every phase
+        diag = CapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, 0.0, dev,
+                            record_events="all")
+        diag.capture(samples[0])
+        nd = min(5, args.steps)
+        for i in range(args.warmup, args.warmup + nd):
+            flush.zero_()
+            diag.run(samples[i])
+            torch.cuda.synchronize()
+            for k, v in diag.step.phase_ms().items():
+                phases[k] = phases.get(k, 0.0) + v / nd
         # graph replays launch the captured kernels: count them from one eager step
         # (which also times the layer-1 SpMM with events if the in-graph
         # event nodes were not readable)
@@ -419,6 +431,7 @@ def main():
             "e2e": {"value": e2e, "unit": "edges/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": 4 + (0 if g == 1 else 0), "ms_per_step": e2e_ms / args.steps},
             "gpu_launches": int(launches),
+            "phases_ms": {k: round(v, 5) for k, v in sorted(phases.items(), key=lambda x: -x[1])},
             "clocks": clocks.summary(),
             "wall_s_timed": t_wall,
             "loss_last": losses[-1] if losses else None,

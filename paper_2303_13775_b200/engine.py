@@ -65,7 +65,9 @@ class SplitStep:
         self.h = [None] * (self.L + 1)
         self.keep = [None] * (self.L + 1)
         self.grads = None
+        # record_events: False | True/"all" (every phase) | "agg" (layer-1 SpMM only)
         self.events = {} if record_events else None
+        self.ev_mode = "agg" if record_events == "agg" else "all"
         self.wire_bytes = 0
         self.host_bytes = 0
 
@@ -85,6 +87,8 @@ class SplitStep:
 
     def _ev(self, name):
         if self.events is None:
+            return None
+        if self.ev_mode == "agg" and not name.startswith("agg1"):
             return None
         try:  # external=True: a real event-record node when captured in a CUDA graph
             e = torch.cuda.Event(enable_timing=True, external=True)
@@ -122,12 +126,40 @@ class SplitStep:
                 self._dperm[d] = (perm, ws, keys, ndev)
         return self._dperm
 
+    def phase(self, name):
+        """Context manager recording start/end events of a phase (profiling)."""
+        step = self
+
+        class _P:
+            def __enter__(self_):
+                if step.events is not None:
+                    step._ev(f"ph:{name}:s")
+
+            def __exit__(self_, *a):
+                if step.events is not None:
+                    step._ev(f"ph:{name}:e")
+        return _P()
+
+    def phase_ms(self):
+        """{phase: ms} from the most recent recording (after synchronisation)."""
+        out = {}
+        if not self.events:
+            return out
+        for k, v in self.events.items():
+            if k.startswith("ph:") and k.endswith(":s"):
+                name = k[3:-2]
+                e = self.events.get(f"ph:{name}:e")
+                if e:
+                    out[name] = out.get(name, 0.0) + sum(a.elapsed_time(b) for a, b in zip(v, e))
+        return out
+
     def forward(self):
         if self.kind != "graphsage":
             from paper_2303_13775_b200.gat import gat_forward
             return gat_forward(self)
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
-        self.layer0()
+        with self.phase("layer0"):
+            self.layer0()
         dperm = self._dst_perm()
         self.h[0] = self.f.table
         for l in range(1, self.L + 1):
@@ -142,6 +174,7 @@ class SplitStep:
             send = _f32(P, SW, device=self.dev)
             recv = _f32(P, SW, device=self.dev)
             self._ev(f"agg{l}_start")
+            self._ev(f"ph:agg{l}:s")
             for d in self.devices:
                 if dperm is None:
                     _lib.call("sg_sage_agg_fwd", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
@@ -152,18 +185,21 @@ class SplitStep:
                               _lib.ptr(src_row), w, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
                               SW, _lib.ptr(dperm[d][0]), self.n_rows(l, d), st)
             self._ev(f"agg{l}_end")
+            self._ev(f"ph:agg{l}:e")
             if self.g > 1 and P > 0:
                 self.transport.to_owner(ds, l, send, recv, SW)
                 if self.meta is not None:
                     self.wire_bytes += int(self.meta.npairs[l]) * SW * 4
             mean = _f32(nV, w, device=self.dev)
             h = _f32(nV, dout, device=self.dev)
+            self._ev(f"ph:update{l}:s")
             for d in self.devices:
                 _lib.call("sg_sage_update", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
                           _lib.ptr(src_row), w, dout, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(recv),
                           SW, _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
                           _lib.ptr(p.view(f"layer{l-1}.bias")), final, _lib.ptr(mean), _lib.ptr(h),
                           self.n_own(l, d), st)
+            self._ev(f"ph:update{l}:e")
             self.h[l] = h
             self.keep[l] = dict(mean=mean, counts=counts)
             if DEBUG_CHECK_FINITE and not torch.isfinite(h[:nV]).all():
@@ -218,8 +254,10 @@ class SplitStep:
             self.reduce()
             return
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
-        self.loss()
-        csr, kb = self._src_csr(2) if self.L >= 2 else ({}, {})
+        with self.phase("loss"):
+            self.loss()
+        with self.phase("src_csr"):
+            csr, kb = self._src_csr(2) if self.L >= 2 else ({}, {})
         d_h = self.d_h
         for l in range(self.L, 0, -1):
             w, dout = p.layer_dims(l - 1)
@@ -230,6 +268,7 @@ class SplitStep:
             d_self = _f32(nV, w, device=self.dev) if need_prev else None
             d_sums = _f32(nV, w, device=self.dev) if need_prev else None
             npart = 2 * w * dout + dout
+            self._ev(f"ph:bwd_rows{l}:s")
             for d in self.devices:
                 nb = _nblocks(self.n_own(l, d))
                 part = _f32(nb * npart, device=self.dev)
@@ -241,6 +280,7 @@ class SplitStep:
                           self.n_own(l, d), st)
                 self.jobs.append((part, nb, npart, self.grads[d], p.offset(f"layer{l-1}.w_self")))
                 self._partials.append(part)
+            self._ev(f"ph:bwd_rows{l}:e")
             if not need_prev:
                 break
             SWb = _r4(w)
@@ -255,13 +295,16 @@ class SplitStep:
                 if self.meta is not None:
                     self.wire_bytes += int(self.meta.npairs[l]) * SWb * 4
             d_prev = _f32(ds.nV[l - 1], w, device=self.dev)
+            self._ev(f"ph:scatter{l}:s")
             for d in self.devices:
                 perm, beg, end = csr[d][:3]
                 _lib.call("sg_sage_scatter_bwd", _lib.ptr(ds.ws), ds.lay, l, d, w, _lib.ptr(d_self),
                           _lib.ptr(d_sums), _lib.ptr(brecv), SWb, _lib.ptr(perm), _lib.ptr(beg),
                           _lib.ptr(end), kb[l], _lib.ptr(d_prev), self.n_own(l - 1, d), st)
+            self._ev(f"ph:scatter{l}:e")
             d_h = d_prev
-        self.reduce()
+        with self.phase("reduce"):
+            self.reduce()
 
     def reduce(self):
         """Per-block partials -> per-device flat gradients (+ loss slot)."""
@@ -705,9 +748,22 @@ class CapturedStep:
 
     def _body(self):
         inp = self.inp
+        ev = []
+        if self.record_events and self.record_events != "agg":
+            for _ in range(2):
+                try:
+                    ev.append(torch.cuda.Event(enable_timing=True, external=True))
+                except TypeError:
+                    ev.append(torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         ds = DeviceSplit(inp.V, inp.es, inp.ed, inp.cap_nV, inp.cap_nE, self.pm, self.cache, True,
                          self.dev, sizes=inp.sizes)
+        if ev:
+            ev[1].record()
         step = SplitStep(self.p, ds, self.f, self.labels, exact=False, record_events=self.record_events)
+        if ev:
+            step.events["ph:split:s"] = [ev[0]]
+            step.events["ph:split:e"] = [ev[1]]
         step.run()
         gbuf = step.grads[0]
         ptrs = np.asarray([gbuf.data_ptr()], dtype=np.int64)
