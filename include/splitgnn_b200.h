@@ -36,6 +36,10 @@ extern "C" {
 
 #define SG_ERR_MISSING_VERTEX 1 /* SgMeta.err bit: scheduler.py:177-178 */
 
+/* sg_split_run flags */
+#define SG_SPLIT_DST_GROUPED 1 /* each destination's in-edges are contiguous */
+#define SG_SPLIT_ALL_CACHED 2  /* every sampled vertex is cached (load_gids empty) */
+
 /* Per-iteration split descriptor written by sg_split_run into device memory.
  * Counts / offsets of the reference's LocalSplit + ShufflePlan
  * (scheduler.py:24-122). Index conventions: [l] layer 0..L, [l-1] for edge
@@ -114,14 +118,15 @@ void sg_struct_sizes(int64_t* out /* [sizeof(SgMeta), sizeof(SgSplitLayout)] */)
  * actual sizes from device memory, so one captured CUDA graph serves every
  * sample that fits the capacities. asn: uint8 device of each
  * global vertex (PartitionMap.assignment, partition.py:20-52). cache_bits:
- * nullable bitmap of CacheState.global_mask (partition.py:70-75). dst_grouped:
- * 1 if every layer's edges list each destination's in-edges contiguously
- * (true for sample_minibatch output, sampling.py:148-169). */
+ * nullable bitmap of CacheState.global_mask (partition.py:70-75). flags:
+ * SG_SPLIT_DST_GROUPED if every layer's edges list each destination's in-edges
+ * contiguously (true for sample_minibatch output, sampling.py:148-169);
+ * SG_SPLIT_ALL_CACHED if the cache holds every vertex (no host loads). */
 int sg_split_layout(int32_t L, int32_t g, const int64_t* nV, const int64_t* nE,
                     int64_t n_vertices, SgSplitLayout* out);
 int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V,
                  const int32_t* esrc, const int32_t* edst, const int64_t* sizes,
-                 const uint8_t* asn, const uint32_t* cache_bits, int32_t dst_grouped,
+                 const uint8_t* asn, const uint32_t* cache_bits, int32_t flags,
                  void* stream);
 
 /* Stable LSD radix sort of (key,value) pairs (keys < 2^key_bits), used to

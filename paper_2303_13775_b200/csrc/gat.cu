@@ -306,14 +306,14 @@ __global__ void k_gat_combine(const SgMeta* __restrict__ meta, CombArgs a) {
     const int64_t G = own0 + q;
     const int* cb = a.contrib + (int64_t)g * a.voff_l + G * g;
     float m = a.loc_m[G];
-    for (int s = 0; s < g; ++s) {
+    for (int s = 0; g > 1 && s < g; ++s) {
       const int rs = cb[s];
       if (rs >= 0) m = fmaxf(m, a.recv[(int64_t)rs * a.stride + dout]);
     }
     float f = expf(a.loc_m[G] - m);
     float den = a.loc_s[G] * f;
     float U = a.loc_U[G * dout + j] * f;
-    for (int s = 0; s < g; ++s) {  // ascending sender order
+    for (int s = 0; g > 1 && s < g; ++s) {  // ascending sender order
       const int rs = cb[s];
       if (rs >= 0) {
         const float* r = a.recv + (int64_t)rs * a.stride;
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ 
       const int64_t v = own0 + a.rank[a.voff_l + p];
       float dt = a.dt_loc[v];
       const int* cb = a.contrib + (int64_t)a.g * a.voff_l + v * a.g;
-      for (int s = 0; s < a.g; ++s) {
+      for (int s = 0; a.g > 1 && s < a.g; ++s) {
         const int rs = cb[s];
         if (rs >= 0) dt += a.dt_recv[rs];
       }

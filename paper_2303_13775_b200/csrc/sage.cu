@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
         const int G = own0 + q;
         float N = a.counts[G];
         const int* cb = a.contrib + (int64_t)g * a.voff_l + (int64_t)G * g;
-        for (int s = 0; s < g; ++s) {  // ascending sender order (engine.py:130-138)
+        for (int s = 0; g > 1 && s < g; ++s) {  // ascending sender order (engine.py:130-138)
           const int rs = cb[s];
           cs_s[rr * g + s] = rs;
           if (rs >= 0) N += a.recv[(int64_t)rs * a.stride + w];
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
         const int rr = idx / w, c = idx - rr * w;
         const int64_t G = own0 + tile * UTR + rr;
         float S = a.sums[G * w + c];
-        for (int s = 0; s < g; ++s) {
+        for (int s = 0; g > 1 && s < g; ++s) {
           const int rs = cs_s[rr * g + s];
           if (rs >= 0) S += a.recv[(int64_t)rs * a.stride + c];
         }

@@ -587,6 +587,63 @@ __global__ void k_local_edges(const int32_t* __restrict__ esrc, const int32_t* _
   }
 }
 
+// g == 1 with no partial cache and destination-grouped edges: the split is the
+// identity (_group_by with one key keeps everything in order), so one pass
+// writes every array the executor reads.
+__global__ void k_split_single(const int32_t* __restrict__ V, const int32_t* __restrict__ esrc,
+                               const int32_t* __restrict__ edst, MetaHeader h, SgMeta* meta,
+                               int64_t n_asn, int all_cached, int32_t* __restrict__ rank,
+                               int32_t* __restrict__ grouped, int32_t* __restrict__ egrouped,
+                               LocalOut out) {
+  const int L = h.L;
+  const int64_t nVtot = h.voff[L + 1], nE = h.eoff[L];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int l = 0; l <= L; ++l) {
+      meta->n_own[l][0] = (int32_t)meta->nV[l];
+      meta->own_off[l][0] = 0;
+      meta->own_off[l][1] = (int32_t)meta->nV[l];
+    }
+    for (int li = 0; li < L; ++li) {
+      meta->n_edge[li][0] = (int32_t)meta->nE[li];
+      meta->edge_off[li][0] = 0;
+      meta->edge_off[li][1] = (int32_t)meta->nE[li];
+    }
+    const int32_t nl = all_cached ? 0 : (int32_t)meta->nV[0];
+    meta->n_load[0] = nl;
+    meta->load_off[0] = 0;
+    meta->load_off[1] = nl;
+  }
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nVtot + nE;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    if (x < nVtot) {
+      const int l = layer_of(h.voff, L + 1, x);
+      const int64_t p = x - h.voff[l];
+      if (p >= meta->nV[l]) continue;
+      const int32_t gid = V[x];
+      if (gid < 0 || gid >= n_asn) atomicOr(&meta->err, SG_ERR_MISSING_VERTEX);
+      rank[x] = (int32_t)p;
+      grouped[x] = (int32_t)p;
+      if (l >= 1) out.selfrow[x] = (int32_t)p;
+      if (l == 0 && !all_cached) {
+        rank[nVtot + p] = (int32_t)p;
+        grouped[nVtot + p] = (int32_t)p;
+      }
+    } else {
+      const int64_t y = x - nVtot;
+      const int li = layer_of(h.eoff, L, y);
+      const int i = (int)(y - h.eoff[li]);
+      if (i >= meta->nE[li]) continue;
+      const int32_t src = esrc[y], dst = edst[y];
+      egrouped[y] = i;
+      out.lsrc[y] = src;
+      out.ldst[y] = dst;
+      const int64_t R = h.rbase[li] + dst;
+      if (i == 0 || edst[y - 1] != dst) out.rowbeg[R] = i;
+      if (i == meta->nE[li] - 1 || edst[y + 1] != dst) out.rowend[R] = i + 1;
+    }
+  }
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host side
@@ -695,8 +752,10 @@ extern "C" int sg_split_layout(int32_t L, int32_t g, const int64_t* nV, const in
 
 extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V,
                             const int32_t* esrc, const int32_t* edst, const int64_t* sizes,
-                            const uint8_t* asn, const uint32_t* cache_bits, int32_t dst_grouped,
+                            const uint8_t* asn, const uint32_t* cache_bits, int32_t flags,
                             void* stream) {
+  const int32_t dst_grouped = flags & SG_SPLIT_DST_GROUPED;
+  const int all_cached = (flags & SG_SPLIT_ALL_CACHED) ? 1 : 0;
   SG_REQUIRE(ws && lay, "split: null workspace");
   const SgSplitLayout& y = *lay;
   const int L = y.L, g = y.g;
@@ -718,6 +777,17 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   for (int l = 0; l < SG_MAXL + 1; ++l) h.eoff[l] = l <= L ? y.eoff[l] : y.eoff[L];
   for (int l = 0; l <= SG_MAXL; ++l) h.rbase[l] = l <= L ? y.rbase[l] : y.rbase[L];
 
+  if (g == 1 && dst_grouped && (cache_bits == nullptr || all_cached)) {
+    k_meta_init<<<1, 256, 0, st>>>(h, sizes, meta);
+    SG_CHECK_LAUNCH("k_meta_init");
+    LocalOut lo{P32(y.o_lsrc), P32(y.o_ldst), P32(y.o_rowbeg), P32(y.o_rowend), P32(y.o_selfrow)};
+    const int64_t tot = y.nVtot + y.nEtot;
+    k_split_single<<<clamp_grid(div_up(tot, 256), kSMs * 8), 256, 0, st>>>(
+        V, esrc, edst, h, meta, y.n_vertices, all_cached, P32(y.o_rank), P32(y.o_grouped),
+        P32(y.o_egrouped), lo);
+    SG_CHECK_LAUNCH("k_split_single");
+    return SG_OK;
+  }
   // zero-initialised regions: pair masks, gid bitmaps, rows; contrib = -1.
   SG_CUDA(cudaMemsetAsync(base + y.o_pmask, 0, 4 * y.nVtot, st));
   if (g > 1) SG_CUDA(cudaMemsetAsync(base + y.o_bitmap, 0, 4 * y.bm_words * L, st));

@@ -30,7 +30,7 @@ from paper_2303_13775_b200.sampling import epoch_batches, sample_minibatch
 from paper_2303_13775_b200.scheduler import DeviceSplit, split_minibatch
 
 DEBUG_CHECK_FINITE = False
-NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions
+NB_PARTIAL = 6 * 148  # max blocks of the deterministic partial reductions
 
 
 def _nblocks(rows, tile=32):
@@ -101,6 +101,11 @@ class SplitStep:
     # -- forward ----------------------------------------------------------------
     def layer0(self):
         ds, st = self.ds, _lib.stream_ptr()
+        if self.g == 1 and self.f.identity:
+            # one device, whole table cached in id order: the layer-0 owned rows
+            # are the sample positions and their table rows are the gids
+            self.src_row0 = ds.V
+            return
         self.src_row0 = torch.empty(max(ds.nV[0], 1), dtype=torch.int32, device=self.dev)
         if self.meta is not None and int(self.meta.load_off[self.g]) > 0:
             self.host_bytes += self.f.stage_misses(ds, self.meta)
@@ -238,7 +243,7 @@ class SplitStep:
         ncls = hid * C + C + 1
         self._partials = []
         for d in self.devices:
-            nb = _nblocks(self.n_own(L, d))
+            nb = _nblocks(self.n_own(L, d), tile=8)
             part = _f32(nb * ncls, device=self.dev)
             _lib.call("sg_cls_loss", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(ds.V), _lib.ptr(self.labels),
                       _lib.ptr(self.h[L]), hid, C, _lib.ptr(p.view("cls.w")), _lib.ptr(p.view("cls.b")),

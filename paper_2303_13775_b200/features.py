@@ -17,12 +17,13 @@ from paper_2303_13775_b200 import _lib
 
 
 class FeatureStore:
-    def __init__(self, table, cache_slot, n_cached, feat_dim, host_features=None):
+    def __init__(self, table, cache_slot, n_cached, feat_dim, host_features=None, identity=False):
         self.table = table                  # [n_cached + staging, F] fp32 cuda
         self.cache_slot = cache_slot        # [n] int32 cuda
         self.n_cached = int(n_cached)
         self.feat_dim = int(feat_dim)
         self.host_features = host_features  # numpy [n, F] for misses (or None)
+        self.identity = bool(identity)      # row of vertex v is v (whole graph cached in id order)
 
     @property
     def device(self):
@@ -57,7 +58,7 @@ class FeatureStore:
             _lib.check(lib.sg_fill_uniform(_lib.ptr(table), rows, int(feat_dim), int(seed), 0,
                                            _lib.stream_ptr()), "fill_uniform")
             slot = torch.arange(n, dtype=torch.int32, device=device)
-            return cls(table, slot, rows, feat_dim, None)
+            return cls(table, slot, rows, feat_dim, None, identity=True)
         row_ids = np.asarray(row_ids, dtype=np.int64)
         table = torch.empty((len(row_ids), feat_dim), dtype=torch.float32, device=device)
         # contiguous runs are generated directly

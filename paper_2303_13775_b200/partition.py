@@ -99,6 +99,10 @@ class CacheState:
             self._bits = torch.from_numpy(packed.view(np.uint32).copy()).to(device)
         return self._bits
 
+    def covers_all(self, n):
+        """True when every vertex is cached somewhere (no host loads ever)."""
+        return int(sum(len(c) for c in self.cached)) >= n and bool(self.global_mask(n).all())
+
     def validate(self, pm, n):
         cap = math.ceil(self.capacity_fraction * n - 1e-9)
         for d, ids in enumerate(self.cached):

@@ -156,10 +156,15 @@ class DeviceSplit:
         self.V, self.esrc, self.edst = V, esrc, edst
         self.host_V = host_V
         bits = cache.device_bits(len(pm.assignment), self.device) if cache is not None else None
+        n = len(pm.assignment)
+        if cache is not None and getattr(cache, "_all", None) is None:
+            cache._all = cache.covers_all(n)
+        flags = (1 if self.dst_grouped else 0) | (2 if cache is not None and cache._all else 0)
+        self.all_cached = bool(flags & 2)
         self.sizes = sizes
         _lib.check(lib.sg_split_run(_lib.ptr(self.ws), C.byref(lay), _lib.ptr(V), _lib.ptr(esrc),
                                     _lib.ptr(edst), _lib.ptr(sizes), _lib.ptr(pm.device_u8(self.device)),
-                                    _lib.ptr(bits), int(self.dst_grouped), _lib.stream_ptr()),
+                                    _lib.ptr(bits), flags, _lib.stream_ptr()),
                    "split_run")
         self._meta = None
         self._views = None
