@@ -185,6 +185,15 @@ int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t
                          const float* h_prev, const int32_t* src_row, int32_t w, float* sums,
                          float* counts, float* sendbuf, int32_t send_stride,
                          const int32_t* dperm, int64_t max_rows, void* stream);
+/* Single-device split (g = 1: no reference rows, no remote contributions):
+ * aggregation + mean + both GEMVs + bias + ReLU in one kernel
+ * (engine.py:180-226 with the exchange vacuous). Also writes mean, counts and
+ * the compact self rows hs (n_own x w) the backward pass reads. */
+int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                      const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                      const float* w_self, const float* w_neigh, const float* bias,
+                      int32_t final_layer, float* mean, float* counts, float* hs, float* h,
+                      int64_t max_rows, void* stream);
 /* Owner combine + update (engine.py:197-226): adds the holders' partial
  * (sum,count) rows from recvbuf in ascending sender order, mean = S/N,
  * pre = h_self@W_self + mean@W_neigh + b, h = relu(pre) unless final.
@@ -197,14 +206,16 @@ int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l, in
 /* Backward row pass (engine.py:228-254): d_pre = d_h*[h>0] (or d_h if final);
  * per-block partial sums of h_self^T d_pre, mean^T d_pre and sum(d_pre)
  * (reduced later by sg_reduce_partials, deterministic order); optionally
- * d_self = d_pre W_self^T and d_sums = (d_pre W_neigh^T)/counts. */
+ * d_self = d_pre W_self^T and d_sums = (d_pre W_neigh^T)/counts.
+ * self_compact: h_prev is the compact self-row buffer (hs of
+ * sg_sage_fused_fwd) indexed by owned row, instead of the layer input. */
 int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                      const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
                      const float* d_h, const float* h, int32_t final_layer,
                      const float* mean, const float* counts,
                      const float* w_self, const float* w_neigh,
                      float* partial, int32_t nblocks, float* d_self, float* d_sums,
-                     int64_t max_rows, void* stream);
+                     int32_t self_compact, int64_t max_rows, void* stream);
 /* Transpose SpMM (engine.py:263-273): for each owned row u at l-1,
  * d_prev[u] = [u is the self row of v] d_self[v] + sum over out-edges of
  * d_sums_all[dst], where reference destinations read the owners' returned

@@ -203,6 +203,189 @@ int launch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStrea
   return SG_OK;
 }
 
+// ---------------------------------------------------------------- fused forward (g == 1)
+// Single-device split: no row has remote contributions, so the update runs in
+// the aggregation kernel. The row team holds the row sums (lanes x float4);
+// each lane forms partial dot products for all dout outputs against the
+// TRANSPOSED weights in smem (conflict-free LDS.128), then a recursive-halving
+// xor reduction leaves each output on one lane (fixed order: deterministic).
+struct FusedArgs {
+  int l, d, w, dout, final_;
+  int64_t eoff_li, rbase_li, voff_l;
+  const int32_t* rowbeg;
+  const int32_t* rowend;
+  const int32_t* lsrc;
+  const int32_t* selfrow;
+  const int32_t* src_row;
+  const float* h_prev;
+  const float* ws;
+  const float* wn;
+  const float* bias;
+  float* mean;
+  float* counts;
+  float* hs;
+  float* h;
+};
+
+template <int LPR, int EG, int DO>
+__global__ void __launch_bounds__(256) k_sage_fused(const SgMeta* __restrict__ meta, FusedArgs a) {
+  extern __shared__ __align__(16) float smem[];
+  constexpr int RL = LPR * EG;
+  constexpr int RPW = 32 / RL;
+  const int w = a.w, dout = a.dout;
+  float* wsT = smem;            // [DO][w]
+  float* wnT = wsT + DO * w;    // [DO][w]
+  for (int i = threadIdx.x; i < w * DO; i += blockDim.x) {
+    const int c = i / DO, j = i - c * DO;
+    const bool ok = j < dout;
+    wsT[j * w + c] = ok ? a.ws[c * dout + j] : 0.f;
+    wnT[j * w + c] = ok ? a.wn[c * dout + j] : 0.f;
+  }
+  __syncthreads();
+  const int l = a.l, d = a.d;
+  const int n_own = meta->n_own[l][d];
+  const int own0 = meta->own_off[l][d];
+  const int prev0 = meta->own_off[l - 1][d];
+  const int64_t rb = a.rbase_li + own0;
+  const int lane = threadIdx.x & 31;
+  const int team = lane / RL, tl = lane % RL, eg = tl / LPR, lr = tl % LPR;
+  const unsigned tmask = (RL == 32) ? 0xffffffffu : (((1u << RL) - 1u) << (team * RL));
+  const int col = lr * 4;
+  const bool colok = col < w;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = gw * RPW + team; q < n_own; q += nw * RPW) {
+    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
+    const int64_t G = own0 + q;
+    int rself = prev0 + a.selfrow[a.voff_l + G];
+    if (a.src_row) rself = a.src_row[rself];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int jb = b; jb < e; jb += RL) {
+      const int j = jb + tl;
+      int r = 0;
+      if (j < e) {
+        r = prev0 + a.lsrc[a.eoff_li + j];
+        if (a.src_row) r = a.src_row[r];
+      }
+      const int cnt = min(RL, e - jb);
+      const int rounds = (cnt + EG - 1) / EG;
+      int kk = 0;
+      for (; kk + 4 <= rounds; kk += 4) {
+        int rr[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = (kk + u) * EG + eg;
+          rr[u] = __shfl_sync(tmask, r, k < RL ? k : RL - 1, RL);
+          ok[u] = k < cnt;
+        }
+        if (colok) {
+          float4 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            v[u] = ok[u] ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr[u] * w + col))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+          }
+        }
+      }
+      for (; kk < rounds; ++kk) {
+        const int k = kk * EG + eg;
+        const int r0 = __shfl_sync(tmask, r, k < RL ? k : RL - 1, RL);
+        if (k < cnt && colok) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)r0 * w + col));
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < RL; o <<= 1) {
+      acc.x += __shfl_xor_sync(tmask, acc.x, o, RL);
+      acc.y += __shfl_xor_sync(tmask, acc.y, o, RL);
+      acc.z += __shfl_xor_sync(tmask, acc.z, o, RL);
+      acc.w += __shfl_xor_sync(tmask, acc.w, o, RL);
+    }
+    const float cntf = (float)(e - b);
+    const float inv = 1.0f / cntf;
+    const float4 mn = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    const float4 hv = colok ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (eg == 0 && colok) {
+      *reinterpret_cast<float4*>(a.mean + G * w + col) = mn;
+      *reinterpret_cast<float4*>(a.hs + G * w + col) = hv;
+    }
+    if (tl == 0) a.counts[G] = cntf;
+    // partial dot products over this lane's 4 columns for every output
+    float p[DO];
+#pragma unroll
+    for (int j = 0; j < DO; ++j) {
+      float t = 0.f;
+      if (colok) {
+        const float4 s4 = *reinterpret_cast<const float4*>(wsT + j * w + col);
+        const float4 n4 = *reinterpret_cast<const float4*>(wnT + j * w + col);
+        t = fmaf(hv.x, s4.x, fmaf(hv.y, s4.y, fmaf(hv.z, s4.z, hv.w * s4.w)));
+        t = fmaf(mn.x, n4.x, fmaf(mn.y, n4.y, fmaf(mn.z, n4.z, fmaf(mn.w, n4.w, t))));
+      }
+      p[j] = t;
+    }
+    // recursive halving over the LPR lanes of group eg (all groups hold the same sums)
+    int n = DO, base = 0;
+#pragma unroll
+    for (int o = LPR >> 1; o >= 1; o >>= 1) {
+      if (n > 1) {
+        const int half = n >> 1;
+        const bool up = (lr & o) != 0;
+#pragma unroll
+        for (int k = 0; k < DO / 2; ++k) {
+          if (k < half) {
+            const float send = up ? p[k] : p[k + half];
+            const float keep = up ? p[k + half] : p[k];
+            p[k] = keep + __shfl_xor_sync(tmask, send, o, RL);
+          }
+        }
+        if (up) base += half;
+        n = half;
+      } else {
+        p[0] += __shfl_xor_sync(tmask, p[0], o, RL);
+      }
+    }
+    if (eg == 0) {
+      // lanes with identical 'base' hold the same outputs; the lowest writes
+      const int dup = LPR / (DO < LPR ? DO : LPR);  // lanes per output group
+      if ((lr % dup) == 0) {
+#pragma unroll
+        for (int k = 0; k < DO; ++k) {
+          if (k < n) {
+            const int j = base + k;
+            if (j < dout) {
+              const float v = p[k] + a.bias[j];
+              a.h[G * dout + j] = a.final_ ? v : fmaxf(v, 0.f);
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
+template <int LPR, int EG, int DO>
+int launch_fused(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
+  constexpr int RPB = 8 * (32 / (LPR * EG));
+  const size_t smem = sizeof(float) * 2 * (size_t)DO * a.w;
+  if (smem > 227 * 1024) {
+    set_error("sage_fused_fwd: width too large");
+    return SG_ERR_ARG;
+  }
+  const cudaError_t attr = allow_max_smem<k_sage_fused<LPR, EG, DO>>();
+  SG_CUDA(attr);
+  const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
+  k_sage_fused<LPR, EG, DO><<<grid, 256, smem, st>>>(meta, a);
+  SG_CHECK_LAUNCH("k_sage_fused");
+  return SG_OK;
+}
+
 // dispatch on width: VEC=4 needs w%4==0 (16B aligned rows)
 int dispatch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStream_t st) {
   const int w = a.w;
@@ -359,7 +542,7 @@ constexpr int BMAXQ = 4;    // float4 slots per thread per weight matrix (w*dout
 constexpr int BMAXACC = 16;  // scalar slots (dout % 4 != 0 path)
 
 struct BwdArgs {
-  int l, d, w, dout, final_;
+  int l, d, w, dout, final_, self_compact;
   int64_t voff_l;
   const float* h_prev;
   const int32_t* src_row;
@@ -415,8 +598,13 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
       const int q = tile * BTR + rr;
       if (q < n_own) {
         const int G = own0 + q;
-        int r = prev0 + a.selfrow[a.voff_l + G];
-        if (a.src_row) r = a.src_row[r];
+        int r;
+        if (a.self_compact) {
+          r = G;  // h_prev is the compact self-row buffer written by the forward
+        } else {
+          r = prev0 + a.selfrow[a.voff_l + G];
+          if (a.src_row) r = a.src_row[r];
+        }
         prow_s[rr] = r;
         cnt_s[rr] = 1.0f / a.counts[G];
       } else {
@@ -721,6 +909,48 @@ extern "C" int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* l
                     dperm, max_rows, stream);
 }
 
+extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
+                                 int32_t d, const float* h_prev, const int32_t* src_row, int32_t w,
+                                 int32_t dout, const float* w_self, const float* w_neigh,
+                                 const float* bias, int32_t final_layer, float* mean, float* counts,
+                                 float* hs, float* h, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay, "sage_fused_fwd: null workspace");
+  SPLIT_PTRS
+  SG_REQUIRE(y.g == 1, "sage_fused_fwd: single-device split only (no remote contributions)");
+  SG_REQUIRE(l >= 1 && l <= y.L && d == 0, "sage_fused_fwd: bad layer/device");
+  SG_REQUIRE(w % 4 == 0 && w <= 128 && dout >= 1 && dout <= 32,
+             "sage_fused_fwd: needs w % 4 == 0, w <= 128, dout <= 32");
+  if (max_rows <= 0) return SG_OK;
+  FusedArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.w = w; a.dout = dout; a.final_ = final_layer;
+  a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.voff_l = y.voff[l];
+  a.rowbeg = I32(y.o_rowbeg); a.rowend = I32(y.o_rowend); a.lsrc = I32(y.o_lsrc);
+  a.selfrow = I32(y.o_selfrow); a.src_row = src_row; a.h_prev = h_prev;
+  a.ws = w_self; a.wn = w_neigh; a.bias = bias;
+  a.mean = mean; a.counts = counts; a.hs = hs; a.h = h;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int DOp = dout <= 8 ? 8 : (dout <= 16 ? 16 : 32);
+  if (w <= 16) {
+    if (DOp == 8) return launch_fused<4, 4, 8>(meta, a, max_rows, st);
+    if (DOp == 16) return launch_fused<4, 4, 16>(meta, a, max_rows, st);
+    return launch_fused<4, 4, 32>(meta, a, max_rows, st);
+  }
+  if (w <= 32) {
+    if (DOp == 8) return launch_fused<8, 4, 8>(meta, a, max_rows, st);
+    if (DOp == 16) return launch_fused<8, 4, 16>(meta, a, max_rows, st);
+    return launch_fused<8, 4, 32>(meta, a, max_rows, st);
+  }
+  if (w <= 64) {
+    if (DOp == 8) return launch_fused<16, 2, 8>(meta, a, max_rows, st);
+    if (DOp == 16) return launch_fused<16, 2, 16>(meta, a, max_rows, st);
+    return launch_fused<16, 2, 32>(meta, a, max_rows, st);
+  }
+  if (DOp == 8) return launch_fused<32, 1, 8>(meta, a, max_rows, st);
+  if (DOp == 16) return launch_fused<32, 1, 16>(meta, a, max_rows, st);
+  return launch_fused<32, 1, 32>(meta, a, max_rows, st);
+}
+
 extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l,
                               int32_t d, const float* h_prev, const int32_t* src_row, int32_t w,
                               int32_t dout, const float* sums, float* counts,
@@ -776,8 +1006,8 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
                                 int32_t dout, const float* d_h, const float* h,
                                 int32_t final_layer, const float* mean, const float* counts,
                                 const float* w_self, const float* w_neigh, float* partial,
-                                int32_t nblocks, float* d_self, float* d_sums, int64_t max_rows,
-                                void* stream) {
+                                int32_t nblocks, float* d_self, float* d_sums, int32_t self_compact,
+                                int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "sage_bwd_rows: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_bwd_rows: bad layer/device");
@@ -794,6 +1024,7 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   a.w = w;
   a.dout = dout;
   a.final_ = final_layer;
+  a.self_compact = self_compact;
   a.voff_l = y.voff[l];
   a.h_prev = h_prev;
   a.src_row = src_row;

@@ -113,6 +113,11 @@ class SplitStep:
             _lib.call("sg_layer0_rows", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(ds.V),
                       _lib.ptr(self.f.cache_slot), int(self.f.n_cached), _lib.ptr(self.src_row0), st)
 
+    def _fused_ok(self, w, dout, dperm):
+        """Single-device split: the update can run inside the aggregation."""
+        return (self.g == 1 and dperm is None and w % 4 == 0 and w <= 128 and 1 <= dout <= 32
+                and not getattr(self, "no_fuse", False))
+
     def _dst_perm(self):
         """CSR-by-destination for samples whose edges are not grouped by dst."""
         if self.ds.dst_grouped:
@@ -172,6 +177,23 @@ class SplitStep:
             final = int(l == self.L)
             h_prev, src_row = (self.f.table, self.src_row0) if l == 1 else (self.h[l - 1], None)
             nV = ds.nV[l]
+            if self._fused_ok(w, dout, dperm):
+                mean = _f32(nV, w, device=self.dev)
+                counts = _f32(nV, device=self.dev)
+                hs = _f32(nV, w, device=self.dev)
+                h = _f32(nV, dout, device=self.dev)
+                self._ev(f"agg{l}_start")
+                self._ev(f"ph:agg+update{l}:s")
+                _lib.call("sg_sage_fused_fwd", _lib.ptr(ds.ws), ds.lay, l, 0, _lib.ptr(h_prev),
+                          _lib.ptr(src_row), w, dout, _lib.ptr(p.view(f"layer{l-1}.w_self")),
+                          _lib.ptr(p.view(f"layer{l-1}.w_neigh")), _lib.ptr(p.view(f"layer{l-1}.bias")),
+                          final, _lib.ptr(mean), _lib.ptr(counts), _lib.ptr(hs), _lib.ptr(h),
+                          self.n_own(l, 0), st)
+                self._ev(f"agg{l}_end")
+                self._ev(f"ph:agg+update{l}:e")
+                self.h[l] = h
+                self.keep[l] = dict(mean=mean, counts=counts, hs=hs)
+                continue
             sums = _f32(nV, w, device=self.dev)
             counts = _f32(nV, device=self.dev)
             SW = _r4(w + 1)
@@ -274,6 +296,9 @@ class SplitStep:
             d_sums = _f32(nV, w, device=self.dev) if need_prev else None
             npart = 2 * w * dout + dout
             self._ev(f"ph:bwd_rows{l}:s")
+            hs = self.keep[l].get("hs")
+            if hs is not None:
+                h_prev, src_row = hs, None
             for d in self.devices:
                 nb = _nblocks(self.n_own(l, d))
                 part = _f32(nb * npart, device=self.dev)
@@ -282,7 +307,7 @@ class SplitStep:
                           _lib.ptr(self.keep[l]["mean"]), _lib.ptr(self.keep[l]["counts"]),
                           _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
                           _lib.ptr(part), nb, _lib.ptr(d_self), _lib.ptr(d_sums),
-                          self.n_own(l, d), st)
+                          int(hs is not None), self.n_own(l, d), st)
                 self.jobs.append((part, nb, npart, self.grads[d], p.offset(f"layer{l-1}.w_self")))
                 self._partials.append(part)
             self._ev(f"ph:bwd_rows{l}:e")

@@ -159,3 +159,24 @@ def test_sage_step_is_deterministic():
     for a, b in zip(outs[0][1], outs[1][1]):
         for k in a:
             assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("F,hid", [(8, 6), (100, 16), (64, 32), (16, 8), (12, 4), (128, 16), (20, 3)])
+def test_sage_single_device_fused_shapes(F, hid):
+    """g = 1 runs the fused aggregate+update kernel (no remote contributions);
+    every (width, hidden) shape matches the oracle."""
+    import paper_2303_13775_b200 as sg
+    graph, pm, sample, _ = random_partition_case(70 + F, n=4000, m=40000, g=1, batch=96, fanouts=(7, 5))
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=5)
+    labels = sg.synthetic_labels(graph.num_vertices, 5, seed=6)
+    params = sg.init_params("graphsage", F, hid, 5, 2, seed=7)
+    splits, plan = sg.split_minibatch(sample, pm)
+    ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+    loss, grads = ex.run()
+    ws, wp = split_sample(sample.layer_vertices, sample.layer_edges, pm.assignment, 1)
+    ref = CoopRun(glorot_params("graphsage", F, hid, 5, 2, seed=7), ws, wp, feats.astype(np.float64), labels)
+    rloss, rgrads = ref.run()
+    assert abs(loss - rloss) <= TOL * abs(rloss)
+    assert_grads_close(grads[0], rgrads[0], TOL, 0)
+    for l in range(3):
+        assert rel_err(ex.states[0].h[l], ref.h[0][l]) < TOL, l
