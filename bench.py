@@ -131,6 +131,13 @@ def sage_fwd_bytes(E, R, w):
     return 4 * w * E + 4 * E + 4 * (R + 1) + 4 * (w + 1) * R
 
 
+def sage_fused_fwd_bytes(E, R, w, dout):
+    """Fused single-device layer (SpMM + update): the SpMM's per-edge source
+    rows, edge and row indices, then per destination row the self row read,
+    mean / self-row / count / output writes (the sums never leave the chip)."""
+    return 4 * w * E + 4 * E + 4 * (R + 1) + 4 * w * R + 4 * (2 * w + 1 + dout) * R
+
+
 def cpu_baseline(graph, labels, samples, pm_assign, g, n_iter=2):
     """Reference algorithm (oracle NumPy port) on this host, 1 thread, on the
     first n_iter samples of the same workload: split + forward + backward +
@@ -391,7 +398,7 @@ def main():
         # dominant kernel: layer-1 SpMM (agg) of this rank's split
         E1 = np.mean([samples[i].sizes()[1][0] for i in range(args.warmup, n_steps)]) / g
         R1 = np.mean([samples[i].sizes()[0][1] for i in range(args.warmup, n_steps)]) / g
-        alg = sage_fwd_bytes(E1, R1, FEAT)
+        alg = sage_fused_fwd_bytes(E1, R1, FEAT, HIDDEN) if g == 1 else sage_fwd_bytes(E1, R1, FEAT)
         agg_avg = float(np.mean(agg_ms))
         achieved = alg / (agg_avg / 1e3) / 1e9
         traffic = None
@@ -423,7 +430,8 @@ def main():
                        "epoch_time_s": iters_per_epoch * my_ms / args.steps / 1e3,
                        "edges_per_step": edges / args.steps, "graph_gen_s": round(gen_s, 1),
                        "sample_sizes_first": {"V": nV, "E": nE}},
-            "roofline": {"bound": "hbm", "kernel": "k_sage_agg<4,32,1> layer 1 (F=100)",
+            "roofline": {"bound": "hbm", "kernel": ("k_sage_fused<32,1,16> layer 1 (SpMM + update, F=100)" if g == 1
+                                                    else "k_sage_agg<4,32,1,1> layer 1 (F=100)"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg, "avg_launch_ms": agg_avg,

@@ -30,7 +30,7 @@ from paper_2303_13775_b200.sampling import epoch_batches, sample_minibatch
 from paper_2303_13775_b200.scheduler import DeviceSplit, split_minibatch
 
 DEBUG_CHECK_FINITE = False
-NB_PARTIAL = 6 * 148  # max blocks of the deterministic partial reductions
+NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions
 
 
 def _nblocks(rows, tile=32):
@@ -171,6 +171,7 @@ class SplitStep:
         with self.phase("layer0"):
             self.layer0()
         dperm = self._dst_perm()
+        self._launch_src_csr_async(2)
         self.h[0] = self.f.table
         for l in range(1, self.L + 1):
             w, dout = p.layer_dims(l - 1)
@@ -254,6 +255,32 @@ class SplitStep:
             acc += ds.nV[l - 1]
         return out, kb
 
+    def _launch_src_csr_async(self, lmin):
+        """The CSR-by-source build depends only on the split: run it on a side
+        stream so it overlaps the forward pass (also inside a captured graph)."""
+        self._csr_async = None
+        if self.L < lmin or self.events is not None and self.ev_mode == "all":
+            return  # phase-profiling runs keep it serial so its time is visible
+        main = torch.cuda.current_stream()
+        side = getattr(self, "_side", None)
+        if side is None:
+            side = torch.cuda.Stream(device=self.dev)
+            self._side = side
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            out = self._src_csr(lmin, val_mode=1 if self.kind == "graphsage" else 0)
+        self._csr_async = (lmin, out, side)
+
+    def _join_src_csr(self, lmin):
+        pending = getattr(self, "_csr_async", None)
+        if pending is not None and pending[0] == lmin:
+            torch.cuda.current_stream().wait_stream(pending[2])
+            self._csr_async = None
+            return pending[1]
+        if self.L < lmin:
+            return {}, {}
+        return self._src_csr(lmin, val_mode=1 if self.kind == "graphsage" else 0)
+
     def loss(self):
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
         L = self.L
@@ -283,8 +310,8 @@ class SplitStep:
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
         with self.phase("loss"):
             self.loss()
-        with self.phase("src_csr"):
-            csr, kb = self._src_csr(2) if self.L >= 2 else ({}, {})
+        with self.phase("src_csr_join"):
+            csr, kb = self._join_src_csr(2)
         d_h = self.d_h
         for l in range(self.L, 0, -1):
             w, dout = p.layer_dims(l - 1)

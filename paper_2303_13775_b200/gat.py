@@ -45,6 +45,7 @@ def gat_forward(step):
     slope = float(p.leaky_slope)
     step.layer0()
     dperm = step._dst_perm()
+    step._launch_src_csr_async(1)
     dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
     nEtot = int(ds.lay.nEtot)
     step.h[0] = step.f.table
@@ -103,7 +104,7 @@ def gat_backward(step):
     dperm = step._dst_perm()
     dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
     nEtot = int(ds.lay.nEtot)
-    csr, kb = step._src_csr(1, val_mode=0)
+    csr, kb = step._join_src_csr(1)
     d_h = step.d_h
     from paper_2303_13775_b200.engine import _nblocks
     for l in range(step.L, 0, -1):
