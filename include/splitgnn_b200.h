@@ -197,12 +197,15 @@ int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
 /* Owner combine + update (engine.py:197-226): adds the holders' partial
  * (sum,count) rows from recvbuf in ascending sender order, mean = S/N,
  * pre = h_self@W_self + mean@W_neigh + b, h = relu(pre) unless final.
- * Writes mean (n_own x w), counts (combined), h (n_own x dout). */
+ * Writes mean (n_own x w), counts (combined), h (n_own x dout); with hs_out
+ * (nullable) it also writes the compact self rows and runs the dense part as
+ * the register-tiled FP32 GEMM k_sage_linear. */
 int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                    const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
                    const float* sums, float* counts, const float* recvbuf, int32_t recv_stride,
                    const float* w_self, const float* w_neigh, const float* bias,
-                   int32_t final_layer, float* mean, float* h, int64_t max_rows, void* stream);
+                   int32_t final_layer, float* mean, float* h, float* hs_out, int64_t max_rows,
+                   void* stream);
 /* Backward row pass (engine.py:228-254): d_pre = d_h*[h>0] (or d_h if final);
  * per-block partial sums of h_self^T d_pre, mean^T d_pre and sum(d_pre)
  * (reduced later by sg_reduce_partials, deterministic order); optionally

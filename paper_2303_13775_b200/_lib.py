@@ -85,7 +85,7 @@ _SIGS = {
     "sg_sage_fused_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32, vp, vp,
                                 vp, vp, i64, vp]),
     "sg_sage_update": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32,
-                             vp, vp, vp, i32, vp, vp, i64, vp]),
+                             vp, vp, vp, i32, vp, vp, vp, i64, vp]),
     "sg_sage_bwd_rows": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, i32, vp,
                                vp, vp, vp, vp, i32, vp, vp, i32, i64, vp]),
     "sg_sage_scatter_bwd": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, vp, i32, vp, vp,

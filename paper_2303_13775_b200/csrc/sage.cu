@@ -227,21 +227,11 @@ struct FusedArgs {
   float* h;
 };
 
-template <int LPR, int EG, int DO>
-__global__ void __launch_bounds__(256) k_sage_fused(const SgMeta* __restrict__ meta, FusedArgs a) {
-  extern __shared__ __align__(16) float smem[];
+template <int LPR, int EG>
+__global__ void __launch_bounds__(256) k_sage_agg_mean(const SgMeta* __restrict__ meta, FusedArgs a) {
   constexpr int RL = LPR * EG;
   constexpr int RPW = 32 / RL;
-  const int w = a.w, dout = a.dout;
-  float* wsT = smem;            // [DO][w]
-  float* wnT = wsT + DO * w;    // [DO][w]
-  for (int i = threadIdx.x; i < w * DO; i += blockDim.x) {
-    const int c = i / DO, j = i - c * DO;
-    const bool ok = j < dout;
-    wsT[j * w + c] = ok ? a.ws[c * dout + j] : 0.f;
-    wnT[j * w + c] = ok ? a.wn[c * dout + j] : 0.f;
-  }
-  __syncthreads();
+  const int w = a.w;
   const int l = a.l, d = a.d;
   const int n_own = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];
@@ -269,24 +259,25 @@ __global__ void __launch_bounds__(256) k_sage_fused(const SgMeta* __restrict__ m
       }
       const int cnt = min(RL, e - jb);
       const int rounds = (cnt + EG - 1) / EG;
+      constexpr int UN = EG == 1 ? 8 : 4;  // loads in flight per lane
       int kk = 0;
-      for (; kk + 4 <= rounds; kk += 4) {
-        int rr[4];
-        bool ok[4];
+      for (; kk + UN <= rounds; kk += UN) {
+        int rr[UN];
+        bool ok[UN];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < UN; ++u) {
           const int k = (kk + u) * EG + eg;
           rr[u] = __shfl_sync(tmask, r, k < RL ? k : RL - 1, RL);
           ok[u] = k < cnt;
         }
         if (colok) {
-          float4 v[4];
+          float4 v[UN];
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < UN; ++u)
             v[u] = ok[u] ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr[u] * w + col))
                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < UN; ++u) {
             acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
           }
         }
@@ -317,73 +308,135 @@ __global__ void __launch_bounds__(256) k_sage_fused(const SgMeta* __restrict__ m
       *reinterpret_cast<float4*>(a.hs + G * w + col) = hv;
     }
     if (tl == 0) a.counts[G] = cntf;
-    // partial dot products over this lane's 4 columns for every output
-    float p[DO];
+  }
+}
+
+template <int LPR, int EG>
+int launch_agg_mean(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
+  constexpr int RPB = 8 * (32 / (LPR * EG));
+  const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
+  k_sage_agg_mean<LPR, EG><<<grid, 256, 0, st>>>(meta, a);
+  SG_CHECK_LAUNCH("k_sage_agg_mean");
+  return SG_OK;
+}
+
+// ---------------------------------------------------------------- tiled dense transforms
+// h = act(hs @ W_self + mean @ W_neigh + b) for the owned rows: a register-
+// tiled FP32 GEMM ([rows x 2w] @ [2w x dout]). K is staged in chunks of 32,
+// transposed in smem so each thread reads its RPT consecutive rows with one
+// vector load; each thread owns RPT rows x 4 outputs (RPT*4 FFMA per 2 loads).
+struct LinArgs {
+  int l, d, w, dout, final_;
+  const float* hs;
+  const float* mean;
+  const float* ws;
+  const float* wn;
+  const float* bias;
+  float* h;
+};
+
+template <int NQ>
+__global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ meta, LinArgs a) {
+  constexpr int RG = 256 / NQ;
+  constexpr int TM = RG >= 128 ? RG : 128;
+  constexpr int RPT = TM / RG;
+  constexpr int KC = 32;
+  constexpr int TMP = TM + 4;
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, dout = a.dout, K = 2 * w;
+  float* W_s = smem;             // [2w][dout]: W_self rows then W_neigh rows
+  float* A_s = W_s + K * dout;   // [KC][TM+4] transposed chunk
+  for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
+    W_s[i] = a.ws[i];
+    W_s[w * dout + i] = a.wn[i];
+  }
+  const int n = meta->n_own[a.l][a.d];
+  const int own0 = meta->own_off[a.l][a.d];
+  const int jg = threadIdx.x % NQ, rg = threadIdx.x / NQ;
+  const float4 b4 = *reinterpret_cast<const float4*>(a.bias + 4 * jg);
+  for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
+    float acc[RPT][4];
 #pragma unroll
-    for (int j = 0; j < DO; ++j) {
-      float t = 0.f;
-      if (colok) {
-        const float4 s4 = *reinterpret_cast<const float4*>(wsT + j * w + col);
-        const float4 n4 = *reinterpret_cast<const float4*>(wnT + j * w + col);
-        t = fmaf(hv.x, s4.x, fmaf(hv.y, s4.y, fmaf(hv.z, s4.z, hv.w * s4.w)));
-        t = fmaf(mn.x, n4.x, fmaf(mn.y, n4.y, fmaf(mn.z, n4.z, fmaf(mn.w, n4.w, t))));
-      }
-      p[j] = t;
-    }
-    // recursive halving over the LPR lanes of group eg (all groups hold the same sums)
-    int n = DO, base = 0;
-#pragma unroll
-    for (int o = LPR >> 1; o >= 1; o >>= 1) {
-      if (n > 1) {
-        const int half = n >> 1;
-        const bool up = (lr & o) != 0;
-#pragma unroll
-        for (int k = 0; k < DO / 2; ++k) {
-          if (k < half) {
-            const float send = up ? p[k] : p[k + half];
-            const float keep = up ? p[k + half] : p[k];
-            p[k] = keep + __shfl_xor_sync(tmask, send, o, RL);
-          }
+    for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    for (int k0 = 0; k0 < K; k0 += KC) {
+      __syncthreads();
+      for (int idx = threadIdx.x; idx < TM * (KC / 4); idx += 256) {
+        const int r = idx / (KC / 4), q = idx - r * (KC / 4);
+        const int k = k0 + 4 * q;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r0 + r < n && k < K) {
+          const float* src = k < w ? a.hs + (int64_t)(own0 + r0 + r) * w + k
+                                   : a.mean + (int64_t)(own0 + r0 + r) * w + (k - w);
+          v = *reinterpret_cast<const float4*>(src);
         }
-        if (up) base += half;
-        n = half;
-      } else {
-        p[0] += __shfl_xor_sync(tmask, p[0], o, RL);
+        A_s[(4 * q + 0) * TMP + r] = v.x;
+        A_s[(4 * q + 1) * TMP + r] = v.y;
+        A_s[(4 * q + 2) * TMP + r] = v.z;
+        A_s[(4 * q + 3) * TMP + r] = v.w;
+      }
+      __syncthreads();
+      const int kmax = min(KC, K - k0);
+#pragma unroll 8
+      for (int kk = 0; kk < kmax; ++kk) {
+        const float4 w4 = *reinterpret_cast<const float4*>(W_s + (k0 + kk) * dout + 4 * jg);
+        float av[RPT];
+        if constexpr (RPT == 4) {
+          const float4 t = *reinterpret_cast<const float4*>(A_s + kk * TMP + rg * RPT);
+          av[0] = t.x; av[1] = t.y; av[2] = t.z; av[3] = t.w;
+        } else if constexpr (RPT == 2) {
+          const float2 t = *reinterpret_cast<const float2*>(A_s + kk * TMP + rg * RPT);
+          av[0] = t.x; av[1] = t.y;
+        } else {
+          av[0] = A_s[kk * TMP + rg * RPT];
+        }
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+          acc[i][0] = fmaf(av[i], w4.x, acc[i][0]);
+          acc[i][1] = fmaf(av[i], w4.y, acc[i][1]);
+          acc[i][2] = fmaf(av[i], w4.z, acc[i][2]);
+          acc[i][3] = fmaf(av[i], w4.w, acc[i][3]);
+        }
       }
     }
-    if (eg == 0) {
-      // lanes with identical 'base' hold the same outputs; the lowest writes
-      const int dup = LPR / (DO < LPR ? DO : LPR);  // lanes per output group
-      if ((lr % dup) == 0) {
 #pragma unroll
-        for (int k = 0; k < DO; ++k) {
-          if (k < n) {
-            const int j = base + k;
-            if (j < dout) {
-              const float v = p[k] + a.bias[j];
-              a.h[G * dout + j] = a.final_ ? v : fmaxf(v, 0.f);
-            }
-          }
+    for (int i = 0; i < RPT; ++i) {
+      const int r = r0 + rg * RPT + i;
+      if (r < n) {
+        float4 o = make_float4(acc[i][0] + b4.x, acc[i][1] + b4.y, acc[i][2] + b4.z, acc[i][3] + b4.w);
+        if (!a.final_) {
+          o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
         }
+        *reinterpret_cast<float4*>(a.h + (int64_t)(own0 + r) * dout + 4 * jg) = o;
       }
     }
   }
 }
 
-template <int LPR, int EG, int DO>
-int launch_fused(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
-  constexpr int RPB = 8 * (32 / (LPR * EG));
-  const size_t smem = sizeof(float) * 2 * (size_t)DO * a.w;
+template <int NQ>
+int launch_linear_q(const SgMeta* meta, const LinArgs& a, int64_t max_rows, cudaStream_t st) {
+  constexpr int RG = 256 / NQ;
+  constexpr int TM = RG >= 128 ? RG : 128;
+  const size_t smem = sizeof(float) * (2 * (size_t)a.w * a.dout + 32 * (size_t)(TM + 4));
   if (smem > 227 * 1024) {
-    set_error("sage_fused_fwd: width too large");
+    set_error("sage_linear: width too large");
     return SG_ERR_ARG;
   }
-  const cudaError_t attr = allow_max_smem<k_sage_fused<LPR, EG, DO>>();
+  const cudaError_t attr = allow_max_smem<k_sage_linear<NQ>>();
   SG_CUDA(attr);
-  const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
-  k_sage_fused<LPR, EG, DO><<<grid, 256, smem, st>>>(meta, a);
-  SG_CHECK_LAUNCH("k_sage_fused");
+  const int grid = clamp_grid(div_up(max_rows, TM), kSMs * 4);
+  k_sage_linear<NQ><<<grid, 256, smem, st>>>(meta, a);
+  SG_CHECK_LAUNCH("k_sage_linear");
   return SG_OK;
+}
+
+int launch_linear(const SgMeta* meta, const LinArgs& a, int64_t max_rows, cudaStream_t st) {
+  switch (a.dout / 4) {
+    case 1: return launch_linear_q<1>(meta, a, max_rows, st);
+    case 2: return launch_linear_q<2>(meta, a, max_rows, st);
+    case 4: return launch_linear_q<4>(meta, a, max_rows, st);
+    case 8: return launch_linear_q<8>(meta, a, max_rows, st);
+    default: set_error("sage_linear: dout must be 4, 8, 16 or 32"); return SG_ERR_ARG;
+  }
 }
 
 // dispatch on width: VEC=4 needs w%4==0 (16B aligned rows)
@@ -424,6 +477,7 @@ struct UpdArgs {
   const float* bias;
   float* mean;
   float* h;
+  float* hs_out;  // when set: write the self rows and leave the GEMM to k_sage_linear
 };
 
 template <bool Q4>
@@ -483,10 +537,13 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
         const float mv = S * n_s[rr];
         mn_s[rr * wp + c] = mv;
         a.mean[G * w + c] = mv;
-        hs_s[rr * wp + c] = __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c);
+        const float hv = __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c);
+        hs_s[rr * wp + c] = hv;
+        if (a.hs_out) a.hs_out[G * w + c] = hv;
       }
     }
     __syncthreads();
+    if (a.hs_out) continue;  // dense transform done by k_sage_linear
     if (Q4) {
       const int nq = dout >> 2;
       for (int idx = threadIdx.x; idx < UTR * nq; idx += blockDim.x) {
@@ -738,6 +795,123 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
   if (threadIdx.x < dout) out[2 * nwd + threadIdx.x] = ab;
 }
 
+// Tiled weight gradients (self-compact forward): dW_self = hs^T d_pre,
+// dW_neigh = mean^T d_pre over this block's rows, each thread a 4x4 register
+// tile (2 LDS.128 per 16 FFMA), per-block partial in the parameter layout.
+template <int NQ>
+__global__ void __launch_bounds__(256) k_sage_wgrad(const SgMeta* __restrict__ meta, BwdArgs a) {
+  constexpr int TR = 32;
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, dout = a.dout, K = 2 * w, KP = K + 4, wst = dout + 4;
+  const bool need_c = a.d_self != nullptr || a.d_sums != nullptr;
+  float* A_s = smem;                  // [TR][2w+4]  hs | mean
+  float* dp_s = A_s + TR * KP;        // [TR][dout]
+  float* cnt_s = dp_s + TR * dout;    // [TR]
+  float* ws_s = cnt_s + TR;           // [w][dout+4] (need_c)
+  float* wn_s = ws_s + w * wst;
+  if (need_c)
+    for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
+      const int c = i / dout, j = i - c * dout;
+      ws_s[c * wst + j] = a.ws[i];
+      wn_s[c * wst + j] = a.wn[i];
+    }
+  const int n = meta->n_own[a.l][a.d];
+  const int own0 = meta->own_off[a.l][a.d];
+  const int ncg = K / 4, nslots = ncg * NQ;
+  float acc[2][4][4];
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[s2][i][0] = acc[s2][i][1] = acc[s2][i][2] = acc[s2][i][3] = 0.f;
+  float ab = 0.f;
+  const int ntiles = (n + TR - 1) / TR;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();
+    const int r0 = tile * TR;
+    for (int idx = threadIdx.x; idx < TR * ncg; idx += blockDim.x) {
+      const int r = idx / ncg, q = idx - r * ncg;
+      const int k = 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r0 + r < n) {
+        const int64_t G = own0 + r0 + r;
+        v = k < w ? *reinterpret_cast<const float4*>(a.h_prev + G * w + k)
+                  : *reinterpret_cast<const float4*>(a.mean + G * w + (k - w));
+      }
+      *reinterpret_cast<float4*>(A_s + r * KP + k) = v;
+    }
+    for (int idx = threadIdx.x; idx < TR * dout; idx += blockDim.x) {
+      const int r = idx / dout, j = idx - r * dout;
+      float v = 0.f;
+      if (r0 + r < n) {
+        const int64_t G = own0 + r0 + r;
+        v = a.d_h[G * dout + j];
+        if (!a.final_ && !(a.h[G * dout + j] > 0.f)) v = 0.f;
+      }
+      dp_s[idx] = v;
+    }
+    if (threadIdx.x < TR) {
+      const int r = threadIdx.x;
+      cnt_s[r] = (r0 + r < n) ? 1.0f / a.counts[own0 + r0 + r] : 1.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int slot = threadIdx.x + 256 * s2;
+      if (slot < nslots) {
+        const int cg = slot / NQ, jg = slot - cg * NQ;
+#pragma unroll 4
+        for (int r = 0; r < TR; ++r) {
+          const float4 a4 = *reinterpret_cast<const float4*>(A_s + r * KP + 4 * cg);
+          const float4 g4 = *reinterpret_cast<const float4*>(dp_s + r * dout + 4 * jg);
+          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            acc[s2][i][0] = fmaf(av[i], g4.x, acc[s2][i][0]);
+            acc[s2][i][1] = fmaf(av[i], g4.y, acc[s2][i][1]);
+            acc[s2][i][2] = fmaf(av[i], g4.z, acc[s2][i][2]);
+            acc[s2][i][3] = fmaf(av[i], g4.w, acc[s2][i][3]);
+          }
+        }
+      }
+    }
+    if (threadIdx.x < dout)
+      for (int r = 0; r < TR; ++r) ab += dp_s[r * dout + threadIdx.x];
+    if (need_c) {
+      const int nrow = min(TR, n - r0);
+      for (int idx = threadIdx.x; idx < nrow * w; idx += blockDim.x) {
+        const int r = idx / w, c = idx - r * w;
+        const int64_t G = own0 + r0 + r;
+        float s1 = 0.f, s2v = 0.f;
+        for (int jq = 0; jq < NQ; ++jq) {
+          const float4 g4 = *reinterpret_cast<const float4*>(dp_s + r * dout + 4 * jq);
+          const float4 w1 = *reinterpret_cast<const float4*>(ws_s + c * wst + 4 * jq);
+          const float4 w2 = *reinterpret_cast<const float4*>(wn_s + c * wst + 4 * jq);
+          s1 = fmaf(g4.x, w1.x, fmaf(g4.y, w1.y, fmaf(g4.z, w1.z, fmaf(g4.w, w1.w, s1))));
+          s2v = fmaf(g4.x, w2.x, fmaf(g4.y, w2.y, fmaf(g4.z, w2.z, fmaf(g4.w, w2.w, s2v))));
+        }
+        if (a.d_self) a.d_self[G * w + c] = s1;
+        if (a.d_sums) a.d_sums[G * w + c] = s2v * cnt_s[r];
+      }
+    }
+  }
+  const int nwd = w * dout;
+  float* out = a.partial + (int64_t)blockIdx.x * (2 * (int64_t)nwd + dout);
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2) {
+    const int slot = threadIdx.x + 256 * s2;
+    if (slot < nslots) {
+      const int cg = slot / NQ, jg = slot - cg * NQ;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = 4 * cg + i;
+        float* o = (c < w ? out + c * dout : out + nwd + (c - w) * dout) + 4 * jg;
+        *reinterpret_cast<float4*>(o) = make_float4(acc[s2][i][0], acc[s2][i][1], acc[s2][i][2], acc[s2][i][3]);
+      }
+    }
+  }
+  if (threadIdx.x < dout) out[2 * nwd + threadIdx.x] = ab;
+}
+
 // ---------------------------------------------------------------- scatter (transpose SpMM)
 struct ScatArgs {
   int l, d, w, stride;
@@ -918,8 +1092,8 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   SPLIT_PTRS
   SG_REQUIRE(y.g == 1, "sage_fused_fwd: single-device split only (no remote contributions)");
   SG_REQUIRE(l >= 1 && l <= y.L && d == 0, "sage_fused_fwd: bad layer/device");
-  SG_REQUIRE(w % 4 == 0 && w <= 128 && dout >= 1 && dout <= 32,
-             "sage_fused_fwd: needs w % 4 == 0, w <= 128, dout <= 32");
+  SG_REQUIRE(w % 4 == 0 && w <= 128 && (dout == 4 || dout == 8 || dout == 16 || dout == 32),
+             "sage_fused_fwd: needs w % 4 == 0, w <= 128, dout in {4, 8, 16, 32}");
   if (max_rows <= 0) return SG_OK;
   FusedArgs a;
   memset(&a, 0, sizeof(a));
@@ -927,28 +1101,16 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.voff_l = y.voff[l];
   a.rowbeg = I32(y.o_rowbeg); a.rowend = I32(y.o_rowend); a.lsrc = I32(y.o_lsrc);
   a.selfrow = I32(y.o_selfrow); a.src_row = src_row; a.h_prev = h_prev;
-  a.ws = w_self; a.wn = w_neigh; a.bias = bias;
-  a.mean = mean; a.counts = counts; a.hs = hs; a.h = h;
+  a.mean = mean; a.counts = counts; a.hs = hs;
   cudaStream_t st = (cudaStream_t)stream;
-  const int DOp = dout <= 8 ? 8 : (dout <= 16 ? 16 : 32);
-  if (w <= 16) {
-    if (DOp == 8) return launch_fused<4, 4, 8>(meta, a, max_rows, st);
-    if (DOp == 16) return launch_fused<4, 4, 16>(meta, a, max_rows, st);
-    return launch_fused<4, 4, 32>(meta, a, max_rows, st);
-  }
-  if (w <= 32) {
-    if (DOp == 8) return launch_fused<8, 4, 8>(meta, a, max_rows, st);
-    if (DOp == 16) return launch_fused<8, 4, 16>(meta, a, max_rows, st);
-    return launch_fused<8, 4, 32>(meta, a, max_rows, st);
-  }
-  if (w <= 64) {
-    if (DOp == 8) return launch_fused<16, 2, 8>(meta, a, max_rows, st);
-    if (DOp == 16) return launch_fused<16, 2, 16>(meta, a, max_rows, st);
-    return launch_fused<16, 2, 32>(meta, a, max_rows, st);
-  }
-  if (DOp == 8) return launch_fused<32, 1, 8>(meta, a, max_rows, st);
-  if (DOp == 16) return launch_fused<32, 1, 16>(meta, a, max_rows, st);
-  return launch_fused<32, 1, 32>(meta, a, max_rows, st);
+  int rc;
+  if (w <= 16) rc = launch_agg_mean<4, 4>(meta, a, max_rows, st);
+  else if (w <= 32) rc = launch_agg_mean<8, 4>(meta, a, max_rows, st);
+  else if (w <= 64) rc = launch_agg_mean<16, 2>(meta, a, max_rows, st);
+  else rc = launch_agg_mean<32, 1>(meta, a, max_rows, st);
+  if (rc) return rc;
+  LinArgs la{l, d, w, dout, final_layer, hs, mean, w_self, w_neigh, bias, h};
+  return launch_linear(meta, la, max_rows, st);
 }
 
 extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l,
@@ -956,7 +1118,8 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
                               int32_t dout, const float* sums, float* counts,
                               const float* recvbuf, int32_t recv_stride, const float* w_self,
                               const float* w_neigh, const float* bias, int32_t final_layer,
-                              float* mean, float* h, int64_t max_rows, void* stream) {
+                              float* mean, float* h, float* hs_out, int64_t max_rows,
+                              void* stream) {
   SG_REQUIRE(split_ws && lay, "sage_update: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_update: bad layer/device");
@@ -985,6 +1148,9 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
   a.bias = bias;
   a.mean = mean;
   a.h = h;
+  const bool tiled = hs_out != nullptr && w % 4 == 0 &&
+                     (dout == 4 || dout == 8 || dout == 16 || dout == 32);
+  a.hs_out = tiled ? hs_out : nullptr;
   const size_t smem = sizeof(float) * (2 * (size_t)w * dout + 2 * (size_t)UTR * (w + 1) +
                                        (size_t)UTR * (2 + y.g));
   SG_REQUIRE(smem <= 227 * 1024, "sage_update: width too large for shared memory");
@@ -998,6 +1164,10 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
     k_sage_update<false><<<grid, 256, smem, st>>>(meta, a);
   }
   SG_CHECK_LAUNCH("k_sage_update");
+  if (tiled) {
+    LinArgs la{l, d, w, dout, final_layer, hs_out, mean, w_self, w_neigh, bias, h};
+    return launch_linear(meta, la, max_rows, st);
+  }
   return SG_OK;
 }
 
@@ -1038,6 +1208,21 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   a.partial = partial;
   a.d_self = d_self;
   a.d_sums = d_sums;
+  if (self_compact && q4 && w % 4 == 0 && dout <= 32 && 2 * w * (dout / 4) <= 4 * 512) {
+    const size_t sm2 = sizeof(float) * (32 * (size_t)(2 * w + 4) + 32 * (size_t)dout + 32 +
+                                        2 * (size_t)w * (dout + 4));
+    SG_REQUIRE(sm2 <= 227 * 1024, "sage_wgrad: width too large for shared memory");
+    cudaStream_t st2 = (cudaStream_t)stream;
+    cudaError_t attr = cudaSuccess;
+    switch (dout / 4) {
+      case 1: attr = allow_max_smem<k_sage_wgrad<1>>(); SG_CUDA(attr); k_sage_wgrad<1><<<nblocks, 256, sm2, st2>>>(meta, a); break;
+      case 2: attr = allow_max_smem<k_sage_wgrad<2>>(); SG_CUDA(attr); k_sage_wgrad<2><<<nblocks, 256, sm2, st2>>>(meta, a); break;
+      case 4: attr = allow_max_smem<k_sage_wgrad<4>>(); SG_CUDA(attr); k_sage_wgrad<4><<<nblocks, 256, sm2, st2>>>(meta, a); break;
+      default: attr = allow_max_smem<k_sage_wgrad<8>>(); SG_CUDA(attr); k_sage_wgrad<8><<<nblocks, 256, sm2, st2>>>(meta, a); break;
+    }
+    SG_CHECK_LAUNCH("k_sage_wgrad");
+    return SG_OK;
+  }
   const int wst = q4 ? dout + 4 : dout + 1;
   const size_t smem = sizeof(float) * ((size_t)BTR * dout + 2 * (size_t)w * wst +
                                        2 * (size_t)BTR * (w + 1) + 2 * BTR);

@@ -115,7 +115,7 @@ class SplitStep:
 
     def _fused_ok(self, w, dout, dperm):
         """Single-device split: the update can run inside the aggregation."""
-        return (self.g == 1 and dperm is None and w % 4 == 0 and w <= 128 and 1 <= dout <= 32
+        return (self.g == 1 and dperm is None and w % 4 == 0 and w <= 128 and dout in (4, 8, 16, 32)
                 and not getattr(self, "no_fuse", False))
 
     def _dst_perm(self):
@@ -220,16 +220,20 @@ class SplitStep:
                     self.wire_bytes += int(self.meta.npairs[l]) * SW * 4
             mean = _f32(nV, w, device=self.dev)
             h = _f32(nV, dout, device=self.dev)
+            tiled = w % 4 == 0 and dout in (4, 8, 16, 32)
+            hs = _f32(nV, w, device=self.dev) if tiled else None
             self._ev(f"ph:update{l}:s")
             for d in self.devices:
                 _lib.call("sg_sage_update", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
                           _lib.ptr(src_row), w, dout, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(recv),
                           SW, _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
                           _lib.ptr(p.view(f"layer{l-1}.bias")), final, _lib.ptr(mean), _lib.ptr(h),
-                          self.n_own(l, d), st)
+                          _lib.ptr(hs), self.n_own(l, d), st)
             self._ev(f"ph:update{l}:e")
             self.h[l] = h
             self.keep[l] = dict(mean=mean, counts=counts)
+            if hs is not None:
+                self.keep[l]["hs"] = hs
             if DEBUG_CHECK_FINITE and not torch.isfinite(h[:nV]).all():
                 raise FloatingPointError(f"non-finite values in graphsage layer {l} output")
 
