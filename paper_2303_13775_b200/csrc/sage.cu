@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(256) k_sage_agg_mean(const SgMeta* __restrict_
       }
       const int cnt = min(RL, e - jb);
       const int rounds = (cnt + EG - 1) / EG;
-      constexpr int UN = EG == 1 ? 8 : 4;  // loads in flight per lane
+      constexpr int UN = 4;  // loads in flight per lane
       int kk = 0;
       for (; kk + UN <= rounds; kk += UN) {
         int rr[UN];
@@ -335,95 +335,94 @@ struct LinArgs {
   float* h;
 };
 
+// 64-row tiles; the whole K = 2w slice of the tile is staged once (all loads
+// in flight), K is split over NS thread slices, each thread owns a 4-row x
+// 4-output register tile (2 LDS.128 per 16 FFMA), slices are added in a fixed
+// order through shared memory (deterministic).
 template <int NQ>
 __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ meta, LinArgs a) {
-  constexpr int RG = 256 / NQ;
-  constexpr int TM = RG >= 128 ? RG : 128;
-  constexpr int RPT = TM / RG;
-  constexpr int KC = 32;
+  constexpr int TM = 64;
   constexpr int TMP = TM + 4;
+  constexpr int NT = (TM / 4) * NQ;  // register tiles per K slice
+  constexpr int NS = 256 / NT;       // K slices
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, K = 2 * w;
-  float* W_s = smem;             // [2w][dout]: W_self rows then W_neigh rows
-  float* A_s = W_s + K * dout;   // [KC][TM+4] transposed chunk
+  float* W_s = smem;                 // [2w][dout]
+  float* A_s = W_s + K * dout;       // [2w][TM+4] transposed
+  float* red = A_s + K * TMP;        // [NS][TM][dout]
   for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
     W_s[i] = a.ws[i];
     W_s[w * dout + i] = a.wn[i];
   }
   const int n = meta->n_own[a.l][a.d];
   const int own0 = meta->own_off[a.l][a.d];
-  const int jg = threadIdx.x % NQ, rg = threadIdx.x / NQ;
-  const float4 b4 = *reinterpret_cast<const float4*>(a.bias + 4 * jg);
+  const int tile = threadIdx.x % NT, ks = threadIdx.x / NT;
+  const int rt = tile / NQ, jq = tile - rt * NQ;
+  const int kchunk = (K + NS - 1) / NS;
+  const int kb = ks * kchunk, ke = min(K, kb + kchunk);
+  const int w4 = w / 4;
   for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
-    float acc[RPT][4];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-    for (int k0 = 0; k0 < K; k0 += KC) {
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < TM * (KC / 4); idx += 256) {
-        const int r = idx / (KC / 4), q = idx - r * (KC / 4);
-        const int k = k0 + 4 * q;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r0 + r < n && k < K) {
-          const float* src = k < w ? a.hs + (int64_t)(own0 + r0 + r) * w + k
-                                   : a.mean + (int64_t)(own0 + r0 + r) * w + (k - w);
-          v = *reinterpret_cast<const float4*>(src);
-        }
-        A_s[(4 * q + 0) * TMP + r] = v.x;
-        A_s[(4 * q + 1) * TMP + r] = v.y;
-        A_s[(4 * q + 2) * TMP + r] = v.z;
-        A_s[(4 * q + 3) * TMP + r] = v.w;
+    __syncthreads();
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < TM * 2 * w4; idx += 256) {
+      const int r = idx / (2 * w4), q = idx - r * (2 * w4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r0 + r < n) {
+        const int64_t G = own0 + r0 + r;
+        v = q < w4 ? *reinterpret_cast<const float4*>(a.hs + G * w + 4 * q)
+                   : *reinterpret_cast<const float4*>(a.mean + G * w + 4 * (q - w4));
       }
-      __syncthreads();
-      const int kmax = min(KC, K - k0);
-#pragma unroll 8
-      for (int kk = 0; kk < kmax; ++kk) {
-        const float4 w4 = *reinterpret_cast<const float4*>(W_s + (k0 + kk) * dout + 4 * jg);
-        float av[RPT];
-        if constexpr (RPT == 4) {
-          const float4 t = *reinterpret_cast<const float4*>(A_s + kk * TMP + rg * RPT);
-          av[0] = t.x; av[1] = t.y; av[2] = t.z; av[3] = t.w;
-        } else if constexpr (RPT == 2) {
-          const float2 t = *reinterpret_cast<const float2*>(A_s + kk * TMP + rg * RPT);
-          av[0] = t.x; av[1] = t.y;
-        } else {
-          av[0] = A_s[kk * TMP + rg * RPT];
-        }
+      A_s[(4 * q + 0) * TMP + r] = v.x;
+      A_s[(4 * q + 1) * TMP + r] = v.y;
+      A_s[(4 * q + 2) * TMP + r] = v.z;
+      A_s[(4 * q + 3) * TMP + r] = v.w;
+    }
+    __syncthreads();
+    float acc[4][4];
 #pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-          acc[i][0] = fmaf(av[i], w4.x, acc[i][0]);
-          acc[i][1] = fmaf(av[i], w4.y, acc[i][1]);
-          acc[i][2] = fmaf(av[i], w4.z, acc[i][2]);
-          acc[i][3] = fmaf(av[i], w4.w, acc[i][3]);
-        }
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      const float4 av = *reinterpret_cast<const float4*>(A_s + k * TMP + 4 * rt);
+      const float4 wv = *reinterpret_cast<const float4*>(W_s + k * dout + 4 * jq);
+      const float ar[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] = fmaf(ar[i], wv.x, acc[i][0]);
+        acc[i][1] = fmaf(ar[i], wv.y, acc[i][1]);
+        acc[i][2] = fmaf(ar[i], wv.z, acc[i][2]);
+        acc[i][3] = fmaf(ar[i], wv.w, acc[i][3]);
       }
     }
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int r = r0 + rg * RPT + i;
-      if (r < n) {
-        float4 o = make_float4(acc[i][0] + b4.x, acc[i][1] + b4.y, acc[i][2] + b4.z, acc[i][3] + b4.w);
-        if (!a.final_) {
-          o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f); o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
-        }
-        *reinterpret_cast<float4*>(a.h + (int64_t)(own0 + r) * dout + 4 * jg) = o;
-      }
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<float4*>(red + (ks * TM + 4 * rt + i) * dout + 4 * jq) =
+          make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TM * dout; idx += 256) {
+      const int r = idx / dout, j = idx - r * dout;
+      if (r0 + r >= n) continue;
+      float v = a.bias[j];
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) v += red[(s2 * TM + r) * dout + j];
+      a.h[(int64_t)(own0 + r0 + r) * dout + j] = a.final_ ? v : fmaxf(v, 0.f);
     }
   }
 }
 
 template <int NQ>
 int launch_linear_q(const SgMeta* meta, const LinArgs& a, int64_t max_rows, cudaStream_t st) {
-  constexpr int RG = 256 / NQ;
-  constexpr int TM = RG >= 128 ? RG : 128;
-  const size_t smem = sizeof(float) * (2 * (size_t)a.w * a.dout + 32 * (size_t)(TM + 4));
+  constexpr int TM = 64;
+  constexpr int NS = 256 / ((TM / 4) * NQ);
+  const size_t smem = sizeof(float) * (2 * (size_t)a.w * a.dout + 2 * (size_t)a.w * (TM + 4) +
+                                       (size_t)NS * TM * a.dout);
   if (smem > 227 * 1024) {
     set_error("sage_linear: width too large");
     return SG_ERR_ARG;
   }
   const cudaError_t attr = allow_max_smem<k_sage_linear<NQ>>();
   SG_CUDA(attr);
-  const int grid = clamp_grid(div_up(max_rows, TM), kSMs * 4);
+  const int grid = clamp_grid(div_up(max_rows, TM), kSMs * 8);
   k_sage_linear<NQ><<<grid, 256, smem, st>>>(meta, a);
   SG_CHECK_LAUNCH("k_sage_linear");
   return SG_OK;
