@@ -350,9 +350,23 @@ __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ 
   float* W_s = smem;                 // [2w][dout]
   float* A_s = W_s + K * dout;       // [2w][TM+4] transposed
   float* red = A_s + K * TMP;        // [NS][TM][dout]
-  for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
-    W_s[i] = a.ws[i];
-    W_s[w * dout + i] = a.wn[i];
+  {
+    // all weight loads in flight before any store (w*dout % 4 == 0)
+    constexpr int MW = 8;  // float4 per thread: 2*w*dout/4 <= 2048
+    const int nw4 = w * dout / 4;
+    float4 wb[MW];
+#pragma unroll
+    for (int u = 0; u < MW; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      if (i < 2 * nw4)
+        wb[u] = i < nw4 ? reinterpret_cast<const float4*>(a.ws)[i]
+                        : reinterpret_cast<const float4*>(a.wn)[i - nw4];
+    }
+#pragma unroll
+    for (int u = 0; u < MW; ++u) {
+      const int i = threadIdx.x + 256 * u;
+      if (i < 2 * nw4) reinterpret_cast<float4*>(W_s)[i] = wb[u];
+    }
   }
   const int n = meta->n_own[a.l][a.d];
   const int own0 = meta->own_off[a.l][a.d];
@@ -363,19 +377,35 @@ __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ 
   const int w4 = w / 4;
   for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
     __syncthreads();
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < TM * 2 * w4; idx += 256) {
-      const int r = idx / (2 * w4), q = idx - r * (2 * w4);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r0 + r < n) {
-        const int64_t G = own0 + r0 + r;
-        v = q < w4 ? *reinterpret_cast<const float4*>(a.hs + G * w + 4 * q)
-                   : *reinterpret_cast<const float4*>(a.mean + G * w + 4 * (q - w4));
+    {
+      // issue every load of the tile (<= 16 float4 per thread), then store transposed
+      constexpr int MA = 16;
+      const int tot = TM * 2 * w4;
+      float4 ab[MA];
+#pragma unroll
+      for (int u = 0; u < MA; ++u) {
+        const int idx = threadIdx.x + 256 * u;
+        ab[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (idx < tot) {
+          const int r = idx / (2 * w4), q = idx - r * (2 * w4);
+          if (r0 + r < n) {
+            const int64_t G = own0 + r0 + r;
+            ab[u] = q < w4 ? *reinterpret_cast<const float4*>(a.hs + G * w + 4 * q)
+                           : *reinterpret_cast<const float4*>(a.mean + G * w + 4 * (q - w4));
+          }
+        }
       }
-      A_s[(4 * q + 0) * TMP + r] = v.x;
-      A_s[(4 * q + 1) * TMP + r] = v.y;
-      A_s[(4 * q + 2) * TMP + r] = v.z;
-      A_s[(4 * q + 3) * TMP + r] = v.w;
+#pragma unroll
+      for (int u = 0; u < MA; ++u) {
+        const int idx = threadIdx.x + 256 * u;
+        if (idx < tot) {
+          const int r = idx / (2 * w4), q = idx - r * (2 * w4);
+          A_s[(4 * q + 0) * TMP + r] = ab[u].x;
+          A_s[(4 * q + 1) * TMP + r] = ab[u].y;
+          A_s[(4 * q + 2) * TMP + r] = ab[u].z;
+          A_s[(4 * q + 3) * TMP + r] = ab[u].w;
+        }
+      }
     }
     __syncthreads();
     float acc[4][4];
