@@ -340,8 +340,8 @@ struct LinArgs {
 // 4-output register tile (2 LDS.128 per 16 FFMA), slices are added in a fixed
 // order through shared memory (deterministic).
 template <int NQ>
-__global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ meta, LinArgs a) {
-  constexpr int TM = 64;
+__global__ void __launch_bounds__(256, 3) k_sage_linear(const SgMeta* __restrict__ meta, LinArgs a) {
+  constexpr int TM = 32;
   constexpr int TMP = TM + 4;
   constexpr int NT = (TM / 4) * NQ;  // register tiles per K slice
   constexpr int NS = 256 / NT;       // K slices
@@ -352,20 +352,22 @@ __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ 
   float* red = A_s + K * TMP;        // [NS][TM][dout]
   {
     // all weight loads in flight before any store (w*dout % 4 == 0)
-    constexpr int MW = 8;  // float4 per thread: 2*w*dout/4 <= 2048
+    constexpr int MW = 4;  // float4 per thread per pass: 2*w*dout/4 <= 2048 (two passes)
     const int nw4 = w * dout / 4;
-    float4 wb[MW];
+    for (int pass = 0; pass < 2; ++pass) {
+      float4 wb[MW];
 #pragma unroll
-    for (int u = 0; u < MW; ++u) {
-      const int i = threadIdx.x + 256 * u;
-      if (i < 2 * nw4)
-        wb[u] = i < nw4 ? reinterpret_cast<const float4*>(a.ws)[i]
-                        : reinterpret_cast<const float4*>(a.wn)[i - nw4];
-    }
+      for (int u = 0; u < MW; ++u) {
+        const int i = threadIdx.x + 256 * (u + MW * pass);
+        if (i < 2 * nw4)
+          wb[u] = i < nw4 ? reinterpret_cast<const float4*>(a.ws)[i]
+                          : reinterpret_cast<const float4*>(a.wn)[i - nw4];
+      }
 #pragma unroll
-    for (int u = 0; u < MW; ++u) {
-      const int i = threadIdx.x + 256 * u;
-      if (i < 2 * nw4) reinterpret_cast<float4*>(W_s)[i] = wb[u];
+      for (int u = 0; u < MW; ++u) {
+        const int i = threadIdx.x + 256 * (u + MW * pass);
+        if (i < 2 * nw4) reinterpret_cast<float4*>(W_s)[i] = wb[u];
+      }
     }
   }
   const int n = meta->n_own[a.l][a.d];
@@ -378,8 +380,9 @@ __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ 
   for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
     __syncthreads();
     {
-      // issue every load of the tile (<= 16 float4 per thread), then store transposed
-      constexpr int MA = 16;
+      // issue every load of the tile (<= 8 float4 per thread), then store
+      // transposed; row index fastest: shift/mask indexing, conflict-free stores
+      constexpr int MA = 8;
       const int tot = TM * 2 * w4;
       float4 ab[MA];
 #pragma unroll
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ 
         const int idx = threadIdx.x + 256 * u;
         ab[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (idx < tot) {
-          const int r = idx / (2 * w4), q = idx - r * (2 * w4);
+          const int r = idx & (TM - 1), q = idx / TM;
           if (r0 + r < n) {
             const int64_t G = own0 + r0 + r;
             ab[u] = q < w4 ? *reinterpret_cast<const float4*>(a.hs + G * w + 4 * q)
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ 
       for (int u = 0; u < MA; ++u) {
         const int idx = threadIdx.x + 256 * u;
         if (idx < tot) {
-          const int r = idx / (2 * w4), q = idx - r * (2 * w4);
+          const int r = idx & (TM - 1), q = idx / TM;
           A_s[(4 * q + 0) * TMP + r] = ab[u].x;
           A_s[(4 * q + 1) * TMP + r] = ab[u].y;
           A_s[(4 * q + 2) * TMP + r] = ab[u].z;
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(256) k_sage_linear(const SgMeta* __restrict__ 
 
 template <int NQ>
 int launch_linear_q(const SgMeta* meta, const LinArgs& a, int64_t max_rows, cudaStream_t st) {
-  constexpr int TM = 64;
+  constexpr int TM = 32;
   constexpr int NS = 256 / ((TM / 4) * NQ);
   const size_t smem = sizeof(float) * (2 * (size_t)a.w * a.dout + 2 * (size_t)a.w * (TM + 4) +
                                        (size_t)NS * TM * a.dout);
