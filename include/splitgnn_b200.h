@@ -229,45 +229,50 @@ int sg_sage_scatter_bwd(const void* split_ws, const SgSplitLayout* lay, int32_t 
                         const int32_t* enc, const int32_t* srcbeg, const int32_t* srcend,
                         int64_t key_base, float* d_prev, int64_t max_rows, void* stream);
 
-/* ---------------------------------------------------------------- GAT (one head)
+/* ---------------------------------------------------------------- GAT
  * _gat_forward / _gat_backward (engine.py:280-552), models.py:217-261, with
  * 5 exchange rounds per layer instead of 10 (online-softmax merge + softmax
- * backward identity, see gat.cu). Per-edge arrays are indexed by the split's
- * grouped edge slot (eoff[l-1] + i). */
+ * backward identity, see gat.cu). `heads` H >= 1: dout = D = H * d_head
+ * (H = 1 is the reference layer; H > 1 concatenates H single-head layers).
+ * Per-edge arrays are [edge slot][head] with the split's grouped edge slot
+ * (eoff[l-1] + i); per-row scalars are [row][head]. */
 int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                    const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
-                   const float* W, const float* a_src, const float* a_dst, float* z, float* s,
-                   float* t, int64_t max_rows, void* stream);
+                   int32_t heads, const float* W, const float* a_src, const float* a_dst,
+                   float* z, float* s, float* t, int64_t max_rows, void* stream);
 int sg_gat_agg(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d, int32_t dout,
-               float slope, const float* z, const float* s, const float* t, const float* t_recv,
-               const int32_t* dperm, float* pre_e, float* loc_m, float* loc_s, float* loc_U,
-               float* sendbuf, int32_t send_stride, int64_t max_rows, void* stream);
+               int32_t heads, float slope, const float* z, const float* s, const float* t,
+               const float* t_recv, const int32_t* dperm, float* pre_e, float* loc_m,
+               float* loc_s, float* loc_U, float* sendbuf, int32_t send_stride,
+               int64_t max_rows, void* stream);
 int sg_gat_combine(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                   int32_t dout, const float* loc_m, const float* loc_s, const float* loc_U,
-                   const float* recv, int32_t recv_stride, int32_t final_layer, float* md,
-                   float* num, float* h, int64_t max_rows, void* stream);
-int sg_gat_alpha(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d, float slope,
-                 const float* pre_e, const float* md, const float* md_recv, float* alpha,
-                 int64_t max_edges, void* stream);
+                   int32_t dout, int32_t heads, const float* loc_m, const float* loc_s,
+                   const float* loc_U, const float* recv, int32_t recv_stride,
+                   int32_t final_layer, float* md, float* num, float* h, int64_t max_rows,
+                   void* stream);
+int sg_gat_alpha(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                 int32_t heads, float slope, const float* pre_e, const float* md,
+                 const float* md_recv, float* alpha, int64_t max_edges, void* stream);
 int sg_gat_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                    int32_t dout, const float* d_h, const float* num, int32_t final_layer,
-                    float* dnc, int64_t max_rows, void* stream);
+                    int32_t dout, int32_t heads, const float* d_h, const float* num,
+                    int32_t final_layer, float* dnc, int64_t max_rows, void* stream);
 int sg_gat_bwd_dst(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                   int32_t dout, float slope, const float* z, const float* alpha,
+                   int32_t dout, int32_t heads, float slope, const float* z, const float* alpha,
                    const float* pre_e, const float* dnc, const float* dnc_recv,
                    int32_t recv_stride, const int32_t* dperm, float* d_pre, float* dt_loc,
                    float* sendbuf, int64_t max_rows, void* stream);
 int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                   int32_t dout, const int32_t* perm, const int32_t* srcbeg, const int32_t* srcend,
-                   int64_t key_base, const float* alpha, const float* d_pre, const float* dnc,
-                   const float* dnc_recv, int32_t dnc_stride, const float* dt_loc,
-                   const float* dt_recv, const float* a_src, const float* a_dst, float* d_z,
-                   float* ds, float* dt_tot, int64_t max_rows, void* stream);
+                   int32_t dout, int32_t heads, const int32_t* perm, const int32_t* srcbeg,
+                   const int32_t* srcend, int64_t key_base, const float* alpha, const float* d_pre,
+                   const float* dnc, const float* dnc_recv, int32_t dnc_stride,
+                   const float* dt_loc, const float* dt_recv, const float* a_src,
+                   const float* a_dst, float* d_z, float* ds, float* dt_tot, int64_t max_rows,
+                   void* stream);
 int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                      const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
-                     const float* z, const float* d_z, const float* ds, const float* dt_tot,
-                     const float* W, float* partial, int32_t nblocks, float* d_prev,
-                     int64_t max_rows, void* stream);
+                     int32_t heads, const float* z, const float* d_z, const float* ds,
+                     const float* dt_tot, const float* W, float* partial, int32_t nblocks,
+                     float* d_prev, int64_t max_rows, void* stream);
 
 /* ---------------------------------------------------------------- exchange
  * Pack / transport helpers for the push-to-owner / push-from-owner rounds

@@ -90,20 +90,20 @@ _SIGS = {
                                vp, vp, vp, vp, i32, vp, vp, i32, i64, vp]),
     "sg_sage_scatter_bwd": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, vp, i32, vp, vp,
                                   vp, i64, vp, i64, vp]),
-    "sg_gat_project": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp,
-                             i64, vp]),
-    "sg_gat_agg": (i32, [vp, P(SgSplitLayout), i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                         vp, i32, i64, vp]),
-    "sg_gat_combine": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, vp, vp, i32, i32, vp, vp, vp,
-                             i64, vp]),
-    "sg_gat_alpha": (i32, [vp, P(SgSplitLayout), i32, i32, f32, vp, vp, vp, vp, i64, vp]),
-    "sg_gat_bwd_rows": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, i32, vp, i64, vp]),
-    "sg_gat_bwd_dst": (i32, [vp, P(SgSplitLayout), i32, i32, i32, f32, vp, vp, vp, vp, vp, i32, vp, vp,
-                             vp, vp, i64, vp]),
-    "sg_gat_bwd_src": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, vp, i32,
-                             vp, vp, vp, vp, vp, vp, vp, i64, vp]),
-    "sg_gat_bwd_param": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, vp, vp, vp,
-                               i32, vp, i64, vp]),
+    "sg_gat_project": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
+                             vp, i64, vp]),
+    "sg_gat_agg": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp,
+                         vp, vp, i32, i64, vp]),
+    "sg_gat_combine": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, vp, vp, vp, vp, i32, i32, vp, vp,
+                             vp, i64, vp]),
+    "sg_gat_alpha": (i32, [vp, P(SgSplitLayout), i32, i32, i32, f32, vp, vp, vp, vp, i64, vp]),
+    "sg_gat_bwd_rows": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, vp, vp, i32, vp, i64, vp]),
+    "sg_gat_bwd_dst": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, f32, vp, vp, vp, vp, vp, i32, vp,
+                             vp, vp, vp, i64, vp]),
+    "sg_gat_bwd_src": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, vp,
+                             i32, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
+    "sg_gat_bwd_param": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
+                               vp, i32, vp, i64, vp]),
     "sg_xfer_to_owner": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, vp]),
     "sg_xfer_from_owner": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, vp]),
     "sg_pack_from_owner": (i32, [vp, P(SgSplitLayout), i32, i32, vp, i32, vp, i32, i64, vp]),

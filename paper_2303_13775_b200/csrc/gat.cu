@@ -1,36 +1,26 @@
-// GAT (single head; multi-head = heads stacked by the host) forward/backward for
-// one device of a split — replaces _gat_forward / _gat_backward
-// (engine.py:280-552) and the layer math of models.py:217-261.
+// GAT forward/backward for one device of a split — replaces _gat_forward /
+// _gat_backward (engine.py:280-552) and the layer math of models.py:217-261.
+// H heads are computed together (H = 1 is the reference's single-head layer;
+// H > 1 is the concatenation of H single-head layers on the same input,
+// SURVEY §8(a) row 11): z = h W with W = [W_1 | ... | W_H], per-head scores,
+// per-head softmax, outputs concatenated, input gradients summed.
 //
 // The reference runs 10 barrier exchange rounds per layer (test_engine.py:
 // 376-384). Here they are 5, with identical mathematics:
-//   forward   from_owner t (w 1)            t_v = z_v.a_dst for reference dsts
-//             to_owner (U, m, s) (w d+2)     ONLINE-SOFTMAX partials: local max
-//                                            m, s = sum e^(e-m), U = sum e^(e-m) z_u;
-//                                            the owner merges with rescaling
-//             from_owner (m, den) (w 2)      global stabiliser + denominator, so
-//                                            every holder materialises alpha
-//   backward  from_owner (d_num, c) (w d+1)  c_v = d_num_v . num_v; the softmax
-//                                            backward identity
-//                                            d_e = alpha_e (d_num_v.z_u - c_v)
-//                                            replaces the dd to/from rounds
-//             to_owner dt (w 1)
+//   forward   from_owner t (w H)              t_v = z_v.a_dst per head
+//             to_owner (U, m, s) (w D+2H)      ONLINE-SOFTMAX partials: local max
+//                                              m, s = sum e^(e-m), U = sum e^(e-m) z_u;
+//                                              the owner merges with rescaling
+//             from_owner (m, den) (w 2H)       global stabiliser + denominator, so
+//                                              every holder materialises alpha
+//   backward  from_owner (d_num, c) (w D+H)    c_v = d_num_v . num_v per head; the
+//                                              softmax backward identity
+//                                              d_e = alpha_e (d_num_v.z_u - c_v)
+//                                              replaces the dd to/from rounds
+//             to_owner dt (w H)
 //   (SURVEY §7 hard part 5; verified there to 1e-15 in float64.)
-//
-// Kernels (per layer l, device d):
-//   k_gat_project   z = h_prev W, s = z.a_src, t = z_self.a_dst (tile GEMV, FP32)
-//   k_gat_agg       per destination row: e = leaky(s_u + t_v), online softmax
-//                   (m, s, U) over its in-edges (team per row, EG edge groups
-//                   merged by a fixed xor tree); pre_e stored per edge; ref rows
-//                   packed into the push-to-owner buffer
-//   k_gat_combine   owner merge of local + holders' (m, s, U) in ascending
-//                   sender order -> m, den, num, h
-//   k_gat_alpha     alpha_e = exp(e - m_v) / den_v per local edge
-//   k_gat_bwd_rows  d_num, c
-//   k_gat_bwd_dst   per destination row: d_alpha, d_pre_e (stored), dt partial
-//   k_gat_bwd_src   per source row (CSR-by-source): d_z = sum alpha d_num +
-//                   ds a_src (+ dt a_dst on self rows), ds
-//   k_gat_bwd_param per-block partials of [dW | da_src | da_dst] and d_h_prev
+// Per-edge arrays hold H values per edge ([edge][head]); per-row scalars H
+// values per row ([row][head]); D = H * d_head.
 #include <cstring>
 #include <type_traits>
 
@@ -41,11 +31,49 @@ namespace {
 
 __device__ __forceinline__ float leaky(float x, float slope) { return x > 0.f ? x : slope * x; }
 
+template <int VEC>
+struct V4;
+template <>
+struct V4<4> {
+  using T = float4;
+  __device__ static T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  __device__ static T ld(const float* p) { return *reinterpret_cast<const float4*>(p); }
+  __device__ static T ld_any(const float* p) { return make_float4(p[0], p[1], p[2], p[3]); }
+  __device__ static void st(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
+  __device__ static void st_any(float* p, T v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w; }
+  __device__ static T axpby(float a, T x, float b, T y) {
+    return make_float4(fmaf(a, x.x, b * y.x), fmaf(a, x.y, b * y.y), fmaf(a, x.z, b * y.z), fmaf(a, x.w, b * y.w));
+  }
+  __device__ static void fma_(T& acc, float a, T x) {
+    acc.x = fmaf(a, x.x, acc.x); acc.y = fmaf(a, x.y, acc.y); acc.z = fmaf(a, x.z, acc.z); acc.w = fmaf(a, x.w, acc.w);
+  }
+  __device__ static float dot(T x, T y) { return fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, x.w * y.w))); }
+  __device__ static T shfl_xor(unsigned m, T v, int o, int w) {
+    return make_float4(__shfl_xor_sync(m, v.x, o, w), __shfl_xor_sync(m, v.y, o, w),
+                       __shfl_xor_sync(m, v.z, o, w), __shfl_xor_sync(m, v.w, o, w));
+  }
+  __device__ static void add(T& a, T b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+};
+template <>
+struct V4<1> {
+  using T = float;
+  __device__ static T zero() { return 0.f; }
+  __device__ static T ld(const float* p) { return *p; }
+  __device__ static T ld_any(const float* p) { return *p; }
+  __device__ static void st(float* p, T v) { *p = v; }
+  __device__ static void st_any(float* p, T v) { *p = v; }
+  __device__ static T axpby(float a, T x, float b, T y) { return fmaf(a, x, b * y); }
+  __device__ static void fma_(T& acc, float a, T x) { acc = fmaf(a, x, acc); }
+  __device__ static float dot(T x, T y) { return x * y; }
+  __device__ static T shfl_xor(unsigned m, T v, int o, int w) { return __shfl_xor_sync(m, v, o, w); }
+  __device__ static void add(T& a, T b) { a += b; }
+};
+
 // ---------------------------------------------------------------- projection
 constexpr int PTR = 32;
 
 struct ProjArgs {
-  int l, d, w, dout;
+  int l, d, w, dout, heads;
   int64_t voff_lm1, voff_l;
   const float* h_prev;
   const int32_t* src_row;
@@ -55,14 +83,14 @@ struct ProjArgs {
   const float* a_src;
   const float* a_dst;
   float* z;
-  float* s;
-  float* t;
+  float* s;  // [row][head]
+  float* t;  // [owned row at l][head]
 };
 
 template <bool Q4>
 __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ meta, ProjArgs a) {
   extern __shared__ __align__(16) float smem[];
-  const int w = a.w, dout = a.dout, wp = w + 1, dp = dout + 1;
+  const int w = a.w, dout = a.dout, wp = w + 1, dp = dout + 1, H = a.heads, dh = dout / H;
   float* W_s = smem;               // [w][dout]
   float* h_s = W_s + w * dout;     // [PTR][w+1]
   float* z_s = h_s + PTR * wp;     // [PTR][dout+1]
@@ -126,17 +154,18 @@ __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ 
       }
     }
     __syncthreads();
-    if (threadIdx.x < nrow) {
-      const int rr = threadIdx.x;
+    for (int idx = threadIdx.x; idx < nrow * H; idx += blockDim.x) {
+      const int rr = idx / H, hh = idx - rr * H;
       const int G = own0 + tile * PTR + rr;
+      const float* zr = z_s + rr * dp + hh * dh;
       float sv = 0.f;
-      for (int j = 0; j < dout; ++j) sv = fmaf(z_s[rr * dp + j], a.a_src[j], sv);
-      a.s[G] = sv;
+      for (int j = 0; j < dh; ++j) sv = fmaf(zr[j], a.a_src[hh * dh + j], sv);
+      a.s[(int64_t)G * H + hh] = sv;
       const int p = a.grouped[a.voff_lm1 + G];
       if (p < nVl) {  // self row of owned v at layer l
         float tv = 0.f;
-        for (int j = 0; j < dout; ++j) tv = fmaf(z_s[rr * dp + j], a.a_dst[j], tv);
-        a.t[ownl + a.rank[a.voff_l + p]] = tv;
+        for (int j = 0; j < dh; ++j) tv = fmaf(zr[j], a.a_dst[hh * dh + j], tv);
+        a.t[(int64_t)(ownl + a.rank[a.voff_l + p]) * H + hh] = tv;
       }
     }
   }
@@ -144,7 +173,7 @@ __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ 
 
 // ---------------------------------------------------------------- online-softmax aggregation
 struct AggArgs {
-  int l, d, dout, stride;
+  int l, d, dout, heads, stride;
   float slope;
   int64_t eoff_li, rbase_li, pbase_l;
   const int32_t* rowbeg;
@@ -155,62 +184,23 @@ struct AggArgs {
   const float* z;
   const float* s;
   const float* t;
-  const float* t_recv;  // pair layout, stride 1
-  float* pre_e;
-  float* loc_m;
+  const float* t_recv;  // pair layout, stride H
+  float* pre_e;         // [edge][head]
+  float* loc_m;         // [row][head]
   float* loc_s;
-  float* loc_U;
-  float* sendbuf;  // [U | m | s]
+  float* loc_U;         // [row][D]
+  float* sendbuf;       // [U (D) | m (H) | s (H)]
 };
 
-template <int VEC>
-struct V4;
-template <>
-struct V4<4> {
-  using T = float4;
-  __device__ static T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-  __device__ static T ld(const float* p) { return *reinterpret_cast<const float4*>(p); }
-  __device__ static T ld_any(const float* p) { return make_float4(p[0], p[1], p[2], p[3]); }
-  __device__ static void st(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
-  __device__ static void st_any(float* p, T v) { p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w; }
-  __device__ static T axpby(float a, T x, float b, T y) {  // a*x + b*y
-    return make_float4(fmaf(a, x.x, b * y.x), fmaf(a, x.y, b * y.y), fmaf(a, x.z, b * y.z), fmaf(a, x.w, b * y.w));
-  }
-  __device__ static void fma_(T& acc, float a, T x) {
-    acc.x = fmaf(a, x.x, acc.x); acc.y = fmaf(a, x.y, acc.y); acc.z = fmaf(a, x.z, acc.z); acc.w = fmaf(a, x.w, acc.w);
-  }
-  __device__ static T scale(T x, float a) { return make_float4(x.x * a, x.y * a, x.z * a, x.w * a); }
-  __device__ static float dot(T x, T y) { return fmaf(x.x, y.x, fmaf(x.y, y.y, fmaf(x.z, y.z, x.w * y.w))); }
-  __device__ static T shfl_xor(unsigned m, T v, int o, int w) {
-    return make_float4(__shfl_xor_sync(m, v.x, o, w), __shfl_xor_sync(m, v.y, o, w),
-                       __shfl_xor_sync(m, v.z, o, w), __shfl_xor_sync(m, v.w, o, w));
-  }
-  __device__ static void add(T& a, T b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
-};
-template <>
-struct V4<1> {
-  using T = float;
-  __device__ static T zero() { return 0.f; }
-  __device__ static T ld(const float* p) { return *p; }
-  __device__ static T ld_any(const float* p) { return *p; }
-  __device__ static void st(float* p, T v) { *p = v; }
-  __device__ static void st_any(float* p, T v) { *p = v; }
-  __device__ static T axpby(float a, T x, float b, T y) { return fmaf(a, x, b * y); }
-  __device__ static void fma_(T& acc, float a, T x) { acc = fmaf(a, x, acc); }
-  __device__ static T scale(T x, float a) { return x * a; }
-  __device__ static float dot(T x, T y) { return x * y; }
-  __device__ static T shfl_xor(unsigned m, T v, int o, int w) { return __shfl_xor_sync(m, v, o, w); }
-  __device__ static void add(T& a, T b) { a += b; }
-};
-
-// Team of RL = LPR*EG lanes per destination row; LPR lanes span dout (VEC each).
+// Team of RL = LPR*EG lanes per destination row; LPR lanes span D (VEC each),
+// LH = LPR/H lanes per head; EG edge groups merged by a fixed xor tree.
 template <int VEC, int LPR, int EG>
 __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta, AggArgs a) {
   using V = V4<VEC>;
   using T = typename V::T;
   constexpr int RL = LPR * EG;
   constexpr int RPW = 32 / RL;
-  const int l = a.l, d = a.d, dout = a.dout;
+  const int l = a.l, d = a.d, dout = a.dout, H = a.heads, LH = LPR / H;
   const int n_own = meta->n_own[l][d];
   const int R = n_own + meta->n_ref[l][d];
   const int own0 = meta->own_off[l][d], ref0 = meta->ref_off[l][d];
@@ -218,6 +208,8 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
   const int64_t rb = a.rbase_li + own0 + ref0;
   const int lane = threadIdx.x & 31;
   const int team = lane / RL, tl = lane % RL, eg = tl / LPR, lr = tl % LPR;
+  const int hl = lr / LH;           // this lane's head
+  const bool head_lead = (lr % LH) == 0;
   const unsigned tmask = (RL == 32) ? 0xffffffffu : (((1u << RL) - 1u) << (team * RL));
   const int col = lr * VEC;
   const bool colok = col < dout;
@@ -226,16 +218,16 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
   for (int64_t q = gw * RPW + team; q < R; q += nw * RPW) {
     const bool own = q < n_own;
     const int slot = own ? 0 : a.sendpos[a.pbase_l + ref0 + (q - n_own)];
-    const float tq = own ? a.t[own0 + q] : a.t_recv[slot];
+    const float tq = own ? a.t[(int64_t)(own0 + q) * H + hl] : a.t_recv[(int64_t)slot * H + hl];
     const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
     float m = -INFINITY, ssum = 0.f;
     T U = V::zero();
     for (int j = b + eg; j < e; j += EG) {
       const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
       const int u = prev0 + a.lsrc[x];
-      const float pre = a.s[u] + tq;
+      const float pre = a.s[(int64_t)u * H + hl] + tq;
       const float ev = leaky(pre, a.slope);
-      if (lr == 0) a.pre_e[x] = pre;
+      if (head_lead && colok) a.pre_e[x * H + hl] = pre;
       const T zu = colok ? V::ld(a.z + (int64_t)u * dout + col) : V::zero();
       if (ev > m) {
         const float sc = expf(m - ev);  // 0 on the first edge (m = -inf)
@@ -248,7 +240,6 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
         V::fma_(U, wv, zu);
       }
     }
-    // merge the EG edge groups with a fixed xor tree
 #pragma unroll
     for (int o = LPR; o < RL; o <<= 1) {
       const float m2 = __shfl_xor_sync(tmask, m, o, RL);
@@ -263,20 +254,20 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
     }
     if (eg != 0) continue;
     if (own) {
-      const int G = own0 + q;
-      if (colok) V::st(a.loc_U + (int64_t)G * dout + col, U);
-      if (lr == 0) {
-        a.loc_m[G] = m;
-        a.loc_s[G] = ssum;
+      const int64_t G = own0 + q;
+      if (colok) V::st(a.loc_U + G * dout + col, U);
+      if (head_lead && colok) {
+        a.loc_m[G * H + hl] = m;
+        a.loc_s[G * H + hl] = ssum;
       }
     } else {
       float* out = a.sendbuf + (int64_t)slot * a.stride;
       if (colok) {
         if ((a.stride & 3) == 0 && VEC == 4) V::st(out + col, U); else V::st_any(out + col, U);
       }
-      if (lr == 0) {
-        out[dout] = m;
-        out[dout + 1] = ssum;
+      if (head_lead && colok) {
+        out[dout + hl] = m;
+        out[dout + H + hl] = ssum;
       }
     }
   }
@@ -284,109 +275,116 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
 
 // ---------------------------------------------------------------- owner combine
 struct CombArgs {
-  int l, d, dout, g, stride, final_;
+  int l, d, dout, heads, g, stride, final_;
   int64_t voff_l;
   const int32_t* contrib;
   const float* loc_m;
   const float* loc_s;
   const float* loc_U;
   const float* recv;  // [U | m | s] rows, receive layout
-  float* md;          // [m, den] per owned row
+  float* md;          // [m (H) | den (H)] per owned row
   float* num;
   float* h;
 };
 
 __global__ void k_gat_combine(const SgMeta* __restrict__ meta, CombArgs a) {
-  const int l = a.l, d = a.d, dout = a.dout, g = a.g;
+  const int l = a.l, d = a.d, dout = a.dout, g = a.g, H = a.heads, dh = dout / H;
   const int n = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)n * dout;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int q = (int)(idx / dout), j = (int)(idx - (int64_t)q * dout);
+    const int hh = j / dh;
     const int64_t G = own0 + q;
     const int* cb = a.contrib + (int64_t)g * a.voff_l + G * g;
-    float m = a.loc_m[G];
+    const float m0 = a.loc_m[G * H + hh];
+    float m = m0;
     for (int s = 0; g > 1 && s < g; ++s) {
       const int rs = cb[s];
-      if (rs >= 0) m = fmaxf(m, a.recv[(int64_t)rs * a.stride + dout]);
+      if (rs >= 0) m = fmaxf(m, a.recv[(int64_t)rs * a.stride + dout + hh]);
     }
-    float f = expf(a.loc_m[G] - m);
-    float den = a.loc_s[G] * f;
+    const float f = expf(m0 - m);
+    float den = a.loc_s[G * H + hh] * f;
     float U = a.loc_U[G * dout + j] * f;
     for (int s = 0; g > 1 && s < g; ++s) {  // ascending sender order
       const int rs = cb[s];
       if (rs >= 0) {
         const float* r = a.recv + (int64_t)rs * a.stride;
-        const float fs = expf(r[dout] - m);
-        den = fmaf(r[dout + 1], fs, den);
+        const float fs = expf(r[dout + hh] - m);
+        den = fmaf(r[dout + H + hh], fs, den);
         U = fmaf(r[j], fs, U);
       }
     }
     const float nv = U / den;
     a.num[G * dout + j] = nv;
     a.h[G * dout + j] = a.final_ ? nv : fmaxf(nv, 0.f);
-    if (j == 0) {
-      a.md[2 * G] = m;
-      a.md[2 * G + 1] = den;
+    if (j - hh * dh == 0) {
+      a.md[G * 2 * H + hh] = m;
+      a.md[G * 2 * H + H + hh] = den;
     }
   }
 }
 
-// ---------------------------------------------------------------- alpha per edge
+// ---------------------------------------------------------------- alpha per edge and head
 struct AlphaArgs {
-  int l, d;
+  int l, d, heads;
   float slope;
   int64_t eoff_li, pbase_l;
   const int32_t* ldst;
   const int32_t* sendpos;
   const float* pre_e;
-  const float* md;        // owned rows
-  const float* md_recv;   // pair layout, stride 2
+  const float* md;        // owned rows, stride 2H
+  const float* md_recv;   // pair layout, stride 2H
   float* alpha;
 };
 
 __global__ void k_gat_alpha(const SgMeta* __restrict__ meta, AlphaArgs a) {
-  const int l = a.l, d = a.d, li = l - 1;
+  const int l = a.l, d = a.d, li = l - 1, H = a.heads;
   const int b = meta->edge_off[li][d], e = meta->edge_off[li][d + 1];
   const int n_own = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d], ref0 = meta->ref_off[l][d];
-  for (int i = b + blockIdx.x * blockDim.x + threadIdx.x; i < e; i += gridDim.x * blockDim.x) {
+  const int64_t tot = (int64_t)(e - b) * H;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < tot;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int i = b + (int)(k / H), hh = (int)(k % H);
     const int64_t x = a.eoff_li + i;
     const int q = a.ldst[x];
-    const float* mdp = q < n_own ? a.md + 2 * (int64_t)(own0 + q)
-                                 : a.md_recv + 2 * (int64_t)a.sendpos[a.pbase_l + ref0 + (q - n_own)];
-    a.alpha[x] = expf(leaky(a.pre_e[x], a.slope) - mdp[0]) / mdp[1];
+    const float* mdp = q < n_own ? a.md + 2 * (int64_t)H * (own0 + q)
+                                 : a.md_recv + 2 * (int64_t)H * a.sendpos[a.pbase_l + ref0 + (q - n_own)];
+    a.alpha[x * H + hh] = expf(leaky(a.pre_e[x * H + hh], a.slope) - mdp[hh]) / mdp[H + hh];
   }
 }
 
 // ---------------------------------------------------------------- backward
 struct BRowsArgs {
-  int l, d, dout, final_;
+  int l, d, dout, heads, final_;
   const float* d_h;
   const float* num;
-  float* dnc;  // [d_num | c] per owned row (stride dout+1)
+  float* dnc;  // [d_num (D) | c (H)] per owned row (stride D+H)
 };
 
 __global__ void k_gat_bwd_rows(const SgMeta* __restrict__ meta, BRowsArgs a) {
-  const int l = a.l, d = a.d, dout = a.dout;
+  const int l = a.l, d = a.d, dout = a.dout, H = a.heads, dh = dout / H, st = dout + H;
   const int n = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < (int64_t)n * H;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(k / H), hh = (int)(k % H);
     const int64_t G = own0 + q;
     float c = 0.f;
-    for (int j = 0; j < dout; ++j) {
+    for (int j = hh * dh; j < (hh + 1) * dh; ++j) {
       const float nv = a.num[G * dout + j];
       float dn = a.d_h[G * dout + j];
       if (!a.final_ && !(nv > 0.f)) dn = 0.f;
-      a.dnc[G * (dout + 1) + j] = dn;
+      a.dnc[G * st + j] = dn;
       c = fmaf(dn, nv, c);
     }
-    a.dnc[G * (dout + 1) + dout] = c;
+    a.dnc[G * st + dout + hh] = c;
   }
 }
 
 struct BDstArgs {
-  int l, d, dout, stride;
+  int l, d, dout, heads, stride;
   float slope;
   int64_t eoff_li, rbase_li, pbase_l;
   const int32_t* rowbeg;
@@ -397,11 +395,11 @@ struct BDstArgs {
   const float* z;
   const float* alpha;
   const float* pre_e;
-  const float* dnc;       // owned rows, stride dout+1
+  const float* dnc;       // owned rows, stride D+H
   const float* dnc_recv;  // pair layout, stride `stride`
-  float* d_pre;
-  float* dt_loc;
-  float* sendbuf;  // dt per pair slot (stride 1)
+  float* d_pre;           // [edge][head]
+  float* dt_loc;          // [row][head]
+  float* sendbuf;         // dt per pair slot (stride H)
 };
 
 template <int VEC, int LPR, int EG>
@@ -410,7 +408,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ 
   using T = typename V::T;
   constexpr int RL = LPR * EG;
   constexpr int RPW = 32 / RL;
-  const int l = a.l, d = a.d, dout = a.dout;
+  const int l = a.l, d = a.d, dout = a.dout, H = a.heads, LH = LPR / H;
   const int n_own = meta->n_own[l][d];
   const int R = n_own + meta->n_ref[l][d];
   const int own0 = meta->own_off[l][d], ref0 = meta->ref_off[l][d];
@@ -418,6 +416,8 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ 
   const int64_t rb = a.rbase_li + own0 + ref0;
   const int lane = threadIdx.x & 31;
   const int team = lane / RL, tl = lane % RL, eg = tl / LPR, lr = tl % LPR;
+  const int hl = lr / LH;
+  const bool head_lead = (lr % LH) == 0;
   const unsigned tmask = (RL == 32) ? 0xffffffffu : (((1u << RL) - 1u) << (team * RL));
   const int col = lr * VEC;
   const bool colok = col < dout;
@@ -426,10 +426,9 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ 
   for (int64_t q = gw * RPW + team; q < R; q += nw * RPW) {
     const bool own = q < n_own;
     const int slot = own ? 0 : a.sendpos[a.pbase_l + ref0 + (q - n_own)];
-    const float* dn_row = own ? a.dnc + (int64_t)(own0 + q) * (dout + 1) : a.dnc_recv + (int64_t)slot * a.stride;
-    // rows of stride dout+1 are not 16B aligned: element-wise loads
-    const T dn = colok ? V::ld_any(dn_row + col) : V::zero();
-    const float c = dn_row[dout];
+    const float* dn_row = own ? a.dnc + (int64_t)(own0 + q) * (dout + H) : a.dnc_recv + (int64_t)slot * a.stride;
+    const T dn = colok ? V::ld_any(dn_row + col) : V::zero();  // stride D+H: not 16B aligned
+    const float c = dn_row[dout + hl];
     const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
     float dt = 0.f;
     const int rounds = (e - b + EG - 1) / EG;
@@ -443,26 +442,25 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ 
         const int u = prev0 + a.lsrc[x];
         if (colok) part = V::dot(dn, V::ld(a.z + (int64_t)u * dout + col));
       }
-      // d_alpha = d_num . z_u : reduce over the LPR lanes of this edge group
-#pragma unroll
-      for (int o = 1; o < LPR; o <<= 1) part += __shfl_xor_sync(tmask, part, o, RL);
+      // d_alpha = d_num . z_u per head: reduce over the LH lanes of the head
+      for (int o = 1; o < LH; o <<= 1) part += __shfl_xor_sync(tmask, part, o, RL);
       if (ok) {
-        const float de = a.alpha[x] * (part - c);
-        const float dp = de * (a.pre_e[x] > 0.f ? 1.f : a.slope);
-        if (lr == 0) a.d_pre[x] = dp;
+        const float de = a.alpha[x * H + hl] * (part - c);
+        const float dp = de * (a.pre_e[x * H + hl] > 0.f ? 1.f : a.slope);
+        if (head_lead && colok) a.d_pre[x * H + hl] = dp;
         dt += dp;
       }
     }
 #pragma unroll
     for (int o = LPR; o < RL; o <<= 1) dt += __shfl_xor_sync(tmask, dt, o, RL);
-    if (tl != 0) continue;
-    if (own) a.dt_loc[own0 + q] = dt;
-    else a.sendbuf[slot] = dt;
+    if (eg != 0 || !head_lead || !colok) continue;
+    if (own) a.dt_loc[(int64_t)(own0 + q) * H + hl] = dt;
+    else a.sendbuf[(int64_t)slot * H + hl] = dt;
   }
 }
 
 struct BSrcArgs {
-  int l, d, dout, g, stride;
+  int l, d, dout, heads, g, stride;
   int64_t voff_lm1, voff_l, pbase_l, key_base;
   const int32_t* grouped;
   const int32_t* rank;
@@ -478,12 +476,12 @@ struct BSrcArgs {
   const float* dnc_recv;
   int dnc_stride;
   const float* dt_loc;
-  const float* dt_recv;  // receive layout, stride 1
+  const float* dt_recv;  // receive layout, stride H
   const float* a_src;
   const float* a_dst;
   float* d_z;
-  float* ds;
-  float* dt_tot;
+  float* ds;      // [row][head]
+  float* dt_tot;  // [row][head]
 };
 
 // warp per source row; NG = 32/LPR lane groups split the out-edges
@@ -492,13 +490,15 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ 
   using V = V4<VEC>;
   using T = typename V::T;
   constexpr int NG = 32 / LPR;
-  const int l = a.l, d = a.d, dout = a.dout;
+  const int l = a.l, d = a.d, dout = a.dout, H = a.heads, LH = LPR / H;
   const int n_prev = meta->n_own[l - 1][d];
   const int prev0 = meta->own_off[l - 1][d];
   const int own0 = meta->own_off[l][d], n_own = meta->n_own[l][d], ref0 = meta->ref_off[l][d];
   const int64_t nVl = meta->nV[l];
   const int lane = threadIdx.x & 31;
   const int gi = lane / LPR, lr = lane % LPR;
+  const int hl = lr / LH;
+  const bool head_lead = (lr % LH) == 0;
   const int col = lr * VEC;
   const bool colok = col < dout;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -519,11 +519,12 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ 
         if (k < cnt) {
           const int q = a.ldst[x];
           const float* dn_row = q < n_own
-              ? a.dnc + (int64_t)(own0 + q) * (dout + 1)
+              ? a.dnc + (int64_t)(own0 + q) * (dout + H)
               : a.dnc_recv + (int64_t)a.sendpos[a.pbase_l + ref0 + (q - n_own)] * a.dnc_stride;
-          const float al = a.alpha[x];
-          if (colok) V::fma_(acc, al, V::ld_any(dn_row + col));
-          if (lr == 0) dsv += a.d_pre[x];
+          if (colok) {
+            V::fma_(acc, a.alpha[(int64_t)x * H + hl], V::ld_any(dn_row + col));
+            dsv += a.d_pre[(int64_t)x * H + hl];
+          }
         }
       }
     }
@@ -532,33 +533,31 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ 
       V::add(acc, V::shfl_xor(0xffffffffu, acc, o, 32));
       dsv += __shfl_xor_sync(0xffffffffu, dsv, o);
     }
-    dsv = __shfl_sync(0xffffffffu, dsv, 0);  // lane 0 holds the full sum
     if (gi != 0) continue;
-    // d_z += ds * a_src
-    if (colok) V::fma_(acc, dsv, V::ld_any(a.a_src + col));
+    if (colok) V::fma_(acc, dsv, V::ld_any(a.a_src + col));  // d_z += ds * a_src
     const int p = a.grouped[a.voff_lm1 + U];
     if (p < nVl) {  // self row of owned v: d_z += dt_v * a_dst (owner combines holders' dt)
       const int64_t v = own0 + a.rank[a.voff_l + p];
-      float dt = a.dt_loc[v];
+      float dt = a.dt_loc[v * H + hl];
       const int* cb = a.contrib + (int64_t)a.g * a.voff_l + v * a.g;
       for (int s = 0; a.g > 1 && s < a.g; ++s) {
         const int rs = cb[s];
-        if (rs >= 0) dt += a.dt_recv[rs];
+        if (rs >= 0) dt += a.dt_recv[(int64_t)rs * H + hl];
       }
       if (colok) V::fma_(acc, dt, V::ld_any(a.a_dst + col));
-      if (lr == 0) a.dt_tot[v] = dt;
+      if (head_lead && colok) a.dt_tot[v * H + hl] = dt;
     }
     if (colok) V::st(a.d_z + U * dout + col, acc);  // dout % VEC == 0: aligned
-    if (lr == 0) a.ds[U] = dsv;
+    if (head_lead && colok) a.ds[U * H + hl] = dsv;
   }
 }
 
 // per-block partials of [dW | da_src | da_dst] over source rows; d_h_prev
 constexpr int QTR = 32;
-constexpr int QMAXQ = 8;  // float4 slots: w*dout/4 <= 2048
+constexpr int QMAXQ = 8;  // scalar slots / 4 per thread: w*dout <= 8192
 
 struct BParamArgs {
-  int l, d, w, dout;
+  int l, d, w, dout, heads;
   int64_t voff_lm1, voff_l;
   const float* h_prev;
   const int32_t* src_row;
@@ -575,14 +574,14 @@ struct BParamArgs {
 
 __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict__ meta, BParamArgs a) {
   extern __shared__ __align__(16) float smem[];
-  const int w = a.w, dout = a.dout, wp = w + 1, wst = dout + 4;
+  const int w = a.w, dout = a.dout, wp = w + 1, wst = dout + 4, H = a.heads, dh = dout / H;
   float* dz_s = smem;               // [QTR][dout]
   float* W_s = dz_s + QTR * dout;   // [w][dout+4] (for d_prev)
   float* h_s = W_s + w * wst;       // [QTR][w+1]
   float* z_s = h_s + QTR * wp;      // [QTR][dout]
-  float* ds_s = z_s + QTR * dout;   // [QTR]
-  float* dt_s = ds_s + QTR;         // [QTR] (0 when not a self row)
-  int* prow_s = (int*)(dt_s + QTR);
+  float* ds_s = z_s + QTR * dout;   // [QTR][H]
+  float* dt_s = ds_s + QTR * H;     // [QTR][H] (0 when not a self row)
+  int* prow_s = (int*)(dt_s + QTR * H);
   if (a.d_prev)
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
@@ -604,19 +603,25 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
     const int nrow = min(QTR, n - tile * QTR);
     if (threadIdx.x < QTR) {
       const int rr = threadIdx.x;
+      prow_s[rr] = -1;
       if (rr < nrow) {
         const int G = own0 + tile * QTR + rr;
         int r = G;
         if (a.src_row) r = a.src_row[r];
         prow_s[rr] = r;
-        ds_s[rr] = a.ds[G];
-        const int p = a.grouped[a.voff_lm1 + G];
-        dt_s[rr] = p < nVl ? a.dt_tot[ownl + a.rank[a.voff_l + p]] : 0.f;
-      } else {
-        prow_s[rr] = -1;
-        ds_s[rr] = 0.f;
-        dt_s[rr] = 0.f;
       }
+    }
+    for (int idx = threadIdx.x; idx < QTR * H; idx += blockDim.x) {
+      const int rr = idx / H, hh = idx - rr * H;
+      float dsv = 0.f, dtv = 0.f;
+      if (rr < nrow) {
+        const int G = own0 + tile * QTR + rr;
+        dsv = a.ds[(int64_t)G * H + hh];
+        const int p = a.grouped[a.voff_lm1 + G];
+        if (p < nVl) dtv = a.dt_tot[(int64_t)(ownl + a.rank[a.voff_l + p]) * H + hh];
+      }
+      ds_s[idx] = dsv;
+      dt_s[idx] = dtv;
     }
     for (int idx = threadIdx.x; idx < QTR * dout; idx += blockDim.x) {
       const int rr = idx / dout;
@@ -644,10 +649,10 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
       }
     }
     if (threadIdx.x < dout) {
-      const int j = threadIdx.x;
+      const int j = threadIdx.x, hh = j / dh;
       for (int rr = 0; rr < QTR; ++rr) {
-        as = fmaf(z_s[rr * dout + j], ds_s[rr], as);
-        ad = fmaf(z_s[rr * dout + j], dt_s[rr], ad);
+        as = fmaf(z_s[rr * dout + j], ds_s[rr * H + hh], as);
+        ad = fmaf(z_s[rr * dout + j], dt_s[rr * H + hh], ad);
       }
     }
     if (a.d_prev) {
@@ -673,9 +678,11 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
 }
 
 // ---------------------------------------------------------------- dispatch helpers
-#define GAT_TEAM_DISPATCH(KERNEL, DOUT, GRIDROWS, ST, ...)                                 \
+// Team shape from (D, H): LPR lanes span D (a power of two, multiple of H),
+// EG edge groups fill the team to 8..32 lanes.
+#define GAT_TEAM_DISPATCH(KERNEL, DOUT, HEADS, GRIDROWS, ST, ...)                          \
   do {                                                                                    \
-    const int dd_ = (DOUT);                                                               \
+    const int dd_ = (DOUT), hh_ = (HEADS);                                                \
     auto go_ = [&](auto vec_, auto lpr_, auto eg_) {                                      \
       constexpr int VEC_ = decltype(vec_)::value, LPR_ = decltype(lpr_)::value,           \
                     EG_ = decltype(eg_)::value;                                           \
@@ -689,18 +696,21 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
     using I8 = std::integral_constant<int, 8>;                                            \
     using I16 = std::integral_constant<int, 16>;                                          \
     using I32 = std::integral_constant<int, 32>;                                          \
-    if (dd_ % 4 == 0 && dd_ <= 4) go_(I4(), I1(), I8());                                  \
-    else if (dd_ % 4 == 0 && dd_ <= 8) go_(I4(), I2(), I8());                             \
-    else if (dd_ % 4 == 0 && dd_ <= 16) go_(I4(), I4(), I4());                            \
-    else if (dd_ % 4 == 0 && dd_ <= 32) go_(I4(), I8(), I2());                            \
-    else if (dd_ % 4 == 0 && dd_ <= 64) go_(I4(), I16(), I2());                           \
-    else if (dd_ % 4 == 0 && dd_ <= 128) go_(I4(), I32(), I1());                          \
-    else if (dd_ <= 4) go_(I1(), I4(), I4());                                             \
-    else if (dd_ <= 8) go_(I1(), I8(), I2());                                             \
-    else if (dd_ <= 16) go_(I1(), I16(), I2());                                           \
-    else if (dd_ <= 32) go_(I1(), I32(), I1());                                           \
+    const int q_ = dd_ / (4 * hh_);                                                       \
+    const bool v4_ = dd_ % (4 * hh_) == 0 && (q_ & (q_ - 1)) == 0 && (hh_ & (hh_ - 1)) == 0; \
+    if (v4_ && dd_ <= 4) go_(I4(), I1(), I8());                                           \
+    else if (v4_ && dd_ <= 8) go_(I4(), I2(), I8());                                      \
+    else if (v4_ && dd_ <= 16) go_(I4(), I4(), I4());                                     \
+    else if (v4_ && dd_ <= 32) go_(I4(), I8(), I2());                                     \
+    else if (v4_ && dd_ <= 64) go_(I4(), I16(), I2());                                    \
+    else if (v4_ && dd_ <= 128) go_(I4(), I32(), I1());                                   \
+    else if (hh_ == 1 && dd_ <= 4) go_(I1(), I4(), I4());                                 \
+    else if (hh_ == 1 && dd_ <= 8) go_(I1(), I8(), I2());                                 \
+    else if (hh_ == 1 && dd_ <= 16) go_(I1(), I16(), I2());                               \
+    else if (hh_ == 1 && dd_ <= 32) go_(I1(), I32(), I1());                               \
     else {                                                                                \
-      set_error("gat: hidden width unsupported (<=128 with %4==0, else <=32)");           \
+      set_error("gat: unsupported width/heads (multi-head needs power-of-two heads and "  \
+                "d_head/4, D <= 128; one head: D <= 128)");                               \
       return SG_ERR_ARG;                                                                  \
     }                                                                                     \
   } while (0)
@@ -713,17 +723,21 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
   const SgMeta* meta = (const SgMeta*)(base + y.o_meta);               \
   auto I32p = [&](int64_t o) { return (const int32_t*)(base + o); };
 
+#define GAT_HEADS_CHECK(dout, heads)                                              \
+  SG_REQUIRE((heads) >= 1 && (dout) % (heads) == 0, "gat: dout must be a multiple of heads")
+
 extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                               const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
-                              const float* W, const float* a_src, const float* a_dst, float* z,
-                              float* s, float* t, int64_t max_rows, void* stream) {
+                              int32_t heads, const float* W, const float* a_src, const float* a_dst,
+                              float* z, float* s, float* t, int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_project: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_project: bad layer/device");
+  GAT_HEADS_CHECK(dout, heads);
   if (max_rows <= 0) return SG_OK;
   ProjArgs a;
   memset(&a, 0, sizeof(a));
-  a.l = l; a.d = d; a.w = w; a.dout = dout;
+  a.l = l; a.d = d; a.w = w; a.dout = dout; a.heads = heads;
   a.voff_lm1 = y.voff[l - 1];
   a.voff_l = y.voff[l];
   a.h_prev = h_prev; a.src_row = src_row;
@@ -747,41 +761,44 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
 }
 
 extern "C" int sg_gat_agg(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                          int32_t dout, float slope, const float* z, const float* s, const float* t,
-                          const float* t_recv, const int32_t* dperm, float* pre_e, float* loc_m,
-                          float* loc_s, float* loc_U, float* sendbuf, int32_t send_stride,
-                          int64_t max_rows, void* stream) {
+                          int32_t dout, int32_t heads, float slope, const float* z, const float* s,
+                          const float* t, const float* t_recv, const int32_t* dperm, float* pre_e,
+                          float* loc_m, float* loc_s, float* loc_U, float* sendbuf,
+                          int32_t send_stride, int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_agg: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_agg: bad layer/device");
-  SG_REQUIRE(send_stride >= dout + 2 || y.g == 1, "gat_agg: send stride < dout+2");
+  GAT_HEADS_CHECK(dout, heads);
+  SG_REQUIRE(send_stride >= dout + 2 * heads || y.g == 1, "gat_agg: send stride < D+2H");
   if (max_rows <= 0) return SG_OK;
   AggArgs a;
   memset(&a, 0, sizeof(a));
-  a.l = l; a.d = d; a.dout = dout; a.stride = send_stride; a.slope = slope;
+  a.l = l; a.d = d; a.dout = dout; a.heads = heads; a.stride = send_stride; a.slope = slope;
   a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.pbase_l = y.pbase[l];
   a.rowbeg = I32p(y.o_rowbeg); a.rowend = I32p(y.o_rowend); a.lsrc = I32p(y.o_lsrc);
   a.dperm = dperm; a.sendpos = I32p(y.o_sendpos);
   a.z = z; a.s = s; a.t = t; a.t_recv = t_recv;
   a.pre_e = pre_e; a.loc_m = loc_m; a.loc_s = loc_s; a.loc_U = loc_U; a.sendbuf = sendbuf;
   cudaStream_t st = (cudaStream_t)stream;
-  GAT_TEAM_DISPATCH(k_gat_agg, dout, max_rows, st, meta, a);
+  GAT_TEAM_DISPATCH(k_gat_agg, dout, heads, max_rows, st, meta, a);
   SG_CHECK_LAUNCH("k_gat_agg");
   return SG_OK;
 }
 
 extern "C" int sg_gat_combine(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                              int32_t dout, const float* loc_m, const float* loc_s,
+                              int32_t dout, int32_t heads, const float* loc_m, const float* loc_s,
                               const float* loc_U, const float* recv, int32_t recv_stride,
                               int32_t final_layer, float* md, float* num, float* h,
                               int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_combine: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_combine: bad layer/device");
+  GAT_HEADS_CHECK(dout, heads);
   if (max_rows <= 0) return SG_OK;
   CombArgs a;
   memset(&a, 0, sizeof(a));
-  a.l = l; a.d = d; a.dout = dout; a.g = y.g; a.stride = recv_stride; a.final_ = final_layer;
+  a.l = l; a.d = d; a.dout = dout; a.heads = heads; a.g = y.g; a.stride = recv_stride;
+  a.final_ = final_layer;
   a.voff_l = y.voff[l]; a.contrib = I32p(y.o_contrib);
   a.loc_m = loc_m; a.loc_s = loc_s; a.loc_U = loc_U; a.recv = recv; a.md = md; a.num = num; a.h = h;
   k_gat_combine<<<clamp_grid(div_up(max_rows * dout, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(meta, a);
@@ -790,58 +807,61 @@ extern "C" int sg_gat_combine(const void* split_ws, const SgSplitLayout* lay, in
 }
 
 extern "C" int sg_gat_alpha(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                            float slope, const float* pre_e, const float* md, const float* md_recv,
-                            float* alpha, int64_t max_edges, void* stream) {
+                            int32_t heads, float slope, const float* pre_e, const float* md,
+                            const float* md_recv, float* alpha, int64_t max_edges, void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_alpha: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "gat_alpha: bad layer/device");
   if (max_edges <= 0) return SG_OK;
   AlphaArgs a;
   memset(&a, 0, sizeof(a));
-  a.l = l; a.d = d; a.slope = slope; a.eoff_li = y.eoff[l - 1]; a.pbase_l = y.pbase[l];
+  a.l = l; a.d = d; a.heads = heads; a.slope = slope; a.eoff_li = y.eoff[l - 1]; a.pbase_l = y.pbase[l];
   a.ldst = I32p(y.o_ldst); a.sendpos = I32p(y.o_sendpos);
   a.pre_e = pre_e; a.md = md; a.md_recv = md_recv; a.alpha = alpha;
-  k_gat_alpha<<<clamp_grid(div_up(max_edges, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  k_gat_alpha<<<clamp_grid(div_up(max_edges * heads, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(meta, a);
   SG_CHECK_LAUNCH("k_gat_alpha");
   return SG_OK;
 }
 
 extern "C" int sg_gat_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                               int32_t dout, const float* d_h, const float* num, int32_t final_layer,
-                               float* dnc, int64_t max_rows, void* stream) {
+                               int32_t dout, int32_t heads, const float* d_h, const float* num,
+                               int32_t final_layer, float* dnc, int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_bwd_rows: null workspace");
   SPLIT_PTRS
+  GAT_HEADS_CHECK(dout, heads);
   if (max_rows <= 0) return SG_OK;
-  BRowsArgs a{l, d, dout, final_layer, d_h, num, dnc};
-  k_gat_bwd_rows<<<clamp_grid(div_up(max_rows, 256), kSMs * 4), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  BRowsArgs a{l, d, dout, heads, final_layer, d_h, num, dnc};
+  k_gat_bwd_rows<<<clamp_grid(div_up(max_rows * heads, 256), kSMs * 4), 256, 0, (cudaStream_t)stream>>>(meta, a);
   SG_CHECK_LAUNCH("k_gat_bwd_rows");
   return SG_OK;
 }
 
 extern "C" int sg_gat_bwd_dst(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                              int32_t dout, float slope, const float* z, const float* alpha,
-                              const float* pre_e, const float* dnc, const float* dnc_recv,
-                              int32_t recv_stride, const int32_t* dperm, float* d_pre,
-                              float* dt_loc, float* sendbuf, int64_t max_rows, void* stream) {
+                              int32_t dout, int32_t heads, float slope, const float* z,
+                              const float* alpha, const float* pre_e, const float* dnc,
+                              const float* dnc_recv, int32_t recv_stride, const int32_t* dperm,
+                              float* d_pre, float* dt_loc, float* sendbuf, int64_t max_rows,
+                              void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_bwd_dst: null workspace");
   SPLIT_PTRS
+  GAT_HEADS_CHECK(dout, heads);
   if (max_rows <= 0) return SG_OK;
   BDstArgs a;
   memset(&a, 0, sizeof(a));
-  a.l = l; a.d = d; a.dout = dout; a.stride = recv_stride; a.slope = slope;
+  a.l = l; a.d = d; a.dout = dout; a.heads = heads; a.stride = recv_stride; a.slope = slope;
   a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.pbase_l = y.pbase[l];
   a.rowbeg = I32p(y.o_rowbeg); a.rowend = I32p(y.o_rowend); a.lsrc = I32p(y.o_lsrc);
   a.dperm = dperm; a.sendpos = I32p(y.o_sendpos);
   a.z = z; a.alpha = alpha; a.pre_e = pre_e; a.dnc = dnc; a.dnc_recv = dnc_recv;
   a.d_pre = d_pre; a.dt_loc = dt_loc; a.sendbuf = sendbuf;
   cudaStream_t st = (cudaStream_t)stream;
-  GAT_TEAM_DISPATCH(k_gat_bwd_dst, dout, max_rows, st, meta, a);
+  GAT_TEAM_DISPATCH(k_gat_bwd_dst, dout, heads, max_rows, st, meta, a);
   SG_CHECK_LAUNCH("k_gat_bwd_dst");
   return SG_OK;
 }
 
 extern "C" int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                              int32_t dout, const int32_t* perm, const int32_t* srcbeg,
+                              int32_t dout, int32_t heads, const int32_t* perm, const int32_t* srcbeg,
                               const int32_t* srcend, int64_t key_base, const float* alpha,
                               const float* d_pre, const float* dnc, const float* dnc_recv,
                               int32_t dnc_stride, const float* dt_loc, const float* dt_recv,
@@ -849,10 +869,11 @@ extern "C" int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, in
                               float* dt_tot, int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_bwd_src: null workspace");
   SPLIT_PTRS
+  GAT_HEADS_CHECK(dout, heads);
   if (max_rows <= 0) return SG_OK;
   BSrcArgs a;
   memset(&a, 0, sizeof(a));
-  a.l = l; a.d = d; a.dout = dout; a.g = y.g;
+  a.l = l; a.d = d; a.dout = dout; a.heads = heads; a.g = y.g;
   a.voff_lm1 = y.voff[l - 1]; a.voff_l = y.voff[l]; a.pbase_l = y.pbase[l]; a.key_base = key_base;
   a.grouped = I32p(y.o_grouped); a.rank = I32p(y.o_rank); a.contrib = I32p(y.o_contrib);
   a.ldst = I32p(y.o_ldst); a.sendpos = I32p(y.o_sendpos);
@@ -862,14 +883,16 @@ extern "C" int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, in
   a.d_z = d_z; a.ds = ds; a.dt_tot = dt_tot;
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = clamp_grid(div_up(max_rows, 8), kSMs * 8);
-  if (dout % 4 == 0 && dout <= 16) k_gat_bwd_src<4, 4><<<grid, 256, 0, st>>>(meta, a);
-  else if (dout % 4 == 0 && dout <= 32) k_gat_bwd_src<4, 8><<<grid, 256, 0, st>>>(meta, a);
-  else if (dout % 4 == 0 && dout <= 64) k_gat_bwd_src<4, 16><<<grid, 256, 0, st>>>(meta, a);
-  else if (dout % 4 == 0 && dout <= 128) k_gat_bwd_src<4, 32><<<grid, 256, 0, st>>>(meta, a);
-  else if (dout <= 8) k_gat_bwd_src<1, 8><<<grid, 256, 0, st>>>(meta, a);
-  else if (dout <= 32) k_gat_bwd_src<1, 32><<<grid, 256, 0, st>>>(meta, a);
+  const int q = dout / (4 * heads);
+  const bool v4 = dout % (4 * heads) == 0 && (q & (q - 1)) == 0 && (heads & (heads - 1)) == 0;
+  if (v4 && dout <= 16) k_gat_bwd_src<4, 4><<<grid, 256, 0, st>>>(meta, a);
+  else if (v4 && dout <= 32) k_gat_bwd_src<4, 8><<<grid, 256, 0, st>>>(meta, a);
+  else if (v4 && dout <= 64) k_gat_bwd_src<4, 16><<<grid, 256, 0, st>>>(meta, a);
+  else if (v4 && dout <= 128) k_gat_bwd_src<4, 32><<<grid, 256, 0, st>>>(meta, a);
+  else if (heads == 1 && dout <= 8) k_gat_bwd_src<1, 8><<<grid, 256, 0, st>>>(meta, a);
+  else if (heads == 1 && dout <= 32) k_gat_bwd_src<1, 32><<<grid, 256, 0, st>>>(meta, a);
   else {
-    set_error("gat_bwd_src: hidden width unsupported");
+    set_error("gat_bwd_src: unsupported width/heads");
     return SG_ERR_ARG;
   }
   SG_CHECK_LAUNCH("k_gat_bwd_src");
@@ -878,22 +901,23 @@ extern "C" int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, in
 
 extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                                 const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
-                                const float* z, const float* d_z, const float* ds,
+                                int32_t heads, const float* z, const float* d_z, const float* ds,
                                 const float* dt_tot, const float* W, float* partial, int32_t nblocks,
                                 float* d_prev, int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "gat_bwd_param: null workspace");
   SPLIT_PTRS
+  GAT_HEADS_CHECK(dout, heads);
   SG_REQUIRE((int64_t)w * dout <= 256 * QMAXQ * 4, "gat_bwd_param: w*dout > 8192 unsupported");
   SG_REQUIRE(nblocks >= 1, "gat_bwd_param: nblocks >= 1");
   (void)max_rows;
   BParamArgs a;
   memset(&a, 0, sizeof(a));
-  a.l = l; a.d = d; a.w = w; a.dout = dout;
+  a.l = l; a.d = d; a.w = w; a.dout = dout; a.heads = heads;
   a.voff_lm1 = y.voff[l - 1]; a.voff_l = y.voff[l];
   a.h_prev = h_prev; a.src_row = src_row; a.grouped = I32p(y.o_grouped); a.rank = I32p(y.o_rank);
   a.z = z; a.d_z = d_z; a.ds = ds; a.dt_tot = dt_tot; a.W = W; a.partial = partial; a.d_prev = d_prev;
   const size_t smem = sizeof(float) * (2 * (size_t)QTR * dout + (size_t)w * (dout + 4) +
-                                       (size_t)QTR * (w + 1) + 3 * QTR);
+                                       (size_t)QTR * (w + 1) + 2 * (size_t)QTR * heads + QTR);
   SG_REQUIRE(smem <= 227 * 1024, "gat_bwd_param: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   SG_CUDA(allow_max_smem<k_gat_bwd_param>());

@@ -55,24 +55,25 @@ def gat_forward(step):
         h_prev, src_row = (step.f.table, step.src_row0) if l == 1 else (step.h[l - 1], None)
         nVp, nV, P = ds.nV[l - 1], ds.nV[l], ds.pair_bound(l)
         W, a_s, a_d = (p.view(f"layer{l-1}.{k}") for k in ("w", "a_src", "a_dst"))
+        H = p.heads_of(l - 1)
         z = _f32(nVp, dout, device=step.dev)
-        s = _f32(nVp, device=step.dev)
-        t = _f32(nV, device=step.dev)
+        s = _f32(nVp, H, device=step.dev)
+        t = _f32(nV, H, device=step.dev)
         for d in step.devices:
             _lib.call("sg_gat_project", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
-                      w, dout, _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(z), _lib.ptr(s),
+                      w, dout, H, _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(z), _lib.ptr(s),
                       _lib.ptr(t), step.n_own(l - 1, d), st)
-        t_recv = _from_owner(step, l, t, 1)
-        SW = _r4(dout + 2)
+        t_recv = _from_owner(step, l, t, H)
+        SW = _r4(dout + 2 * H)
         send = _f32(P, SW, device=step.dev)
         recv = _f32(P, SW, device=step.dev)
-        pre_e = _f32(nEtot, device=step.dev)
-        loc_m = _f32(nV, device=step.dev)
-        loc_s = _f32(nV, device=step.dev)
+        pre_e = _f32(nEtot, H, device=step.dev)
+        loc_m = _f32(nV, H, device=step.dev)
+        loc_s = _f32(nV, H, device=step.dev)
         loc_U = _f32(nV, dout, device=step.dev)
         step._ev(f"agg{l}_start")
         for d in step.devices:
-            _lib.call("sg_gat_agg", _lib.ptr(ds.ws), ds.lay, l, d, dout, slope, _lib.ptr(z), _lib.ptr(s),
+            _lib.call("sg_gat_agg", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(z), _lib.ptr(s),
                       _lib.ptr(t), _lib.ptr(t_recv), dp_ptr(d), _lib.ptr(pre_e), _lib.ptr(loc_m),
                       _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(send), SW, step.n_rows(l, d), st)
         step._ev(f"agg{l}_end")
@@ -80,18 +81,18 @@ def gat_forward(step):
             step.transport.to_owner(ds, l, send, recv, SW)
             if step.meta is not None:
                 step.wire_bytes += int(step.meta.npairs[l]) * SW * 4
-        md = _f32(nV, 2, device=step.dev)
+        md = _f32(nV, 2 * H, device=step.dev)
         num = _f32(nV, dout, device=step.dev)
         h = _f32(nV, dout, device=step.dev)
         for d in step.devices:
-            _lib.call("sg_gat_combine", _lib.ptr(ds.ws), ds.lay, l, d, dout, _lib.ptr(loc_m), _lib.ptr(loc_s),
-                      _lib.ptr(loc_U), _lib.ptr(recv), SW, final, _lib.ptr(md), _lib.ptr(num), _lib.ptr(h),
-                      step.n_own(l, d), st)
-        md_recv = _from_owner(step, l, md, 2)
-        alpha = _f32(nEtot, device=step.dev)
+            _lib.call("sg_gat_combine", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(loc_m),
+                      _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(recv), SW, final, _lib.ptr(md), _lib.ptr(num),
+                      _lib.ptr(h), step.n_own(l, d), st)
+        md_recv = _from_owner(step, l, md, 2 * H)
+        alpha = _f32(nEtot, H, device=step.dev)
         for d in step.devices:
             ne = int(step.meta.n_edge[l - 1][d]) if step.meta is not None else ds.nE[l - 1]
-            _lib.call("sg_gat_alpha", _lib.ptr(ds.ws), ds.lay, l, d, slope, _lib.ptr(pre_e), _lib.ptr(md),
+            _lib.call("sg_gat_alpha", _lib.ptr(ds.ws), ds.lay, l, d, H, slope, _lib.ptr(pre_e), _lib.ptr(md),
                       _lib.ptr(md_recv), _lib.ptr(alpha), ne, st)
         step.h[l] = h
         step.keep[l] = dict(z=z, s=s, num=num, md=md, alpha=alpha, pre_e=pre_e)
@@ -114,31 +115,32 @@ def gat_backward(step):
         h_prev, src_row = (step.f.table, step.src_row0) if l == 1 else (step.h[l - 1], None)
         nVp, nV, P = ds.nV[l - 1], ds.nV[l], ds.pair_bound(l)
         W, a_s, a_d = (p.view(f"layer{l-1}.{k}") for k in ("w", "a_src", "a_dst"))
-        DS = dout + 1
+        H = p.heads_of(l - 1)
+        DS = dout + H
         dnc = _f32(nV, DS, device=step.dev)
         for d in step.devices:
-            _lib.call("sg_gat_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, dout, _lib.ptr(d_h),
+            _lib.call("sg_gat_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(d_h),
                       _lib.ptr(keep["num"]), final, _lib.ptr(dnc), step.n_own(l, d), st)
         dnc_recv = _from_owner(step, l, dnc, DS)
-        d_pre = _f32(nEtot, device=step.dev)
-        dt_loc = _f32(nV, device=step.dev)
-        dt_send = _f32(P, device=step.dev)
-        dt_recv = _f32(P, device=step.dev)
+        d_pre = _f32(nEtot, H, device=step.dev)
+        dt_loc = _f32(nV, H, device=step.dev)
+        dt_send = _f32(P, H, device=step.dev)
+        dt_recv = _f32(P, H, device=step.dev)
         for d in step.devices:
-            _lib.call("sg_gat_bwd_dst", _lib.ptr(ds.ws), ds.lay, l, d, dout, slope, _lib.ptr(keep["z"]),
+            _lib.call("sg_gat_bwd_dst", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(keep["z"]),
                       _lib.ptr(keep["alpha"]), _lib.ptr(keep["pre_e"]), _lib.ptr(dnc), _lib.ptr(dnc_recv),
                       DS, dp_ptr(d), _lib.ptr(d_pre), _lib.ptr(dt_loc), _lib.ptr(dt_send),
                       step.n_rows(l, d), st)
         if step.g > 1 and P > 0:
-            step.transport.to_owner(ds, l, dt_send, dt_recv, 1)
+            step.transport.to_owner(ds, l, dt_send, dt_recv, H)
             if step.meta is not None:
-                step.wire_bytes += int(step.meta.npairs[l]) * 4
+                step.wire_bytes += int(step.meta.npairs[l]) * 4 * H
         d_z = _f32(nVp, dout, device=step.dev)
-        dsb = _f32(nVp, device=step.dev)
-        dt_tot = _f32(nV, device=step.dev)
+        dsb = _f32(nVp, H, device=step.dev)
+        dt_tot = _f32(nV, H, device=step.dev)
         for d in step.devices:
             perm, beg, end = csr[d][:3]
-            _lib.call("sg_gat_bwd_src", _lib.ptr(ds.ws), ds.lay, l, d, dout, _lib.ptr(perm), _lib.ptr(beg),
+            _lib.call("sg_gat_bwd_src", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(perm), _lib.ptr(beg),
                       _lib.ptr(end), kb[l], _lib.ptr(keep["alpha"]), _lib.ptr(d_pre), _lib.ptr(dnc),
                       _lib.ptr(dnc_recv), DS, _lib.ptr(dt_loc), _lib.ptr(dt_recv), _lib.ptr(a_s), _lib.ptr(a_d),
                       _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), step.n_own(l - 1, d), st)
@@ -149,7 +151,7 @@ def gat_backward(step):
             nb = _nblocks(step.n_own(l - 1, d))
             part = _f32(nb * npart, device=step.dev)
             _lib.call("sg_gat_bwd_param", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
-                      w, dout, _lib.ptr(keep["z"]), _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), _lib.ptr(W),
+                      w, dout, H, _lib.ptr(keep["z"]), _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), _lib.ptr(W),
                       _lib.ptr(part), nb, _lib.ptr(d_prev), step.n_own(l - 1, d), st)
             step.jobs.append((part, nb, npart, step.grads[d], p.offset(f"layer{l-1}.w")))
             step._partials.append(part)

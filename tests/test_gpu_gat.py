@@ -97,3 +97,38 @@ def test_gat_loss_curve_50_steps():
         losses.append(loss / len(V[-1]))
     diff = np.abs(np.asarray(losses) - z["losses"])
     assert diff.max() < LOSS_TOL, diff.max()
+
+
+@pytest.mark.parametrize("g", [1, 2, 4])
+def test_gat_multihead_matches_composed_oracle(g):
+    """C3's 4-head GAT: parity by per-head composition of the reference layer
+    (SURVEY §8(a) row 11): split run summed over devices == composed single-
+    device oracle."""
+    import paper_2303_13775_b200 as sg
+    from oracle.multihead_oracle import multihead_run
+    graph, pm, sample, cache = random_partition_case(80 + g, n=5000, m=60000, g=g, batch=96,
+                                                     fanouts=(6, 5, 4), cache_frac=0.3)
+    F, H, dh, C = 24, 4, 16, 7
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=3)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=4)
+    params = sg.init_params("gat", F, dh, C, 3, seed=5, heads=H)
+    splits, plan = sg.split_minibatch(sample, pm, cache)
+    ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+    loss, grads = ex.run()
+    rloss, rgrads, rh = multihead_run(sample.layer_vertices, sample.layer_edges,
+                                      {k: np.asarray(v, dtype=np.float64) for k, v in params.tensors().items()},
+                                      feats.astype(np.float64), labels, H)
+    assert abs(loss - rloss) <= TOL * abs(rloss), (loss, rloss)
+    tot = {k: sum(gd[k] for gd in grads) for k in rgrads}
+    assert_grads_close(tot, rgrads, TOL, "sum")
+    for d in range(g):
+        for l in range(1, 4):
+            want = rh[l][splits[d].owned_pos[l]]
+            assert rel_err(ex.states[d].h[l], want) < TOL, (d, l)
+
+
+def test_multihead_init_is_reference_for_one_head():
+    import paper_2303_13775_b200 as sg
+    a = sg.init_params("gat", 10, 8, 3, 2, seed=1).tensors()
+    b = sg.init_params("gat", 10, 8, 3, 2, seed=1, heads=1).tensors()
+    assert all(np.array_equal(a[k], b[k]) for k in a)
