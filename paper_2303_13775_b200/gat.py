@@ -22,6 +22,11 @@ def _r4(x):
     return (int(x) + 3) // 4 * 4
 
 
+def _hs(H):
+    """Trailing head dimension (omitted for one head: reference shapes)."""
+    return (H,) if H > 1 else ()
+
+
 def _from_owner(step, l, rows, width):
     """Owner rows (global owned index) -> holders' pair-layout rows."""
     ds = step.ds
@@ -57,8 +62,8 @@ def gat_forward(step):
         W, a_s, a_d = (p.view(f"layer{l-1}.{k}") for k in ("w", "a_src", "a_dst"))
         H = p.heads_of(l - 1)
         z = _f32(nVp, dout, device=step.dev)
-        s = _f32(nVp, H, device=step.dev)
-        t = _f32(nV, H, device=step.dev)
+        s = _f32(nVp, *_hs(H), device=step.dev)
+        t = _f32(nV, *_hs(H), device=step.dev)
         for d in step.devices:
             _lib.call("sg_gat_project", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
                       w, dout, H, _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(z), _lib.ptr(s),
@@ -67,9 +72,9 @@ def gat_forward(step):
         SW = _r4(dout + 2 * H)
         send = _f32(P, SW, device=step.dev)
         recv = _f32(P, SW, device=step.dev)
-        pre_e = _f32(nEtot, H, device=step.dev)
-        loc_m = _f32(nV, H, device=step.dev)
-        loc_s = _f32(nV, H, device=step.dev)
+        pre_e = _f32(nEtot, *_hs(H), device=step.dev)
+        loc_m = _f32(nV, *_hs(H), device=step.dev)
+        loc_s = _f32(nV, *_hs(H), device=step.dev)
         loc_U = _f32(nV, dout, device=step.dev)
         step._ev(f"agg{l}_start")
         for d in step.devices:
@@ -89,7 +94,7 @@ def gat_forward(step):
                       _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(recv), SW, final, _lib.ptr(md), _lib.ptr(num),
                       _lib.ptr(h), step.n_own(l, d), st)
         md_recv = _from_owner(step, l, md, 2 * H)
-        alpha = _f32(nEtot, H, device=step.dev)
+        alpha = _f32(nEtot, *_hs(H), device=step.dev)
         for d in step.devices:
             ne = int(step.meta.n_edge[l - 1][d]) if step.meta is not None else ds.nE[l - 1]
             _lib.call("sg_gat_alpha", _lib.ptr(ds.ws), ds.lay, l, d, H, slope, _lib.ptr(pre_e), _lib.ptr(md),
@@ -122,10 +127,10 @@ def gat_backward(step):
             _lib.call("sg_gat_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(d_h),
                       _lib.ptr(keep["num"]), final, _lib.ptr(dnc), step.n_own(l, d), st)
         dnc_recv = _from_owner(step, l, dnc, DS)
-        d_pre = _f32(nEtot, H, device=step.dev)
-        dt_loc = _f32(nV, H, device=step.dev)
-        dt_send = _f32(P, H, device=step.dev)
-        dt_recv = _f32(P, H, device=step.dev)
+        d_pre = _f32(nEtot, *_hs(H), device=step.dev)
+        dt_loc = _f32(nV, *_hs(H), device=step.dev)
+        dt_send = _f32(P, *_hs(H), device=step.dev)
+        dt_recv = _f32(P, *_hs(H), device=step.dev)
         for d in step.devices:
             _lib.call("sg_gat_bwd_dst", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(keep["z"]),
                       _lib.ptr(keep["alpha"]), _lib.ptr(keep["pre_e"]), _lib.ptr(dnc), _lib.ptr(dnc_recv),
@@ -136,8 +141,8 @@ def gat_backward(step):
             if step.meta is not None:
                 step.wire_bytes += int(step.meta.npairs[l]) * 4 * H
         d_z = _f32(nVp, dout, device=step.dev)
-        dsb = _f32(nVp, H, device=step.dev)
-        dt_tot = _f32(nV, H, device=step.dev)
+        dsb = _f32(nVp, *_hs(H), device=step.dev)
+        dt_tot = _f32(nV, *_hs(H), device=step.dev)
         for d in step.devices:
             perm, beg, end = csr[d][:3]
             _lib.call("sg_gat_bwd_src", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(perm), _lib.ptr(beg),

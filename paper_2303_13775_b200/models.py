@@ -95,9 +95,12 @@ class ModelParams:
                    np.array(params.b_cls, dtype=np.float64), float(params.leaky_slope))
 
 
-def init_params(kind, feat_dim, hidden, num_classes, num_layers, seed=0, leaky_slope=0.2):
+def init_params(kind, feat_dim, hidden, num_classes, num_layers, seed=0, leaky_slope=0.2, heads=1):
     """Glorot-uniform weights, zero biases, reference draw order
-    (models.py:107-142)."""
+    (models.py:107-142). GAT with heads > 1 (not in the reference)
+    draws each head as a reference single-head layer, in head order, and
+    concatenates: W = [W_1 | ... | W_H] (d_in x H*hidden), a_src / a_dst
+    (H x hidden); the next layer's input width is H*hidden."""
     if kind not in MODEL_KINDS:
         raise ValueError(f"unknown model kind {kind!r}")
     if num_layers < 1:
@@ -108,16 +111,26 @@ def init_params(kind, feat_dim, hidden, num_classes, num_layers, seed=0, leaky_s
         lim = np.sqrt(6.0 / (fi + fo))
         return rng.uniform(-lim, lim, size=shape)
 
+    if heads < 1 or (heads > 1 and kind != "gat"):
+        raise ValueError("heads > 1 is only defined for GAT")
     layers = []
+    width = hidden * heads
     for i in range(num_layers):
-        d_in = feat_dim if i == 0 else hidden
+        d_in = feat_dim if i == 0 else width
         if kind == "graphsage":
             layers.append(SageLayer(glorot(d_in, hidden, (d_in, hidden)),
                                     glorot(d_in, hidden, (d_in, hidden)), np.zeros(hidden)))
-        else:
+        elif heads == 1:
             layers.append(GatLayer(glorot(d_in, hidden, (d_in, hidden)),
                                    glorot(hidden, 1, (hidden,)), glorot(hidden, 1, (hidden,))))
-    w_cls = glorot(hidden, num_classes, (hidden, num_classes))
+        else:
+            ws, as_, ad = [], [], []
+            for _ in range(heads):
+                ws.append(glorot(d_in, hidden, (d_in, hidden)))
+                as_.append(glorot(hidden, 1, (hidden,)))
+                ad.append(glorot(hidden, 1, (hidden,)))
+            layers.append(GatLayer(np.concatenate(ws, axis=1), np.stack(as_), np.stack(ad), heads))
+    w_cls = glorot(width, num_classes, (width, num_classes))
     return ModelParams(kind, layers, w_cls, np.zeros(num_classes), leaky_slope)
 
 
@@ -153,6 +166,13 @@ class DeviceParams:
         s = self.shapes[self.names.index(f"layer{i}.w_self" if self.kind == "graphsage" else f"layer{i}.w")]
         return int(s[0]), int(s[1])
 
+    def heads_of(self, i):
+        """GAT heads of layer i (a_src is (heads, d_head) for heads > 1)."""
+        if self.kind != "gat":
+            return 1
+        s = self.shapes[self.names.index(f"layer{i}.a_src")]
+        return int(s[0]) if len(s) == 2 else 1
+
     @property
     def num_classes(self):
         return int(self.shapes[self.names.index("cls.w")][1])
@@ -173,6 +193,6 @@ class DeviceParams:
             layers = [SageLayer(d[f"layer{i}.w_self"], d[f"layer{i}.w_neigh"], d[f"layer{i}.bias"])
                       for i in range(L)]
         else:
-            layers = [GatLayer(d[f"layer{i}.w"], d[f"layer{i}.a_src"], d[f"layer{i}.a_dst"])
-                      for i in range(L)]
+            layers = [GatLayer(d[f"layer{i}.w"], d[f"layer{i}.a_src"], d[f"layer{i}.a_dst"],
+                               self.heads_of(i)) for i in range(L)]
         return ModelParams(self.kind, layers, d["cls.w"], d["cls.b"], self.leaky_slope)

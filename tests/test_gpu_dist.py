@@ -62,7 +62,17 @@ def test_rank_local_path_two_processes(kind):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in procs], key=lambda r: r[0])
+    import queue
+    import time
+    res, t0 = [], time.time()
+    while len(res) < len(procs):
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [p for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"a rank failed (exit codes {[p.exitcode for p in procs]})"
+            assert time.time() - t0 < 300, "ranks timed out"
+    res = sorted(res, key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
     (_, l0, p0), (_, l1, p1) = res
