@@ -31,7 +31,23 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# ogbn-products shape
+# Workloads (BASELINE.json configs, SURVEY §8 shapes). C2 is the headline.
+CONFIGS = {
+    "c2": dict(kind="graphsage", heads=1, n=2_449_029, m=61_859_140, feat=100, classes=47,
+               train_frac=0.0803, p_local=0.92,
+               desc="C2 GraphSAGE-3L mean, products-shape synthetic power-law (2.45M nodes / "
+                    "61.9M edges, F=100, 47 classes)"),
+    "c3": dict(kind="gat", heads=4, n=2_449_029, m=61_859_140, feat=100, classes=47,
+               train_frac=0.0803, p_local=0.92,
+               desc="C3 GAT-3L 4 heads x 16 (concat), products-shape synthetic power-law "
+                    "(2.45M nodes / 61.9M edges, F=100, 47 classes)"),
+    "c4": dict(kind="graphsage", heads=1, n=111_059_956, m=1_615_685_872, feat=128, classes=172,
+               train_frac=0.0109, p_local=0.95,
+               desc="C4 GraphSAGE-3L mean, papers100M-shape synthetic power-law (111M nodes / "
+                    "1.62B edges, F=128, 172 classes), whole feature table resident"),
+}
+CFG_NAME = "c2"
+KIND, HEADS = "graphsage", 1
 N_NODES = 2_449_029
 N_EDGES = 61_859_140
 FEAT = 100
@@ -40,8 +56,18 @@ HIDDEN = 16
 FANOUTS = [15, 10, 5]
 BATCH = 1024
 TRAIN_FRAC = 0.0803
+P_LOCAL = 0.92
+DESC = CONFIGS["c2"]["desc"]
 LR = 0.1
 GRAPH_SEED, FEAT_SEED, LABEL_SEED, TRAIN_SEED, RUN_SEED = 0, 1, 2, 3, 0
+
+
+def select_config(name):
+    global CFG_NAME, KIND, HEADS, N_NODES, N_EDGES, FEAT, CLASSES, TRAIN_FRAC, P_LOCAL, DESC
+    c = CONFIGS[name]
+    CFG_NAME, KIND, HEADS = name, c["kind"], c["heads"]
+    N_NODES, N_EDGES, FEAT, CLASSES = c["n"], c["m"], c["feat"], c["classes"]
+    TRAIN_FRAC, P_LOCAL, DESC = c["train_frac"], c["p_local"], c["desc"]
 
 
 def parse():
@@ -53,13 +79,14 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/baseline)")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     return ap.parse_args()
 
 
 def build_workload(threads):
     import paper_2303_13775_b200 as sg
     t = time.time()
-    graph = sg.generate_powerlaw(N_NODES, N_EDGES, blocks=64, p_local=0.92, gamma=2.1,
+    graph = sg.generate_powerlaw(N_NODES, N_EDGES, blocks=64, p_local=P_LOCAL, gamma=2.1,
                                  seed=GRAPH_SEED, threads=threads)
     labels = sg.synthetic_labels(N_NODES, CLASSES, LABEL_SEED)
     perm = np.random.default_rng(TRAIN_SEED).permutation(N_NODES)
@@ -138,6 +165,13 @@ def sage_fused_fwd_bytes(E, R, w, dout):
     return 4 * w * E + 4 * E + 4 * (R + 1) + 4 * w * R + 4 * (2 * w + 1 + dout) * R
 
 
+def gat_agg_bytes(E, R, dh, H):
+    """SURVEY §8(d) GAT forward scores+softmax+aggregation bytes, per head:
+    E*20 (src/dst index, s_src, t_dst, e) + E*(12 + 4 dh) (e, index, alpha, z
+    row) + R*(4 dh + 8) (num, m, den)."""
+    return H * (20 * E + (12 + 4 * dh) * E + (4 * dh + 8) * R)
+
+
 def cpu_baseline(graph, labels, samples, pm_assign, g, n_iter=2):
     """Reference algorithm (oracle NumPy port) on this host, 1 thread, on the
     first n_iter samples of the same workload: split + forward + backward +
@@ -148,7 +182,13 @@ def cpu_baseline(graph, labels, samples, pm_assign, g, n_iter=2):
     from oracle.coop_oracle import CoopRun, reduce_and_sgd
     from oracle.model_oracle import glorot_params
     from oracle.split_oracle import split_sample
-    params = glorot_params("graphsage", FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED)
+    if KIND == "gat" and HEADS > 1:
+        from oracle.multihead_oracle import multihead_run
+        params = {k: np.asarray(v, dtype=np.float64) for k, v in
+                  sg.init_params("gat", FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED,
+                                 heads=HEADS).tensors().items()}
+    else:
+        params = glorot_params(KIND, FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED)
     edges = 0
     t_total = 0.0
     with threadpool_limits(limits=1):
@@ -163,8 +203,12 @@ def cpu_baseline(graph, labels, samples, pm_assign, g, n_iter=2):
             lab = np.asarray(labels, dtype=np.int64)[uniq]
             t0 = time.perf_counter()
             splits, plan = split_sample(Vc, Ec, asn, g, None)
-            run = CoopRun(params, splits, plan, X, lab)
-            _, grads = run.run()
+            if KIND == "gat" and HEADS > 1:  # per-head composition of the reference layer (g=1)
+                _, gr, _ = multihead_run(Vc, Ec, params, X, lab, HEADS)
+                grads = [gr]
+            else:
+                run = CoopRun(params, splits, plan, X, lab)
+                _, grads = run.run()
             reduce_and_sgd(params, grads, LR, len(V[-1]))
             t_total += time.perf_counter() - t0
             edges += smp.total_edges
@@ -175,6 +219,7 @@ def run_reference_arm(args, rank, world):
     import torch  # noqa: F401
     if rank != 0:
         return
+    select_config(args.config)
     threads = os.cpu_count() or 1
     graph, labels, train, _ = build_workload(threads)
     samples, _ = make_samples(graph, train, args.warmup + args.steps, args.batch, threads)
@@ -206,6 +251,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
+    select_config(args.config)
 
     import torch
     import torch.distributed as dist
@@ -229,7 +275,7 @@ def main():
     labels_dev = torch.from_numpy(labels).to(dev)
     n_steps = args.warmup + args.steps
     samples, iters_per_epoch = make_samples(graph, train, n_steps, args.batch, threads)
-    params = sg.init_params("graphsage", FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED)
+    params = sg.init_params(KIND, FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED, heads=HEADS)
     dp = sg.DeviceParams.from_host(params, dev)
     transport = sg.NcclTransport(rank, world) if g > 1 else sg.LocalTransport()
     # device-resident inputs
@@ -398,7 +444,10 @@ def main():
         # dominant kernel: layer-1 SpMM (agg) of this rank's split
         E1 = np.mean([samples[i].sizes()[1][0] for i in range(args.warmup, n_steps)]) / g
         R1 = np.mean([samples[i].sizes()[0][1] for i in range(args.warmup, n_steps)]) / g
-        alg = sage_fused_fwd_bytes(E1, R1, FEAT, HIDDEN) if g == 1 else sage_fwd_bytes(E1, R1, FEAT)
+        if KIND == "gat":
+            alg = gat_agg_bytes(E1, R1, HIDDEN, HEADS)
+        else:
+            alg = sage_fused_fwd_bytes(E1, R1, FEAT, HIDDEN) if g == 1 else sage_fwd_bytes(E1, R1, FEAT)
         agg_avg = float(np.mean(agg_ms))
         achieved = alg / (agg_avg / 1e3) / 1e9
         traffic = None
@@ -419,19 +468,20 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": my_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": "C2 GraphSAGE-3L mean, products-shape synthetic power-law "
-                                   "(2.45M nodes / 61.9M edges, F=100, 47 classes), batch "
-                                   f"{args.batch}, fanout {FANOUTS}, hidden 16, split parts g={g}, "
+            "config": {"workload": f"{DESC}, batch {args.batch}, fanout {FANOUTS}, hidden 16, split parts g={g}, "
                                    "range partition, full feature cache",
-                       "model": "graphsage-3l-h16", "global_batch": args.batch, "seq_len": None,
+                       "config_id": CFG_NAME,
+                       "model": f"{KIND}-3l-h16" + (f"x{HEADS}" if HEADS > 1 else ""),
+                       "global_batch": args.batch, "seq_len": None,
                        "parallelism": f"split{g}", "l2": "flushed between timed steps (256 MB write, "
                                                           "outside the per-step events)",
                        "epoch_iterations": iters_per_epoch,
                        "epoch_time_s": iters_per_epoch * my_ms / args.steps / 1e3,
                        "edges_per_step": edges / args.steps, "graph_gen_s": round(gen_s, 1),
                        "sample_sizes_first": {"V": nV, "E": nE}},
-            "roofline": {"bound": "hbm", "kernel": ("k_sage_fused<32,1,16> layer 1 (SpMM + update, F=100)" if g == 1
-                                                    else "k_sage_agg<4,32,1,1> layer 1 (F=100)"),
+            "roofline": {"bound": "hbm", "kernel": (f"k_gat_agg layer 1 (online softmax, {HEADS} heads)" if KIND == "gat"
+                                                    else f"k_sage_agg_mean + k_sage_linear layer 1 (F={FEAT})" if g == 1
+                                                    else f"k_sage_agg layer 1 (F={FEAT})"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg, "avg_launch_ms": agg_avg,
