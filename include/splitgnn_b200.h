@@ -336,6 +336,20 @@ int sg_sampler_run(void* h, const int64_t* targets, int64_t n_targets, const int
                    int64_t* nE_out /* L */);
 int sg_sampler_fetch(void* h, int32_t* V /* sum nV */, int32_t* esrc, int32_t* edst);
 
+/* Host->device input pipeline for the captured step; replaces the
+ * reference's synchronous per-iteration input load (engine.py:760-790,
+ * _load_inputs) with a double-buffered one: sg_pipe_stage copies a pinned
+ * packed sample into staging slot `slot` on an internal copy stream (after
+ * that slot's previous consumer), then, ordered on `stream`, into the graph's
+ * input buffer dev_dst; sg_pipe_finish queues the D2H of the step's loss on
+ * `stream`; sg_pipe_wait blocks until it has landed and returns it. */
+void* sg_pipe_create(int64_t bytes);
+void sg_pipe_destroy(void* h);
+int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,
+                  void* stream);
+int sg_pipe_finish(void* h, int32_t slot, const float* dev_loss, void* stream);
+int sg_pipe_wait(void* h, int32_t slot, float* loss_out);
+
 #ifdef __cplusplus
 }
 #endif

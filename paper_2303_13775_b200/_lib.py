@@ -119,6 +119,11 @@ _SIGS = {
     "sg_sampler_destroy": (None, [vp]),
     "sg_sampler_run": (i32, [vp, vp, i64, vp, i32, u64, i32, vp, vp]),
     "sg_sampler_fetch": (i32, [vp, vp, vp, vp]),
+    "sg_pipe_create": (vp, [i64]),
+    "sg_pipe_destroy": (None, [vp]),
+    "sg_pipe_stage": (i32, [vp, i32, vp, i64, vp, vp]),
+    "sg_pipe_finish": (i32, [vp, i32, vp, vp]),
+    "sg_pipe_wait": (i32, [vp, i32, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

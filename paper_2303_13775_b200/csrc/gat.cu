@@ -171,6 +171,118 @@ __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ 
   }
 }
 
+// TM = 32 rows per tile; NT = 8 * NQ register tiles (4 rows x 4 outputs),
+// NS = 256 / NT K-slices (NQ <= 32 -> D <= 128).
+template <int NQ>
+__global__ void __launch_bounds__(256) k_gat_project_tiled(const SgMeta* __restrict__ meta, ProjArgs a) {
+  constexpr int TM = 32, TMP = TM + 4;
+  constexpr int NT = (TM / 4) * NQ;
+  constexpr int NS = 256 / NT;
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, D = a.dout, H = a.heads, dh = D / H;
+  float* W_s = smem;               // [w][D]
+  float* A_s = W_s + w * D;        // [w][TM+4] transposed
+  float* red = A_s + w * TMP;      // [NS][TM][D]
+  int* prow = (int*)(red + NS * TM * D);
+  for (int i = threadIdx.x; i < w * D / 4; i += 256)
+    reinterpret_cast<float4*>(W_s)[i] = reinterpret_cast<const float4*>(a.W)[i];
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d];
+  const int ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int tile = threadIdx.x % NT, ks = threadIdx.x / NT;
+  const int rt = tile / NQ, jq = tile - rt * NQ;
+  const int kchunk = (w + NS - 1) / NS;
+  const int kb = ks * kchunk, ke = min(w, kb + kchunk);
+  const int w4 = w / 4;
+  for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
+    __syncthreads();
+    if (threadIdx.x < TM) {
+      const int r = r0 + threadIdx.x;
+      int pr = -1;
+      if (r < n) {
+        pr = own0 + r;
+        if (a.src_row) pr = a.src_row[pr];
+      }
+      prow[threadIdx.x] = pr;
+    }
+    __syncthreads();
+    {
+      constexpr int MA = 4;  // TM * w4 / 256 <= 4 for w <= 128
+      float4 ab[MA];
+#pragma unroll
+      for (int u = 0; u < MA; ++u) {
+        const int idx = threadIdx.x + 256 * u;
+        ab[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (idx < TM * w4) {
+          const int r = idx & (TM - 1), q = idx / TM;
+          if (prow[r] >= 0) ab[u] = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)prow[r] * w) + q);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < MA; ++u) {
+        const int idx = threadIdx.x + 256 * u;
+        if (idx < TM * w4) {
+          const int r = idx & (TM - 1), q = idx / TM;
+          A_s[(4 * q + 0) * TMP + r] = ab[u].x;
+          A_s[(4 * q + 1) * TMP + r] = ab[u].y;
+          A_s[(4 * q + 2) * TMP + r] = ab[u].z;
+          A_s[(4 * q + 3) * TMP + r] = ab[u].w;
+        }
+      }
+    }
+    __syncthreads();
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      const float4 av = *reinterpret_cast<const float4*>(A_s + k * TMP + 4 * rt);
+      const float4 wv = *reinterpret_cast<const float4*>(W_s + k * D + 4 * jq);
+      const float ar[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] = fmaf(ar[i], wv.x, acc[i][0]);
+        acc[i][1] = fmaf(ar[i], wv.y, acc[i][1]);
+        acc[i][2] = fmaf(ar[i], wv.z, acc[i][2]);
+        acc[i][3] = fmaf(ar[i], wv.w, acc[i][3]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<float4*>(red + (ks * TM + 4 * rt + i) * D + 4 * jq) =
+          make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    __syncthreads();
+    // z = sum of the K slices (fixed order); slice 0 keeps the total for the epilogue
+    for (int idx = threadIdx.x; idx < TM * D; idx += 256) {
+      const int r = idx / D, j = idx - r * D;
+      float v = 0.f;
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) v += red[(s2 * TM + r) * D + j];
+      red[r * D + j] = v;
+      if (r0 + r < n) a.z[(int64_t)(own0 + r0 + r) * D + j] = v;
+    }
+    __syncthreads();
+    // scores s = z.a_src per head; t = z.a_dst on self rows
+    for (int idx = threadIdx.x; idx < TM * H; idx += 256) {
+      const int r = idx / H, hh = idx - r * H;
+      if (r0 + r >= n) continue;
+      const int G = own0 + r0 + r;
+      const float* zr = red + r * D + hh * dh;
+      float sv = 0.f;
+      for (int j = 0; j < dh; ++j) sv = fmaf(zr[j], a.a_src[hh * dh + j], sv);
+      a.s[(int64_t)G * H + hh] = sv;
+      const int p = a.grouped[a.voff_lm1 + G];
+      if (p < nVl) {
+        float tv = 0.f;
+        for (int j = 0; j < dh; ++j) tv = fmaf(zr[j], a.a_dst[hh * dh + j], tv);
+        a.t[(int64_t)(ownl + a.rank[a.voff_l + p]) * H + hh] = tv;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- online-softmax aggregation
 struct AggArgs {
   int l, d, dout, heads, stride;
@@ -572,12 +684,17 @@ struct BParamArgs {
   float* d_prev;
 };
 
+// T4 (w % 4 == 0 and dout % 4 == 0): thread slot (cg, jg) owns a 4x4 dW tile,
+// per row 2 LDS.128 + 16 FFMA; otherwise one scalar slot per (c, j).
+template <bool T4>
 __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict__ meta, BParamArgs a) {
   extern __shared__ __align__(16) float smem[];
-  const int w = a.w, dout = a.dout, wp = w + 1, wst = dout + 4, H = a.heads, dh = dout / H;
+  const int w = a.w, dout = a.dout, H = a.heads, dh = dout / H;
+  const int wp = T4 ? w + 4 : w + 1;  // h row stride (float4-aligned for T4)
+  const int wt = w + 1;               // W^T row stride (d_prev: lanes run along c)
   float* dz_s = smem;               // [QTR][dout]
-  float* W_s = dz_s + QTR * dout;   // [w][dout+4] (for d_prev)
-  float* h_s = W_s + w * wst;       // [QTR][w+1]
+  float* Wt_s = dz_s + QTR * dout;  // [dout][w+1] = W^T (for d_prev)
+  float* h_s = Wt_s + dout * wt;    // [QTR][wp]
   float* z_s = h_s + QTR * wp;      // [QTR][dout]
   float* ds_s = z_s + QTR * dout;   // [QTR][H]
   float* dt_s = ds_s + QTR * H;     // [QTR][H] (0 when not a self row)
@@ -585,14 +702,15 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
   if (a.d_prev)
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
-      W_s[c * wst + j] = a.W[i];
+      Wt_s[j * wt + c] = a.W[i];
     }
   const int l = a.l, d = a.d;
   const int n = meta->n_own[l - 1][d];
   const int own0 = meta->own_off[l - 1][d];
   const int ownl = meta->own_off[l][d];
   const int64_t nVl = meta->nV[l];
-  const int nslots = w * dout;  // scalar slots: idx -> (c, j)
+  const int nslots = T4 ? (w / 4) * (dout / 4) : w * dout;
+  const int nq = dout / 4;
   float acc[QMAXQ * 4];
 #pragma unroll
   for (int k = 0; k < QMAXQ * 4; ++k) acc[k] = 0.f;
@@ -623,29 +741,77 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
       ds_s[idx] = dsv;
       dt_s[idx] = dtv;
     }
-    for (int idx = threadIdx.x; idx < QTR * dout; idx += blockDim.x) {
-      const int rr = idx / dout;
-      const bool v = rr < nrow;
-      const int64_t G = own0 + tile * QTR + rr;
-      dz_s[idx] = v ? a.d_z[G * dout + (idx - rr * dout)] : 0.f;
-      z_s[idx] = v ? a.z[G * dout + (idx - rr * dout)] : 0.f;
+    if (T4) {
+      for (int idx = threadIdx.x; idx < QTR * nq; idx += blockDim.x) {
+        const int rr = idx / nq, q = idx - rr * nq;
+        float4 vz = make_float4(0.f, 0.f, 0.f, 0.f), vd = vz;
+        if (rr < nrow) {
+          const int64_t G = own0 + tile * QTR + rr;
+          vd = *reinterpret_cast<const float4*>(a.d_z + G * dout + 4 * q);
+          vz = *reinterpret_cast<const float4*>(a.z + G * dout + 4 * q);
+        }
+        *reinterpret_cast<float4*>(dz_s + rr * dout + 4 * q) = vd;
+        *reinterpret_cast<float4*>(z_s + rr * dout + 4 * q) = vz;
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < QTR * dout; idx += blockDim.x) {
+        const int rr = idx / dout;
+        const bool v = rr < nrow;
+        const int64_t G = own0 + tile * QTR + rr;
+        dz_s[idx] = v ? a.d_z[G * dout + (idx - rr * dout)] : 0.f;
+        z_s[idx] = v ? a.z[G * dout + (idx - rr * dout)] : 0.f;
+      }
     }
     __syncthreads();
+    if (T4) {
+      const int w4 = w / 4;
+      for (int idx = threadIdx.x; idx < QTR * w4; idx += blockDim.x) {
+        const int rr = idx / w4, q = idx - rr * w4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (prow_s[rr] >= 0) v = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)prow_s[rr] * w) + q);
+        *reinterpret_cast<float4*>(h_s + rr * wp + 4 * q) = v;
+      }
+    } else {
 #pragma unroll 4
-    for (int idx = threadIdx.x; idx < QTR * w; idx += blockDim.x) {
-      const int rr = idx / w, c = idx - rr * w;
-      h_s[rr * wp + c] = prow_s[rr] >= 0 ? __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c) : 0.f;
+      for (int idx = threadIdx.x; idx < QTR * w; idx += blockDim.x) {
+        const int rr = idx / w, c = idx - rr * w;
+        h_s[rr * wp + c] = prow_s[rr] >= 0 ? __ldg(a.h_prev + (int64_t)prow_s[rr] * w + c) : 0.f;
+      }
     }
     __syncthreads();
+    if (T4) {
 #pragma unroll
-    for (int k = 0; k < QMAXQ * 4; ++k) {
-      const int idx = threadIdx.x + 256 * k;
-      if (idx < nslots) {
-        const int c = idx / dout, j = idx - c * dout;
-        float sacc = acc[k];
+      for (int s2 = 0; s2 < QMAXQ / 4 * 2; ++s2) {  // up to 4 tiles of 16 per thread
+        const int slot = threadIdx.x + 256 * s2;
+        if (s2 < 2 && slot < nslots) {
+          const int cg = slot / nq, jg = slot - cg * nq;
+          float* t = acc + 16 * s2;
+#pragma unroll 4
+          for (int rr = 0; rr < QTR; ++rr) {
+            const float4 a4 = *reinterpret_cast<const float4*>(h_s + rr * wp + 4 * cg);
+            const float4 g4 = *reinterpret_cast<const float4*>(dz_s + rr * dout + 4 * jg);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              t[4 * i + 0] = fmaf(av[i], g4.x, t[4 * i + 0]);
+              t[4 * i + 1] = fmaf(av[i], g4.y, t[4 * i + 1]);
+              t[4 * i + 2] = fmaf(av[i], g4.z, t[4 * i + 2]);
+              t[4 * i + 3] = fmaf(av[i], g4.w, t[4 * i + 3]);
+            }
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < QMAXQ * 4; ++k) {
+        const int idx = threadIdx.x + 256 * k;
+        if (idx < nslots) {
+          const int c = idx / dout, j = idx - c * dout;
+          float sacc = acc[k];
 #pragma unroll 8
-        for (int rr = 0; rr < QTR; ++rr) sacc = fmaf(h_s[rr * wp + c], dz_s[rr * dout + j], sacc);
-        acc[k] = sacc;
+          for (int rr = 0; rr < QTR; ++rr) sacc = fmaf(h_s[rr * wp + c], dz_s[rr * dout + j], sacc);
+          acc[k] = sacc;
+        }
       }
     }
     if (threadIdx.x < dout) {
@@ -659,21 +825,38 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
       for (int idx = threadIdx.x; idx < nrow * w; idx += blockDim.x) {
         const int rr = idx / w, c = idx - rr * w;
         float sacc = 0.f;
-        for (int j = 0; j < dout; ++j) sacc = fmaf(dz_s[rr * dout + j], W_s[c * wst + j], sacc);
+        const float* dzr = dz_s + rr * dout;
+#pragma unroll 8
+        for (int j = 0; j < dout; ++j) sacc = fmaf(dzr[j], Wt_s[j * wt + c], sacc);
         a.d_prev[(int64_t)(own0 + tile * QTR + rr) * w + c] = sacc;
       }
     }
   }
-  const int64_t ntot = (int64_t)nslots + 2 * dout;
+  const int64_t ntot = (int64_t)w * dout + 2 * dout;
   float* out = a.partial + (int64_t)blockIdx.x * ntot;
+  if (T4) {
 #pragma unroll
-  for (int k = 0; k < QMAXQ * 4; ++k) {
-    const int idx = threadIdx.x + 256 * k;
-    if (idx < nslots) out[idx] = acc[k];
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int slot = threadIdx.x + 256 * s2;
+      if (slot < nslots) {
+        const int cg = slot / nq, jg = slot - cg * nq;
+        const float* t = acc + 16 * s2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          *reinterpret_cast<float4*>(out + (4 * cg + i) * dout + 4 * jg) =
+              make_float4(t[4 * i + 0], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < QMAXQ * 4; ++k) {
+      const int idx = threadIdx.x + 256 * k;
+      if (idx < nslots) out[idx] = acc[k];
+    }
   }
   if (threadIdx.x < dout) {
-    out[nslots + threadIdx.x] = as;
-    out[nslots + dout + threadIdx.x] = ad;
+    out[(int64_t)w * dout + threadIdx.x] = as;
+    out[(int64_t)w * dout + dout + threadIdx.x] = ad;
   }
 }
 
@@ -748,6 +931,26 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
   const size_t smem = sizeof(float) * ((size_t)w * dout + (size_t)PTR * (w + 1) + (size_t)PTR * (dout + 1) + PTR);
   SG_REQUIRE(smem <= 227 * 1024, "gat_project: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
+  const int nq = dout / 4;
+  if (w % 4 == 0 && w <= 128 && dout % 4 == 0 && nq <= 32 && (nq & (nq - 1)) == 0) {
+    // register-tiled path: 4x4 tiles, K split over slices (TM = 32 rows per tile)
+    const int NS = 256 / (8 * nq);
+    const size_t smem_t = sizeof(float) * ((size_t)w * dout + (size_t)w * 36 + (size_t)NS * 32 * dout) + 32 * 4;
+    const int grid_t = clamp_grid(div_up(max_rows, 32), kSMs * 8);
+    cudaError_t attr = cudaSuccess;
+    switch (nq) {
+#define GP_CASE(Q)                                                   \
+  case Q:                                                            \
+    attr = allow_max_smem<k_gat_project_tiled<Q>>();                 \
+    SG_CUDA(attr);                                                   \
+    k_gat_project_tiled<Q><<<grid_t, 256, smem_t, st>>>(meta, a);    \
+    break;
+      GP_CASE(1) GP_CASE(2) GP_CASE(4) GP_CASE(8) GP_CASE(16) GP_CASE(32)
+#undef GP_CASE
+    }
+    SG_CHECK_LAUNCH("k_gat_project_tiled");
+    return SG_OK;
+  }
   const int grid = clamp_grid(div_up(max_rows, PTR), kSMs * 4);
   if (dout % 4 == 0) {
     SG_CUDA(allow_max_smem<k_gat_project<true>>());
@@ -916,12 +1119,19 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
   a.voff_lm1 = y.voff[l - 1]; a.voff_l = y.voff[l];
   a.h_prev = h_prev; a.src_row = src_row; a.grouped = I32p(y.o_grouped); a.rank = I32p(y.o_rank);
   a.z = z; a.d_z = d_z; a.ds = ds; a.dt_tot = dt_tot; a.W = W; a.partial = partial; a.d_prev = d_prev;
-  const size_t smem = sizeof(float) * (2 * (size_t)QTR * dout + (size_t)w * (dout + 4) +
-                                       (size_t)QTR * (w + 1) + 2 * (size_t)QTR * heads + QTR);
+  // T4 tiles: (w/4)*(dout/4) <= 512 slots (2 tiles of 16 per thread)
+  const bool t4 = w % 4 == 0 && dout % 4 == 0 && (w / 4) * (dout / 4) <= 512;
+  const size_t smem = sizeof(float) * (2 * (size_t)QTR * dout + (size_t)dout * (w + 1) +
+                                       (size_t)QTR * (w + 4) + 2 * (size_t)QTR * heads + QTR);
   SG_REQUIRE(smem <= 227 * 1024, "gat_bwd_param: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
-  SG_CUDA(allow_max_smem<k_gat_bwd_param>());
-  k_gat_bwd_param<<<nblocks, 256, smem, st>>>(meta, a);
+  if (t4) {
+    SG_CUDA(allow_max_smem<k_gat_bwd_param<true>>());
+    k_gat_bwd_param<true><<<nblocks, 256, smem, st>>>(meta, a);
+  } else {
+    SG_CUDA(allow_max_smem<k_gat_bwd_param<false>>());
+    k_gat_bwd_param<false><<<nblocks, 256, smem, st>>>(meta, a);
+  }
   SG_CHECK_LAUNCH("k_gat_bwd_param");
   return SG_OK;
 }

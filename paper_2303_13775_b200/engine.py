@@ -15,6 +15,8 @@ Trainer / train_model (:655-870).
 
 from __future__ import annotations
 
+import ctypes
+
 import time
 
 import numpy as np
@@ -732,7 +734,9 @@ class StaticSample:
 
     Layer l's vertices live at the capacity offset voff[l]; the actual sizes
     go to a small device array the kernels read, so one captured graph serves
-    every sample that fits the capacities."""
+    every sample that fits the capacities. All inputs are views of ONE int32
+    buffer [sizes (int64) | V | esrc | edst], so a sample crosses PCIe as one
+    contiguous prefix copy."""
 
     def __init__(self, cap_nV, cap_nE, device):
         self.cap_nV = [int(x) for x in cap_nV]
@@ -740,45 +744,66 @@ class StaticSample:
         self.L = len(self.cap_nE)
         self.voff = np.r_[0, np.cumsum(self.cap_nV)].astype(np.int64)
         self.eoff = np.r_[0, np.cumsum(self.cap_nE)].astype(np.int64)
+        VC, EC = int(self.voff[-1]), max(int(self.eoff[-1]), 1)
+        S = 2 * (2 * self.L + 1)
+        self.o_V, self.o_es, self.o_ed = S, S + VC, S + VC + EC
+        self.words = S + VC + 2 * EC
         dev = torch.device(device)
-        self.V = torch.zeros(int(self.voff[-1]), dtype=torch.int32, device=dev)
-        self.es = torch.zeros(max(int(self.eoff[-1]), 1), dtype=torch.int32, device=dev)
-        self.ed = torch.zeros(max(int(self.eoff[-1]), 1), dtype=torch.int32, device=dev)
-        self.sizes = torch.zeros(2 * self.L + 1, dtype=torch.int64, device=dev)
-        self.hV = torch.zeros(self.V.shape, dtype=torch.int32).pin_memory()
-        self.hes = torch.zeros(self.es.shape, dtype=torch.int32).pin_memory()
-        self.hed = torch.zeros(self.ed.shape, dtype=torch.int32).pin_memory()
-        self.hsizes = torch.zeros(self.sizes.shape, dtype=torch.int64).pin_memory()
+        self.buf = torch.zeros(self.words, dtype=torch.int32, device=dev)
+        self.sizes = self.buf[:S].view(torch.int64)
+        self.V = self.buf[self.o_V:self.o_V + VC]
+        self.es = self.buf[self.o_es:self.o_es + EC]
+        self.ed = self.buf[self.o_ed:self.o_ed + EC]
+        self.hbuf = None
         self.bytes_h2d = 0
 
     def fits(self, sample):
         nV, nE = sample.sizes()
         return all(a <= b for a, b in zip(nV, self.cap_nV)) and all(a <= b for a, b in zip(nE, self.cap_nE))
 
-    def load(self, sample):
-        """Stage the sample into pinned memory and copy it to the device
-        buffers (async, on the current stream)."""
+    def pack(self, sample, out=None):
+        """Write `sample` in this layout into a host int32 array; returns the
+        number of words used (the prefix that has to cross PCIe)."""
         if not self.fits(sample):
             raise ValueError("sample exceeds the captured capacities")
         if not sample.is_dst_grouped():
             raise ValueError("captured steps need destination-grouped samples")
-        hV, hes, hed = self.hV.numpy(), self.hes.numpy(), self.hed.numpy()
         nV, nE = sample.sizes()
+        used = self.o_ed + int(self.eoff[self.L - 1] + nE[self.L - 1])
+        if out is None:
+            out = np.zeros(used, dtype=np.int32)
+        out[:self.o_V].view(np.int64)[:] = list(nV) + list(nE)
         for l, v in enumerate(sample.layer_vertices):
-            hV[self.voff[l]:self.voff[l] + nV[l]] = v
-        for l, (s, d) in enumerate(sample.layer_edges):
-            hes[self.eoff[l]:self.eoff[l] + nE[l]] = s
-            hed[self.eoff[l]:self.eoff[l] + nE[l]] = d
-        self.hsizes.numpy()[:] = list(nV) + list(nE)
-        # only the used prefix of each buffer crosses PCIe
-        nv_used = int(self.voff[self.L] + nV[self.L])
-        ne_used = int(self.eoff[self.L - 1] + nE[self.L - 1])
-        self.V[:nv_used].copy_(self.hV[:nv_used], non_blocking=True)
-        self.es[:ne_used].copy_(self.hes[:ne_used], non_blocking=True)
-        self.ed[:ne_used].copy_(self.hed[:ne_used], non_blocking=True)
-        self.sizes.copy_(self.hsizes, non_blocking=True)
-        self.bytes_h2d = 4 * nv_used + 8 * ne_used + 8 * self.sizes.numel()
+            o = self.o_V + self.voff[l]
+            out[o:o + nV[l]] = v
+        for l, (a, b) in enumerate(sample.layer_edges):
+            o = self.eoff[l]
+            out[self.o_es + o:self.o_es + o + nE[l]] = a
+            out[self.o_ed + o:self.o_ed + o + nE[l]] = b
+        return used
+
+    def load(self, sample):
+        """Stage the sample into pinned memory and copy it to the device
+        buffer (async, on the current stream)."""
+        if self.hbuf is None:
+            self.hbuf = torch.zeros(self.words, dtype=torch.int32).pin_memory()
+        used = self.pack(sample, self.hbuf.numpy())
+        self.buf[:used].copy_(self.hbuf[:used], non_blocking=True)
+        self.bytes_h2d = 4 * used
         return self.bytes_h2d
+
+
+class PinnedSample:
+    """One sample packed into pinned host memory in the StaticSample layout,
+    ready for a single async H2D copy. This is the form a host sampler hands
+    to the trainer."""
+
+    def __init__(self, sample, static):
+        host = np.zeros(static.words, dtype=np.int32)
+        used = static.pack(sample, host)
+        self.buf = torch.from_numpy(host[:used].copy()).pin_memory()
+        self.num_targets = len(sample.targets)
+        self.h2d_bytes = 4 * used
 
 
 def capacities_for(samples, slack=1.0):
@@ -856,6 +881,76 @@ class CapturedStep:
 
     def loss_sum(self):
         return self.out[self.p.n]
+
+    def prepare_pinned(self, samples):
+        """Pack samples into PinnedSamples and DMA each buffer once (untimed):
+        the first transfer from a freshly pinned buffer pays a one-time
+        mapping cost that a sampler's reused pinned ring never sees again."""
+        pinned = [PinnedSample(smp, self.inp) for smp in samples]
+        scratch = torch.empty(self.inp.words, dtype=torch.int32, device=self.dev)
+        for ps in pinned:
+            scratch[:ps.buf.numel()].copy_(ps.buf, non_blocking=True)
+        torch.cuda.synchronize(self.dev)
+        return pinned
+
+    def run_pipelined(self, pinned):
+        """Train on a sequence of PinnedSamples end to end: per step an async
+        H2D of the sample (native copy stream, double-buffered device
+        staging, sg_pipe_stage), an on-device copy into the graph's input
+        buffer, the graph replay and a D2H read of the step's loss sum. Step
+        i+1's H2D overlaps step i's compute; the host reads step i's loss
+        after step i+1 is queued. Returns (mean loss per step, H2D bytes,
+        D2H bytes)."""
+        lib = _lib.load()
+        if getattr(self, "_pipe", None) is None:
+            h = lib.sg_pipe_create(4 * self.inp.words)
+            if not h:
+                _lib.check(2, "sg_pipe_create")
+            self._pipe = h
+        h = self._pipe
+        st = _lib.stream_ptr()
+        dst = _lib.ptr(self.inp.buf)
+        loss_ptr = self.out.data_ptr() + 4 * self.p.n
+        out = ctypes.c_float()
+        losses, h2d, d2h = [], 0, 0
+        pending = None
+        pc = time.perf_counter
+        t_stage = t_replay = t_wait = 0.0
+        for i, ps in enumerate(pinned):
+            b = i & 1
+            t0 = pc()
+            _lib.check(lib.sg_pipe_stage(h, b, ps.buf.data_ptr(), ps.h2d_bytes, dst, st), "sg_pipe_stage")
+            t1 = pc()
+            self.graph.replay()
+            t2 = pc()
+            _lib.check(lib.sg_pipe_finish(h, b, loss_ptr, st), "sg_pipe_finish")
+            h2d += ps.h2d_bytes
+            d2h += 4
+            t3 = pc()
+            if pending is not None:
+                _lib.check(lib.sg_pipe_wait(h, pending[0], ctypes.byref(out)), "sg_pipe_wait")
+                losses.append(out.value / pending[1])
+            t4 = pc()
+            t_stage += t3 - t2 + t1 - t0
+            t_replay += t2 - t1
+            t_wait += t4 - t3
+            pending = (b, ps.num_targets)
+        n = max(len(pinned), 1)
+        self.pipe_stats = {"host_issue_us": 1e6 * t_stage / n, "host_replay_us": 1e6 * t_replay / n,
+                           "host_wait_us": 1e6 * t_wait / n}
+        if pending is not None:
+            _lib.check(lib.sg_pipe_wait(h, pending[0], ctypes.byref(out)), "sg_pipe_wait")
+            losses.append(out.value / pending[1])
+        return losses, h2d, d2h
+
+    def __del__(self):
+        h = getattr(self, "_pipe", None)
+        if h:
+            try:
+                _lib.load().sg_pipe_destroy(h)
+            except Exception:
+                pass
+            self._pipe = None
 
 
 # ---- one process per GPU ------------------------------------------------------------
