@@ -336,6 +336,30 @@ int sg_sampler_run(void* h, const int64_t* targets, int64_t n_targets, const int
                    int64_t* nE_out /* L */);
 int sg_sampler_fetch(void* h, int32_t* V /* sum nV */, int32_t* esrc, int32_t* edst);
 
+/* Load-balanced transposed SpMM (tspmm.cu): the source-row sums of the
+ * SAGE scatter backward (replaces sg_sage_scatter_bwd's row-per-warp loop;
+ * engine.py:470-520) and of the GAT source backward (sg_gat_bwd_src;
+ * engine.py:430-552), over the CSR-by-source from sg_src_csr (its sorted
+ * `keys` and values, built with first layer `lmin`). Work is split into
+ * chunks of 32 sorted edges so power-law hub rows do not serialise; rows
+ * crossing chunks are combined in chunk order (deterministic). `part` holds
+ * sg_tspmm_part_floats(max_edges, width, extra) floats (extra = heads for
+ * GAT, 0 for SAGE); max_edges bounds layer l's local edges. Widths: width +
+ * extra <= 192. */
+int64_t sg_tspmm_part_floats(int64_t max_edges, int32_t width, int32_t extra);
+int sg_sage_scatter_bwd_lb(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                           int32_t w, const float* d_self, const float* d_sums, const float* bwd_recv,
+                           int32_t recv_stride, const uint32_t* keys, const int32_t* enc,
+                           const int32_t* srcbeg, const int32_t* srcend, int64_t key_base, int32_t lmin,
+                           float* part, int64_t max_edges, float* d_prev, int64_t max_rows, void* stream);
+int sg_gat_bwd_src_lb(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d, int32_t dout,
+                      int32_t heads, const uint32_t* keys, const int32_t* perm, const int32_t* srcbeg,
+                      const int32_t* srcend, int64_t key_base, int32_t lmin, const float* alpha,
+                      const float* d_pre, const float* dnc, const float* dnc_recv, int32_t dnc_stride,
+                      const float* dt_loc, const float* dt_recv, const float* a_src, const float* a_dst,
+                      float* d_z, float* ds, float* dt_tot, float* part, int64_t max_edges,
+                      int64_t max_rows, void* stream);
+
 /* Host->device input pipeline for the captured step; replaces the
  * reference's synchronous per-iteration input load (engine.py:760-790,
  * _load_inputs) with a double-buffered one: sg_pipe_stage copies a pinned

@@ -119,6 +119,11 @@ _SIGS = {
     "sg_sampler_destroy": (None, [vp]),
     "sg_sampler_run": (i32, [vp, vp, i64, vp, i32, u64, i32, vp, vp]),
     "sg_sampler_fetch": (i32, [vp, vp, vp, vp]),
+    "sg_tspmm_part_floats": (i64, [i64, i32, i32]),
+    "sg_sage_scatter_bwd_lb": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, i64, i32, vp,
+                                     i64, vp, i64, vp]),
+    "sg_gat_bwd_src_lb": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, vp, vp, vp, vp, i64, i32, vp, vp, vp, vp, i32,
+                                vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp]),
     "sg_pipe_create": (vp, [i64]),
     "sg_pipe_destroy": (None, [vp]),
     "sg_pipe_stage": (i32, [vp, i32, vp, i64, vp, vp]),

@@ -33,6 +33,10 @@ from paper_2303_13775_b200.scheduler import DeviceSplit, split_minibatch
 
 DEBUG_CHECK_FINITE = False
 NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions
+# layers with at least this many edges (capacity) take the load-balanced
+# transposed SpMM (tspmm.cu); below it hub rows are short (max out-degree
+# ~25-125 at C2 layers 2-3) and the single-kernel row-per-warp path is faster
+TSPMM_MIN_EDGES = 65536
 
 
 def _nblocks(rows, tile=32):
@@ -360,10 +364,18 @@ class SplitStep:
             d_prev = _f32(ds.nV[l - 1], w, device=self.dev)
             self._ev(f"ph:scatter{l}:s")
             for d in self.devices:
-                perm, beg, end = csr[d][:3]
-                _lib.call("sg_sage_scatter_bwd", _lib.ptr(ds.ws), ds.lay, l, d, w, _lib.ptr(d_self),
-                          _lib.ptr(d_sums), _lib.ptr(brecv), SWb, _lib.ptr(perm), _lib.ptr(beg),
-                          _lib.ptr(end), kb[l], _lib.ptr(d_prev), self.n_own(l - 1, d), st)
+                perm, beg, end, _, keys = csr[d][:5]
+                if (w + 3) // 4 * 4 <= 192 and ds.nE[l - 1] >= TSPMM_MIN_EDGES:  # load-balanced pieces
+                    nf = int(_lib.load().sg_tspmm_part_floats(ds.nE[l - 1], w, 0))
+                    part = _f32(nf, device=self.dev)
+                    _lib.call("sg_sage_scatter_bwd_lb", _lib.ptr(ds.ws), ds.lay, l, d, w, _lib.ptr(d_self),
+                              _lib.ptr(d_sums), _lib.ptr(brecv), SWb, _lib.ptr(keys), _lib.ptr(perm),
+                              _lib.ptr(beg), _lib.ptr(end), kb[l], 2, _lib.ptr(part), ds.nE[l - 1],
+                              _lib.ptr(d_prev), self.n_own(l - 1, d), st)
+                else:
+                    _lib.call("sg_sage_scatter_bwd", _lib.ptr(ds.ws), ds.lay, l, d, w, _lib.ptr(d_self),
+                              _lib.ptr(d_sums), _lib.ptr(brecv), SWb, _lib.ptr(perm), _lib.ptr(beg),
+                              _lib.ptr(end), kb[l], _lib.ptr(d_prev), self.n_own(l - 1, d), st)
             self._ev(f"ph:scatter{l}:e")
             d_h = d_prev
         with self.phase("reduce"):

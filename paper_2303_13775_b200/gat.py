@@ -48,7 +48,8 @@ def gat_forward(step):
     ds, p = step.ds, step.p
     st = _lib.stream_ptr()
     slope = float(p.leaky_slope)
-    step.layer0()
+    with step.phase("layer0"):
+        step.layer0()
     dperm = step._dst_perm()
     step._launch_src_csr_async(1)
     dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
@@ -64,10 +65,11 @@ def gat_forward(step):
         z = _f32(nVp, dout, device=step.dev)
         s = _f32(nVp, *_hs(H), device=step.dev)
         t = _f32(nV, *_hs(H), device=step.dev)
-        for d in step.devices:
-            _lib.call("sg_gat_project", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
-                      w, dout, H, _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(z), _lib.ptr(s),
-                      _lib.ptr(t), step.n_own(l - 1, d), st)
+        with step.phase(f"project{l}"):
+            for d in step.devices:
+                _lib.call("sg_gat_project", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
+                          w, dout, H, _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(z), _lib.ptr(s),
+                          _lib.ptr(t), step.n_own(l - 1, d), st)
         t_recv = _from_owner(step, l, t, H)
         SW = _r4(dout + 2 * H)
         send = _f32(P, SW, device=step.dev)
@@ -76,12 +78,14 @@ def gat_forward(step):
         loc_m = _f32(nV, *_hs(H), device=step.dev)
         loc_s = _f32(nV, *_hs(H), device=step.dev)
         loc_U = _f32(nV, dout, device=step.dev)
-        step._ev(f"agg{l}_start")
-        for d in step.devices:
-            _lib.call("sg_gat_agg", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(z), _lib.ptr(s),
-                      _lib.ptr(t), _lib.ptr(t_recv), dp_ptr(d), _lib.ptr(pre_e), _lib.ptr(loc_m),
-                      _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(send), SW, step.n_rows(l, d), st)
-        step._ev(f"agg{l}_end")
+        with step.phase(f"agg{l}"):
+            step._ev(f"agg{l}_start")
+            for d in step.devices:
+                _lib.call("sg_gat_agg", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(z),
+                          _lib.ptr(s), _lib.ptr(t), _lib.ptr(t_recv), dp_ptr(d), _lib.ptr(pre_e),
+                          _lib.ptr(loc_m), _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(send), SW,
+                          step.n_rows(l, d), st)
+            step._ev(f"agg{l}_end")
         if step.g > 1 and P > 0:
             step.transport.to_owner(ds, l, send, recv, SW)
             if step.meta is not None:
@@ -89,16 +93,18 @@ def gat_forward(step):
         md = _f32(nV, 2 * H, device=step.dev)
         num = _f32(nV, dout, device=step.dev)
         h = _f32(nV, dout, device=step.dev)
-        for d in step.devices:
-            _lib.call("sg_gat_combine", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(loc_m),
-                      _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(recv), SW, final, _lib.ptr(md), _lib.ptr(num),
-                      _lib.ptr(h), step.n_own(l, d), st)
+        with step.phase(f"combine{l}"):
+            for d in step.devices:
+                _lib.call("sg_gat_combine", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(loc_m),
+                          _lib.ptr(loc_s), _lib.ptr(loc_U), _lib.ptr(recv), SW, final, _lib.ptr(md), _lib.ptr(num),
+                          _lib.ptr(h), step.n_own(l, d), st)
         md_recv = _from_owner(step, l, md, 2 * H)
         alpha = _f32(nEtot, *_hs(H), device=step.dev)
-        for d in step.devices:
-            ne = int(step.meta.n_edge[l - 1][d]) if step.meta is not None else ds.nE[l - 1]
-            _lib.call("sg_gat_alpha", _lib.ptr(ds.ws), ds.lay, l, d, H, slope, _lib.ptr(pre_e), _lib.ptr(md),
-                      _lib.ptr(md_recv), _lib.ptr(alpha), ne, st)
+        with step.phase(f"alpha{l}"):
+            for d in step.devices:
+                ne = int(step.meta.n_edge[l - 1][d]) if step.meta is not None else ds.nE[l - 1]
+                _lib.call("sg_gat_alpha", _lib.ptr(ds.ws), ds.lay, l, d, H, slope, _lib.ptr(pre_e), _lib.ptr(md),
+                          _lib.ptr(md_recv), _lib.ptr(alpha), ne, st)
         step.h[l] = h
         step.keep[l] = dict(z=z, s=s, num=num, md=md, alpha=alpha, pre_e=pre_e)
 
@@ -110,9 +116,10 @@ def gat_backward(step):
     dperm = step._dst_perm()
     dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
     nEtot = int(ds.lay.nEtot)
-    csr, kb = step._join_src_csr(1)
+    with step.phase("src_csr_join"):
+        csr, kb = step._join_src_csr(1)
     d_h = step.d_h
-    from paper_2303_13775_b200.engine import _nblocks
+    from paper_2303_13775_b200.engine import TSPMM_MIN_EDGES, _nblocks
     for l in range(step.L, 0, -1):
         w, dout = p.layer_dims(l - 1)
         final = int(l == step.L)
@@ -123,19 +130,21 @@ def gat_backward(step):
         H = p.heads_of(l - 1)
         DS = dout + H
         dnc = _f32(nV, DS, device=step.dev)
-        for d in step.devices:
-            _lib.call("sg_gat_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(d_h),
-                      _lib.ptr(keep["num"]), final, _lib.ptr(dnc), step.n_own(l, d), st)
+        with step.phase(f"bwd_rows{l}"):
+            for d in step.devices:
+                _lib.call("sg_gat_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(d_h),
+                          _lib.ptr(keep["num"]), final, _lib.ptr(dnc), step.n_own(l, d), st)
         dnc_recv = _from_owner(step, l, dnc, DS)
         d_pre = _f32(nEtot, *_hs(H), device=step.dev)
         dt_loc = _f32(nV, *_hs(H), device=step.dev)
         dt_send = _f32(P, *_hs(H), device=step.dev)
         dt_recv = _f32(P, *_hs(H), device=step.dev)
-        for d in step.devices:
-            _lib.call("sg_gat_bwd_dst", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(keep["z"]),
-                      _lib.ptr(keep["alpha"]), _lib.ptr(keep["pre_e"]), _lib.ptr(dnc), _lib.ptr(dnc_recv),
-                      DS, dp_ptr(d), _lib.ptr(d_pre), _lib.ptr(dt_loc), _lib.ptr(dt_send),
-                      step.n_rows(l, d), st)
+        with step.phase(f"bwd_dst{l}"):
+            for d in step.devices:
+                _lib.call("sg_gat_bwd_dst", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(keep["z"]),
+                          _lib.ptr(keep["alpha"]), _lib.ptr(keep["pre_e"]), _lib.ptr(dnc), _lib.ptr(dnc_recv),
+                          DS, dp_ptr(d), _lib.ptr(d_pre), _lib.ptr(dt_loc), _lib.ptr(dt_send),
+                          step.n_rows(l, d), st)
         if step.g > 1 and P > 0:
             step.transport.to_owner(ds, l, dt_send, dt_recv, H)
             if step.meta is not None:
@@ -143,21 +152,33 @@ def gat_backward(step):
         d_z = _f32(nVp, dout, device=step.dev)
         dsb = _f32(nVp, *_hs(H), device=step.dev)
         dt_tot = _f32(nV, *_hs(H), device=step.dev)
-        for d in step.devices:
-            perm, beg, end = csr[d][:3]
-            _lib.call("sg_gat_bwd_src", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(perm), _lib.ptr(beg),
-                      _lib.ptr(end), kb[l], _lib.ptr(keep["alpha"]), _lib.ptr(d_pre), _lib.ptr(dnc),
-                      _lib.ptr(dnc_recv), DS, _lib.ptr(dt_loc), _lib.ptr(dt_recv), _lib.ptr(a_s), _lib.ptr(a_d),
-                      _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), step.n_own(l - 1, d), st)
+        with step.phase(f"bwd_src{l}"):
+            for d in step.devices:
+                perm, beg, end, _, keys = csr[d][:5]
+                if (dout + H + 3) // 4 * 4 <= 192 and ds.nE[l - 1] >= TSPMM_MIN_EDGES:  # load-balanced pieces
+                    nf = int(_lib.load().sg_tspmm_part_floats(ds.nE[l - 1], dout, H))
+                    part = _f32(nf, device=step.dev)
+                    _lib.call("sg_gat_bwd_src_lb", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(keys),
+                              _lib.ptr(perm), _lib.ptr(beg), _lib.ptr(end), kb[l], 1, _lib.ptr(keep["alpha"]),
+                              _lib.ptr(d_pre), _lib.ptr(dnc), _lib.ptr(dnc_recv), DS, _lib.ptr(dt_loc),
+                              _lib.ptr(dt_recv), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(d_z), _lib.ptr(dsb),
+                              _lib.ptr(dt_tot), _lib.ptr(part), ds.nE[l - 1], step.n_own(l - 1, d), st)
+                else:
+                    _lib.call("sg_gat_bwd_src", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(perm),
+                              _lib.ptr(beg), _lib.ptr(end), kb[l], _lib.ptr(keep["alpha"]), _lib.ptr(d_pre),
+                              _lib.ptr(dnc), _lib.ptr(dnc_recv), DS, _lib.ptr(dt_loc), _lib.ptr(dt_recv),
+                              _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot),
+                              step.n_own(l - 1, d), st)
         need_prev = l > 1
         d_prev = _f32(nVp, w, device=step.dev) if need_prev else None
         npart = w * dout + 2 * dout
-        for d in step.devices:
-            nb = _nblocks(step.n_own(l - 1, d))
-            part = _f32(nb * npart, device=step.dev)
-            _lib.call("sg_gat_bwd_param", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
-                      w, dout, H, _lib.ptr(keep["z"]), _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), _lib.ptr(W),
-                      _lib.ptr(part), nb, _lib.ptr(d_prev), step.n_own(l - 1, d), st)
-            step.jobs.append((part, nb, npart, step.grads[d], p.offset(f"layer{l-1}.w")))
-            step._partials.append(part)
+        with step.phase(f"bwd_param{l}"):
+            for d in step.devices:
+                nb = _nblocks(step.n_own(l - 1, d))
+                part = _f32(nb * npart, device=step.dev)
+                _lib.call("sg_gat_bwd_param", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
+                          w, dout, H, _lib.ptr(keep["z"]), _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), _lib.ptr(W),
+                          _lib.ptr(part), nb, _lib.ptr(d_prev), step.n_own(l - 1, d), st)
+                step.jobs.append((part, nb, npart, step.grads[d], p.offset(f"layer{l-1}.w")))
+                step._partials.append(part)
         d_h = d_prev
