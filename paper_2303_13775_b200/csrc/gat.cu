@@ -25,6 +25,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "dense.cuh"
 
 namespace sg {
 namespace {
@@ -860,6 +861,68 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
   }
 }
 
+// ---------------------------------------------------------------- wide layers (dense.cu GEMMs)
+// scores after a dense projection: s = z . a_src per head; t on self rows
+__global__ void __launch_bounds__(256) k_gat_scores(const SgMeta* __restrict__ meta, ProjArgs a) {
+  const int H = a.heads, D = a.dout, dh = D / H;
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d], ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t item = gw; item < (int64_t)n * H; item += nw) {  // warp per (row, head)
+    const int64_t r = item / H;
+    const int hh = (int)(item - r * H);
+    const int64_t G = own0 + r;
+    const float* zr = a.z + G * D + hh * dh;
+    float sv = 0.f, tv = 0.f;
+    for (int j = lane; j < dh; j += 32) {
+      sv = fmaf(zr[j], a.a_src[hh * dh + j], sv);
+      tv = fmaf(zr[j], a.a_dst[hh * dh + j], tv);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      tv += __shfl_xor_sync(0xffffffffu, tv, o);
+    }
+    if (lane == 0) {
+      a.s[G * H + hh] = sv;
+      const int p = a.grouped[a.voff_lm1 + G];
+      if (p < nVl) a.t[(int64_t)(ownl + a.rank[a.voff_l + p]) * H + hh] = tv;
+    }
+  }
+}
+
+// per-split partials of da_src = sum_r z_r * ds_r(head), da_dst = sum_self z_r * dt(head)
+// into partial[s][w*D .. w*D + 2D) (dW comes from dense_gemm_tn_partial)
+__global__ void __launch_bounds__(256) k_gat_attn_partial(const SgMeta* __restrict__ meta, BParamArgs a,
+                                                         int nsplit) {
+  const int D = a.dout, H = a.heads, dh = D / H, w = a.w;
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d], ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int s = blockIdx.x;
+  const int per = (n + nsplit - 1) / nsplit;
+  const int rb = s * per, re = min(n, rb + per);
+  float* out = a.partial + (int64_t)s * ((int64_t)w * D + 2 * D) + (int64_t)w * D;
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    const int hh = j / dh;
+    float as = 0.f, ad = 0.f;
+    for (int r = rb; r < re; ++r) {
+      const int64_t G = own0 + r;
+      const float zv = a.z[G * D + j];
+      as = fmaf(zv, a.ds[G * H + hh], as);
+      const int p = a.grouped[a.voff_lm1 + G];
+      if (p < nVl) ad = fmaf(zv, a.dt_tot[(int64_t)(ownl + a.rank[a.voff_l + p]) * H + hh], ad);
+    }
+    out[j] = as;
+    out[D + j] = ad;
+  }
+}
+
 // ---------------------------------------------------------------- dispatch helpers
 // Team shape from (D, H): LPR lanes span D (a power of two, multiple of H),
 // EG edge groups fill the team to 8..32 lanes.
@@ -929,7 +992,6 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
   a.W = W; a.a_src = a_src; a.a_dst = a_dst;
   a.z = z; a.s = s; a.t = t;
   const size_t smem = sizeof(float) * ((size_t)w * dout + (size_t)PTR * (w + 1) + (size_t)PTR * (dout + 1) + PTR);
-  SG_REQUIRE(smem <= 227 * 1024, "gat_project: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   const int nq = dout / 4;
   if (w % 4 == 0 && w <= 128 && dout % 4 == 0 && nq <= 32 && (nq & (nq - 1)) == 0) {
@@ -949,6 +1011,20 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
 #undef GP_CASE
     }
     SG_CHECK_LAUNCH("k_gat_project_tiled");
+    return SG_OK;
+  }
+  if (smem > 227 * 1024) {
+    // wide layer: z = h_prev[rows] W as a dense GEMM, then the per-head scores
+    GemmArgs g;
+    memset(&g, 0, sizeof(g));
+    g.R_dev = &meta->n_own[l - 1][d];
+    g.K = w; g.N = dout; g.A = h_prev; g.lda = w;
+    g.ar.mode = src_row ? 1 : 0; g.ar.map = src_row; g.ar.base_dev = &meta->own_off[l - 1][d];
+    g.B = W; g.ldb = dout; g.C = z; g.ldc = dout; g.c_base_dev = &meta->own_off[l - 1][d];
+    int rc = dense_gemm_rows(g, max_rows, st);
+    if (rc) return rc;
+    k_gat_scores<<<clamp_grid(div_up(max_rows * heads, 8), kSMs * 8), 256, 0, st>>>(meta, a);
+    SG_CHECK_LAUNCH("k_gat_scores");
     return SG_OK;
   }
   const int grid = clamp_grid(div_up(max_rows, PTR), kSMs * 4);
@@ -1110,9 +1186,7 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
   SG_REQUIRE(split_ws && lay, "gat_bwd_param: null workspace");
   SPLIT_PTRS
   GAT_HEADS_CHECK(dout, heads);
-  SG_REQUIRE((int64_t)w * dout <= 256 * QMAXQ * 4, "gat_bwd_param: w*dout > 8192 unsupported");
   SG_REQUIRE(nblocks >= 1, "gat_bwd_param: nblocks >= 1");
-  (void)max_rows;
   BParamArgs a;
   memset(&a, 0, sizeof(a));
   a.l = l; a.d = d; a.w = w; a.dout = dout; a.heads = heads;
@@ -1123,8 +1197,32 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
   const bool t4 = w % 4 == 0 && dout % 4 == 0 && (w / 4) * (dout / 4) <= 512;
   const size_t smem = sizeof(float) * (2 * (size_t)QTR * dout + (size_t)dout * (w + 1) +
                                        (size_t)QTR * (w + 4) + 2 * (size_t)QTR * heads + QTR);
-  SG_REQUIRE(smem <= 227 * 1024, "gat_bwd_param: width too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
+  if ((int64_t)w * dout > 256 * QMAXQ * 4 || smem > 227 * 1024) {
+    // wide layer: dW partials as a dense GEMM, attention-vector partials, d_prev = d_z W^T
+    TnArgs t;
+    memset(&t, 0, sizeof(t));
+    t.R_dev = &meta->n_own[l - 1][d];
+    t.K = w; t.N = dout; t.A = h_prev; t.lda = w;
+    t.ar.mode = src_row ? 1 : 0; t.ar.map = src_row; t.ar.base_dev = &meta->own_off[l - 1][d];
+    t.G = d_z; t.ldg = dout; t.g_base_dev = &meta->own_off[l - 1][d];
+    t.P = partial; t.pstride = (int64_t)w * dout + 2 * dout; t.p_off = 0; t.nsplit = nblocks;
+    int rc = dense_gemm_tn_partial(t, st);
+    if (rc) return rc;
+    k_gat_attn_partial<<<nblocks, 256, 0, st>>>(meta, a, nblocks);
+    SG_CHECK_LAUNCH("k_gat_attn_partial");
+    if (d_prev) {
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.R_dev = &meta->n_own[l - 1][d];
+      g.K = dout; g.N = w; g.A = d_z; g.lda = dout; g.ar.mode = 0;
+      g.ar.base_dev = &meta->own_off[l - 1][d];
+      g.B = W; g.ldb = dout; g.bt = 1; g.C = d_prev; g.ldc = w; g.c_base_dev = &meta->own_off[l - 1][d];
+      rc = dense_gemm_rows(g, max_rows, st);
+      if (rc) return rc;
+    }
+    return SG_OK;
+  }
   if (t4) {
     SG_CUDA(allow_max_smem<k_gat_bwd_param<true>>());
     k_gat_bwd_param<true><<<nblocks, 256, smem, st>>>(meta, a);

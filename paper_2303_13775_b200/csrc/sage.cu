@@ -26,6 +26,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "dense.cuh"
 
 namespace sg {
 namespace {
@@ -510,20 +511,22 @@ struct UpdArgs {
   float* mean;
   float* h;
   float* hs_out;  // when set: write the self rows and leave the GEMM to k_sage_linear
+  int no_linear;  // mean / counts (/ hs_out) only: the dense transform runs in dense.cu
 };
 
 template <bool Q4>
 __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ meta, UpdArgs a) {
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, wp = w + 1;
-  float* ws_s = smem;              // [w][dout]
-  float* wn_s = ws_s + w * dout;   // [w][dout]
-  float* hs_s = wn_s + w * dout;   // [UTR][w+1]
+  const int wsz = a.no_linear ? 0 : w * dout;
+  float* ws_s = smem;              // [w][dout] (none when no_linear)
+  float* wn_s = ws_s + wsz;        // [w][dout]
+  float* hs_s = wn_s + wsz;        // [UTR][w+1]
   float* mn_s = hs_s + UTR * wp;   // [UTR][w+1]
   float* n_s = mn_s + UTR * wp;    // [UTR]
   int* prow_s = (int*)(n_s + UTR); // [UTR]
   int* cs_s = prow_s + UTR;        // [UTR][g]
-  for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
+  for (int i = threadIdx.x; i < wsz; i += blockDim.x) {
     ws_s[i] = a.ws[i];
     wn_s[i] = a.wn[i];
   }
@@ -575,7 +578,7 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
       }
     }
     __syncthreads();
-    if (a.hs_out) continue;  // dense transform done by k_sage_linear
+    if (a.hs_out || a.no_linear) continue;  // dense transform done by k_sage_linear / dense.cu
     if (Q4) {
       const int nq = dout >> 2;
       for (int idx = threadIdx.x; idx < UTR * nq; idx += blockDim.x) {
@@ -1155,9 +1158,47 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
   SG_REQUIRE(split_ws && lay, "sage_update: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_update: bad layer/device");
-  SG_REQUIRE(dout >= 1 && dout <= 256, "sage_update: dout out of range");
+  SG_REQUIRE(dout >= 1 && w >= 1, "sage_update: dout/w out of range");
   SG_REQUIRE(y.g <= 32, "sage_update: g > 32");
   if (max_rows <= 0) return SG_OK;
+  const size_t smem_fast = sizeof(float) * (2 * (size_t)w * dout + 2 * (size_t)UTR * (w + 1) +
+                                            (size_t)UTR * (2 + y.g));
+  if (dout > 256 || smem_fast > 227 * 1024) {
+    // wide layer: mean / counts (/ self rows) here, then h = act(hs Ws + b + mean Wn)
+    UpdArgs u;
+    memset(&u, 0, sizeof(u));
+    u.l = l; u.d = d; u.w = w; u.dout = dout; u.final_ = final_layer; u.g = y.g; u.stride = recv_stride;
+    u.voff_l = y.voff[l]; u.h_prev = h_prev; u.src_row = src_row; u.selfrow = I32(y.o_selfrow);
+    u.contrib = I32(y.o_contrib); u.sums = sums; u.counts = counts; u.recv = recvbuf;
+    u.mean = mean; u.h = h; u.hs_out = hs_out; u.no_linear = 1;
+    const size_t sm = sizeof(float) * (2 * (size_t)UTR * (w + 1) + (size_t)UTR * (2 + y.g));
+    SG_REQUIRE(sm <= 227 * 1024, "sage_update: input width too large for shared memory");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = clamp_grid(div_up(max_rows, UTR), kSMs * 3);
+    SG_CUDA(allow_max_smem<k_sage_update<false>>());
+    k_sage_update<false><<<grid, 256, sm, st>>>(meta, u);
+    SG_CHECK_LAUNCH("k_sage_update(mean)");
+    GemmArgs g1;
+    memset(&g1, 0, sizeof(g1));
+    g1.R_dev = &meta->n_own[l][d];
+    g1.K = w; g1.N = dout;
+    if (hs_out) {
+      g1.A = hs_out; g1.ar.mode = 0; g1.ar.base_dev = &meta->own_off[l][d];
+    } else {
+      g1.A = h_prev; g1.ar.mode = 2; g1.ar.base_dev = &meta->own_off[l][d];
+      g1.ar.selfrow = I32(y.o_selfrow); g1.ar.prev0_dev = &meta->own_off[l - 1][d];
+      g1.ar.voff_l = y.voff[l]; g1.ar.map = src_row;
+    }
+    g1.lda = w; g1.B = w_self; g1.ldb = dout; g1.C = h; g1.ldc = dout;
+    g1.c_base_dev = &meta->own_off[l][d]; g1.bias = bias;
+    int rc = dense_gemm_rows(g1, max_rows, st);
+    if (rc) return rc;
+    GemmArgs g2 = g1;
+    memset(&g2.ar, 0, sizeof(g2.ar));
+    g2.A = mean; g2.ar.mode = 0; g2.ar.base_dev = &meta->own_off[l][d];
+    g2.B = w_neigh; g2.bias = nullptr; g2.accum = 1; g2.relu = final_layer ? 0 : 1;
+    return dense_gemm_rows(g2, max_rows, st);
+  }
   UpdArgs a;
   memset(&a, 0, sizeof(a));
   a.l = l;
@@ -1213,11 +1254,53 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   SG_REQUIRE(split_ws && lay, "sage_bwd_rows: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_bwd_rows: bad layer/device");
-  SG_REQUIRE(dout >= 1 && dout <= 32, "sage_bwd_rows: dout must be <= 32");
-  const bool q4 = dout % 4 == 0;
-  SG_REQUIRE(q4 ? (int64_t)w * (dout / 4) <= 256 * BMAXQ : (int64_t)w * dout <= 256 * BMAXACC,
-             "sage_bwd_rows: w*dout > 4096 unsupported");
+  SG_REQUIRE(dout >= 1 && w >= 1, "sage_bwd_rows: dout/w out of range");
   SG_REQUIRE(nblocks >= 1, "sage_bwd_rows: nblocks >= 1");
+  const bool q4 = dout % 4 == 0;
+  const bool fits = dout <= 32 && (q4 ? (int64_t)w * (dout / 4) <= 256 * BMAXQ
+                                      : (int64_t)w * dout <= 256 * BMAXACC);
+  if (!fits) {
+    // wide layer: per-split weight-gradient partials [dW_self | dW_neigh | db]
+    // and the input gradients as dense GEMMs (dense.cu); d_pre = d_h * ReLU'(h)
+    cudaStream_t st = (cudaStream_t)stream;
+    const int32_t* own = &meta->own_off[l][d];
+    const float* gmask = final_layer ? nullptr : h;
+    TnArgs t;
+    memset(&t, 0, sizeof(t));
+    t.R_dev = &meta->n_own[l][d];
+    t.K = w; t.N = dout; t.lda = w;
+    if (self_compact) {
+      t.A = h_prev; t.ar.mode = 0; t.ar.base_dev = own;
+    } else {
+      t.A = h_prev; t.ar.mode = 2; t.ar.base_dev = own; t.ar.selfrow = I32(y.o_selfrow);
+      t.ar.prev0_dev = &meta->own_off[l - 1][d]; t.ar.voff_l = y.voff[l]; t.ar.map = src_row;
+    }
+    t.G = d_h; t.ldg = dout; t.g_base_dev = own; t.gmask = gmask;
+    t.P = partial; t.pstride = 2 * (int64_t)w * dout + dout; t.p_off = 0; t.nsplit = nblocks;
+    int rc = dense_gemm_tn_partial(t, st);
+    if (rc) return rc;
+    TnArgs t2 = t;
+    memset(&t2.ar, 0, sizeof(t2.ar));
+    t2.A = mean; t2.ar.mode = 0; t2.ar.base_dev = own; t2.ones = 1; t2.p_off = (int64_t)w * dout;
+    rc = dense_gemm_tn_partial(t2, st);
+    if (rc) return rc;
+    for (int which = 0; which < 2; ++which) {
+      float* out = which == 0 ? d_self : d_sums;
+      if (!out) continue;
+      GemmArgs g;
+      memset(&g, 0, sizeof(g));
+      g.R_dev = &meta->n_own[l][d];
+      g.K = dout; g.N = w;
+      g.A = d_h; g.lda = dout; g.ar.mode = 0; g.ar.base_dev = own;
+      g.amask = gmask; g.lda_mask = dout;
+      g.B = which == 0 ? w_self : w_neigh; g.ldb = dout; g.bt = 1;
+      g.C = out; g.ldc = w; g.c_base_dev = own;
+      g.rdiv = which == 0 ? nullptr : counts;
+      rc = dense_gemm_rows(g, max_rows, st);
+      if (rc) return rc;
+    }
+    return SG_OK;
+  }
   (void)max_rows;
   BwdArgs a;
   memset(&a, 0, sizeof(a));
