@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/splitgnn_b200.h"
 
@@ -44,6 +45,40 @@ void set_error(const std::string& msg);
   } while (0)
 
 constexpr int kSMs = 148;
+
+// ---- programmatic dependent launch (PDL)
+// Every library kernel is launched with programmatic stream serialisation
+// allowed and starts with SG_PDL_ENTRY(): griddepcontrol.wait blocks until the
+// preceding grid in the stream has completed and its writes are visible (so
+// no kernel ever reads a predecessor's output early), then
+// launch_dependents lets the NEXT grid be scheduled while this one runs. In a
+// captured CUDA graph this turns each kernel->kernel edge into a programmatic
+// edge: the successor's launch latency and block scheduling overlap the
+// predecessor instead of following it. griddepcontrol.wait is a no-op for a
+// grid launched without the attribute. SG_PDL=0 disables the attribute.
+#define SG_PDL_ENTRY()                                        \
+  do {                                                        \
+    asm volatile("griddepcontrol.wait;" ::: "memory");        \
+    asm volatile("griddepcontrol.launch_dependents;" :::);    \
+  } while (0)
+
+extern bool g_pdl;
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Raise a kernel's dynamic shared-memory limit to the sm_100 maximum once per
 // process (never inside a later CUDA-graph capture).

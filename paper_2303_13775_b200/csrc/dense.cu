@@ -39,6 +39,7 @@ __device__ __forceinline__ int64_t dense_row(const DenseRows& d, int64_t base, i
 __device__ __forceinline__ int64_t dev_or0(const int32_t* p) { return p ? (int64_t)*p : 0; }
 
 __global__ void __launch_bounds__(256) k_gemm_rows(GemmArgs a) {
+  SG_PDL_ENTRY();
   __shared__ __align__(16) float As[GK][GM + GP];
   __shared__ __align__(16) float Bs[GK][GN + GP];
   __shared__ int64_t arow[GM];
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(256) k_gemm_rows(GemmArgs a) {
 
 // P[s][p_off + k * N + n] over split s's rows (ascending); grid (tiles, nsplit)
 __global__ void __launch_bounds__(256) k_gemm_tn_partial(TnArgs a) {
+  SG_PDL_ENTRY();
   constexpr int GR = 16;
   __shared__ __align__(16) float As[GR][GM + GP];
   __shared__ __align__(16) float Gs[GR][GN + GP];
@@ -197,7 +199,7 @@ int dense_gemm_rows(const GemmArgs& a, int64_t max_rows, cudaStream_t st) {
   SG_REQUIRE(a.K >= 0 && a.A && a.B && a.C && a.R_dev, "gemm_rows: bad arguments");
   const int gx = clamp_grid(div_up(max_rows, GM), kSMs * 4);
   dim3 grid(gx, (unsigned)div_up(a.N, GN));
-  k_gemm_rows<<<grid, 256, 0, st>>>(a);
+  ::sg::launch(k_gemm_rows, grid, 256, 0, st, a);
   SG_CHECK_LAUNCH("k_gemm_rows");
   return SG_OK;
 }
@@ -207,7 +209,7 @@ int dense_gemm_tn_partial(const TnArgs& a, cudaStream_t st) {
   const int Ke = a.K + (a.ones ? 1 : 0);
   if (Ke <= 0 || a.N <= 0) return SG_OK;
   dim3 grid((unsigned)(div_up(Ke, GM) * div_up(a.N, GN)), (unsigned)a.nsplit);
-  k_gemm_tn_partial<<<grid, 256, 0, st>>>(a);
+  ::sg::launch(k_gemm_tn_partial, grid, 256, 0, st, a);
   SG_CHECK_LAUNCH("k_gemm_tn_partial");
   return SG_OK;
 }

@@ -16,6 +16,7 @@ namespace {
 __global__ void k_xfer(const SgMeta* __restrict__ meta, int l, const int32_t* __restrict__ xfer,
                        const float* __restrict__ in, float* __restrict__ out, int stride,
                        int forward) {
+  SG_PDL_ENTRY();
   const int n = meta->npairs[l];
   const int64_t total = (int64_t)n * stride;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -32,6 +33,7 @@ __global__ void k_pack_from_owner(const SgMeta* __restrict__ meta, int l, int d,
                                   const int32_t* __restrict__ recv_row,
                                   const float* __restrict__ rows, int w, float* __restrict__ out,
                                   int stride) {
+  SG_PDL_ENTRY();
   const int b = meta->recv_off[l][d], e = meta->recv_off[l][d + 1];
   const int64_t total = (int64_t)(e - b) * w;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -46,6 +48,7 @@ __global__ void k_pack_from_owner(const SgMeta* __restrict__ meta, int l, int d,
 __global__ void k_unpack_refs(const SgMeta* __restrict__ meta, int l, int d,
                               const int32_t* __restrict__ sendpos, const float* __restrict__ in,
                               int stride, int w, float* __restrict__ out) {
+  SG_PDL_ENTRY();
   const int n = meta->n_ref[l][d];
   const int r0 = meta->ref_off[l][d];
   const int64_t total = (int64_t)n * w;
@@ -67,8 +70,7 @@ extern "C" int sg_xfer_to_owner(const void* split_ws, const SgSplitLayout* lay, 
   const SgSplitLayout& y = *lay;
   const int64_t P = y.pbase[l + 1] - y.pbase[l];
   if (P <= 0) return SG_OK;
-  k_xfer<<<clamp_grid(div_up(P * stride, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
-      (const SgMeta*)(base + y.o_meta), l, (const int32_t*)(base + y.o_xfer) + y.pbase[l],
+  ::sg::launch(k_xfer, clamp_grid(div_up(P * stride, 256), kSMs * 8), 256, 0, (cudaStream_t)stream, (const SgMeta*)(base + y.o_meta), l, (const int32_t*)(base + y.o_xfer) + y.pbase[l],
       sendbuf, recvbuf, stride, 1);
   SG_CHECK_LAUNCH("k_xfer(to_owner)");
   return SG_OK;
@@ -82,8 +84,7 @@ extern "C" int sg_xfer_from_owner(const void* split_ws, const SgSplitLayout* lay
   const SgSplitLayout& y = *lay;
   const int64_t P = y.pbase[l + 1] - y.pbase[l];
   if (P <= 0) return SG_OK;
-  k_xfer<<<clamp_grid(div_up(P * stride, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
-      (const SgMeta*)(base + y.o_meta), l, (const int32_t*)(base + y.o_xfer) + y.pbase[l],
+  ::sg::launch(k_xfer, clamp_grid(div_up(P * stride, 256), kSMs * 8), 256, 0, (cudaStream_t)stream, (const SgMeta*)(base + y.o_meta), l, (const int32_t*)(base + y.o_xfer) + y.pbase[l],
       sendbuf_recv_layout, recvbuf_pair_layout, stride, 0);
   SG_CHECK_LAUNCH("k_xfer(from_owner)");
   return SG_OK;
@@ -96,8 +97,8 @@ extern "C" int sg_pack_from_owner(const void* split_ws, const SgSplitLayout* lay
   const char* base = (const char*)split_ws;
   const SgSplitLayout& y = *lay;
   if (max_slots <= 0) return SG_OK;
-  k_pack_from_owner<<<clamp_grid(div_up(max_slots * w, 256), kSMs * 8), 256, 0,
-                      (cudaStream_t)stream>>>((const SgMeta*)(base + y.o_meta), l, d,
+  ::sg::launch(k_pack_from_owner, clamp_grid(div_up(max_slots * w, 256), kSMs * 8), 256, 0,
+                      (cudaStream_t)stream, (const SgMeta*)(base + y.o_meta), l, d,
                                               (const int32_t*)(base + y.o_recv_row) + y.pbase[l],
                                               rows, w, out, stride);
   SG_CHECK_LAUNCH("k_pack_from_owner");
@@ -111,8 +112,8 @@ extern "C" int sg_unpack_refs(const void* split_ws, const SgSplitLayout* lay, in
   const char* base = (const char*)split_ws;
   const SgSplitLayout& y = *lay;
   if (max_rows <= 0) return SG_OK;
-  k_unpack_refs<<<clamp_grid(div_up(max_rows * w, 256), kSMs * 8), 256, 0,
-                  (cudaStream_t)stream>>>((const SgMeta*)(base + y.o_meta), l, d,
+  ::sg::launch(k_unpack_refs, clamp_grid(div_up(max_rows * w, 256), kSMs * 8), 256, 0,
+                  (cudaStream_t)stream, (const SgMeta*)(base + y.o_meta), l, d,
                                           (const int32_t*)(base + y.o_sendpos) + y.pbase[l],
                                           recv_pair_layout, stride, w, out);
   SG_CHECK_LAUNCH("k_unpack_refs");

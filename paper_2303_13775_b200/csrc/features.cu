@@ -19,6 +19,7 @@ __global__ void k_layer0_rows(const SgMeta* __restrict__ meta, int d,
                               const int32_t* __restrict__ V, const int32_t* __restrict__ cache_slot,
                               int32_t miss_base, int64_t nVtot, int miss_global,
                               int32_t* __restrict__ src_row0) {
+  SG_PDL_ENTRY();
   const int n = meta->n_own[0][d];
   const int own0 = meta->own_off[0][d];
   const int lbase = miss_global ? meta->load_off[d] : 0;
@@ -33,6 +34,7 @@ __global__ void k_layer0_rows(const SgMeta* __restrict__ meta, int d,
 
 __global__ void k_gather_rows(const float* __restrict__ table, const int32_t* __restrict__ rows,
                               int64_t n, int w, float* __restrict__ out) {
+  SG_PDL_ENTRY();
   const int64_t total = n * w;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -44,6 +46,7 @@ __global__ void k_gather_rows(const float* __restrict__ table, const int32_t* __
 
 __global__ void k_fill_uniform(float* __restrict__ out, int64_t rows, int w, uint64_t seed,
                                int64_t row0) {
+  SG_PDL_ENTRY();
   const int64_t total = rows * w;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -67,8 +70,7 @@ extern "C" int sg_layer0_rows(const void* split_ws, const SgSplitLayout* lay, in
   // the rank inside this device's load list; otherwise the global load index.
   const int miss_global = miss_base >= 0 ? 1 : 0;
   const int32_t mb = miss_base >= 0 ? miss_base : -miss_base - 1;
-  k_layer0_rows<<<clamp_grid(div_up(y.nV[0], 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(
-      (const SgMeta*)(base + y.o_meta), d, (const int32_t*)(base + y.o_grouped),
+  ::sg::launch(k_layer0_rows, clamp_grid(div_up(y.nV[0], 256), kSMs * 8), 256, 0, (cudaStream_t)stream, (const SgMeta*)(base + y.o_meta), d, (const int32_t*)(base + y.o_grouped),
       (const int32_t*)(base + y.o_rank), V, cache_slot, mb, y.nVtot, miss_global, src_row0);
   SG_CHECK_LAUNCH("k_layer0_rows");
   return SG_OK;
@@ -77,8 +79,8 @@ extern "C" int sg_layer0_rows(const void* split_ws, const SgSplitLayout* lay, in
 extern "C" int sg_gather_rows(const float* table, const int32_t* rows, int64_t n_rows,
                               int32_t width, float* out, void* stream) {
   if (n_rows <= 0 || width <= 0) return SG_OK;
-  k_gather_rows<<<clamp_grid(div_up(n_rows * width, 256), kSMs * 8), 256, 0,
-                  (cudaStream_t)stream>>>(table, rows, n_rows, width, out);
+  ::sg::launch(k_gather_rows, clamp_grid(div_up(n_rows * width, 256), kSMs * 8), 256, 0,
+                  (cudaStream_t)stream, table, rows, n_rows, width, out);
   SG_CHECK_LAUNCH("k_gather_rows");
   return SG_OK;
 }
@@ -86,8 +88,8 @@ extern "C" int sg_gather_rows(const float* table, const int32_t* rows, int64_t n
 extern "C" int sg_fill_uniform(float* out, int64_t rows, int32_t width, uint64_t seed,
                                int64_t row0, void* stream) {
   if (rows <= 0 || width <= 0) return SG_OK;
-  k_fill_uniform<<<clamp_grid(div_up(rows * width, 256), kSMs * 16), 256, 0,
-                   (cudaStream_t)stream>>>(out, rows, width, seed, row0);
+  ::sg::launch(k_fill_uniform, clamp_grid(div_up(rows * width, 256), kSMs * 16), 256, 0,
+                   (cudaStream_t)stream, out, rows, width, seed, row0);
   SG_CHECK_LAUNCH("k_fill_uniform");
   return SG_OK;
 }

@@ -90,6 +90,7 @@ struct ProjArgs {
 
 template <bool Q4>
 __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ meta, ProjArgs a) {
+  SG_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, wp = w + 1, dp = dout + 1, H = a.heads, dh = dout / H;
   float* W_s = smem;               // [w][dout]
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ 
 // NS = 256 / NT K-slices (NQ <= 32 -> D <= 128).
 template <int NQ>
 __global__ void __launch_bounds__(256) k_gat_project_tiled(const SgMeta* __restrict__ meta, ProjArgs a) {
+  SG_PDL_ENTRY();
   constexpr int TM = 32, TMP = TM + 4;
   constexpr int NT = (TM / 4) * NQ;
   constexpr int NS = 256 / NT;
@@ -309,6 +311,7 @@ struct AggArgs {
 // LH = LPR/H lanes per head; EG edge groups merged by a fixed xor tree.
 template <int VEC, int LPR, int EG>
 __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta, AggArgs a) {
+  SG_PDL_ENTRY();
   using V = V4<VEC>;
   using T = typename V::T;
   constexpr int RL = LPR * EG;
@@ -401,6 +404,7 @@ struct CombArgs {
 };
 
 __global__ void k_gat_combine(const SgMeta* __restrict__ meta, CombArgs a) {
+  SG_PDL_ENTRY();
   const int l = a.l, d = a.d, dout = a.dout, g = a.g, H = a.heads, dh = dout / H;
   const int n = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];
@@ -452,6 +456,7 @@ struct AlphaArgs {
 };
 
 __global__ void k_gat_alpha(const SgMeta* __restrict__ meta, AlphaArgs a) {
+  SG_PDL_ENTRY();
   const int l = a.l, d = a.d, li = l - 1, H = a.heads;
   const int b = meta->edge_off[li][d], e = meta->edge_off[li][d + 1];
   const int n_own = meta->n_own[l][d];
@@ -477,6 +482,7 @@ struct BRowsArgs {
 };
 
 __global__ void k_gat_bwd_rows(const SgMeta* __restrict__ meta, BRowsArgs a) {
+  SG_PDL_ENTRY();
   const int l = a.l, d = a.d, dout = a.dout, H = a.heads, dh = dout / H, st = dout + H;
   const int n = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];
@@ -517,6 +523,7 @@ struct BDstArgs {
 
 template <int VEC, int LPR, int EG>
 __global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ meta, BDstArgs a) {
+  SG_PDL_ENTRY();
   using V = V4<VEC>;
   using T = typename V::T;
   constexpr int RL = LPR * EG;
@@ -600,6 +607,7 @@ struct BSrcArgs {
 // warp per source row; NG = 32/LPR lane groups split the out-edges
 template <int VEC, int LPR>
 __global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ meta, BSrcArgs a) {
+  SG_PDL_ENTRY();
   using V = V4<VEC>;
   using T = typename V::T;
   constexpr int NG = 32 / LPR;
@@ -689,6 +697,7 @@ struct BParamArgs {
 // per row 2 LDS.128 + 16 FFMA; otherwise one scalar slot per (c, j).
 template <bool T4>
 __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict__ meta, BParamArgs a) {
+  SG_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, H = a.heads, dh = dout / H;
   const int wp = T4 ? w + 4 : w + 1;  // h row stride (float4-aligned for T4)
@@ -864,6 +873,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
 // ---------------------------------------------------------------- wide layers (dense.cu GEMMs)
 // scores after a dense projection: s = z . a_src per head; t on self rows
 __global__ void __launch_bounds__(256) k_gat_scores(const SgMeta* __restrict__ meta, ProjArgs a) {
+  SG_PDL_ENTRY();
   const int H = a.heads, D = a.dout, dh = D / H;
   const int l = a.l, d = a.d;
   const int n = meta->n_own[l - 1][d];
@@ -899,6 +909,7 @@ __global__ void __launch_bounds__(256) k_gat_scores(const SgMeta* __restrict__ m
 // into partial[s][w*D .. w*D + 2D) (dW comes from dense_gemm_tn_partial)
 __global__ void __launch_bounds__(256) k_gat_attn_partial(const SgMeta* __restrict__ meta, BParamArgs a,
                                                          int nsplit) {
+  SG_PDL_ENTRY();
   const int D = a.dout, H = a.heads, dh = D / H, w = a.w;
   const int l = a.l, d = a.d;
   const int n = meta->n_own[l - 1][d];
@@ -934,7 +945,7 @@ __global__ void __launch_bounds__(256) k_gat_attn_partial(const SgMeta* __restri
                     EG_ = decltype(eg_)::value;                                           \
       constexpr int RPB_ = 8 * (32 / (LPR_ * EG_));                                       \
       const int grid_ = clamp_grid(div_up((GRIDROWS), RPB_), kSMs * 8);                   \
-      KERNEL<VEC_, LPR_, EG_><<<grid_, 256, 0, ST>>>(__VA_ARGS__);                        \
+      ::sg::launch(KERNEL<VEC_, LPR_, EG_>, grid_, 256, 0, ST, __VA_ARGS__);                        \
     };                                                                                    \
     using I1 = std::integral_constant<int, 1>;                                            \
     using I2 = std::integral_constant<int, 2>;                                            \
@@ -1005,7 +1016,7 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
   case Q:                                                            \
     attr = allow_max_smem<k_gat_project_tiled<Q>>();                 \
     SG_CUDA(attr);                                                   \
-    k_gat_project_tiled<Q><<<grid_t, 256, smem_t, st>>>(meta, a);    \
+    ::sg::launch(k_gat_project_tiled<Q>, grid_t, 256, smem_t, st, meta, a);    \
     break;
       GP_CASE(1) GP_CASE(2) GP_CASE(4) GP_CASE(8) GP_CASE(16) GP_CASE(32)
 #undef GP_CASE
@@ -1023,17 +1034,17 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
     g.B = W; g.ldb = dout; g.C = z; g.ldc = dout; g.c_base_dev = &meta->own_off[l - 1][d];
     int rc = dense_gemm_rows(g, max_rows, st);
     if (rc) return rc;
-    k_gat_scores<<<clamp_grid(div_up(max_rows * heads, 8), kSMs * 8), 256, 0, st>>>(meta, a);
+    ::sg::launch(k_gat_scores, clamp_grid(div_up(max_rows * heads, 8), kSMs * 8), 256, 0, st, meta, a);
     SG_CHECK_LAUNCH("k_gat_scores");
     return SG_OK;
   }
   const int grid = clamp_grid(div_up(max_rows, PTR), kSMs * 4);
   if (dout % 4 == 0) {
     SG_CUDA(allow_max_smem<k_gat_project<true>>());
-    k_gat_project<true><<<grid, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_gat_project<true>, grid, 256, smem, st, meta, a);
   } else {
     SG_CUDA(allow_max_smem<k_gat_project<false>>());
-    k_gat_project<false><<<grid, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_gat_project<false>, grid, 256, smem, st, meta, a);
   }
   SG_CHECK_LAUNCH("k_gat_project");
   return SG_OK;
@@ -1080,7 +1091,7 @@ extern "C" int sg_gat_combine(const void* split_ws, const SgSplitLayout* lay, in
   a.final_ = final_layer;
   a.voff_l = y.voff[l]; a.contrib = I32p(y.o_contrib);
   a.loc_m = loc_m; a.loc_s = loc_s; a.loc_U = loc_U; a.recv = recv; a.md = md; a.num = num; a.h = h;
-  k_gat_combine<<<clamp_grid(div_up(max_rows * dout, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  ::sg::launch(k_gat_combine, clamp_grid(div_up(max_rows * dout, 256), kSMs * 8), 256, 0, (cudaStream_t)stream, meta, a);
   SG_CHECK_LAUNCH("k_gat_combine");
   return SG_OK;
 }
@@ -1097,7 +1108,7 @@ extern "C" int sg_gat_alpha(const void* split_ws, const SgSplitLayout* lay, int3
   a.l = l; a.d = d; a.heads = heads; a.slope = slope; a.eoff_li = y.eoff[l - 1]; a.pbase_l = y.pbase[l];
   a.ldst = I32p(y.o_ldst); a.sendpos = I32p(y.o_sendpos);
   a.pre_e = pre_e; a.md = md; a.md_recv = md_recv; a.alpha = alpha;
-  k_gat_alpha<<<clamp_grid(div_up(max_edges * heads, 256), kSMs * 8), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  ::sg::launch(k_gat_alpha, clamp_grid(div_up(max_edges * heads, 256), kSMs * 8), 256, 0, (cudaStream_t)stream, meta, a);
   SG_CHECK_LAUNCH("k_gat_alpha");
   return SG_OK;
 }
@@ -1110,7 +1121,7 @@ extern "C" int sg_gat_bwd_rows(const void* split_ws, const SgSplitLayout* lay, i
   GAT_HEADS_CHECK(dout, heads);
   if (max_rows <= 0) return SG_OK;
   BRowsArgs a{l, d, dout, heads, final_layer, d_h, num, dnc};
-  k_gat_bwd_rows<<<clamp_grid(div_up(max_rows * heads, 256), kSMs * 4), 256, 0, (cudaStream_t)stream>>>(meta, a);
+  ::sg::launch(k_gat_bwd_rows, clamp_grid(div_up(max_rows * heads, 256), kSMs * 4), 256, 0, (cudaStream_t)stream, meta, a);
   SG_CHECK_LAUNCH("k_gat_bwd_rows");
   return SG_OK;
 }
@@ -1164,12 +1175,12 @@ extern "C" int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, in
   const int grid = clamp_grid(div_up(max_rows, 8), kSMs * 8);
   const int q = dout / (4 * heads);
   const bool v4 = dout % (4 * heads) == 0 && (q & (q - 1)) == 0 && (heads & (heads - 1)) == 0;
-  if (v4 && dout <= 16) k_gat_bwd_src<4, 4><<<grid, 256, 0, st>>>(meta, a);
-  else if (v4 && dout <= 32) k_gat_bwd_src<4, 8><<<grid, 256, 0, st>>>(meta, a);
-  else if (v4 && dout <= 64) k_gat_bwd_src<4, 16><<<grid, 256, 0, st>>>(meta, a);
-  else if (v4 && dout <= 128) k_gat_bwd_src<4, 32><<<grid, 256, 0, st>>>(meta, a);
-  else if (heads == 1 && dout <= 8) k_gat_bwd_src<1, 8><<<grid, 256, 0, st>>>(meta, a);
-  else if (heads == 1 && dout <= 32) k_gat_bwd_src<1, 32><<<grid, 256, 0, st>>>(meta, a);
+  if (v4 && dout <= 16) ::sg::launch(k_gat_bwd_src<4, 4>, grid, 256, 0, st, meta, a);
+  else if (v4 && dout <= 32) ::sg::launch(k_gat_bwd_src<4, 8>, grid, 256, 0, st, meta, a);
+  else if (v4 && dout <= 64) ::sg::launch(k_gat_bwd_src<4, 16>, grid, 256, 0, st, meta, a);
+  else if (v4 && dout <= 128) ::sg::launch(k_gat_bwd_src<4, 32>, grid, 256, 0, st, meta, a);
+  else if (heads == 1 && dout <= 8) ::sg::launch(k_gat_bwd_src<1, 8>, grid, 256, 0, st, meta, a);
+  else if (heads == 1 && dout <= 32) ::sg::launch(k_gat_bwd_src<1, 32>, grid, 256, 0, st, meta, a);
   else {
     set_error("gat_bwd_src: unsupported width/heads");
     return SG_ERR_ARG;
@@ -1209,7 +1220,7 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
     t.P = partial; t.pstride = (int64_t)w * dout + 2 * dout; t.p_off = 0; t.nsplit = nblocks;
     int rc = dense_gemm_tn_partial(t, st);
     if (rc) return rc;
-    k_gat_attn_partial<<<nblocks, 256, 0, st>>>(meta, a, nblocks);
+    ::sg::launch(k_gat_attn_partial, nblocks, 256, 0, st, meta, a, nblocks);
     SG_CHECK_LAUNCH("k_gat_attn_partial");
     if (d_prev) {
       GemmArgs g;
@@ -1225,10 +1236,10 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
   }
   if (t4) {
     SG_CUDA(allow_max_smem<k_gat_bwd_param<true>>());
-    k_gat_bwd_param<true><<<nblocks, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_gat_bwd_param<true>, nblocks, 256, smem, st, meta, a);
   } else {
     SG_CUDA(allow_max_smem<k_gat_bwd_param<false>>());
-    k_gat_bwd_param<false><<<nblocks, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_gat_bwd_param<false>, nblocks, 256, smem, st, meta, a);
   }
   SG_CHECK_LAUNCH("k_gat_bwd_param");
   return SG_OK;

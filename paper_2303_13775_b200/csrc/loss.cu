@@ -34,6 +34,7 @@ struct LossArgs {
 };
 
 __global__ void __launch_bounds__(256) k_cls_loss(const SgMeta* __restrict__ meta, LossArgs a) {
+  SG_PDL_ENTRY();
   extern __shared__ float smem[];
   const int hid = a.hid, C = a.ncls, cp = C + 1;
   float* w_s = smem;                // [hid][C] when staged
@@ -154,6 +155,7 @@ struct DevPtrs {
 // Block = 32 output columns x 8 warps; warp w sums partial rows b = w, w+8, ...
 // (4 loads in flight), then the 8 warp sums are added in warp order.
 __global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs) {
+  SG_PDL_ENTRY();
   __shared__ float red[8][33];
   const int jb = blockIdx.y;
   const float* p = (const float*)jobs.v[4 * jb + 0];
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs) {
 
 __global__ void k_sum_sgd(float* __restrict__ params, float* __restrict__ gout, DevPtrs gptrs,
                           int ndev, int64_t n, float scale) {
+  SG_PDL_ENTRY();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     float s = ((const float*)gptrs.v[0])[k];
@@ -232,7 +235,7 @@ extern "C" int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32
   SG_REQUIRE(smem <= 227 * 1024, "cls_loss: hidden too large for shared memory");
   cudaStream_t st = (cudaStream_t)stream;
   SG_CUDA(allow_max_smem<k_cls_loss>());
-  k_cls_loss<<<nblocks, 256, smem, st>>>((const SgMeta*)(base + y.o_meta), a);
+  ::sg::launch(k_cls_loss, nblocks, 256, smem, st, (const SgMeta*)(base + y.o_meta), a);
   SG_CHECK_LAUNCH("k_cls_loss");
   return SG_OK;
 }
@@ -247,7 +250,7 @@ extern "C" int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t m
     memset(&jb, 0, sizeof(jb));
     memcpy(jb.v, jobs + 4 * j0, sizeof(int64_t) * 4 * nj);
     dim3 grid(clamp_grid(div_up(max_n, 32), kSMs * 2), nj);
-    k_reduce_partials<<<grid, 256, 0, (cudaStream_t)stream>>>(jb);
+    ::sg::launch(k_reduce_partials, grid, 256, 0, (cudaStream_t)stream, jb);
     SG_CHECK_LAUNCH("k_reduce_partials");
   }
   return SG_OK;
@@ -260,8 +263,7 @@ extern "C" int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_p
   DevPtrs gp;
   memset(&gp, 0, sizeof(gp));
   for (int d = 0; d < n_dev; ++d) gp.v[d] = grad_ptrs[d];
-  k_sum_sgd<<<clamp_grid(div_up(n, 256), kSMs * 4), 256, 0, (cudaStream_t)stream>>>(
-      params, grads_out, gp, n_dev, n, scale);
+  ::sg::launch(k_sum_sgd, clamp_grid(div_up(n, 256), kSMs * 4), 256, 0, (cudaStream_t)stream, params, grads_out, gp, n_dev, n, scale);
   SG_CHECK_LAUNCH("k_sum_sgd");
   return SG_OK;
 }

@@ -23,6 +23,8 @@
 //                       gradients from the push-from-owner payload (fused
 //                       unpack).
 // All arithmetic is FP32 (parity target rel 1e-4 vs the float64 reference).
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -91,6 +93,7 @@ struct AggArgs {
 // once (both index hops in parallel), then issues the row loads back to back.
 template <int VEC, int LPR, int EG, int NCH>
 __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ meta, AggArgs a) {
+  SG_PDL_ENTRY();
   using V = VecT<VEC>;
   using T = typename V::T;
   constexpr int RL = LPR * EG;
@@ -199,7 +202,7 @@ template <int VEC, int LPR, int EG, int NCH>
 int launch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStream_t st) {
   constexpr int RPB = 8 * (32 / (LPR * EG));  // rows per 256-thread block
   const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
-  k_sage_agg<VEC, LPR, EG, NCH><<<grid, 256, 0, st>>>(meta, a);
+  ::sg::launch(k_sage_agg<VEC, LPR, EG, NCH>, grid, 256, 0, st, meta, a);
   SG_CHECK_LAUNCH("k_sage_agg");
   return SG_OK;
 }
@@ -230,6 +233,7 @@ struct FusedArgs {
 
 template <int LPR, int EG>
 __global__ void __launch_bounds__(256) k_sage_agg_mean(const SgMeta* __restrict__ meta, FusedArgs a) {
+  SG_PDL_ENTRY();
   constexpr int RL = LPR * EG;
   constexpr int RPW = 32 / RL;
   const int w = a.w;
@@ -316,7 +320,7 @@ template <int LPR, int EG>
 int launch_agg_mean(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
   constexpr int RPB = 8 * (32 / (LPR * EG));
   const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
-  k_sage_agg_mean<LPR, EG><<<grid, 256, 0, st>>>(meta, a);
+  ::sg::launch(k_sage_agg_mean<LPR, EG>, grid, 256, 0, st, meta, a);
   SG_CHECK_LAUNCH("k_sage_agg_mean");
   return SG_OK;
 }
@@ -342,6 +346,7 @@ struct LinArgs {
 // order through shared memory (deterministic).
 template <int NQ>
 __global__ void __launch_bounds__(256, 3) k_sage_linear(const SgMeta* __restrict__ meta, LinArgs a) {
+  SG_PDL_ENTRY();
   constexpr int TM = 32;
   constexpr int TMP = TM + 4;
   constexpr int NT = (TM / 4) * NQ;  // register tiles per K slice
@@ -457,9 +462,195 @@ int launch_linear_q(const SgMeta* meta, const LinArgs& a, int64_t max_rows, cuda
   const cudaError_t attr = allow_max_smem<k_sage_linear<NQ>>();
   SG_CUDA(attr);
   const int grid = clamp_grid(div_up(max_rows, TM), kSMs * 8);
-  k_sage_linear<NQ><<<grid, 256, smem, st>>>(meta, a);
+  ::sg::launch(k_sage_linear<NQ>, grid, 256, smem, st, meta, a);
   SG_CHECK_LAUNCH("k_sage_linear");
   return SG_OK;
+}
+
+// ---------------------------------------------------------------- one-kernel layer (g == 1)
+// Aggregation and dense transform in ONE kernel: a 32-row tile's [hs | mean]
+// operand never leaves the SM. Each warp aggregates 4 destination rows; per
+// row all in-edges' 128-bit row loads (up to UN per lane) are in flight at
+// once and the NEXT row's edge indices are fetched while they land (the
+// rowbeg -> lsrc -> src_row chain is off the critical path). Rows go
+// transposed into smem ([2w][TM+4]) and to global (mean, hs: the backward's
+// operands); then the same register-tiled FP32 GEMM as k_sage_linear.
+template <int NQ, int UN, int RPW, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restrict__ meta, FusedArgs a) {
+  SG_PDL_ENTRY();
+  constexpr int TM = 8 * RPW;  // rows per tile (RPW per warp)
+  constexpr int TMP = TM + 4;
+  constexpr int NT = (TM / 4) * NQ;
+  constexpr int NS = 256 / NT;
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, dout = a.dout, K = 2 * w;
+  const int l = a.l, d = a.d;
+  float* W_s = smem;            // [2w][dout]
+  float* A_s = W_s + K * dout;  // [2w][TMP] transposed; reused as the slice reduction
+  for (int i = threadIdx.x; i < w * dout / 4; i += 256) {
+    reinterpret_cast<float4*>(W_s)[i] = reinterpret_cast<const float4*>(a.ws)[i];
+    reinterpret_cast<float4*>(W_s)[w * dout / 4 + i] = reinterpret_cast<const float4*>(a.wn)[i];
+  }
+  const int n = meta->n_own[l][d];
+  const int own0 = meta->own_off[l][d];
+  const int prev0 = meta->own_off[l - 1][d];
+  const int64_t rb = a.rbase_li + own0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int col = lane * 4;
+  const bool colok = col < w;
+  const int tile = threadIdx.x % NT, ks = threadIdx.x / NT;
+  const int rt = tile / NQ, jq = tile - rt * NQ;
+  const int kchunk = (K + NS - 1) / NS;
+  const int kb = ks * kchunk, ke = min(K, kb + kchunk);
+  auto edge_row = [&](int j) {
+    int r = prev0 + a.lsrc[a.eoff_li + j];
+    return a.src_row ? a.src_row[r] : r;
+  };
+  for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
+    // ---- aggregation: warp wid owns tile rows [wid*RPW, wid*RPW + RPW)
+    const int q0 = r0 + wid * RPW;
+    int be = 0;
+    if (lane < 2 * RPW && q0 + (lane >> 1) < n)
+      be = (lane & 1) ? a.rowend[rb + q0 + (lane >> 1)] : a.rowbeg[rb + q0 + (lane >> 1)];
+    int b = __shfl_sync(0xffffffffu, be, 0), e = __shfl_sync(0xffffffffu, be, 1);
+    int rnext = (q0 < n && lane < e - b) ? edge_row(b + lane) : 0;
+    __syncthreads();  // previous tile's GEMM done with A_s
+    for (int i = 0; i < RPW; ++i) {
+      const int q = q0 + i;
+      if (q >= n) break;  // warp-uniform
+      const int rcur = rnext;
+      const int bc = b, ec = e;
+      const int64_t G = own0 + q;
+      int rself = prev0 + a.selfrow[a.voff_l + G];
+      if (a.src_row) rself = a.src_row[rself];
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
+      // next row's bounds + first index hop, issued before this row's loads
+      int nb = 0, ne = 0, lnext = 0;
+      if (i + 1 < RPW && q + 1 < n) {
+        nb = __shfl_sync(0xffffffffu, be, 2 * (i + 1));
+        ne = __shfl_sync(0xffffffffu, be, 2 * (i + 1) + 1);
+        if (lane < ne - nb) lnext = prev0 + a.lsrc[a.eoff_li + nb + lane];
+      }
+      const int cnt0 = min(32, ec - bc);
+      for (int kk = 0; kk < cnt0; kk += UN) {
+        float4 v[UN];
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          const int k = kk + u;
+          const int rr = __shfl_sync(0xffffffffu, rcur, k < 32 ? k : 31);
+          v[u] = (k < cnt0 && colok) ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * w + col))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (kk == 0 && colok) hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col));
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
+        }
+      }
+      // rows with more than 32 in-edges: remaining rounds (rare in forward)
+      for (int jb = bc + 32; jb < ec; jb += 32) {
+        const int rr0 = (jb + lane < ec) ? edge_row(jb + lane) : 0;
+        const int cnt = min(32, ec - jb);
+        for (int k = 0; k < cnt; ++k) {
+          const int rr = __shfl_sync(0xffffffffu, rr0, k);
+          if (colok) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * w + col));
+            acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+          }
+        }
+      }
+      if (ec == bc && colok) hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col));
+      // second index hop of the next row, overlapping this row's tail
+      if (i + 1 < RPW && q + 1 < n) {
+        rnext = (lane < ne - nb) ? (a.src_row ? a.src_row[lnext] : lnext) : 0;
+        b = nb;
+        e = ne;
+      }
+      const float cntf = (float)(ec - bc);
+      const float inv = 1.0f / cntf;
+      const float4 mn = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+      const int rr = wid * RPW + i;
+      if (colok) {
+        *reinterpret_cast<float4*>(a.mean + G * w + col) = mn;
+        if (a.hs) *reinterpret_cast<float4*>(a.hs + G * w + col) = hv;
+        A_s[(col + 0) * TMP + rr] = hv.x;
+        A_s[(col + 1) * TMP + rr] = hv.y;
+        A_s[(col + 2) * TMP + rr] = hv.z;
+        A_s[(col + 3) * TMP + rr] = hv.w;
+        A_s[(w + col + 0) * TMP + rr] = mn.x;
+        A_s[(w + col + 1) * TMP + rr] = mn.y;
+        A_s[(w + col + 2) * TMP + rr] = mn.z;
+        A_s[(w + col + 3) * TMP + rr] = mn.w;
+      }
+      if (lane == 0) a.counts[G] = cntf;
+    }
+    __syncthreads();
+    // ---- dense transform from smem (rows past n hold garbage: never stored)
+    float acc2[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc2[i][0] = acc2[i][1] = acc2[i][2] = acc2[i][3] = 0.f;
+#pragma unroll 4
+    for (int k = kb; k < ke; ++k) {
+      const float4 av = *reinterpret_cast<const float4*>(A_s + k * TMP + 4 * rt);
+      const float4 wv = *reinterpret_cast<const float4*>(W_s + k * dout + 4 * jq);
+      const float ar[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc2[i][0] = fmaf(ar[i], wv.x, acc2[i][0]);
+        acc2[i][1] = fmaf(ar[i], wv.y, acc2[i][1]);
+        acc2[i][2] = fmaf(ar[i], wv.z, acc2[i][2]);
+        acc2[i][3] = fmaf(ar[i], wv.w, acc2[i][3]);
+      }
+    }
+    __syncthreads();
+    float* red = A_s;  // [NS][TM][dout]
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<float4*>(red + (ks * TM + 4 * rt + i) * dout + 4 * jq) =
+          make_float4(acc2[i][0], acc2[i][1], acc2[i][2], acc2[i][3]);
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TM * dout; idx += 256) {
+      const int r = idx / dout, j = idx - r * dout;
+      if (r0 + r >= n) continue;
+      float v = a.bias[j];
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) v += red[(s2 * TM + r) * dout + j];
+      a.h[(int64_t)(own0 + r0 + r) * dout + j] = a.final_ ? v : fmaxf(v, 0.f);
+    }
+  }
+}
+
+template <int NQ, int UN, int RPW, int MINB>
+int launch_layer_q(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
+  constexpr int TM = 8 * RPW;
+  constexpr int NS = 256 / ((TM / 4) * NQ);
+  const size_t a_floats = std::max<size_t>(2 * (size_t)a.w * (TM + 4), (size_t)NS * TM * a.dout);
+  const size_t smem = sizeof(float) * (2 * (size_t)a.w * a.dout + a_floats);
+  if (smem > 227 * 1024) {
+    set_error("sage_layer: width too large");
+    return SG_ERR_ARG;
+  }
+  const cudaError_t attr = allow_max_smem<k_sage_layer<NQ, UN, RPW, MINB>>();
+  SG_CUDA(attr);
+  int per_sm = MINB;
+  const size_t by_smem = (228 * 1024) / (smem + 1024);
+  if ((int)by_smem < per_sm) per_sm = (int)std::max<size_t>(1, by_smem);
+  const int grid = clamp_grid(div_up(max_rows, TM), kSMs * per_sm);
+  ::sg::launch(k_sage_layer<NQ, UN, RPW, MINB>, grid, 256, smem, st, meta, a);
+  SG_CHECK_LAUNCH("k_sage_layer");
+  return SG_OK;
+}
+
+template <int UN, int RPW, int MINB>
+int launch_layer(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
+  switch (a.dout / 4) {
+    case 1: return launch_layer_q<1, UN, RPW, MINB>(meta, a, max_rows, st);
+    case 2: return launch_layer_q<2, UN, RPW, MINB>(meta, a, max_rows, st);
+    case 4: return launch_layer_q<4, UN, RPW, MINB>(meta, a, max_rows, st);
+    case 8: return launch_layer_q<8, UN, RPW, MINB>(meta, a, max_rows, st);
+    default: set_error("sage_layer: dout must be 4, 8, 16 or 32"); return SG_ERR_ARG;
+  }
 }
 
 int launch_linear(const SgMeta* meta, const LinArgs& a, int64_t max_rows, cudaStream_t st) {
@@ -516,6 +707,7 @@ struct UpdArgs {
 
 template <bool Q4>
 __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ meta, UpdArgs a) {
+  SG_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, wp = w + 1;
   const int wsz = a.no_linear ? 0 : w * dout;
@@ -652,6 +844,7 @@ struct BwdArgs {
 
 template <bool Q4>
 __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict__ meta, BwdArgs a) {
+  SG_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, wp = w + 1;
   const int wst = Q4 ? dout + 4 : dout + 1;  // padded weight row stride
@@ -835,6 +1028,7 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
 // tile (2 LDS.128 per 16 FFMA), per-block partial in the parameter layout.
 template <int NQ>
 __global__ void __launch_bounds__(256) k_sage_wgrad(const SgMeta* __restrict__ meta, BwdArgs a) {
+  SG_PDL_ENTRY();
   constexpr int TR = 32;
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, K = 2 * w, KP = K + 4, wst = dout + 4;
@@ -964,6 +1158,7 @@ struct ScatArgs {
 
 template <int VEC, int LPR, int NCH>
 __global__ void __launch_bounds__(256) k_sage_scatter(const SgMeta* __restrict__ meta, ScatArgs a) {
+  SG_PDL_ENTRY();
   using V = VecT<VEC>;
   using T = typename V::T;
   constexpr int NG = 32 / LPR;  // lane groups per warp, each takes every NG-th edge
@@ -1039,7 +1234,7 @@ __global__ void __launch_bounds__(256) k_sage_scatter(const SgMeta* __restrict__
 template <int VEC, int LPR, int NCH>
 int launch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaStream_t st) {
   const int grid = clamp_grid(div_up(max_rows, 8), kSMs * 8);
-  k_sage_scatter<VEC, LPR, NCH><<<grid, 256, 0, st>>>(meta, a);
+  ::sg::launch(k_sage_scatter<VEC, LPR, NCH>, grid, 256, 0, st, meta, a);
   SG_CHECK_LAUNCH("k_sage_scatter");
   return SG_OK;
 }
@@ -1137,7 +1332,16 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   a.rowbeg = I32(y.o_rowbeg); a.rowend = I32(y.o_rowend); a.lsrc = I32(y.o_lsrc);
   a.selfrow = I32(y.o_selfrow); a.src_row = src_row; a.h_prev = h_prev;
   a.mean = mean; a.counts = counts; a.hs = hs;
+  a.ws = w_self; a.wn = w_neigh; a.bias = bias; a.h = h;
   cudaStream_t st = (cudaStream_t)stream;
+  // wide layers: one kernel (8 loads in flight per lane, 16-row tiles, 4 CTAs/SM)
+  static const int variant = [] {
+    const char* s = getenv("SG_SAGE_LAYER");
+    return s ? atoi(s) : 2;
+  }();
+  if (w > 64 && variant == 2) return launch_layer<8, 2, 4>(meta, a, max_rows, st);
+  if (w > 64 && variant == 3) return launch_layer<8, 2, 2>(meta, a, max_rows, st);
+  if (w > 64 && variant == 4) return launch_layer<8, 4, 3>(meta, a, max_rows, st);
   int rc;
   if (w <= 16) rc = launch_agg_mean<4, 4>(meta, a, max_rows, st);
   else if (w <= 32) rc = launch_agg_mean<8, 4>(meta, a, max_rows, st);
@@ -1176,7 +1380,7 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
     cudaStream_t st = (cudaStream_t)stream;
     const int grid = clamp_grid(div_up(max_rows, UTR), kSMs * 3);
     SG_CUDA(allow_max_smem<k_sage_update<false>>());
-    k_sage_update<false><<<grid, 256, sm, st>>>(meta, u);
+    ::sg::launch(k_sage_update<false>, grid, 256, sm, st, meta, u);
     SG_CHECK_LAUNCH("k_sage_update(mean)");
     GemmArgs g1;
     memset(&g1, 0, sizeof(g1));
@@ -1231,10 +1435,10 @@ extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, in
   const int grid = clamp_grid(div_up(max_rows, UTR), kSMs * 3);
   if (dout % 4 == 0) {
     SG_CUDA(allow_max_smem<k_sage_update<true>>());
-    k_sage_update<true><<<grid, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_sage_update<true>, grid, 256, smem, st, meta, a);
   } else {
     SG_CUDA(allow_max_smem<k_sage_update<false>>());
-    k_sage_update<false><<<grid, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_sage_update<false>, grid, 256, smem, st, meta, a);
   }
   SG_CHECK_LAUNCH("k_sage_update");
   if (tiled) {
@@ -1330,10 +1534,10 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
     cudaStream_t st2 = (cudaStream_t)stream;
     cudaError_t attr = cudaSuccess;
     switch (dout / 4) {
-      case 1: attr = allow_max_smem<k_sage_wgrad<1>>(); SG_CUDA(attr); k_sage_wgrad<1><<<nblocks, 256, sm2, st2>>>(meta, a); break;
-      case 2: attr = allow_max_smem<k_sage_wgrad<2>>(); SG_CUDA(attr); k_sage_wgrad<2><<<nblocks, 256, sm2, st2>>>(meta, a); break;
-      case 4: attr = allow_max_smem<k_sage_wgrad<4>>(); SG_CUDA(attr); k_sage_wgrad<4><<<nblocks, 256, sm2, st2>>>(meta, a); break;
-      default: attr = allow_max_smem<k_sage_wgrad<8>>(); SG_CUDA(attr); k_sage_wgrad<8><<<nblocks, 256, sm2, st2>>>(meta, a); break;
+      case 1: attr = allow_max_smem<k_sage_wgrad<1>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<1>, nblocks, 256, sm2, st2, meta, a); break;
+      case 2: attr = allow_max_smem<k_sage_wgrad<2>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<2>, nblocks, 256, sm2, st2, meta, a); break;
+      case 4: attr = allow_max_smem<k_sage_wgrad<4>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<4>, nblocks, 256, sm2, st2, meta, a); break;
+      default: attr = allow_max_smem<k_sage_wgrad<8>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<8>, nblocks, 256, sm2, st2, meta, a); break;
     }
     SG_CHECK_LAUNCH("k_sage_wgrad");
     return SG_OK;
@@ -1345,10 +1549,10 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   cudaStream_t st = (cudaStream_t)stream;
   if (q4) {
     SG_CUDA(allow_max_smem<k_sage_bwd_rows<true>>());
-    k_sage_bwd_rows<true><<<nblocks, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_sage_bwd_rows<true>, nblocks, 256, smem, st, meta, a);
   } else {
     SG_CUDA(allow_max_smem<k_sage_bwd_rows<false>>());
-    k_sage_bwd_rows<false><<<nblocks, 256, smem, st>>>(meta, a);
+    ::sg::launch(k_sage_bwd_rows<false>, nblocks, 256, smem, st, meta, a);
   }
   SG_CHECK_LAUNCH("k_sage_bwd_rows");
   return SG_OK;

@@ -23,6 +23,7 @@ constexpr int RADIX = 256;
 __global__ void __launch_bounds__(RS_THREADS) rs_hist(const uint32_t* __restrict__ keys,
                                                       const int32_t* __restrict__ n_dev, int shift,
                                                       int ntiles, int32_t* __restrict__ hist) {
+  SG_PDL_ENTRY();
   __shared__ int cnt[RADIX];
   const int t = blockIdx.x;
   const int n = *n_dev;
@@ -39,6 +40,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_hist(const uint32_t* __restrict
 // and the digit total. The scatter kernel scans the 256 totals itself.
 __global__ void __launch_bounds__(256) rs_scan(int32_t* __restrict__ hist, int ntiles,
                                                int32_t* __restrict__ dtot) {
+  SG_PDL_ENTRY();
   __shared__ int wsum[8];
   __shared__ int carry;
   const int dg = blockIdx.x;
@@ -76,6 +78,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint32_t* __restr
                                                          const int32_t* __restrict__ dtot,
                                                          uint32_t* __restrict__ kout,
                                                          int32_t* __restrict__ vout) {
+  SG_PDL_ENTRY();
   __shared__ int wcnt[RS_THREADS / 32][RADIX];
   __shared__ int dsum[8];
   const int t = blockIdx.x;
@@ -142,6 +145,7 @@ __global__ void __launch_bounds__(RS_THREADS) rs_scatter(const uint32_t* __restr
 __global__ void k_copy_pairs(const uint32_t* __restrict__ ks, const int32_t* __restrict__ vs,
                              const int32_t* __restrict__ n_dev, uint32_t* __restrict__ kd,
                              int32_t* __restrict__ vd) {
+  SG_PDL_ENTRY();
   const int n = *n_dev;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     kd[i] = ks[i];
@@ -164,6 +168,7 @@ __global__ void k_edge_row_keys(const SgMeta* __restrict__ meta, const int32_t* 
                                 int d, int lmin, int mode, int val_mode, KeyBase kb,
                                 uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
                                 int32_t* __restrict__ n_dev) {
+  SG_PDL_ENTRY();
   const int L = meta->L;
   const int64_t e0 = meta->eoff[lmin - 1], e1 = meta->eoff[L];
   int flat0[SG_MAXL];
@@ -200,6 +205,7 @@ __global__ void k_edge_row_keys(const SgMeta* __restrict__ meta, const int32_t* 
 // Run boundaries of a sorted key array -> [beg, end) per key.
 __global__ void k_runs(const uint32_t* __restrict__ keys, const int32_t* __restrict__ n_dev,
                        int32_t* __restrict__ beg, int32_t* __restrict__ end) {
+  SG_PDL_ENTRY();
   const int n = *n_dev;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint32_t k = keys[i];
@@ -236,17 +242,17 @@ extern "C" int sg_sort_pairs(void* ws, int64_t n_max, const int32_t* n_dev, uint
   int32_t* vb = v2;
   for (int p = 0; p < passes; ++p) {
     const int shift = 8 * p;
-    rs_hist<<<ntiles, RS_THREADS, 0, st>>>(ka, n_dev, shift, ntiles, hist);
+    ::sg::launch(rs_hist, ntiles, RS_THREADS, 0, st, ka, n_dev, shift, ntiles, hist);
     SG_CHECK_LAUNCH("rs_hist");
-    rs_scan<<<RADIX, 256, 0, st>>>(hist, ntiles, dtot);
+    ::sg::launch(rs_scan, RADIX, 256, 0, st, hist, ntiles, dtot);
     SG_CHECK_LAUNCH("rs_scan");
-    rs_scatter<<<ntiles, RS_THREADS, 0, st>>>(ka, va, n_dev, shift, ntiles, hist, dtot, kb, vb);
+    ::sg::launch(rs_scatter, ntiles, RS_THREADS, 0, st, ka, va, n_dev, shift, ntiles, hist, dtot, kb, vb);
     SG_CHECK_LAUNCH("rs_scatter");
     std::swap(ka, kb);
     std::swap(va, vb);
   }
   if (ka != keys) {
-    k_copy_pairs<<<clamp_grid(div_up(n_max, 256), kSMs * 4), 256, 0, st>>>(ka, va, n_dev, keys,
+    ::sg::launch(k_copy_pairs, clamp_grid(div_up(n_max, 256), kSMs * 4), 256, 0, st, ka, va, n_dev, keys,
                                                                           vals);
     SG_CHECK_LAUNCH("k_copy_pairs");
   }
@@ -278,13 +284,12 @@ extern "C" int sg_src_csr(const void* split_ws, const SgSplitLayout* lay, int32_
   SG_CUDA(cudaMemsetAsync(srcend, 0, 4 * acc, st));
   const int64_t e_span = y.eoff[y.L] - y.eoff[lmin - 1];
   for (int l = 0; l <= y.L + 1; ++l) kb.pbase[l] = y.pbase[l];
-  k_edge_row_keys<<<clamp_grid(div_up(e_span, 256), kSMs * 8), 256, 0, st>>>(
-      meta, (const int32_t*)(base + y.o_lsrc), (const int32_t*)(base + y.o_ldst),
+  ::sg::launch(k_edge_row_keys, clamp_grid(div_up(e_span, 256), kSMs * 8), 256, 0, st, meta, (const int32_t*)(base + y.o_lsrc), (const int32_t*)(base + y.o_ldst),
       (const int32_t*)(base + y.o_sendpos), d, lmin, 0, val_mode, kb, keys, perm, n_dev);
   SG_CHECK_LAUNCH("k_edge_row_keys(src)");
   int rc = sg_sort_pairs(sort_ws, n_max, n_dev, keys, perm, bits, stream);
   if (rc) return rc;
-  k_runs<<<clamp_grid(div_up(n_max, 256), kSMs * 8), 256, 0, st>>>(keys, n_dev, srcbeg, srcend);
+  ::sg::launch(k_runs, clamp_grid(div_up(n_max, 256), kSMs * 8), 256, 0, st, keys, n_dev, srcbeg, srcend);
   SG_CHECK_LAUNCH("k_runs(src)");
   return SG_OK;
 }
@@ -303,13 +308,11 @@ extern "C" int sg_dst_csr(void* split_ws, const SgSplitLayout* lay, int32_t d, v
   for (int l = 1; l <= y.L; ++l) kb.v[l - 1] = y.rbase[l - 1];
   int bits = 0;
   while ((int64_t(1) << bits) < y.rbase[y.L]) ++bits;
-  k_edge_row_keys<<<clamp_grid(div_up(y.nEtot, 256), kSMs * 8), 256, 0, st>>>(
-      meta, (const int32_t*)(base + y.o_ldst), nullptr, nullptr, d, 1, 1, 0, kb, keys, perm, n_dev);
+  ::sg::launch(k_edge_row_keys, clamp_grid(div_up(y.nEtot, 256), kSMs * 8), 256, 0, st, meta, (const int32_t*)(base + y.o_ldst), nullptr, nullptr, d, 1, 1, 0, kb, keys, perm, n_dev);
   SG_CHECK_LAUNCH("k_edge_row_keys(dst)");
   int rc = sg_sort_pairs(sort_ws, n_max, n_dev, keys, perm, bits, stream);
   if (rc) return rc;
-  k_runs<<<clamp_grid(div_up(n_max, 256), kSMs * 8), 256, 0, st>>>(
-      keys, n_dev, (int32_t*)(base + y.o_rowbeg), (int32_t*)(base + y.o_rowend));
+  ::sg::launch(k_runs, clamp_grid(div_up(n_max, 256), kSMs * 8), 256, 0, st, keys, n_dev, (int32_t*)(base + y.o_rowbeg), (int32_t*)(base + y.o_rowend));
   SG_CHECK_LAUNCH("k_runs(dst)");
   return SG_OK;
 }

@@ -78,6 +78,7 @@ __device__ __forceinline__ int layer_of(const int64_t* off, int nl, int64_t i) {
 // Header (capacity offsets) + ACTUAL sizes (device array nV[0..L], nE[0..L-1],
 // or the capacities when sizes == nullptr) -> SgMeta with zero counts.
 __global__ void k_meta_init(MetaHeader h, const int64_t* __restrict__ sizes, SgMeta* meta) {
+  SG_PDL_ENTRY();
   int32_t* w = reinterpret_cast<int32_t*>(meta);
   const int nwords = sizeof(SgMeta) / 4;
   for (int i = threadIdx.x; i < nwords; i += blockDim.x) w[i] = 0;
@@ -106,6 +107,7 @@ __global__ void k_owner_keys(const int32_t* __restrict__ V, MetaHeader h, int64_
                              int64_t nV0, const uint8_t* __restrict__ asn, int64_t n_asn,
                              const uint32_t* __restrict__ cache_bits, int g,
                              uint8_t* __restrict__ keys, SgMeta* meta) {
+  SG_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nVtot;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int l = layer_of(h.voff, h.L + 1, i);
@@ -131,6 +133,7 @@ __global__ void k_owner_keys(const int32_t* __restrict__ V, MetaHeader h, int64_
 __global__ void __launch_bounds__(MS_THREADS) ms_count(const uint8_t* __restrict__ keys, SegDesc sd,
                                                        const SgMeta* __restrict__ meta,
                                                        int32_t* __restrict__ tilecnt) {
+  SG_PDL_ENTRY();
   __shared__ int cnt[MAXKEY];
   const int64_t t = blockIdx.x;
   const int s = seg_of_tile(sd, t);
@@ -150,6 +153,7 @@ __global__ void __launch_bounds__(MS_THREADS) ms_count(const uint8_t* __restrict
 __global__ void ms_scan(SegDesc sd, const int32_t* __restrict__ tilecnt,
                         int32_t* __restrict__ tilebase, int32_t* __restrict__ keyoff, int mode,
                         SgMeta* meta) {
+  SG_PDL_ENTRY();
   __shared__ int tot[MAXKEY];
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -201,6 +205,7 @@ __global__ void __launch_bounds__(MS_THREADS) ms_scatter(const uint8_t* __restri
                                                          const int32_t* __restrict__ keyoff,
                                                          int32_t* __restrict__ rank_out,
                                                          int32_t* __restrict__ grouped_out) {
+  SG_PDL_ENTRY();
   __shared__ int wcnt[MS_THREADS / 32][MAXKEY];
   __shared__ int wbase[MS_THREADS / 32][MAXKEY];
   const int64_t t = blockIdx.x;
@@ -255,6 +260,7 @@ __global__ void k_edge_keys(const int32_t* __restrict__ esrc, const int32_t* __r
                             MetaHeader h, const SgMeta* __restrict__ meta,
                             const uint8_t* __restrict__ keys, uint8_t* __restrict__ ekey,
                             uint32_t* __restrict__ pmask, int32_t* __restrict__ egrouped_identity) {
+  SG_PDL_ENTRY();
   const int64_t n = h.eoff[h.L];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -271,6 +277,7 @@ __global__ void k_edge_keys(const int32_t* __restrict__ esrc, const int32_t* __r
 
 // g == 1: one device owns every edge, grouping is the identity.
 __global__ void k_single_edge_meta(SgMeta* meta) {
+  SG_PDL_ENTRY();
   const int li = threadIdx.x;
   if (li < meta->L) {
     meta->n_edge[li][0] = (int32_t)meta->nE[li];
@@ -283,6 +290,7 @@ __global__ void k_single_edge_meta(SgMeta* meta) {
 __global__ void k_ref_bits(const int32_t* __restrict__ V, MetaHeader h,
                            const uint32_t* __restrict__ pmask, uint32_t* __restrict__ bm,
                            int64_t words, int clear) {
+  SG_PDL_ENTRY();
   const int64_t b = h.voff[1], e = h.voff[h.L + 1];
   for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -298,6 +306,7 @@ __global__ void k_ref_bits(const int32_t* __restrict__ V, MetaHeader h,
 __global__ void __launch_bounds__(256) k_ref_scan(const uint32_t* __restrict__ bm,
                                                   int32_t* __restrict__ wpre,
                                                   int32_t* __restrict__ ctot) {
+  SG_PDL_ENTRY();
   __shared__ int wsum[8];
   const int64_t c = blockIdx.x;
   const int64_t w0 = c * CHUNK_WORDS + threadIdx.x * 4;
@@ -325,6 +334,7 @@ __global__ void __launch_bounds__(256) k_ref_scan(const uint32_t* __restrict__ b
 // the number of distinct reference vertices.
 __global__ void k_ref_chunks(int32_t* __restrict__ ctot, int64_t chunks_per_layer, int L,
                              SgMeta* meta) {
+  SG_PDL_ENTRY();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int l = 1 + warp; l <= L; l += blockDim.x >> 5) {
     int32_t* c = ctot + (int64_t)(l - 1) * chunks_per_layer;
@@ -349,6 +359,7 @@ __global__ void k_ref_rank(const int32_t* __restrict__ V, MetaHeader h,
                            const uint32_t* __restrict__ pmask, const uint32_t* __restrict__ bm,
                            const int32_t* __restrict__ wpre, const int32_t* __restrict__ cpre,
                            int64_t words, int32_t* __restrict__ uorder) {
+  SG_PDL_ENTRY();
   const int64_t b = h.voff[1], e = h.voff[h.L + 1];
   const int64_t cpl = words / CHUNK_WORDS;
   for (int64_t i = b + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < e;
@@ -383,6 +394,7 @@ __global__ void __launch_bounds__(PAIR_T) k_pair_count(PairDesc pd, const SgMeta
                                                        const uint32_t* __restrict__ pmask,
                                                        const uint8_t* __restrict__ keys,
                                                        int32_t* __restrict__ tilecnt) {
+  SG_PDL_ENTRY();
   __shared__ int cnt[MAXKQ];
   const int64_t t = blockIdx.x;
   const int l = layer_of_pair_tile(pd, t);
@@ -408,6 +420,7 @@ __global__ void __launch_bounds__(PAIR_T) k_pair_count(PairDesc pd, const SgMeta
 // plan's count matrix and every derived offset.
 __global__ void k_pair_scan(PairDesc pd, const int32_t* __restrict__ tilecnt,
                             int32_t* __restrict__ tilebase, SgMeta* meta) {
+  SG_PDL_ENTRY();
   __shared__ int tot[MAXKQ];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int g = pd.g, kq = pd.kq;
@@ -478,6 +491,7 @@ __global__ void __launch_bounds__(PAIR_T) k_pair_scatter(PairDesc pd, const SgMe
                                                          const int32_t* __restrict__ rank,
                                                          const int32_t* __restrict__ tilebase,
                                                          PairOut out) {
+  SG_PDL_ENTRY();
   __shared__ int wcnt[PAIR_T / 32][MAXKQ];
   __shared__ int wbase[PAIR_T / 32][MAXKQ];
   const int64_t t = blockIdx.x;
@@ -550,6 +564,7 @@ __global__ void k_local_edges(const int32_t* __restrict__ esrc, const int32_t* _
                               const int32_t* __restrict__ grouped,
                               const int32_t* __restrict__ egrouped,
                               const int32_t* __restrict__ refrank, LocalOut out) {
+  SG_PDL_ENTRY();
   const int g = h.g;
   const int64_t nE = h.eoff[h.L];
   const int64_t nS = h.voff[h.L + 1] - h.voff[1];  // owned positions of layers 1..L
@@ -595,6 +610,7 @@ __global__ void k_split_single(const int32_t* __restrict__ V, const int32_t* __r
                                int64_t n_asn, int all_cached, int32_t* __restrict__ rank,
                                int32_t* __restrict__ grouped, int32_t* __restrict__ egrouped,
                                LocalOut out) {
+  SG_PDL_ENTRY();
   const int L = h.L;
   const int64_t nVtot = h.voff[L + 1], nE = h.eoff[L];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -778,12 +794,11 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   for (int l = 0; l <= SG_MAXL; ++l) h.rbase[l] = l <= L ? y.rbase[l] : y.rbase[L];
 
   if (g == 1 && dst_grouped && (cache_bits == nullptr || all_cached)) {
-    k_meta_init<<<1, 256, 0, st>>>(h, sizes, meta);
+    ::sg::launch(k_meta_init, 1, 256, 0, st, h, sizes, meta);
     SG_CHECK_LAUNCH("k_meta_init");
     LocalOut lo{P32(y.o_lsrc), P32(y.o_ldst), P32(y.o_rowbeg), P32(y.o_rowend), P32(y.o_selfrow)};
     const int64_t tot = y.nVtot + y.nEtot;
-    k_split_single<<<clamp_grid(div_up(tot, 256), kSMs * 8), 256, 0, st>>>(
-        V, esrc, edst, h, meta, y.n_vertices, all_cached, P32(y.o_rank), P32(y.o_grouped),
+    ::sg::launch(k_split_single, clamp_grid(div_up(tot, 256), kSMs * 8), 256, 0, st, V, esrc, edst, h, meta, y.n_vertices, all_cached, P32(y.o_rank), P32(y.o_grouped),
         P32(y.o_egrouped), lo);
     SG_CHECK_LAUNCH("k_split_single");
     return SG_OK;
@@ -798,13 +813,12 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
     SG_CUDA(cudaMemsetAsync(base + y.o_rowend, 0, 4 * rows_total, st));
   }
 
-  k_meta_init<<<1, 256, 0, st>>>(h, sizes, meta);
+  ::sg::launch(k_meta_init, 1, 256, 0, st, h, sizes, meta);
   SG_CHECK_LAUNCH("k_meta_init");
 
   const int64_t nVtot = y.nVtot, nV0 = y.nV[0];
   if (nVtot > 0) {
-    k_owner_keys<<<clamp_grid(div_up(nVtot, 256), kSMs * 8), 256, 0, st>>>(
-        V, h, nVtot, nV0, asn, y.n_vertices, cache_bits, g, P8(y.o_keys), meta);
+    ::sg::launch(k_owner_keys, clamp_grid(div_up(nVtot, 256), kSMs * 8), 256, 0, st, V, h, nVtot, nV0, asn, y.n_vertices, cache_bits, g, P8(y.o_keys), meta);
     SG_CHECK_LAUNCH("k_owner_keys");
   }
 
@@ -830,13 +844,13 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   int32_t* tb_pos = P32(y.o_tilebase_pos);
   int32_t* keyoff_pos = tb_pos + y.pos_tiles * (g + 1);
   if (y.pos_tiles > 0) {
-    ms_count<<<(int)y.pos_tiles, MS_THREADS, 0, st>>>(P8(y.o_keys), sp, meta, P32(y.o_tiles_pos));
+    ::sg::launch(ms_count, (int)y.pos_tiles, MS_THREADS, 0, st, P8(y.o_keys), sp, meta, P32(y.o_tiles_pos));
     SG_CHECK_LAUNCH("ms_count(pos)");
   }
-  ms_scan<<<sp.nseg, 1024, 0, st>>>(sp, P32(y.o_tiles_pos), tb_pos, keyoff_pos, 0, meta);
+  ::sg::launch(ms_scan, sp.nseg, 1024, 0, st, sp, P32(y.o_tiles_pos), tb_pos, keyoff_pos, 0, meta);
   SG_CHECK_LAUNCH("ms_scan(pos)");
   if (y.pos_tiles > 0) {
-    ms_scatter<<<(int)y.pos_tiles, MS_THREADS, 0, st>>>(P8(y.o_keys), sp, meta, tb_pos, keyoff_pos,
+    ::sg::launch(ms_scatter, (int)y.pos_tiles, MS_THREADS, 0, st, P8(y.o_keys), sp, meta, tb_pos, keyoff_pos,
                                                         P32(y.o_rank), P32(y.o_grouped));
     SG_CHECK_LAUNCH("ms_scatter(pos)");
   }
@@ -844,8 +858,7 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   // edges: key = source device, pair masks
   const int64_t nEtot = y.nEtot;
   if (nEtot > 0) {
-    k_edge_keys<<<clamp_grid(div_up(nEtot, 256), kSMs * 8), 256, 0, st>>>(
-        esrc, edst, h, meta, P8(y.o_keys), P8(y.o_ekey), U32(y.o_pmask),
+    ::sg::launch(k_edge_keys, clamp_grid(div_up(nEtot, 256), kSMs * 8), 256, 0, st, esrc, edst, h, meta, P8(y.o_keys), P8(y.o_ekey), U32(y.o_pmask),
         g == 1 ? P32(y.o_egrouped) : nullptr);
     SG_CHECK_LAUNCH("k_edge_keys");
   }
@@ -867,18 +880,18 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   int32_t* tb_edge = P32(y.o_tilebase_edge);
   int32_t* keyoff_edge = tb_edge + y.edge_tiles * g;
   if (g == 1) {
-    k_single_edge_meta<<<1, 32, 0, st>>>(meta);
+    ::sg::launch(k_single_edge_meta, 1, 32, 0, st, meta);
     SG_CHECK_LAUNCH("k_single_edge_meta");
   } else if (y.edge_tiles > 0) {
-    ms_count<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, meta, P32(y.o_tiles_edge));
+    ::sg::launch(ms_count, (int)y.edge_tiles, MS_THREADS, 0, st, P8(y.o_ekey), se, meta, P32(y.o_tiles_edge));
     SG_CHECK_LAUNCH("ms_count(edge)");
   }
   if (g > 1) {
-    ms_scan<<<se.nseg, 1024, 0, st>>>(se, P32(y.o_tiles_edge), tb_edge, keyoff_edge, 1, meta);
+    ::sg::launch(ms_scan, se.nseg, 1024, 0, st, se, P32(y.o_tiles_edge), tb_edge, keyoff_edge, 1, meta);
     SG_CHECK_LAUNCH("ms_scan(edge)");
   }
   if (g > 1 && y.edge_tiles > 0) {
-    ms_scatter<<<(int)y.edge_tiles, MS_THREADS, 0, st>>>(P8(y.o_ekey), se, meta, tb_edge, keyoff_edge,
+    ::sg::launch(ms_scatter, (int)y.edge_tiles, MS_THREADS, 0, st, P8(y.o_ekey), se, meta, tb_edge, keyoff_edge,
                                                          nullptr, P32(y.o_egrouped));
     SG_CHECK_LAUNCH("ms_scatter(edge)");
   }
@@ -887,16 +900,14 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   const int64_t words = y.bm_words;
   const int64_t nref_pos = y.voff[L + 1] - y.voff[1];
   if (g > 1 && nref_pos > 0) {
-    k_ref_bits<<<clamp_grid(div_up(nref_pos, 256), kSMs * 8), 256, 0, st>>>(
-        V, h, U32(y.o_pmask), U32(y.o_bitmap), words, 0);
+    ::sg::launch(k_ref_bits, clamp_grid(div_up(nref_pos, 256), kSMs * 8), 256, 0, st, V, h, U32(y.o_pmask), U32(y.o_bitmap), words, 0);
     SG_CHECK_LAUNCH("k_ref_bits");
-    k_ref_scan<<<(int)((words / CHUNK_WORDS) * L), 256, 0, st>>>(U32(y.o_bitmap), P32(y.o_wpre),
+    ::sg::launch(k_ref_scan, (int)((words / CHUNK_WORDS) * L), 256, 0, st, U32(y.o_bitmap), P32(y.o_wpre),
                                                                  P32(y.o_ctot));
     SG_CHECK_LAUNCH("k_ref_scan");
-    k_ref_chunks<<<1, 256, 0, st>>>(P32(y.o_ctot), words / CHUNK_WORDS, L, meta);
+    ::sg::launch(k_ref_chunks, 1, 256, 0, st, P32(y.o_ctot), words / CHUNK_WORDS, L, meta);
     SG_CHECK_LAUNCH("k_ref_chunks");
-    k_ref_rank<<<clamp_grid(div_up(nref_pos, 256), kSMs * 8), 256, 0, st>>>(
-        V, h, U32(y.o_pmask), U32(y.o_bitmap), P32(y.o_wpre), P32(y.o_ctot), words,
+    ::sg::launch(k_ref_rank, clamp_grid(div_up(nref_pos, 256), kSMs * 8), 256, 0, st, V, h, U32(y.o_pmask), U32(y.o_bitmap), P32(y.o_wpre), P32(y.o_ctot), words,
         P32(y.o_uorder));
     SG_CHECK_LAUNCH("k_ref_rank");
   }
@@ -918,14 +929,14 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   }
   for (int l = 0; l <= L + 1; ++l) pd.pbase[l] = y.pbase[l];
   if (g > 1 && y.pair_tiles > 0) {
-    k_pair_count<<<(int)y.pair_tiles, PAIR_T, 0, st>>>(pd, meta, P32(y.o_uorder), U32(y.o_pmask),
+    ::sg::launch(k_pair_count, (int)y.pair_tiles, PAIR_T, 0, st, pd, meta, P32(y.o_uorder), U32(y.o_pmask),
                                                         P8(y.o_keys), P32(y.o_tiles_pair));
     SG_CHECK_LAUNCH("k_pair_count");
-    k_pair_scan<<<1, 1024, 0, st>>>(pd, P32(y.o_tiles_pair), P32(y.o_tilebase_pair), meta);
+    ::sg::launch(k_pair_scan, 1, 1024, 0, st, pd, P32(y.o_tiles_pair), P32(y.o_tilebase_pair), meta);
     SG_CHECK_LAUNCH("k_pair_scan");
     PairOut po{P32(y.o_pairs), P32(y.o_pair_hidx), P32(y.o_sendpos), P32(y.o_xfer),
                P32(y.o_recv_row), P32(y.o_refrank), P32(y.o_contrib)};
-    k_pair_scatter<<<(int)y.pair_tiles, PAIR_T, 0, st>>>(pd, meta, P32(y.o_uorder), U32(y.o_pmask),
+    ::sg::launch(k_pair_scatter, (int)y.pair_tiles, PAIR_T, 0, st, pd, meta, P32(y.o_uorder), U32(y.o_pmask),
                                                           P8(y.o_keys), P32(y.o_rank),
                                                           P32(y.o_tilebase_pair), po);
     SG_CHECK_LAUNCH("k_pair_scatter");
@@ -934,8 +945,7 @@ extern "C" int sg_split_run(void* ws, const SgSplitLayout* lay, const int32_t* V
   const int64_t nS = y.voff[L + 1] - y.voff[1];
   if (nEtot + nS > 0) {
     LocalOut lo{P32(y.o_lsrc), P32(y.o_ldst), P32(y.o_rowbeg), P32(y.o_rowend), P32(y.o_selfrow)};
-    k_local_edges<<<clamp_grid(div_up(nEtot + nS, 256), kSMs * 8), 256, 0, st>>>(
-        esrc, edst, h, meta, P8(y.o_keys), P32(y.o_rank), P32(y.o_grouped), P32(y.o_egrouped),
+    ::sg::launch(k_local_edges, clamp_grid(div_up(nEtot + nS, 256), kSMs * 8), 256, 0, st, esrc, edst, h, meta, P8(y.o_keys), P32(y.o_rank), P32(y.o_grouped), P32(y.o_egrouped),
         P32(y.o_refrank), lo);
     SG_CHECK_LAUNCH("k_local_edges");
   }

@@ -165,6 +165,7 @@ struct GatPol {
 // its latency overlaps the edge loads.
 template <class P, int VEC, int LPR>
 __global__ void __launch_bounds__(256) k_tspmm_pieces(const SgMeta* __restrict__ meta, P pol, TsGeom t) {
+  SG_PDL_ENTRY();
   constexpr int TPW = 32 / LPR;  // teams per warp
   const int lane = threadIdx.x & 31, lr = lane % LPR;
   const int W = pol.width(), X = pol.extra();
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(256) k_tspmm_pieces(const SgMeta* __restrict__
 // ---------------------------------------------------------------- K2: rows that span chunks
 template <class P, int VEC>
 __global__ void __launch_bounds__(256) k_tspmm_spans(const SgMeta* __restrict__ meta, P pol, TsGeom t) {
+  SG_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int WS = t.ws, W = pol.width(), X = pol.extra(), WX = W + X;
@@ -310,11 +312,11 @@ int launch_pieces(const SgMeta* meta, const P& pol, const TsGeom& t, int64_t max
   const int64_t tasks = max_rows + chunks;
   if (tasks <= 0) return SG_OK;
   const int64_t warps = div_up(tasks, 32 / LPR);
-  k_tspmm_pieces<P, VEC, LPR><<<clamp_grid(div_up(warps, TWARPS), kSMs * 16), 256, 0, st>>>(meta, pol, t);
+  ::sg::launch(k_tspmm_pieces<P, VEC, LPR>, clamp_grid(div_up(warps, TWARPS), kSMs * 16), 256, 0, st, meta, pol, t);
   SG_CHECK_LAUNCH("k_tspmm_pieces");
   if (chunks > 0) {
     const size_t smem2 = sizeof(float) * (size_t)TWARPS * t.ws;
-    k_tspmm_spans<P, VEC><<<clamp_grid(div_up(chunks, TWARPS), kSMs * 8), 256, smem2, st>>>(meta, pol, t);
+    ::sg::launch(k_tspmm_spans<P, VEC>, clamp_grid(div_up(chunks, TWARPS), kSMs * 8), 256, smem2, st, meta, pol, t);
     SG_CHECK_LAUNCH("k_tspmm_spans");
   }
   return SG_OK;
