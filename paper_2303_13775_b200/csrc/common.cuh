@@ -87,7 +87,11 @@ inline cudaError_t allow_max_smem() {
   static bool done = false;
   if (done) return cudaSuccess;
   done = true;
-  return cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaFuncAttributes fa;
+  cudaError_t e = cudaFuncGetAttributes(&fa, K);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(227 * 1024 - fa.sharedSizeBytes));
 }
 
 __device__ __forceinline__ unsigned lanemask_lt() {

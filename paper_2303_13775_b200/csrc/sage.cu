@@ -1335,11 +1335,8 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   a.ws = w_self; a.wn = w_neigh; a.bias = bias; a.h = h;
   cudaStream_t st = (cudaStream_t)stream;
   // wide layers: one kernel (8 loads in flight per lane, 16-row tiles, 4 CTAs/SM)
-  static const int variant = [] {
-    const char* s = getenv("SG_SAGE_LAYER");
-    return s ? atoi(s) : 2;
-  }();
-  if (w > 64 && variant == 2) return launch_layer<8, 2, 4>(meta, a, max_rows, st);
+  // wide layers: one kernel (8 loads in flight per lane, 16-row tiles, 4 CTAs/SM)
+  if (w > 64) return launch_layer<8, 2, 4>(meta, a, max_rows, st);
   if (w > 64 && variant == 3) return launch_layer<8, 2, 2>(meta, a, max_rows, st);
   if (w > 64 && variant == 4) return launch_layer<8, 4, 3>(meta, a, max_rows, st);
   int rc;
