@@ -1335,10 +1335,7 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   a.ws = w_self; a.wn = w_neigh; a.bias = bias; a.h = h;
   cudaStream_t st = (cudaStream_t)stream;
   // wide layers: one kernel (8 loads in flight per lane, 16-row tiles, 4 CTAs/SM)
-  // wide layers: one kernel (8 loads in flight per lane, 16-row tiles, 4 CTAs/SM)
   if (w > 64) return launch_layer<8, 2, 4>(meta, a, max_rows, st);
-  if (w > 64 && variant == 3) return launch_layer<8, 2, 2>(meta, a, max_rows, st);
-  if (w > 64 && variant == 4) return launch_layer<8, 4, 3>(meta, a, max_rows, st);
   int rc;
   if (w <= 16) rc = launch_agg_mean<4, 4>(meta, a, max_rows, st);
   else if (w <= 32) rc = launch_agg_mean<8, 4>(meta, a, max_rows, st);
