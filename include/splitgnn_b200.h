@@ -101,6 +101,10 @@ typedef struct SgSplitLayout {
 const char* sg_last_error(void);
 const char* sg_version(void);
 unsigned long long sg_launch_count(void); /* kernels launched by this library */
+/* Programmatic dependent launch for every library kernel (default on;
+ * SG_PDL=0 in the environment disables it at load). */
+void sg_set_pdl(int on);
+int sg_get_pdl(void);
 int sg_device_sm_count(void);
 void sg_struct_sizes(int64_t* out /* [sizeof(SgMeta), sizeof(SgSplitLayout)] */);
 
@@ -194,6 +198,20 @@ int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
                       const float* w_self, const float* w_neigh, const float* bias,
                       int32_t final_layer, float* mean, float* counts, float* hs, float* h,
                       int64_t max_rows, void* stream);
+/* Single-device split, LAST layer: aggregation + update (no ReLU) +
+ * classifier_loss (models.py:287-302) + the layer's row-local backward
+ * (engine.py:237-244: d_pre = d_h, weight/bias partials, d_self, d_sums) in
+ * one kernel. part_cls gets nblocks x (dout*ncls + ncls + 1) partials in the
+ * sg_cls_loss layout, part_lay nblocks x (2*w*dout + dout) in the
+ * sg_sage_bwd_rows layout; both are summed by sg_reduce_partials. Also
+ * writes mean, counts and h (n_own x dout). */
+int sg_sage_final_fused(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                        const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                        int32_t ncls, const float* w_self, const float* w_neigh,
+                        const float* bias, const float* w_cls, const float* b_cls,
+                        const int32_t* V, const int32_t* labels, float* mean, float* counts,
+                        float* h, float* d_self, float* d_sums, float* part_cls,
+                        float* part_lay, int32_t nblocks, int64_t max_rows, void* stream);
 /* Owner combine + update (engine.py:197-226): adds the holders' partial
  * (sum,count) rows from recvbuf in ascending sender order, mean = S/N,
  * pre = h_self@W_self + mean@W_neigh + b, h = relu(pre) unless final.

@@ -1026,18 +1026,31 @@ __global__ void __launch_bounds__(256) k_sage_bwd_rows(const SgMeta* __restrict_
 // Tiled weight gradients (self-compact forward): dW_self = hs^T d_pre,
 // dW_neigh = mean^T d_pre over this block's rows, each thread a 4x4 register
 // tile (2 LDS.128 per 16 FFMA), per-block partial in the parameter layout.
+// Tiles are double-buffered: the [hs | mean] rows, d_h and (for the ReLU mask)
+// h of tile t+1 are copied to shared memory with cp.async while tile t is
+// multiplied, so each CTA pays one memory latency, not one per tile.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
 template <int NQ>
-__global__ void __launch_bounds__(256) k_sage_wgrad(const SgMeta* __restrict__ meta, BwdArgs a) {
+__global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict__ meta, BwdArgs a) {
   SG_PDL_ENTRY();
   constexpr int TR = 32;
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, K = 2 * w, KP = K + 4, wst = dout + 4;
   const bool need_c = a.d_self != nullptr || a.d_sums != nullptr;
-  float* A_s = smem;                  // [TR][2w+4]  hs | mean
-  float* dp_s = A_s + TR * KP;        // [TR][dout]
-  float* cnt_s = dp_s + TR * dout;    // [TR]
-  float* ws_s = cnt_s + TR;           // [w][dout+4] (need_c)
+  const int stage_f = TR * KP + 2 * TR * dout + TR;  // A | d_h | h | counts
+  float* ws_s = smem;                  // [w][dout+4] (need_c)
   float* wn_s = ws_s + w * wst;
+  float* stg = wn_s + w * wst;         // 2 x stage
   if (need_c)
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
@@ -1046,42 +1059,60 @@ __global__ void __launch_bounds__(256) k_sage_wgrad(const SgMeta* __restrict__ m
     }
   const int n = meta->n_own[a.l][a.d];
   const int own0 = meta->own_off[a.l][a.d];
-  const int ncg = K / 4, nslots = ncg * NQ;
+  const int ncg = K / 4, nslots = ncg * NQ, dq = dout / 4;
+  const int ntiles = (n + TR - 1) / TR;
+  auto issue = [&](int tile, int s) {
+    float* A_s = stg + s * stage_f;
+    float* dh_s = A_s + TR * KP;
+    float* hh_s = dh_s + TR * dout;
+    float* cn_s = hh_s + TR * dout;
+    const int r0 = tile * TR;
+    for (int idx = threadIdx.x; idx < TR * ncg; idx += 256) {
+      const int r = idx / ncg, q = idx - r * ncg;
+      const int k = 4 * q;
+      float* dst = A_s + r * KP + k;
+      if (r0 + r < n) {
+        const int64_t G = own0 + r0 + r;
+        cp_async16(dst, k < w ? a.h_prev + G * w + k : a.mean + G * w + (k - w));
+      } else {
+        *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    for (int idx = threadIdx.x; idx < TR * dq; idx += 256) {
+      const int r = idx / dq, q = idx - r * dq;
+      if (r0 + r < n) {
+        const int64_t G = own0 + r0 + r;
+        cp_async16(dh_s + r * dout + 4 * q, a.d_h + G * dout + 4 * q);
+        if (!a.final_) cp_async16(hh_s + r * dout + 4 * q, a.h + G * dout + 4 * q);
+      } else {
+        *reinterpret_cast<float4*>(dh_s + r * dout + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (need_c && threadIdx.x < TR && r0 + (int)threadIdx.x < n)
+      cp_async4(cn_s + threadIdx.x, a.counts + own0 + r0 + threadIdx.x);
+  };
   float acc[2][4][4];
 #pragma unroll
   for (int s2 = 0; s2 < 2; ++s2)
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[s2][i][0] = acc[s2][i][1] = acc[s2][i][2] = acc[s2][i][3] = 0.f;
   float ab = 0.f;
-  const int ntiles = (n + TR - 1) / TR;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    __syncthreads();
+  if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  int s = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, s ^= 1) {
     const int r0 = tile * TR;
-    for (int idx = threadIdx.x; idx < TR * ncg; idx += blockDim.x) {
-      const int r = idx / ncg, q = idx - r * ncg;
-      const int k = 4 * q;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r0 + r < n) {
-        const int64_t G = own0 + r0 + r;
-        v = k < w ? *reinterpret_cast<const float4*>(a.h_prev + G * w + k)
-                  : *reinterpret_cast<const float4*>(a.mean + G * w + (k - w));
-      }
-      *reinterpret_cast<float4*>(A_s + r * KP + k) = v;
-    }
-    for (int idx = threadIdx.x; idx < TR * dout; idx += blockDim.x) {
-      const int r = idx / dout, j = idx - r * dout;
-      float v = 0.f;
-      if (r0 + r < n) {
-        const int64_t G = own0 + r0 + r;
-        v = a.d_h[G * dout + j];
-        if (!a.final_ && !(a.h[G * dout + j] > 0.f)) v = 0.f;
-      }
-      dp_s[idx] = v;
-    }
-    if (threadIdx.x < TR) {
-      const int r = threadIdx.x;
-      cnt_s[r] = (r0 + r < n) ? 1.0f / a.counts[own0 + r0 + r] : 1.f;
-    }
+    if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, s ^ 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const float* A_s = stg + s * stage_f;
+    float* dp_s = const_cast<float*>(A_s) + TR * KP;
+    const float* hh_s = dp_s + TR * dout;
+    const float* cn_s = hh_s + TR * dout;
+    if (!a.final_)
+      for (int idx = threadIdx.x; idx < TR * dout; idx += 256)
+        if (!(hh_s[idx] > 0.f)) dp_s[idx] = 0.f;
     __syncthreads();
 #pragma unroll
     for (int s2 = 0; s2 < 2; ++s2) {
@@ -1119,10 +1150,12 @@ __global__ void __launch_bounds__(256) k_sage_wgrad(const SgMeta* __restrict__ m
           s2v = fmaf(g4.x, w2.x, fmaf(g4.y, w2.y, fmaf(g4.z, w2.z, fmaf(g4.w, w2.w, s2v))));
         }
         if (a.d_self) a.d_self[G * w + c] = s1;
-        if (a.d_sums) a.d_sums[G * w + c] = s2v * cnt_s[r];
+        if (a.d_sums) a.d_sums[G * w + c] = s2v / cn_s[r];
       }
     }
+    __syncthreads();  // buffer s is refilled next iteration
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   const int nwd = w * dout;
   float* out = a.partial + (int64_t)blockIdx.x * (2 * (int64_t)nwd + dout);
 #pragma unroll
@@ -1522,7 +1555,7 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   a.d_self = d_self;
   a.d_sums = d_sums;
   if (self_compact && q4 && w % 4 == 0 && dout <= 32 && 2 * w * (dout / 4) <= 4 * 512) {
-    const size_t sm2 = sizeof(float) * (32 * (size_t)(2 * w + 4) + 32 * (size_t)dout + 32 +
+    const size_t sm2 = sizeof(float) * (2 * (32 * (size_t)(2 * w + 4) + 2 * 32 * (size_t)dout + 32) +
                                         2 * (size_t)w * (dout + 4));
     SG_REQUIRE(sm2 <= 227 * 1024, "sage_wgrad: width too large for shared memory");
     cudaStream_t st2 = (cudaStream_t)stream;

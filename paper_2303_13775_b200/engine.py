@@ -124,6 +124,51 @@ class SplitStep:
         return (self.g == 1 and dperm is None and w % 4 == 0 and w <= 128 and dout in (4, 8, 16, 32)
                 and not getattr(self, "no_fuse", False))
 
+    def _final_fused_ok(self, w, dout, dperm):
+        """Single-device split: the last layer, the loss and the last layer's
+        row-local backward run as one kernel (sg_sage_final_fused)."""
+        return (self.g == 1 and dperm is None and w % 4 == 0 and w <= 128 and dout <= 64
+                and self.p.num_classes <= 1024 and not getattr(self, "no_fuse", False)
+                and not getattr(self, "no_fuse_final", False))
+
+    def _begin_grads(self):
+        """Flat per-device gradient buffers (+ loss slot) and the partial-sum jobs."""
+        if self.grads is None:
+            self.grads = {d: torch.empty(self.p.n + 1, dtype=torch.float32, device=self.dev)
+                          for d in self.devices}
+            self.jobs = []
+            self._partials = []
+
+    def _final_fused(self, l, w, dout, h_prev, src_row):
+        ds, p, st = self.ds, self.p, _lib.stream_ptr()
+        self._begin_grads()
+        C = p.num_classes
+        nV = ds.nV[l]
+        n = self.n_own(l, 0)
+        nb = max(1, min(_nblocks(n, tile=8), 2 * 148))
+        mean = _f32(nV, w, device=self.dev)
+        counts = _f32(nV, device=self.dev)
+        h = _f32(nV, dout, device=self.dev)
+        need_prev = l > 1
+        d_self = _f32(nV, w, device=self.dev) if need_prev else None
+        d_sums = _f32(nV, w, device=self.dev) if need_prev else None
+        ncls, nlay = dout * C + C + 1, 2 * w * dout + dout
+        part_c = _f32(nb * ncls, device=self.dev)
+        part_l = _f32(nb * nlay, device=self.dev)
+        self._ev(f"ph:final{l}:s")
+        _lib.call("sg_sage_final_fused", _lib.ptr(ds.ws), ds.lay, 0, _lib.ptr(h_prev), _lib.ptr(src_row),
+                  w, dout, C, _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
+                  _lib.ptr(p.view(f"layer{l-1}.bias")), _lib.ptr(p.view("cls.w")), _lib.ptr(p.view("cls.b")),
+                  _lib.ptr(ds.V), _lib.ptr(self.labels), _lib.ptr(mean), _lib.ptr(counts), _lib.ptr(h),
+                  _lib.ptr(d_self), _lib.ptr(d_sums), _lib.ptr(part_c), _lib.ptr(part_l), nb, n, st)
+        self._ev(f"ph:final{l}:e")
+        self.jobs.append((part_c, nb, ncls, self.grads[0], p.offset("cls.w")))
+        self.jobs.append((part_l, nb, nlay, self.grads[0], p.offset(f"layer{l-1}.w_self")))
+        self._partials += [part_c, part_l]
+        self.h[l] = h
+        self.keep[l] = dict(mean=mean, counts=counts)
+        self._final_rows = (d_self, d_sums)
+
     def _dst_perm(self):
         """CSR-by-destination for samples whose edges are not grouped by dst."""
         if self.ds.dst_grouped:
@@ -174,6 +219,7 @@ class SplitStep:
             from paper_2303_13775_b200.gat import gat_forward
             return gat_forward(self)
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
+        self.grads, self._final_rows = None, None
         with self.phase("layer0"):
             self.layer0()
         dperm = self._dst_perm()
@@ -184,6 +230,9 @@ class SplitStep:
             final = int(l == self.L)
             h_prev, src_row = (self.f.table, self.src_row0) if l == 1 else (self.h[l - 1], None)
             nV = ds.nV[l]
+            if l == self.L and self._final_fused_ok(w, dout, dperm):
+                self._final_fused(l, w, dout, h_prev, src_row)
+                continue
             if self._fused_ok(w, dout, dperm):
                 mean = _f32(nV, w, device=self.dev)
                 counts = _f32(nV, device=self.dev)
@@ -296,11 +345,9 @@ class SplitStep:
         L = self.L
         hid, C = p.hidden, p.num_classes
         # every parameter block (and the loss slot) is written by a reduction job
-        self.grads = {d: torch.empty(p.n + 1, dtype=torch.float32, device=self.dev) for d in self.devices}
-        self.jobs = []
+        self._begin_grads()
         self.d_h = _f32(ds.nV[L], hid, device=self.dev)
         ncls = hid * C + C + 1
-        self._partials = []
         for d in self.devices:
             nb = _nblocks(self.n_own(L, d), tile=8)
             part = _f32(nb * ncls, device=self.dev)
@@ -318,25 +365,32 @@ class SplitStep:
             self.reduce()
             return
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
-        with self.phase("loss"):
-            self.loss()
+        fused_final = getattr(self, "_final_rows", None) is not None
+        if not fused_final:
+            with self.phase("loss"):
+                self.loss()
         with self.phase("src_csr_join"):
             csr, kb = self._join_src_csr(2)
-        d_h = self.d_h
+        d_h = None if fused_final else self.d_h
         for l in range(self.L, 0, -1):
             w, dout = p.layer_dims(l - 1)
             final = int(l == self.L)
             need_prev = l > 1  # d(loss)/d(features) is never used
             h_prev, src_row = (self.f.table, self.src_row0) if l == 1 else (self.h[l - 1], None)
             nV = ds.nV[l]
-            d_self = _f32(nV, w, device=self.dev) if need_prev else None
-            d_sums = _f32(nV, w, device=self.dev) if need_prev else None
+            if l == self.L and fused_final:
+                d_self, d_sums = self._final_rows
+                devs = []
+            else:
+                d_self = _f32(nV, w, device=self.dev) if need_prev else None
+                d_sums = _f32(nV, w, device=self.dev) if need_prev else None
+                devs = self.devices
             npart = 2 * w * dout + dout
             self._ev(f"ph:bwd_rows{l}:s")
             hs = self.keep[l].get("hs")
             if hs is not None:
                 h_prev, src_row = hs, None
-            for d in self.devices:
+            for d in devs:
                 nb = _nblocks(self.n_own(l, d))
                 part = _f32(nb * npart, device=self.dev)
                 _lib.call("sg_sage_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),

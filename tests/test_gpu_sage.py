@@ -180,3 +180,47 @@ def test_sage_single_device_fused_shapes(F, hid):
     assert_grads_close(grads[0], rgrads[0], TOL, 0)
     for l in range(3):
         assert rel_err(ex.states[0].h[l], ref.h[0][l]) < TOL, l
+
+
+@pytest.mark.parametrize("F", [100, 24])
+def test_single_device_fused_paths_match_unfused(F):
+    """g = 1: the one-kernel layers (sg_sage_fused_fwd) and the fused last
+    layer + loss + row backward (sg_sage_final_fused) give the same loss,
+    gradients and activations as the separate aggregate/update/loss/bwd-rows
+    kernels, and both match the oracle."""
+    import torch
+
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import _lib
+    from paper_2303_13775_b200.engine import SplitStep
+    graph, pm, sample, cache = random_partition_case(5, n=8000, m=120000, g=1, batch=256,
+                                                     fanouts=(15, 10, 5), cache_frac=1.0)
+    feats_h = sg.synthetic_features(graph.num_vertices, F, seed=3)
+    labels = sg.synthetic_labels(graph.num_vertices, 47, seed=4)
+    params = sg.init_params("graphsage", F, 16, 47, 3, seed=5)
+    dp = sg.DeviceParams.from_host(params)
+    fs = sg.FeatureStore.from_host(feats_h, cache)
+    lab = torch.from_numpy(labels).cuda()
+    out = {}
+    for mode in ("fused", "final_unfused", "unfused"):
+        ds = sg.DeviceSplit.from_sample(sample, pm, cache)
+        step = SplitStep(dp, ds, fs, lab, exact=True)
+        step.no_fuse = mode == "unfused"
+        step.no_fuse_final = mode != "fused"
+        n0 = _lib.launch_count()
+        step.run()
+        torch.cuda.synchronize()
+        hs = [step.h[l][:step.n_own(l, 0)].cpu().numpy().copy() for l in range(1, 4)]
+        out[mode] = (step.grads[0].cpu().numpy().copy(), hs, _lib.launch_count() - n0)
+    g_f, h_f, n_f = out["fused"]
+    for mode in ("final_unfused", "unfused"):
+        g_u, h_u, n_u = out[mode]
+        assert rel_err(g_f, g_u) < 1e-5, mode
+        for a, b in zip(h_f, h_u):
+            assert rel_err(a, b) < 1e-5, mode
+        assert n_f < n_u, (n_f, n_u, mode)  # the fused step launches fewer kernels
+    ws, wp = split_sample(sample.layer_vertices, sample.layer_edges, pm.assignment, 1, cache.cached)
+    ref = CoopRun(glorot_params("graphsage", F, 16, 47, 3, seed=5), ws, wp, feats_h.astype(np.float64), labels)
+    rloss, rgrads = ref.run()
+    assert abs(float(g_f[dp.n]) - rloss) <= TOL * abs(rloss)
+    assert_grads_close(dp.grads_to_dict(torch.from_numpy(g_f)), rgrads[0], TOL, 0)
