@@ -322,6 +322,12 @@ int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32_t d,
  * (ascending b). jobs: HOST array of n_jobs quadruples (partial device ptr,
  * nblocks, n, out device ptr), passed to the kernel by value. */
 int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n, void* stream);
+/* sg_reduce_partials with the SGD step fused (single device, nothing to
+ * all-reduce): jobs are 6 int64 per job {partials, nblocks, n, out, param,
+ * n_sgd}; the first n_sgd summed columns g also update param: p -= scale*g
+ * (ModelParams.sgd_step, models.py:95-99). param = 0 skips the step. */
+int sg_reduce_partials_sgd(const int64_t* jobs, int32_t n_jobs, int64_t max_n, float scale,
+                           void* stream);
 /* allreduce_and_step (engine.py:633-647): grads = sum over devices in device
  * order (grad_ptrs: HOST array of n_dev device pointers to flat buffers), then
  * p -= lr/num_targets * grads; grads_out (nullable) receives the sum. */

@@ -153,8 +153,17 @@ struct DevPtrs {
 };
 
 // Block = 32 output columns x 8 warps; warp w sums partial rows b = w, w+8, ...
-// (4 loads in flight), then the 8 warp sums are added in warp order.
-__global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs) {
+// (8 loads in flight), then the 8 warp sums are added in warp order. With a
+// parameter pointer (sgd job), the summed gradient g of the first n_sgd
+// columns also takes the SGD step p -= scale * g in the same pass (g = 1:
+// allreduce_and_step has nothing to sum, engine.py:633-647).
+struct SgdJobs {
+  int64_t param[MAXJOBS];
+  int64_t n_sgd[MAXJOBS];
+  float scale;
+};
+
+__global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs, SgdJobs sj) {
   SG_PDL_ENTRY();
   __shared__ float red[8][33];
   const int jb = blockIdx.y;
@@ -162,28 +171,34 @@ __global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs) {
   const int nb = (int)jobs.v[4 * jb + 1];
   const int64_t n = jobs.v[4 * jb + 2];
   float* out = (float*)jobs.v[4 * jb + 3];
+  float* prm = (float*)sj.param[jb];
+  const int64_t n_sgd = sj.n_sgd[jb];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t k0 = (int64_t)blockIdx.x * 32; k0 < n; k0 += (int64_t)gridDim.x * 32) {
     const int64_t k = k0 + lane;
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    float s[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s[u] = 0.f;
     if (k < n) {
       int b = warp;
-      for (; b + 24 < nb; b += 32) {
-        s0 += p[(int64_t)b * n + k];
-        s1 += p[(int64_t)(b + 8) * n + k];
-        s2 += p[(int64_t)(b + 16) * n + k];
-        s3 += p[(int64_t)(b + 24) * n + k];
+      for (; b + 56 < nb; b += 64) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = p[(int64_t)(b + 8 * u) * n + k];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] += v[u];
       }
-      for (; b < nb; b += 8) s0 += p[(int64_t)b * n + k];
+      for (; b < nb; b += 8) s[0] += p[(int64_t)b * n + k];
     }
     __syncthreads();
-    red[warp][lane] = (s0 + s1) + (s2 + s3);
+    red[warp][lane] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
     __syncthreads();
     if (warp == 0 && k < n) {
       float t = 0.f;
 #pragma unroll
       for (int w = 0; w < 8; ++w) t += red[w][lane];
       out[k] = t;
+      if (prm && k < n_sgd) prm[k] -= sj.scale * t;
     }
   }
 }
@@ -240,20 +255,40 @@ extern "C" int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32
   return SG_OK;
 }
 
-extern "C" int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n,
-                                  void* stream) {
+static int reduce_partials(const int64_t* jobs, int stride, int32_t n_jobs, int64_t max_n, float scale,
+                           void* stream) {
   if (n_jobs <= 0 || max_n <= 0) return SG_OK;
   SG_REQUIRE(jobs != nullptr, "reduce_partials: null job table");
   for (int j0 = 0; j0 < n_jobs; j0 += MAXJOBS) {
     const int nj = std::min(MAXJOBS, n_jobs - j0);
     Jobs jb;
+    SgdJobs sj;
     memset(&jb, 0, sizeof(jb));
-    memcpy(jb.v, jobs + 4 * j0, sizeof(int64_t) * 4 * nj);
+    memset(&sj, 0, sizeof(sj));
+    sj.scale = scale;
+    for (int j = 0; j < nj; ++j) {
+      const int64_t* r = jobs + (int64_t)stride * (j0 + j);
+      for (int f = 0; f < 4; ++f) jb.v[4 * j + f] = r[f];
+      if (stride >= 6) {
+        sj.param[j] = r[4];
+        sj.n_sgd[j] = r[5];
+      }
+    }
     dim3 grid(clamp_grid(div_up(max_n, 32), kSMs * 2), nj);
-    ::sg::launch(k_reduce_partials, grid, 256, 0, (cudaStream_t)stream, jb);
+    ::sg::launch(k_reduce_partials, grid, 256, 0, (cudaStream_t)stream, jb, sj);
     SG_CHECK_LAUNCH("k_reduce_partials");
   }
   return SG_OK;
+}
+
+extern "C" int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n,
+                                  void* stream) {
+  return reduce_partials(jobs, 4, n_jobs, max_n, 0.f, stream);
+}
+
+extern "C" int sg_reduce_partials_sgd(const int64_t* jobs, int32_t n_jobs, int64_t max_n, float scale,
+                                      void* stream) {
+  return reduce_partials(jobs, 6, n_jobs, max_n, scale, stream);
 }
 
 extern "C" int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_ptrs,

@@ -439,11 +439,18 @@ class SplitStep:
         """Per-block partials -> per-device flat gradients (+ loss slot)."""
         jobs = []
         max_n = 1
+        sgd = getattr(self, "sgd", None)  # (flat params, scale): g = 1, SGD fused into the reduction
         for part, nb, n, gbuf, off in self.jobs:
             jobs += [part.data_ptr(), nb, n, gbuf.data_ptr() + 4 * off]
+            if sgd is not None:
+                jobs += [sgd[0].data_ptr() + 4 * off, max(0, min(n, self.p.n - off))]
             max_n = max(max_n, n)
         table = np.asarray(jobs, dtype=np.int64)
-        _lib.call("sg_reduce_partials", _lib.ptr(table), len(self.jobs), max_n, _lib.stream_ptr())
+        if sgd is not None:
+            _lib.call("sg_reduce_partials_sgd", _lib.ptr(table), len(self.jobs), max_n, float(sgd[1]),
+                      _lib.stream_ptr())
+        else:
+            _lib.call("sg_reduce_partials", _lib.ptr(table), len(self.jobs), max_n, _lib.stream_ptr())
 
     def loss_sum_dev(self):
         return sum(self.grads[d][self.p.n] for d in self.devices)
@@ -916,11 +923,9 @@ class CapturedStep:
         if ev:
             step.events["ph:split:s"] = [ev[0]]
             step.events["ph:split:e"] = [ev[1]]
+        step.sgd = (self.p.flat, self.scale)  # one device: the SGD step rides on the reduction
         step.run()
         gbuf = step.grads[0]
-        ptrs = np.asarray([gbuf.data_ptr()], dtype=np.int64)
-        _lib.call("sg_sum_sgd", _lib.ptr(self.p.flat), None, _lib.ptr(ptrs), 1, self.p.n,
-                  self.scale, _lib.stream_ptr())
         self.ds, self.step = ds, step
         return gbuf
 
