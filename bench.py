@@ -459,7 +459,7 @@ def main():
         agg_avg = float(np.mean(agg_ms))
         achieved = alg / (agg_avg / 1e3) / 1e9
         traffic = None
-        tpath = os.path.join(ROOT, "profiles", "agg1_traffic.json")
+        tpath = os.path.join(ROOT, "profiles", f"agg1_traffic_{CFG_NAME}.json")
         if os.path.exists(tpath):
             try:
                 traffic = json.load(open(tpath)).get("bytes_per_launch")

@@ -11,7 +11,5 @@ timeout 600 python bench.py --config $CFG > gpurun_out/${TAG}_bench_${CFG}.json 
 tail -c 600 gpurun_out/${TAG}_bench_${CFG}.json
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_${CFG}.csv \
    python bench.py --config $CFG --profile --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${KREGEX:-k_sage_layer|k_sage_wgrad|k_sage_scatter|k_tspmm|k_gat_agg}" -c ${KCOUNT:-8} \
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${KREGEX:-k_sage_layer|k_sage_wgrad|k_sage_final|k_tspmm|k_reduce_partials}" -c ${KCOUNT:-8} \
    -o gpurun_out/${TAG}_full_${CFG} -f python bench.py --config $CFG --profile --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
-for i in 1 2 3; do for p in 1 0; do SG_PDL=$p timeout 300 python bench.py --config $CFG --no-cpu-baseline --steps 20 2>/dev/null | python -c "
-import json,sys;d=json.loads(sys.stdin.read().strip().splitlines()[-1]);print('PDL=$p',round(d['ms_per_step'],4),'e2e',round(d['e2e']['ms_per_step'],4))"; done; done

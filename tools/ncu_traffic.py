@@ -1,4 +1,4 @@
-"""Write profiles/agg1_traffic.json from an ncu --set full report: DRAM bytes
+"""Write profiles/agg1_traffic_<cfg>.json from an ncu --set full report: DRAM bytes
 (read + write) of the layer-1 aggregation launch (the largest launch of the
 named kernel), which bench.py reports as roofline.traffic.
 
@@ -11,7 +11,7 @@ import subprocess
 import sys
 
 rep, kname = sys.argv[1], sys.argv[2]
-out = sys.argv[3] if len(sys.argv) > 3 else "profiles/agg1_traffic.json"
+out = sys.argv[3] if len(sys.argv) > 3 else "profiles/agg1_traffic_c2.json"
 txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                       "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
                      capture_output=True, text=True).stdout
