@@ -41,6 +41,9 @@ CONFIGS = {
                train_frac=0.0803, p_local=0.92,
                desc="C3 GAT-3L 4 heads x 16 (concat), products-shape synthetic power-law "
                     "(2.45M nodes / 61.9M edges, F=100, 47 classes)"),
+    "c5": dict(kind="exchange", heads=1, n=0, m=0, feat=100, classes=0, train_frac=0.0, p_local=0.0,
+               desc="C5 push-to-owner / push-from-owner exchange microbench: remote-partial rows per "
+                    "peer swept 2^8..2^20, width 101 (push-to-owner, d_in+1) and 100 (push-from-owner) fp32"),
     "c4": dict(kind="graphsage", heads=1, n=111_059_956, m=1_615_685_872, feat=128, classes=172,
                train_frac=0.0109, p_local=0.95,
                desc="C4 GraphSAGE-3L mean, papers100M-shape synthetic power-law (111M nodes / "
@@ -220,6 +223,10 @@ def run_reference_arm(args, rank, world):
     if rank != 0:
         return
     select_config(args.config)
+    if KIND == "exchange":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference exchanges in-process with "
+                          "NumPy copies (engine.py:121-156); there is no transport to microbenchmark"}))
+        return
     threads = os.cpu_count() or 1
     graph, labels, train, _ = build_workload(threads)
     samples, _ = make_samples(graph, train, args.warmup + args.steps, args.batch, threads)
@@ -244,6 +251,63 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_exchange_bench(args, rank, world, local):
+    """C5: the split exchange's transport (NcclTransport: one all-to-all-v per
+    round, engine.py:121-156 / PAPER.md:820) on uniform synthetic plans, rows
+    per peer swept; bytes sent per GPU / device time (max over ranks) against
+    NVLink 5 (900 GB/s per direction). At N = 1 there is no peer link: the
+    line reports NCCL's self-copy through the same call, marked as such."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world,
+                            init_method=None if "MASTER_ADDR" in os.environ else "tcp://127.0.0.1:29512")
+    sweep = []
+    for width in (101, 100):
+        for lg in range(8, 21, 2):
+            rows = 1 << lg
+            if rows * width * 4 * world > 8 << 30:
+                break
+            send = torch.rand(rows * world, width, device=dev)
+            recv = torch.empty_like(send)
+            splits = [rows * width] * world
+            for _ in range(args.warmup):
+                dist.all_to_all_single(recv.view(-1), send.view(-1), splits, splits)
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                dist.all_to_all_single(recv.view(-1), send.view(-1), splits, splits)
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            # bytes each GPU sends to its peers (N = 1: the self-copy reads and writes its block)
+            peer_bytes = rows * width * 4 * (world - 1) if world > 1 else 2 * rows * width * 4
+            sweep.append({"rows_per_peer": rows, "width": width, "bytes_sent_per_gpu": peer_bytes,
+                          "us": ms * 1e3, "GBps_per_gpu": peer_bytes / (ms * 1e-3) / 1e9})
+            del send, recv
+    best = max(sweep, key=lambda r: r["GBps_per_gpu"])
+    if rank == 0:
+        line = {"metric": "exchange_GBps_per_gpu", "value": best["GBps_per_gpu"], "unit": "GB/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": best["us"] / 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic",
+                "config": {"workload": DESC, "config_id": "c5", "parallelism": f"split{world}",
+                           "peer_link": "NVLink 5 / NVSwitch" if world > 1 else "none (N=1: NCCL self-copy)"},
+                "roofline": {"bound": "nvlink" if world > 1 else "hbm",
+                             "achieved": best["GBps_per_gpu"], "peak": 900.0 if world > 1 else 6551.7,
+                             "unit": "GB/s", "frac": best["GBps_per_gpu"] / (900.0 if world > 1 else 6551.7),
+                             "traffic": None},
+                "sweep": sweep}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -252,6 +316,8 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
     select_config(args.config)
+    if KIND == "exchange":
+        return run_exchange_bench(args, rank, world, local)
 
     import torch
     import torch.distributed as dist
