@@ -326,10 +326,28 @@ def main():
     from paper_2303_13775_b200 import _lib
     from paper_2303_13775_b200.engine import SplitStep
 
+    # SG_BENCH_HOST_STAGED=1: every rank on cuda:0, payloads staged through host
+    # memory over gloo -- exercises the N > 1 code path on a single-GPU box
+    # (the numbers are not NVLink numbers and are marked as such).
+    staged = os.environ.get("SG_BENCH_HOST_STAGED") == "1" and world > 1
+    if staged:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if staged:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def allreduce(t, op=None):
+        op = dist.ReduceOp.SUM if op is None else op
+        if not staged:
+            dist.all_reduce(t, op=op)
+            return
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
     g = world
     threads = max(1, (os.cpu_count() or 1) // max(1, world))
     graph, labels, train, gen_s = build_workload(threads)
@@ -343,7 +361,7 @@ def main():
     samples, iters_per_epoch = make_samples(graph, train, n_steps, args.batch, threads)
     params = sg.init_params(KIND, FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED, heads=HEADS)
     dp = sg.DeviceParams.from_host(params, dev)
-    transport = sg.NcclTransport(rank, world) if g > 1 else sg.LocalTransport()
+    transport = sg.NcclTransport(rank, world, stage_on_host=staged) if g > 1 else sg.LocalTransport()
     # device-resident inputs
     dev_samples = []
     for s in samples:
@@ -448,7 +466,7 @@ def main():
                              exact=True, record_events=record_events)
             step.run()
             gbuf = step.grads[rank]
-            dist.all_reduce(gbuf)
+            allreduce(gbuf)
             ptrs_h = np.asarray([gbuf.data_ptr()], dtype=np.int64)
             _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs_h), 1, dp.n,
                       LR / len(samples[i].targets), _lib.stream_ptr())
@@ -488,7 +506,7 @@ def main():
             step = SplitStep(dp, ds, feats, labels_dev, devices=[rank], transport=transport, exact=True)
             step.run()
             gbuf = step.grads[rank]
-            dist.all_reduce(gbuf)
+            allreduce(gbuf)
             ptrs_h = np.asarray([gbuf.data_ptr()], dtype=np.int64)
             _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs_h), 1, dp.n,
                       LR / len(smp.targets), _lib.stream_ptr())
@@ -500,7 +518,7 @@ def main():
         e2e_ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([my_ms, e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        allreduce(t, op=dist.ReduceOp.MAX)
         my_ms, e2e_ms = float(t[0].item()), float(t[1].item())
     value = edges / (my_ms / 1e3)
     e2e = edges / (e2e_ms / 1e3)
@@ -547,7 +565,8 @@ def main():
                        "config_id": CFG_NAME,
                        "model": f"{KIND}-3l-h16" + (f"x{HEADS}" if HEADS > 1 else ""),
                        "global_batch": args.batch, "seq_len": None,
-                       "parallelism": f"split{g}", "l2": "flushed between timed steps (256 MB write, "
+                       "parallelism": f"split{g}" + (" host-staged (gloo, one GPU): not an NVLink number"
+                                                      if staged else ""), "l2": "flushed between timed steps (256 MB write, "
                                                           "outside the per-step events)",
                        "epoch_iterations": iters_per_epoch,
                        "epoch_time_s": iters_per_epoch * my_ms / args.steps / 1e3,

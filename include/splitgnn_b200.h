@@ -322,6 +322,17 @@ int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32_t d,
  * (ascending b). jobs: HOST array of n_jobs quadruples (partial device ptr,
  * nblocks, n, out device ptr), passed to the kernel by value. */
 int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t max_n, void* stream);
+/* split_cost (scheduler.py:257-309) on the device for a packed sample
+ * (V, esrc, edst as sg_split_run; nV[0..L], nE[0..L-1] host arrays):
+ * counts[(l-1)*g + d] = edges of E^l whose source lives on d, local[l-1] =
+ * edges with source and destination on one device, cost_rows = C[v^l] for
+ * every position of V^1..V^L (concatenated), cost[l-1] = sum of C over V^l.
+ * mask_ws: sum_{l>=1} nV[l] uint32 scratch. *err != 0 when a sampled vertex is
+ * outside the map. Integer atomics only (exact). */
+int sg_split_cost(const int32_t* V, const int32_t* esrc, const int32_t* edst, const int64_t* nV,
+                  const int64_t* nE, int32_t L, const uint8_t* assignment, int64_t n_vertices,
+                  int32_t g, uint32_t* mask_ws, int32_t* cost_rows, int64_t* counts,
+                  int64_t* local, int64_t* cost, int32_t* err, void* stream);
 /* sg_reduce_partials with the SGD step fused (single device, nothing to
  * all-reduce): jobs are 6 int64 per job {partials, nblocks, n, out, param,
  * n_sgd}; the first n_sgd summed columns g also update param: p -= scale*g

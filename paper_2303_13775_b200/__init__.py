@@ -22,17 +22,21 @@ from paper_2303_13775_b200.partition import (
     max_part_size,
     range_partition,
 )
-from paper_2303_13775_b200.sampling import MiniBatchSample, NativeSampler, epoch_batches, sample_minibatch
+from paper_2303_13775_b200.sampling import (MiniBatchSample, NativeSampler, epoch_batches, sample_microbatches,
+                                            sample_minibatch)
 from paper_2303_13775_b200.scheduler import (
     DeviceSplit,
     LocalSplit,
     PlanEntry,
     ShufflePlan,
+    SplitCostReport,
+    split_cost,
     split_minibatch,
     transfer_manifest,
 )
 from paper_2303_13775_b200.models import DeviceParams, GatLayer, ModelParams, SageLayer, init_params
-from paper_2303_13775_b200.metrics import EpochMetrics, IterationMetrics, account_transfer
+from paper_2303_13775_b200.metrics import (EpochMetrics, IterationMetrics, account_transfer, redundancy_report,
+                                           union_edge_count)
 from paper_2303_13775_b200.features import FeatureStore
 from paper_2303_13775_b200.exchange import LocalTransport, NcclTransport
 from paper_2303_13775_b200.engine import (

@@ -87,6 +87,7 @@ _SIGS = {
     "sg_sage_final_fused": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
     "sg_set_pdl": (None, [i32]),
+    "sg_split_cost": (i32, [vp, vp, vp, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
     "sg_reduce_partials_sgd": (i32, [vp, i32, i64, f32, vp]),
     "sg_get_pdl": (i32, []),
     "sg_sage_update": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32,

@@ -25,11 +25,11 @@ import torch
 from paper_2303_13775_b200 import _lib
 from paper_2303_13775_b200.exchange import LocalTransport
 from paper_2303_13775_b200.features import FeatureStore
-from paper_2303_13775_b200.metrics import EpochMetrics, IterationMetrics, account_transfer
+from paper_2303_13775_b200.metrics import EpochMetrics, IterationMetrics, account_transfer, union_edge_count
 from paper_2303_13775_b200.models import DeviceParams, ModelParams, init_params
-from paper_2303_13775_b200.partition import CacheState, PartitionMap
-from paper_2303_13775_b200.sampling import epoch_batches, sample_minibatch
-from paper_2303_13775_b200.scheduler import DeviceSplit, split_minibatch
+from paper_2303_13775_b200.partition import CacheState, PartitionMap, full_cache
+from paper_2303_13775_b200.sampling import epoch_batches, sample_microbatches, sample_minibatch
+from paper_2303_13775_b200.scheduler import DeviceSplit, split_cost_packed, split_minibatch
 
 DEBUG_CHECK_FINITE = False
 NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions
@@ -726,7 +726,55 @@ class Trainer:
         self.num_devices = pm.num_devices
         self.device = torch.device(device)
         self.feats = feats if isinstance(feats, FeatureStore) else FeatureStore.from_host(feats, cache, device=device)
+        self._host_feats = None if isinstance(feats, FeatureStore) else np.asarray(feats)
         self.labels_dev = _labels_dev(self.labels, self.device)
+        self._one = None
+
+    def _one_device(self):
+        """Single-device context for the `single` and `data_parallel` modes: a
+        one-part map and the whole feature table resident (each micro-batch /
+        mini-batch runs as the g = 1 case of the same kernels)."""
+        if self._one is None:
+            n = self.graph.num_vertices
+            pm1 = PartitionMap(np.zeros(n, dtype=np.int64), 1, 0.0)
+            cache1 = full_cache(pm1)
+            if self._host_feats is not None:
+                f1 = FeatureStore.from_host(self._host_feats, cache1, device=self.device)
+            elif getattr(self.feats, "identity", False):
+                f1 = self.feats
+            else:
+                raise ValueError("single/data_parallel modes need the whole feature table "
+                                 "(construct the Trainer with host features)")
+            masks = (self.cache.device_masks(n) if self.cache is not None and hasattr(self.cache, "device_masks")
+                     else [np.zeros(n, dtype=bool) for _ in range(self.num_devices)])
+            self._one = (pm1, cache1, f1, masks)
+        return self._one
+
+    def single_step(self, sample, dparams):
+        """One device runs the whole mini-batch (engine.py:677-683)."""
+        pm1, cache1, f1, _ = self._one_device()
+        ds = DeviceSplit.from_sample(sample, pm1, cache1, self.device)
+        step = SplitStep(dparams, ds, f1, self.labels_dev)
+        step.run()
+        return step
+
+    def data_parallel_step(self, micro_samples, dparams, record=None):
+        """Each device trains on its own independently sampled micro-batch
+        (engine.py:701-725); returns the per-device steps (gradients in
+        step.grads[0]), summed in device order by the caller."""
+        pm1, cache1, f1, masks = self._one_device()
+        if record is not None:
+            for d, m in enumerate(micro_samples):
+                v0 = np.asarray(m.vertices(0), dtype=np.int64)
+                missed = int(np.count_nonzero(~masks[d][v0]))
+                account_transfer(record, "host", missed * self.graph_feat_dim() * 8)
+        steps = []
+        for m in micro_samples:
+            ds = DeviceSplit.from_sample(m, pm1, cache1, self.device)
+            st = SplitStep(dparams, ds, f1, self.labels_dev)
+            st.run()
+            steps.append(st)
+        return steps
 
     def split_step(self, sample, dparams, record=None):
         ds = DeviceSplit.from_sample(sample, self.pm, self.cache, self.device)
@@ -738,8 +786,6 @@ class Trainer:
                   train_set=None):
         if mode not in ("single", "split", "data_parallel"):
             raise ValueError(f"unknown mode {mode!r}")
-        if mode != "split":
-            raise NotImplementedError(f"mode {mode!r} is outside the B200 hot path (SURVEY §8(f))")
         g = self.num_devices
         if train_set is None:
             train_set = np.arange(self.graph.num_vertices, dtype=np.int64)
@@ -752,9 +798,38 @@ class Trainer:
             brng = np.random.default_rng(ss.spawn(1)[0])
             rec = IterationMetrics(iteration=it, mode=mode, num_devices=g)
             t0 = time.perf_counter()
-            sample = sample_minibatch(self.graph, targets, fanouts, brng)
+            if mode == "data_parallel":
+                micros = sample_microbatches(self.graph, targets, g, fanouts, brng)
+            else:
+                sample = sample_minibatch(self.graph, targets, fanouts, brng)
             t1 = time.perf_counter()
             rec.sample_ms = (t1 - t0) * 1e3
+            if mode != "split":
+                t2 = time.perf_counter()
+                if mode == "single":
+                    rec.host_bytes = len(sample.vertices(0)) * self.graph_feat_dim() * 8
+                    steps = [self.single_step(sample, dp)]
+                    rec.edges_per_device[0] = sample.total_edges
+                    rec.local_edge_fraction = 1.0
+                else:
+                    steps = self.data_parallel_step(micros, dp, rec)
+                    for d in range(g):
+                        rec.edges_per_device[d] = micros[d].total_edges
+                    total = int(sum(m.total_edges for m in micros))
+                    rec.redundant_edges = total - union_edge_count(micros)
+                    counts = rec.edges_per_device.astype(np.float64)
+                    mean = counts.mean()
+                    rec.edge_skew = float((counts.max() - counts.min()) / mean) if mean else 0.0
+                    rec.local_edge_fraction = 1.0
+                ptrs = np.asarray([st.grads[0].data_ptr() for st in steps], dtype=np.int64)
+                _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), None, _lib.ptr(ptrs), len(steps), dp.n,
+                          float(lr) / len(targets), _lib.stream_ptr())
+                loss = sum(float(st.grads[0][dp.n].item()) for st in steps)
+                t3 = time.perf_counter()
+                rec.train_ms = (t3 - t2) * 1e3
+                rec.loss = loss / len(targets)
+                metrics.iterations.append(rec)
+                continue
             ds = DeviceSplit.from_sample(sample, self.pm, self.cache, self.device)
             m = ds.host_meta()
             t2 = time.perf_counter()
@@ -773,6 +848,9 @@ class Trainer:
             rec.wire_bytes = step.wire_bytes
             rec.edges_per_device = np.array([sum(int(m.n_edge[l][d]) for l in range(ds.L)) for d in range(g)],
                                             dtype=np.int64)
+            report = split_cost_packed(ds.V, ds.esrc, ds.edst, ds.nV, ds.nE, self.pm, g)
+            rec.edge_skew = report.edge_skew
+            rec.local_edge_fraction = report.local_edge_fraction
             t3 = time.perf_counter()
             rec.train_ms = (t3 - t2) * 1e3
             rec.loss = loss / len(targets)

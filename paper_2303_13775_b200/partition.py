@@ -88,6 +88,15 @@ class CacheState:
             mask[ids] = True
         return mask
 
+    def device_masks(self, n):
+        """Per-device boolean cache masks (partition.py:77-83)."""
+        masks = []
+        for ids in self.cached:
+            m = np.zeros(n, dtype=bool)
+            m[ids] = True
+            masks.append(m)
+        return masks
+
     def device_bits(self, n, device="cuda"):
         """Global cache mask as a uint32 bitmap on the GPU (cached)."""
         import torch

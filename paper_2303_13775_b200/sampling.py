@@ -61,6 +61,16 @@ class MiniBatchSample:
             self.dst_grouped = ok
         return bool(self.dst_grouped)
 
+    def edge_gid_triples(self) -> np.ndarray:
+        """All edges as (layer, src_gid, dst_gid) rows (sampling.py:52-66)."""
+        rows = []
+        for l in range(1, len(self.layer_edges) + 1):
+            src, dst = self.layer_edges[l - 1]
+            rows.append(np.column_stack([np.full(len(src), l, dtype=np.int64),
+                                         np.asarray(self.layer_vertices[l - 1], np.int64)[src],
+                                         np.asarray(self.layer_vertices[l], np.int64)[dst]]))
+        return np.concatenate(rows) if rows else np.empty((0, 3), dtype=np.int64)
+
     def packed(self):
         """(V, esrc, edst) int32 concatenations used by the device splitter."""
         V = np.concatenate([np.asarray(v, dtype=np.int32) for v in self.layer_vertices])
@@ -162,6 +172,21 @@ def sample_minibatch(graph, targets, fanouts, rng) -> MiniBatchSample:
         _SAMPLERS.clear()
         _SAMPLERS[key] = s
     return s.sample(targets, fanouts, seed)
+
+
+def sample_microbatches(graph, targets, g, fanouts, rng) -> list:
+    """Round-robin split of `targets` into g independently sampled batches
+    (sampling.py:180-196): the data-parallel baseline's micro-batches."""
+    targets = np.asarray(targets, dtype=np.int64)
+    if g < 1:
+        raise ValueError("g must be >= 1")
+    if g == 1:
+        return [sample_minibatch(graph, targets, fanouts, rng)]
+    groups = [targets[i::g] for i in range(g)]
+    if any(len(gr) == 0 for gr in groups):
+        raise ValueError(f"cannot split {len(targets)} targets into {g} micro-batches")
+    children = rng.spawn(g)
+    return [sample_minibatch(graph, gr, fanouts, child) for gr, child in zip(groups, children)]
 
 
 def epoch_batches(train_set, batch_size, rng) -> list:

@@ -317,3 +317,113 @@ def transfer_manifest(splits, cache, feat_dim) -> TransferManifest:
         cached = np.concatenate(cache.cached) if cache.cached else loads[:0]
         assert not np.intersect1d(loads, cached).size, "splits predate this cache"
     return TransferManifest(host, np.zeros((g, g), dtype=np.int64))
+
+
+@dataclass
+class SplitCostReport:
+    """Communication-cost view of one sample under a vertex assignment
+    (scheduler.py:126-147)."""
+
+    num_devices: int
+    per_layer_cost: list  # per layer 1..L: C[v^l] array over V^(l)
+    cost_per_layer: list
+    cost_total: int
+    edges_per_device_per_layer: list
+    edges_per_device: np.ndarray
+    edges_local_per_layer: list
+    edges_total_per_layer: list
+    skew_per_layer: list
+    edge_skew: float
+    local_edge_fraction: float
+
+    @property
+    def edges_total(self) -> int:
+        return int(sum(self.edges_total_per_layer))
+
+    @property
+    def edges_local(self) -> int:
+        return int(sum(self.edges_local_per_layer))
+
+
+def _skew(counts) -> float:
+    """(max - min) / mean (scheduler.py:150-154)."""
+    counts = np.asarray(counts)
+    mean = counts.mean() if len(counts) else 0.0
+    if mean == 0:
+        return 0.0
+    return float((counts.max() - counts.min()) / mean)
+
+
+def split_cost(sample, assignment, num_devices: int | None = None, device=None) -> SplitCostReport:
+    """scheduler.py:257-309 on the GPU (sg_split_cost): per-vertex shuffle cost
+    C[v^l] = number of foreign devices holding a source of v's in-edges, edge
+    skew and edge locality of the sample under `assignment`."""
+    sample = as_sample(sample)
+    if isinstance(assignment, PartitionMap):
+        pm = assignment
+        if num_devices is None:
+            num_devices = pm.num_devices
+    else:
+        asn = np.asarray(assignment, dtype=np.int64)
+        gg = int(num_devices if num_devices is not None else asn.max() + 1)
+        pm = PartitionMap(asn, gg, float(gg))
+    g = int(num_devices if num_devices is not None else pm.num_devices)
+    if g > pm.num_devices:
+        pm = PartitionMap(pm.assignment, g, float(g))
+    dev = torch.device(device or "cuda")
+    nV, nE = sample.sizes()
+    L = len(nE)
+    n = len(pm.assignment)
+    for v in sample.layer_vertices:
+        v = np.asarray(v)
+        if len(v) and (v.max() >= n or v.min() < 0):
+            raise ValueError("sample vertex missing from partition map")
+    V, es, ed = sample.packed()
+    return split_cost_packed(torch.from_numpy(V).to(dev), torch.from_numpy(es).to(dev),
+                             torch.from_numpy(ed).to(dev), nV, nE, pm, g)
+
+
+def split_cost_packed(Vt, st_, dt_, nV, nE, pm: PartitionMap, g: int) -> SplitCostReport:
+    """split_cost on a sample already resident on the device (packed int32
+    V / esrc / edst, as DeviceSplit holds it)."""
+    dev = Vt.device
+    L = len(nE)
+    n = len(pm.assignment)
+    nrows = max(sum(nV[1:]), 1)
+    mask = torch.empty(nrows, dtype=torch.int32, device=dev)
+    cost_rows = torch.empty(nrows, dtype=torch.int32, device=dev)
+    counts = torch.empty(L * g, dtype=torch.int64, device=dev)
+    local = torch.empty(L, dtype=torch.int64, device=dev)
+    cost = torch.empty(L, dtype=torch.int64, device=dev)
+    err = torch.empty(1, dtype=torch.int32, device=dev)
+    nVa = np.asarray(nV, dtype=np.int64)
+    nEa = np.asarray(nE, dtype=np.int64)
+    _lib.call("sg_split_cost", _lib.ptr(Vt), _lib.ptr(st_), _lib.ptr(dt_), _lib.ptr(nVa), _lib.ptr(nEa), L,
+              _lib.ptr(pm.device_u8(dev)), n, g, _lib.ptr(mask), _lib.ptr(cost_rows), _lib.ptr(counts),
+              _lib.ptr(local), _lib.ptr(cost), _lib.ptr(err), _lib.stream_ptr())
+    if int(err.item()):
+        raise ValueError("sample vertex missing from partition map")
+    cr = cost_rows.cpu().numpy().astype(np.int64)
+    cnt = counts.cpu().numpy().reshape(L, g) if L else np.zeros((0, g), np.int64)
+    loc = local.cpu().numpy()
+    cpl = cost.cpu().numpy()
+    per_layer_cost, off = [], 0
+    for l in range(1, L + 1):
+        per_layer_cost.append(cr[off:off + nV[l]].copy())
+        off += nV[l]
+    edges_pd_pl = [cnt[l].astype(np.int64) for l in range(L)]
+    edges_per_device = np.sum(edges_pd_pl, axis=0) if edges_pd_pl else np.zeros(g, dtype=np.int64)
+    total = int(sum(nE))
+    return SplitCostReport(
+        num_devices=g,
+        per_layer_cost=per_layer_cost,
+        cost_per_layer=[int(c) for c in cpl],
+        cost_total=int(cpl.sum()),
+        edges_per_device_per_layer=edges_pd_pl,
+        edges_per_device=edges_per_device,
+        edges_local_per_layer=[int(x) for x in loc],
+        edges_total_per_layer=[int(x) for x in nE],
+        skew_per_layer=[_skew(c) for c in edges_pd_pl],
+        edge_skew=_skew(edges_per_device),
+        local_edge_fraction=(int(loc.sum()) / total) if total else 1.0,
+    )

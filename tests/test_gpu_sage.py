@@ -224,3 +224,53 @@ def test_single_device_fused_paths_match_unfused(F):
     rloss, rgrads = ref.run()
     assert abs(float(g_f[dp.n]) - rloss) <= TOL * abs(rloss)
     assert_grads_close(dp.grads_to_dict(torch.from_numpy(g_f)), rgrads[0], TOL, 0)
+
+
+@pytest.mark.parametrize("mode", ["split", "single", "data_parallel"])
+def test_trainer_modes_match_oracle(mode):
+    """Trainer.run_epoch (engine.py:729-826) in all three reference modes: the
+    parameters after an epoch equal the oracle's replay of the same samples
+    (split: cooperative g = 2; single: one device; data_parallel: g
+    independently sampled micro-batches, gradients summed in device order),
+    and the iteration metrics follow the reference's definitions."""
+    import paper_2303_13775_b200 as sg
+    from oracle.model_oracle import single_device_run
+    graph = sg.generate_powerlaw(3000, 30000, blocks=4, p_local=0.7, seed=21)
+    g = 2
+    pm = sg.range_partition(graph.num_vertices, g)
+    cache = sg.build_cache(graph, pm, 0.3)
+    F, C = 12, 5
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=1)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
+    graph = graph.with_features(feats)
+    params = sg.init_params("graphsage", F, 8, C, 2, seed=3)
+    ref = glorot_params("graphsage", F, 8, C, 2, seed=3)
+    train = np.arange(0, 3000, 7)
+    tr = sg.Trainer(graph, pm, cache, labels)
+    rec = tr.run_epoch(mode, params, seed=5, epoch=0, fanouts=[4, 3], batch_size=128, lr=0.1, train_set=train)
+    # replay the epoch's samples on the oracle (same seed protocol, engine.py:752-759)
+    ss = np.random.SeedSequence([5, 0])
+    batches = sg.epoch_batches(train, 128, np.random.default_rng(ss.spawn(1)[0]))
+    for it, targets in enumerate(batches):
+        brng = np.random.default_rng(ss.spawn(1)[0])
+        if mode == "data_parallel":
+            micros = sg.sample_microbatches(graph, targets, g, [4, 3], brng)
+            per = [single_device_run(m.layer_vertices, m.layer_edges, ref, feats.astype(np.float64), labels)[1]
+                   for m in micros]
+            r = rec.iterations[it]
+            assert r.edges_per_device.tolist() == [m.total_edges for m in micros]
+            assert r.redundant_edges == sum(m.total_edges for m in micros) - sg.union_edge_count(micros)
+        else:
+            smp = sg.sample_minibatch(graph, targets, [4, 3], brng)
+            if mode == "single":
+                per = [single_device_run(smp.layer_vertices, smp.layer_edges, ref, feats.astype(np.float64),
+                                         labels)[1]]
+            else:
+                ws, wp = split_sample(smp.layer_vertices, smp.layer_edges, pm.assignment, g, cache.cached)
+                per = CoopRun(ref, ws, wp, feats.astype(np.float64), labels).run()[1]
+                cost = sg.split_cost(smp, pm, g)
+                assert rec.iterations[it].local_edge_fraction == cost.local_edge_fraction
+                assert rec.iterations[it].edge_skew == cost.edge_skew
+        reduce_and_sgd(ref, per, 0.1, len(targets))
+    for k, v in params.tensors().items():
+        assert rel_err(v, ref[k]) < 1e-4, k

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from golden_io import unpack_sample, unpack_splits
-from helpers import (GOLD, assert_split_equal, cached_lists, plan_as_dict, random_partition_case,
+from helpers import (GOLD, assert_split_equal, cached_lists, load_golden, plan_as_dict, random_partition_case,
                      splits_as_dicts)
 from oracle.split_oracle import split_sample
 
@@ -95,3 +95,24 @@ def test_split_is_pure_and_deterministic():
     b = sg.split_minibatch(sample, pm, cache)
     assert_split_equal(splits_as_dicts(a[0]), plan_as_dict(a[1]), splits_as_dicts(b[0]),
                        plan_as_dict(b[1]))
+
+
+@pytest.mark.parametrize("name", ["split_random_0", "split_random_1", "split_random_2", "split_random_3",
+                                  "split_random_4", "split_random_5", "edge_single_cross", "edge_all_on_one",
+                                  "workload3_graphsage"])
+def test_split_cost_matches_reference_golden(name):
+    """split_cost (scheduler.py:257-309) on the GPU: cost per layer, per-device
+    edge counts bit-exact; skew and locality equal to the reference's."""
+    import paper_2303_13775_b200 as sg
+    z = load_golden(name)
+    V, E = unpack_sample(z)
+    g = int(z["g"])
+    pm = sg.PartitionMap(z["assignment"], g, float(g))
+    rep = sg.split_cost(sg.MiniBatchSample(len(E), V, E), pm, g)
+    assert rep.cost_per_layer == [int(x) for x in z["cost_per_layer"]]
+    assert np.array_equal(rep.edges_per_device, z["edges_per_device"])
+    assert abs(rep.local_edge_fraction - float(z["local_edge_fraction"])) < 1e-12
+    assert abs(rep.edge_skew - float(z["edge_skew"])) < 1e-12
+    assert rep.cost_per_layer == [int(x) for x in z["pair_count"]]  # C[v^l] summed == pair_count(l)
+    for l, c in enumerate(rep.per_layer_cost):
+        assert len(c) == len(V[l + 1]) and c.sum() == rep.cost_per_layer[l]

@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for i in 1 2; do timeout 120 python bench.py --no-cpu-baseline --steps 20 2>gpurun_out/e.err | python -c "
-import json,sys;d=json.loads(sys.stdin.read().strip().splitlines()[-1]);print(round(d['ms_per_step'],4),'agg1',round(d['roofline']['avg_launch_ms'],4), round(d['roofline']['frac'],3),'e2e',round(d['e2e']['ms_per_step'],4), d['loss_last'], d['gpu_launches'], d['phases_ms'])"; done
+SG_BENCH_HOST_STAGED=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/n2.json 2> gpurun_out/n2.err; echo rc=$?
+grep -v "^frame" gpurun_out/n2.err | tail -5; tail -c 1500 gpurun_out/n2.json
+timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --impl reference --gpus 2 --steps 2 --warmup 1 2>&1 | tail -2
