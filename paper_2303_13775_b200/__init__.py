@@ -11,6 +11,8 @@ from paper_2303_13775_b200.graph import (
     GraphError,
     from_edges,
     generate_powerlaw,
+    load_binary_csr,
+    save_binary_csr,
     synthetic_features,
     synthetic_labels,
 )
@@ -35,8 +37,8 @@ from paper_2303_13775_b200.scheduler import (
     transfer_manifest,
 )
 from paper_2303_13775_b200.models import DeviceParams, GatLayer, ModelParams, SageLayer, init_params
-from paper_2303_13775_b200.metrics import (EpochMetrics, IterationMetrics, account_transfer, redundancy_report,
-                                           union_edge_count)
+from paper_2303_13775_b200.metrics import (EpochMetrics, IterationMetrics, account_transfer, emit_csv, read_csv,
+                                           redundancy_report, union_edge_count)
 from paper_2303_13775_b200.features import FeatureStore
 from paper_2303_13775_b200.exchange import LocalTransport, NcclTransport
 from paper_2303_13775_b200.engine import (

@@ -118,3 +118,54 @@ def synthetic_labels(n, num_classes, seed) -> np.ndarray:
     out = np.empty(int(n), dtype=np.int32)
     _lib.check(lib.sg_gen_labels(int(n), int(num_classes), int(seed), _lib.ptr(out)), "gen_labels")
     return out
+
+
+# ---- SPLG binary CSR (graph.py:238-273 of the reference: same byte layout) -------
+BINARY_MAGIC = b"SPLG"
+BINARY_VERSION = 1
+
+
+def save_binary_csr(graph: Graph, path):
+    """magic, u32 version, u64 n, m, feat_dim, then i64 row_offsets, i64
+    col_indices and (feat_dim > 0) f64 features, little-endian."""
+    import struct
+    with open(path, "wb") as fh:
+        fh.write(BINARY_MAGIC)
+        fh.write(struct.pack("<I", BINARY_VERSION))
+        fh.write(struct.pack("<QQQ", graph.num_vertices, graph.num_edges, graph.feat_dim))
+        fh.write(graph.row_offsets.astype("<i8").tobytes())
+        chunk = 1 << 26
+        for i in range(0, graph.num_edges, chunk):
+            fh.write(graph.col_indices[i:i + chunk].astype("<i8").tobytes())
+        if graph.features is not None:
+            for i in range(0, graph.num_vertices, 1 << 20):
+                fh.write(graph.features[i:i + (1 << 20)].astype("<f8").tobytes())
+
+
+def load_binary_csr(path) -> Graph:
+    """Memory-mapped SPLG reader: the i64 arrays are mapped, not read, and
+    narrowed chunk by chunk (papers100M: 1.6B edges)."""
+    import struct
+    with open(path, "rb") as fh:
+        magic = fh.read(4)
+        if magic != BINARY_MAGIC:
+            raise GraphError(f"{path}: bad magic {magic!r}")
+        (version,) = struct.unpack("<I", fh.read(4))
+        if version != BINARY_VERSION:
+            raise GraphError(f"{path}: unsupported version {version}")
+        n, m, fd = struct.unpack("<QQQ", fh.read(24))
+    base = 4 + 4 + 24
+    mm = np.memmap(path, dtype="<i8", mode="r", offset=base, shape=(n + 1 + m,))
+    offsets = np.asarray(mm[:n + 1], dtype=np.int64)
+    indices = np.empty(m, dtype=np.int32)
+    chunk = 1 << 26
+    for i in range(0, m, chunk):
+        indices[i:i + chunk] = mm[n + 1 + i:n + 1 + min(m, i + chunk)]
+    feats = None
+    if fd:
+        fm = np.memmap(path, dtype="<f8", mode="r", offset=base + 8 * (n + 1 + m), shape=(n, fd))
+        feats = np.empty((n, fd), dtype=np.float32)
+        for i in range(0, n, 1 << 20):
+            feats[i:i + (1 << 20)] = fm[i:i + (1 << 20)]
+    del mm
+    return Graph(int(n), offsets, indices, feats)
