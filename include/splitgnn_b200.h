@@ -333,6 +333,38 @@ int sg_split_cost(const int32_t* V, const int32_t* esrc, const int32_t* edst, co
                   const int64_t* nE, int32_t L, const uint8_t* assignment, int64_t n_vertices,
                   int32_t g, uint32_t* mask_ws, int32_t* cost_rows, int64_t* counts,
                   int64_t* local, int64_t* cost, int32_t* err, void* stream);
+/* ---- peer-memory transport (one rank per GPU; replaces the NCCL
+ * all-to-all-v of engine.py:121-156 with IPC-mapped buffers) ----------------
+ * peer_bufs / peer_flags: g device pointers (this rank's own entry included),
+ * each a peer's buffer mapped into this process.
+ * sg_peer_exchange push=1 (push-to-owner): this rank's pair-slot rows of
+ * `local` are written into each owner's buffer at their receive slot.
+ * push=0 (push-from-owner): this rank's pair-slot rows of `local` are read
+ * from each owner's buffer (packed at receive slots by sg_pack_from_owner).
+ * sg_peer_signal stores the current epoch into slot [round][rank] of every
+ * peer's flag array; sg_peer_wait blocks the stream until every peer has
+ * signalled `round` for the current epoch (*timeout set if a peer vanished);
+ * sg_peer_epoch bumps the epoch once per step. */
+int sg_peer_rounds(void);
+int sg_peer_exchange(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t rank,
+                     int32_t push, float* local, int32_t stride, const int64_t* peer_bufs,
+                     void* stream);
+int sg_peer_signal(const int64_t* peer_flags, int32_t rank, int32_t g, int32_t round,
+                   const int32_t* epoch, void* stream);
+int sg_peer_wait(const int32_t* my_flags, int32_t rank, int32_t g, int32_t round,
+                 const int32_t* epoch, int32_t* timeout, void* stream);
+int sg_peer_epoch(int32_t* epoch, void* stream);
+/* Gradient all-reduce + SGD over peer memory (allreduce_and_step,
+ * engine.py:633-647): stage this rank's n1 = n + 1 floats (gradient + loss
+ * slot) into slot (epoch & 1) of its shared slots (2 x slot_stride floats),
+ * then, after a signal/wait round, every rank sums all ranks' slots in rank
+ * order (identical on every rank), writes the sum to grads_out (optional) and
+ * applies params[k] -= scale * sum[k] for k < n. */
+int sg_peer_grad_stage(const float* grads, float* my_slots, int64_t n1, int64_t slot_stride,
+                       const int32_t* epoch, void* stream);
+int sg_peer_allreduce_sgd(const int64_t* peer_slots, int32_t g, int64_t n, int64_t n1,
+                          int64_t slot_stride, const int32_t* epoch, float* params, float* grads_out,
+                          float scale, void* stream);
 /* sg_reduce_partials with the SGD step fused (single device, nothing to
  * all-reduce): jobs are 6 int64 per job {partials, nblocks, n, out, param,
  * n_sgd}; the first n_sgd summed columns g also update param: p -= scale*g

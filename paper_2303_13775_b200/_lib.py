@@ -87,6 +87,13 @@ _SIGS = {
     "sg_sage_final_fused": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
     "sg_set_pdl": (None, [i32]),
+    "sg_peer_rounds": (i32, []),
+    "sg_peer_exchange": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, i32, vp, vp]),
+    "sg_peer_signal": (i32, [vp, i32, i32, i32, vp, vp]),
+    "sg_peer_wait": (i32, [vp, i32, i32, i32, vp, vp, vp]),
+    "sg_peer_epoch": (i32, [vp, vp]),
+    "sg_peer_grad_stage": (i32, [vp, vp, i64, i64, vp, vp]),
+    "sg_peer_allreduce_sgd": (i32, [vp, i32, i64, i64, i64, vp, vp, vp, f32, vp]),
     "sg_split_cost": (i32, [vp, vp, vp, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
     "sg_reduce_partials_sgd": (i32, [vp, i32, i64, f32, vp]),
     "sg_get_pdl": (i32, []),

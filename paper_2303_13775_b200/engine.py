@@ -124,6 +124,15 @@ class SplitStep:
         return (self.g == 1 and dperm is None and w % 4 == 0 and w <= 128 and dout in (4, 8, 16, 32)
                 and not getattr(self, "no_fuse", False))
 
+    def _xbuf(self, P, *shape):
+        """A round's exchange buffer: the peer-mapped one of a PeerTransport
+        (same request order on every rank), else a plain device tensor."""
+        shared = getattr(self.transport, "shared", None)
+        if shared is None or self.g == 1 or P <= 0:
+            return _f32(P, *shape, device=self.dev)
+        width = int(np.prod(shape)) if shape else 1
+        return shared(P, width).view(P, *shape)
+
     def _final_fused_ok(self, w, dout, dperm):
         """Single-device split: the last layer, the loss and the last layer's
         row-local backward run as one kernel (sg_sage_final_fused)."""
@@ -215,6 +224,8 @@ class SplitStep:
         return out
 
     def forward(self):
+        if hasattr(self.transport, "begin_step"):
+            self.transport.begin_step()
         if self.kind != "graphsage":
             from paper_2303_13775_b200.gat import gat_forward
             return gat_forward(self)
@@ -255,7 +266,7 @@ class SplitStep:
             SW = _r4(w + 1)
             P = ds.pair_bound(l)
             send = _f32(P, SW, device=self.dev)
-            recv = _f32(P, SW, device=self.dev)
+            recv = self._xbuf(P, SW)
             self._ev(f"agg{l}_start")
             self._ev(f"ph:agg{l}:s")
             for d in self.devices:
@@ -406,7 +417,7 @@ class SplitStep:
                 break
             SWb = _r4(w)
             P = ds.pair_bound(l)
-            bsend = _f32(P, SWb, device=self.dev)
+            bsend = self._xbuf(P, SWb)
             brecv = _f32(P, SWb, device=self.dev)
             if self.g > 1 and P > 0:
                 for d in self.devices:
@@ -1123,13 +1134,56 @@ class RankSplitTrainer:
 
     def step(self, sample, lr, record_events=False, dsplit=None):
         ds = dsplit if dsplit is not None else DeviceSplit.from_sample(sample, self.pm, self.cache, self.dev)
+        peer = hasattr(self.transport, "all_reduce_sgd")
         st = SplitStep(self.dp, ds, self.feats, self.labels, devices=[self.rank],
-                       transport=self.transport, exact=True, record_events=record_events)
+                       transport=self.transport, exact=not peer, record_events=record_events)
         st.run()
         gbuf = st.grads[self.rank]
-        self.transport.all_reduce(gbuf)          # sum over ranks (includes the loss slot)
-        ptrs = np.asarray([gbuf.data_ptr()], dtype=np.int64)
-        _lib.call("sg_sum_sgd", _lib.ptr(self.dp.flat), None, _lib.ptr(ptrs), 1, self.dp.n,
-                  float(lr) / len(sample.targets), _lib.stream_ptr())
+        scale = float(lr) / len(sample.targets)
+        if peer:  # all-reduce + SGD over peer memory (no host round trip)
+            out = torch.empty_like(gbuf)
+            self.transport.all_reduce_sgd(gbuf, self.dp.n, self.dp.flat, scale, grads_out=out)
+            gbuf = out
+        else:
+            self.transport.all_reduce(gbuf)          # sum over ranks (includes the loss slot)
+            ptrs = np.asarray([gbuf.data_ptr()], dtype=np.int64)
+            _lib.call("sg_sum_sgd", _lib.ptr(self.dp.flat), None, _lib.ptr(ptrs), 1, self.dp.n,
+                      scale, _lib.stream_ptr())
         self.last = st
         return gbuf
+
+
+class RankCapturedStep(CapturedStep):
+    """This rank's part of the multi-GPU split step (rank = split part) as ONE
+    CUDA graph: replicated split -> rank-local forward/backward whose exchange
+    rounds run over the PeerTransport's mapped buffers -> peer all-reduce +
+    SGD. Sizes are read on the device; nothing returns to the host."""
+
+    def __init__(self, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale, rank, transport,
+                 device="cuda", record_events=False):
+        if not hasattr(transport, "all_reduce_sgd"):
+            raise ValueError("RankCapturedStep needs a PeerTransport (no host-side sizes inside a graph)")
+        self.p = dparams
+        self.pm, self.cache, self.f, self.labels = pm, cache, feats, labels_dev
+        self.dev = torch.device(device)
+        self.inp = StaticSample(cap_nV, cap_nE, self.dev)
+        self.scale = float(lr_scale)
+        self.record_events = record_events
+        self.graph = None
+        self.rank = int(rank)
+        self.transport = transport
+        self.gsum = None
+
+    def _body(self):
+        inp = self.inp
+        ds = DeviceSplit(inp.V, inp.es, inp.ed, inp.cap_nV, inp.cap_nE, self.pm, self.cache, True,
+                         self.dev, sizes=inp.sizes)
+        step = SplitStep(self.p, ds, self.f, self.labels, devices=[self.rank], transport=self.transport,
+                         exact=False, record_events=self.record_events)
+        step.run()
+        gbuf = step.grads[self.rank]
+        if self.gsum is None:
+            self.gsum = torch.empty_like(gbuf)
+        self.transport.all_reduce_sgd(gbuf, self.p.n, self.p.flat, self.scale, grads_out=self.gsum)
+        self.ds, self.step = ds, step
+        return self.gsum

@@ -87,3 +87,134 @@ class NcclTransport:
         r0, r1 = int(m.ref_off[l][r]), int(m.ref_off[l][r + 1])
         self._a2a(recv_pair_layout[r0:r1].reshape(-1), send_recv_layout[s0:s1].reshape(-1),
                   [c * stride for c in send_rows], [c * stride for c in recv_rows])
+
+
+class PeerTransport:
+    """One rank per GPU, exchanges over peer memory (csrc/peer.cu): every
+    round's buffer of every rank is mapped into its peers with CUDA IPC
+    (torch's storage sharing), rows move with one kernel writing (push-to-
+    owner) or reading (push-from-owner) the peers' buffers at the GLOBAL slot
+    numbering every rank knows from the replicated split, and device flags
+    tagged with a per-step epoch order the rounds. No sizes go to the host, so
+    the rank-local step is capturable as one CUDA graph
+    (engine.RankCapturedStep). The gradient all-reduce + SGD runs over the same
+    mapped memory (all_reduce_sgd) and doubles as the step barrier.
+
+    Buffers are requested per round with `shared(rows, stride)` in the same
+    order on every rank (the engine's program order); the first request of a
+    round allocates and exchanges handles (a collective over `group`)."""
+
+    kind = "peer"
+
+    def __init__(self, rank, world_size, group=None, device=None):
+        import torch
+        self.rank = int(rank)
+        self.world = int(world_size)
+        self.group = group
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        lib = _lib.load()
+        self.rounds = int(lib.sg_peer_rounds())
+        self._keep = []
+        nflag = self.rounds * 16
+        self.flags = torch.zeros(nflag + 64, dtype=torch.int32, device=self.dev)
+        self.epoch = self.flags[nflag:nflag + 1]
+        self.timeout = self.flags[nflag + 32:nflag + 33]
+        self.peer_flags = self._share(self.flags)
+        self._bufs = {}
+        self._nbuf = 0
+        self._nx = 0
+        self._grad = None
+
+    # -- CUDA IPC mapping -----------------------------------------------------
+    def _share(self, t):
+        """All-gather IPC handles of `t`'s storage; returns the g peer pointers
+        (own entry = t itself) as an int64 array."""
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        st = t.untyped_storage()
+        h = st._share_cuda_()
+        off = t.data_ptr() - st.data_ptr()
+        hs = [None] * self.world
+        dist.all_gather_object(hs, (h, off), group=self.group)
+        ptrs = []
+        for r, (hr, offr) in enumerate(hs):
+            if r == self.rank:
+                ptrs.append(t.data_ptr())
+                continue
+            ps = torch.UntypedStorage._new_shared_cuda(*hr)
+            self._keep.append(ps)
+            ptrs.append(ps.data_ptr() + offr)
+        self._keep.append(t)
+        return np.asarray(ptrs, dtype=np.int64)
+
+    # -- per-step protocol ------------------------------------------------------
+    def begin_step(self):
+        self._nbuf = 0
+        self._nx = 0
+        _lib.call("sg_peer_epoch", _lib.ptr(self.epoch), _lib.stream_ptr())
+
+    def shared(self, rows, stride):
+        """This round's exchange buffer (rows x stride fp32), mapped into every peer."""
+        import torch
+        k = self._nbuf
+        self._nbuf += 1
+        if k >= self.rounds:
+            raise RuntimeError(f"more than {self.rounds} exchange rounds in one step")
+        need = max(int(rows) * int(stride), 4)
+        cur = self._bufs.get(k)
+        if cur is None or cur[0].numel() < need:
+            t = torch.empty(need, dtype=torch.float32, device=self.dev)
+            cur = (t, self._share(t))
+            self._bufs[k] = cur
+        return cur[0][:need].view(-1, int(stride)) if rows else cur[0][:0].view(0, int(stride))
+
+    def _round(self, buf):
+        k = self._nx
+        self._nx += 1
+        t, peers = self._bufs[k]
+        if buf.data_ptr() != t.data_ptr():
+            raise RuntimeError("exchange buffer was not requested from this transport for this round")
+        return k, peers
+
+    def _signal_wait(self, k):
+        st = _lib.stream_ptr()
+        _lib.call("sg_peer_signal", _lib.ptr(self.peer_flags), self.rank, self.world, k, _lib.ptr(self.epoch), st)
+        _lib.call("sg_peer_wait", _lib.ptr(self.flags), self.rank, self.world, k, _lib.ptr(self.epoch),
+                  _lib.ptr(self.timeout), st)
+
+    def to_owner(self, dsplit, l, send, recv, stride):
+        """Push this rank's pair-slot rows into the owners' receive buffers."""
+        k, peers = self._round(recv)
+        _lib.call("sg_peer_exchange", _lib.ptr(dsplit.ws), dsplit.lay, l, self.rank, 1, _lib.ptr(send),
+                  int(stride), _lib.ptr(peers), _lib.stream_ptr())
+        self._signal_wait(k)
+
+    def from_owner(self, dsplit, l, send_recv_layout, recv_pair_layout, stride):
+        """Owners packed their rows (receive-slot layout) into this round's
+        shared buffer; after the round's flags, pull this rank's pair slots."""
+        k, peers = self._round(send_recv_layout)
+        self._signal_wait(k)
+        _lib.call("sg_peer_exchange", _lib.ptr(dsplit.ws), dsplit.lay, l, self.rank, 0,
+                  _lib.ptr(recv_pair_layout), int(stride), _lib.ptr(peers), _lib.stream_ptr())
+
+    def all_reduce_sgd(self, gbuf, n, params_flat, scale, grads_out=None):
+        """Sum the ranks' flat gradients (+ loss slot) in rank order and apply
+        the SGD step, over peer memory (the step barrier)."""
+        import torch
+        n1 = int(gbuf.numel())
+        stride = (n1 + 63) // 64 * 64
+        if self._grad is None or self._grad[2] != stride:
+            t = torch.zeros(2 * stride, dtype=torch.float32, device=self.dev)
+            self._grad = (t, self._share(t), stride)
+        t, peers, stride = self._grad
+        st = _lib.stream_ptr()
+        _lib.call("sg_peer_grad_stage", _lib.ptr(gbuf), _lib.ptr(t), n1, stride, _lib.ptr(self.epoch), st)
+        self._signal_wait(self.rounds - 1)
+        _lib.call("sg_peer_allreduce_sgd", _lib.ptr(peers), self.world, int(n), n1, stride, _lib.ptr(self.epoch),
+                  _lib.ptr(params_flat), _lib.ptr(grads_out), float(scale), st)
+
+    def check(self):
+        """Raise if a peer wait timed out (a peer process is gone)."""
+        if int(self.timeout.item()):
+            raise RuntimeError("peer transport: a peer never signalled (timed out)")

@@ -33,7 +33,7 @@ def _from_owner(step, l, rows, width):
     P = ds.pair_bound(l)
     out = _f32(P, width, device=step.dev)
     if step.g > 1 and P > 0:
-        send = _f32(P, width, device=step.dev)
+        send = step._xbuf(P, width)
         st = _lib.stream_ptr()
         for d in step.devices:
             _lib.call("sg_pack_from_owner", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(rows), width,
@@ -73,7 +73,7 @@ def gat_forward(step):
         t_recv = _from_owner(step, l, t, H)
         SW = _r4(dout + 2 * H)
         send = _f32(P, SW, device=step.dev)
-        recv = _f32(P, SW, device=step.dev)
+        recv = step._xbuf(P, SW)
         pre_e = _f32(nEtot, *_hs(H), device=step.dev)
         loc_m = _f32(nV, *_hs(H), device=step.dev)
         loc_s = _f32(nV, *_hs(H), device=step.dev)
@@ -138,7 +138,7 @@ def gat_backward(step):
         d_pre = _f32(nEtot, *_hs(H), device=step.dev)
         dt_loc = _f32(nV, *_hs(H), device=step.dev)
         dt_send = _f32(P, *_hs(H), device=step.dev)
-        dt_recv = _f32(P, *_hs(H), device=step.dev)
+        dt_recv = step._xbuf(P, *_hs(H))
         with step.phase(f"bwd_dst{l}"):
             for d in step.devices:
                 _lib.call("sg_gat_bwd_dst", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, slope, _lib.ptr(keep["z"]),

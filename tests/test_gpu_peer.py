@@ -1,0 +1,120 @@
+"""Peer-memory transport (csrc/peer.cu, exchange.PeerTransport): two ranks as
+two processes sharing cuda:0, buffers mapped with CUDA IPC, rounds ordered by
+device epoch flags, gradients all-reduced over the mapped memory. Eager
+(RankSplitTrainer) and CUDA-graph captured (RankCapturedStep) steps must leave
+both replicas bit-identical and match the oracle's cooperative g = 2 run
+(engine.py:95-647) -- the multi-GPU step with no host round trip."""
+
+import os
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _setup(L=2):
+    import paper_2303_13775_b200 as sg
+    graph = sg.generate_powerlaw(8000, 80000, blocks=8, p_local=0.6, seed=2)
+    pm = sg.range_partition(graph.num_vertices, 2)
+    cache = sg.full_cache(pm)
+    rng = np.random.default_rng(7)
+    fan = [6, 4] if L == 2 else [6, 4, 3]
+    samples = [sg.sample_minibatch(graph, rng.choice(graph.num_vertices, 64, replace=False), fan, rng)
+               for _ in range(4)]
+    return graph, pm, cache, samples
+
+
+def _worker(rank, world, port, kind, captured, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2303_13775_b200 as sg
+        from paper_2303_13775_b200.engine import RankCapturedStep, RankSplitTrainer, capacities_for
+        torch.cuda.set_device(0)
+        L = 3 if captured else 2
+        graph, pm, cache, samples = _setup(L)
+        F, C = 12, 4
+        feats_host = sg.synthetic_features(graph.num_vertices, F, seed=1)
+        feats = sg.FeatureStore.from_host(feats_host, cache, devices=[rank])  # own shard only
+        labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
+        params = sg.init_params(kind, F, 8, C, L, seed=3)
+        tp = sg.PeerTransport(rank, world)
+        losses = []
+        if not captured:
+            tr = RankSplitTrainer(params, pm, cache, feats, labels, rank, world, tp)
+            for s in samples:
+                g = tr.step(s, 0.1)
+                losses.append(float(g[tr.dp.n].item()))
+            flat = tr.dp.flat
+        else:
+            dp = sg.DeviceParams.from_host(params)
+            lab = torch.from_numpy(labels).cuda()
+            cap_nV, cap_nE = capacities_for(samples, slack=1.1)
+            cs = RankCapturedStep(dp, pm, cache, feats, lab, cap_nV, cap_nE, 0.1 / 64, rank, tp)
+            cs.capture(samples[0])                 # step 0 (eager) + capture
+            losses.append(float(cs.out[dp.n].item()))
+            for s in samples[1:]:
+                cs.run(s)
+                losses.append(float(cs.out[dp.n].item()))
+            flat = dp.flat
+        torch.cuda.synchronize()
+        tp.check()
+        q.put((rank, losses, flat.cpu().numpy()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(kind, captured, port):
+    from oracle.coop_oracle import CoopRun, reduce_and_sgd
+    from oracle.model_oracle import glorot_params
+    from oracle.split_oracle import split_sample
+    import paper_2303_13775_b200 as sg
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, captured, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    import queue
+    import time
+    res, t0 = [], time.time()
+    while len(res) < len(procs):
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [p for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"a rank failed (exit codes {[p.exitcode for p in procs]})"
+            assert time.time() - t0 < 300, "ranks timed out"
+    res = sorted(res, key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+    (_, l0, p0), (_, l1, p1) = res
+    assert np.array_equal(p0, p1)            # replicas identical (rank-order sum on every rank)
+    assert l0 == l1
+    L = 3 if captured else 2
+    graph, pm, cache, samples = _setup(L)
+    F, C = 12, 4
+    X = sg.synthetic_features(graph.num_vertices, F, seed=1).astype(np.float64)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
+    ref = glorot_params(kind, F, 8, C, L, seed=3)
+    for i, s in enumerate(samples):
+        ws, wp = split_sample(s.layer_vertices, s.layer_edges, pm.assignment, 2, cache.cached)
+        loss, grads = CoopRun(ref, ws, wp, X, labels).run()
+        reduce_and_sgd(ref, grads, 0.1, len(s.targets))
+        assert abs(l0[i] - loss) <= 1e-4 * abs(loss), (i, l0[i], loss)
+    flat = np.concatenate([v.reshape(-1) for v in ref.values()])
+    assert np.abs(p0 - flat).max() / np.abs(flat).max() < 1e-4
+
+
+@pytest.mark.parametrize("kind", ["graphsage", "gat"])
+def test_peer_transport_eager_two_processes(kind):
+    _run(kind, False, 33000 + os.getpid() % 2000 + (7 if kind == "gat" else 0))
+
+
+def test_peer_transport_captured_step_two_processes():
+    _run("graphsage", True, 35100 + os.getpid() % 2000)
