@@ -361,7 +361,26 @@ def main():
     samples, iters_per_epoch = make_samples(graph, train, n_steps, args.batch, threads)
     params = sg.init_params(KIND, FEAT, HIDDEN, CLASSES, len(FANOUTS), seed=RUN_SEED, heads=HEADS)
     dp = sg.DeviceParams.from_host(params, dev)
-    transport = sg.NcclTransport(rank, world, stage_on_host=staged) if g > 1 else sg.LocalTransport()
+    # N > 1: the peer-memory transport (IPC-mapped buffers, device flags; the
+    # rank step is one CUDA graph) unless SG_TRANSPORT=nccl asks for the eager
+    # NCCL all-to-all-v path.
+    use_peer = g > 1 and os.environ.get("SG_TRANSPORT", "peer") == "peer"
+    if g == 1:
+        transport = sg.LocalTransport()
+    elif use_peer:
+        try:  # CUDA IPC between the ranks' GPUs; every rank must succeed
+            transport = sg.PeerTransport(rank, world, device=dev)
+            ok = 1
+        except Exception as exc:  # noqa: BLE001 - reported, then the NCCL path runs
+            print(f"[rank {rank}] peer transport unavailable ({exc}); using NCCL", file=sys.stderr)
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev if not staged else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            use_peer = False
+            transport = sg.NcclTransport(rank, world, stage_on_host=staged)
+    else:
+        transport = sg.NcclTransport(rank, world, stage_on_host=staged)
     # device-resident inputs
     dev_samples = []
     for s in samples:
@@ -380,12 +399,18 @@ def main():
     agg_ms, step_ms = [], []
     phases = {}
     clocks = ClockSampler(local)
-    if g == 1:
-        # ---- single GPU: the whole step is one captured CUDA graph ----------------
-        from paper_2303_13775_b200.engine import CapturedStep, capacities_for
+    if g == 1 or use_peer:
+        # ---- the whole (rank) step is one captured CUDA graph ----------------------
+        from paper_2303_13775_b200.engine import CapturedStep, RankCapturedStep, capacities_for
         cap_nV, cap_nE = capacities_for(samples)
-        cs = CapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, LR / args.batch, dev,
-                          record_events="agg")
+
+        def make_step(scale, record_events=False):
+            if g == 1:
+                return CapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, scale, dev,
+                                    record_events=record_events)
+            return RankCapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, scale, rank, transport,
+                                    dev, record_events=record_events)
+        cs = make_step(LR / args.batch, record_events="agg")
         cs.capture(samples[0])                     # eager warm-up step 0 + capture
         agg_in_graph = True
         for i in range(1, args.warmup):
@@ -412,8 +437,7 @@ def main():
             barrier()
             t_wall = time.perf_counter() - t_wall
         # diagnostic (untimed): a second capture with an event around every phase
-        diag = CapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, 0.0, dev,
-                            record_events="all")
+        diag = make_step(0.0, record_events="all")
         diag.capture(samples[0])
         nd = min(5, args.steps)
         for i in range(args.warmup, args.warmup + nd):
@@ -444,7 +468,7 @@ def main():
         # the user-facing captured step (no timing-event nodes in the graph),
         # fed from the sampler's output in pinned host memory (packed untimed)
         del diag
-        ce = CapturedStep(dp, pm, cache, feats, labels_dev, cap_nV, cap_nE, LR / args.batch, dev)
+        ce = make_step(LR / args.batch)
         ce.capture(samples[0])
         pinned = ce.prepare_pinned(samples[args.warmup:n_steps])
         ce.run_pipelined(pinned[:2])  # allocate the staging buffers (untimed)
@@ -566,7 +590,10 @@ def main():
                        "model": f"{KIND}-3l-h16" + (f"x{HEADS}" if HEADS > 1 else ""),
                        "global_batch": args.batch, "seq_len": None,
                        "parallelism": f"split{g}" + (" host-staged (gloo, one GPU): not an NVLink number"
-                                                      if staged else ""), "l2": "flushed between timed steps (256 MB write, "
+                                                      if staged else ""),
+                       "transport": "local" if g == 1 else ("peer (CUDA IPC, graph-captured rank step)"
+                                                            if use_peer else "nccl all-to-all-v (eager)"),
+                       "l2": "flushed between timed steps (256 MB write, "
                                                           "outside the per-step events)",
                        "epoch_iterations": iters_per_epoch,
                        "epoch_time_s": iters_per_epoch * my_ms / args.steps / 1e3,
