@@ -212,6 +212,27 @@ int sg_sage_final_fused(const void* split_ws, const SgSplitLayout* lay, int32_t 
                         const int32_t* V, const int32_t* labels, float* mean, float* counts,
                         float* h, float* d_self, float* d_sums, float* part_cls,
                         float* part_lay, int32_t nblocks, int64_t max_rows, void* stream);
+/* g > 1 owner side of a layer in one kernel: combine the local partial
+ * (sums, counts from sg_sage_agg_fwd) with the holders' partials in recv
+ * (receive slots, ascending sender: engine.py:197-210), mean, the two GEMVs,
+ * bias, ReLU unless final (:212-226). counts is updated to the combined N;
+ * mean, hs (self rows, n_own x w) and h are written. recv_stride % 4 == 0. */
+int sg_sage_combine_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                        const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                        const float* w_self, const float* w_neigh, const float* bias,
+                        int32_t final_layer, const float* sums, float* counts, const float* recv,
+                        int32_t recv_stride, float* mean, float* hs, float* h, int64_t max_rows,
+                        void* stream);
+/* sg_sage_final_fused for any g: the last layer's combine (as
+ * sg_sage_combine_fwd) + update + loss + row-local backward on device d. */
+int sg_sage_final_combine(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                          const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                          int32_t ncls, const float* w_self, const float* w_neigh,
+                          const float* bias, const float* w_cls, const float* b_cls,
+                          const int32_t* V, const int32_t* labels, const float* sums,
+                          const float* recv, int32_t recv_stride, float* mean, float* counts,
+                          float* h, float* d_self, float* d_sums, float* part_cls,
+                          float* part_lay, int32_t nblocks, int64_t max_rows, void* stream);
 /* Owner combine + update (engine.py:197-226): adds the holders' partial
  * (sum,count) rows from recvbuf in ascending sender order, mean = S/N,
  * pre = h_self@W_self + mean@W_neigh + b, h = relu(pre) unless final.

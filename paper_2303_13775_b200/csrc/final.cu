@@ -45,6 +45,11 @@ struct FinalArgs {
   float* d_sums;
   float* part_cls;
   float* part_lay;
+  // combine mode (g > 1): local partial + holders' partials (ascending sender)
+  const float* sums;
+  const float* recv;
+  const int32_t* contrib;
+  int stride, g;
 };
 
 __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ meta, FinalArgs a) {
@@ -99,16 +104,34 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
       const int r = warp;
       if (r < rows) {
         const int q = r0 + r;
-        const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
+        const int b = a.sums ? 0 : a.rowbeg[rb + q], e = a.sums ? 0 : a.rowend[rb + q];
         const int64_t G = own0 + q;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         const bool colok = lr < w4;
-        for (int j = b + eg; j < e; j += EG) {
-          int rr = prev0 + a.lsrc[a.eoff_li + j];
-          if (a.src_row) rr = a.src_row[rr];
-          if (colok) {
-            const float4 v = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * w + 4 * lr));
-            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        float cntf = (float)(e - b);
+        if (a.sums) {  // combine mode: eg == 0 lanes hold the row, the xor tree adds zeros
+          float N = a.counts[G];
+          if (eg == 0 && colok) acc = *reinterpret_cast<const float4*>(a.sums + G * w + 4 * lr);
+          const int32_t* cb = a.contrib + (int64_t)a.g * a.voff_l + G * a.g;
+          for (int s = 0; s < a.g; ++s) {
+            const int rs = cb[s];
+            if (rs < 0) continue;
+            const float* rrow = a.recv + (int64_t)rs * a.stride;
+            if (eg == 0 && colok) {
+              const float4 t = *reinterpret_cast<const float4*>(rrow + 4 * lr);
+              acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+            }
+            N += rrow[w];
+          }
+          cntf = N;
+        } else {
+          for (int j = b + eg; j < e; j += EG) {
+            int rr = prev0 + a.lsrc[a.eoff_li + j];
+            if (a.src_row) rr = a.src_row[rr];
+            if (colok) {
+              const float4 v = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * w + 4 * lr));
+              acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
           }
         }
         for (int o = LPR; o < 32; o <<= 1) {
@@ -121,7 +144,6 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
           int rs = prev0 + a.selfrow[a.voff_l + G];
           if (a.src_row) rs = a.src_row[rs];
           const float4 hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rs * w + 4 * lr));
-          const float cntf = (float)(e - b);
           const float inv = 1.0f / cntf;
           const float4 mn = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
           *reinterpret_cast<float4*>(A_s + r * K + 4 * lr) = hv;
@@ -248,22 +270,23 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
 
 using namespace sg;
 
-extern "C" int sg_sage_final_fused(const void* split_ws, const SgSplitLayout* lay, int32_t d,
-                                   const float* h_prev, const int32_t* src_row, int32_t w,
-                                   int32_t dout, int32_t ncls, const float* w_self,
-                                   const float* w_neigh, const float* bias, const float* w_cls,
-                                   const float* b_cls, const int32_t* V, const int32_t* labels,
-                                   float* mean, float* counts, float* h, float* d_self,
-                                   float* d_sums, float* part_cls, float* part_lay,
-                                   int32_t nblocks, int64_t max_rows, void* stream) {
+static int final_impl(const void* split_ws, const SgSplitLayout* lay, int32_t d, const float* h_prev,
+                      const int32_t* src_row, int32_t w, int32_t dout, int32_t ncls, const float* w_self,
+                      const float* w_neigh, const float* bias, const float* w_cls, const float* b_cls,
+                      const int32_t* V, const int32_t* labels, const float* sums, const float* recv,
+                      int32_t recv_stride, float* mean, float* counts, float* h, float* d_self, float* d_sums,
+                      float* part_cls, float* part_lay, int32_t nblocks, int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "sage_final_fused: null workspace");
   const char* base = (const char*)split_ws;
   const SgSplitLayout& y = *lay;
-  SG_REQUIRE(y.g == 1 && d == 0, "sage_final_fused: single-device split only");
+  SG_REQUIRE(d >= 0 && d < y.g, "sage_final_fused: bad device");
+  SG_REQUIRE(sums != nullptr || y.g == 1, "sage_final_fused: aggregate mode is single-device only");
+  SG_REQUIRE(y.g == 1 || (recv && recv_stride % 4 == 0 && recv_stride >= w + 1),
+             "sage_final_combine: recv stride must be a multiple of 4 and >= w + 1");
   SG_REQUIRE(w % 4 == 0 && w <= 128 && dout >= 1 && dout <= 64 && ncls >= 1 && ncls <= 1024,
              "sage_final_fused: needs w % 4 == 0, w <= 128, dout <= 64, classes <= 1024");
   SG_REQUIRE(nblocks >= 1, "sage_final_fused: nblocks >= 1");
-  if (max_rows <= 0) return SG_OK;
+  (void)max_rows;  // n_own is read on the device; an idle device still writes zero partials
   const int L = y.L;
   FinalArgs a;
   memset(&a, 0, sizeof(a));
@@ -278,6 +301,8 @@ extern "C" int sg_sage_final_fused(const void* split_ws, const SgSplitLayout* la
   a.ws = w_self; a.wn = w_neigh; a.bias = bias; a.wc = w_cls; a.bc = b_cls;
   a.mean = mean; a.counts = counts; a.h = h; a.d_self = d_self; a.d_sums = d_sums;
   a.part_cls = part_cls; a.part_lay = part_lay;
+  a.sums = sums; a.recv = recv; a.stride = recv_stride; a.g = (sums && y.g > 1) ? y.g : 0;
+  a.contrib = (const int32_t*)(base + y.o_contrib);
   const size_t nwd = (size_t)w * dout, nwc = (size_t)dout * ncls;
   auto r4 = [](size_t x) { return (x + 3) & ~(size_t)3; };
   const size_t floats = 2 * r4(nwd) + r4(dout) + r4(nwc) + r4(ncls) + FTR * 2 * (size_t)w +
@@ -289,4 +314,31 @@ extern "C" int sg_sage_final_fused(const void* split_ws, const SgSplitLayout* la
   ::sg::launch(k_sage_final, nblocks, 256, smem, (cudaStream_t)stream, (const SgMeta*)(base + y.o_meta), a);
   SG_CHECK_LAUNCH("k_sage_final");
   return SG_OK;
+}
+
+extern "C" int sg_sage_final_fused(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                                   const float* h_prev, const int32_t* src_row, int32_t w,
+                                   int32_t dout, int32_t ncls, const float* w_self,
+                                   const float* w_neigh, const float* bias, const float* w_cls,
+                                   const float* b_cls, const int32_t* V, const int32_t* labels,
+                                   float* mean, float* counts, float* h, float* d_self,
+                                   float* d_sums, float* part_cls, float* part_lay,
+                                   int32_t nblocks, int64_t max_rows, void* stream) {
+  return final_impl(split_ws, lay, d, h_prev, src_row, w, dout, ncls, w_self, w_neigh, bias, w_cls, b_cls, V,
+                    labels, nullptr, nullptr, 0, mean, counts, h, d_self, d_sums, part_cls, part_lay, nblocks,
+                    max_rows, stream);
+}
+
+extern "C" int sg_sage_final_combine(const void* split_ws, const SgSplitLayout* lay, int32_t d,
+                                     const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                                     int32_t ncls, const float* w_self, const float* w_neigh, const float* bias,
+                                     const float* w_cls, const float* b_cls, const int32_t* V,
+                                     const int32_t* labels, const float* sums, const float* recv,
+                                     int32_t recv_stride, float* mean, float* counts, float* h, float* d_self,
+                                     float* d_sums, float* part_cls, float* part_lay, int32_t nblocks,
+                                     int64_t max_rows, void* stream) {
+  SG_REQUIRE(sums && counts, "sage_final_combine: null sums/counts");
+  return final_impl(split_ws, lay, d, h_prev, src_row, w, dout, ncls, w_self, w_neigh, bias, w_cls, b_cls, V,
+                    labels, sums, recv, recv_stride, mean, counts, h, d_self, d_sums, part_cls, part_lay, nblocks,
+                    max_rows, stream);
 }

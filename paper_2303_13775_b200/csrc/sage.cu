@@ -229,6 +229,13 @@ struct FusedArgs {
   float* counts;
   float* hs;
   float* h;
+  // combine mode (g > 1, set by sg_sage_combine_fwd): the row's local partial
+  // (sums, counts) plus the holders' partials from recv in ascending sender
+  // order (engine.py:197-210) replace the aggregation
+  const float* sums;
+  const float* recv;
+  const int32_t* contrib;
+  int stride, g;
 };
 
 template <int LPR, int EG>
@@ -509,11 +516,12 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
   for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
     // ---- aggregation: warp wid owns tile rows [wid*RPW, wid*RPW + RPW)
     const int q0 = r0 + wid * RPW;
+    const bool comb = a.sums != nullptr;
     int be = 0;
-    if (lane < 2 * RPW && q0 + (lane >> 1) < n)
+    if (!comb && lane < 2 * RPW && q0 + (lane >> 1) < n)
       be = (lane & 1) ? a.rowend[rb + q0 + (lane >> 1)] : a.rowbeg[rb + q0 + (lane >> 1)];
     int b = __shfl_sync(0xffffffffu, be, 0), e = __shfl_sync(0xffffffffu, be, 1);
-    int rnext = (q0 < n && lane < e - b) ? edge_row(b + lane) : 0;
+    int rnext = (!comb && q0 < n && lane < e - b) ? edge_row(b + lane) : 0;
     __syncthreads();  // previous tile's GEMM done with A_s
     for (int i = 0; i < RPW; ++i) {
       const int q = q0 + i;
@@ -525,6 +533,26 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
       if (a.src_row) rself = a.src_row[rself];
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       float4 hv = make_float4(0.f, 0.f, 0.f, 0.f);
+      float cntf;
+      if (comb) {
+        float N = a.counts[G];
+        if (colok) {
+          acc = *reinterpret_cast<const float4*>(a.sums + G * w + col);
+          hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col));
+        }
+        const int32_t* cb = a.contrib + (int64_t)a.g * a.voff_l + G * a.g;
+        for (int s = 0; s < a.g; ++s) {
+          const int rs = cb[s];
+          if (rs < 0) continue;
+          const float* rrow = a.recv + (int64_t)rs * a.stride;
+          if (colok) {
+            const float4 t = *reinterpret_cast<const float4*>(rrow + col);
+            acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+          }
+          N += rrow[w];
+        }
+        cntf = N;
+      } else {
       // next row's bounds + first index hop, issued before this row's loads
       int nb = 0, ne = 0, lnext = 0;
       if (i + 1 < RPW && q + 1 < n) {
@@ -567,7 +595,8 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
         b = nb;
         e = ne;
       }
-      const float cntf = (float)(ec - bc);
+      cntf = (float)(ec - bc);
+      }
       const float inv = 1.0f / cntf;
       const float4 mn = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
       const int rr = wid * RPW + i;
@@ -1377,6 +1406,31 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   if (rc) return rc;
   LinArgs la{l, d, w, dout, final_layer, hs, mean, w_self, w_neigh, bias, h};
   return launch_linear(meta, la, max_rows, st);
+}
+
+extern "C" int sg_sage_combine_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                                   const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                                   const float* w_self, const float* w_neigh, const float* bias,
+                                   int32_t final_layer, const float* sums, float* counts, const float* recv,
+                                   int32_t recv_stride, float* mean, float* hs, float* h, int64_t max_rows,
+                                   void* stream) {
+  SG_REQUIRE(split_ws && lay && sums && counts, "sage_combine_fwd: null argument");
+  SPLIT_PTRS
+  SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_combine_fwd: bad layer/device");
+  SG_REQUIRE(w % 4 == 0 && w <= 128 && (dout == 4 || dout == 8 || dout == 16 || dout == 32),
+             "sage_combine_fwd: needs w % 4 == 0, w <= 128, dout in {4, 8, 16, 32}");
+  SG_REQUIRE(y.g == 1 || (recv && recv_stride % 4 == 0 && recv_stride >= w + 1),
+             "sage_combine_fwd: recv stride must be a multiple of 4 and >= w + 1");
+  if (max_rows <= 0) return SG_OK;
+  FusedArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = d; a.w = w; a.dout = dout; a.final_ = final_layer;
+  a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.voff_l = y.voff[l];
+  a.selfrow = I32(y.o_selfrow); a.src_row = src_row; a.h_prev = h_prev;
+  a.mean = mean; a.counts = counts; a.hs = hs;
+  a.ws = w_self; a.wn = w_neigh; a.bias = bias; a.h = h;
+  a.sums = sums; a.recv = recv; a.contrib = I32(y.o_contrib); a.stride = recv_stride; a.g = y.g > 1 ? y.g : 0;
+  return launch_layer<8, 2, 4>(meta, a, max_rows, (cudaStream_t)stream);
 }
 
 extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l,

@@ -133,10 +133,11 @@ class SplitStep:
         width = int(np.prod(shape)) if shape else 1
         return shared(P, width).view(P, *shape)
 
-    def _final_fused_ok(self, w, dout, dperm):
-        """Single-device split: the last layer, the loss and the last layer's
-        row-local backward run as one kernel (sg_sage_final_fused)."""
-        return (self.g == 1 and dperm is None and w % 4 == 0 and w <= 128 and dout <= 64
+    def _final_fused_ok(self, w, dout, dperm, any_g=False):
+        """The last layer, the loss and the last layer's row-local backward run
+        as one kernel (sg_sage_final_fused at g = 1; sg_sage_final_combine after
+        the push-to-owner round otherwise)."""
+        return ((self.g == 1 and dperm is None or any_g) and w % 4 == 0 and w <= 128 and dout <= 64
                 and self.p.num_classes <= 1024 and not getattr(self, "no_fuse", False)
                 and not getattr(self, "no_fuse_final", False))
 
@@ -148,35 +149,52 @@ class SplitStep:
             self.jobs = []
             self._partials = []
 
-    def _final_fused(self, l, w, dout, h_prev, src_row):
+    def _final_fused(self, l, w, dout, h_prev, src_row, comb=None):
+        """Last layer + loss + the layer's row-local backward, one kernel per
+        device: aggregating itself (g = 1) or combining the local partial with
+        the holders' partials after the push-to-owner round (comb = (sums,
+        counts, recv, stride))."""
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
         self._begin_grads()
         C = p.num_classes
         nV = ds.nV[l]
-        n = self.n_own(l, 0)
-        nb = max(1, min(_nblocks(n, tile=8), 2 * 148))
         mean = _f32(nV, w, device=self.dev)
-        counts = _f32(nV, device=self.dev)
+        counts = comb[1] if comb is not None else _f32(nV, device=self.dev)
         h = _f32(nV, dout, device=self.dev)
         need_prev = l > 1
         d_self = _f32(nV, w, device=self.dev) if need_prev else None
         d_sums = _f32(nV, w, device=self.dev) if need_prev else None
         ncls, nlay = dout * C + C + 1, 2 * w * dout + dout
-        part_c = _f32(nb * ncls, device=self.dev)
-        part_l = _f32(nb * nlay, device=self.dev)
+        W = [_lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
+             _lib.ptr(p.view(f"layer{l-1}.bias")), _lib.ptr(p.view("cls.w")), _lib.ptr(p.view("cls.b"))]
         self._ev(f"ph:final{l}:s")
-        _lib.call("sg_sage_final_fused", _lib.ptr(ds.ws), ds.lay, 0, _lib.ptr(h_prev), _lib.ptr(src_row),
-                  w, dout, C, _lib.ptr(p.view(f"layer{l-1}.w_self")), _lib.ptr(p.view(f"layer{l-1}.w_neigh")),
-                  _lib.ptr(p.view(f"layer{l-1}.bias")), _lib.ptr(p.view("cls.w")), _lib.ptr(p.view("cls.b")),
-                  _lib.ptr(ds.V), _lib.ptr(self.labels), _lib.ptr(mean), _lib.ptr(counts), _lib.ptr(h),
-                  _lib.ptr(d_self), _lib.ptr(d_sums), _lib.ptr(part_c), _lib.ptr(part_l), nb, n, st)
+        for d in self.devices:
+            n = self.n_own(l, d)
+            nb = max(1, min(_nblocks(n, tile=8), 2 * 148))
+            part_c = _f32(nb * ncls, device=self.dev)
+            part_l = _f32(nb * nlay, device=self.dev)
+            if comb is None:
+                _lib.call("sg_sage_final_fused", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(h_prev), _lib.ptr(src_row),
+                          w, dout, C, *W, _lib.ptr(ds.V), _lib.ptr(self.labels), _lib.ptr(mean),
+                          _lib.ptr(counts), _lib.ptr(h), _lib.ptr(d_self), _lib.ptr(d_sums), _lib.ptr(part_c),
+                          _lib.ptr(part_l), nb, n, st)
+            else:
+                sums, _, recv, SW = comb
+                _lib.call("sg_sage_final_combine", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(h_prev),
+                          _lib.ptr(src_row), w, dout, C, *W, _lib.ptr(ds.V), _lib.ptr(self.labels),
+                          _lib.ptr(sums), _lib.ptr(recv), SW, _lib.ptr(mean), _lib.ptr(counts), _lib.ptr(h),
+                          _lib.ptr(d_self), _lib.ptr(d_sums), _lib.ptr(part_c), _lib.ptr(part_l), nb, n, st)
+            self.jobs.append((part_c, nb, ncls, self.grads[d], p.offset("cls.w")))
+            self.jobs.append((part_l, nb, nlay, self.grads[d], p.offset(f"layer{l-1}.w_self")))
+            self._partials += [part_c, part_l]
         self._ev(f"ph:final{l}:e")
-        self.jobs.append((part_c, nb, ncls, self.grads[0], p.offset("cls.w")))
-        self.jobs.append((part_l, nb, nlay, self.grads[0], p.offset(f"layer{l-1}.w_self")))
-        self._partials += [part_c, part_l]
         self.h[l] = h
         self.keep[l] = dict(mean=mean, counts=counts)
         self._final_rows = (d_self, d_sums)
+
+    def _combine_ok(self, w, dout, SW):
+        return (w % 4 == 0 and w <= 128 and dout in (4, 8, 16, 32) and SW % 4 == 0
+                and not getattr(self, "no_fuse", False))
 
     def _dst_perm(self):
         """CSR-by-destination for samples whose edges are not grouped by dst."""
@@ -284,6 +302,24 @@ class SplitStep:
                 self.transport.to_owner(ds, l, send, recv, SW)
                 if self.meta is not None:
                     self.wire_bytes += int(self.meta.npairs[l]) * SW * 4
+            if self._combine_ok(w, dout, SW):
+                if l == self.L and self._final_fused_ok(w, dout, None, any_g=True):
+                    self._final_fused(l, w, dout, h_prev, src_row, comb=(sums, counts, recv, SW))
+                    continue
+                mean = _f32(nV, w, device=self.dev)
+                h = _f32(nV, dout, device=self.dev)
+                hs = _f32(nV, w, device=self.dev)
+                self._ev(f"ph:update{l}:s")
+                for d in self.devices:
+                    _lib.call("sg_sage_combine_fwd", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
+                              _lib.ptr(src_row), w, dout, _lib.ptr(p.view(f"layer{l-1}.w_self")),
+                              _lib.ptr(p.view(f"layer{l-1}.w_neigh")), _lib.ptr(p.view(f"layer{l-1}.bias")),
+                              final, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(recv), SW, _lib.ptr(mean),
+                              _lib.ptr(hs), _lib.ptr(h), self.n_own(l, d), st)
+                self._ev(f"ph:update{l}:e")
+                self.h[l] = h
+                self.keep[l] = dict(mean=mean, counts=counts, hs=hs)
+                continue
             mean = _f32(nV, w, device=self.dev)
             h = _f32(nV, dout, device=self.dev)
             tiled = w % 4 == 0 and dout in (4, 8, 16, 32)
