@@ -258,6 +258,21 @@ int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, 
                      const float* w_self, const float* w_neigh,
                      float* partial, int32_t nblocks, float* d_self, float* d_sums,
                      int32_t self_compact, int64_t max_rows, void* stream);
+/* Transposed SpMM of layer l (engine.py:263-273) fused with the row-local
+ * backward of layer l-1 (engine.py:237-244): the d_h rows of layer l-1 are
+ * formed in shared memory tile by tile (scatter args as sg_sage_scatter_bwd)
+ * while the tile's [hs | mean] rows of layer l-1 stream in, then masked by
+ * ReLU'(h) and turned into weight-gradient partials (sg_sage_bwd_rows layout,
+ * nblocks rows) and, if given, d_self_prev / d_sums_prev of layer l-1.
+ * d_h width w in {4, 8, 16, 32}; w_in = layer l-1's input width (% 4 == 0). */
+int sg_sage_scatter_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                             const float* d_self, const float* d_sums, const float* bwd_recv,
+                             int32_t recv_stride, const int32_t* enc, const int32_t* srcbeg,
+                             const int32_t* srcend, int64_t key_base, const float* hs, int32_t w_in,
+                             int32_t w, const float* h, const float* mean, const float* counts,
+                             const float* w_self, const float* w_neigh, float* partial,
+                             int32_t nblocks, float* d_self_prev, float* d_sums_prev,
+                             int64_t max_rows, void* stream);
 /* Transpose SpMM (engine.py:263-273): for each owned row u at l-1,
  * d_prev[u] = [u is the self row of v] d_self[v] + sum over out-edges of
  * d_sums_all[dst], where reference destinations read the owners' returned

@@ -869,6 +869,18 @@ struct BwdArgs {
   float* partial;
   float* d_self;
   float* d_sums;
+  // scatter mode (k_sage_wgrad): d_h of this layer's rows is not read but
+  // computed in the tile as the transposed SpMM of layer l+1 (engine.py:263-273)
+  const int32_t* sc_enc;
+  const int32_t* sc_beg;
+  const int32_t* sc_end;
+  const int32_t* sc_grouped;
+  const int32_t* sc_rank;
+  const float* sc_dself;   // layer l+1 d_self (owned rows of l+1)
+  const float* sc_dsums;   // layer l+1 d_sums
+  const float* sc_recv;    // push-from-owner rows (pair slots), g > 1
+  int64_t sc_key_base, sc_voff_src, sc_voff_dst;
+  int sc_stride;
 };
 
 template <bool Q4>
@@ -1090,6 +1102,7 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
   const int own0 = meta->own_off[a.l][a.d];
   const int ncg = K / 4, nslots = ncg * NQ, dq = dout / 4;
   const int ntiles = (n + TR - 1) / TR;
+  const bool scat = a.sc_enc != nullptr;
   auto issue = [&](int tile, int s) {
     float* A_s = stg + s * stage_f;
     float* dh_s = A_s + TR * KP;
@@ -1111,9 +1124,9 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
       const int r = idx / dq, q = idx - r * dq;
       if (r0 + r < n) {
         const int64_t G = own0 + r0 + r;
-        cp_async16(dh_s + r * dout + 4 * q, a.d_h + G * dout + 4 * q);
+        if (!scat) cp_async16(dh_s + r * dout + 4 * q, a.d_h + G * dout + 4 * q);
         if (!a.final_) cp_async16(hh_s + r * dout + 4 * q, a.h + G * dout + 4 * q);
-      } else {
+      } else if (!scat) {
         *reinterpret_cast<float4*>(dh_s + r * dout + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
@@ -1133,6 +1146,48 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
     const int r0 = tile * TR;
     if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, s ^ 1);
     asm volatile("cp.async.commit_group;" ::: "memory");
+    if (scat) {
+      // d_h rows of the tile = transposed SpMM of layer l+1 while the [hs | mean]
+      // tile lands: 4 rows per warp at once, each row's out-edges split over
+      // GPR lane groups of LPR lanes (one float4 of the row per lane), fixed
+      // xor tree over the groups (deterministic), + d_self on self rows.
+      float* dh_w = stg + s * stage_f + TR * KP;
+      const int LPR = dq, GPR = 8 / dq;  // dout in {4, 8, 16, 32}
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+      const int slot = lane / LPR, lr = lane - slot * LPR;
+      const int rl = warp * 4 + slot / GPR, grp = slot % GPR;
+      const int q = r0 + rl;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      int64_t U = 0;
+      if (q < n) {
+        U = own0 + q;
+        const int b = a.sc_beg[a.sc_key_base + U], e = a.sc_end[a.sc_key_base + U];
+        for (int j = b + grp; j < e; j += GPR) {
+          const int code = a.sc_enc[j];
+          const float* row = code >= 0 ? a.sc_dsums + (int64_t)code * dout
+                                       : a.sc_recv + (int64_t)(-code - 1) * a.sc_stride;
+          const float4 v = *reinterpret_cast<const float4*>(row + 4 * lr);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+      }
+      for (int o = LPR; o < LPR * GPR; o <<= 1) {  // the group bits of the lane
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, o);
+      }
+      if (grp == 0) {
+        if (q < n) {
+          const int p = a.sc_grouped[a.sc_voff_src + U];
+          if (p < meta->nV[a.l + 1]) {
+            const int64_t v = meta->own_off[a.l + 1][a.d] + a.sc_rank[a.sc_voff_dst + p];
+            const float4 sv = *reinterpret_cast<const float4*>(a.sc_dself + v * dout + 4 * lr);
+            acc.x = sv.x + acc.x; acc.y = sv.y + acc.y; acc.z = sv.z + acc.z; acc.w = sv.w + acc.w;
+          }
+        }
+        *reinterpret_cast<float4*>(dh_w + rl * dout + 4 * lr) = acc;  // rows past n: zeros
+      }
+    }
     asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncthreads();
     const float* A_s = stg + s * stage_f;
@@ -1636,6 +1691,49 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
     ::sg::launch(k_sage_bwd_rows<false>, nblocks, 256, smem, st, meta, a);
   }
   SG_CHECK_LAUNCH("k_sage_bwd_rows");
+  return SG_OK;
+}
+
+// Transposed SpMM of layer l (d_prev rows of layer l-1, engine.py:263-273) fused
+// with the row-local backward of layer l-1 (engine.py:237-244): k_sage_wgrad in
+// scatter mode. hs / mean / counts / h are layer l-1's (self-compact forward).
+extern "C" int sg_sage_scatter_bwd_rows(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                                        const float* d_self, const float* d_sums, const float* bwd_recv,
+                                        int32_t recv_stride, const int32_t* enc, const int32_t* srcbeg,
+                                        const int32_t* srcend, int64_t key_base, const float* hs, int32_t w_in,
+                                        int32_t w, const float* h, const float* mean, const float* counts,
+                                        const float* w_self, const float* w_neigh, float* partial,
+                                        int32_t nblocks, float* d_self_prev, float* d_sums_prev,
+                                        int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay && enc && srcbeg && srcend && hs && h && mean, "sage_scatter_bwd_rows: null argument");
+  SPLIT_PTRS
+  SG_REQUIRE(l >= 2 && l <= y.L && d >= 0 && d < y.g, "sage_scatter_bwd_rows: bad layer/device");
+  SG_REQUIRE(nblocks >= 1, "sage_scatter_bwd_rows: nblocks >= 1");
+  SG_REQUIRE((w == 4 || w == 8 || w == 16 || w == 32) && w_in % 4 == 0 && 2 * w_in * (w / 4) <= 4 * 512,
+             "sage_scatter_bwd_rows: needs d_h width in {4, 8, 16, 32} and a tiled input width");
+  SG_REQUIRE(y.g == 1 || (bwd_recv && recv_stride % 4 == 0), "sage_scatter_bwd_rows: recv stride % 4 != 0");
+  (void)max_rows;
+  BwdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l - 1; a.d = d; a.w = w_in; a.dout = w; a.final_ = 0; a.self_compact = 1;
+  a.voff_l = y.voff[l - 1]; a.h_prev = hs; a.selfrow = I32(y.o_selfrow);
+  a.h = h; a.mean = mean; a.counts = counts; a.ws = w_self; a.wn = w_neigh;
+  a.partial = partial; a.d_self = d_self_prev; a.d_sums = d_sums_prev;
+  a.sc_enc = enc; a.sc_beg = srcbeg; a.sc_end = srcend; a.sc_grouped = I32(y.o_grouped);
+  a.sc_rank = I32(y.o_rank); a.sc_dself = d_self; a.sc_dsums = d_sums; a.sc_recv = bwd_recv;
+  a.sc_key_base = key_base; a.sc_voff_src = y.voff[l - 1]; a.sc_voff_dst = y.voff[l]; a.sc_stride = recv_stride;
+  const size_t sm2 = sizeof(float) * (2 * (32 * (size_t)(2 * w_in + 4) + 2 * 32 * (size_t)w + 32) +
+                                      2 * (size_t)w_in * (w + 4));
+  SG_REQUIRE(sm2 <= 227 * 1024, "sage_scatter_bwd_rows: width too large for shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t attr = cudaSuccess;
+  switch (w / 4) {
+    case 1: attr = allow_max_smem<k_sage_wgrad<1>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<1>, nblocks, 256, sm2, st, meta, a); break;
+    case 2: attr = allow_max_smem<k_sage_wgrad<2>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<2>, nblocks, 256, sm2, st, meta, a); break;
+    case 4: attr = allow_max_smem<k_sage_wgrad<4>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<4>, nblocks, 256, sm2, st, meta, a); break;
+    default: attr = allow_max_smem<k_sage_wgrad<8>>(); SG_CUDA(attr); ::sg::launch(k_sage_wgrad<8>, nblocks, 256, sm2, st, meta, a); break;
+  }
+  SG_CHECK_LAUNCH("k_sage_wgrad(scatter)");
   return SG_OK;
 }
 

@@ -419,6 +419,7 @@ class SplitStep:
         with self.phase("src_csr_join"):
             csr, kb = self._join_src_csr(2)
         d_h = None if fused_final else self.d_h
+        rows_done = None  # (d_self, d_sums) of a layer whose row backward ran inside the scatter
         for l in range(self.L, 0, -1):
             w, dout = p.layer_dims(l - 1)
             final = int(l == self.L)
@@ -427,6 +428,10 @@ class SplitStep:
             nV = ds.nV[l]
             if l == self.L and fused_final:
                 d_self, d_sums = self._final_rows
+                devs = []
+            elif rows_done is not None:
+                d_self, d_sums = rows_done
+                rows_done = None
                 devs = []
             else:
                 d_self = _f32(nV, w, device=self.dev) if need_prev else None
@@ -462,6 +467,34 @@ class SplitStep:
                 self.transport.from_owner(ds, l, bsend, brecv, SWb)
                 if self.meta is not None:
                     self.wire_bytes += int(self.meta.npairs[l]) * SWb * 4
+            w_in, _ = p.layer_dims(l - 2)
+            hs_prev = self.keep[l - 1].get("hs")
+            # (measured: a win for narrow rows; for the wide layer-1 rows the tile's
+            # scatter latency and hub rows stall the weight-gradient pipeline)
+            if (w in (4, 8, 16, 32) and w_in % 4 == 0 and w_in <= 64 and hs_prev is not None
+                    and ds.nE[l - 1] < TSPMM_MIN_EDGES and not getattr(self, "no_fuse", False)):
+                # transposed SpMM of layer l fused with layer l-1's row backward
+                need2 = l - 1 > 1
+                d_self2 = _f32(ds.nV[l - 1], w_in, device=self.dev) if need2 else None
+                d_sums2 = _f32(ds.nV[l - 1], w_in, device=self.dev) if need2 else None
+                npart2 = 2 * w_in * w + w
+                self._ev(f"ph:scatter_rows{l}:s")
+                for d in self.devices:
+                    perm, beg, end, _, keys = csr[d][:5]
+                    nb = _nblocks(self.n_own(l - 1, d))
+                    part = _f32(nb * npart2, device=self.dev)
+                    _lib.call("sg_sage_scatter_bwd_rows", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(d_self),
+                              _lib.ptr(d_sums), _lib.ptr(brecv), SWb, _lib.ptr(perm), _lib.ptr(beg), _lib.ptr(end),
+                              kb[l], _lib.ptr(hs_prev), w_in, w, _lib.ptr(self.h[l - 1]),
+                              _lib.ptr(self.keep[l - 1]["mean"]), _lib.ptr(self.keep[l - 1]["counts"]),
+                              _lib.ptr(p.view(f"layer{l-2}.w_self")), _lib.ptr(p.view(f"layer{l-2}.w_neigh")),
+                              _lib.ptr(part), nb, _lib.ptr(d_self2), _lib.ptr(d_sums2), self.n_own(l - 1, d), st)
+                    self.jobs.append((part, nb, npart2, self.grads[d], p.offset(f"layer{l-2}.w_self")))
+                    self._partials.append(part)
+                self._ev(f"ph:scatter_rows{l}:e")
+                rows_done = (d_self2, d_sums2)
+                d_h = None
+                continue
             d_prev = _f32(ds.nV[l - 1], w, device=self.dev)
             self._ev(f"ph:scatter{l}:s")
             for d in self.devices:
