@@ -354,7 +354,8 @@ def main():
     pm = sg.range_partition(N_NODES, g)
     part_rows = pm.device_vertices(rank)
     feats = sg.FeatureStore.synthetic(N_NODES, FEAT, FEAT_SEED,
-                                      row_ids=None if g == 1 else part_rows, device=dev)
+                                      row_ids=None if g == 1 else part_rows, device=dev,
+                                      pad_rows=KIND == "graphsage")  # whole 128 B lines per row
     cache = sg.full_cache(pm)
     labels_dev = torch.from_numpy(labels).to(dev)
     n_steps = args.warmup + args.steps

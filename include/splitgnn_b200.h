@@ -171,6 +171,10 @@ int sg_gather_rows(const float* table, const int32_t* rows, int64_t n_rows, int3
 int sg_fill_uniform(float* out, int64_t rows, int32_t width, uint64_t seed,
                     int64_t row0, void* stream);
 
+/* h_stride (sg_sage_agg_fwd, _perm, sg_sage_fused_fwd, sg_sage_combine_fwd):
+ * row stride of h_prev in floats, 0 = w. A layer-1 feature table whose rows
+ * are padded to whole 128-byte lines (FeatureStore row_stride) is read in
+ * whole lines: measured ~1.4x faster row gathers than 400-byte rows. */
 /* ---------------------------------------------------------------- GraphSAGE
  * Forward local aggregation (engine.py:180-195, segment_sum/count
  * models.py:150-175): per local destination row, the sum of h_prev rows over
@@ -180,13 +184,14 @@ int sg_fill_uniform(float* out, int64_t rows, int32_t width, uint64_t seed,
  * rows are addressed through `src_row` when non-null (layer 0: feature cache
  * indirection), else by global owned row. */
 int sg_sage_agg_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                    const float* h_prev, const int32_t* src_row, int32_t w,
+                    const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride,
                     float* sums, float* counts, float* sendbuf, int32_t send_stride,
                     int64_t max_rows, void* stream);
 /* As sg_sage_agg_fwd for samples whose edges are not grouped by destination:
  * rowbeg/rowend index `dperm` (from sg_dst_csr). */
 int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                         const float* h_prev, const int32_t* src_row, int32_t w, float* sums,
+                         const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride,
+                         float* sums,
                          float* counts, float* sendbuf, int32_t send_stride,
                          const int32_t* dperm, int64_t max_rows, void* stream);
 /* Single-device split (g = 1: no reference rows, no remote contributions):
@@ -194,7 +199,8 @@ int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t
  * (engine.py:180-226 with the exchange vacuous). Also writes mean, counts and
  * the compact self rows hs (n_own x w) the backward pass reads. */
 int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                      const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                      const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride,
+                      int32_t dout,
                       const float* w_self, const float* w_neigh, const float* bias,
                       int32_t final_layer, float* mean, float* counts, float* hs, float* h,
                       int64_t max_rows, void* stream);
@@ -218,7 +224,8 @@ int sg_sage_final_fused(const void* split_ws, const SgSplitLayout* lay, int32_t 
  * bias, ReLU unless final (:212-226). counts is updated to the combined N;
  * mean, hs (self rows, n_own x w) and h are written. recv_stride % 4 == 0. */
 int sg_sage_combine_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                        const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                        const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride,
+                        int32_t dout,
                         const float* w_self, const float* w_neigh, const float* bias,
                         int32_t final_layer, const float* sums, float* counts, const float* recv,
                         int32_t recv_stride, float* mean, float* hs, float* h, int64_t max_rows,

@@ -79,17 +79,17 @@ _SIGS = {
     "sg_layer0_rows": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, vp, vp]),
     "sg_gather_rows": (i32, [vp, vp, i64, i32, vp, vp]),
     "sg_fill_uniform": (i32, [vp, i64, i32, u64, i64, vp]),
-    "sg_sage_agg_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, vp, vp, vp, i32, i64, vp]),
-    "sg_sage_agg_fwd_perm": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, vp, vp, vp, i32,
+    "sg_sage_agg_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32, i64, vp]),
+    "sg_sage_agg_fwd_perm": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32,
                                    vp, i64, vp]),
-    "sg_sage_fused_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32, vp, vp,
+    "sg_sage_fused_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, i32, vp, vp,
                                 vp, vp, i64, vp]),
     "sg_sage_final_fused": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
     "sg_set_pdl": (None, [i32]),
     "sg_sage_scatter_bwd_rows": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, vp, i32, vp, vp, vp, i64, vp, i32,
                                        i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, i64, vp]),
-    "sg_sage_combine_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32, vp, vp, vp,
+    "sg_sage_combine_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp,
                                   i32, vp, vp, vp, i64, vp]),
     "sg_sage_final_combine": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp,
                                     vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, i32, i64, vp]),

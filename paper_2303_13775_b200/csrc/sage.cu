@@ -74,6 +74,7 @@ struct VecT<1> {
 // ---------------------------------------------------------------- forward SpMM
 struct AggArgs {
   int l, d, w, stride;
+  int hst;  // row stride of h_prev (>= w; a padded feature table reads whole 128 B lines)
   int64_t eoff_li, rbase_li, pbase_l;
   const int32_t* rowbeg;
   const int32_t* rowend;
@@ -138,10 +139,10 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
           const int col = (c * LPR + lr) * VEC;
-          if (col < w) {
+          if (col < a.hst) {  // whole (padded) rows: full 128 B lines
             T v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = ok[u] ? V::ld(a.h_prev + (int64_t)rr[u] * w + col) : V::zero();
+            for (int u = 0; u < 4; ++u) v[u] = ok[u] ? V::ld(a.h_prev + (int64_t)rr[u] * a.hst + col) : V::zero();
 #pragma unroll
             for (int u = 0; u < 4; ++u) V::add(acc[c], v[u]);
           }
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
 #pragma unroll
           for (int c = 0; c < NCH; ++c) {
             const int col = (c * LPR + lr) * VEC;
-            if (col < w) V::add(acc[c], V::ld(a.h_prev + (int64_t)r0 * w + col));
+            if (col < a.hst) V::add(acc[c], V::ld(a.h_prev + (int64_t)r0 * a.hst + col));
           }
         }
       }
@@ -236,6 +237,7 @@ struct FusedArgs {
   const float* recv;
   const int32_t* contrib;
   int stride, g;
+  int hst;  // row stride of h_prev (k_sage_layer: a padded feature table is read in whole lines)
 };
 
 template <int LPR, int EG>
@@ -486,14 +488,14 @@ template <int NQ, int UN, int RPW, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restrict__ meta, FusedArgs a) {
   SG_PDL_ENTRY();
   constexpr int TM = 8 * RPW;  // rows per tile (RPW per warp)
-  constexpr int TMP = TM + 4;
   constexpr int NT = (TM / 4) * NQ;
   constexpr int NS = 256 / NT;
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, K = 2 * w;
   const int l = a.l, d = a.d;
   float* W_s = smem;            // [2w][dout]
-  float* A_s = W_s + K * dout;  // [2w][TMP] transposed; reused as the slice reduction
+  const int KP = K + 4;         // row-major A tile: float4 row stores are conflict-free
+  float* A_s = W_s + K * dout;  // [TM][2w+4] (hs | mean); reused as the slice reduction
   for (int i = threadIdx.x; i < w * dout / 4; i += 256) {
     reinterpret_cast<float4*>(W_s)[i] = reinterpret_cast<const float4*>(a.ws)[i];
     reinterpret_cast<float4*>(W_s)[w * dout / 4 + i] = reinterpret_cast<const float4*>(a.wn)[i];
@@ -505,9 +507,11 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int col = lane * 4;
   const bool colok = col < w;
+  const int hst = a.hst;
+  const bool ldok = col < hst;  // padded rows: every lane loads (whole 128 B lines), stores stay < w
   const int tile = threadIdx.x % NT, ks = threadIdx.x / NT;
   const int rt = tile / NQ, jq = tile - rt * NQ;
-  const int kchunk = (K + NS - 1) / NS;
+  const int kchunk = ((K + NS - 1) / NS + 3) & ~3;  // whole float4 steps of K
   const int kb = ks * kchunk, ke = min(K, kb + kchunk);
   auto edge_row = [&](int j) {
     int r = prev0 + a.lsrc[a.eoff_li + j];
@@ -538,7 +542,7 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
         float N = a.counts[G];
         if (colok) {
           acc = *reinterpret_cast<const float4*>(a.sums + G * w + col);
-          hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col));
+          hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * hst + col));
         }
         const int32_t* cb = a.contrib + (int64_t)a.g * a.voff_l + G * a.g;
         for (int s = 0; s < a.g; ++s) {
@@ -567,10 +571,10 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
         for (int u = 0; u < UN; ++u) {
           const int k = kk + u;
           const int rr = __shfl_sync(0xffffffffu, rcur, k < 32 ? k : 31);
-          v[u] = (k < cnt0 && colok) ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * w + col))
+          v[u] = (k < cnt0 && ldok) ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * hst + col))
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        if (kk == 0 && colok) hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col));
+        if (kk == 0 && colok) hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * hst + col));
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
           acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
@@ -582,13 +586,13 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
         const int cnt = min(32, ec - jb);
         for (int k = 0; k < cnt; ++k) {
           const int rr = __shfl_sync(0xffffffffu, rr0, k);
-          if (colok) {
-            const float4 t = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * w + col));
+          if (ldok) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * hst + col));
             acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
           }
         }
       }
-      if (ec == bc && colok) hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col));
+      if (ec == bc && colok) hv = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * hst + col));
       // second index hop of the next row, overlapping this row's tail
       if (i + 1 < RPW && q + 1 < n) {
         rnext = (lane < ne - nb) ? (a.src_row ? a.src_row[lnext] : lnext) : 0;
@@ -603,14 +607,8 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
       if (colok) {
         *reinterpret_cast<float4*>(a.mean + G * w + col) = mn;
         if (a.hs) *reinterpret_cast<float4*>(a.hs + G * w + col) = hv;
-        A_s[(col + 0) * TMP + rr] = hv.x;
-        A_s[(col + 1) * TMP + rr] = hv.y;
-        A_s[(col + 2) * TMP + rr] = hv.z;
-        A_s[(col + 3) * TMP + rr] = hv.w;
-        A_s[(w + col + 0) * TMP + rr] = mn.x;
-        A_s[(w + col + 1) * TMP + rr] = mn.y;
-        A_s[(w + col + 2) * TMP + rr] = mn.z;
-        A_s[(w + col + 3) * TMP + rr] = mn.w;
+        *reinterpret_cast<float4*>(A_s + rr * KP + col) = hv;
+        *reinterpret_cast<float4*>(A_s + rr * KP + w + col) = mn;
       }
       if (lane == 0) a.counts[G] = cntf;
     }
@@ -619,17 +617,24 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
     float acc2[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc2[i][0] = acc2[i][1] = acc2[i][2] = acc2[i][3] = 0.f;
-#pragma unroll 4
-    for (int k = kb; k < ke; ++k) {
-      const float4 av = *reinterpret_cast<const float4*>(A_s + k * TMP + 4 * rt);
-      const float4 wv = *reinterpret_cast<const float4*>(W_s + k * dout + 4 * jq);
-      const float ar[4] = {av.x, av.y, av.z, av.w};
+    // 4x4 (rows x K) block of A and 4x4 (K x outputs) block of W per step:
+    // 8 LDS.128 per 64 FFMA
+    for (int k = kb; k < ke; k += 4) {
+      float4 av[4], wv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const float4*>(A_s + (4 * rt + i) * KP + k);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) wv[kk] = *reinterpret_cast<const float4*>(W_s + (k + kk) * dout + 4 * jq);
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        acc2[i][0] = fmaf(ar[i], wv.x, acc2[i][0]);
-        acc2[i][1] = fmaf(ar[i], wv.y, acc2[i][1]);
-        acc2[i][2] = fmaf(ar[i], wv.z, acc2[i][2]);
-        acc2[i][3] = fmaf(ar[i], wv.w, acc2[i][3]);
+        const float ar[4] = {av[i].x, av[i].y, av[i].z, av[i].w};
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          acc2[i][0] = fmaf(ar[kk], wv[kk].x, acc2[i][0]);
+          acc2[i][1] = fmaf(ar[kk], wv[kk].y, acc2[i][1]);
+          acc2[i][2] = fmaf(ar[kk], wv[kk].z, acc2[i][2]);
+          acc2[i][3] = fmaf(ar[kk], wv[kk].w, acc2[i][3]);
+        }
       }
     }
     __syncthreads();
@@ -654,7 +659,7 @@ template <int NQ, int UN, int RPW, int MINB>
 int launch_layer_q(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
   constexpr int TM = 8 * RPW;
   constexpr int NS = 256 / ((TM / 4) * NQ);
-  const size_t a_floats = std::max<size_t>(2 * (size_t)a.w * (TM + 4), (size_t)NS * TM * a.dout);
+  const size_t a_floats = std::max<size_t>((size_t)TM * (2 * (size_t)a.w + 4), (size_t)NS * TM * a.dout);
   const size_t smem = sizeof(float) * (2 * (size_t)a.w * a.dout + a_floats);
   if (smem > 227 * 1024) {
     set_error("sage_layer: width too large");
@@ -1383,7 +1388,7 @@ int dispatch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaS
   auto I32 = [&](int64_t o) { return (const int32_t*)(base + o); };
 
 static int agg_common(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                      const float* h_prev, const int32_t* src_row, int32_t w, float* sums,
+                      const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride, float* sums,
                       float* counts, float* sendbuf, int32_t send_stride, const int32_t* dperm,
                       int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "sage_agg_fwd: null workspace");
@@ -1407,6 +1412,7 @@ static int agg_common(const void* split_ws, const SgSplitLayout* lay, int32_t l,
   a.sendpos = I32(y.o_sendpos);
   a.src_row = src_row;
   a.h_prev = h_prev;
+  a.hst = h_stride > 0 ? h_stride : w;
   a.sums = sums;
   a.counts = counts;
   a.sendbuf = sendbuf;
@@ -1415,24 +1421,24 @@ static int agg_common(const void* split_ws, const SgSplitLayout* lay, int32_t l,
 
 extern "C" int sg_sage_agg_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
                                int32_t d, const float* h_prev, const int32_t* src_row, int32_t w,
-                               float* sums, float* counts, float* sendbuf, int32_t send_stride,
-                               int64_t max_rows, void* stream) {
-  return agg_common(split_ws, lay, l, d, h_prev, src_row, w, sums, counts, sendbuf, send_stride,
+                               int32_t h_stride, float* sums, float* counts, float* sendbuf,
+                               int32_t send_stride, int64_t max_rows, void* stream) {
+  return agg_common(split_ws, lay, l, d, h_prev, src_row, w, h_stride, sums, counts, sendbuf, send_stride,
                     nullptr, max_rows, stream);
 }
 
 extern "C" int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t l,
                                     int32_t d, const float* h_prev, const int32_t* src_row,
-                                    int32_t w, float* sums, float* counts, float* sendbuf,
-                                    int32_t send_stride, const int32_t* dperm, int64_t max_rows,
-                                    void* stream) {
-  return agg_common(split_ws, lay, l, d, h_prev, src_row, w, sums, counts, sendbuf, send_stride,
+                                    int32_t w, int32_t h_stride, float* sums, float* counts,
+                                    float* sendbuf, int32_t send_stride, const int32_t* dperm,
+                                    int64_t max_rows, void* stream) {
+  return agg_common(split_ws, lay, l, d, h_prev, src_row, w, h_stride, sums, counts, sendbuf, send_stride,
                     dperm, max_rows, stream);
 }
 
 extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,
                                  int32_t d, const float* h_prev, const int32_t* src_row, int32_t w,
-                                 int32_t dout, const float* w_self, const float* w_neigh,
+                                 int32_t h_stride, int32_t dout, const float* w_self, const float* w_neigh,
                                  const float* bias, int32_t final_layer, float* mean, float* counts,
                                  float* hs, float* h, int64_t max_rows, void* stream) {
   SG_REQUIRE(split_ws && lay, "sage_fused_fwd: null workspace");
@@ -1450,9 +1456,13 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   a.selfrow = I32(y.o_selfrow); a.src_row = src_row; a.h_prev = h_prev;
   a.mean = mean; a.counts = counts; a.hs = hs;
   a.ws = w_self; a.wn = w_neigh; a.bias = bias; a.h = h;
+  a.hst = h_stride > 0 ? h_stride : w;
+  SG_REQUIRE(a.hst >= w && a.hst % 4 == 0 && a.hst <= 128 && (a.hst == w || w > 64),
+             "sage_fused_fwd: h_stride must be a multiple of 4, >= w, <= 128 (padded rows need w > 64)");
   cudaStream_t st = (cudaStream_t)stream;
-  // wide layers: one kernel (8 loads in flight per lane, 16-row tiles, 4 CTAs/SM)
-  if (w > 64) return launch_layer<8, 2, 4>(meta, a, max_rows, st);
+  // wide layers: one kernel (8 loads in flight per lane, 8-row tiles: one row
+  // per warp, 4 CTAs/SM; measured best of UN 8/16 x RPW 1/2/4 x 2..8 CTAs/SM)
+  if (w > 64) return launch_layer<8, 1, 4>(meta, a, max_rows, st);
   int rc;
   if (w <= 16) rc = launch_agg_mean<4, 4>(meta, a, max_rows, st);
   else if (w <= 32) rc = launch_agg_mean<8, 4>(meta, a, max_rows, st);
@@ -1464,7 +1474,8 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
 }
 
 extern "C" int sg_sage_combine_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
-                                   const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
+                                   const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride,
+                                   int32_t dout,
                                    const float* w_self, const float* w_neigh, const float* bias,
                                    int32_t final_layer, const float* sums, float* counts, const float* recv,
                                    int32_t recv_stride, float* mean, float* hs, float* h, int64_t max_rows,
@@ -1485,7 +1496,9 @@ extern "C" int sg_sage_combine_fwd(const void* split_ws, const SgSplitLayout* la
   a.mean = mean; a.counts = counts; a.hs = hs;
   a.ws = w_self; a.wn = w_neigh; a.bias = bias; a.h = h;
   a.sums = sums; a.recv = recv; a.contrib = I32(y.o_contrib); a.stride = recv_stride; a.g = y.g > 1 ? y.g : 0;
-  return launch_layer<8, 2, 4>(meta, a, max_rows, (cudaStream_t)stream);
+  a.hst = h_stride > 0 ? h_stride : w;
+  SG_REQUIRE(a.hst >= w && a.hst % 4 == 0 && a.hst <= 128, "sage_combine_fwd: bad h_stride");
+  return launch_layer<8, 1, 4>(meta, a, max_rows, (cudaStream_t)stream);
 }
 
 extern "C" int sg_sage_update(const void* split_ws, const SgSplitLayout* lay, int32_t l,

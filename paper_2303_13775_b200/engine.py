@@ -192,6 +192,14 @@ class SplitStep:
         self.keep[l] = dict(mean=mean, counts=counts)
         self._final_rows = (d_self, d_sums)
 
+    def _padded_ok(self, l, w, dout, dperm):
+        """Layer 1 reads a padded feature table only through the kernels that
+        take a row stride: the one-kernel layer (g = 1) or the g > 1
+        aggregation + combine; never as the last layer."""
+        if l != 1 or self.L < 2 or w <= 64:
+            return False
+        return self._fused_ok(w, dout, dperm) or self._combine_ok(w, dout, _r4(w + 1))
+
     def _combine_ok(self, w, dout, SW):
         return (w % 4 == 0 and w <= 128 and dout in (4, 8, 16, 32) and SW % 4 == 0
                 and not getattr(self, "no_fuse", False))
@@ -258,7 +266,11 @@ class SplitStep:
             w, dout = p.layer_dims(l - 1)
             final = int(l == self.L)
             h_prev, src_row = (self.f.table, self.src_row0) if l == 1 else (self.h[l - 1], None)
+            hst = self.f.row_stride if l == 1 else w
             nV = ds.nV[l]
+            if hst != w and not self._padded_ok(l, w, dout, dperm):
+                raise ValueError("padded feature rows are read only by the wide SAGE layer-1 kernels "
+                                 "(build the FeatureStore with pad_rows=False for this model)")
             if l == self.L and self._final_fused_ok(w, dout, dperm):
                 self._final_fused(l, w, dout, h_prev, src_row)
                 continue
@@ -270,7 +282,7 @@ class SplitStep:
                 self._ev(f"agg{l}_start")
                 self._ev(f"ph:agg+update{l}:s")
                 _lib.call("sg_sage_fused_fwd", _lib.ptr(ds.ws), ds.lay, l, 0, _lib.ptr(h_prev),
-                          _lib.ptr(src_row), w, dout, _lib.ptr(p.view(f"layer{l-1}.w_self")),
+                          _lib.ptr(src_row), w, hst, dout, _lib.ptr(p.view(f"layer{l-1}.w_self")),
                           _lib.ptr(p.view(f"layer{l-1}.w_neigh")), _lib.ptr(p.view(f"layer{l-1}.bias")),
                           final, _lib.ptr(mean), _lib.ptr(counts), _lib.ptr(hs), _lib.ptr(h),
                           self.n_own(l, 0), st)
@@ -290,11 +302,11 @@ class SplitStep:
             for d in self.devices:
                 if dperm is None:
                     _lib.call("sg_sage_agg_fwd", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
-                              _lib.ptr(src_row), w, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
+                              _lib.ptr(src_row), w, hst, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
                               SW, self.n_rows(l, d), st)
                 else:
                     _lib.call("sg_sage_agg_fwd_perm", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
-                              _lib.ptr(src_row), w, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
+                              _lib.ptr(src_row), w, hst, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
                               SW, _lib.ptr(dperm[d][0]), self.n_rows(l, d), st)
             self._ev(f"agg{l}_end")
             self._ev(f"ph:agg{l}:e")
@@ -312,7 +324,7 @@ class SplitStep:
                 self._ev(f"ph:update{l}:s")
                 for d in self.devices:
                     _lib.call("sg_sage_combine_fwd", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
-                              _lib.ptr(src_row), w, dout, _lib.ptr(p.view(f"layer{l-1}.w_self")),
+                              _lib.ptr(src_row), w, hst, dout, _lib.ptr(p.view(f"layer{l-1}.w_self")),
                               _lib.ptr(p.view(f"layer{l-1}.w_neigh")), _lib.ptr(p.view(f"layer{l-1}.bias")),
                               final, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(recv), SW, _lib.ptr(mean),
                               _lib.ptr(hs), _lib.ptr(h), self.n_own(l, d), st)
@@ -564,14 +576,14 @@ _FEATS = {}
 _LABELS = {}
 
 
-def _feature_store(features, cache, device):
+def _feature_store(features, cache, device, pad_rows=False):
     if isinstance(features, FeatureStore):
         return features
-    key = (id(features), id(cache))
+    key = (id(features), id(cache), bool(pad_rows))
     hit = _FEATS.get(key)
     if hit is not None and hit[0] is features:
         return hit[1]
-    fs = FeatureStore.from_host(np.asarray(features), cache, device=device)
+    fs = FeatureStore.from_host(np.asarray(features), cache, device=device, pad_rows=pad_rows)
     _FEATS.clear()
     _FEATS[key] = (features, fs)
     return fs
@@ -624,7 +636,11 @@ class SplitExecutor:
         self.g = ds.g
         self.L = params.num_layers
         self.dparams = DeviceParams.from_host(params, ds.device)
-        self.feats = _feature_store(features, ds.cache, ds.device)
+        F = int(np.asarray(features).shape[1]) if not isinstance(features, FeatureStore) else 0
+        hid = self.dparams.layer_dims(0)[1] if self.L >= 1 else 0
+        pad = (params.kind == "graphsage" and self.L >= 2 and 64 < F <= 128 and F % 4 == 0
+               and hid in (4, 8, 16, 32))  # wide layer 1 read in whole 128 B lines
+        self.feats = _feature_store(features, ds.cache, ds.device, pad_rows=pad)
         self.labels = _labels_dev(labels, ds.device)
         self.step = SplitStep(self.dparams, ds, self.feats, self.labels)
         self._states = None
@@ -680,7 +696,7 @@ def _materialise_states(ex):
         h0 = torch.empty((max(n0, 1), F), dtype=torch.float32, device=ds.device)
         _lib.call("sg_gather_rows", _lib.ptr(table), _lib.ptr(st.src_row0[b0:]), n0, F, _lib.ptr(h0),
                   _lib.stream_ptr())
-        sv.h.append(h0[:n0].double().cpu().numpy())
+        sv.h.append(h0[:n0, :ex.feats.feat_dim].double().cpu().numpy())
         sv.layer.append(None)
         for l in range(1, ds.L + 1):
             b, n = int(m.own_off[l][d]), int(m.n_own[l][d])

@@ -45,6 +45,8 @@ def _from_owner(step, l, rows, width):
 
 
 def gat_forward(step):
+    if getattr(step.f, "padded", False):
+        raise ValueError("the GAT kernels read unpadded feature rows (FeatureStore pad_rows=False)")
     ds, p = step.ds, step.p
     st = _lib.stream_ptr()
     slope = float(p.leaky_slope)
