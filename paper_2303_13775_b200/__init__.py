@@ -24,8 +24,8 @@ from paper_2303_13775_b200.partition import (
     max_part_size,
     range_partition,
 )
-from paper_2303_13775_b200.sampling import (MiniBatchSample, NativeSampler, epoch_batches, sample_microbatches,
-                                            sample_minibatch)
+from paper_2303_13775_b200.sampling import (GpuSampler, MiniBatchSample, NativeSampler, epoch_batches,
+                                            sample_microbatches, sample_minibatch)
 from paper_2303_13775_b200.scheduler import (
     DeviceSplit,
     LocalSplit,

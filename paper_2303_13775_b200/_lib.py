@@ -18,6 +18,7 @@ MAXL = 8
 MAXG = 16
 
 i32, i64, u64, f32, f64, vp = C.c_int32, C.c_int64, C.c_uint64, C.c_float, C.c_double, C.c_void_p
+u32 = C.c_uint32
 
 
 class SgMeta(C.Structure):
@@ -87,6 +88,9 @@ _SIGS = {
     "sg_sage_final_fused": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
     "sg_set_pdl": (None, [i32]),
+    "sg_gpu_sampler_ws_bytes": (i64, [i64, i64, i64, i32]),
+    "sg_gpu_sampler_ws_init": (i32, [vp, i64, vp]),
+    "sg_gpu_sample": (i32, [vp, vp, i64, vp, i64, vp, i32, u64, u32, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
     "sg_sage_scatter_bwd_rows": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, vp, i32, vp, vp, vp, i64, vp, i32,
                                        i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, i64, vp]),
     "sg_sage_combine_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, i32, vp, vp, vp,

@@ -195,3 +195,98 @@ def epoch_batches(train_set, batch_size, rng) -> list:
         raise ValueError("batch_size must be >= 1")
     perm = rng.permutation(np.asarray(train_set, dtype=np.int64))
     return [perm[i:i + batch_size] for i in range(0, len(perm), batch_size)]
+
+
+class GpuSampler:
+    """sample_minibatch (sampling.py:118-177) on the GPU (csrc/sampler.cu)
+    from a device-resident copy of the graph's in-CSR. Same semantics and the
+    same counter-based RNG as the native host sampler, so for the same seed
+    both produce the identical sample. `sample()` returns a host
+    MiniBatchSample; `sample_into()` writes a packed sample straight into a
+    StaticSample's device buffers (a captured step's inputs) with no host
+    round trip."""
+
+    def __init__(self, graph, device="cuda"):
+        import torch
+        self.graph = graph
+        self.n = int(graph.num_vertices)
+        self.dev = torch.device(device)
+        self.ro = torch.from_numpy(np.asarray(graph.row_offsets, dtype=np.int64)).to(self.dev)
+        self.ci = torch.from_numpy(np.asarray(graph.col_indices, dtype=np.int32)).to(self.dev)
+        self._ws = None
+        self._ws_key = None
+        self._gen = 0
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    @staticmethod
+    def bounds(n_targets, fanouts):
+        """Fanout-derived capacities: |V^L| = B, |E^l| <= |V^l|(1+f), |V^{l-1}| <= |E^l|."""
+        L = len(fanouts)
+        nV = [0] * (L + 1)
+        nE = [0] * L
+        nV[L] = int(n_targets)
+        for l in range(L, 0, -1):
+            nE[l - 1] = nV[l] * (1 + int(fanouts[l - 1]))
+            nV[l - 1] = nE[l - 1]
+        return nV, nE
+
+    def _scratch(self, max_dst, max_edges, fmax):
+        import torch
+        key = (int(max_dst), int(max_edges), int(fmax))
+        if self._ws is None or self._ws_key is None or any(a > b for a, b in zip(key, self._ws_key)):
+            nbytes = int(_lib.load().sg_gpu_sampler_ws_bytes(self.n, key[0], key[1], key[2]))
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
+            _lib.call("sg_gpu_sampler_ws_init", _lib.ptr(self._ws), self.n, _lib.stream_ptr())
+            self._ws_key = key
+        return self._ws
+
+    def sample_into(self, targets_dev, fanouts, seed, V, esrc, edst, sizes, voff, eoff):
+        """Launch the sampler (current stream) into packed device buffers with
+        capacity offsets voff (L+2) / eoff (L+1); sizes: device int64[2L+1]."""
+        L = len(fanouts)
+        fan = np.asarray(fanouts, dtype=np.int32)
+        if fan.min(initial=0) < 0 or fan.max(initial=0) > 64:
+            raise ValueError("fanouts must be in [0, 64] for the GPU sampler")
+        cap_v = np.diff(np.asarray(voff, dtype=np.int64))
+        cap_e = np.diff(np.asarray(eoff, dtype=np.int64))
+        max_dst = int(cap_v.max())
+        max_edges = int(max(cap_e.max(), 1))
+        ws = self._scratch(max_dst, max_edges, max(int(fan.max(initial=1)), 1))
+        gen0 = self._gen
+        self._gen += L + 1
+        vo = np.ascontiguousarray(voff, dtype=np.int64)
+        eo = np.ascontiguousarray(eoff, dtype=np.int64)
+        _lib.call("sg_gpu_sample", _lib.ptr(self.ro), _lib.ptr(self.ci), self.n, _lib.ptr(targets_dev),
+                  int(targets_dev.numel()), _lib.ptr(fan), L, int(seed) & (2**64 - 1), gen0 & 0xFFFFFFFF,
+                  _lib.ptr(vo), _lib.ptr(eo), max_dst, max_edges, _lib.ptr(V), _lib.ptr(esrc), _lib.ptr(edst),
+                  _lib.ptr(sizes), _lib.ptr(ws), _lib.ptr(self.err), _lib.stream_ptr())
+
+    def sample(self, targets, fanouts, seed) -> MiniBatchSample:
+        import torch
+        targets = np.asarray(targets, dtype=np.int64)
+        if targets.size == 0:
+            raise ValueError("targets must be non-empty")
+        if len(np.unique(targets)) != len(targets):
+            raise ValueError("targets must be distinct")
+        if targets.min() < 0 or targets.max() >= self.n:
+            raise ValueError("target id out of range")
+        if not list(fanouts):
+            raise ValueError("fanouts must be non-empty")
+        nV, nE = self.bounds(len(targets), fanouts)
+        voff = np.r_[0, np.cumsum(nV)].astype(np.int64)
+        eoff = np.r_[0, np.cumsum(nE)].astype(np.int64)
+        V = torch.empty(int(voff[-1]), dtype=torch.int32, device=self.dev)
+        es = torch.empty(max(int(eoff[-1]), 1), dtype=torch.int32, device=self.dev)
+        ed = torch.empty_like(es)
+        sizes = torch.zeros(2 * len(fanouts) + 1, dtype=torch.int64, device=self.dev)
+        t = torch.from_numpy(targets).to(self.dev)
+        self.sample_into(t, fanouts, seed, V, es, ed, sizes, voff, eoff)
+        if int(self.err.item()):
+            raise RuntimeError("GPU sampler: capacity exceeded or target out of range")
+        sz = sizes.cpu().numpy()
+        L = len(fanouts)
+        Vh, esh, edh = V.cpu().numpy(), es.cpu().numpy(), ed.cpu().numpy()
+        layers = [Vh[voff[l]:voff[l] + sz[l]].astype(np.int64) for l in range(L + 1)]
+        edges = [(esh[eoff[l]:eoff[l] + sz[L + 1 + l]].astype(np.int64),
+                  edh[eoff[l]:eoff[l] + sz[L + 1 + l]].astype(np.int64)) for l in range(L)]
+        return MiniBatchSample(L, layers, edges)
