@@ -103,11 +103,17 @@ def make_samples(graph, train, k, batch, threads):
     ss = np.random.SeedSequence([RUN_SEED, 0])
     batches = sg.epoch_batches(train, batch, np.random.default_rng(ss.spawn(1)[0]))
     out = []
+    global PLAN
+    PLAN = []
     for i in range(k):
         tg = batches[i % len(batches)]
         seed = int(np.random.default_rng(ss.spawn(1)[0]).integers(0, 2**63 - 1))
         out.append(sampler.sample(tg, FANOUTS, seed))
+        PLAN.append((tg, seed))
     return out, len(batches)
+
+
+PLAN = []  # (targets, seed) of every pre-sampled step, for the on-GPU sampling pipeline
 
 
 class ClockSampler:
@@ -481,8 +487,33 @@ def main():
         e1.record()
         barrier()
         e2e_ms = e0.elapsed_time(e1)
+        # ---- end to end from host TARGETS: the GPU sampler inside the graph ------------
+        e2e_s = None
+        pipe_stats = getattr(ce, "pipe_stats", None)
+        if g == 1 and all(len(t) == args.batch for t, _ in PLAN):
+            from paper_2303_13775_b200.engine import SampledCapturedStep
+            del ce
+            gs = sg.GpuSampler(graph, device=dev)
+            cz = SampledCapturedStep(gs, FANOUTS, args.batch, dp, pm, cache, feats, labels_dev, cap_nV, cap_nE,
+                                     LR / args.batch, dev)
+            cz.capture_targets(*PLAN[0])
+            pz = cz.pin_targets(PLAN[args.warmup:n_steps])
+            cz.run_pipelined_targets(pz[:2])
+            barrier()
+            z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            z0.record()
+            zl, zh2d, zd2h = cz.run_pipelined_targets(pz)
+            z1.record()
+            barrier()
+            cz.check()
+            zms = z0.elapsed_time(z1)
+            e2e_s = {"value": edges / (zms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": zh2d // args.steps,
+                     "d2h_bytes_per_step": zd2h // args.steps, "ms_per_step": zms / args.steps,
+                     "what": "host targets + seed -> GPU sampler (bit-identical to the native sampler) + split + "
+                             "train + SGD in one CUDA graph -> loss to host; includes sampling, which `value` "
+                             "and the CPU reference exclude"}
     else:
-        t_e2e, ce = None, None
+        t_e2e, ce, e2e_s, pipe_stats = None, None, None, None
         # ---- one rank per GPU: eager step, NCCL all-to-all-v + all-reduce ---------
         def one_step(i, record_events=False):
             V, es, ed, (nV, nE) = dev_samples[i]
@@ -610,7 +641,8 @@ def main():
             "e2e": {"value": e2e, "unit": "edges/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms / args.steps,
                     "wall_ms_per_step": (t_e2e * 1e3 / args.steps) if g == 1 else None,
-                    "host_us_per_step": getattr(ce, "pipe_stats", None) if g == 1 else None},
+                    "host_us_per_step": pipe_stats if g == 1 else None},
+            "e2e_with_sampling": e2e_s,
             "gpu_launches": int(launches),
             "phases_ms": {k: round(v, 5) for k, v in sorted(phases.items(), key=lambda x: -x[1])},
             "clocks": clocks.summary(),

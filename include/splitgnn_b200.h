@@ -413,14 +413,17 @@ int sg_peer_allreduce_sgd(const int64_t* peer_slots, int32_t g, int64_t n, int64
  * device int64 targets[nt]: the packed sample (V^l at voff[l], E^l at
  * eoff_cap[l-1], sizes = [nV_0..nV_L, nE_1..nE_L]) identical to the native
  * host sampler's for the same seed. ws: sg_gpu_sampler_ws_bytes(n, max_dst,
- * max_edges, max fanout) bytes, initialised once with sg_gpu_sampler_ws_init;
- * gen0 advances by L + 1 per call. *err: 1 target out of range, 2/4 edge /
- * vertex capacity exceeded. Fanouts in [0, 64]. */
+ * max_edges, max fanout) bytes, initialised once with sg_gpu_sampler_ws_init
+ * (it keeps a device generation counter, so calls replay inside a CUDA graph).
+ * seed_dev (optional): read the seed from device memory (per replay).
+ * *err: 1 target out of range, 2/4 edge / vertex capacity exceeded.
+ * Fanouts in [0, 64]. */
 int64_t sg_gpu_sampler_ws_bytes(int64_t n, int64_t max_dst, int64_t max_edges, int32_t fmax);
-int sg_gpu_sampler_ws_init(void* ws, int64_t n, void* stream);
+int sg_gpu_sampler_ws_init(void* ws, int64_t n, int64_t ws_bytes, void* stream);
 int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indices, int64_t n,
                   const int64_t* targets, int64_t nt, const int32_t* fanouts, int32_t L, uint64_t seed,
-                  uint32_t gen0, const int64_t* voff, const int64_t* eoff_cap, int64_t max_dst,
+                  const uint64_t* seed_dev, int64_t ws_bytes, const int64_t* voff, const int64_t* eoff_cap,
+                  int64_t max_dst,
                   int64_t max_edges, int32_t* V, int32_t* esrc, int32_t* edst, int64_t* sizes, void* ws,
                   int32_t* err, void* stream);
 /* sg_reduce_partials with the SGD step fused (single device, nothing to

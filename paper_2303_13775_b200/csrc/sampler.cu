@@ -26,12 +26,14 @@
 namespace sg {
 namespace {
 
-constexpr int SMP_FMAX = 64;  // max fanout (sparse swap map: 2 * fanout entries per thread)
+constexpr int SMP_FMAX = 64;  // max fanout (swap map <= 128 entries: 4 register slots per lane)
 
 struct SmpLayer {
   int l, f;
-  uint32_t gen;
+  uint32_t gen_off;           // this layer's generation = *gen_dev + gen_off
+  const uint32_t* gen_dev;    // per-call base generation (device: graph replays advance it)
   uint64_t seed;
+  const uint64_t* seed_dev;   // if set, the seed is read from device memory (per replay)
   int64_t cur_off, prev_off;  // capacity offsets of V^l and V^{l-1} in the packed V
   int64_t e_off;              // capacity offset of E^l in the packed edge arrays
   int size_cur, size_prev;    // indices into sizes[]: nV[l], nV[l-1]; edges at size_e
@@ -57,64 +59,177 @@ __global__ void k_smp_mark(const int32_t* __restrict__ V, const int64_t* __restr
                            uint32_t* __restrict__ stamp, int32_t* __restrict__ pos) {
   SG_PDL_ENTRY();
   const int nc = nv_of(sizes, s.size_cur);
+  const uint32_t gen = *s.gen_dev + s.gen_off;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
     const int32_t v = V[s.cur_off + i];
-    stamp[v] = s.gen;
+    stamp[v] = gen;
     pos[v] = i;
   }
 }
 
-__global__ void k_smp_pick(const int32_t* __restrict__ V, const int64_t* __restrict__ sizes, SmpLayer s,
-                           const int64_t* __restrict__ ro, const int32_t* __restrict__ ci,
-                           int32_t* __restrict__ picks, int32_t* __restrict__ npk) {
+// One WARP per destination. The partial Fisher-Yates' sparse swap map
+// (<= 2k entries) and the accepted list (<= k) live in registers spread over
+// the lanes (4 map slots, 2 output slots per lane) and are searched with
+// ballots; every random position r_j depends only on (seed, l, i, j, m), so
+// all of them -- and the column entries at positions j and r_j -- are loaded
+// in two parallel rounds before the (inherently sequential) swaps run.
+// Semantically the same as the host sampler's per-thread loop (same order,
+// same hash, same accept rules), so the output is identical.
+__global__ void __launch_bounds__(256) k_smp_pick(const int32_t* __restrict__ V, const int64_t* __restrict__ sizes,
+                                                  SmpLayer s, const int64_t* __restrict__ ro,
+                                                  const int32_t* __restrict__ ci, int32_t* __restrict__ picks,
+                                                  int32_t* __restrict__ npk) {
   SG_PDL_ENTRY();
   const int nc = nv_of(sizes, s.size_cur);
   const int f = s.f;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+  const uint64_t seed = s.seed_dev ? *s.seed_dev : s.seed;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = gw; i < nc; i += nw) {
     const int32_t v = V[s.cur_off + i];
-    const int64_t s0 = ro[v], m = ro[v + 1] - s0;
-    const int64_t k = m < f ? m : f;
+    const int64_t s0 = ro[v];
+    const int m = (int)(ro[v + 1] - s0);
+    const int k = m < f ? m : f;
+    int32_t outv0 = 0, outv1 = 0;
     int cnt = 0;
-    int32_t* out = picks + (int64_t)i * f;
     auto accept = [&](int32_t u) {
       if (u == v) return;  // the input's own self-loop
-      for (int t = 0; t < cnt; ++t)
-        if (out[t] == u) return;  // parallel edge
-      out[cnt++] = u;
+      const unsigned b = __ballot_sync(0xffffffffu, (lane < cnt && outv0 == u) || (32 + lane < cnt && outv1 == u));
+      if (b) return;  // parallel edge
+      if (lane == (cnt & 31)) {
+        if (cnt < 32) outv0 = u; else outv1 = u;
+      }
+      ++cnt;
     };
+    if (k > 0 && k <= 32 && (k < m || m <= 32)) {
+      // ---- all k steps at once (k <= 32, one lane per step). Step t swaps
+      // positions t and r_t (r_t >= t); position t is never touched after
+      // step t, so the pick of step j is the value at r_j before step j:
+      // the value W(t) that the LAST earlier step t with r_t == r_j moved
+      // there, else the column entry itself. W(t) (position t's value before
+      // step t) is likewise the W of the last earlier step that targeted t,
+      // else ci[t]: a chain resolved by pointer jumping. Duplicates / self
+      // loops are then dropped keeping first occurrences (match_any), which
+      // is exactly the sequential accept loop.
+      __shared__ int lw_s[8][32];
+      int* lw = lw_s[threadIdx.x >> 5];
+      const bool act = lane < k;
+      const int32_t pj = (lane < m && act) ? ci[s0 + lane] : 0;
+      int r = -1 - lane;  // unique dummy for idle lanes
+      int32_t pr = 0;
+      if (k < m && act) {
+        r = lane + (int)sg_bounded(sg_hash3(seed, ((uint64_t)s.l << 40) ^ (uint64_t)i, (uint64_t)lane),
+                                   (uint64_t)(m - lane));
+        pr = ci[s0 + r];
+      }
+      int32_t picked = pj;
+      if (k < m) {
+        const unsigned grp = __match_any_sync(0xffffffffu, r);
+        const unsigned below = grp & lanemask_lt();
+        const int prev = below ? 31 - __clz(below) : -1;
+        lw[lane] = -1;
+        __syncwarp();
+        if (act && r < k && r != lane) atomicMax(&lw[r], lane);
+        __syncwarp();
+        int nxt = (act && lw[lane] >= 0) ? lw[lane] : lane;
+#pragma unroll
+        for (int it = 0; it < 5; ++it) nxt = __shfl_sync(0xffffffffu, nxt, nxt);
+        const int32_t W = __shfl_sync(0xffffffffu, pj, nxt);
+        const int32_t fromW = __shfl_sync(0xffffffffu, W, prev >= 0 ? prev : lane);
+        picked = prev >= 0 ? fromW : pr;
+      }
+      const bool valid = act && picked != v;
+      const unsigned g2 = __match_any_sync(0xffffffffu, valid ? picked : (int32_t)(-1 - lane));
+      const bool first = valid && lane == __ffs(g2) - 1;
+      const unsigned acc = __ballot_sync(0xffffffffu, first);
+      if (first) picks[i * f + __popc(acc & lanemask_lt())] = picked;
+      if (lane == 0) npk[i] = 1 + __popc(acc);
+      continue;
+    }
     if (k > 0) {
+      // column entries at positions 0..63 (all that the take-all case and the
+      // j positions of the partial shuffle need)
+      const int32_t pj0 = lane < m ? ci[s0 + lane] : 0;
+      const int32_t pj1 = 32 + lane < m ? ci[s0 + 32 + lane] : 0;
       if (k >= m) {
-        for (int64_t j = 0; j < m; ++j) accept(ci[s0 + j]);
+        for (int j = 0; j < m; ++j) accept(__shfl_sync(0xffffffffu, j < 32 ? pj0 : pj1, j & 31));
       } else {
-        int64_t mk[2 * SMP_FMAX];
-        int64_t mv[2 * SMP_FMAX];
+        // r_j for j = lane, lane + 32 and the column entries there
+        int r0 = 0, r1 = 0;
+        if (lane < k)
+          r0 = lane + (int)sg_bounded(sg_hash3(seed, ((uint64_t)s.l << 40) ^ (uint64_t)i, (uint64_t)lane),
+                                      (uint64_t)(m - lane));
+        if (32 + lane < k)
+          r1 = 32 + lane + (int)sg_bounded(sg_hash3(seed, ((uint64_t)s.l << 40) ^ (uint64_t)i, (uint64_t)(32 + lane)),
+                                           (uint64_t)(m - 32 - lane));
+        const int32_t pr0 = lane < k ? ci[s0 + r0] : 0;
+        const int32_t pr1 = 32 + lane < k ? ci[s0 + r1] : 0;
+        int keys[4], vals[4];
         int nm = 0;
-        auto get = [&](int64_t x) -> int64_t {
-          for (int t = 0; t < nm; ++t)
-            if (mk[t] == x) return mv[t];
-          return ci[s0 + x];
-        };
-        auto set = [&](int64_t x, int64_t val) {
-          for (int t = 0; t < nm; ++t)
-            if (mk[t] == x) {
-              mv[t] = val;
-              return;
+        auto find = [&](int x, int& slot) -> int {  // lane holding key x, or -1
+          // only the occupied slots (one ballot while the map has <= 32 entries)
+          unsigned b = __ballot_sync(0xffffffffu, lane < nm && keys[0] == x);
+          if (b) {
+            slot = 0;
+            return __ffs(b) - 1;
+          }
+#pragma unroll
+          for (int t = 1; t < 4; ++t) {
+            if (t * 32 >= nm) break;
+            b = __ballot_sync(0xffffffffu, t * 32 + lane < nm && keys[t] == x);
+            if (b) {
+              slot = t;
+              return __ffs(b) - 1;
             }
-          mk[nm] = x;
-          mv[nm] = val;
+          }
+          return -1;
+        };
+        auto value_at = [&](int slot, int src) -> int {
+          int mine = vals[0];
+#pragma unroll
+          for (int t = 1; t < 4; ++t)
+            if (slot == t) mine = vals[t];
+          return __shfl_sync(0xffffffffu, mine, src);
+        };
+        auto set = [&](int x, int val) {
+          int slot = 0;
+          const int at = find(x, slot);
+          if (at >= 0) {
+            if (lane == at) {
+#pragma unroll
+              for (int t = 0; t < 4; ++t)
+                if (slot == t) vals[t] = val;
+            }
+            return;
+          }
+          if (lane == (nm & 31)) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if ((nm >> 5) == t) {
+                keys[t] = x;
+                vals[t] = val;
+              }
+          }
           ++nm;
         };
-        for (int64_t j = 0; j < k; ++j) {
-          const uint64_t h = sg_hash3(s.seed, ((uint64_t)s.l << 40) ^ (uint64_t)i, (uint64_t)j);
-          const int64_t r = j + (int64_t)sg_bounded(h, (uint64_t)(m - j));
-          const int64_t vj = get(j), vr = get(r);
+        for (int j = 0; j < k; ++j) {
+          const int r = __shfl_sync(0xffffffffu, j < 32 ? r0 : r1, j & 31);
+          int slot = 0;
+          int at = find(j, slot);
+          const int vj = at >= 0 ? value_at(slot, at) : __shfl_sync(0xffffffffu, j < 32 ? pj0 : pj1, j & 31);
+          at = find(r, slot);
+          const int vr = at >= 0 ? value_at(slot, at) : __shfl_sync(0xffffffffu, j < 32 ? pr0 : pr1, j & 31);
           set(r, vj);
           set(j, vr);
-          accept((int32_t)vr);
+          accept(vr);
         }
       }
     }
-    npk[i] = 1 + cnt;  // the self edge plus the picks
+    int32_t* out = picks + i * f;
+    if (lane < cnt) out[lane] = outv0;
+    if (32 + lane < cnt) out[32 + lane] = outv1;
+    if (lane == 0) npk[i] = 1 + cnt;  // the self edge plus the picks
   }
 }
 
@@ -207,18 +322,23 @@ __global__ void __launch_bounds__(256) k_scan_local(const int32_t* __restrict__ 
   }
 }
 
+// The per-pick kernels run one thread per (destination, pick slot): slot
+// t < f is pick t of destination i (edge position eoff[i] + 1 + t), slot f is
+// the destination's self edge (position eoff[i]).
 __global__ void k_smp_first(const int64_t* __restrict__ sizes, SmpLayer s, const int32_t* __restrict__ picks,
                             const int32_t* __restrict__ npk, const int32_t* __restrict__ eoff,
                             const uint32_t* __restrict__ stamp, unsigned long long* __restrict__ first) {
   SG_PDL_ENTRY();
   const int nc = nv_of(sizes, s.size_cur);
-  const unsigned long long hi = (unsigned long long)(0xFFFFFFFFu - s.gen) << 32;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
-    const int c = npk[i] - 1;
-    for (int t = 0; t < c; ++t) {
-      const int32_t u = picks[(int64_t)i * s.f + t];
-      if (stamp[u] != s.gen) atomicMin(&first[u], hi | (unsigned)(eoff[i] + 1 + t));
-    }
+  const int f = s.f;
+  const uint32_t gen = *s.gen_dev + s.gen_off;
+  const unsigned long long hi = (unsigned long long)(0xFFFFFFFFu - gen) << 32;
+  const int64_t tot = (int64_t)nc * f;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(x / f), t = (int)(x - (int64_t)i * f);
+    if (t >= npk[i] - 1) continue;
+    const int32_t u = picks[x];
+    if (stamp[u] != gen) atomicMin(&first[u], hi | (unsigned)(eoff[i] + 1 + t));
   }
 }
 
@@ -228,19 +348,23 @@ __global__ void k_smp_isfirst(const int64_t* __restrict__ sizes, SmpLayer s, con
                               int32_t* __restrict__ isfirst) {
   SG_PDL_ENTRY();
   const int nc = nv_of(sizes, s.size_cur);
-  const unsigned long long hi = (unsigned long long)(0xFFFFFFFFu - s.gen) << 32;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
-    const int e0 = eoff[i];
-    const int c = npk[i] - 1;
+  const int f = s.f, f1 = f + 1;
+  const uint32_t gen = *s.gen_dev + s.gen_off;
+  const unsigned long long hi = (unsigned long long)(0xFFFFFFFFu - gen) << 32;
+  const int64_t tot = (int64_t)nc * f1;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(x / f1), t = (int)(x - (int64_t)i * f1);
+    const int c = npk[i] - 1, e0 = eoff[i];
     if (e0 + c >= s.cap_e) {  // E^l over capacity
-      atomicOr(s.err, 2);
+      if (t == f) atomicOr(s.err, 2);
       continue;
     }
-    isfirst[e0] = 0;
-    for (int t = 0; t < c; ++t) {
-      const int32_t u = picks[(int64_t)i * s.f + t];
+    if (t == f) {
+      isfirst[e0] = 0;
+    } else if (t < c) {
+      const int32_t u = picks[(int64_t)i * f + t];
       const unsigned p = (unsigned)(e0 + 1 + t);
-      isfirst[e0 + 1 + t] = (stamp[u] != s.gen && first[u] == (hi | p)) ? 1 : 0;
+      isfirst[p] = (stamp[u] != gen && first[u] == (hi | p)) ? 1 : 0;
     }
   }
 }
@@ -252,23 +376,28 @@ __global__ void k_smp_assign(int32_t* __restrict__ V, int64_t* __restrict__ size
                              uint32_t* __restrict__ stamp, int32_t* __restrict__ pos) {
   SG_PDL_ENTRY();
   const int nc = nv_of(sizes, s.size_cur);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
-    V[s.prev_off + i] = V[s.cur_off + i];  // V^l is a prefix of V^{l-1}
-    const int e0 = eoff[i];
-    const int c = npk[i] - 1;
-    for (int t = 0; t < c; ++t) {
-      const int p = e0 + 1 + t;
-      if (!isfirst[p]) continue;
-      const int32_t u = picks[(int64_t)i * s.f + t];
-      const int j = nc + newidx[p];
-      if (j >= s.cap_prev) {  // V^{l-1} over capacity
-        atomicOr(s.err, 4);
-        continue;
-      }
-      V[s.prev_off + j] = u;
-      pos[u] = j;
-      stamp[u] = s.gen;
+  const int f = s.f, f1 = f + 1;
+  const uint32_t gen = *s.gen_dev + s.gen_off;
+  const int64_t tot = (int64_t)nc * f1;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(x / f1), t = (int)(x - (int64_t)i * f1);
+    if (t == f) {
+      V[s.prev_off + i] = V[s.cur_off + i];  // V^l is a prefix of V^{l-1}
+      continue;
     }
+    const int c = npk[i] - 1, e0 = eoff[i];
+    if (t >= c || e0 + c >= s.cap_e) continue;
+    const int p = e0 + 1 + t;
+    if (!isfirst[p]) continue;
+    const int32_t u = picks[(int64_t)i * f + t];
+    const int j = nc + newidx[p];
+    if (j >= s.cap_prev) {  // V^{l-1} over capacity
+      atomicOr(s.err, 4);
+      continue;
+    }
+    V[s.prev_off + j] = u;
+    pos[u] = j;
+    stamp[u] = gen;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     sizes[s.size_prev] = nc + totals[1];  // new vertices
@@ -281,17 +410,26 @@ __global__ void k_smp_edges(const int64_t* __restrict__ sizes, SmpLayer s, const
                             const int32_t* __restrict__ pos, int32_t* __restrict__ esrc, int32_t* __restrict__ edst) {
   SG_PDL_ENTRY();
   const int nc = nv_of(sizes, s.size_cur);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+  const int f = s.f, f1 = f + 1;
+  const int64_t tot = (int64_t)nc * f1;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < tot; x += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(x / f1), t = (int)(x - (int64_t)i * f1);
     const int c = npk[i] - 1;
     if (eoff[i] + c >= s.cap_e) continue;
     const int64_t e0 = s.e_off + eoff[i];
-    esrc[e0] = i;
-    edst[e0] = i;
-    for (int t = 0; t < c; ++t) {
-      esrc[e0 + 1 + t] = pos[picks[(int64_t)i * s.f + t]];
+    if (t == f) {
+      esrc[e0] = i;
+      edst[e0] = i;
+    } else if (t < c) {
+      esrc[e0 + 1 + t] = pos[picks[(int64_t)i * f + t]];
       edst[e0 + 1 + t] = i;
     }
   }
+}
+
+__global__ void k_smp_advance(uint32_t* gen_dev, uint32_t by) {
+  SG_PDL_ENTRY();
+  if (threadIdx.x == 0 && blockIdx.x == 0) *gen_dev += by;
 }
 
 }  // namespace
@@ -299,13 +437,20 @@ __global__ void k_smp_edges(const int64_t* __restrict__ sizes, SmpLayer s, const
 
 using namespace sg;
 
+// The per-call generation counter lives in its own 16-byte word at the end of
+// the scratch (zeroed by sg_gpu_sampler_ws_init with the scratch size).
+static uint32_t* gen_word(void* ws, int64_t ws_bytes) {
+  return (uint32_t*)((char*)ws + ((ws_bytes - 16) & ~(int64_t)15));
+}
+
 // One-time scratch initialisation: generation stamps 0, first-occurrence keys
 // all-ones (any current generation's key is smaller).
-extern "C" int sg_gpu_sampler_ws_init(void* ws, int64_t n, void* stream) {
-  SG_REQUIRE(ws && n > 0, "gpu_sampler_ws_init: bad argument");
+extern "C" int sg_gpu_sampler_ws_init(void* ws, int64_t n, int64_t ws_bytes, void* stream) {
+  SG_REQUIRE(ws && n > 0 && ws_bytes >= 16 * n + 16, "gpu_sampler_ws_init: bad argument");
   cudaStream_t st = (cudaStream_t)stream;
   SG_CUDA(cudaMemsetAsync(ws, 0, 8 * (size_t)n, st));
   SG_CUDA(cudaMemsetAsync((char*)ws + 8 * n, 0xFF, 8 * (size_t)n, st));
+  SG_CUDA(cudaMemsetAsync(gen_word(ws, ws_bytes), 0, 16, st));
   return SG_OK;
 }
 
@@ -316,6 +461,7 @@ extern "C" int64_t sg_gpu_sampler_ws_bytes(int64_t n, int64_t max_dst, int64_t m
   return 4 * n + 4 * n + 8 * n + 4 * max_dst * (int64_t)fmax + 4 * max_dst * 3 + 4 * max_edges * 2 + 4 * nb + 64;
 }
 
+
 // sample_minibatch on the device. targets: device int64[nt]. Output at the
 // capacity offsets of a packed sample: V^l at voff[l], E^l at eoff[l-1]
 // (esrc/edst), sizes = [nV_0..nV_L, nE_1..nE_L] (device int64). ws: the
@@ -323,7 +469,8 @@ extern "C" int64_t sg_gpu_sampler_ws_bytes(int64_t n, int64_t max_dst, int64_t m
 // gen0: a per-call base generation, advanced by L + 1 per call by the caller.
 extern "C" int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indices, int64_t n,
                              const int64_t* targets, int64_t nt, const int32_t* fanouts, int32_t L,
-                             uint64_t seed, uint32_t gen0, const int64_t* voff, const int64_t* eoff_cap,
+                             uint64_t seed, const uint64_t* seed_dev, int64_t ws_bytes, const int64_t* voff,
+                             const int64_t* eoff_cap,
                              int64_t max_dst, int64_t max_edges, int32_t* V, int32_t* esrc, int32_t* edst,
                              int64_t* sizes, void* ws, int32_t* err, void* stream) {
   SG_REQUIRE(row_offsets && col_indices && targets && fanouts && V && esrc && edst && sizes && ws && err,
@@ -357,8 +504,10 @@ extern "C" int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indi
     SmpLayer s;
     s.l = l;
     s.f = std::max(1, (int)fanouts[l - 1]);
-    s.gen = gen0 + (uint32_t)(L - l) + 1;
+    s.gen_off = (uint32_t)(L - l) + 1;
+    s.gen_dev = gen_word(ws, ws_bytes);
     s.seed = seed;
+    s.seed_dev = seed_dev;
     s.cur_off = voff[l];
     s.prev_off = voff[l - 1];
     s.e_off = eoff_cap[l - 1];
@@ -370,13 +519,14 @@ extern "C" int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indi
     s.err = err;
     ::sg::launch(k_smp_mark, gd, 256, 0, st, (const int32_t*)V, (const int64_t*)sizes, s, stamp, pos);
     SG_CHECK_LAUNCH("k_smp_mark");
+    const int gw = clamp_grid(div_up(max_dst, 8), kSMs * 16);  // a warp per destination
     if (fanouts[l - 1] > 0) {
-      ::sg::launch(k_smp_pick, gd, 256, 0, st, (const int32_t*)V, (const int64_t*)sizes, s, row_offsets,
+      ::sg::launch(k_smp_pick, gw, 256, 0, st, (const int32_t*)V, (const int64_t*)sizes, s, row_offsets,
                    col_indices, picks, npk);
     } else {
       SmpLayer s1 = s;
       s1.f = 0;
-      ::sg::launch(k_smp_pick, gd, 256, 0, st, (const int32_t*)V, (const int64_t*)sizes, s1, row_offsets,
+      ::sg::launch(k_smp_pick, gw, 256, 0, st, (const int32_t*)V, (const int64_t*)sizes, s1, row_offsets,
                    col_indices, picks, npk);
     }
     SG_CHECK_LAUNCH("k_smp_pick");
@@ -387,9 +537,10 @@ extern "C" int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indi
     ::sg::launch(k_scan_local, nbd, 256, 0, st, (const int32_t*)npk, (const int64_t*)sizes, l, (int64_t)0,
                  (const int32_t*)bsum, eoffs);
     SG_CHECK_LAUNCH("sampler scan (edges)");
-    ::sg::launch(k_smp_first, gd, 256, 0, st, (const int64_t*)sizes, s, (const int32_t*)picks, (const int32_t*)npk,
+    const int gs = clamp_grid(div_up(max_dst * (int64_t)(s.f + 1), 256), kSMs * 8);  // per pick slot
+    ::sg::launch(k_smp_first, gs, 256, 0, st, (const int64_t*)sizes, s, (const int32_t*)picks, (const int32_t*)npk,
                  (const int32_t*)eoffs, (const uint32_t*)stamp, first);
-    ::sg::launch(k_smp_isfirst, gd, 256, 0, st, (const int64_t*)sizes, s, (const int32_t*)picks,
+    ::sg::launch(k_smp_isfirst, gs, 256, 0, st, (const int64_t*)sizes, s, (const int32_t*)picks,
                  (const int32_t*)npk, (const int32_t*)eoffs, (const uint32_t*)stamp,
                  (const unsigned long long*)first, isfirst);
     SG_CHECK_LAUNCH("k_smp_first/isfirst");
@@ -400,12 +551,14 @@ extern "C" int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indi
     ::sg::launch(k_scan_local, nbe, 256, 0, st, (const int32_t*)isfirst, (const int64_t*)totals, 0, (int64_t)0,
                  (const int32_t*)bsum, newidx);
     SG_CHECK_LAUNCH("sampler scan (new vertices)");
-    ::sg::launch(k_smp_assign, gd, 256, 0, st, V, sizes, s, (const int32_t*)picks, (const int32_t*)npk,
+    ::sg::launch(k_smp_assign, gs, 256, 0, st, V, sizes, s, (const int32_t*)picks, (const int32_t*)npk,
                  (const int32_t*)eoffs, (const int32_t*)isfirst, (const int32_t*)newidx, (const int64_t*)totals,
                  stamp, pos);
-    ::sg::launch(k_smp_edges, gd, 256, 0, st, (const int64_t*)sizes, s, (const int32_t*)picks, (const int32_t*)npk,
+    ::sg::launch(k_smp_edges, gs, 256, 0, st, (const int64_t*)sizes, s, (const int32_t*)picks, (const int32_t*)npk,
                  (const int32_t*)eoffs, (const int32_t*)pos, esrc, edst);
     SG_CHECK_LAUNCH("k_smp_assign/edges");
   }
+  ::sg::launch(k_smp_advance, 1, 32, 0, st, gen_word(ws, ws_bytes), (uint32_t)(L + 1));
+  SG_CHECK_LAUNCH("k_smp_advance");
   return SG_OK;
 }

@@ -1200,6 +1200,81 @@ class CapturedStep:
 
 # ---- one process per GPU ------------------------------------------------------------
 
+class SampledCapturedStep(CapturedStep):
+    """The single-GPU step with the k-hop sampler inside the same CUDA graph:
+    targets + seed (one small H2D) -> GpuSampler -> split -> forward/backward
+    -> reduction + SGD. The sample never exists on the host; the captured
+    capacities must cover every sample (the sampler flags an overflow in
+    `sampler.err`, checked by `check()`)."""
+
+    def __init__(self, sampler, fanouts, batch, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE,
+                 lr_scale, device="cuda", record_events=False):
+        super().__init__(dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale, device, record_events)
+        self.sampler = sampler
+        self.fanouts = [int(f) for f in fanouts]
+        self.batch = int(batch)
+        self.tgt = torch.zeros(self.batch + 1, dtype=torch.int64, device=self.dev)  # targets | seed
+        self.htgt = torch.zeros(self.batch + 1, dtype=torch.int64).pin_memory()
+
+    def _body(self):
+        inp = self.inp
+        self.sampler.sample_into(self.tgt[:self.batch], self.fanouts, 0, inp.V, inp.es, inp.ed, inp.sizes,
+                                 inp.voff, inp.eoff, seed_dev=self.tgt[self.batch:])
+        return super()._body()
+
+    def load_targets(self, targets, seed):
+        t = np.asarray(targets, dtype=np.int64)
+        if len(t) != self.batch:
+            raise ValueError(f"the captured step samples exactly {self.batch} targets")
+        h = self.htgt.numpy()
+        h[:self.batch] = t
+        h[self.batch] = np.int64(np.uint64(int(seed) & (2**64 - 1)).view(np.int64))
+        self.tgt.copy_(self.htgt, non_blocking=True)
+
+    def capture_targets(self, targets, seed):
+        self.load_targets(targets, seed)
+        self._body()
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.out = self._body()
+        torch.cuda.synchronize()
+        return self
+
+    def run_targets(self, targets, seed):
+        self.load_targets(targets, seed)
+        return self.replay()
+
+    def check(self):
+        if int(self.sampler.err.item()):
+            raise RuntimeError("GPU sampler: a sample exceeded the captured capacities")
+
+    def pin_targets(self, plan):
+        """Pack [(targets, seed), ...] into pinned host buffers (untimed)."""
+        out = []
+        for t, sd in plan:
+            h = torch.zeros(self.batch + 1, dtype=torch.int64).pin_memory()
+            a = h.numpy()
+            a[:self.batch] = np.asarray(t, dtype=np.int64)
+            a[self.batch] = np.int64(np.uint64(int(sd) & (2**64 - 1)).view(np.int64))
+            out.append(h)
+        return out
+
+    def run_pipelined_targets(self, pinned):
+        """End to end from host targets: per step an async H2D of the targets
+        and seed (8 B x (batch + 1)), the graph replay (sample + split + step)
+        and an async D2H of the step's loss sum; one synchronisation at the
+        end. Returns (loss sums, H2D bytes, D2H bytes)."""
+        n = self.p.n
+        outs = torch.zeros(len(pinned), dtype=torch.float32).pin_memory()
+        for i, h in enumerate(pinned):
+            self.tgt.copy_(h, non_blocking=True)
+            self.graph.replay()
+            outs[i:i + 1].copy_(self.out[n:n + 1], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return outs.tolist(), sum(8 * h.numel() for h in pinned), 4 * len(pinned)
+
+
 class RankSplitTrainer:
     """Split-parallel training where this process is device `rank` of a
     `world`-GPU split (torchrun, one process per GPU). Every rank runs the

@@ -215,7 +215,6 @@ class GpuSampler:
         self.ci = torch.from_numpy(np.asarray(graph.col_indices, dtype=np.int32)).to(self.dev)
         self._ws = None
         self._ws_key = None
-        self._gen = 0
         self.err = torch.zeros(1, dtype=torch.int32, device=self.dev)
 
     @staticmethod
@@ -236,13 +235,14 @@ class GpuSampler:
         if self._ws is None or self._ws_key is None or any(a > b for a, b in zip(key, self._ws_key)):
             nbytes = int(_lib.load().sg_gpu_sampler_ws_bytes(self.n, key[0], key[1], key[2]))
             self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.dev)
-            _lib.call("sg_gpu_sampler_ws_init", _lib.ptr(self._ws), self.n, _lib.stream_ptr())
+            _lib.call("sg_gpu_sampler_ws_init", _lib.ptr(self._ws), self.n, self._ws.numel(), _lib.stream_ptr())
             self._ws_key = key
         return self._ws
 
-    def sample_into(self, targets_dev, fanouts, seed, V, esrc, edst, sizes, voff, eoff):
+    def sample_into(self, targets_dev, fanouts, seed, V, esrc, edst, sizes, voff, eoff, seed_dev=None):
         """Launch the sampler (current stream) into packed device buffers with
-        capacity offsets voff (L+2) / eoff (L+1); sizes: device int64[2L+1]."""
+        capacity offsets voff (L+2) / eoff (L+1); sizes: device int64[2L+1].
+        seed_dev (device uint64[1]) replaces `seed` when given (graph replays)."""
         L = len(fanouts)
         fan = np.asarray(fanouts, dtype=np.int32)
         if fan.min(initial=0) < 0 or fan.max(initial=0) > 64:
@@ -252,13 +252,11 @@ class GpuSampler:
         max_dst = int(cap_v.max())
         max_edges = int(max(cap_e.max(), 1))
         ws = self._scratch(max_dst, max_edges, max(int(fan.max(initial=1)), 1))
-        gen0 = self._gen
-        self._gen += L + 1
         vo = np.ascontiguousarray(voff, dtype=np.int64)
         eo = np.ascontiguousarray(eoff, dtype=np.int64)
         _lib.call("sg_gpu_sample", _lib.ptr(self.ro), _lib.ptr(self.ci), self.n, _lib.ptr(targets_dev),
-                  int(targets_dev.numel()), _lib.ptr(fan), L, int(seed) & (2**64 - 1), gen0 & 0xFFFFFFFF,
-                  _lib.ptr(vo), _lib.ptr(eo), max_dst, max_edges, _lib.ptr(V), _lib.ptr(esrc), _lib.ptr(edst),
+                  int(targets_dev.numel()), _lib.ptr(fan), L, int(seed) & (2**64 - 1), _lib.ptr(seed_dev),
+                  int(ws.numel()), _lib.ptr(vo), _lib.ptr(eo), max_dst, max_edges, _lib.ptr(V), _lib.ptr(esrc), _lib.ptr(edst),
                   _lib.ptr(sizes), _lib.ptr(ws), _lib.ptr(self.err), _lib.stream_ptr())
 
     def sample(self, targets, fanouts, seed) -> MiniBatchSample:

@@ -43,3 +43,49 @@ def test_gpu_sampler_repeated_calls_and_errors():
         gs.sample([1, 1], [3], 0)
     with pytest.raises(ValueError):
         gs.sample([graph.num_vertices], [3], 0)
+
+
+def test_sampled_captured_step_trains_like_oracle():
+    """Sampler + split + step in ONE CUDA graph (SampledCapturedStep), fed only
+    targets and a seed: the samples equal the native sampler's for the same
+    seeds, and the parameters after several replays equal the oracle's."""
+    import torch
+
+    import paper_2303_13775_b200 as sg
+    from helpers import rel_err
+    from oracle.coop_oracle import CoopRun, reduce_and_sgd
+    from oracle.model_oracle import glorot_params
+    from oracle.split_oracle import split_sample
+    from paper_2303_13775_b200.engine import SampledCapturedStep, capacities_for
+    graph = sg.generate_powerlaw(20000, 200000, blocks=16, p_local=0.8, seed=9)
+    pm = sg.range_partition(graph.num_vertices, 1)
+    cache = sg.full_cache(pm)
+    F, C, B, fan = 32, 6, 96, [8, 6, 4]
+    feats = sg.FeatureStore.synthetic(graph.num_vertices, F, seed=1)
+    hostX = sg.synthetic_features(graph.num_vertices, F, seed=1).astype(np.float64)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
+    rng = np.random.default_rng(3)
+    plan = [(rng.choice(graph.num_vertices, B, replace=False), 1000 + i) for i in range(6)]
+    ns = sg.NativeSampler(graph)
+    samples = [ns.sample(t, fan, sd) for t, sd in plan]
+    cap_nV, cap_nE = capacities_for(samples, slack=1.2)
+    params = sg.init_params("graphsage", F, 16, C, 3, seed=4)
+    dp = sg.DeviceParams.from_host(params)
+    lab = torch.from_numpy(labels).cuda()
+    cs = SampledCapturedStep(sg.GpuSampler(graph), fan, B, dp, pm, cache, feats, lab, cap_nV, cap_nE, 0.1 / B)
+    ref = glorot_params("graphsage", F, 16, C, 3, seed=4)
+    for i, ((t, sd), smp) in enumerate(zip(plan, samples)):
+        if i == 0:
+            cs.capture_targets(t, sd)      # applies step 0 eagerly
+        else:
+            cs.run_targets(t, sd)
+        loss = float(cs.out[dp.n].item())
+        ws, wp = split_sample(smp.layer_vertices, smp.layer_edges, pm.assignment, 1, cache.cached)
+        rl, rg = CoopRun(ref, ws, wp, hostX, labels).run()
+        reduce_and_sgd(ref, rg, 0.1, B)
+        if i > 0:
+            assert abs(loss - rl) <= 1e-4 * abs(rl), (i, loss, rl)
+    cs.check()
+    got = dp.to_host().tensors()
+    for k in ref:
+        assert rel_err(got[k], ref[k]) < 1e-4, k
