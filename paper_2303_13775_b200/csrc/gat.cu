@@ -24,6 +24,9 @@
 #include <cstring>
 #include <type_traits>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "dense.cuh"
 
@@ -171,6 +174,150 @@ __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ 
       }
     }
   }
+}
+
+// ---------------------------------------------------------------- tensor-core projection
+// z = h W on the tensor pipe with FP32-level accuracy: 3xTF32 (x = hi + lo,
+// hi = tf32(x), lo = tf32(x - hi); x*y ~= lo*hi + hi*lo + hi*hi, the dropped
+// lo*lo term is ~2^-22 relative) on warp-level mma.sync m16n8k8 (HMMA),
+// FP32 accumulation. A 32-row tile of gathered rows sits row-major in smem
+// (pitch K+4: conflict-free fragment loads), W is split into hi/lo once per
+// CTA (pitch D+8). Warp (mb, cg): rows 16mb..16mb+15, columns cg*D/4 ...
+// Then the per-head scores exactly as the FFMA kernel.
+__device__ __forceinline__ uint32_t tf32_of(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void cp_async16g(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+template <int NT8>  // n8 tiles per warp: D = 32 * NT8
+__global__ void __launch_bounds__(256) k_gat_project_mma(const SgMeta* __restrict__ meta, ProjArgs a) {
+  SG_PDL_ENTRY();
+  constexpr int TM = 32;
+  constexpr int D = 32 * NT8, DP = D + 8;
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, H = a.heads, dh = D / H;
+  const int KPAD = (w + 7) & ~7, KP = KPAD + 4;
+  float* W_s = smem;                   // [KPAD][DP] fp32 (hi/lo split at use)
+  float* A_s = W_s + KPAD * DP;        // [2][TM][KP] double-buffered gathered rows
+  float* red = A_s + 2 * TM * KP;      // [TM][D]
+  int* prow = reinterpret_cast<int*>(red + TM * D);  // [2][TM]
+  for (int i = threadIdx.x; i < KPAD * D; i += 256) {
+    const int k = i / D, jj = i - k * D;
+    W_s[k * DP + jj] = k < w ? a.W[k * D + jj] : 0.f;
+  }
+  for (int i = threadIdx.x; i < 2 * TM * (KP - w); i += 256) {  // K padding columns stay zero
+    const int r = i / (KP - w), c = w + (i - r * (KP - w));
+    A_s[r * KP + c] = 0.f;
+  }
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d];
+  const int ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int mb = warp >> 2, cg = warp & 3;
+  const int w4 = w / 4;
+  const int G = gridDim.x;
+  auto src_of = [&](int tile) {  // gathered row of this thread's tile row (threads < TM)
+    const int r = tile * TM + (int)threadIdx.x;
+    if (r >= n) return -1;
+    const int pr = own0 + r;
+    return a.src_row ? a.src_row[pr] : pr;
+  };
+  auto issue = [&](int tile, int buf) {
+    float* Ab = A_s + buf * TM * KP;
+    const int* pb = prow + buf * TM;
+    for (int idx = threadIdx.x; idx < TM * w4; idx += 256) {
+      const int r = idx / w4, q = idx - r * w4;
+      if (pb[r] >= 0 && tile * TM < n) cp_async16g(Ab + r * KP + 4 * q, a.h_prev + (int64_t)pb[r] * w + 4 * q);
+      else *reinterpret_cast<float4*>(Ab + r * KP + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int tile = blockIdx.x;
+  if (threadIdx.x < TM) prow[threadIdx.x] = src_of(tile);
+  int pnext = (threadIdx.x < TM) ? src_of(tile + G) : -1;
+  __syncthreads();
+  issue(tile, 0);
+  for (int k = 0; tile < (n + TM - 1) / TM; ++k, tile += G) {
+    const int buf = k & 1;
+    if (threadIdx.x < TM) prow[(buf ^ 1) * TM + threadIdx.x] = pnext;
+    __syncthreads();  // prow of the next tile visible; A_s[buf ^ 1] free
+    issue(tile + G, buf ^ 1);
+    if (threadIdx.x < TM) pnext = src_of(tile + 2 * G);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const int r0 = tile * TM;
+    float acc[NT8][4];
+#pragma unroll
+    for (int jj = 0; jj < NT8; ++jj) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0.f;
+    const float* Ar = A_s + buf * TM * KP + (16 * mb + g) * KP;
+    for (int k0 = 0; k0 < KPAD; k0 += 8) {
+      const float x[4] = {Ar[k0 + t], Ar[8 * KP + k0 + t], Ar[k0 + t + 4], Ar[8 * KP + k0 + t + 4]};
+      uint32_t ah[4], al[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ah[u] = tf32_of(x[u]);
+        al[u] = tf32_of(x[u] - __uint_as_float(ah[u]));
+      }
+#pragma unroll
+      for (int jj = 0; jj < NT8; ++jj) {
+        const int n0 = cg * (D / 4) + 8 * jj;
+        const float w0 = W_s[(k0 + t) * DP + n0 + g], w1 = W_s[(k0 + t + 4) * DP + n0 + g];
+        const uint32_t bh0 = tf32_of(w0), bh1 = tf32_of(w1);
+        const uint32_t bl0 = tf32_of(w0 - __uint_as_float(bh0)), bl1 = tf32_of(w1 - __uint_as_float(bh1));
+        mma_tf32(acc[jj], al, bh0, bh1);
+        mma_tf32(acc[jj], ah, bl0, bl1);
+        mma_tf32(acc[jj], ah, bh0, bh1);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < NT8; ++jj) {
+      const int n0 = cg * (D / 4) + 8 * jj;
+      const int ra = 16 * mb + g;
+      red[ra * D + n0 + 2 * t] = acc[jj][0];
+      red[ra * D + n0 + 2 * t + 1] = acc[jj][1];
+      red[(ra + 8) * D + n0 + 2 * t] = acc[jj][2];
+      red[(ra + 8) * D + n0 + 2 * t + 1] = acc[jj][3];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < TM * D / 4; idx += 256) {
+      const int r = idx / (D / 4), q = idx - r * (D / 4);
+      if (r0 + r < n)
+        reinterpret_cast<float4*>(a.z + (int64_t)(own0 + r0 + r) * D)[q] = reinterpret_cast<const float4*>(red + r * D)[q];
+    }
+    // scores s = z.a_src per head; t = z.a_dst on self rows
+    for (int idx = threadIdx.x; idx < TM * H; idx += 256) {
+      const int r = idx / H, hh = idx - r * H;
+      if (r0 + r >= n) continue;
+      const int G2 = own0 + r0 + r;
+      const float* zr = red + r * D + hh * dh;
+      float sv = 0.f;
+      for (int jj = 0; jj < dh; ++jj) sv = fmaf(zr[jj], a.a_src[hh * dh + jj], sv);
+      a.s[(int64_t)G2 * H + hh] = sv;
+      const int p = a.grouped[a.voff_lm1 + G2];
+      if (p < nVl) {
+        float tv = 0.f;
+        for (int jj = 0; jj < dh; ++jj) tv = fmaf(zr[jj], a.a_dst[hh * dh + jj], tv);
+        a.t[(int64_t)(ownl + a.rank[a.voff_l + p]) * H + hh] = tv;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // TM = 32 rows per tile; NT = 8 * NQ register tiles (4 rows x 4 outputs),
@@ -1005,6 +1152,30 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
   const size_t smem = sizeof(float) * ((size_t)w * dout + (size_t)PTR * (w + 1) + (size_t)PTR * (dout + 1) + PTR);
   cudaStream_t st = (cudaStream_t)stream;
   const int nq = dout / 4;
+  static const bool use_mma = !getenv("SG_NO_MMA");
+  if (use_mma && w % 4 == 0 && w > 32 && w <= 256 && (dout == 32 || dout == 64 || dout == 128)) {
+    // tensor-core path (3xTF32 HMMA) for the wide layer-1 projection
+    const int KPAD = (w + 7) & ~7;
+    const size_t smem_m = sizeof(float) * ((size_t)KPAD * (dout + 8) + 2 * 32 * (size_t)(KPAD + 4) +
+                                           32 * (size_t)dout) + 2 * 32 * 4;
+    if (smem_m <= 227 * 1024) {
+      const int per_sm = std::max<int>(1, std::min<int>(4, (int)((228 * 1024) / (smem_m + 1024))));
+      const int grid_m = clamp_grid(div_up(max_rows, 32), kSMs * per_sm);
+      cudaError_t attr = cudaSuccess;
+      switch (dout) {
+#define GM_CASE(DD, NT)                                              \
+  case DD:                                                           \
+    attr = allow_max_smem<k_gat_project_mma<NT>>();                  \
+    SG_CUDA(attr);                                                   \
+    ::sg::launch(k_gat_project_mma<NT>, grid_m, 256, smem_m, st, meta, a); \
+    break;
+        GM_CASE(32, 1) GM_CASE(64, 2) GM_CASE(128, 4)
+#undef GM_CASE
+      }
+      SG_CHECK_LAUNCH("k_gat_project_mma");
+      return SG_OK;
+    }
+  }
   if (w % 4 == 0 && w <= 128 && dout % 4 == 0 && nq <= 32 && (nq & (nq - 1)) == 0) {
     // register-tiled path: 4x4 tiles, K split over slices (TM = 32 rows per tile)
     const int NS = 256 / (8 * nq);
