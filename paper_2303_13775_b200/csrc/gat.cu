@@ -842,15 +842,25 @@ struct BParamArgs {
 
 // T4 (w % 4 == 0 and dout % 4 == 0): thread slot (cg, jg) owns a 4x4 dW tile,
 // per row 2 LDS.128 + 16 FFMA; otherwise one scalar slot per (c, j).
-template <bool T4>
+template <int MODE>  // 0 scalar FFMA, 1 4x4 FFMA tiles, 2 3xTF32 HMMA (dout == 64)
 __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict__ meta, BParamArgs a) {
   SG_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, H = a.heads, dh = dout / H;
-  const int wp = T4 ? w + 4 : w + 1;  // h row stride (float4-aligned for T4)
+  constexpr bool T4 = MODE >= 1;
+  constexpr bool MMA = MODE == 2;
+  const int MB = (w + 15) / 16;        // MMA: 16-row blocks of dW (M = w padded)
+  // h row stride: float4-aligned for T4; for MMA >= 16*MB (zero padding) and
+  // == 24 mod 32 (conflict-free A fragments)
+  int wp = T4 ? w + 4 : w + 1;
+  if (MMA) {
+    wp = (16 * MB + 8 + 31) / 32 * 32 - 8;
+    if (wp < 16 * MB) wp += 32;
+  }
+  const int dzp = MMA ? dout + 8 : dout;  // d_z row stride (conflict-free B fragments)
   const int wt = w + 1;               // W^T row stride (d_prev: lanes run along c)
-  float* dz_s = smem;               // [QTR][dout]
-  float* Wt_s = dz_s + QTR * dout;  // [dout][w+1] = W^T (for d_prev)
+  float* dz_s = smem;               // [QTR][dzp]
+  float* Wt_s = dz_s + QTR * dzp;   // [dout][w+1] = W^T (for d_prev)
   float* h_s = Wt_s + dout * wt;    // [QTR][wp]
   float* z_s = h_s + QTR * wp;      // [QTR][dout]
   float* ds_s = z_s + QTR * dout;   // [QTR][H]
@@ -860,6 +870,11 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
       Wt_s[j * wt + c] = a.W[i];
+    }
+  if (MMA)  // zero padding columns w..wp of the h tile (never written by the row loads)
+    for (int i = threadIdx.x; i < QTR * (wp - w); i += blockDim.x) {
+      const int rr = i / (wp - w);
+      h_s[rr * wp + w + (i - rr * (wp - w))] = 0.f;
     }
   const int l = a.l, d = a.d;
   const int n = meta->n_own[l - 1][d];
@@ -907,7 +922,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
           vd = *reinterpret_cast<const float4*>(a.d_z + G * dout + 4 * q);
           vz = *reinterpret_cast<const float4*>(a.z + G * dout + 4 * q);
         }
-        *reinterpret_cast<float4*>(dz_s + rr * dout + 4 * q) = vd;
+        *reinterpret_cast<float4*>(dz_s + rr * dzp + 4 * q) = vd;
         *reinterpret_cast<float4*>(z_s + rr * dout + 4 * q) = vz;
       }
     } else {
@@ -936,7 +951,34 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
       }
     }
     __syncthreads();
-    if (T4) {
+    if (MMA) {
+      // dW[c][j] += sum_rr h[rr][c] dz[rr][j]: M = c (MB blocks of 16), N = j
+      // (warp = n-block of 8), K = the tile's 32 rows; 3xTF32 on HMMA
+      const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, nb = threadIdx.x >> 5;
+#pragma unroll
+      for (int k0 = 0; k0 < QTR; k0 += 8) {
+        const float bx0 = dz_s[(k0 + t) * dzp + nb * 8 + g], bx1 = dz_s[(k0 + t + 4) * dzp + nb * 8 + g];
+        const uint32_t bh0 = tf32_of(bx0), bh1 = tf32_of(bx1);
+        const uint32_t bl0 = tf32_of(bx0 - __uint_as_float(bh0)), bl1 = tf32_of(bx1 - __uint_as_float(bh1));
+#pragma unroll
+        for (int mb = 0; mb < 8; ++mb) {
+          if (mb >= MB) break;
+          const float* hr = h_s + mb * 16 + g;
+          const float x[4] = {hr[(k0 + t) * wp], hr[(k0 + t) * wp + 8], hr[(k0 + t + 4) * wp],
+                              hr[(k0 + t + 4) * wp + 8]};
+          uint32_t ah[4], al[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ah[u] = tf32_of(x[u]);
+            al[u] = tf32_of(x[u] - __uint_as_float(ah[u]));
+          }
+          float (&c4)[4] = *reinterpret_cast<float (*)[4]>(acc + 4 * mb);
+          mma_tf32(c4, al, bh0, bh1);
+          mma_tf32(c4, ah, bl0, bl1);
+          mma_tf32(c4, ah, bh0, bh1);
+        }
+      }
+    } else if (T4) {
 #pragma unroll
       for (int s2 = 0; s2 < QMAXQ / 4 * 2; ++s2) {  // up to 4 tiles of 16 per thread
         const int slot = threadIdx.x + 256 * s2;
@@ -946,7 +988,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
 #pragma unroll 4
           for (int rr = 0; rr < QTR; ++rr) {
             const float4 a4 = *reinterpret_cast<const float4*>(h_s + rr * wp + 4 * cg);
-            const float4 g4 = *reinterpret_cast<const float4*>(dz_s + rr * dout + 4 * jg);
+            const float4 g4 = *reinterpret_cast<const float4*>(dz_s + rr * dzp + 4 * jg);
             const float av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -982,7 +1024,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
       for (int idx = threadIdx.x; idx < nrow * w; idx += blockDim.x) {
         const int rr = idx / w, c = idx - rr * w;
         float sacc = 0.f;
-        const float* dzr = dz_s + rr * dout;
+        const float* dzr = dz_s + rr * dzp;
 #pragma unroll 8
         for (int j = 0; j < dout; ++j) sacc = fmaf(dzr[j], Wt_s[j * wt + c], sacc);
         a.d_prev[(int64_t)(own0 + tile * QTR + rr) * w + c] = sacc;
@@ -991,7 +1033,23 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
   }
   const int64_t ntot = (int64_t)w * dout + 2 * dout;
   float* out = a.partial + (int64_t)blockIdx.x * ntot;
-  if (T4) {
+  if (MMA) {
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, nb = threadIdx.x >> 5;
+#pragma unroll
+    for (int mb = 0; mb < 8; ++mb) {
+      if (mb >= MB) break;
+      const float* c4 = acc + 4 * mb;
+      const int m0 = mb * 16 + g, n0 = nb * 8 + 2 * t;
+      if (m0 < w) {
+        out[m0 * dout + n0] = c4[0];
+        out[m0 * dout + n0 + 1] = c4[1];
+      }
+      if (m0 + 8 < w) {
+        out[(m0 + 8) * dout + n0] = c4[2];
+        out[(m0 + 8) * dout + n0 + 1] = c4[3];
+      }
+    }
+  } else if (T4) {
 #pragma unroll
     for (int s2 = 0; s2 < 2; ++s2) {
       const int slot = threadIdx.x + 256 * s2;
@@ -1405,12 +1463,21 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
     }
     return SG_OK;
   }
-  if (t4) {
-    SG_CUDA(allow_max_smem<k_gat_bwd_param<true>>());
-    ::sg::launch(k_gat_bwd_param<true>, nblocks, 256, smem, st, meta, a);
+  static const bool use_mma = !getenv("SG_NO_MMA");
+  if (use_mma && dout == 64 && w % 4 == 0 && w > 32 && w <= 128) {
+    const int MB = (w + 15) / 16;
+    int wp = (16 * MB + 8 + 31) / 32 * 32 - 8;
+    if (wp < 16 * MB) wp += 32;
+    const size_t smem_m = sizeof(float) * ((size_t)QTR * (dout + 8) + (size_t)QTR * dout + (size_t)dout * (w + 1) +
+                                           (size_t)QTR * wp + 2 * (size_t)QTR * heads + QTR);
+    SG_CUDA(allow_max_smem<k_gat_bwd_param<2>>());
+    ::sg::launch(k_gat_bwd_param<2>, nblocks, 256, smem_m, st, meta, a);
+  } else if (t4) {
+    SG_CUDA(allow_max_smem<k_gat_bwd_param<1>>());
+    ::sg::launch(k_gat_bwd_param<1>, nblocks, 256, smem, st, meta, a);
   } else {
-    SG_CUDA(allow_max_smem<k_gat_bwd_param<false>>());
-    ::sg::launch(k_gat_bwd_param<false>, nblocks, 256, smem, st, meta, a);
+    SG_CUDA(allow_max_smem<k_gat_bwd_param<0>>());
+    ::sg::launch(k_gat_bwd_param<0>, nblocks, 256, smem, st, meta, a);
   }
   SG_CHECK_LAUNCH("k_gat_bwd_param");
   return SG_OK;

@@ -99,8 +99,8 @@ def test_gat_loss_curve_50_steps():
     assert diff.max() < LOSS_TOL, diff.max()
 
 
-@pytest.mark.parametrize("g", [1, 2, 4])
-def test_gat_multihead_matches_composed_oracle(g):
+@pytest.mark.parametrize("g,F", [(1, 24), (2, 24), (4, 24), (1, 100), (2, 100)])
+def test_gat_multihead_matches_composed_oracle(g, F):
     """C3's 4-head GAT: parity by per-head composition of the reference layer
     (SURVEY §8(a) row 11): split run summed over devices == composed single-
     device oracle."""
@@ -108,7 +108,7 @@ def test_gat_multihead_matches_composed_oracle(g):
     from oracle.multihead_oracle import multihead_run
     graph, pm, sample, cache = random_partition_case(80 + g, n=5000, m=60000, g=g, batch=96,
                                                      fanouts=(6, 5, 4), cache_frac=0.3)
-    F, H, dh, C = 24, 4, 16, 7
+    H, dh, C = 4, 16, 7  # F = 100: the C3 layer-1 shape (tensor-core projection / weight gradient)
     feats = sg.synthetic_features(graph.num_vertices, F, seed=3)
     labels = sg.synthetic_labels(graph.num_vertices, C, seed=4)
     params = sg.init_params("gat", F, dh, C, 3, seed=5, heads=H)
