@@ -32,7 +32,7 @@ from paper_2303_13775_b200.sampling import epoch_batches, sample_microbatches, s
 from paper_2303_13775_b200.scheduler import DeviceSplit, split_cost_packed, split_minibatch
 
 DEBUG_CHECK_FINITE = False
-NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions
+NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions (measured best vs 592, 888)
 # layers with at least this many edges (capacity) take the load-balanced
 # transposed SpMM (tspmm.cu); below it hub rows are short (max out-degree
 # ~25-125 at C2 layers 2-3) and the single-kernel row-per-warp path is faster
