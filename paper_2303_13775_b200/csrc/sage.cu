@@ -8,6 +8,9 @@
 //                       source-row loads (128-bit) back to back, 8 in flight.
 //                       Reference rows are packed straight into the
 //                       push-to-owner send buffer (fused pack epilogue).
+//   sg_sage_fused_fwd / sg_sage_combine_fwd
+//                       one kernel per layer (k_sage_layer): aggregation (g = 1)
+//                       or owner combine (g > 1), mean, and the GEMM from smem
 //   sg_sage_update      owner combine in ascending sender order + mean +
 //                       h_self@W_self + mean@W_neigh + b + ReLU (:197-226);
 //                       FP32 FFMA, weights in smem, each thread a 1x4 output
@@ -208,12 +211,9 @@ int launch_agg(const SgMeta* meta, const AggArgs& a, int64_t max_rows, cudaStrea
   return SG_OK;
 }
 
-// ---------------------------------------------------------------- fused forward (g == 1)
-// Single-device split: no row has remote contributions, so the update runs in
-// the aggregation kernel. The row team holds the row sums (lanes x float4);
-// each lane forms partial dot products for all dout outputs against the
-// TRANSPOSED weights in smem (conflict-free LDS.128), then a recursive-halving
-// xor reduction leaves each output on one lane (fixed order: deterministic).
+// ---------------------------------------------------------------- one-kernel layer arguments
+// Single-device split (no row has remote contributions) or the owner side after
+// the push-to-owner round: aggregation (or combine) + update in k_sage_layer.
 struct FusedArgs {
   int l, d, w, dout, final_;
   int64_t eoff_li, rbase_li, voff_l;
@@ -240,99 +240,6 @@ struct FusedArgs {
   int hst;  // row stride of h_prev (k_sage_layer: a padded feature table is read in whole lines)
 };
 
-template <int LPR, int EG>
-__global__ void __launch_bounds__(256) k_sage_agg_mean(const SgMeta* __restrict__ meta, FusedArgs a) {
-  SG_PDL_ENTRY();
-  constexpr int RL = LPR * EG;
-  constexpr int RPW = 32 / RL;
-  const int w = a.w;
-  const int l = a.l, d = a.d;
-  const int n_own = meta->n_own[l][d];
-  const int own0 = meta->own_off[l][d];
-  const int prev0 = meta->own_off[l - 1][d];
-  const int64_t rb = a.rbase_li + own0;
-  const int lane = threadIdx.x & 31;
-  const int team = lane / RL, tl = lane % RL, eg = tl / LPR, lr = tl % LPR;
-  const unsigned tmask = (RL == 32) ? 0xffffffffu : (((1u << RL) - 1u) << (team * RL));
-  const int col = lr * 4;
-  const bool colok = col < w;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t q = gw * RPW + team; q < n_own; q += nw * RPW) {
-    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
-    const int64_t G = own0 + q;
-    int rself = prev0 + a.selfrow[a.voff_l + G];
-    if (a.src_row) rself = a.src_row[rself];
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int jb = b; jb < e; jb += RL) {
-      const int j = jb + tl;
-      int r = 0;
-      if (j < e) {
-        r = prev0 + a.lsrc[a.eoff_li + j];
-        if (a.src_row) r = a.src_row[r];
-      }
-      const int cnt = min(RL, e - jb);
-      const int rounds = (cnt + EG - 1) / EG;
-      constexpr int UN = 4;  // loads in flight per lane
-      int kk = 0;
-      for (; kk + UN <= rounds; kk += UN) {
-        int rr[UN];
-        bool ok[UN];
-#pragma unroll
-        for (int u = 0; u < UN; ++u) {
-          const int k = (kk + u) * EG + eg;
-          rr[u] = __shfl_sync(tmask, r, k < RL ? k : RL - 1, RL);
-          ok[u] = k < cnt;
-        }
-        if (colok) {
-          float4 v[UN];
-#pragma unroll
-          for (int u = 0; u < UN; ++u)
-            v[u] = ok[u] ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr[u] * w + col))
-                         : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-          for (int u = 0; u < UN; ++u) {
-            acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w;
-          }
-        }
-      }
-      for (; kk < rounds; ++kk) {
-        const int k = kk * EG + eg;
-        const int r0 = __shfl_sync(tmask, r, k < RL ? k : RL - 1, RL);
-        if (k < cnt && colok) {
-          const float4 v = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)r0 * w + col));
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-      }
-    }
-#pragma unroll
-    for (int o = LPR; o < RL; o <<= 1) {
-      acc.x += __shfl_xor_sync(tmask, acc.x, o, RL);
-      acc.y += __shfl_xor_sync(tmask, acc.y, o, RL);
-      acc.z += __shfl_xor_sync(tmask, acc.z, o, RL);
-      acc.w += __shfl_xor_sync(tmask, acc.w, o, RL);
-    }
-    const float cntf = (float)(e - b);
-    const float inv = 1.0f / cntf;
-    const float4 mn = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-    const float4 hv = colok ? __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rself * w + col))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (eg == 0 && colok) {
-      *reinterpret_cast<float4*>(a.mean + G * w + col) = mn;
-      *reinterpret_cast<float4*>(a.hs + G * w + col) = hv;
-    }
-    if (tl == 0) a.counts[G] = cntf;
-  }
-}
-
-template <int LPR, int EG>
-int launch_agg_mean(const SgMeta* meta, const FusedArgs& a, int64_t max_rows, cudaStream_t st) {
-  constexpr int RPB = 8 * (32 / (LPR * EG));
-  const int grid = clamp_grid(div_up(max_rows, RPB), kSMs * 8);
-  ::sg::launch(k_sage_agg_mean<LPR, EG>, grid, 256, 0, st, meta, a);
-  SG_CHECK_LAUNCH("k_sage_agg_mean");
-  return SG_OK;
-}
 
 // ---------------------------------------------------------------- tiled dense transforms
 // h = act(hs @ W_self + mean @ W_neigh + b) for the owned rows: a register-
@@ -1460,17 +1367,10 @@ extern "C" int sg_sage_fused_fwd(const void* split_ws, const SgSplitLayout* lay,
   SG_REQUIRE(a.hst >= w && a.hst % 4 == 0 && a.hst <= 128 && (a.hst == w || w > 64),
              "sage_fused_fwd: h_stride must be a multiple of 4, >= w, <= 128 (padded rows need w > 64)");
   cudaStream_t st = (cudaStream_t)stream;
-  // wide layers: one kernel (8 loads in flight per lane, 8-row tiles: one row
-  // per warp, 4 CTAs/SM; measured best of UN 8/16 x RPW 1/2/4 x 2..8 CTAs/SM)
-  if (w > 64) return launch_layer<8, 1, 4>(meta, a, max_rows, st);
-  int rc;
-  if (w <= 16) rc = launch_agg_mean<4, 4>(meta, a, max_rows, st);
-  else if (w <= 32) rc = launch_agg_mean<8, 4>(meta, a, max_rows, st);
-  else if (w <= 64) rc = launch_agg_mean<16, 2>(meta, a, max_rows, st);
-  else rc = launch_agg_mean<32, 1>(meta, a, max_rows, st);
-  if (rc) return rc;
-  LinArgs la{l, d, w, dout, final_layer, hs, mean, w_self, w_neigh, bias, h};
-  return launch_linear(meta, la, max_rows, st);
+  // one kernel for every width (8 loads in flight per lane, 8-row tiles: one
+  // row per warp, 4 CTAs/SM; measured best of UN 8/16 x RPW 1/2/4 x 2..8
+  // CTAs/SM; for narrow rows level with aggregation + a separate GEMM)
+  return launch_layer<8, 1, 4>(meta, a, max_rows, st);
 }
 
 extern "C" int sg_sage_combine_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
