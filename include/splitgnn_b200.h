@@ -426,6 +426,19 @@ int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indices, int64_
                   int64_t max_dst,
                   int64_t max_edges, int32_t* V, int32_t* esrc, int32_t* edst, int64_t* sizes, void* ws,
                   int32_t* err, void* stream);
+/* ---- balanced k-way partitioning (partition.py:236-349) --------------------
+ * sg_partition_cut: directed arcs whose endpoints lie in different parts.
+ * sg_partition_round: one parallel refinement round on the symmetrised graph
+ * (in-CSR + out-CSR, g <= 16 parts, part sizes <= cap): seeded half of the
+ * vertices propose their best strictly positive gain move (lowest part on
+ * ties), admitted per target in descending gain within the cap; updates part
+ * and sizes; ws >= 8n + 4 * 16 * 65 bytes; *moved_out = moves (device). */
+int sg_partition_cut(const int64_t* row_offsets, const int32_t* col_indices, int64_t n, const int32_t* part,
+                     unsigned long long* cut_out, void* stream);
+int sg_partition_round(const int64_t* row_offsets, const int32_t* col_indices, const int64_t* out_offsets,
+                       const int32_t* out_indices, int64_t n, int32_t g, int64_t cap, uint64_t seed,
+                       int32_t round, int32_t* part, int64_t* sizes, void* ws, unsigned long long* moved_out,
+                       void* stream);
 /* sg_reduce_partials with the SGD step fused (single device, nothing to
  * all-reduce): jobs are 6 int64 per job {partials, nblocks, n, out, param,
  * n_sgd}; the first n_sgd summed columns g also update param: p -= scale*g

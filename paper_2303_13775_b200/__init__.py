@@ -20,9 +20,12 @@ from paper_2303_13775_b200.partition import (
     CacheState,
     PartitionMap,
     build_cache,
+    cut_size,
     full_cache,
     max_part_size,
+    partition_graph,
     range_partition,
+    refine_assignment,
 )
 from paper_2303_13775_b200.sampling import (GpuSampler, MiniBatchSample, NativeSampler, epoch_batches,
                                             sample_microbatches, sample_minibatch)
