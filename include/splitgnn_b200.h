@@ -194,6 +194,14 @@ int sg_sage_agg_fwd_perm(const void* split_ws, const SgSplitLayout* lay, int32_t
                          float* sums,
                          float* counts, float* sendbuf, int32_t send_stride,
                          const int32_t* dperm, int64_t max_rows, void* stream);
+/* sg_sage_agg_fwd with the push-to-owner fused into the epilogue (peer
+ * transport, one rank per GPU): reference rows go straight into the owners'
+ * peer-mapped receive buffers peer_recv[0..g) (receive-slot layout, row stride
+ * send_stride) at xfer[pair slot]; dperm may be null. */
+int sg_sage_agg_fwd_peer(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                         const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride,
+                         float* sums, float* counts, const int64_t* peer_recv, int32_t send_stride,
+                         const int32_t* dperm, int64_t max_rows, void* stream);
 /* Single-device split (g = 1: no reference rows, no remote contributions):
  * aggregation + mean + both GEMVs + bias + ReLU in one kernel
  * (engine.py:180-226 with the exchange vacuous). Also writes mean, counts and

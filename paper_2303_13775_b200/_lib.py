@@ -88,6 +88,7 @@ _SIGS = {
     "sg_sage_final_fused": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
                                   vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i64, vp]),
     "sg_set_pdl": (None, [i32]),
+    "sg_sage_agg_fwd_peer": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32, vp, i64, vp]),
     "sg_partition_cut": (i32, [vp, vp, i64, vp, vp, vp]),
     "sg_partition_round": (i32, [vp, vp, vp, vp, i64, i32, i64, u64, i32, vp, vp, vp, vp, vp]),
     "sg_gpu_sampler_ws_bytes": (i64, [i64, i64, i64, i32]),

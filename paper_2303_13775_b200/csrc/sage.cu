@@ -89,6 +89,12 @@ struct AggArgs {
   float* sums;
   float* counts;
   float* sendbuf;
+  // peer transport (one rank per GPU): reference rows go straight into the
+  // owners' mapped receive buffers at xfer[pair slot] (push fused into the
+  // aggregation epilogue); peer[0] == 0 -> write sendbuf
+  int g;
+  const int32_t* xfer;
+  struct { int64_t p[SG_MAXG]; } peer;
 };
 
 // A row "team" of RL = LPR*EG lanes: LPR lanes cover the row width (VEC floats
@@ -189,7 +195,13 @@ __global__ void __launch_bounds__(256) k_sage_agg(const SgMeta* __restrict__ met
       if (lr == 0) a.counts[own0 + q] = cntf;
     } else {
       const int slot = a.sendpos[a.pbase_l + ref0 + (q - n_own)];
-      float* out = a.sendbuf + (int64_t)slot * a.stride;
+      float* out;
+      if (a.peer.p[0]) {  // store over NVLink into the owner's receive slot
+        const int rs = a.xfer[slot];
+        out = (float*)a.peer.p[find_bucket(meta->recv_off[l], a.g, rs)] + (int64_t)rs * a.stride;
+      } else {
+        out = a.sendbuf + (int64_t)slot * a.stride;
+      }
 #pragma unroll
       for (int c = 0; c < NCH; ++c) {
         const int col = (c * LPR + lr) * VEC;
@@ -1297,7 +1309,7 @@ int dispatch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaS
 static int agg_common(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                       const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride, float* sums,
                       float* counts, float* sendbuf, int32_t send_stride, const int32_t* dperm,
-                      int64_t max_rows, void* stream) {
+                      int64_t max_rows, void* stream, const int64_t* peer_recv = nullptr) {
   SG_REQUIRE(split_ws && lay, "sage_agg_fwd: null workspace");
   SPLIT_PTRS
   SG_REQUIRE(l >= 1 && l <= y.L && d >= 0 && d < y.g, "sage_agg_fwd: bad layer/device");
@@ -1323,7 +1335,27 @@ static int agg_common(const void* split_ws, const SgSplitLayout* lay, int32_t l,
   a.sums = sums;
   a.counts = counts;
   a.sendbuf = sendbuf;
+  a.g = y.g;
+  if (peer_recv) {
+    SG_REQUIRE(y.g > 1, "sage_agg_fwd_peer: needs g > 1");
+    a.xfer = I32(y.o_xfer) + y.pbase[l];
+    for (int i = 0; i < y.g; ++i) a.peer.p[i] = peer_recv[i];
+    SG_REQUIRE(a.peer.p[0] != 0, "sage_agg_fwd_peer: null peer buffer");
+  }
   return dispatch_agg(meta, a, max_rows, (cudaStream_t)stream);
+}
+
+// sg_sage_agg_fwd with the push-to-owner fused into the epilogue: reference
+// rows are stored straight into the owners' receive buffers (peer_recv: the g
+// peer-mapped receive buffers of this round, receive-slot layout, row stride
+// send_stride) instead of a local send buffer. dperm may be null.
+extern "C" int sg_sage_agg_fwd_peer(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
+                                    const float* h_prev, const int32_t* src_row, int32_t w, int32_t h_stride,
+                                    float* sums, float* counts, const int64_t* peer_recv, int32_t send_stride,
+                                    const int32_t* dperm, int64_t max_rows, void* stream) {
+  SG_REQUIRE(peer_recv, "sage_agg_fwd_peer: null peer table");
+  return agg_common(split_ws, lay, l, d, h_prev, src_row, w, h_stride, sums, counts, nullptr, send_stride, dperm,
+                    max_rows, stream, peer_recv);
 }
 
 extern "C" int sg_sage_agg_fwd(const void* split_ws, const SgSplitLayout* lay, int32_t l,

@@ -295,12 +295,18 @@ class SplitStep:
             counts = _f32(nV, device=self.dev)
             SW = _r4(w + 1)
             P = ds.pair_bound(l)
-            send = _f32(P, SW, device=self.dev)
             recv = self._xbuf(P, SW)
+            peer_push = hasattr(self.transport, "peers_of") and self.g > 1 and P > 0
+            send = None if peer_push else _f32(P, SW, device=self.dev)
             self._ev(f"agg{l}_start")
             self._ev(f"ph:agg{l}:s")
             for d in self.devices:
-                if dperm is None:
+                if peer_push:  # push-to-owner fused into the aggregation epilogue
+                    _lib.call("sg_sage_agg_fwd_peer", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
+                              _lib.ptr(src_row), w, hst, _lib.ptr(sums), _lib.ptr(counts),
+                              _lib.ptr(self.transport.peers_of(recv)), SW,
+                              _lib.ptr(dperm[d][0]) if dperm is not None else None, self.n_rows(l, d), st)
+                elif dperm is None:
                     _lib.call("sg_sage_agg_fwd", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev),
                               _lib.ptr(src_row), w, hst, _lib.ptr(sums), _lib.ptr(counts), _lib.ptr(send),
                               SW, self.n_rows(l, d), st)
@@ -311,7 +317,10 @@ class SplitStep:
             self._ev(f"agg{l}_end")
             self._ev(f"ph:agg{l}:e")
             if self.g > 1 and P > 0:
-                self.transport.to_owner(ds, l, send, recv, SW)
+                if peer_push:
+                    self.transport.to_owner(ds, l, None, recv, SW, pushed=True)
+                else:
+                    self.transport.to_owner(ds, l, send, recv, SW)
                 if self.meta is not None:
                     self.wire_bytes += int(self.meta.npairs[l]) * SW * 4
             if self._combine_ok(w, dout, SW):

@@ -183,11 +183,21 @@ class PeerTransport:
         _lib.call("sg_peer_wait", _lib.ptr(self.flags), self.rank, self.world, k, _lib.ptr(self.epoch),
                   _lib.ptr(self.timeout), st)
 
-    def to_owner(self, dsplit, l, send, recv, stride):
-        """Push this rank's pair-slot rows into the owners' receive buffers."""
+    def peers_of(self, buf):
+        """The g peer-mapped pointers of the round buffer `buf` (int64 array),
+        for kernels that store into the owners' buffers themselves."""
+        for t, peers in self._bufs.values():
+            if t.data_ptr() == buf.data_ptr():
+                return peers
+        raise RuntimeError("buffer was not requested from this transport")
+
+    def to_owner(self, dsplit, l, send, recv, stride, pushed=False):
+        """Push this rank's pair-slot rows into the owners' receive buffers
+        (pushed=True: the producing kernel already stored them there)."""
         k, peers = self._round(recv)
-        _lib.call("sg_peer_exchange", _lib.ptr(dsplit.ws), dsplit.lay, l, self.rank, 1, _lib.ptr(send),
-                  int(stride), _lib.ptr(peers), _lib.stream_ptr())
+        if not pushed:
+            _lib.call("sg_peer_exchange", _lib.ptr(dsplit.ws), dsplit.lay, l, self.rank, 1, _lib.ptr(send),
+                      int(stride), _lib.ptr(peers), _lib.stream_ptr())
         self._signal_wait(k)
 
     def from_owner(self, dsplit, l, send_recv_layout, recv_pair_layout, stride):
