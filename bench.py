@@ -65,6 +65,18 @@ LR = 0.1
 GRAPH_SEED, FEAT_SEED, LABEL_SEED, TRAIN_SEED, RUN_SEED = 0, 1, 2, 3, 0
 
 
+def _trace(what, x):
+    """SG_BENCH_TRACE=1: checksums of intermediate state on stderr (determinism checks)."""
+    if os.environ.get("SG_BENCH_TRACE") != "1":
+        return
+    if hasattr(x, "detach"):
+        a = x.detach().float().cpu().numpy()
+        bad = np.flatnonzero(~np.isfinite(a))
+        x = (float(np.abs(a).sum()), int(a.view(np.uint32).astype(np.uint64).sum() % (1 << 32)), len(a),
+             f"non-finite {len(bad)} at {bad[:6].tolist()}")
+    print(f"[trace] {what}: {x}", file=sys.stderr, flush=True)
+
+
 def select_config(name):
     global CFG_NAME, KIND, HEADS, N_NODES, N_EDGES, FEAT, CLASSES, TRAIN_FRAC, P_LOCAL, DESC
     c = CONFIGS[name]
@@ -419,6 +431,7 @@ def main():
                                     dev, record_events=record_events)
         cs = make_step(LR / args.batch, record_events="agg")
         cs.capture(samples[0])                     # eager warm-up step 0 + capture
+        _trace("params after capture", dp.flat)
         agg_in_graph = True
         for i in range(1, args.warmup):
             cs.run(samples[i])
@@ -443,6 +456,7 @@ def main():
                     agg_in_graph = False
             barrier()
             t_wall = time.perf_counter() - t_wall
+        _trace("params after timed", dp.flat)
         # diagnostic (untimed): a second capture with an event around every phase
         diag = make_step(0.0, record_events="all")
         diag.capture(samples[0])
@@ -468,6 +482,7 @@ def main():
         my_ms = sum(step_ms)
         # ---- end to end: host sample -> pinned -> H2D -> graph -> D2H loss ----------
         barrier()
+        _trace("params before e2e", dp.flat)
         losses = []
         h2d = 0
         e0 = torch.cuda.Event(enable_timing=True)
@@ -484,6 +499,7 @@ def main():
         t_e2e = time.perf_counter()
         losses, h2d, d2h = ce.run_pipelined(pinned)
         t_e2e = time.perf_counter() - t_e2e
+        _trace("e2e losses", losses)
         e1.record()
         barrier()
         e2e_ms = e0.elapsed_time(e1)

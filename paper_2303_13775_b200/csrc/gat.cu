@@ -178,16 +178,20 @@ __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ 
 
 // ---------------------------------------------------------------- tensor-core projection
 // z = h W on the tensor pipe with FP32-level accuracy: 3xTF32 (x = hi + lo,
-// hi = tf32(x), lo = tf32(x - hi); x*y ~= lo*hi + hi*lo + hi*hi, the dropped
-// lo*lo term is ~2^-22 relative) on warp-level mma.sync m16n8k8 (HMMA),
-// FP32 accumulation. A 32-row tile of gathered rows sits row-major in smem
-// (pitch K+4: conflict-free fragment loads), W is split into hi/lo once per
-// CTA (pitch D+8). Warp (mb, cg): rows 16mb..16mb+15, columns cg*D/4 ...
+// split_tf32; x*y ~= lo*hi + hi*lo + hi*hi, the dropped lo*lo term is
+// ~2^-20 relative) on warp-level mma.sync m16n8k8 (HMMA), FP32
+// accumulation. A 32-row tile of gathered rows sits row-major in smem
+// (pitch K+4: conflict-free fragment loads), W in FP32 (pitch D+8), both
+// split into hi/lo as the fragments are loaded. Warp (mb, cg): rows 16mb..16mb+15, columns cg*D/4 ...
 // Then the per-head scores exactly as the FFMA kernel.
-__device__ __forceinline__ uint32_t tf32_of(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
+// hi = x with the low 13 mantissa bits cleared (a TF32 value, exact split by
+// truncation), lo = x - hi (exact in FP32); lo goes to the MMA as raw FP32
+// bits, which the tensor pipe reads as TF32 (low bits ignored): the dropped
+// part is < 2^-10 |lo| <= 2^-20 |x|. Two instructions instead of the
+// multi-instruction cvt.rna.tf32 sequence (sm_100a has no single-op form).
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
 }
 __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -271,15 +275,15 @@ __global__ void __launch_bounds__(256) k_gat_project_mma(const SgMeta* __restric
       uint32_t ah[4], al[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        ah[u] = tf32_of(x[u]);
-        al[u] = tf32_of(x[u] - __uint_as_float(ah[u]));
+        split_tf32(x[u], ah[u], al[u]);
       }
 #pragma unroll
       for (int jj = 0; jj < NT8; ++jj) {
         const int n0 = cg * (D / 4) + 8 * jj;
         const float w0 = W_s[(k0 + t) * DP + n0 + g], w1 = W_s[(k0 + t + 4) * DP + n0 + g];
-        const uint32_t bh0 = tf32_of(w0), bh1 = tf32_of(w1);
-        const uint32_t bl0 = tf32_of(w0 - __uint_as_float(bh0)), bl1 = tf32_of(w1 - __uint_as_float(bh1));
+        uint32_t bh0, bh1, bl0, bl1;
+        split_tf32(w0, bh0, bl0);
+        split_tf32(w1, bh1, bl1);
         mma_tf32(acc[jj], al, bh0, bh1);
         mma_tf32(acc[jj], ah, bl0, bl1);
         mma_tf32(acc[jj], ah, bh0, bh1);
@@ -958,8 +962,9 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
 #pragma unroll
       for (int k0 = 0; k0 < QTR; k0 += 8) {
         const float bx0 = dz_s[(k0 + t) * dzp + nb * 8 + g], bx1 = dz_s[(k0 + t + 4) * dzp + nb * 8 + g];
-        const uint32_t bh0 = tf32_of(bx0), bh1 = tf32_of(bx1);
-        const uint32_t bl0 = tf32_of(bx0 - __uint_as_float(bh0)), bl1 = tf32_of(bx1 - __uint_as_float(bh1));
+        uint32_t bh0, bh1, bl0, bl1;
+        split_tf32(bx0, bh0, bl0);
+        split_tf32(bx1, bh1, bl1);
 #pragma unroll
         for (int mb = 0; mb < 8; ++mb) {
           if (mb >= MB) break;
@@ -969,8 +974,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
           uint32_t ah[4], al[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            ah[u] = tf32_of(x[u]);
-            al[u] = tf32_of(x[u] - __uint_as_float(ah[u]));
+            split_tf32(x[u], ah[u], al[u]);
           }
           float (&c4)[4] = *reinterpret_cast<float (*)[4]>(acc + 4 * mb);
           mma_tf32(c4, al, bh0, bh1);

@@ -1063,11 +1063,24 @@ class StaticSample:
 
     def load(self, sample):
         """Stage the sample into pinned memory and copy it to the device
-        buffer (async, on the current stream)."""
+        buffer (async, on the current stream). Two pinned staging slots, each
+        reused only after its previous H2D copy has completed (the copy is
+        asynchronous: packing the next sample into a slot whose copy is still
+        queued behind a running step would corrupt that step's input)."""
         if self.hbuf is None:
-            self.hbuf = torch.zeros(self.words, dtype=torch.int32).pin_memory()
-        used = self.pack(sample, self.hbuf.numpy())
-        self.buf[:used].copy_(self.hbuf[:used], non_blocking=True)
+            self.hbuf = [torch.zeros(self.words, dtype=torch.int32).pin_memory() for _ in range(2)]
+            self.hev = [None, None]
+            self.slot = 0
+        k = self.slot
+        self.slot ^= 1
+        if self.hev[k] is not None:
+            self.hev[k].synchronize()
+        hb = self.hbuf[k]
+        used = self.pack(sample, hb.numpy())
+        self.buf[:used].copy_(hb[:used], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.hev[k] = ev
         self.bytes_h2d = 4 * used
         return self.bytes_h2d
 
@@ -1246,7 +1259,9 @@ class SampledCapturedStep(CapturedStep):
         self.fanouts = [int(f) for f in fanouts]
         self.batch = int(batch)
         self.tgt = torch.zeros(self.batch + 1, dtype=torch.int64, device=self.dev)  # targets | seed
-        self.htgt = torch.zeros(self.batch + 1, dtype=torch.int64).pin_memory()
+        self.htgt = [torch.zeros(self.batch + 1, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self.tev = [None, None]
+        self.tslot = 0
 
     def _body(self):
         inp = self.inp
@@ -1258,10 +1273,17 @@ class SampledCapturedStep(CapturedStep):
         t = np.asarray(targets, dtype=np.int64)
         if len(t) != self.batch:
             raise ValueError(f"the captured step samples exactly {self.batch} targets")
-        h = self.htgt.numpy()
+        k = self.tslot  # two pinned slots, each reused after its copy completed (see StaticSample.load)
+        self.tslot ^= 1
+        if self.tev[k] is not None:
+            self.tev[k].synchronize()
+        h = self.htgt[k].numpy()
         h[:self.batch] = t
         h[self.batch] = np.int64(np.uint64(int(seed) & (2**64 - 1)).view(np.int64))
-        self.tgt.copy_(self.htgt, non_blocking=True)
+        self.tgt.copy_(self.htgt[k], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.tev[k] = ev
 
     def capture_targets(self, targets, seed):
         self.load_targets(targets, seed)
