@@ -337,6 +337,9 @@ int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, int32_t l, in
                    const float* dt_loc, const float* dt_recv, const float* a_src,
                    const float* a_dst, float* d_z, float* ds, float* dt_tot, int64_t max_rows,
                    void* stream);
+/* Partial slices (CTAs) sg_gat_bwd_param wants for `rows` rows: the caller
+ * sizes `partial` as nblocks x (w*dout + 2*dout) floats with this count. */
+int32_t sg_gat_bwd_param_blocks(int32_t w, int32_t dout, int32_t heads, int64_t rows);
 int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                      const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
                      int32_t heads, const float* z, const float* d_z, const float* ds,

@@ -129,6 +129,7 @@ _SIGS = {
                              vp, vp, vp, i64, vp]),
     "sg_gat_bwd_src": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, vp, vp, vp, i64, vp, vp, vp, vp,
                              i32, vp, vp, vp, vp, vp, vp, vp, i64, vp]),
+    "sg_gat_bwd_param_blocks": (i32, [i32, i32, i32, i64]),
     "sg_gat_bwd_param": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp,
                                vp, i32, vp, i64, vp]),
     "sg_xfer_to_owner": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, vp]),

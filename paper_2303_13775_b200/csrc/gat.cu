@@ -846,22 +846,14 @@ struct BParamArgs {
 
 // T4 (w % 4 == 0 and dout % 4 == 0): thread slot (cg, jg) owns a 4x4 dW tile,
 // per row 2 LDS.128 + 16 FFMA; otherwise one scalar slot per (c, j).
-template <int MODE>  // 0 scalar FFMA, 1 4x4 FFMA tiles, 2 3xTF32 HMMA (dout == 64)
+template <int MODE>  // 0 scalar FFMA, 1 4x4 FFMA tiles (dout == 64 runs k_gat_wgrad_mma)
 __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict__ meta, BParamArgs a) {
   SG_PDL_ENTRY();
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, H = a.heads, dh = dout / H;
   constexpr bool T4 = MODE >= 1;
-  constexpr bool MMA = MODE == 2;
-  const int MB = (w + 15) / 16;        // MMA: 16-row blocks of dW (M = w padded)
-  // h row stride: float4-aligned for T4; for MMA >= 16*MB (zero padding) and
-  // == 24 mod 32 (conflict-free A fragments)
-  int wp = T4 ? w + 4 : w + 1;
-  if (MMA) {
-    wp = (16 * MB + 8 + 31) / 32 * 32 - 8;
-    if (wp < 16 * MB) wp += 32;
-  }
-  const int dzp = MMA ? dout + 8 : dout;  // d_z row stride (conflict-free B fragments)
+  const int wp = T4 ? w + 4 : w + 1;  // h row stride (float4-aligned for T4)
+  const int dzp = dout;
   const int wt = w + 1;               // W^T row stride (d_prev: lanes run along c)
   float* dz_s = smem;               // [QTR][dzp]
   float* Wt_s = dz_s + QTR * dzp;   // [dout][w+1] = W^T (for d_prev)
@@ -874,11 +866,6 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
       Wt_s[j * wt + c] = a.W[i];
-    }
-  if (MMA)  // zero padding columns w..wp of the h tile (never written by the row loads)
-    for (int i = threadIdx.x; i < QTR * (wp - w); i += blockDim.x) {
-      const int rr = i / (wp - w);
-      h_s[rr * wp + w + (i - rr * (wp - w))] = 0.f;
     }
   const int l = a.l, d = a.d;
   const int n = meta->n_own[l - 1][d];
@@ -955,34 +942,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
       }
     }
     __syncthreads();
-    if (MMA) {
-      // dW[c][j] += sum_rr h[rr][c] dz[rr][j]: M = c (MB blocks of 16), N = j
-      // (warp = n-block of 8), K = the tile's 32 rows; 3xTF32 on HMMA
-      const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, nb = threadIdx.x >> 5;
-#pragma unroll
-      for (int k0 = 0; k0 < QTR; k0 += 8) {
-        const float bx0 = dz_s[(k0 + t) * dzp + nb * 8 + g], bx1 = dz_s[(k0 + t + 4) * dzp + nb * 8 + g];
-        uint32_t bh0, bh1, bl0, bl1;
-        split_tf32(bx0, bh0, bl0);
-        split_tf32(bx1, bh1, bl1);
-#pragma unroll
-        for (int mb = 0; mb < 8; ++mb) {
-          if (mb >= MB) break;
-          const float* hr = h_s + mb * 16 + g;
-          const float x[4] = {hr[(k0 + t) * wp], hr[(k0 + t) * wp + 8], hr[(k0 + t + 4) * wp],
-                              hr[(k0 + t + 4) * wp + 8]};
-          uint32_t ah[4], al[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            split_tf32(x[u], ah[u], al[u]);
-          }
-          float (&c4)[4] = *reinterpret_cast<float (*)[4]>(acc + 4 * mb);
-          mma_tf32(c4, al, bh0, bh1);
-          mma_tf32(c4, ah, bl0, bl1);
-          mma_tf32(c4, ah, bh0, bh1);
-        }
-      }
-    } else if (T4) {
+    if (T4) {
 #pragma unroll
       for (int s2 = 0; s2 < QMAXQ / 4 * 2; ++s2) {  // up to 4 tiles of 16 per thread
         const int slot = threadIdx.x + 256 * s2;
@@ -1037,23 +997,7 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
   }
   const int64_t ntot = (int64_t)w * dout + 2 * dout;
   float* out = a.partial + (int64_t)blockIdx.x * ntot;
-  if (MMA) {
-    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, nb = threadIdx.x >> 5;
-#pragma unroll
-    for (int mb = 0; mb < 8; ++mb) {
-      if (mb >= MB) break;
-      const float* c4 = acc + 4 * mb;
-      const int m0 = mb * 16 + g, n0 = nb * 8 + 2 * t;
-      if (m0 < w) {
-        out[m0 * dout + n0] = c4[0];
-        out[m0 * dout + n0 + 1] = c4[1];
-      }
-      if (m0 + 8 < w) {
-        out[(m0 + 8) * dout + n0] = c4[2];
-        out[(m0 + 8) * dout + n0 + 1] = c4[3];
-      }
-    }
-  } else if (T4) {
+  if (T4) {
 #pragma unroll
     for (int s2 = 0; s2 < 2; ++s2) {
       const int slot = threadIdx.x + 256 * s2;
@@ -1077,6 +1021,200 @@ __global__ void __launch_bounds__(256) k_gat_bwd_param(const SgMeta* __restrict_
     out[(int64_t)w * dout + threadIdx.x] = as;
     out[(int64_t)w * dout + dout + threadIdx.x] = ad;
   }
+}
+
+// dout == 64 weight gradient on HMMA (3xTF32), cp.async double-buffered: the
+// next tile's gathered h rows, d_z / z rows, ds and the self rows' dt land
+// while this tile multiplies (the row indirections -- src_row for h, grouped
+// -> rank for dt -- are resolved one tile further ahead). dW[c][j] += sum_r
+// h[r][c] dz[r][j]: M = c (MB blocks of 16), N = j (warp = n-block of 8),
+// K = the tile's 32 rows. Same partial layout as k_gat_bwd_param.
+__device__ __forceinline__ void cp_async4g(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+template <int MB>
+__global__ void __launch_bounds__(256, 2) k_gat_wgrad_mma(const SgMeta* __restrict__ meta, BParamArgs a) {
+  SG_PDL_ENTRY();
+  constexpr int D = 64, DZP = D + 8;
+  constexpr int WP = ((16 * MB + 8 + 31) / 32 * 32 - 8) < 16 * MB ? (16 * MB + 8 + 31) / 32 * 32 + 24
+                                                                   : (16 * MB + 8 + 31) / 32 * 32 - 8;
+  extern __shared__ __align__(16) float smem[];
+  const int w = a.w, H = a.heads, dh = D / H, w4 = w / 4;
+  const int wt = w + 1;
+  const int stage_f = QTR * WP + QTR * DZP + QTR * D + 2 * QTR * H;
+  float* Wt_s = smem;                                      // [D][w+1] (d_prev only)
+  float* stg = Wt_s + (a.d_prev ? D * wt : 0);             // 2 x stage
+  int* idx_s = reinterpret_cast<int*>(stg + 2 * stage_f);  // [2][2][QTR]: h row, dt row
+  if (a.d_prev)
+    for (int i = threadIdx.x; i < w * D; i += blockDim.x) {
+      const int c = i / D, j = i - c * D;
+      Wt_s[j * wt + c] = a.W[i];
+    }
+  for (int i = threadIdx.x; i < 2 * QTR * (WP - w); i += blockDim.x) {  // K padding columns stay zero
+    const int r = i / (WP - w), c = w + (i - r * (WP - w));
+    stg[(r / QTR) * stage_f + (r % QTR) * WP + c] = 0.f;
+  }
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d];
+  const int ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int ntiles = (n + QTR - 1) / QTR;
+  const int G = gridDim.x;
+  auto rows_of = [&](int tile, int& hr, int& tr) {  // thread < QTR: its tile row's h row and dt row
+    hr = -1;
+    tr = -1;
+    const int r = tile * QTR + (int)threadIdx.x;
+    if (tile >= ntiles || r >= n) return;
+    const int g = own0 + r;
+    hr = a.src_row ? a.src_row[g] : g;
+    const int p = a.grouped[a.voff_lm1 + g];
+    if (p < nVl) tr = ownl + a.rank[a.voff_l + p];
+  };
+  auto issue = [&](int tile, int b) {
+    float* h_s = stg + b * stage_f;
+    float* dz_s = h_s + QTR * WP;
+    float* z_s = dz_s + QTR * DZP;
+    float* ds_s = z_s + QTR * D;
+    float* dt_s = ds_s + QTR * H;
+    const int* hrow = idx_s + b * 2 * QTR;
+    const int* trow = hrow + QTR;
+    if (tile < ntiles) {
+      const int r0 = tile * QTR;
+      for (int i = threadIdx.x; i < QTR * w4; i += 256) {
+        const int r = i / w4, q = i - r * w4;
+        float* dst = h_s + r * WP + 4 * q;
+        if (hrow[r] >= 0) cp_async16g(dst, a.h_prev + (int64_t)hrow[r] * w + 4 * q);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int i = threadIdx.x; i < QTR * (D / 4); i += 256) {
+        const int r = i / (D / 4), q = i - r * (D / 4);
+        if (r0 + r < n) {
+          const int64_t g = own0 + r0 + r;
+          cp_async16g(dz_s + r * DZP + 4 * q, a.d_z + g * D + 4 * q);
+          cp_async16g(z_s + r * D + 4 * q, a.z + g * D + 4 * q);
+        } else {
+          *reinterpret_cast<float4*>(dz_s + r * DZP + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+          *reinterpret_cast<float4*>(z_s + r * D + 4 * q) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      for (int i = threadIdx.x; i < QTR * H; i += 256) {
+        const int r = i / H, hh = i - r * H;
+        if (r0 + r < n) cp_async4g(ds_s + i, a.ds + (int64_t)(own0 + r0 + r) * H + hh);
+        else ds_s[i] = 0.f;
+        if (trow[r] >= 0) cp_async4g(dt_s + i, a.dt_tot + (int64_t)trow[r] * H + hh);
+        else dt_s[i] = 0.f;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float acc[MB][4];
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) acc[mb][0] = acc[mb][1] = acc[mb][2] = acc[mb][3] = 0.f;
+  float as = 0.f, ad = 0.f;
+  int hn = -1, tn = -1;
+  if (threadIdx.x < QTR) {
+    int h0, t0;
+    rows_of(blockIdx.x, h0, t0);
+    idx_s[threadIdx.x] = h0;
+    idx_s[QTR + threadIdx.x] = t0;
+    rows_of(blockIdx.x + G, hn, tn);
+  }
+  __syncthreads();
+  issue(blockIdx.x, 0);
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3, nb = threadIdx.x >> 5;
+  for (int k = 0, tile = blockIdx.x; tile < ntiles; ++k, tile += G) {
+    const int b = k & 1;
+    if (threadIdx.x < QTR) {
+      idx_s[(b ^ 1) * 2 * QTR + threadIdx.x] = hn;
+      idx_s[(b ^ 1) * 2 * QTR + QTR + threadIdx.x] = tn;
+    }
+    __syncthreads();  // buffer b ^ 1 is free (tile k - 1 done) and its row indices visible
+    issue(tile + G, b ^ 1);
+    if (threadIdx.x < QTR) rows_of(tile + 2 * G, hn, tn);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();  // tile k landed
+    const float* h_s = stg + b * stage_f;
+    const float* dz_s = h_s + QTR * WP;
+    const float* z_s = dz_s + QTR * DZP;
+    const float* ds_s = z_s + QTR * D;
+    const float* dt_s = ds_s + QTR * H;
+#pragma unroll
+    for (int k0 = 0; k0 < QTR; k0 += 8) {
+      uint32_t bh0, bh1, bl0, bl1;
+      split_tf32(dz_s[(k0 + t) * DZP + nb * 8 + g], bh0, bl0);
+      split_tf32(dz_s[(k0 + t + 4) * DZP + nb * 8 + g], bh1, bl1);
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) {
+        const float* hr = h_s + mb * 16 + g;
+        const float x[4] = {hr[(k0 + t) * WP], hr[(k0 + t) * WP + 8], hr[(k0 + t + 4) * WP],
+                            hr[(k0 + t + 4) * WP + 8]};
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) split_tf32(x[u], ah[u], al[u]);
+        mma_tf32(acc[mb], al, bh0, bh1);
+        mma_tf32(acc[mb], ah, bl0, bl1);
+        mma_tf32(acc[mb], ah, bh0, bh1);
+      }
+    }
+    if (threadIdx.x < D) {
+      const int j = threadIdx.x, hh = j / dh;
+#pragma unroll 8
+      for (int rr = 0; rr < QTR; ++rr) {
+        as = fmaf(z_s[rr * D + j], ds_s[rr * H + hh], as);
+        ad = fmaf(z_s[rr * D + j], dt_s[rr * H + hh], ad);
+      }
+    }
+    if (a.d_prev) {
+      const int nrow = min(QTR, n - tile * QTR);
+      for (int i = threadIdx.x; i < nrow * w; i += blockDim.x) {
+        const int rr = i / w, c = i - rr * w;
+        float sacc = 0.f;
+        const float* dzr = dz_s + rr * DZP;
+#pragma unroll 8
+        for (int j = 0; j < D; ++j) sacc = fmaf(dzr[j], Wt_s[j * wt + c], sacc);
+        a.d_prev[(int64_t)(own0 + tile * QTR + rr) * w + c] = sacc;
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  const int64_t ntot = (int64_t)w * D + 2 * D;
+  float* out = a.partial + (int64_t)blockIdx.x * ntot;
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
+    const int m0 = mb * 16 + g, n0 = nb * 8 + 2 * t;
+    if (m0 < w) {
+      out[m0 * D + n0] = acc[mb][0];
+      out[m0 * D + n0 + 1] = acc[mb][1];
+    }
+    if (m0 + 8 < w) {
+      out[(m0 + 8) * D + n0] = acc[mb][2];
+      out[(m0 + 8) * D + n0 + 1] = acc[mb][3];
+    }
+  }
+  if (threadIdx.x < D) {
+    out[(int64_t)w * D + threadIdx.x] = as;
+    out[(int64_t)w * D + D + threadIdx.x] = ad;
+  }
+}
+
+template <int MB>
+int launch_wgrad_mma(const SgMeta* meta, const BParamArgs& a, int nblocks, cudaStream_t st) {
+  constexpr int D = 64;
+  constexpr int WP = ((16 * MB + 8 + 31) / 32 * 32 - 8) < 16 * MB ? (16 * MB + 8 + 31) / 32 * 32 + 24
+                                                                   : (16 * MB + 8 + 31) / 32 * 32 - 8;
+  const size_t stage_f = (size_t)QTR * WP + (size_t)QTR * (D + 8) + (size_t)QTR * D + 2 * (size_t)QTR * a.heads;
+  const size_t smem = sizeof(float) * ((a.d_prev ? (size_t)D * (a.w + 1) : 0) + 2 * stage_f) + sizeof(int) * 4 * QTR;
+  if (smem > 227 * 1024) {
+    set_error("gat_bwd_param: width too large for the MMA path");
+    return SG_ERR_ARG;
+  }
+  SG_CUDA(allow_max_smem<k_gat_wgrad_mma<MB>>());
+  ::sg::launch(k_gat_wgrad_mma<MB>, nblocks, 256, smem, st, meta, a);
+  SG_CHECK_LAUNCH("k_gat_wgrad_mma");
+  return SG_OK;
 }
 
 // ---------------------------------------------------------------- wide layers (dense.cu GEMMs)
@@ -1422,6 +1560,15 @@ extern "C" int sg_gat_bwd_src(const void* split_ws, const SgSplitLayout* lay, in
   return SG_OK;
 }
 
+// CTAs the weight-gradient launch wants (the partial buffer holds one slice per CTA)
+extern "C" int32_t sg_gat_bwd_param_blocks(int32_t w, int32_t dout, int32_t heads, int64_t rows) {
+  (void)heads;
+  const int64_t tiles = std::max<int64_t>(1, (rows + QTR - 1) / QTR);
+  const bool mma = !getenv("SG_NO_MMA") && dout == 64 && w % 4 == 0 && w > 32 && w <= 128;
+  const int64_t cap = mma ? 2 * kSMs : 6 * kSMs;  // pipelined MMA tiles: 2 CTAs per SM; else latency-bound
+  return (int32_t)std::min(tiles, cap);
+}
+
 extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                                 const float* h_prev, const int32_t* src_row, int32_t w, int32_t dout,
                                 int32_t heads, const float* z, const float* d_z, const float* ds,
@@ -1469,13 +1616,14 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
   }
   static const bool use_mma = !getenv("SG_NO_MMA");
   if (use_mma && dout == 64 && w % 4 == 0 && w > 32 && w <= 128) {
-    const int MB = (w + 15) / 16;
-    int wp = (16 * MB + 8 + 31) / 32 * 32 - 8;
-    if (wp < 16 * MB) wp += 32;
-    const size_t smem_m = sizeof(float) * ((size_t)QTR * (dout + 8) + (size_t)QTR * dout + (size_t)dout * (w + 1) +
-                                           (size_t)QTR * wp + 2 * (size_t)QTR * heads + QTR);
-    SG_CUDA(allow_max_smem<k_gat_bwd_param<2>>());
-    ::sg::launch(k_gat_bwd_param<2>, nblocks, 256, smem_m, st, meta, a);
+    switch ((w + 15) / 16) {
+      case 3: return launch_wgrad_mma<3>(meta, a, nblocks, st);
+      case 4: return launch_wgrad_mma<4>(meta, a, nblocks, st);
+      case 5: return launch_wgrad_mma<5>(meta, a, nblocks, st);
+      case 6: return launch_wgrad_mma<6>(meta, a, nblocks, st);
+      case 7: return launch_wgrad_mma<7>(meta, a, nblocks, st);
+      default: return launch_wgrad_mma<8>(meta, a, nblocks, st);
+    }
   } else if (t4) {
     SG_CUDA(allow_max_smem<k_gat_bwd_param<1>>());
     ::sg::launch(k_gat_bwd_param<1>, nblocks, 256, smem, st, meta, a);

@@ -14,7 +14,6 @@ import torch
 from paper_2303_13775_b200 import _lib
 
 
-_GAT_PARAM_NB = 6 * 148  # more CTAs than NB_PARTIAL: the weight-gradient tiles are latency-bound
 
 
 def _f32(n, *shape, device):
@@ -179,7 +178,7 @@ def gat_backward(step):
         npart = w * dout + 2 * dout
         with step.phase(f"bwd_param{l}"):
             for d in step.devices:
-                nb = max(1, min(_GAT_PARAM_NB, (int(step.n_own(l - 1, d)) + 31) // 32))
+                nb = int(_lib.load().sg_gat_bwd_param_blocks(w, dout, H, step.n_own(l - 1, d)))
                 part = _f32(nb * npart, device=step.dev)
                 _lib.call("sg_gat_bwd_param", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
                           w, dout, H, _lib.ptr(keep["z"]), _lib.ptr(d_z), _lib.ptr(dsb), _lib.ptr(dt_tot), _lib.ptr(W),
