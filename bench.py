@@ -193,6 +193,13 @@ def gat_agg_bytes(E, R, dh, H):
     return H * (20 * E + (12 + 4 * dh) * E + (4 * dh + 8) * R)
 
 
+def gat_project_bytes(n0, n1, w, D, H):
+    """GAT layer-1 projection (k_gat_project_mma), per launch: per V^0 row the
+    gathered feature row (4w) and its row index (4), z (4D) and s (4H) written,
+    grouped (4); per V^1 self row rank (4) and t (4H) written."""
+    return n0 * (4 * w + 4 + 4 * D + 4 * H + 4) + n1 * (4 + 4 * H)
+
+
 def cpu_baseline(graph, labels, samples, pm_assign, g, n_iter=2):
     """Reference algorithm (oracle NumPy port) on this host, 1 thread, on the
     first n_iter samples of the same workload: split + forward + backward +
@@ -415,7 +422,7 @@ def main():
         torch.cuda.synchronize()
 
     edges = sum(samples[i].total_edges for i in range(args.warmup, n_steps))
-    agg_ms, step_ms = [], []
+    agg_ms, step_ms, roof_ms = [], [], []
     phases = {}
     clocks = ClockSampler(local)
     if g == 1 or use_peer:
@@ -452,6 +459,8 @@ def main():
                 ev = cs.step.events
                 try:
                     agg_ms.append(ev["agg1_start"][0].elapsed_time(ev["agg1_end"][0]))
+                    if "roof1_start" in ev:
+                        roof_ms.append(ev["roof1_start"][0].elapsed_time(ev["roof1_end"][0]))
                 except Exception:
                     agg_in_graph = False
             barrier()
@@ -614,6 +623,18 @@ def main():
             alg = sage_fused_fwd_bytes(E1, R1, FEAT, HIDDEN) if g == 1 else sage_fwd_bytes(E1, R1, FEAT)
         agg_avg = float(np.mean(agg_ms))
         achieved = alg / (agg_avg / 1e3) / 1e9
+        roof_gat = None
+        if KIND == "gat" and roof_ms:
+            # C3's dominant forward kernel is the layer-1 projection, not the aggregation
+            n0 = np.mean([samples[i].sizes()[0][0] for i in range(args.warmup, n_steps)]) / g
+            pb = gat_project_bytes(n0, R1, FEAT, HIDDEN * HEADS, HEADS)
+            pms = float(np.mean(roof_ms))
+            roof_gat = {"bound": "hbm", "kernel": f"k_gat_project_mma layer 1 (3xTF32 HMMA, F={FEAT} -> "
+                                                  f"{HEADS}x{HIDDEN})",
+                        "achieved": pb / (pms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                        "frac": pb / (pms / 1e3) / 1e9 / hbm, "traffic": None, "peak_source": peak_src,
+                        "alg_bytes_per_launch": pb, "avg_launch_ms": pms, "share_of_step": pms / (my_ms / args.steps),
+                        "tensor_flops_per_launch": 3 * 2 * n0 * FEAT * HIDDEN * HEADS}
         traffic = None
         tpath = os.path.join(ROOT, "profiles", f"agg1_traffic_{CFG_NAME}.json")
         if os.path.exists(tpath):
@@ -647,13 +668,14 @@ def main():
                        "epoch_time_s": iters_per_epoch * my_ms / args.steps / 1e3,
                        "edges_per_step": edges / args.steps, "graph_gen_s": round(gen_s, 1),
                        "sample_sizes_first": {"V": nV, "E": nE}},
-            "roofline": {"bound": "hbm", "kernel": (f"k_gat_agg layer 1 (online softmax, {HEADS} heads)" if KIND == "gat"
+            "roofline_agg" if roof_gat else "roofline": {"bound": "hbm", "kernel": (f"k_gat_agg layer 1 (online softmax, {HEADS} heads)" if KIND == "gat"
                                                     else f"k_sage_agg_mean + k_sage_linear layer 1 (F={FEAT})" if g == 1
                                                     else f"k_sage_agg layer 1 (F={FEAT})"),
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic, "peak_source": peak_src,
                          "alg_bytes_per_launch": alg, "avg_launch_ms": agg_avg,
                          "share_of_step": agg_avg / (my_ms / args.steps)},
+            **({"roofline": roof_gat} if roof_gat else {}),
             "e2e": {"value": e2e, "unit": "edges/s", "h2d_bytes_per_step": h2d // args.steps,
                     "d2h_bytes_per_step": 4, "ms_per_step": e2e_ms / args.steps,
                     "wall_ms_per_step": (t_e2e * 1e3 / args.steps) if g == 1 else None,

@@ -72,7 +72,8 @@ class SplitStep:
         self.h = [None] * (self.L + 1)
         self.keep = [None] * (self.L + 1)
         self.grads = None
-        # record_events: False | True/"all" (every phase) | "agg" (layer-1 SpMM only)
+        # record_events: False | True/"all" (every phase) | "agg" (layer-1 SpMM, and
+        # the GAT layer-1 projection: the bench's roofline kernels, only)
         self.events = {} if record_events else None
         self.ev_mode = "agg" if record_events == "agg" else "all"
         self.wire_bytes = 0
@@ -95,7 +96,7 @@ class SplitStep:
     def _ev(self, name):
         if self.events is None:
             return None
-        if self.ev_mode == "agg" and not name.startswith("agg1"):
+        if self.ev_mode == "agg" and not name.startswith(("agg1", "roof1")):
             return None
         try:  # external=True: a real event-record node when captured in a CUDA graph
             e = torch.cuda.Event(enable_timing=True, external=True)

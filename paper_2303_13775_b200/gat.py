@@ -70,10 +70,14 @@ def gat_forward(step):
         s = _f32(nVp, *_hs(H), device=step.dev)
         t = _f32(nV, *_hs(H), device=step.dev)
         with step.phase(f"project{l}"):
+            if l == 1:
+                step._ev("roof1_start")
             for d in step.devices:
                 _lib.call("sg_gat_project", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(h_prev), _lib.ptr(src_row),
                           w, dout, H, _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(z), _lib.ptr(s),
                           _lib.ptr(t), step.n_own(l - 1, d), st)
+            if l == 1:
+                step._ev("roof1_end")
         t_recv = _from_owner(step, l, t, H)
         SW = _r4(dout + 2 * H)
         send = _f32(P, SW, device=step.dev)
