@@ -324,6 +324,222 @@ __global__ void __launch_bounds__(256) k_gat_project_mma(const SgMeta* __restric
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- tcgen05 projection
+// z = h W on the 5th-generation tensor cores (tcgen05.mma kind::tf32, FP32
+// accumulator in TMEM), 3xTF32 for FP32-level accuracy: per k-step of 8 the
+// elected thread issues lo(A) hi(B) + hi(A) lo(B) + hi(A) hi(B) into the same
+// accumulator. Tile = 128 gathered rows x D = 64 outputs x K = w (<= 104,
+// padded to 8). Operands sit in shared memory in the canonical K-major
+// SWIZZLE_NONE layout: 16-byte chunk c of row m at c * LBO + (m / 8) * 128 +
+// (m % 8) * 16 (core matrices of 8 rows x 16 B, SBO = 128 B, LBO = rows * 16 B).
+// Pipeline per tile: the next tile's rows are gathered by the bulk-copy engine
+// (one cp.async.bulk per 4w-byte row into a row-major raw buffer, completion
+// counted in bytes on an mbarrier: the LSU stays free for the epilogue) while
+// this tile's MMAs run and its epilogue drains TMEM; the raw tile is then split
+// into the canonical hi (low 13 mantissa bits cleared) and lo = x - hi planes.
+// Epilogue: warp w reads TMEM lanes 32 (w % 4).. (rows) and columns
+// 32 (w / 4).. (tcgen05.ld 32x32b.x32), writes z and the per-head scores.
+namespace tc5 {
+constexpr int M = 128, N = 64, KMAX = 104, CH = KMAX / 4;  // 26 chunks of 16 B
+constexpr int A_BYTES = CH * M * 16, B_BYTES = CH * N * 16;
+constexpr int LBO_A = M * 16, LBO_B = N * 16, SBO = 128;
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+constexpr size_t SMEM = 3 * (size_t)A_BYTES + 2 * (size_t)B_BYTES + 2 * 64 * 4 + M * 4 + 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(SBO >> 4) << 32) |
+         (1ull << 46);  // version 1 (sm_100), base offset 0, SWIZZLE_NONE
+}
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+}
+}  // namespace tc5
+
+template <int DH>  // head width (divides 32: a thread's 32 accumulator columns hold whole heads)
+__global__ void __launch_bounds__(256, 1) k_gat_project_tc(const SgMeta* __restrict__ meta, ProjArgs a) {
+  using namespace tc5;
+  SG_PDL_ENTRY();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* A_raw = smem_raw;
+  unsigned char* A_hi = A_raw + A_BYTES;
+  unsigned char* A_lo = A_hi + A_BYTES;
+  unsigned char* B_hi = A_lo + A_BYTES;
+  unsigned char* B_lo = B_hi + B_BYTES;
+  float* av_s = reinterpret_cast<float*>(B_lo + B_BYTES);  // a_src[64] | a_dst[64]
+  int* hrow_s = reinterpret_cast<int*>(av_s + 128);         // [M] gathered rows of the next tile
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(hrow_s + M);  // [0] MMA done, [1] gather landed
+  uint32_t* tmem_s = reinterpret_cast<uint32_t*>(mbar + 2);
+  const int w = a.w, H = N / DH, wc = w / 4;
+  const int kc = ((w + 7) & ~7) / 4;  // 16-byte chunks per row incl. K padding (even)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int l = a.l, d = a.d;
+  const int n = meta->n_own[l - 1][d];
+  const int own0 = meta->own_off[l - 1][d];
+  const int ownl = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int ntiles = (n + M - 1) / M;
+  const int G = gridDim.x;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_s)), "n"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + 1)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // B = W^T split into hi / lo planes (K padding zero), attention vectors, raw K padding
+#pragma unroll 4
+  for (int i = tid; i < (N / 4) * kc * 4; i += 256) {  // coalesced float4 reads of W rows
+    const int k = i / (N / 4), nq = i - k * (N / 4);
+    const float4 x = k < w ? *reinterpret_cast<const float4*>(a.W + k * N + 4 * nq) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int nn = 4 * nq + u;
+      uint32_t hi, lo;
+      split_tf32(xv[u], hi, lo);
+      const int off = (k >> 2) * LBO_B + (nn >> 3) * SBO + (nn & 7) * 16 + (k & 3) * 4;
+      *reinterpret_cast<uint32_t*>(B_hi + off) = hi;
+      *reinterpret_cast<uint32_t*>(B_lo + off) = lo;
+    }
+  }
+  for (int i = tid; i < N; i += 256) {
+    av_s[i] = a.a_src[i];
+    av_s[64 + i] = a.a_dst[i];
+  }
+  auto hrow_of = [&](int tile, int m) {
+    const int r = tile * M + m;
+    if (tile >= ntiles || r >= n) return -1;
+    return a.src_row ? a.src_row[own0 + r] : own0 + r;
+  };
+  const uint32_t rowbytes = 4u * (uint32_t)w;
+  auto expect = [&](int tile) {  // tid 0: the bytes the tile's row copies will deliver
+    if (tile >= ntiles) return;
+    const uint32_t bytes = rowbytes * (uint32_t)min(M, n - tile * M);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar + 1)), "r"(bytes)
+                 : "memory");
+  };
+  auto issue = [&](int tile) {  // thread m < M: one bulk copy of row m (hrow_s) into A_raw
+    if (tile >= ntiles || tid >= M) return;
+    unsigned char* dst = A_raw + tid * rowbytes;
+    const int hr = hrow_s[tid];
+    if (hr >= 0) {
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(dst)),
+                   "l"(a.h_prev + (int64_t)hr * w), "r"(rowbytes), "r"(smem_u32(mbar + 1))
+                   : "memory");
+    } else {
+      for (int c = 0; c < wc; ++c) reinterpret_cast<float4*>(dst)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto wait_bar = [&](uint64_t* bar, uint32_t ph) {
+    const uint32_t mb = smem_u32(bar);
+    uint32_t done = 0, spins = 0;
+    while (!done) {
+      if (++spins > (1u << 28)) __trap();  // never hang the device on a lost arrival
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+          : "=r"(done)
+          : "r"(mb), "r"(ph)
+          : "memory");
+    }
+  };
+  if (tid < M) hrow_s[tid] = hrow_of(blockIdx.x, tid);
+  if (tid == 0) expect(blockIdx.x);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_s;
+  issue(blockIdx.x);
+  const int row = tid & (M - 1), ch = tid >> 7;  // epilogue: TMEM lane = row, columns 32 ch ..
+  for (int k = 0, tile = blockIdx.x; tile < ntiles; ++k, tile += G) {
+    const int r0 = tile * M;
+    // this thread's epilogue row: its self-row target (grouped -> rank) resolved early
+    const int gr = r0 + row < n ? a.grouped[a.voff_lm1 + own0 + r0 + row] : -1;
+    wait_bar(mbar + 1, k & 1);  // the bulk copies of this tile's rows landed
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();  // (and the zero-filled rows); the previous tile's TMEM reads are done
+    for (int i = tid; i < M * kc; i += 256) {
+      // 8 consecutive threads: one core matrix (rows m..m+7 of chunk c, 128
+      // contiguous bytes of each plane); raw reads at row pitch 4w (w % 4 == 0)
+      // hit distinct bank groups
+      const int rest = i >> 3, c = rest % kc, m = (rest / kc) * 8 + (i & 7);
+      const int off = c * LBO_A + (m >> 3) * SBO + (m & 7) * 16;
+      const float4 x = c < wc ? *reinterpret_cast<const float4*>(A_raw + m * rowbytes + 16 * c)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      uint32_t h0, h1, h2, h3, l0, l1, l2, l3;
+      split_tf32(x.x, h0, l0);
+      split_tf32(x.y, h1, l1);
+      split_tf32(x.z, h2, l2);
+      split_tf32(x.w, h3, l3);
+      *reinterpret_cast<uint4*>(A_hi + off) = make_uint4(h0, h1, h2, h3);
+      *reinterpret_cast<uint4*>(A_lo + off) = make_uint4(l0, l1, l2, l3);
+    }
+    if (tid < M) hrow_s[tid] = hrow_of(tile + G, tid);
+    if (tid == 0) expect(tile + G);
+    const int trow = (gr >= 0 && gr < nVl) ? ownl + a.rank[a.voff_l + gr] : -1;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t ah = smem_u32(A_hi), al = smem_u32(A_lo), bh = smem_u32(B_hi), bl = smem_u32(B_lo);
+      for (int s2 = 0; s2 < kc / 2; ++s2) {
+        const uint32_t oa = 2 * s2 * LBO_A, ob = 2 * s2 * LBO_B;
+        mma(tmem, desc(al + oa, LBO_A), desc(bh + ob, LBO_B), s2 > 0);
+        mma(tmem, desc(ah + oa, LBO_A), desc(bl + ob, LBO_B), 1);
+        mma(tmem, desc(ah + oa, LBO_A), desc(bh + ob, LBO_B), 1);
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+                   : "memory");
+    }
+    issue(tile + G);  // raw buffer is free: the split is done (fence.proxy.async above)
+    wait_bar(mbar, k & 1);  // the accumulator
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t v[32];
+    {
+      const uint32_t taddr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + 32 * ch;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+            "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+            "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+    if (r0 + row < n) {
+      const int64_t G2 = own0 + r0 + row;
+      float4* zr = reinterpret_cast<float4*>(a.z + G2 * N + 32 * ch);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        zr[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                            __uint_as_float(v[4 * q + 3]));
+#pragma unroll
+      for (int h0 = 0; h0 < 32; h0 += DH) {  // heads inside this thread's 32 columns (static indices:
+        const int hh = (32 * ch + h0) / DH;  // the accumulator stays in registers)
+        float sv = 0.f, tv = 0.f;
+#pragma unroll
+        for (int j = 0; j < DH; ++j) {
+          const float zv = __uint_as_float(v[h0 + j]);
+          sv = fmaf(zv, av_s[32 * ch + h0 + j], sv);
+          tv = fmaf(zv, av_s[64 + 32 * ch + h0 + j], tv);
+        }
+        a.s[G2 * H + hh] = sv;
+        if (trow >= 0) a.t[(int64_t)trow * H + hh] = tv;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(64));
+}
+
 // TM = 32 rows per tile; NT = 8 * NQ register tiles (4 rows x 4 outputs),
 // NS = 256 / NT K-slices (NQ <= 32 -> D <= 128).
 template <int NQ>
@@ -1353,6 +1569,24 @@ extern "C" int sg_gat_project(const void* split_ws, const SgSplitLayout* lay, in
   cudaStream_t st = (cudaStream_t)stream;
   const int nq = dout / 4;
   static const bool use_mma = !getenv("SG_NO_MMA");
+  static const bool use_tc5 = !getenv("SG_NO_TC05");
+  const int dh = dout / heads;
+  if (use_mma && use_tc5 && dout == tc5::N && w % 4 == 0 && w > 32 && w <= tc5::KMAX &&
+      (dh == 8 || dh == 16 || dh == 32)) {
+    // tcgen05 (TMEM accumulator) 3xTF32 projection, one CTA per SM
+    const int grid = clamp_grid(div_up(max_rows, tc5::M), kSMs);
+    switch (dh) {
+#define TC_CASE(DD)                                                             \
+  case DD:                                                                      \
+    SG_CUDA(allow_max_smem<k_gat_project_tc<DD>>());                            \
+    ::sg::launch(k_gat_project_tc<DD>, grid, 256, tc5::SMEM, st, meta, a);      \
+    break;
+      TC_CASE(8) TC_CASE(16) TC_CASE(32)
+#undef TC_CASE
+    }
+    SG_CHECK_LAUNCH("k_gat_project_tc");
+    return SG_OK;
+  }
   if (use_mma && w % 4 == 0 && w > 32 && w <= 256 && (dout == 32 || dout == 64 || dout == 128)) {
     // tensor-core path (3xTF32 HMMA) for the wide layer-1 projection
     const int KPAD = (w + 7) & ~7;
