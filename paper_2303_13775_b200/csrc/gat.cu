@@ -184,14 +184,17 @@ __global__ void __launch_bounds__(256) k_gat_project(const SgMeta* __restrict__ 
 // (pitch K+4: conflict-free fragment loads), W in FP32 (pitch D+8), both
 // split into hi/lo as the fragments are loaded. Warp (mb, cg): rows 16mb..16mb+15, columns cg*D/4 ...
 // Then the per-head scores exactly as the FFMA kernel.
-// hi = x with the low 13 mantissa bits cleared (a TF32 value, exact split by
-// truncation), lo = x - hi (exact in FP32); lo goes to the MMA as raw FP32
-// bits, which the tensor pipe reads as TF32 (low bits ignored): the dropped
-// part is < 2^-10 |lo| <= 2^-20 |x|. Two instructions instead of the
-// multi-instruction cvt.rna.tf32 sequence (sm_100a has no single-op form).
+// x = hi + lo, both exactly TF32: hi = x rounded to TF32 (add half a TF32 ulp
+// to the magnitude, clear the low 13 mantissa bits), lo = (x - hi) (exact in
+// FP32, |lo| <= 2^-11 |x|) rounded to TF32 the same way; the dropped part is
+// <= 2^-11 |lo| <= 2^-22 |x| with no systematic sign. Four integer/FP
+// instructions instead of two multi-instruction cvt.rna.tf32 sequences
+// (sm_100a has no single-op form). Passing lo unrounded (the tensor pipe then
+// drops its low bits) doubled the roundoff seen in gradients that cancel to
+// zero analytically.
 __device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
-  hi = __float_as_uint(x) & 0xffffe000u;
-  lo = __float_as_uint(x - __uint_as_float(hi));
+  hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+  lo = (__float_as_uint(x - __uint_as_float(hi)) + 0x1000u) & 0xffffe000u;
 }
 __device__ __forceinline__ void mma_tf32(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(256) k_gat_project_mma(const SgMeta* __restric
 // (one cp.async.bulk per 4w-byte row into a row-major raw buffer, completion
 // counted in bytes on an mbarrier: the LSU stays free for the epilogue) while
 // this tile's MMAs run and its epilogue drains TMEM; the raw tile is then split
-// into the canonical hi (low 13 mantissa bits cleared) and lo = x - hi planes.
+// into the canonical hi (x rounded to TF32) and lo = x - hi planes.
 // Epilogue: warp w reads TMEM lanes 32 (w % 4).. (rows) and columns
 // 32 (w / 4).. (tcgen05.ld 32x32b.x32), writes z and the per-head scores.
 namespace tc5 {
