@@ -501,7 +501,8 @@ def main():
         del diag
         ce = make_step(LR / args.batch)
         ce.capture(samples[0])
-        pinned = ce.prepare_pinned(samples[args.warmup:n_steps])
+        # compact staging (run starts instead of per-edge destinations) unless SG_PIPE_COMPACT=0
+        pinned = ce.prepare_pinned(samples[args.warmup:n_steps], compact=os.environ.get("SG_PIPE_COMPACT", "1") != "0")
         ce.run_pipelined(pinned[:2])  # allocate the staging buffers (untimed)
         barrier()
         e0.record()

@@ -520,6 +520,17 @@ int sg_gat_bwd_src_lb(const void* split_ws, const SgSplitLayout* lay, int32_t l,
  * input buffer dev_dst; sg_pipe_finish queues the D2H of the step's loss on
  * `stream`; sg_pipe_wait blocks until it has landed and returns it. */
 void* sg_pipe_create(int64_t bytes);
+/* bytes (a multiple of 16) of staged input layout + `extra` scratch bytes for
+ * the compact form's run starts. */
+void* sg_pipe_create2(int64_t bytes, int64_t extra);
+/* Compact staging of a destination-grouped sample: H2D of the prefix (header,
+ * V, es: prefix_bytes) and of the per-destination run starts (layer by layer,
+ * |V^l| ints each), the ed lists rebuilt from them on the copy stream
+ * (edge_off[l-1] = capacity offset of E^l, o_ed = word offset of the ed
+ * region), then the D2D of full_bytes into dev_dst on `stream`. */
+int sg_pipe_stage_compact(void* h, int32_t slot, const void* host_prefix, int64_t prefix_bytes,
+                          const void* host_starts, int64_t starts_bytes, int32_t L, const int64_t* edge_off,
+                          int64_t o_ed, int64_t full_bytes, void* dev_dst, void* stream);
 void sg_pipe_destroy(void* h);
 int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,
                   void* stream);

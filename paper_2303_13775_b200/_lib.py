@@ -153,6 +153,8 @@ _SIGS = {
     "sg_gat_bwd_src_lb": (i32, [vp, P(SgSplitLayout), i32, i32, i32, i32, vp, vp, vp, vp, i64, i32, vp, vp, vp, vp, i32,
                                 vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp]),
     "sg_pipe_create": (vp, [i64]),
+    "sg_pipe_create2": (vp, [i64, i64]),
+    "sg_pipe_stage_compact": (i32, [vp, i32, vp, i64, vp, i64, i32, vp, i64, i64, vp, vp]),
     "sg_pipe_destroy": (None, [vp]),
     "sg_pipe_stage": (i32, [vp, i32, vp, i64, vp, vp]),
     "sg_pipe_finish": (i32, [vp, i32, vp, vp]),

@@ -16,7 +16,8 @@ namespace sg {
 namespace {
 
 struct Pipe {
-  int64_t bytes = 0;
+  int64_t bytes = 0;  // staged input layout
+  int64_t extra = 0;  // scratch after it (compact staging: the run starts)
   void* stage[2] = {nullptr, nullptr};
   float* loss_h = nullptr;  // pinned, 2 words
   cudaStream_t copy = nullptr;
@@ -38,17 +39,18 @@ void pipe_free(Pipe* p) {
 
 }  // namespace
 
-extern "C" void* sg_pipe_create(int64_t bytes) {
-  if (bytes <= 0) {
-    set_error("pipe_create: bytes must be > 0");
+extern "C" void* sg_pipe_create2(int64_t bytes, int64_t extra) {
+  if (bytes <= 0 || bytes % 16 || extra < 0) {
+    set_error("pipe_create: bytes must be > 0 and a multiple of 16, extra >= 0");
     return nullptr;
   }
   Pipe* p = new Pipe();
   p->bytes = bytes;
+  p->extra = extra;
   bool ok = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking) == cudaSuccess &&
             cudaHostAlloc((void**)&p->loss_h, 2 * sizeof(float), cudaHostAllocDefault) == cudaSuccess;
   for (int s = 0; ok && s < 2; ++s) {
-    ok = cudaMalloc(&p->stage[s], (size_t)bytes) == cudaSuccess &&
+    ok = cudaMalloc(&p->stage[s], (size_t)(bytes + extra)) == cudaSuccess &&
          cudaEventCreateWithFlags(&p->used[s], cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&p->h2d[s], cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&p->done[s], cudaEventDisableTiming) == cudaSuccess;
@@ -61,13 +63,15 @@ extern "C" void* sg_pipe_create(int64_t bytes) {
   return p;
 }
 
+extern "C" void* sg_pipe_create(int64_t bytes) { return sg_pipe_create2((bytes + 15) / 16 * 16, 0); }
+
 extern "C" void sg_pipe_destroy(void* h) { pipe_free((Pipe*)h); }
 
 extern "C" int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,
                              void* stream) {
   Pipe* p = (Pipe*)h;
   SG_REQUIRE(p && (slot == 0 || slot == 1), "pipe_stage: bad handle/slot");
-  SG_REQUIRE(bytes >= 0 && bytes <= p->bytes, "pipe_stage: bytes exceed the staging slot");
+  SG_REQUIRE(bytes >= 0 && bytes <= p->bytes + p->extra, "pipe_stage: bytes exceed the staging slot");
   SG_REQUIRE(host_src && dev_dst, "pipe_stage: null buffer");
   cudaStream_t st = (cudaStream_t)stream;
   SG_CUDA(cudaStreamWaitEvent(p->copy, p->used[slot], 0));
@@ -75,6 +79,73 @@ extern "C" int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_
   SG_CUDA(cudaEventRecord(p->h2d[slot], p->copy));
   SG_CUDA(cudaStreamWaitEvent(st, p->h2d[slot], 0));
   SG_CUDA(cudaMemcpyAsync(dev_dst, p->stage[slot], (size_t)bytes, cudaMemcpyDeviceToDevice, st));
+  SG_CUDA(cudaEventRecord(p->used[slot], st));
+  return SG_OK;
+}
+
+namespace {
+// Destination lists of a destination-grouped sample from per-destination run
+// starts (the compact host->device form): layer l's starts follow layer l-1's
+// (|V^l| words each, sizes from the staged header); one thread per destination
+// writes its run of ed. Runs on the copy stream, in the shadow of the running step.
+struct ExpandGeo {
+  int64_t eoff[SG_MAXL];  // capacity offset of E^l in the es / ed regions (layer l at [l-1])
+  int64_t o_ed;           // word offset of the ed region
+  int64_t starts_off;     // word offset of the staged starts
+  int L;
+};
+
+__global__ void __launch_bounds__(256) k_pipe_expand(int32_t* __restrict__ stage, ExpandGeo geo) {
+  const int64_t* sizes = reinterpret_cast<const int64_t*>(stage);  // [nV (L+1) | nE (L)]
+  int64_t off[SG_MAXL + 1];
+  off[0] = 0;
+  for (int l = 1; l <= geo.L; ++l) off[l] = off[l - 1] + sizes[l];
+  const int32_t* starts = stage + geo.starts_off;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < off[geo.L];
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int l = 1;
+    while (x >= off[l]) ++l;
+    const int64_t i = x - off[l - 1];
+    const int b = starts[x];
+    const int e = i + 1 < sizes[l] ? starts[x + 1] : (int)sizes[geo.L + l];
+    int32_t* ed = stage + geo.o_ed + geo.eoff[l - 1];
+    for (int k = b; k < e; ++k) ed[k] = (int32_t)i;
+  }
+}
+}  // namespace
+
+// Compact staging: H2D of the sample prefix (header, V, es) and of the
+// per-destination run starts, the ed lists rebuilt on the copy stream, then
+// the usual D2D of the full prefix into the graph's input buffer.
+extern "C" int sg_pipe_stage_compact(void* h, int32_t slot, const void* host_prefix, int64_t prefix_bytes,
+                                     const void* host_starts, int64_t starts_bytes, int32_t L,
+                                     const int64_t* edge_off, int64_t o_ed, int64_t full_bytes, void* dev_dst,
+                                     void* stream) {
+  Pipe* p = (Pipe*)h;
+  SG_REQUIRE(p && (slot == 0 || slot == 1), "pipe_stage_compact: bad handle/slot");
+  SG_REQUIRE(L >= 1 && L <= SG_MAXL && edge_off, "pipe_stage_compact: bad geometry");
+  SG_REQUIRE(prefix_bytes >= 0 && full_bytes >= prefix_bytes && full_bytes <= p->bytes && starts_bytes >= 0 &&
+                 starts_bytes <= p->extra,
+             "pipe_stage_compact: bytes exceed the staging slot");
+  SG_REQUIRE(host_prefix && host_starts && dev_dst, "pipe_stage_compact: null buffer");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* stage = (char*)p->stage[slot];
+  SG_CUDA(cudaStreamWaitEvent(p->copy, p->used[slot], 0));
+  SG_CUDA(cudaMemcpyAsync(stage, host_prefix, (size_t)prefix_bytes, cudaMemcpyHostToDevice, p->copy));
+  SG_CUDA(cudaMemcpyAsync(stage + p->bytes, host_starts, (size_t)starts_bytes, cudaMemcpyHostToDevice, p->copy));
+  ExpandGeo geo;
+  memset(&geo, 0, sizeof(geo));
+  geo.L = L;
+  for (int l = 0; l < L; ++l) geo.eoff[l] = edge_off[l];
+  geo.o_ed = o_ed;
+  geo.starts_off = p->bytes / 4;
+  if (starts_bytes > 0) {
+    k_pipe_expand<<<clamp_grid(div_up(starts_bytes / 4, 256), kSMs), 256, 0, p->copy>>>((int32_t*)stage, geo);
+    SG_CHECK_LAUNCH("k_pipe_expand");
+  }
+  SG_CUDA(cudaEventRecord(p->h2d[slot], p->copy));
+  SG_CUDA(cudaStreamWaitEvent(st, p->h2d[slot], 0));
+  SG_CUDA(cudaMemcpyAsync(dev_dst, stage, (size_t)full_bytes, cudaMemcpyDeviceToDevice, st));
   SG_CUDA(cudaEventRecord(p->used[slot], st));
   return SG_OK;
 }

@@ -1089,16 +1089,39 @@ class StaticSample:
 
 
 class PinnedSample:
-    """One sample packed into pinned host memory in the StaticSample layout,
-    ready for a single async H2D copy. This is the form a host sampler hands
-    to the trainer."""
+    """One sample packed into pinned host memory, ready for the pipelined H2D
+    (CapturedStep.run_pipelined). This is the form a host sampler hands to the
+    trainer. compact=True (the default) sends the StaticSample prefix up to
+    the last source position (header, V, es) plus one run start per
+    destination instead of the per-edge destination lists (~40 % fewer bytes
+    across PCIe; sg_pipe_stage_compact rebuilds ed on the copy stream, off the
+    step's critical path). compact=False: the full layout in one buffer."""
 
-    def __init__(self, sample, static):
+    def __init__(self, sample, static, compact=True):
         host = np.zeros(static.words, dtype=np.int32)
         used = static.pack(sample, host)
-        self.buf = torch.from_numpy(host[:used].copy()).pin_memory()
         self.num_targets = len(sample.targets)
-        self.h2d_bytes = 4 * used
+        self.full_bytes = 4 * used
+        self.compact = bool(compact)
+        if not self.compact:
+            self.buf = torch.from_numpy(host[:used].copy()).pin_memory()
+            self.h2d_bytes = 4 * used
+            return
+        nV, nE = sample.sizes()
+        L = static.L
+        prefix = static.o_es + int(static.eoff[L - 1] + nE[L - 1])
+        starts = []
+        for l, (_, b) in enumerate(sample.layer_edges):
+            cnt = np.bincount(np.asarray(b, dtype=np.int64), minlength=nV[l + 1])
+            st = np.zeros(nV[l + 1], dtype=np.int32)
+            np.cumsum(cnt[:-1], out=st[1:])
+            starts.append(st)
+        st = np.concatenate(starts) if starts else np.zeros(0, np.int32)
+        self.prefix_words = prefix
+        self.buf = torch.from_numpy(np.concatenate([host[:prefix], st])).pin_memory()
+        self.starts_off = 4 * prefix
+        self.starts_bytes = 4 * len(st)
+        self.h2d_bytes = 4 * prefix + self.starts_bytes
 
 
 def capacities_for(samples, slack=1.0):
@@ -1175,11 +1198,11 @@ class CapturedStep:
     def loss_sum(self):
         return self.out[self.p.n]
 
-    def prepare_pinned(self, samples):
+    def prepare_pinned(self, samples, compact=True):
         """Pack samples into PinnedSamples and DMA each buffer once (untimed):
         the first transfer from a freshly pinned buffer pays a one-time
         mapping cost that a sampler's reused pinned ring never sees again."""
-        pinned = [PinnedSample(smp, self.inp) for smp in samples]
+        pinned = [PinnedSample(smp, self.inp, compact) for smp in samples]
         scratch = torch.empty(self.inp.words, dtype=torch.int32, device=self.dev)
         for ps in pinned:
             scratch[:ps.buf.numel()].copy_(ps.buf, non_blocking=True)
@@ -1196,10 +1219,12 @@ class CapturedStep:
         D2H bytes)."""
         lib = _lib.load()
         if getattr(self, "_pipe", None) is None:
-            h = lib.sg_pipe_create(4 * self.inp.words)
+            inp = self.inp
+            h = lib.sg_pipe_create2((4 * inp.words + 15) // 16 * 16, 4 * int(sum(inp.cap_nV[1:])) + 16)
             if not h:
                 _lib.check(2, "sg_pipe_create")
             self._pipe = h
+            self._pipe_eoff = np.ascontiguousarray(inp.eoff[:inp.L], dtype=np.int64)
         h = self._pipe
         st = _lib.stream_ptr()
         dst = _lib.ptr(self.inp.buf)
@@ -1212,7 +1237,13 @@ class CapturedStep:
         for i, ps in enumerate(pinned):
             b = i & 1
             t0 = pc()
-            _lib.check(lib.sg_pipe_stage(h, b, ps.buf.data_ptr(), ps.h2d_bytes, dst, st), "sg_pipe_stage")
+            if ps.compact:
+                base = ps.buf.data_ptr()
+                _lib.check(lib.sg_pipe_stage_compact(h, b, base, ps.starts_off, base + ps.starts_off, ps.starts_bytes,
+                                                     self.inp.L, self._pipe_eoff.ctypes.data, self.inp.o_ed,
+                                                     ps.full_bytes, dst, st), "sg_pipe_stage_compact")
+            else:
+                _lib.check(lib.sg_pipe_stage(h, b, ps.buf.data_ptr(), ps.h2d_bytes, dst, st), "sg_pipe_stage")
             t1 = pc()
             self.graph.replay()
             t2 = pc()
