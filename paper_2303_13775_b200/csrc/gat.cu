@@ -343,6 +343,11 @@ __global__ void __launch_bounds__(256) k_gat_project_mma(const SgMeta* __restric
 // Epilogue: warp w reads TMEM lanes 32 (w % 4).. (rows) and columns
 // 32 (w / 4).. (tcgen05.ld 32x32b.x32), writes z and the per-head scores.
 namespace tc5 {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int M = 128, N = 64, KMAX = 104, CH = KMAX / 4;  // 26 chunks of 16 B
 constexpr int A_BYTES = CH * M * 16, B_BYTES = CH * N * 16;
 constexpr int LBO_A = M * 16, LBO_B = N * 16, SBO = 128;
@@ -442,14 +447,15 @@ __global__ void __launch_bounds__(256, 1) k_gat_project_tc(const SgMeta* __restr
   };
   auto wait_bar = [&](uint64_t* bar, uint32_t ph) {
     const uint32_t mb = smem_u32(bar);
-    uint32_t done = 0, spins = 0;
+    uint32_t done = 0;
+    const uint64_t t0 = globaltimer_ns();
     while (!done) {
-      if (++spins > (1u << 28)) __trap();  // never hang the device on a lost arrival
       asm volatile(
           "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
           : "=r"(done)
           : "r"(mb), "r"(ph)
           : "memory");
+      if (!done && globaltimer_ns() - t0 > 2000000000ull) __trap();  // never hang the device on a lost arrival
     }
   };
   if (tid < M) hrow_s[tid] = hrow_of(blockIdx.x, tid);
