@@ -8,3 +8,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_g
    -o gpurun_out/${TAG}_full_c3 -f python bench.py --config c3 --profile --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_c3.log 2>&1; echo "ncu c3 rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_ref.json 2>gpurun_out/${TAG}_bench_ref.err; echo "ref rc=$?"
 timeout 1200 python bench.py --config c4 --steps 10 --warmup 3 > gpurun_out/${TAG}_bench_c4.json 2>gpurun_out/${TAG}_bench_c4.err; echo "c4 rc=$?"
+timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/${TAG}_smoke.log
