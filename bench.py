@@ -624,25 +624,25 @@ def main():
             alg = sage_fused_fwd_bytes(E1, R1, FEAT, HIDDEN) if g == 1 else sage_fwd_bytes(E1, R1, FEAT)
         agg_avg = float(np.mean(agg_ms))
         achieved = alg / (agg_avg / 1e3) / 1e9
+        def _traffic(kind):  # ncu DRAM bytes per launch of the roofline kernel, if captured
+            tpath = os.path.join(ROOT, "profiles", f"{kind}_traffic_{CFG_NAME}.json")
+            try:
+                return json.load(open(tpath)).get("bytes_per_launch")
+            except Exception:
+                return None
+        traffic = _traffic("agg1")
         roof_gat = None
         if KIND == "gat" and roof_ms:
             # C3's dominant forward kernel is the layer-1 projection, not the aggregation
             n0 = np.mean([samples[i].sizes()[0][0] for i in range(args.warmup, n_steps)]) / g
             pb = gat_project_bytes(n0, R1, FEAT, HIDDEN * HEADS, HEADS)
             pms = float(np.mean(roof_ms))
-            roof_gat = {"bound": "hbm", "kernel": f"k_gat_project_mma layer 1 (3xTF32 HMMA, F={FEAT} -> "
-                                                  f"{HEADS}x{HIDDEN})",
+            roof_gat = {"bound": "hbm", "kernel": f"k_gat_project_tc layer 1 (tcgen05 kind::tf32 3xTF32, TMEM "
+                                                  f"accumulator, F={FEAT} -> {HEADS}x{HIDDEN})",
                         "achieved": pb / (pms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
-                        "frac": pb / (pms / 1e3) / 1e9 / hbm, "traffic": None, "peak_source": peak_src,
+                        "frac": pb / (pms / 1e3) / 1e9 / hbm, "traffic": _traffic("roof1"), "peak_source": peak_src,
                         "alg_bytes_per_launch": pb, "avg_launch_ms": pms, "share_of_step": pms / (my_ms / args.steps),
                         "tensor_flops_per_launch": 3 * 2 * n0 * FEAT * HIDDEN * HEADS}
-        traffic = None
-        tpath = os.path.join(ROOT, "profiles", f"agg1_traffic_{CFG_NAME}.json")
-        if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get("bytes_per_launch")
-            except Exception:
-                traffic = None
         base = None
         if not args.no_cpu_baseline and not args.profile:
             rate, secs, n_it, _ = cpu_baseline(graph, labels, samples[args.warmup:], pm.assignment, g, 2)
