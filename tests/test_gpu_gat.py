@@ -132,3 +132,30 @@ def test_multihead_init_is_reference_for_one_head():
     a = sg.init_params("gat", 10, 8, 3, 2, seed=1).tensors()
     b = sg.init_params("gat", 10, 8, 3, 2, seed=1, heads=1).tensors()
     assert all(np.array_equal(a[k], b[k]) for k in a)
+
+
+@pytest.mark.parametrize("F,H", [(36, 2), (64, 8), (100, 4)])
+def test_gat_tcgen05_projection_shapes(F, H):
+    """The tcgen05 projection (D = 64, w <= 104, head width 32 / 8 / 16; K
+    padded to 8) over enough rows that every CTA runs several 128-row tiles
+    (pipelined gathers, partial last tile) against the composed float64
+    oracle."""
+    import paper_2303_13775_b200 as sg
+    from oracle.multihead_oracle import multihead_run
+    graph, pm, sample, cache = random_partition_case(300 + F, n=120000, m=1500000, g=1, batch=2048,
+                                                     fanouts=(10, 8), cache_frac=1.0)
+    assert len(sample.layer_vertices[0]) > 148 * 128  # several tiles on some CTAs
+    dh, C = 64 // H, 5
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=3)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=4)
+    params = sg.init_params("gat", F, dh, C, 2, seed=5, heads=H)
+    splits, plan = sg.split_minibatch(sample, pm, cache)
+    ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+    loss, grads = ex.run()
+    rloss, rgrads, rh = multihead_run(sample.layer_vertices, sample.layer_edges,
+                                      {k: np.asarray(v, dtype=np.float64) for k, v in params.tensors().items()},
+                                      feats.astype(np.float64), labels, H)
+    assert abs(loss - rloss) <= TOL * abs(rloss), (loss, rloss)
+    assert_grads_close(grads[0], rgrads, TOL, "tc")
+    for l in range(1, 3):
+        assert rel_err(ex.states[0].h[l], rh[l][splits[0].owned_pos[l]]) < TOL, l
