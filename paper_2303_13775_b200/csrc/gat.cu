@@ -1000,29 +1000,78 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ 
   const bool colok = col < dout;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // software-pipelined over this warp's rows: the next row's out-edge range is
+  // fetched while the current row's edges land, and the self-row chain
+  // (grouped -> rank -> dt) is issued before the edge loop so the two
+  // dependent chains overlap
+  int nb_ = 0, ne_ = 0;
+  if (gw < n_prev) {
+    nb_ = a.srcbeg[a.key_base + prev0 + gw];
+    ne_ = a.srcend[a.key_base + prev0 + gw];
+  }
   for (int64_t u = gw; u < n_prev; u += nw) {
     const int64_t U = prev0 + u;
     T acc = V::zero();
     float dsv = 0.f;
-    const int b = a.srcbeg[a.key_base + U], e = a.srcend[a.key_base + U];
+    const int b = nb_, e = ne_;
+    if (u + nw < n_prev) {
+      nb_ = a.srcbeg[a.key_base + U + nw];
+      ne_ = a.srcend[a.key_base + U + nw];
+    }
+    const int p = a.grouped[a.voff_lm1 + U];
+    int64_t vself = -1;
+    float dt = 0.f;
+    if (p < nVl) {  // self row of owned v: d_z += dt_v * a_dst (owner combines holders' dt)
+      vself = own0 + a.rank[a.voff_l + p];
+      dt = a.dt_loc[vself * H + hl];
+      const int* cb = a.contrib + (int64_t)a.g * a.voff_l + vself * a.g;
+      for (int s = 0; a.g > 1 && s < a.g; ++s) {
+        const int rs = cb[s];
+        if (rs >= 0) dt += a.dt_recv[(int64_t)rs * H + hl];
+      }
+    }
     for (int jb = b; jb < e; jb += 32) {
       const int j = jb + lane;
       const int my = j < e ? a.perm[j] : 0;
       const int cnt = min(32, e - jb);
       const int rounds = (cnt + NG - 1) / NG;
-      for (int kk = 0; kk < rounds; ++kk) {
-        const int k = kk * NG + gi;
-        const int x = __shfl_sync(0xffffffffu, my, k < 32 ? k : 31);
-        if (k < cnt) {
-          const int q = a.ldst[x];
-          const float* dn_row = q < n_own
-              ? a.dnc + (int64_t)(own0 + q) * (dout + H)
-              : a.dnc_recv + (int64_t)a.sendpos[a.pbase_l + ref0 + (q - n_own)] * a.dnc_stride;
-          if (colok) {
-            V::fma_(acc, a.alpha[(int64_t)x * H + hl], V::ld_any(dn_row + col));
-            dsv += a.d_pre[(int64_t)x * H + hl];
+      // four rounds' edges in flight at once (hub rows have hundreds of
+      // out-edges: one dependent load chain per round was their whole cost);
+      // accumulation order unchanged (rounds ascending)
+      for (int kk = 0; kk < rounds; kk += 4) {
+        int xs[4];
+        bool ok[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int k = (kk + u) * NG + gi;
+          xs[u] = __shfl_sync(0xffffffffu, my, k < 32 ? k : 31);
+          ok[u] = kk + u < rounds && k < cnt;
+        }
+        const float* rows[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          rows[u] = nullptr;
+          if (ok[u]) {
+            const int q = a.ldst[xs[u]];
+            rows[u] = q < n_own ? a.dnc + (int64_t)(own0 + q) * (dout + H)
+                                : a.dnc_recv + (int64_t)a.sendpos[a.pbase_l + ref0 + (q - n_own)] * a.dnc_stride;
           }
         }
+        T vals[4];
+        float al[4], dp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const bool go = ok[u] && colok;
+          vals[u] = go ? V::ld_any(rows[u] + col) : V::zero();
+          al[u] = go ? a.alpha[(int64_t)xs[u] * H + hl] : 0.f;
+          dp[u] = go ? a.d_pre[(int64_t)xs[u] * H + hl] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (ok[u] && colok) {
+            V::fma_(acc, al[u], vals[u]);
+            dsv += dp[u];
+          }
       }
     }
 #pragma unroll
@@ -1032,17 +1081,9 @@ __global__ void __launch_bounds__(256) k_gat_bwd_src(const SgMeta* __restrict__ 
     }
     if (gi != 0) continue;
     if (colok) V::fma_(acc, dsv, V::ld_any(a.a_src + col));  // d_z += ds * a_src
-    const int p = a.grouped[a.voff_lm1 + U];
-    if (p < nVl) {  // self row of owned v: d_z += dt_v * a_dst (owner combines holders' dt)
-      const int64_t v = own0 + a.rank[a.voff_l + p];
-      float dt = a.dt_loc[v * H + hl];
-      const int* cb = a.contrib + (int64_t)a.g * a.voff_l + v * a.g;
-      for (int s = 0; a.g > 1 && s < a.g; ++s) {
-        const int rs = cb[s];
-        if (rs >= 0) dt += a.dt_recv[(int64_t)rs * H + hl];
-      }
+    if (vself >= 0) {
       if (colok) V::fma_(acc, dt, V::ld_any(a.a_dst + col));
-      if (head_lead && colok) a.dt_tot[v * H + hl] = dt;
+      if (head_lead && colok) a.dt_tot[vself * H + hl] = dt;
     }
     if (colok) V::st(a.d_z + U * dout + col, acc);  // dout % VEC == 0: aligned
     if (head_lead && colok) a.ds[U * H + hl] = dsv;
