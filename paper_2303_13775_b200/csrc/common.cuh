@@ -62,6 +62,25 @@ constexpr int kSMs = 148;
     asm volatile("griddepcontrol.launch_dependents;" :::);    \
   } while (0)
 
+// Wait for the completion of the mbarrier phase with parity `parity`; traps
+// after 2 s (%globaltimer) instead of hanging the device on a lost arrival.
+__device__ __forceinline__ void sg_mbar_wait(uint32_t mbar_smem, uint32_t parity) {
+  uint32_t done = 0;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(mbar_smem), "r"(parity)
+        : "memory");
+    if (done) return;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) __trap();
+  }
+}
+
 extern bool g_pdl;
 
 template <typename... KArgs, typename... Args>

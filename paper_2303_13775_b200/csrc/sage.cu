@@ -1010,12 +1010,22 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
   SG_PDL_ENTRY();
   constexpr int TR = 32;
   extern __shared__ __align__(16) float smem[];
-  const int w = a.w, dout = a.dout, K = 2 * w, KP = K + 4, wst = dout + 4;
+  const int w = a.w, dout = a.dout, K = 2 * w, wst = dout + 4;
   const bool need_c = a.d_self != nullptr || a.d_sums != nullptr;
-  const int stage_f = TR * KP + 2 * TR * dout + TR;  // A | d_h | h | counts
+  // A = [hs plane [TR][w] | mean plane [TR][w]]: a tile of each is contiguous in
+  // global memory and lands with ONE bulk copy (byte-counted on bar[s]); d_h,
+  // h, counts by cp.async
+  const int stage_f = TR * K + 2 * TR * dout + TR;  // A | d_h | h | counts
   float* ws_s = smem;                  // [w][dout+4] (need_c)
   float* wn_s = ws_s + w * wst;
   float* stg = wn_s + w * wst;         // 2 x stage
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stg + 2 * stage_f);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(bar + 1)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   if (need_c)
     for (int i = threadIdx.x; i < w * dout; i += blockDim.x) {
       const int c = i / dout, j = i - c * dout;
@@ -1029,20 +1039,28 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
   const bool scat = a.sc_enc != nullptr;
   auto issue = [&](int tile, int s) {
     float* A_s = stg + s * stage_f;
-    float* dh_s = A_s + TR * KP;
+    float* dh_s = A_s + TR * K;
     float* hh_s = dh_s + TR * dout;
     float* cn_s = hh_s + TR * dout;
-    const int r0 = tile * TR;
-    for (int idx = threadIdx.x; idx < TR * ncg; idx += 256) {
-      const int r = idx / ncg, q = idx - r * ncg;
-      const int k = 4 * q;
-      float* dst = A_s + r * KP + k;
-      if (r0 + r < n) {
-        const int64_t G = own0 + r0 + r;
-        cp_async16(dst, k < w ? a.h_prev + G * w + k : a.mean + G * w + (k - w));
-      } else {
-        *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+    const int r0 = tile * TR, nr = min(TR, n - r0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of this stage are done
+    if (threadIdx.x == 0) {
+      const uint32_t mb = (uint32_t)__cvta_generic_to_shared(bar + s);
+      const uint32_t bytes = 4u * (uint32_t)(nr * w);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(2u * bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(A_s)),
+                   "l"(a.h_prev + (int64_t)(own0 + r0) * w), "r"(bytes), "r"(mb)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(A_s + TR * w)),
+                   "l"(a.mean + (int64_t)(own0 + r0) * w), "r"(bytes), "r"(mb)
+                   : "memory");
+    }
+    for (int idx = threadIdx.x; idx < (TR - nr) * K / 4; idx += 256) {  // rows past n: zeros (0 * garbage may be NaN)
+      const int r = nr + idx / (K / 4), q = idx - (r - nr) * (K / 4);
+      float* dst = 4 * q < w ? A_s + r * w + 4 * q : A_s + TR * w + r * w + 4 * q - w;
+      *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     for (int idx = threadIdx.x; idx < TR * dq; idx += 256) {
       const int r = idx / dq, q = idx - r * dq;
@@ -1066,7 +1084,7 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
   if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
   asm volatile("cp.async.commit_group;" ::: "memory");
   int s = 0;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, s ^= 1) {
+  for (int tile = blockIdx.x, it = 0; tile < ntiles; tile += gridDim.x, s ^= 1, ++it) {
     const int r0 = tile * TR;
     if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, s ^ 1);
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -1075,7 +1093,7 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
       // tile lands: 4 rows per warp at once, each row's out-edges split over
       // GPR lane groups of LPR lanes (one float4 of the row per lane), fixed
       // xor tree over the groups (deterministic), + d_self on self rows.
-      float* dh_w = stg + s * stage_f + TR * KP;
+      float* dh_w = stg + s * stage_f + TR * K;
       const int LPR = dq, GPR = 8 / dq;  // dout in {4, 8, 16, 32}
       const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
       const int slot = lane / LPR, lr = lane - slot * LPR;
@@ -1113,9 +1131,10 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
       }
     }
     asm volatile("cp.async.wait_group 1;" ::: "memory");
+    sg_mbar_wait((uint32_t)__cvta_generic_to_shared(bar + s), (it >> 1) & 1);  // this stage's bulk copies
     __syncthreads();
     const float* A_s = stg + s * stage_f;
-    float* dp_s = const_cast<float*>(A_s) + TR * KP;
+    float* dp_s = const_cast<float*>(A_s) + TR * K;
     const float* hh_s = dp_s + TR * dout;
     const float* cn_s = hh_s + TR * dout;
     if (!a.final_)
@@ -1127,9 +1146,10 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
       const int slot = threadIdx.x + 256 * s2;
       if (slot < nslots) {
         const int cg = slot / NQ, jg = slot - cg * NQ;
+        const float* ab = 4 * cg < w ? A_s + 4 * cg : A_s + TR * w + 4 * cg - w;
 #pragma unroll 4
         for (int r = 0; r < TR; ++r) {
-          const float4 a4 = *reinterpret_cast<const float4*>(A_s + r * KP + 4 * cg);
+          const float4 a4 = *reinterpret_cast<const float4*>(ab + r * w);
           const float4 g4 = *reinterpret_cast<const float4*>(dp_s + r * dout + 4 * jg);
           const float av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
@@ -1610,7 +1630,7 @@ extern "C" int sg_sage_bwd_rows(const void* split_ws, const SgSplitLayout* lay, 
   a.d_sums = d_sums;
   if (self_compact && q4 && w % 4 == 0 && dout <= 32 && 2 * w * (dout / 4) <= 4 * 512) {
     const size_t sm2 = sizeof(float) * (2 * (32 * (size_t)(2 * w + 4) + 2 * 32 * (size_t)dout + 32) +
-                                        2 * (size_t)w * (dout + 4));
+                                        2 * (size_t)w * (dout + 4)) + 16;
     SG_REQUIRE(sm2 <= 227 * 1024, "sage_wgrad: width too large for shared memory");
     cudaStream_t st2 = (cudaStream_t)stream;
     cudaError_t attr = cudaSuccess;
