@@ -47,7 +47,12 @@ extern "C" void* sg_pipe_create2(int64_t bytes, int64_t extra) {
   Pipe* p = new Pipe();
   p->bytes = bytes;
   p->extra = extra;
-  bool ok = cudaStreamCreateWithFlags(&p->copy, cudaStreamNonBlocking) == cudaSuccess &&
+  // highest priority: the compact form's expand kernel then takes the first
+  // free SM slots between the running step's kernels instead of queueing
+  // behind them (the next step's D2D waits on it)
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  bool ok = cudaStreamCreateWithPriority(&p->copy, cudaStreamNonBlocking, hi_prio) == cudaSuccess &&
             cudaHostAlloc((void**)&p->loss_h, 2 * sizeof(float), cudaHostAllocDefault) == cudaSuccess;
   for (int s = 0; ok && s < 2; ++s) {
     ok = cudaMalloc(&p->stage[s], (size_t)(bytes + extra)) == cudaSuccess &&
