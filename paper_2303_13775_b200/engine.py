@@ -37,7 +37,7 @@ NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions (meas
 # layers with at least this many edges (capacity) take the load-balanced
 # transposed SpMM (tspmm.cu); below it hub rows are short (max out-degree
 # ~25-125 at C2 layers 2-3) and the single-kernel row-per-warp path is faster
-TSPMM_MIN_EDGES = 65536
+TSPMM_MIN_EDGES = int(os.environ.get("SG_TSPMM_MIN_EDGES", "65536"))  # load-balanced transposed SpMM from this many edges
 
 
 def _nblocks(rows, tile=32):
