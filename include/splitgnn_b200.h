@@ -167,6 +167,24 @@ int sg_layer0_rows(const void* split_ws, const SgSplitLayout* lay, int32_t d,
                    int32_t* src_row0, void* stream);
 int sg_gather_rows(const float* table, const int32_t* rows, int64_t n_rows, int32_t width,
                    float* out, void* stream);
+/* Cache-miss staging (the host loads of _load_inputs, engine.py:160-167, of
+ * the load_gids scheduler.py:193-203 lists): for devices [d0, d1), every
+ * layer-0 row on the load list is read from host feature memory mapped into
+ * the device address space (host_feats = the device address sg_host_map
+ * returns for a row-major [n, feat_dim] fp32 matrix) into table row
+ * n_cached + q, q = global load index (the row sg_layer0_rows assigns with
+ * miss_base = n_cached). Counts come from the device SgMeta: no host sync,
+ * capturable. staging_rows (rows allocated after the cached ones) must be
+ * >= the layer-0 capacity. */
+int sg_stage_misses(const void* split_ws, const SgSplitLayout* lay, int32_t d0, int32_t d1,
+                    const int32_t* V, const float* host_feats, int32_t feat_dim,
+                    float* table, int32_t row_stride, int32_t n_cached,
+                    int64_t staging_rows, void* stream);
+/* Page-lock a caller-owned host range for device access (mapped, read-only
+ * hint) and return its device address; sg_host_unmap releases it. */
+int sg_host_map(void* host_ptr, int64_t bytes, void** dev_ptr);
+int sg_host_unmap(void* host_ptr);
+
 /* Synthetic U[0,1) features (hash of (seed, row, col)), written on the device. */
 int sg_fill_uniform(float* out, int64_t rows, int32_t width, uint64_t seed,
                     int64_t row0, void* stream);
@@ -405,6 +423,8 @@ int sg_peer_exchange(const void* split_ws, const SgSplitLayout* lay, int32_t l, 
                      void* stream);
 int sg_peer_signal(const int64_t* peer_flags, int32_t rank, int32_t g, int32_t round,
                    const int32_t* epoch, void* stream);
+/* k_peer_wait traps (aborting the CUDA context) after 20 s without a peer
+ * signal, after setting *timeout: a lost peer never lets a step continue. */
 int sg_peer_wait(const int32_t* my_flags, int32_t rank, int32_t g, int32_t round,
                  const int32_t* epoch, int32_t* timeout, void* stream);
 int sg_peer_epoch(int32_t* epoch, void* stream);
@@ -419,6 +439,10 @@ int sg_peer_grad_stage(const float* grads, float* my_slots, int64_t n1, int64_t 
 int sg_peer_allreduce_sgd(const int64_t* peer_slots, int32_t g, int64_t n, int64_t n1,
                           int64_t slot_stride, const int32_t* epoch, float* params, float* grads_out,
                           float scale, void* stream);
+/* scale = lr / *num_targets on the device (the replayed sample's target count). */
+int sg_peer_allreduce_sgd_nt(const int64_t* peer_slots, int32_t g, int64_t n, int64_t n1,
+                             int64_t slot_stride, const int32_t* epoch, float* params, float* grads_out,
+                             double lr, const int64_t* num_targets, void* stream);
 /* ---- GPU k-hop sampler (sample_minibatch, sampling.py:118-177) ---------------
  * From a device in-CSR (row_offsets int64[n+1], col_indices int32), for
  * device int64 targets[nt]: the packed sample (V^l at voff[l], E^l at
@@ -456,6 +480,11 @@ int sg_partition_round(const int64_t* row_offsets, const int32_t* col_indices, c
  * (ModelParams.sgd_step, models.py:95-99). param = 0 skips the step. */
 int sg_reduce_partials_sgd(const int64_t* jobs, int32_t n_jobs, int64_t max_n, float scale,
                            void* stream);
+/* As sg_reduce_partials_sgd with scale = lr / *num_targets computed on the
+ * device (in double, like the host's lr / len(targets)): a captured step
+ * normalises by each replayed sample's own target count (device sizes). */
+int sg_reduce_partials_sgd_nt(const int64_t* jobs, int32_t n_jobs, int64_t max_n, double lr,
+                              const int64_t* num_targets, void* stream);
 /* allreduce_and_step (engine.py:633-647): grads = sum over devices in device
  * order (grad_ptrs: HOST array of n_dev device pointers to flat buffers), then
  * p -= lr/num_targets * grads; grads_out (nullable) receives the sum. */

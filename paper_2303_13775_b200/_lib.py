@@ -78,6 +78,9 @@ _SIGS = {
     "sg_src_csr": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, i64, vp]),
     "sg_dst_csr": (i32, [vp, P(SgSplitLayout), i32, vp, i64, vp, vp, vp, vp]),
     "sg_layer0_rows": (i32, [vp, P(SgSplitLayout), i32, vp, vp, i32, vp, vp]),
+    "sg_stage_misses": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, vp, i32, i32, i64, vp]),
+    "sg_host_map": (i32, [vp, i64, P(vp)]),
+    "sg_host_unmap": (i32, [vp]),
     "sg_gather_rows": (i32, [vp, vp, i64, i32, vp, vp]),
     "sg_fill_uniform": (i32, [vp, i64, i32, u64, i64, vp]),
     "sg_sage_agg_fwd": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32, i64, vp]),
@@ -108,8 +111,10 @@ _SIGS = {
     "sg_peer_epoch": (i32, [vp, vp]),
     "sg_peer_grad_stage": (i32, [vp, vp, i64, i64, vp, vp]),
     "sg_peer_allreduce_sgd": (i32, [vp, i32, i64, i64, i64, vp, vp, vp, f32, vp]),
+    "sg_peer_allreduce_sgd_nt": (i32, [vp, i32, i64, i64, i64, vp, vp, vp, f64, vp, vp]),
     "sg_split_cost": (i32, [vp, vp, vp, vp, vp, i32, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
     "sg_reduce_partials_sgd": (i32, [vp, i32, i64, f32, vp]),
+    "sg_reduce_partials_sgd_nt": (i32, [vp, i32, i64, f64, vp, vp]),
     "sg_get_pdl": (i32, []),
     "sg_sage_update": (i32, [vp, P(SgSplitLayout), i32, i32, vp, vp, i32, i32, vp, vp, vp, i32,
                              vp, vp, vp, i32, vp, vp, vp, i64, vp]),

@@ -161,6 +161,8 @@ struct SgdJobs {
   int64_t param[MAXJOBS];
   int64_t n_sgd[MAXJOBS];
   float scale;
+  double lr;                  // with nt: scale = lr / *nt, computed on the device
+  const int64_t* nt;          // device num_targets of the step's sample (nullable)
 };
 
 __global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs, SgdJobs sj) {
@@ -173,6 +175,9 @@ __global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs, SgdJobs sj) 
   float* out = (float*)jobs.v[4 * jb + 3];
   float* prm = (float*)sj.param[jb];
   const int64_t n_sgd = sj.n_sgd[jb];
+  // lr / num_targets (allreduce_and_step, engine.py:633-647) in double, as the
+  // host computes it, from the sample's own target count
+  const float scale = sj.nt ? (float)(sj.lr / (double)max(*sj.nt, (int64_t)1)) : sj.scale;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int64_t k0 = (int64_t)blockIdx.x * 32; k0 < n; k0 += (int64_t)gridDim.x * 32) {
     const int64_t k = k0 + lane;
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(256) k_reduce_partials(Jobs jobs, SgdJobs sj) 
 #pragma unroll
       for (int w = 0; w < 8; ++w) t += red[w][lane];
       out[k] = t;
-      if (prm && k < n_sgd) prm[k] -= sj.scale * t;
+      if (prm && k < n_sgd) prm[k] -= scale * t;
     }
   }
 }
@@ -256,7 +261,7 @@ extern "C" int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32
 }
 
 static int reduce_partials(const int64_t* jobs, int stride, int32_t n_jobs, int64_t max_n, float scale,
-                           void* stream) {
+                           void* stream, double lr = 0.0, const int64_t* nt = nullptr) {
   if (n_jobs <= 0 || max_n <= 0) return SG_OK;
   SG_REQUIRE(jobs != nullptr, "reduce_partials: null job table");
   for (int j0 = 0; j0 < n_jobs; j0 += MAXJOBS) {
@@ -266,6 +271,8 @@ static int reduce_partials(const int64_t* jobs, int stride, int32_t n_jobs, int6
     memset(&jb, 0, sizeof(jb));
     memset(&sj, 0, sizeof(sj));
     sj.scale = scale;
+    sj.lr = lr;
+    sj.nt = nt;
     for (int j = 0; j < nj; ++j) {
       const int64_t* r = jobs + (int64_t)stride * (j0 + j);
       for (int f = 0; f < 4; ++f) jb.v[4 * j + f] = r[f];
@@ -289,6 +296,12 @@ extern "C" int sg_reduce_partials(const int64_t* jobs, int32_t n_jobs, int64_t m
 extern "C" int sg_reduce_partials_sgd(const int64_t* jobs, int32_t n_jobs, int64_t max_n, float scale,
                                       void* stream) {
   return reduce_partials(jobs, 6, n_jobs, max_n, scale, stream);
+}
+
+extern "C" int sg_reduce_partials_sgd_nt(const int64_t* jobs, int32_t n_jobs, int64_t max_n, double lr,
+                                         const int64_t* num_targets, void* stream) {
+  SG_REQUIRE(num_targets != nullptr, "reduce_partials_sgd_nt: null num_targets");
+  return reduce_partials(jobs, 6, n_jobs, max_n, 0.f, stream, lr, num_targets);
 }
 
 extern "C" int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_ptrs,

@@ -31,7 +31,8 @@
 namespace sg {
 namespace {
 
-constexpr int kRounds = 32;  // exchange rounds per step (SAGE 5, GAT 15 at L = 3)
+constexpr int kRounds = 32;
+constexpr uint64_t kPeerTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s without a peer signal  // exchange rounds per step (SAGE 5, GAT 15 at L = 3)
 
 struct PeerTable {
   int64_t p[SG_MAXG];
@@ -82,14 +83,20 @@ __global__ void k_peer_wait(const int* __restrict__ my_flags, int rank, int g, i
   SG_PDL_ENTRY();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   const int e = *epoch;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
   for (int s = 0; s < g; ++s) {
     if (s == rank) continue;
-    long long spins = 0;
     while (ld_acquire_sys(my_flags + round * SG_MAXG + s) < e) {
-      __nanosleep(64);
-      if (++spins > (1ll << 31)) {  // ~minutes: a peer is gone; fail loudly, do not hang forever
+      __nanosleep(256);
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > kPeerTimeoutNs) {
+        // a peer is gone or wedged: record it and abort the context -- the
+        // step must never continue on stale peer buffers
         atomicOr(timeout, 1);
-        return;
+        __threadfence_system();
+        __trap();
       }
     }
   }
@@ -182,8 +189,10 @@ __global__ void k_peer_grad_stage(const float* __restrict__ g, float* __restrict
 
 __global__ void k_peer_allreduce_sgd(PeerTable slots, int g, int64_t n, int64_t n1, int64_t slot_stride,
                                      const int* __restrict__ epoch, float* __restrict__ params,
-                                     float* __restrict__ gout, float scale) {
+                                     float* __restrict__ gout, float scale, double lr,
+                                     const int64_t* __restrict__ nt) {
   SG_PDL_ENTRY();
+  if (nt) scale = (float)(lr / (double)max(*nt, (int64_t)1));  // the sample's own target count
   const int64_t off = (int64_t)(*epoch & 1) * slot_stride;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n1; k += (int64_t)gridDim.x * blockDim.x) {
     float s = ((const float*)slots.p[0])[off + k];
@@ -210,7 +219,19 @@ extern "C" int sg_peer_allreduce_sgd(const int64_t* peer_slots, int32_t g, int64
                                      float scale, void* stream) {
   SG_REQUIRE(peer_slots && epoch && params && g >= 1 && g <= SG_MAXG && n1 >= n, "peer_allreduce_sgd: bad argument");
   ::sg::launch(k_peer_allreduce_sgd, clamp_grid(div_up(n1, 256), kSMs), 256, 0, (cudaStream_t)stream,
-               table_of(peer_slots, g), (int)g, n, n1, slot_stride, epoch, params, grads_out, scale);
+               table_of(peer_slots, g), (int)g, n, n1, slot_stride, epoch, params, grads_out, scale, 0.0,
+               (const int64_t*)nullptr);
+  SG_CHECK_LAUNCH("k_peer_allreduce_sgd");
+  return SG_OK;
+}
+
+extern "C" int sg_peer_allreduce_sgd_nt(const int64_t* peer_slots, int32_t g, int64_t n, int64_t n1,
+                                        int64_t slot_stride, const int32_t* epoch, float* params,
+                                        float* grads_out, double lr, const int64_t* num_targets, void* stream) {
+  SG_REQUIRE(peer_slots && epoch && params && num_targets && g >= 1 && g <= SG_MAXG && n1 >= n,
+             "peer_allreduce_sgd_nt: bad argument");
+  ::sg::launch(k_peer_allreduce_sgd, clamp_grid(div_up(n1, 256), kSMs), 256, 0, (cudaStream_t)stream,
+               table_of(peer_slots, g), (int)g, n, n1, slot_stride, epoch, params, grads_out, 0.f, lr, num_targets);
   SG_CHECK_LAUNCH("k_peer_allreduce_sgd");
   return SG_OK;
 }

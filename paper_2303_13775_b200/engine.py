@@ -115,8 +115,15 @@ class SplitStep:
             self.src_row0 = ds.V
             return
         self.src_row0 = torch.empty(max(ds.nV[0], 1), dtype=torch.int32, device=self.dev)
-        if self.meta is not None and int(self.meta.load_off[self.g]) > 0:
-            self.host_bytes += self.f.stage_misses(ds, self.meta)
+        if not ds.all_cached:
+            # the sample may hold uncached layer-0 rows: stage this step's load
+            # lists on the device (exact or captured alike)
+            if self.meta is not None:
+                self.host_bytes += 4 * self.f.feat_dim * sum(int(self.meta.n_load[d]) for d in self.devices)
+                if sum(int(self.meta.n_load[d]) for d in self.devices):
+                    self.f.stage_misses(ds, self.devices)
+            else:
+                self.f.stage_misses(ds, self.devices)
         for d in self.devices:
             _lib.call("sg_layer0_rows", _lib.ptr(ds.ws), ds.lay, d, _lib.ptr(ds.V),
                       _lib.ptr(self.f.cache_slot), int(self.f.n_cached), _lib.ptr(self.src_row0), st)
@@ -542,14 +549,19 @@ class SplitStep:
         """Per-block partials -> per-device flat gradients (+ loss slot)."""
         jobs = []
         max_n = 1
-        sgd = getattr(self, "sgd", None)  # (flat params, scale): g = 1, SGD fused into the reduction
+        # (flat params, scale) or (flat params, lr, device num_targets): g = 1,
+        # SGD fused into the reduction
+        sgd = getattr(self, "sgd", None)
         for part, nb, n, gbuf, off in self.jobs:
             jobs += [part.data_ptr(), nb, n, gbuf.data_ptr() + 4 * off]
             if sgd is not None:
                 jobs += [sgd[0].data_ptr() + 4 * off, max(0, min(n, self.p.n - off))]
             max_n = max(max_n, n)
         table = np.asarray(jobs, dtype=np.int64)
-        if sgd is not None:
+        if sgd is not None and len(sgd) == 3:
+            _lib.call("sg_reduce_partials_sgd_nt", _lib.ptr(table), len(self.jobs), max_n, float(sgd[1]),
+                      sgd[2].data_ptr(), _lib.stream_ptr())
+        elif sgd is not None:
             _lib.call("sg_reduce_partials_sgd", _lib.ptr(table), len(self.jobs), max_n, float(sgd[1]),
                       _lib.stream_ptr())
         else:
@@ -1102,7 +1114,11 @@ class PinnedSample:
         used = static.pack(sample, host)
         self.num_targets = len(sample.targets)
         self.full_bytes = 4 * used
-        self.compact = bool(compact)
+        # the compact form rebuilds each layer's destination list from run
+        # starts, which holds only when destinations are in ascending order
+        # (a dst-grouped sample may list its groups in any order)
+        self.compact = bool(compact) and all(
+            len(b) < 2 or bool(np.all(np.diff(np.asarray(b)) >= 0)) for _, b in sample.layer_edges)
         if not self.compact:
             self.buf = torch.from_numpy(host[:used].copy()).pin_memory()
             self.h2d_bytes = 4 * used
@@ -1139,16 +1155,32 @@ class CapturedStep:
     sample's H2D copy in front. Kernels read every size from device memory."""
 
     def __init__(self, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale,
-                 device="cuda", record_events=False):
+                 device="cuda", record_events=False, lr=None):
         if pm.num_devices != 1:
             raise ValueError("CapturedStep covers the single-GPU split (g = 1)")
         self.p = dparams
         self.pm, self.cache, self.f, self.labels = pm, cache, feats, labels_dev
         self.dev = torch.device(device)
         self.inp = StaticSample(cap_nV, cap_nE, self.dev)
-        self.scale = float(lr_scale)
+        self._init_lr(lr_scale, lr)
         self.record_events = record_events
         self.graph = None
+
+    def _init_lr(self, lr_scale, lr):
+        """The SGD step inside the graph is p -= lr / num_targets * g with
+        num_targets read on the device from each replayed sample's sizes
+        (allreduce_and_step divides by that sample's target count). `lr`
+        given, or derived at capture as lr_scale x the warm-up sample's
+        target count (the captured batch)."""
+        self.scale = float(lr_scale)
+        self.lr = None if lr is None else float(lr)
+
+    def _num_targets_dev(self):
+        return self.inp.sizes[self.inp.L:self.inp.L + 1]
+
+    def _fix_lr(self, warm_sample):
+        if self.lr is None:
+            self.lr = self.scale * len(warm_sample.targets)
 
     def _body(self):
         inp = self.inp
@@ -1168,7 +1200,7 @@ class CapturedStep:
         if ev:
             step.events["ph:split:s"] = [ev[0]]
             step.events["ph:split:e"] = [ev[1]]
-        step.sgd = (self.p.flat, self.scale)  # one device: the SGD step rides on the reduction
+        step.sgd = (self.p.flat, self.lr, self._num_targets_dev())  # one device: SGD rides on the reduction
         step.run()
         gbuf = step.grads[0]
         self.ds, self.step = ds, step
@@ -1178,6 +1210,7 @@ class CapturedStep:
         """Eager warm-up on the static buffers, then capture. The warm-up
         applies real SGD updates (it is a training step); callers that need
         untouched parameters restore them afterwards."""
+        self._fix_lr(warm_sample)
         self.inp.load(warm_sample)
         self._body()
         torch.cuda.synchronize()
@@ -1320,6 +1353,8 @@ class SampledCapturedStep(CapturedStep):
         self.tev[k] = ev
 
     def capture_targets(self, targets, seed):
+        if self.lr is None:
+            self.lr = self.scale * self.batch
         self.load_targets(targets, seed)
         self._body()
         torch.cuda.synchronize()
@@ -1408,14 +1443,14 @@ class RankCapturedStep(CapturedStep):
     SGD. Sizes are read on the device; nothing returns to the host."""
 
     def __init__(self, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale, rank, transport,
-                 device="cuda", record_events=False):
+                 device="cuda", record_events=False, lr=None):
         if not hasattr(transport, "all_reduce_sgd"):
             raise ValueError("RankCapturedStep needs a PeerTransport (no host-side sizes inside a graph)")
         self.p = dparams
         self.pm, self.cache, self.f, self.labels = pm, cache, feats, labels_dev
         self.dev = torch.device(device)
         self.inp = StaticSample(cap_nV, cap_nE, self.dev)
-        self.scale = float(lr_scale)
+        self._init_lr(lr_scale, lr)
         self.record_events = record_events
         self.graph = None
         self.rank = int(rank)
@@ -1432,6 +1467,7 @@ class RankCapturedStep(CapturedStep):
         gbuf = step.grads[self.rank]
         if self.gsum is None:
             self.gsum = torch.empty_like(gbuf)
-        self.transport.all_reduce_sgd(gbuf, self.p.n, self.p.flat, self.scale, grads_out=self.gsum)
+        self.transport.all_reduce_sgd(gbuf, self.p.n, self.p.flat, None, grads_out=self.gsum, lr=self.lr,
+                                      num_targets=self._num_targets_dev())
         self.ds, self.step = ds, step
         return self.gsum

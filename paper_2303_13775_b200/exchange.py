@@ -208,9 +208,10 @@ class PeerTransport:
         _lib.call("sg_peer_exchange", _lib.ptr(dsplit.ws), dsplit.lay, l, self.rank, 0,
                   _lib.ptr(recv_pair_layout), int(stride), _lib.ptr(peers), _lib.stream_ptr())
 
-    def all_reduce_sgd(self, gbuf, n, params_flat, scale, grads_out=None):
+    def all_reduce_sgd(self, gbuf, n, params_flat, scale, grads_out=None, lr=None, num_targets=None):
         """Sum the ranks' flat gradients (+ loss slot) in rank order and apply
-        the SGD step, over peer memory (the step barrier)."""
+        the SGD step, over peer memory (the step barrier). num_targets (device
+        int64 scalar) + lr: scale = lr / num_targets computed on the device."""
         import torch
         n1 = int(gbuf.numel())
         stride = (n1 + 63) // 64 * 64
@@ -221,6 +222,11 @@ class PeerTransport:
         st = _lib.stream_ptr()
         _lib.call("sg_peer_grad_stage", _lib.ptr(gbuf), _lib.ptr(t), n1, stride, _lib.ptr(self.epoch), st)
         self._signal_wait(self.rounds - 1)
+        if num_targets is not None:
+            _lib.call("sg_peer_allreduce_sgd_nt", _lib.ptr(peers), self.world, int(n), n1, stride,
+                      _lib.ptr(self.epoch), _lib.ptr(params_flat), _lib.ptr(grads_out), float(lr),
+                      num_targets.data_ptr(), st)
+            return
         _lib.call("sg_peer_allreduce_sgd", _lib.ptr(peers), self.world, int(n), n1, stride, _lib.ptr(self.epoch),
                   _lib.ptr(params_flat), _lib.ptr(grads_out), float(scale), st)
 

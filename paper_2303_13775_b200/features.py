@@ -2,8 +2,11 @@
 
 Rows of the cached vertices live in one fp32 table on the device, grouped by
 owner partition; `cache_slot[gid]` maps a vertex to its row (-1 = not cached).
-Per-iteration misses (the reference's load_gids / host_bytes) are gathered on
-the host and copied into a staging area appended to the table. The
+Per-iteration misses (the reference's load_gids / host_bytes) are read by a
+zero-copy device gather from the host feature matrix (page-locked and mapped
+into the device address space) into a staging area appended to the table;
+the counts come from the device split, so the staging runs inside captured
+steps too. The
 aggregation kernels read the table through an int32 row indirection (no h0
 materialisation).
 """
@@ -53,9 +56,11 @@ class FeatureStore:
         return self.table.device
 
     @classmethod
-    def from_host(cls, features, cache=None, devices=None, device="cuda", pad_rows=False):
+    def from_host(cls, features, cache=None, devices=None, device="cuda", pad_rows=False, staging_rows=0):
         """Upload the cached rows of `devices` (default: all) from a host
-        feature matrix; uncached rows are served as misses from `features`."""
+        feature matrix; uncached rows are served as misses from `features`
+        (staging_rows: miss rows to reserve up front, e.g. the captured
+        layer-0 capacity; grown on demand otherwise)."""
         feats = np.ascontiguousarray(features, dtype=np.float32)
         n, F = feats.shape
         S = padded_stride(F, pad_rows)
@@ -67,9 +72,9 @@ class FeatureStore:
         else:
             ids = np.empty(0, dtype=np.int64)
         slot[ids] = np.arange(len(ids), dtype=np.int32)
-        table = cls._alloc(len(ids), F, S, device)
+        table = cls._alloc(len(ids) + int(staging_rows), F, S, device)
         if len(ids):
-            table[:, :F].copy_(torch.from_numpy(feats[ids]))
+            table[:len(ids), :F].copy_(torch.from_numpy(feats[ids]))
         return cls(table, torch.from_numpy(slot).to(device), len(ids), F, feats)
 
     @classmethod
@@ -110,25 +115,90 @@ class FeatureStore:
         slot[row_ids] = np.arange(len(row_ids), dtype=np.int32)
         return cls(table, torch.from_numpy(slot).to(device), len(row_ids), feat_dim, None)
 
-    def stage_misses(self, dsplit, meta):
-        """Copy this iteration's uncached layer-0 rows (all devices' load
-        lists, global load order) behind the cached rows. Returns bytes moved."""
-        total = int(meta.load_off[dsplit.g])
-        if total == 0:
-            return 0
+    # -- cache misses -------------------------------------------------------------
+    def host_device_ptr(self):
+        """Device address of the host feature matrix (mapped once, refcounted
+        per host range): the source of the zero-copy miss gather."""
         if self.host_features is None:
-            raise RuntimeError("feature cache miss but no host feature matrix to load from")
-        lay = dsplit.lay
-        grouped = dsplit.i32(lay.o_grouped, total, start=int(lay.nVtot)).cpu().numpy()
-        V0 = np.asarray(dsplit.host_V[: dsplit.nV[0]]) if dsplit.host_V is not None else \
-            dsplit.V[: dsplit.nV[0]].cpu().numpy()
-        gids = V0[grouped]
-        rows = torch.from_numpy(self.host_features[gids]).pin_memory()
-        need = self.n_cached + total
+            raise RuntimeError("feature cache miss but no host feature matrix to load from "
+                               "(build the FeatureStore with FeatureStore.from_host)")
+        if getattr(self, "_hmap", None) is None:
+            self._hmap = _map_host(self.host_features)
+        return self._hmap
+
+    def ensure_staging(self, rows):
+        """Grow the table so `rows` miss rows fit behind the cached ones (must
+        run outside CUDA-graph capture; a captured step calls it from its eager
+        warm-up)."""
+        need = self.n_cached + int(rows)
         if self.table.shape[0] < need:
+            if torch.cuda.is_current_stream_capturing():
+                raise RuntimeError("feature staging area must be sized before CUDA-graph capture")
             t = self._alloc(need, self.feat_dim, self.row_stride, self.device)
-            t[: self.n_cached] = self.table[: self.n_cached]
+            if self.n_cached:
+                t[: self.n_cached] = self.table[: self.n_cached]
+            # a CUDA graph captured earlier may still read the old table: keep it alive
+            self._retired = getattr(self, "_retired", []) + [self.table]
             self.table = t
-        self.table[self.n_cached:need, :self.feat_dim].copy_(rows, non_blocking=True)
-        self._keep = rows
-        return int(rows.numel() * 4)
+        return self.table
+
+    @property
+    def staging_rows(self):
+        return int(self.table.shape[0]) - self.n_cached
+
+    def stage_misses(self, dsplit, devices=None):
+        """Copy this iteration's uncached layer-0 rows of `devices` (default
+        all; the global load order of scheduler.py:193-203) behind the cached
+        rows, on the device (sg_stage_misses: counts from the device split, no
+        host sync). Returns the table."""
+        devs = list(range(dsplit.g)) if devices is None else sorted(int(d) for d in devices)
+        self.ensure_staging(dsplit.nV[0])
+        src = self.host_device_ptr()
+        st = _lib.stream_ptr()
+        # contiguous device ranges (a rank stages only its own load list)
+        runs, a = [], None
+        for d in devs:
+            if a is None or d != runs[-1][1]:
+                runs.append([d, d + 1])
+            else:
+                runs[-1][1] = d + 1
+            a = d
+        for d0, d1 in runs:
+            _lib.call("sg_stage_misses", _lib.ptr(dsplit.ws), dsplit.lay, d0, d1, _lib.ptr(dsplit.V), src,
+                      self.feat_dim, _lib.ptr(self.table), self.row_stride, self.n_cached, self.staging_rows, st)
+        return self.table
+
+    def __del__(self):
+        h = getattr(self, "_hmap", None)
+        if h is not None and self.host_features is not None:
+            try:
+                _unmap_host(self.host_features)
+            except Exception:
+                pass
+            self._hmap = None
+
+
+_MAPPED = {}  # host address -> [refcount, device address]
+
+
+def _map_host(arr):
+    import ctypes
+    key = int(arr.ctypes.data)
+    ent = _MAPPED.get(key)
+    if ent is None:
+        dptr = ctypes.c_void_p()
+        _lib.check(_lib.load().sg_host_map(key, int(arr.nbytes), ctypes.byref(dptr)), "sg_host_map")
+        ent = _MAPPED[key] = [0, int(dptr.value)]
+    ent[0] += 1
+    return ent[1]
+
+
+def _unmap_host(arr):
+    key = int(arr.ctypes.data)
+    ent = _MAPPED.get(key)
+    if ent is None:
+        return
+    ent[0] -= 1
+    if ent[0] <= 0:
+        del _MAPPED[key]
+        _lib.load().sg_host_unmap(key)

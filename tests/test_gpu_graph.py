@@ -128,3 +128,90 @@ def test_back_to_back_runs_match_synchronized(kind):
     assert runs[0][0] == runs[1][0]
     assert np.array_equal(runs[0][1], runs[1][1])
     assert np.isfinite(runs[1][1]).all()
+
+
+def _reverse_groups(smp):
+    """Same sample with each layer's destination groups listed in descending
+    destination order (still grouped, no longer ascending)."""
+    import paper_2303_13775_b200 as sg
+    edges = []
+    for a, b in smp.layer_edges:
+        a, b = np.asarray(a), np.asarray(b)
+        order = np.argsort(-b, kind="stable")
+        edges.append((a[order], b[order]))
+    return sg.MiniBatchSample(smp.num_layers, list(smp.layer_vertices), edges)
+
+
+def test_pinned_compact_falls_back_for_unordered_groups():
+    """PinnedSample(compact=True) rebuilds destinations from run starts, valid
+    only for ascending destinations: a grouped-but-unordered sample must take
+    the full layout and train exactly like run()."""
+    import torch
+
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200.engine import CapturedStep, PinnedSample, capacities_for
+    graph = sg.generate_powerlaw(20000, 200000, blocks=16, p_local=0.8, seed=11)
+    pm = sg.range_partition(graph.num_vertices, 1)
+    cache = sg.full_cache(pm)
+    F, C, B = 32, 6, 96
+    feats = sg.FeatureStore.synthetic(graph.num_vertices, F, seed=1)
+    labels = torch.from_numpy(sg.synthetic_labels(graph.num_vertices, C, seed=2)).cuda()
+    rng = np.random.default_rng(5)
+    samples = [_reverse_groups(sg.sample_minibatch(graph, rng.choice(graph.num_vertices, B, replace=False),
+                                                   [8, 6, 4], rng)) for _ in range(4)]
+    assert all(s.is_dst_grouped() for s in samples)
+    cap_nV, cap_nE = capacities_for(samples)
+    params = sg.init_params("graphsage", F, 8, C, 3, seed=4)
+    runs = []
+    for mode in ("seq", "pipe"):
+        dp = sg.DeviceParams.from_host(params)
+        cs = CapturedStep(dp, pm, cache, feats, labels, cap_nV, cap_nE, 0.1 / B)
+        cs.capture(samples[0])
+        if mode == "seq":
+            losses = []
+            for smp in samples[1:]:
+                cs.run(smp)
+                losses.append(float(cs.out[dp.n].item()) / len(smp.targets))
+        else:
+            pinned = [PinnedSample(smp, cs.inp, compact=True) for smp in samples[1:]]
+            assert not any(p.compact for p in pinned)
+            losses, _, _ = cs.run_pipelined(pinned)
+        torch.cuda.synchronize()
+        runs.append((losses, dp.flat.cpu().numpy().copy()))
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
+
+
+def test_captured_step_normalises_by_each_samples_target_count():
+    """allreduce_and_step divides by the sample's own num_targets: a short
+    last batch replayed through the captured graph (captured at B = 96) gets
+    lr / 40, read on the device from the sample's sizes."""
+    import torch
+
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200.engine import CapturedStep, capacities_for
+    graph = sg.generate_powerlaw(20000, 200000, blocks=16, p_local=0.8, seed=9)
+    pm = sg.range_partition(graph.num_vertices, 1)
+    cache = sg.full_cache(pm)
+    F, C = 32, 6
+    feats = sg.FeatureStore.synthetic(graph.num_vertices, F, seed=1)
+    hostX = sg.synthetic_features(graph.num_vertices, F, seed=1).astype(np.float64)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
+    rng = np.random.default_rng(3)
+    samples = [sg.sample_minibatch(graph, rng.choice(graph.num_vertices, b, replace=False), [8, 6, 4], rng)
+               for b in (96, 96, 40)]
+    cap_nV, cap_nE = capacities_for(samples, slack=1.1)
+    params = sg.init_params("graphsage", F, 16, C, 3, seed=4)
+    dp = sg.DeviceParams.from_host(params)
+    cs = CapturedStep(dp, pm, cache, feats, torch.from_numpy(labels).cuda(), cap_nV, cap_nE, 0.1 / 96)
+    cs.capture(samples[0])
+    for smp in samples[1:]:
+        cs.run(smp)
+    ref = glorot_params("graphsage", F, 16, C, 3, seed=4)
+    for smp in samples:
+        ws, wp = split_sample(smp.layer_vertices, smp.layer_edges, pm.assignment, 1, cache.cached)
+        _, rg = CoopRun(ref, ws, wp, hostX, labels).run()
+        reduce_and_sgd(ref, rg, 0.1, len(smp.targets))
+    got = dp.to_host().tensors()
+    for k in ref:
+        assert rel_err(got[k], ref[k]) < 1e-4, k

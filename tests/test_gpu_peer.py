@@ -14,11 +14,13 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _setup(L=2):
+def _setup(L=2, partial=False):
     import paper_2303_13775_b200 as sg
     graph = sg.generate_powerlaw(8000, 80000, blocks=8, p_local=0.6, seed=2)
     pm = sg.range_partition(graph.num_vertices, 2)
-    cache = sg.full_cache(pm)
+    # partial: each rank caches 20% of the graph's vertices of its partition;
+    # its other layer-0 rows are staged from host memory inside the step
+    cache = sg.build_cache(graph, pm, 0.2) if partial else sg.full_cache(pm)
     rng = np.random.default_rng(7)
     fan = [6, 4] if L == 2 else [6, 4, 3]
     samples = [sg.sample_minibatch(graph, rng.choice(graph.num_vertices, 64, replace=False), fan, rng)
@@ -26,7 +28,7 @@ def _setup(L=2):
     return graph, pm, cache, samples
 
 
-def _worker(rank, world, port, kind, captured, q):
+def _worker(rank, world, port, kind, captured, q, partial=False):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -37,7 +39,7 @@ def _worker(rank, world, port, kind, captured, q):
         from paper_2303_13775_b200.engine import RankCapturedStep, RankSplitTrainer, capacities_for
         torch.cuda.set_device(0)
         L = 3 if captured else 2
-        graph, pm, cache, samples = _setup(L)
+        graph, pm, cache, samples = _setup(L, partial)
         F, C = 12, 4
         feats_host = sg.synthetic_features(graph.num_vertices, F, seed=1)
         feats = sg.FeatureStore.from_host(feats_host, cache, devices=[rank])  # own shard only
@@ -70,14 +72,14 @@ def _worker(rank, world, port, kind, captured, q):
         dist.destroy_process_group()
 
 
-def _run(kind, captured, port):
+def _run(kind, captured, port, partial=False):
     from oracle.coop_oracle import CoopRun, reduce_and_sgd
     from oracle.model_oracle import glorot_params
     from oracle.split_oracle import split_sample
     import paper_2303_13775_b200 as sg
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, captured, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, captured, q, partial)) for r in range(2)]
     for p in procs:
         p.start()
     import queue
@@ -97,7 +99,7 @@ def _run(kind, captured, port):
     assert np.array_equal(p0, p1)            # replicas identical (rank-order sum on every rank)
     assert l0 == l1
     L = 3 if captured else 2
-    graph, pm, cache, samples = _setup(L)
+    graph, pm, cache, samples = _setup(L, partial)
     F, C = 12, 4
     X = sg.synthetic_features(graph.num_vertices, F, seed=1).astype(np.float64)
     labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
@@ -118,3 +120,11 @@ def test_peer_transport_eager_two_processes(kind):
 
 def test_peer_transport_captured_step_two_processes():
     _run("graphsage", True, 35100 + os.getpid() % 2000)
+
+
+@pytest.mark.parametrize("captured", [False, True])
+def test_peer_transport_partial_cache(captured):
+    """A partial per-rank cache: every rank stages its own load list from host
+    memory (sg_stage_misses inside the eager step and inside the captured
+    rank graph) and the replicas still equal the oracle's g = 2 run."""
+    _run("graphsage", captured, 37200 + os.getpid() % 2000 + (11 if captured else 0), partial=True)
