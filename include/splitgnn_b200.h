@@ -490,6 +490,11 @@ int sg_reduce_partials_sgd_nt(const int64_t* jobs, int32_t n_jobs, int64_t max_n
  * p -= lr/num_targets * grads; grads_out (nullable) receives the sum. */
 int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_ptrs, int32_t n_dev,
                int64_t n, float scale, void* stream);
+/* sg_sum_sgd over n1 >= n columns (e.g. the loss slot; only k < n update
+ * params) with scale = lr / *num_targets computed on the device: the
+ * multi-part single-GPU step captured as one CUDA graph. */
+int sg_sum_sgd_nt(float* params, float* grads_out, const int64_t* grad_ptrs, int32_t n_dev,
+                  int64_t n, int64_t n1, double lr, const int64_t* num_targets, void* stream);
 
 /* ---------------------------------------------------------------- host-side native code
  * Synthetic block-planted Chung-Lu power-law graph as an

@@ -15,6 +15,33 @@ import numpy as np
 from oracle.model_oracle import SLOPE, gat_bwd, gat_fwd, softmax_xent
 
 
+def multihead_init(feat_dim, hidden, num_classes, num_layers, seed, heads):
+    """Glorot draws of an H-head GAT in the product's order (each head drawn
+    as a reference single-head layer, models.py:107-142, heads concatenated):
+    per layer, per head (w, a_src, a_dst); then cls.w; biases zero."""
+    rng = np.random.default_rng(seed)
+
+    def draw(fi, fo, shape):
+        lim = np.sqrt(6.0 / (fi + fo))
+        return rng.uniform(-lim, lim, size=shape)
+
+    p = {}
+    width = hidden * heads
+    for i in range(num_layers):
+        d_in = feat_dim if i == 0 else width
+        ws, as_, ad = [], [], []
+        for _ in range(heads):
+            ws.append(draw(d_in, hidden, (d_in, hidden)))
+            as_.append(draw(hidden, 1, (hidden,)))
+            ad.append(draw(hidden, 1, (hidden,)))
+        p[f"layer{i}.w"] = np.concatenate(ws, axis=1)
+        p[f"layer{i}.a_src"] = np.stack(as_)
+        p[f"layer{i}.a_dst"] = np.stack(ad)
+    p["cls.w"] = draw(width, num_classes, (width, num_classes))
+    p["cls.b"] = np.zeros(num_classes)
+    return p
+
+
 def _head_params(p, i, h, dh):
     return {f"layer{i}.w": p[f"layer{i}.w"][:, h * dh:(h + 1) * dh],
             f"layer{i}.a_src": np.asarray(p[f"layer{i}.a_src"])[h],

@@ -43,7 +43,8 @@ from paper_2303_13775_b200.models import DeviceParams, GatLayer, ModelParams, Sa
 from paper_2303_13775_b200.metrics import (EpochMetrics, IterationMetrics, account_transfer, emit_csv, read_csv,
                                            redundancy_report, union_edge_count)
 from paper_2303_13775_b200.features import FeatureStore
-from paper_2303_13775_b200.exchange import LocalTransport, NcclTransport, PeerTransport
+from paper_2303_13775_b200.exchange import (LocalTransport, NcclTransport, PeerTransport, exchange_microbench,
+                                            uniform_exchange_sample)
 from paper_2303_13775_b200.engine import (
     PhaseRunner,
     SplitExecutor,

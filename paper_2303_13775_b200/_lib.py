@@ -144,6 +144,7 @@ _SIGS = {
     "sg_cls_loss": (i32, [vp, P(SgSplitLayout), i32, vp, vp, vp, i32, i32, vp, vp, vp, vp, i32,
                           i64, vp]),
     "sg_reduce_partials": (i32, [vp, i32, i64, vp]),
+    "sg_sum_sgd_nt": (i32, [vp, vp, vp, i32, i64, i64, f64, vp, vp]),
     "sg_sum_sgd": (i32, [vp, vp, vp, i32, i64, f32, vp]),
     "sg_gen_powerlaw": (i32, [i64, i64, i32, f64, f64, u64, i32, vp, vp]),
     "sg_gen_labels": (i32, [i64, i32, u64, vp]),

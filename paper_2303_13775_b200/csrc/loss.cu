@@ -220,6 +220,21 @@ __global__ void k_sum_sgd(float* __restrict__ params, float* __restrict__ gout, 
   }
 }
 
+// sg_sum_sgd with n1 >= n summed columns (the loss slot rides along) and the
+// scale lr / *nt computed on the device.
+__global__ void k_sum_sgd_nt(float* __restrict__ params, float* __restrict__ gout, DevPtrs gptrs,
+                             int ndev, int64_t n, int64_t n1, double lr, const int64_t* __restrict__ nt) {
+  SG_PDL_ENTRY();
+  const float scale = (float)(lr / (double)max(*nt, (int64_t)1));
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n1;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    float s = ((const float*)gptrs.v[0])[k];
+    for (int d = 1; d < ndev; ++d) s += ((const float*)gptrs.v[d])[k];
+    if (gout) gout[k] = s;
+    if (k < n) params[k] -= scale * s;
+  }
+}
+
 }  // namespace
 
 extern "C" int sg_cls_loss(const void* split_ws, const SgSplitLayout* lay, int32_t d,
@@ -313,6 +328,20 @@ extern "C" int sg_sum_sgd(float* params, float* grads_out, const int64_t* grad_p
   for (int d = 0; d < n_dev; ++d) gp.v[d] = grad_ptrs[d];
   ::sg::launch(k_sum_sgd, clamp_grid(div_up(n, 256), kSMs * 4), 256, 0, (cudaStream_t)stream, params, grads_out, gp, n_dev, n, scale);
   SG_CHECK_LAUNCH("k_sum_sgd");
+  return SG_OK;
+}
+
+extern "C" int sg_sum_sgd_nt(float* params, float* grads_out, const int64_t* grad_ptrs, int32_t n_dev,
+                             int64_t n, int64_t n1, double lr, const int64_t* num_targets, void* stream) {
+  SG_REQUIRE(params && grad_ptrs && num_targets && n_dev >= 1 && n_dev <= SG_MAXG && n1 >= n,
+             "sum_sgd_nt: bad arguments");
+  if (n1 <= 0) return SG_OK;
+  DevPtrs gp;
+  memset(&gp, 0, sizeof(gp));
+  for (int d = 0; d < n_dev; ++d) gp.v[d] = grad_ptrs[d];
+  ::sg::launch(k_sum_sgd_nt, clamp_grid(div_up(n1, 256), kSMs * 4), 256, 0, (cudaStream_t)stream, params, grads_out,
+               gp, n_dev, n, n1, lr, num_targets);
+  SG_CHECK_LAUNCH("k_sum_sgd_nt");
   return SG_OK;
 }
 

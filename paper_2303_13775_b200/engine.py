@@ -1149,15 +1149,17 @@ def capacities_for(samples, slack=1.0):
 
 
 class CapturedStep:
-    """The whole split-parallel training step of the single-GPU (g = 1) case
-    captured once as a CUDA graph: split -> layer-0 rows -> forward -> loss ->
-    backward -> gradient reduction -> SGD, replayed per sample with only the
-    sample's H2D copy in front. Kernels read every size from device memory."""
+    """The whole split-parallel training step on ONE GPU captured once as a
+    CUDA graph: split -> layer-0 rows (+ cache-miss staging) -> forward ->
+    loss -> backward -> gradient reduction -> SGD, replayed per sample with
+    only the sample's H2D copy in front. Kernels read every size from device
+    memory. g = pm.num_devices parts: g = 1 is the single-GPU split; g > 1
+    runs all g parts on this GPU (the reference's simulated devices, its
+    exchange rounds as copy kernels) and sums their gradients in device
+    order before the SGD step."""
 
     def __init__(self, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale,
                  device="cuda", record_events=False, lr=None):
-        if pm.num_devices != 1:
-            raise ValueError("CapturedStep covers the single-GPU split (g = 1)")
         self.p = dparams
         self.pm, self.cache, self.f, self.labels = pm, cache, feats, labels_dev
         self.dev = torch.device(device)
@@ -1200,9 +1202,20 @@ class CapturedStep:
         if ev:
             step.events["ph:split:s"] = [ev[0]]
             step.events["ph:split:e"] = [ev[1]]
-        step.sgd = (self.p.flat, self.lr, self._num_targets_dev())  # one device: SGD rides on the reduction
+        g = self.pm.num_devices
+        if g == 1:
+            step.sgd = (self.p.flat, self.lr, self._num_targets_dev())  # one device: SGD rides on the reduction
         step.run()
         gbuf = step.grads[0]
+        if g > 1:
+            # g parts on this GPU (the reference's simulated devices): device-order
+            # sum of the per-part gradients (+ loss slot) and the SGD step
+            if getattr(self, "_gsum", None) is None:
+                self._gsum = torch.empty(self.p.n + 1, dtype=torch.float32, device=self.dev)
+            ptrs = np.asarray([step.grads[d].data_ptr() for d in range(g)], dtype=np.int64)
+            _lib.call("sg_sum_sgd_nt", _lib.ptr(self.p.flat), _lib.ptr(self._gsum), _lib.ptr(ptrs), g, self.p.n,
+                      self.p.n + 1, float(self.lr), self._num_targets_dev().data_ptr(), _lib.stream_ptr())
+            gbuf = self._gsum
         self.ds, self.step = ds, step
         return gbuf
 
@@ -1212,7 +1225,7 @@ class CapturedStep:
         untouched parameters restore them afterwards."""
         self._fix_lr(warm_sample)
         self.inp.load(warm_sample)
-        self._body()
+        self.warm_out = self._body()  # the eager warm-up step's gradients (+ loss slot)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
@@ -1320,8 +1333,9 @@ class SampledCapturedStep(CapturedStep):
     `sampler.err`, checked by `check()`)."""
 
     def __init__(self, sampler, fanouts, batch, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE,
-                 lr_scale, device="cuda", record_events=False):
-        super().__init__(dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale, device, record_events)
+                 lr_scale, device="cuda", record_events=False, lr=None):
+        super().__init__(dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale, device, record_events,
+                         lr=lr)
         self.sampler = sampler
         self.fanouts = [int(f) for f in fanouts]
         self.batch = int(batch)

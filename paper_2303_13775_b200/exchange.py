@@ -234,3 +234,76 @@ class PeerTransport:
         """Raise if a peer wait timed out (a peer process is gone)."""
         if int(self.timeout.item()):
             raise RuntimeError("peer transport: a peer never signalled (timed out)")
+
+
+# ---- C5 microbenchmark -----------------------------------------------------------------
+
+def uniform_exchange_sample(rows, g):
+    """A one-layer sample whose split plan is a uniform all-to-all: device o
+    owns `rows` destinations, each with an in-edge from one source vertex of
+    every other device, so every (holder, owner) pair holds exactly `rows`
+    reference rows (pair_count = rows * g * (g - 1)). Returns (sample, pm)."""
+    import numpy as np
+
+    from paper_2303_13775_b200.partition import PartitionMap
+    from paper_2303_13775_b200.sampling import MiniBatchSample
+    nt = g * rows
+    asn = np.concatenate([np.repeat(np.arange(g), rows), np.arange(g)]).astype(np.int64)
+    pm = PartitionMap(asn, g, float(g))
+    tgt = np.arange(nt, dtype=np.int64)
+    V0 = np.arange(nt + g, dtype=np.int64)
+    own = tgt // rows
+    # per destination: self edge, then one edge from every foreign device's source
+    srcs = np.broadcast_to(np.arange(g, dtype=np.int64), (nt, g))
+    keep = srcs != own[:, None]
+    cross = (nt + srcs[keep]).reshape(nt, g - 1)
+    src = np.concatenate([tgt[:, None], cross], axis=1).reshape(-1)
+    dst = np.repeat(tgt, g)
+    return MiniBatchSample(1, [V0, tgt], [(src, dst)], dst_grouped=True), pm
+
+
+def exchange_microbench(rows, width, world=1, rank=0, device=None, parts=8, steps=20, warmup=3, transport=None):
+    """Time the split's push-to-owner round on a uniform plan (rows per peer,
+    `width` fp32 per row) through the repo's transport: LocalTransport (all
+    `parts` devices on this GPU, sg_xfer_to_owner) at world = 1, the
+    PeerTransport (peer stores + signal/wait) at world > 1. Returns
+    {"ms": per round, "bytes": bytes sent per GPU (world > 1) or read + written
+    (world = 1)}."""
+    import torch
+
+    from paper_2303_13775_b200.scheduler import DeviceSplit
+    g = world if world > 1 else parts
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    smp, pm = uniform_exchange_sample(rows, g)
+    ds = DeviceSplit.from_sample(smp, pm, None, dev)
+    P = ds.pair_bound(1)
+    stride = (width + 3) // 4 * 4
+    if world == 1:
+        tp = LocalTransport()
+        send = torch.rand(P, stride, device=dev)
+        recv = torch.empty(P, stride, device=dev)
+
+        def one():
+            tp.to_owner(ds, 1, send, recv, stride)
+        nbytes = 2 * rows * g * (g - 1) * stride * 4
+    else:
+        tp = transport if transport is not None else PeerTransport(rank, world, device=dev)
+        send = torch.rand(P, stride, device=dev)
+
+        def one():
+            tp.begin_step()
+            recv = tp.shared(P, stride)
+            tp.to_owner(ds, 1, send, recv, stride)
+        nbytes = rows * (g - 1) * stride * 4
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        tp.check()
+    return {"ms": e0.elapsed_time(e1) / steps, "bytes": nbytes, "pairs": int(ds.pair_count(1))}

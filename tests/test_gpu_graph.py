@@ -215,3 +215,43 @@ def test_captured_step_normalises_by_each_samples_target_count():
     got = dp.to_host().tensors()
     for k in ref:
         assert rel_err(got[k], ref[k]) < 1e-4, k
+
+
+@pytest.mark.parametrize("kind,g", [("graphsage", 4), ("graphsage", 8), ("gat", 3)])
+def test_captured_multi_part_step_matches_oracle(kind, g):
+    """g split parts on ONE GPU captured as one graph (bench --parts g, C1's
+    2 partitions): every exchange round is a device copy, sizes never reach
+    the host, and training equals the oracle's cooperative g-part run."""
+    import torch
+
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200.engine import CapturedStep, capacities_for
+    graph = sg.generate_powerlaw(20000, 200000, blocks=16, p_local=0.8, seed=9)
+    pm = sg.range_partition(graph.num_vertices, g)
+    cache = sg.full_cache(pm)
+    F, C, B = 64, 6, 96
+    feats = sg.FeatureStore.synthetic(graph.num_vertices, F, seed=1)
+    hostX = sg.synthetic_features(graph.num_vertices, F, seed=1).astype(np.float64)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=2)
+    rng = np.random.default_rng(3)
+    samples = [sg.sample_minibatch(graph, rng.choice(graph.num_vertices, B, replace=False), [8, 6, 4], rng)
+               for _ in range(4)]
+    cap_nV, cap_nE = capacities_for(samples, slack=1.1)
+    params = sg.init_params(kind, F, 16, C, 3, seed=4)
+    dp = sg.DeviceParams.from_host(params)
+    cs = CapturedStep(dp, pm, cache, feats, torch.from_numpy(labels).cuda(), cap_nV, cap_nE, 0.1 / B)
+    cs.capture(samples[0])
+    losses = [None]
+    for smp in samples[1:]:
+        cs.run(smp)
+        losses.append(float(cs.out[dp.n].item()))
+    ref = glorot_params(kind, F, 16, C, 3, seed=4)
+    for i, smp in enumerate(samples):
+        ws, wp = split_sample(smp.layer_vertices, smp.layer_edges, pm.assignment, g, cache.cached)
+        rl, rg = CoopRun(ref, ws, wp, hostX, labels).run()
+        reduce_and_sgd(ref, rg, 0.1, B)
+        if i > 0:
+            assert abs(losses[i] - rl) <= 1e-4 * abs(rl), (i, losses[i], rl)
+    got = dp.to_host().tensors()
+    for k in ref:
+        assert rel_err(got[k], ref[k]) < 1e-4, k
