@@ -119,6 +119,10 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+// ReLU with NumPy semantics: np.maximum(x, 0) propagates NaN (fmaxf would
+// return 0 and hide it from DEBUG_CHECK_FINITE, engine.py:49-55).
+__device__ __forceinline__ float sg_relu(float x) { return x < 0.f ? 0.f : x; }
+
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 inline int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }

@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256) k_gemm_rows(GemmArgs a) {
         float* cp = a.C + cr * a.ldc + n;
         if (a.accum) v += *cp;
         if (a.bias) v += a.bias[n];
-        if (a.relu) v = fmaxf(v, 0.f);
+        if (a.relu) v = sg_relu(v);
         *cp = v;
       }
     }

@@ -810,7 +810,7 @@ __global__ void k_gat_combine(const SgMeta* __restrict__ meta, CombArgs a) {
     }
     const float nv = U / den;
     a.num[G * dout + j] = nv;
-    a.h[G * dout + j] = a.final_ ? nv : fmaxf(nv, 0.f);
+    a.h[G * dout + j] = a.final_ ? nv : sg_relu(nv);
     if (j - hh * dh == 0) {
       a.md[G * 2 * H + hh] = m;
       a.md[G * 2 * H + H + hh] = den;

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(256, 3) k_sage_linear(const SgMeta* __restrict
       float v = a.bias[j];
 #pragma unroll
       for (int s2 = 0; s2 < NS; ++s2) v += red[(s2 * TM + r) * dout + j];
-      a.h[(int64_t)(own0 + r0 + r) * dout + j] = a.final_ ? v : fmaxf(v, 0.f);
+      a.h[(int64_t)(own0 + r0 + r) * dout + j] = a.final_ ? v : sg_relu(v);
     }
   }
 }
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
       float v = a.bias[j];
 #pragma unroll
       for (int s2 = 0; s2 < NS; ++s2) v += red[(s2 * TM + r) * dout + j];
-      a.h[(int64_t)(own0 + r0 + r) * dout + j] = a.final_ ? v : fmaxf(v, 0.f);
+      a.h[(int64_t)(own0 + r0 + r) * dout + j] = a.final_ ? v : sg_relu(v);
     }
   }
 }
@@ -751,10 +751,10 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
         }
         float4 acc = make_float4(as.x + an.x, as.y + an.y, as.z + an.z, as.w + an.w);
         if (!a.final_) {
-          acc.x = fmaxf(acc.x, 0.f);
-          acc.y = fmaxf(acc.y, 0.f);
-          acc.z = fmaxf(acc.z, 0.f);
-          acc.w = fmaxf(acc.w, 0.f);
+          acc.x = sg_relu(acc.x);
+          acc.y = sg_relu(acc.y);
+          acc.z = sg_relu(acc.z);
+          acc.w = sg_relu(acc.w);
         }
         *reinterpret_cast<float4*>(a.h + (int64_t)(own0 + q) * dout + 4 * jq) = acc;
       }
@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(256) k_sage_update(const SgMeta* __restrict__ 
         const float* mr = mn_s + rr * wp;
         float acc = a.bias[j];
         for (int c = 0; c < w; ++c) acc = fmaf(hr[c], ws_s[c * dout + j], fmaf(mr[c], wn_s[c * dout + j], acc));
-        a.h[(int64_t)(own0 + q) * dout + j] = a.final_ ? acc : fmaxf(acc, 0.f);
+        a.h[(int64_t)(own0 + q) * dout + j] = a.final_ ? acc : sg_relu(acc);
       }
     }
   }

@@ -263,7 +263,9 @@ class SplitStep:
             self.transport.begin_step()
         if self.kind != "graphsage":
             from paper_2303_13775_b200.gat import gat_forward
-            return gat_forward(self)
+            gat_forward(self)
+            self._check_finite()
+            return
         ds, p, st = self.ds, self.p, _lib.stream_ptr()
         self.grads, self._final_rows = None, None
         with self.phase("layer0"):
@@ -366,8 +368,23 @@ class SplitStep:
             self.keep[l] = dict(mean=mean, counts=counts)
             if hs is not None:
                 self.keep[l]["hs"] = hs
-            if DEBUG_CHECK_FINITE and not torch.isfinite(h[:nV]).all():
-                raise FloatingPointError(f"non-finite values in graphsage layer {l} output")
+
+        self._check_finite()
+
+    def _check_finite(self):
+        """engine.py:49-55 (DEBUG_CHECK_FINITE): scan every layer's owned output
+        rows of every local device; FloatingPointError names the first layer
+        with a NaN / Inf. Covers every forward kernel path (one-kernel layers,
+        the fused last layer, owner combine, GAT). Eager steps only: a
+        captured graph cannot branch on device values."""
+        if not DEBUG_CHECK_FINITE or self.meta is None or torch.cuda.is_current_stream_capturing():
+            return
+        for l in range(1, self.L + 1):
+            h = self.h[l]
+            for d in self.devices:
+                b, n = int(self.meta.own_off[l][d]), int(self.meta.n_own[l][d])
+                if n and not bool(torch.isfinite(h[b:b + n]).all()):
+                    raise FloatingPointError(f"non-finite values in {self.kind} layer {l} output")
 
     # -- loss + backward -----------------------------------------------------------
     def _src_csr(self, lmin, val_mode=1):
@@ -763,47 +780,70 @@ def _materialise_states(ex):
     return states
 
 
-def scatter_shuffle_forward(splits, plan, l, owned_rows, runner=None, record=None):
+def scatter_shuffle_forward(splits, plan, l, owned_rows, runner=None, record=None, transport=None):
     """engine.py:591-630: fill every device's reference rows at layer l from
-    the owners' rows (one push-from-owner round on the GPU)."""
+    the owners' rows (one push-from-owner round on the GPU).
+
+    transport=None moves all g devices' rows in this process (LocalTransport:
+    one copy kernel). With a rank transport (NcclTransport / PeerTransport)
+    this process is device `transport.rank`: only owned_rows[rank] is read
+    (the other entries may be None), its rows are packed into the round's
+    buffer, the round runs over NCCL / peer memory, and the returned list holds
+    this device's reference rows at index `rank` (other entries empty).
+    Meters pair_count(l) * width * 8 bytes like the reference (:620-627)."""
     ds = getattr(splits, "device_split", None) or getattr(plan, "device_split", None)
     if ds is None:
         raise TypeError("splits must come from paper_2303_13775_b200.split_minibatch")
     m = ds.host_meta()
+    devices = list(range(ds.g)) if transport is None else [int(transport.rank)]
+    if transport is not None and int(getattr(transport, "world", ds.g)) != ds.g:
+        raise ValueError("transport world size differs from the split's device count")
     width = 0
-    for r in owned_rows:
-        if np.ndim(r) == 2:
+    for d in devices:
+        r = owned_rows[d]
+        if r is not None and np.ndim(r) == 2:
             width = int(np.shape(r)[1])
             break
+    if transport is not None and width == 0 and ds.pair_bound(l) > 0:
+        raise ValueError("owned_rows[rank] must be a 2-D array (rows x width, rows may be 0): "
+                         "every rank needs the round's width")
     if record is not None:
         account_transfer(record, "peer", int(m.npairs[l]) * width * 8)
     nV = ds.nV[l]
     rows = torch.zeros((max(nV, 1), max(width, 1)), dtype=torch.float32, device=ds.device)
-    for d, r in enumerate(owned_rows):
+    for d in devices:
         n = int(m.n_own[l][d])
         if n and width:
             b = int(m.own_off[l][d])
-            rows[b:b + n] = torch.as_tensor(np.asarray(r, dtype=np.float32), device=ds.device)
-    out = []
+            rows[b:b + n] = torch.as_tensor(np.asarray(owned_rows[d], dtype=np.float32).reshape(n, width),
+                                            device=ds.device)
     P = ds.pair_bound(l)
+    host = None
     if ds.g > 1 and P > 0 and width:
-        stride = width
-        bsend = _f32(P, stride, device=ds.device)
+        stride = _r4(width)
+        tp = transport or LocalTransport()
+        if hasattr(tp, "begin_step"):
+            tp.begin_step()
+        shared = getattr(tp, "shared", None)
+        bsend = shared(P, stride) if shared is not None else _f32(P, stride, device=ds.device)
         brecv = _f32(P, stride, device=ds.device)
         st = _lib.stream_ptr()
-        for d in range(ds.g):
+        for d in devices:
             _lib.call("sg_pack_from_owner", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(rows), width,
                       _lib.ptr(bsend), stride, int(m.recv_off[l][d + 1] - m.recv_off[l][d]), st)
-        LocalTransport().from_owner(ds, l, bsend, brecv, stride)
+        tp.from_owner(ds, l, bsend, brecv, stride)
         refs = _f32(P, width, device=ds.device)
-        for d in range(ds.g):
+        for d in devices:
             _lib.call("sg_unpack_refs", _lib.ptr(ds.ws), ds.lay, l, d, _lib.ptr(brecv), stride, width,
                       _lib.ptr(refs), int(m.n_ref[l][d]), st)
         host = refs.double().cpu().numpy()
+        if hasattr(tp, "check"):
+            tp.check()
+    out = []
     for d in range(ds.g):
         n = int(m.n_ref[l][d])
-        if n == 0 or width == 0:
-            out.append(np.zeros((n, width)))
+        if d not in devices or n == 0 or width == 0 or host is None:
+            out.append(np.zeros((n if d in devices else 0, width)))
         else:
             b = int(m.ref_off[l][d])
             out.append(host[b:b + n].copy())

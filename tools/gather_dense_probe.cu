@@ -162,3 +162,42 @@ extern "C" int probe_bulk(int variant, const float* tab, const int* idx, int n, 
   }
   return (int)cudaGetLastError();
 }
+
+// Projection-shaped gathers at the projection's occupancy: tile = 128 rows x 25
+// chunks, 256 threads, NLD = 13 float4 per thread, all in flight. pattern 0: a
+// warp instruction covers 8 rows x 4 chunks (the plane-friendly mapping);
+// pattern 1: a warp instruction covers one row's 25 chunks (row-contiguous).
+template <int PAT>
+__global__ void __launch_bounds__(256, 1) k_tile(const float4* __restrict__ tab, const int* __restrict__ idx, int n,
+                                                int S4, float* __restrict__ out) {
+  const int tid = threadIdx.x;
+  const int ntiles = (n + 127) / 128;
+  float acc = 0.f;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    float4 R[13];
+#pragma unroll
+    for (int j = 0; j < 13; ++j) {
+      int m, c;
+      if (PAT == 0) {
+        const int i = tid + 256 * j, rest = i >> 3;
+        c = rest % 26;
+        m = (rest / 26) * 8 + (i & 7);
+      } else {
+        const int warp = tid >> 5, lane = tid & 31;
+        m = warp * 16 + j + (j >= 13 ? 0 : 0);  // rows warp*16 .. +12 (13 of 16 rows, enough for the probe)
+        c = lane;
+      }
+      const int r = t * 128 + m;
+      R[j] = (m < 128 && c < 25 && r < n) ? __ldg(tab + (size_t)idx[r] * S4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < 13; ++j) acc += R[j].x + R[j].y + R[j].z + R[j].w;
+  }
+  out[blockIdx.x * 256 + tid] = acc;
+}
+
+extern "C" int probe_tile(int pat, const float* tab, const int* idx, int n, int S4, float* out, int blocks) {
+  if (pat == 0) k_tile<0><<<blocks, 256>>>((const float4*)tab, idx, n, S4, out);
+  else k_tile<1><<<blocks, 256>>>((const float4*)tab, idx, n, S4, out);
+  return (int)cudaGetLastError();
+}
