@@ -462,18 +462,56 @@ int sg_gpu_sample(const int64_t* row_offsets, const int32_t* col_indices, int64_
                   int64_t max_edges, int32_t* V, int32_t* esrc, int32_t* edst, int64_t* sizes, void* ws,
                   int32_t* err, void* stream);
 /* ---- balanced k-way partitioning (partition.py:236-349) --------------------
- * sg_partition_cut: directed arcs whose endpoints lie in different parts.
- * sg_partition_round: one parallel refinement round on the symmetrised graph
- * (in-CSR + out-CSR, g <= 16 parts, part sizes <= cap): seeded half of the
- * vertices propose their best strictly positive gain move (lowest part on
- * ties), admitted per target in descending gain within the cap; updates part
- * and sizes; ws >= 8n + 4 * 16 * 65 bytes; *moved_out = moves (device). */
+ * Multilevel, on symmetric weighted level graphs (off int64[n+1], nbr int32,
+ * wt int32 edge weights, vw int32 vertex weights; level 0 = the input graph
+ * symmetrised, weight = arcs u->v + arcs v->u, partition.py:123-136).
+ * sg_partition_cut: directed arcs whose endpoints lie in different parts, on
+ *   the input in-CSR (cut_size, partition.py:352-355).
+ * sg_partition_cut_w: sum of wt over level-graph entries across parts (twice
+ *   the directed cut at level 0).
+ * sg_partition_sizes: part weights under vw (nullable: unit weights).
+ * sg_partition_match_round: one heavy-edge matching round (partition.py:144-175
+ *   restated as locally-dominant-edge matching): unmatched vertices (match < 0)
+ *   pick the heaviest unmatched neighbour with vw[u] + vw[v] <= wcap (ties by a
+ *   pair-symmetric seeded hash); mutual picks are matched. ws >= 4n bytes;
+ *   *matched_out accumulates the matched vertices (device).
+ * sg_partition_round: one parallel refinement round (partition.py:236-270):
+ *   a seeded half of the vertices propose their best strictly positive gain
+ *   move (lowest part on ties), admitted per target part in descending gain
+ *   within the weight cap; updates part and sizes; ws >= 8n + 8*16*64 + 64
+ *   bytes; *moved_out = moves (device).
+ * sg_partition_coarse_host (HOST memory, CPU): the coarsest level's initial
+ *   partition (partition.py:186-233): greedy region growing + sequential
+ *   refinement, best of `restarts` (a feasible partition preferred); writes
+ *   part_out[n] and *cut_out (level cut, directed-arc units). */
 int sg_partition_cut(const int64_t* row_offsets, const int32_t* col_indices, int64_t n, const int32_t* part,
                      unsigned long long* cut_out, void* stream);
-int sg_partition_round(const int64_t* row_offsets, const int32_t* col_indices, const int64_t* out_offsets,
-                       const int32_t* out_indices, int64_t n, int32_t g, int64_t cap, uint64_t seed,
-                       int32_t round, int32_t* part, int64_t* sizes, void* ws, unsigned long long* moved_out,
-                       void* stream);
+int sg_partition_cut_w(const int64_t* off, const int32_t* nbr, const int32_t* wt, int64_t n, const int32_t* part,
+                       unsigned long long* cut_out, void* stream);
+int sg_partition_sizes(const int32_t* part, const int32_t* vw, int64_t n, int32_t g, int64_t* sizes, void* stream);
+int sg_partition_match_round(const int64_t* off, const int32_t* nbr, const int32_t* wt, const int32_t* vw,
+                             int64_t n, int64_t wcap, uint64_t seed, int32_t round, int32_t* match, void* ws,
+                             unsigned long long* matched_out, void* stream);
+int sg_partition_round(const int64_t* off, const int32_t* nbr, const int32_t* wt, const int32_t* vw, int64_t n,
+                       int32_t g, int64_t cap, uint64_t seed, int32_t round, int32_t* part, int64_t* sizes,
+                       void* ws, unsigned long long* moved_out, void* stream);
+int sg_partition_coarse_host(int64_t n, const int64_t* off, const int32_t* nbr, const int32_t* wt,
+                             const int32_t* vw, int32_t g, int64_t cap, uint64_t seed, int32_t restarts,
+                             int32_t* part_out, int64_t* cut_out);
+/* sg_partition_refine_host (HOST memory, CPU): sequential boundary refinement
+ * of one level (partition.py:236-270: overfull parts repaired, then strictly
+ * positive gain moves within cap, ascending id, lowest part on ties) for the
+ * levels small enough for one core; part updated in place, *cut_out = level cut. */
+/* sg_pack_sample (HOST memory, CPU): a sample's arrays (V^0..V^L, E^l sources,
+ * E^l destinations; each int32 or int64, elem_bytes 4 / 8) copied as int32 to
+ * out + dst_off[i] (words), after an int64 header of the 2L+1 sizes
+ * [nV_0..nV_L, nE_1..nE_L]; split over `threads` host threads (0 = all).
+ * split_minibatch's staging of the sample (scheduler.py:164). */
+int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, const int64_t* dst_off, const void* const* src,
+                   const int32_t* elem_bytes, int32_t threads);
+int sg_partition_refine_host(int64_t n, const int64_t* off, const int32_t* nbr, const int32_t* wt,
+                             const int32_t* vw, int32_t g, int64_t cap, int32_t max_passes, int32_t* part,
+                             int64_t* cut_out);
 /* sg_reduce_partials with the SGD step fused (single device, nothing to
  * all-reduce): jobs are 6 int64 per job {partials, nblocks, n, out, param,
  * n_sgd}; the first n_sgd summed columns g also update param: p -= scale*g

@@ -317,3 +317,263 @@ extern "C" int sg_sampler_fetch(void* h, int32_t* V, int32_t* esrc, int32_t* eds
   }
   return SG_OK;
 }
+
+// ---------------------------------------------------------------- coarsest-level partition
+// Initial partition of the coarsest level of the multilevel partitioner
+// (partition.py drives the GPU levels; the contract is reference
+// partition.py:186-233 + 236-270: greedy region growing, best of a few
+// restarts after sequential boundary refinement, every part within cap).
+// Symmetric weighted CSR (off, nbr, wt), vertex weights vw.
+namespace {
+
+struct CoarseGraph {
+  int64_t n;
+  const int64_t* off;
+  const int32_t* nbr;
+  const int32_t* wt;
+  const int32_t* vw;
+};
+
+int64_t coarse_cut(const CoarseGraph& G, const std::vector<int32_t>& part) {
+  int64_t c = 0;
+  for (int64_t v = 0; v < G.n; ++v)
+    for (int64_t j = G.off[v]; j < G.off[v + 1]; ++j)
+      if (part[G.nbr[j]] != part[v]) c += G.wt[j];
+  return c / 2;
+}
+
+// Grow parts 0..g-2 one at a time from a seeded start vertex, always taking the
+// unassigned vertex most connected to the growing part (ties by a seeded hash);
+// the last part takes the rest.
+void grow(const CoarseGraph& G, int g, int64_t cap, uint64_t seed, std::vector<int32_t>& part) {
+  const int64_t n = G.n;
+  part.assign(n, -1);
+  int64_t total = 0;
+  for (int64_t v = 0; v < n; ++v) total += G.vw[v];
+  std::vector<int64_t> conn(n, 0);
+  std::vector<int64_t> unassigned(n);
+  std::iota(unassigned.begin(), unassigned.end(), 0);
+  int64_t left = total, n_left = n;
+  typedef std::pair<std::pair<int64_t, uint64_t>, int64_t> Item;
+  for (int p = 0; p < g - 1 && n_left > 0; ++p) {
+    const int64_t target = left / (g - p);
+    std::vector<Item> heap;
+    std::vector<int64_t> touched;
+    auto push = [&](int64_t v) {
+      heap.push_back({{conn[v], sg_hash3(seed, (uint64_t)v, (uint64_t)p)}, v});
+      std::push_heap(heap.begin(), heap.end());
+    };
+    int64_t wp = 0;
+    // a seeded unassigned vertex that still fits the part (scanning on from a
+    // random position); false when none does
+    auto random_start = [&]() {
+      int64_t k = 0;
+      for (int64_t v : unassigned)
+        if (part[v] < 0) unassigned[k++] = v;
+      unassigned.resize(k);
+      if (k == 0) return false;
+      const int64_t r = (int64_t)sg_bounded(sg_hash3(seed, 0x5eedull + p, (uint64_t)k), (uint64_t)k);
+      for (int64_t i = 0; i < k; ++i) {
+        const int64_t v = unassigned[(r + i) % k];
+        if (wp + G.vw[v] <= cap) {
+          push(v);
+          return true;
+        }
+      }
+      return false;
+    };
+    if (!random_start()) continue;
+    while (wp < target && n_left > 0) {
+      if (heap.empty() && !random_start()) break;
+      std::pop_heap(heap.begin(), heap.end());
+      const Item it = heap.back();
+      heap.pop_back();
+      const int64_t v = it.second;
+      if (part[v] >= 0 || it.first.first != conn[v]) continue;  // taken or stale
+      if (wp + G.vw[v] > cap) continue;
+      part[v] = p;
+      wp += G.vw[v];
+      left -= G.vw[v];
+      --n_left;
+      for (int64_t j = G.off[v]; j < G.off[v + 1]; ++j) {
+        const int64_t x = G.nbr[j];
+        if (part[x] >= 0) continue;
+        if (conn[x] == 0) touched.push_back(x);
+        conn[x] += G.wt[j];
+        push(x);
+      }
+    }
+    for (int64_t x : touched) conn[x] = 0;
+  }
+  for (int64_t v = 0; v < n; ++v)
+    if (part[v] < 0) part[v] = g - 1;
+}
+
+// Sequential boundary refinement: first repair overfull parts (move the vertex
+// whose move loses the least into a part with room), then passes of strictly
+// positive gain moves within the cap (lowest part on ties) until none applies.
+void refine_seq(const CoarseGraph& G, int g, int64_t cap, std::vector<int32_t>& part, int max_passes) {
+  const int64_t n = G.n;
+  std::vector<int64_t> size(g, 0);
+  for (int64_t v = 0; v < n; ++v) size[part[v]] += G.vw[v];
+  std::vector<int64_t> conn(g);
+  auto connect = [&](int64_t v) {
+    std::fill(conn.begin(), conn.end(), 0);
+    for (int64_t j = G.off[v]; j < G.off[v + 1]; ++j)
+      if (G.nbr[j] != v) conn[part[G.nbr[j]]] += G.wt[j];
+  };
+  for (int guard = 0; guard < 4 * n + 8; ++guard) {
+    int a = -1;
+    for (int p = 0; p < g; ++p)
+      if (size[p] > cap && (a < 0 || size[p] > size[a])) a = p;
+    if (a < 0) break;
+    int64_t bv = -1, bgain = 0;
+    int bq = -1;
+    for (int64_t v = 0; v < n; ++v) {
+      if (part[v] != a) continue;
+      connect(v);
+      for (int q = 0; q < g; ++q) {
+        if (q == a || size[q] + G.vw[v] > cap) continue;
+        const int64_t gain = conn[q] - conn[a];
+        if (bv < 0 || gain > bgain) {
+          bv = v;
+          bgain = gain;
+          bq = q;
+        }
+      }
+    }
+    if (bv < 0) break;  // nothing fits anywhere: leave it to the caller's check
+    part[bv] = bq;
+    size[a] -= G.vw[bv];
+    size[bq] += G.vw[bv];
+  }
+  for (int pass = 0; pass < max_passes; ++pass) {
+    int64_t moved = 0;
+    for (int64_t v = 0; v < n; ++v) {
+      connect(v);
+      const int a = part[v];
+      int best = -1;
+      int64_t bgain = 0;
+      for (int q = 0; q < g; ++q) {
+        if (q == a || size[q] + G.vw[v] > cap) continue;
+        const int64_t gain = conn[q] - conn[a];
+        if (gain > bgain) {
+          bgain = gain;
+          best = q;
+        }
+      }
+      if (best >= 0) {
+        part[v] = best;
+        size[a] -= G.vw[v];
+        size[best] += G.vw[v];
+        ++moved;
+      }
+    }
+    if (!moved) break;
+  }
+}
+
+}  // namespace
+
+extern "C" int sg_partition_coarse_host(int64_t n, const int64_t* off, const int32_t* nbr, const int32_t* wt,
+                                        const int32_t* vw, int32_t g, int64_t cap, uint64_t seed,
+                                        int32_t restarts, int32_t* part_out, int64_t* cut_out) {
+  if (n < 0 || g < 1 || (n > 0 && (!off || !nbr || !wt || !vw)) || !part_out || !cut_out) {
+    sg::set_error("partition_coarse_host: bad argument");
+    return SG_ERR_ARG;
+  }
+  const CoarseGraph G{n, off, nbr, wt, vw};
+  std::vector<int32_t> part, best;
+  int64_t best_cut = -1;
+  bool best_ok = false;
+  for (int r = 0; r < std::max(1, (int)restarts); ++r) {
+    grow(G, g, cap, sg_hash3(seed, 0xC0A55ull, (uint64_t)r), part);
+    refine_seq(G, g, cap, part, 10);
+    std::vector<int64_t> size(g, 0);
+    for (int64_t v = 0; v < n; ++v) size[part[v]] += vw[v];
+    const bool ok = *std::max_element(size.begin(), size.end()) <= cap;
+    const int64_t cut = coarse_cut(G, part);
+    if (best_cut < 0 || (ok && !best_ok) || (ok == best_ok && cut < best_cut)) {
+      best = part;
+      best_cut = cut;
+      best_ok = ok;
+    }
+  }
+  std::memcpy(part_out, best.data(), sizeof(int32_t) * n);
+  *cut_out = best_cut;
+  return SG_OK;
+}
+
+// Sequential boundary refinement of one level (partition.py:236-270 semantics:
+// overfull parts repaired first, then passes of strictly positive gain moves
+// within the cap, ascending vertex id, lowest part on ties). The multilevel
+// driver runs it on the levels small enough for one core; larger levels are
+// refined by the parallel GPU rounds (sg_partition_round).
+extern "C" int sg_partition_refine_host(int64_t n, const int64_t* off, const int32_t* nbr, const int32_t* wt,
+                                        const int32_t* vw, int32_t g, int64_t cap, int32_t max_passes,
+                                        int32_t* part, int64_t* cut_out) {
+  if (n < 0 || g < 1 || (n > 0 && (!off || !nbr || !wt || !vw || !part)) || !cut_out) {
+    sg::set_error("partition_refine_host: bad argument");
+    return SG_ERR_ARG;
+  }
+  const CoarseGraph G{n, off, nbr, wt, vw};
+  std::vector<int32_t> p(part, part + n);
+  refine_seq(G, g, cap, p, max_passes);
+  std::memcpy(part, p.data(), sizeof(int32_t) * n);
+  *cut_out = coarse_cut(G, p);
+  return SG_OK;
+}
+
+// ---------------------------------------------------------------- sample packing
+// split_minibatch's host side (scheduler.py:164 entry): the sample's arrays
+// (V^0..V^L, then E^l sources, then E^l destinations; int32 or int64 each)
+// copied as int32 into one pinned buffer at the given word offsets, after a
+// header of the sizes as int64 [nV_0..nV_L, nE_1..nE_L]. The copy is split
+// evenly over `threads` host threads (it is a few MB per C2 sample).
+extern "C" int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, const int64_t* dst_off,
+                              const void* const* src, const int32_t* elem_bytes, int32_t threads) {
+  if (!out || L < 1 || !sizes || !dst_off || !src || !elem_bytes) {
+    sg::set_error("pack_sample: bad argument");
+    return SG_ERR_ARG;
+  }
+  const int narr = 3 * L + 1;
+  std::memcpy(out, sizes, sizeof(int64_t) * (2 * L + 1));
+  std::vector<int64_t> len(narr), start(narr + 1, 0);
+  for (int i = 0; i < narr; ++i) {
+    len[i] = i <= L ? sizes[i] : sizes[L + 1 + (i - L - 1) % L];
+    if (elem_bytes[i] != 4 && elem_bytes[i] != 8 && len[i] > 0) {
+      sg::set_error("pack_sample: element size must be 4 or 8");
+      return SG_ERR_ARG;
+    }
+    start[i + 1] = start[i] + len[i];
+  }
+  const int64_t total = start[narr];
+  auto copy_range = [&](int64_t a, int64_t b) {  // global element range [a, b)
+    int i = (int)(std::upper_bound(start.begin(), start.end(), a) - start.begin()) - 1;
+    while (a < b && i < narr) {
+      const int64_t e = std::min(b, start[i + 1]);
+      if (e > a) {
+        const int64_t o = a - start[i], k = e - a;
+        int32_t* dst = out + dst_off[i] + o;
+        if (elem_bytes[i] == 4) {
+          std::memcpy(dst, (const int32_t*)src[i] + o, 4 * k);
+        } else {
+          const int64_t* s = (const int64_t*)src[i] + o;
+          for (int64_t j = 0; j < k; ++j) dst[j] = (int32_t)s[j];
+        }
+      }
+      a = e;
+      ++i;
+    }
+  };
+  const int T = std::max(1, std::min<int>(pick_threads(threads), (int)(total / (1 << 16)) + 1));
+  if (T == 1) {
+    copy_range(0, total);
+    return SG_OK;
+  }
+  std::vector<std::thread> pool;
+  for (int t = 0; t < T; ++t)
+    pool.emplace_back(copy_range, total * t / T, total * (t + 1) / T);
+  for (auto& th : pool) th.join();
+  return SG_OK;
+}

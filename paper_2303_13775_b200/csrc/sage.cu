@@ -1292,6 +1292,119 @@ __global__ void __launch_bounds__(256) k_sage_scatter(const SgMeta* __restrict__
   }
 }
 
+// Narrow rows (w <= 4 LPR floats): one LPR-lane group per source row, 32/LPR
+// rows per warp. Most source rows have a handful of out-edges (C2 layer 2:
+// 40K edges over 27K rows), so a warp per row idled most lanes through a
+// chain of dependent loads; here each group walks its row's out-edges in
+// order, four row loads in flight. Rows with more than SC_HEAVY out-edges
+// (power-law hubs) are summed by the whole warp afterwards, as in
+// k_sage_scatter (lane groups take every (32/LPR)-th edge, fixed xor tree).
+constexpr int SC_HEAVY = 12;
+
+template <int LPR>
+__global__ void __launch_bounds__(256) k_sage_scatter_grp(const SgMeta* __restrict__ meta, ScatArgs a) {
+  SG_PDL_ENTRY();
+  constexpr int RW = 32 / LPR;
+  const int l = a.l, d = a.d, w = a.w;
+  const int n_prev = meta->n_own[l - 1][d];
+  const int prev0 = meta->own_off[l - 1][d];
+  const int own0 = meta->own_off[l][d];
+  const int64_t nVl = meta->nV[l];
+  const int lane = threadIdx.x & 31;
+  const int gi = lane / LPR, lr = lane % LPR;
+  const int col = lr * 4;
+  const bool colok = col < w;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  auto row_of = [&](int code) -> const float* {
+    return code >= 0 ? a.d_sums + (int64_t)code * w : a.bwd_recv + (int64_t)(-code - 1) * a.stride;
+  };
+  auto load = [&](int code) -> float4 {
+    const float* row = row_of(code);
+    if (code >= 0 || (a.stride & 3) == 0) return __ldg(reinterpret_cast<const float4*>(row + col));
+    return make_float4(row[col], row[col + 1], row[col + 2], row[col + 3]);
+  };
+  for (int64_t u0 = gw * RW; u0 < n_prev; u0 += nw * RW) {
+    const int64_t u = u0 + gi;
+    const bool valid = u < n_prev;
+    const int64_t U = prev0 + u;
+    int b = 0, e = 0, p = (int)nVl;
+    if (valid) {
+      b = a.srcbeg[a.key_base + U];
+      e = a.srcend[a.key_base + U];
+      p = a.grouped[a.voff_lm1 + U];
+    }
+    const int64_t v = (valid && p < nVl) ? own0 + a.rank[a.voff_l + p] : -1;
+    const bool heavy = e - b > SC_HEAVY;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid && !heavy) {
+      for (int j = b; j < e; j += 4) {
+        int code[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) code[t] = j + t < e ? a.enc[j + t] : 0;
+        float4 x[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          x[t] = (j + t < e && colok) ? load(code[t]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          acc.x += x[t].x; acc.y += x[t].y; acc.z += x[t].z; acc.w += x[t].w;
+        }
+      }
+    }
+    unsigned hm = __ballot_sync(0xffffffffu, valid && heavy && lr == 0);
+    while (hm) {
+      const int owner = __ffs(hm) - 1;
+      hm &= hm - 1;
+      const int hb = __shfl_sync(0xffffffffu, b, owner), he = __shfl_sync(0xffffffffu, e, owner);
+      // 32 edges per chunk: every round's row load issued before any add,
+      // the next chunk's edge codes fetched while this chunk's rows land
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      int my = hb + lane < he ? a.enc[hb + lane] : 0;
+      for (int jb = hb; jb < he; jb += 32) {
+        const int cnt = min(32, he - jb);
+        const int nxt = jb + 32 + lane < he ? a.enc[jb + 32 + lane] : 0;
+        float4 x[LPR];
+#pragma unroll
+        for (int kk = 0; kk < LPR; ++kk) {  // LPR rounds of RW lane groups cover 32 edges
+          const int k = kk * RW + gi;
+          const int code = __shfl_sync(0xffffffffu, my, k);
+          x[kk] = (k < cnt && colok) ? load(code) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int kk = 0; kk < LPR; ++kk) {
+          t.x += x[kk].x; t.y += x[kk].y; t.z += x[kk].z; t.w += x[kk].w;
+        }
+        my = nxt;
+      }
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1) {
+        t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+        t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+        t.z += __shfl_xor_sync(0xffffffffu, t.z, o);
+        t.w += __shfl_xor_sync(0xffffffffu, t.w, o);
+      }
+      if (gi == owner / LPR) acc = t;
+    }
+    if (valid && colok) {
+      if (v >= 0) {
+        float4 s = __ldg(reinterpret_cast<const float4*>(a.d_self + v * w + col));
+        s.x += acc.x; s.y += acc.y; s.z += acc.z; s.w += acc.w;
+        acc = s;
+      }
+      *reinterpret_cast<float4*>(a.d_prev + U * w + col) = acc;
+    }
+  }
+}
+
+template <int LPR>
+int launch_scat_grp(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaStream_t st) {
+  const int grid = clamp_grid(div_up(max_rows, 8 * (32 / LPR)), kSMs * 8);
+  ::sg::launch(k_sage_scatter_grp<LPR>, grid, 256, 0, st, meta, a);
+  SG_CHECK_LAUNCH("k_sage_scatter_grp");
+  return SG_OK;
+}
+
 template <int VEC, int LPR, int NCH>
 int launch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaStream_t st) {
   const int grid = clamp_grid(div_up(max_rows, 8), kSMs * 8);
@@ -1302,6 +1415,12 @@ int launch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaStr
 
 int dispatch_scat(const SgMeta* meta, const ScatArgs& a, int64_t max_rows, cudaStream_t st) {
   const int w = a.w;
+  if (w % 4 == 0 && w <= 32 && std::getenv("SG_SCATTER_WARP") == nullptr) {
+    if (w <= 4) return launch_scat_grp<1>(meta, a, max_rows, st);
+    if (w <= 8) return launch_scat_grp<2>(meta, a, max_rows, st);
+    if (w <= 16) return launch_scat_grp<4>(meta, a, max_rows, st);
+    return launch_scat_grp<8>(meta, a, max_rows, st);
+  }
   if (w % 4 == 0) {
     if (w <= 16) return launch_scat<4, 4, 1>(meta, a, max_rows, st);
     if (w <= 32) return launch_scat<4, 8, 1>(meta, a, max_rows, st);

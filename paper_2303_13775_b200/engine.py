@@ -15,7 +15,9 @@ Trainer / train_model (:655-870).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
+import gc
 import os
 
 import time
@@ -38,6 +40,24 @@ NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions (meas
 # transposed SpMM (tspmm.cu); below it hub rows are short (max out-degree
 # ~25-125 at C2 layers 2-3) and the single-kernel row-per-warp path is faster
 TSPMM_MIN_EDGES = int(os.environ.get("SG_TSPMM_MIN_EDGES", "65536"))  # load-balanced transposed SpMM from this many edges
+
+
+@contextlib.contextmanager
+def _capturing(graph):
+    """CUDA-graph capture that other threads' CUDA calls cannot invalidate
+    (thread-local capture mode) and that no garbage collection interrupts: a
+    collected step object's destructor frees pinned memory (cudaFreeHost), which
+    is illegal while a capture is open (seen as an intermittent
+    cudaErrorStreamCaptureInvalidated in back-to-back tests)."""
+    was = gc.isenabled()
+    gc.collect()
+    gc.disable()
+    try:
+        with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+            yield
+    finally:
+        if was:
+            gc.enable()
 
 
 def _nblocks(rows, tile=32):
@@ -665,9 +685,30 @@ def _labels_dev(labels, device):
 
 class GradDict(dict):
     """dict name -> float64 ndarray (reference type) that also carries the
-    device-resident fp32 flat gradient for allreduce_and_step."""
+    device-resident fp32 flat gradient for allreduce_and_step. Built from the
+    device on first access (a caller that only hands it to
+    allreduce_and_step never pays the D2H)."""
 
     device_flat = None
+    dparams = None
+
+    def __init__(self, data=None, dparams=None, device_flat=None):
+        super().__init__(data or {})
+        self.dparams, self.device_flat = dparams, device_flat
+        self._lazy = data is None and device_flat is not None
+
+    def _fill(self):
+        if self._lazy:
+            self._lazy = False
+            dict.update(self, self.dparams.grads_to_dict(self.device_flat))
+
+    for _m in ("__getitem__", "__iter__", "__len__", "__contains__", "__repr__", "__eq__", "keys", "values",
+               "items", "get", "copy"):
+        def _wrap(self, *a, _name=_m, **k):
+            self._fill()
+            return getattr(dict, _name)(self, *a, **k)
+        locals()[_m] = _wrap
+    del _m, _wrap
 
 
 class _StateView:
@@ -678,9 +719,47 @@ class _StateView:
         self.loss_sum = 0.0
 
 
+class _PinnedFlat:
+    """A pinned host copy of a flat parameter buffer with the event of its
+    last async copy (a buffer is rewritten only after that copy completed)."""
+
+    def __init__(self, n):
+        self.t = torch.empty(n, dtype=torch.float32).pin_memory()
+        self.np = self.t.numpy()
+        self.ev = None
+
+    def wait(self):
+        if self.ev is not None:
+            self.ev.synchronize()
+
+    def record(self):
+        self.ev = torch.cuda.Event()
+        self.ev.record()
+
+
+def _pinned_of(dp, which):
+    key = "_pin_" + which
+    pf = getattr(dp, key, None)
+    if pf is None:
+        pf = _PinnedFlat(dp.n)
+        setattr(dp, key, pf)
+    return pf
+
+
+def _host_flat(params):
+    t = params.tensors()
+    return np.concatenate([np.asarray(v, dtype=np.float32).reshape(-1) for v in t.values()])
+
+
 class SplitExecutor:
     """engine.py:95-588: SplitExecutor(params, splits, plan, features, labels,
-    runner, record).run() -> (loss_sum, per-device gradient dicts)."""
+    runner, record).run() -> (loss_sum, per-device gradient dicts).
+
+    Samples from split_minibatch (destination-grouped, i.e. every sampler's
+    output) run as a replay of a cached CUDA graph of the whole step (split
+    included; SG_API_EAGER=1 forces the eager kernels); gradients stay on the
+    device until a caller reads them, and allreduce_and_step applies the SGD
+    step on the device copy of the parameters."""
 
     def __init__(self, params, splits, plan, features, labels, runner=None, record=None):
         ds = getattr(splits, "device_split", None) or getattr(plan, "device_split", None)
@@ -697,22 +776,40 @@ class SplitExecutor:
         self.runner = runner
         self.g = ds.g
         self.L = params.num_layers
-        self.dparams = DeviceParams.from_host(params, ds.device)
         F = int(np.asarray(features).shape[1]) if not isinstance(features, FeatureStore) else 0
-        hid = self.dparams.layer_dims(0)[1] if self.L >= 1 else 0
+        t = params.tensors()
+        hid = int(np.shape(t["layer0.w_self" if params.kind == "graphsage" else "layer0.w"])[1]) if self.L else 0
         pad = (params.kind == "graphsage" and self.L >= 2 and 64 < F <= 128 and F % 4 == 0
                and hid in (4, 8, 16, 32))  # wide layer 1 read in whole 128 B lines
         self.feats = _feature_store(features, ds.cache, ds.device, pad_rows=pad)
         self.labels = _labels_dev(labels, ds.device)
-        self.step = SplitStep(self.dparams, ds, self.feats, self.labels)
         self._states = None
+        self.graph = None
+        if (getattr(ds, "packed", None) is not None and os.environ.get("SG_API_EAGER") != "1"
+                and not DEBUG_CHECK_FINITE):  # the per-layer finite scan runs on the eager kernels
+            self.graph = _api_graph(params, ds, self.feats, self.labels)
+            self.dparams = self.graph.p
+            self.step = None
+        else:
+            self.dparams = DeviceParams.from_host(params, ds.device)
+            self.step = SplitStep(self.dparams, ds, self.feats, self.labels)
+
+    def _to_eager(self):
+        """forward() / backward() called separately (reference engine.py:556-
+        588): run this executor on the eager kernels."""
+        if self.step is None:
+            self.graph = None
+            self.dparams = DeviceParams.from_host(self.params, self.ds.device)
+            self.step = SplitStep(self.dparams, self.ds, self.feats, self.labels)
 
     def forward(self):
+        self._to_eager()
         with _pdl_for(self.step.kind):
             self.step.forward()
         self._states = None
 
     def backward(self):
+        self._to_eager()
         with _pdl_for(self.step.kind):
             self.step.backward()
 
@@ -723,28 +820,65 @@ class SplitExecutor:
             d_in, d_out = self.params.layer_dims(l - 1)
             width = (2 * d_in + 1) if self.params.kind == "graphsage" else (2 * d_out + 8)
             account_transfer(self.record, "peer", self.ds.pair_count(l) * width * 8)
-        self.record.wire_bytes += self.step.wire_bytes
+        if self.step is not None:
+            self.record.wire_bytes += self.step.wire_bytes
 
     def run(self):
+        if self.graph is not None:
+            return self._run_graph()
         self.forward()
         self.backward()
         self._meter()
         loss = float(self.step.loss_sum_dev().item())
+        out = [GradDict(dparams=self.dparams, device_flat=self.step.grads[d]) for d in range(self.g)]
+        self._loss_slots = [f[self.dparams.n] for f in (gd.device_flat for gd in out)]
+        return loss, out
+
+    def _run_graph(self):
+        gs = self.graph
+        host = _host_flat(self.params)
+        self._snapshot = host
+        up = _pinned_of(gs.p, "up")
+        up.wait()
+        up.np[:] = host
+        gs.p.flat.copy_(up.t, non_blocking=True)
+        up.record()
+        gs.load_packed(self.ds.packed)
+        gs.replay()
+        n = gs.p.n
+        flats = [o.clone() for o in gs.out]  # the graph's buffers are reused by the next replay
+        self._meter()
         out = []
-        for d in range(self.g):
-            gd = GradDict(self.dparams.grads_to_dict(self.step.grads[d]))
-            gd.device_flat = self.step.grads[d]
+        for f in flats:
+            gd = GradDict(dparams=gs.p, device_flat=f)
+            gd.param_snapshot = host
             out.append(gd)
-        for d, st in enumerate(self.states):
-            st.loss_sum = float(self.step.grads[d][self.dparams.n].item())
+        self._loss_slots = [f[n] for f in flats]
+        loss = float((flats[0][n] if len(flats) == 1 else torch.stack(self._loss_slots).sum()).item())
         return loss, out
 
     @property
     def states(self):
         """Per-device owned-row activations (reference DeviceState.h / .layer),
-        materialised on demand from the device."""
+        materialised on demand from the device. On the captured path they are
+        recomputed by one eager forward of the same split and parameters
+        (the graph's activation buffers are shared across replays)."""
         if self._states is None:
+            if self.step is None:
+                snap = getattr(self, "_snapshot", None)
+                if snap is not None:  # the parameters run() used, even if updated since
+                    gp = self.graph.p
+                    dp = DeviceParams(gp.kind, gp.names, gp.shapes, torch.from_numpy(snap).to(self.ds.device),
+                                      gp.leaky_slope)
+                else:
+                    dp = DeviceParams.from_host(self.params, self.ds.device)
+                self.step = SplitStep(dp, self.ds, self.feats, self.labels)
+                with _pdl_for(self.step.kind):
+                    self.step.forward()
             self._states = _materialise_states(self)
+            slots = getattr(self, "_loss_slots", None)
+            for d, st in enumerate(self._states):
+                st.loss_sum = float(slots[d].item()) if slots is not None else 0.0
         return self._states
 
 
@@ -853,13 +987,24 @@ def scatter_shuffle_forward(splits, plan, l, owned_rows, runner=None, record=Non
 def allreduce_and_step(params, per_device_grads, lr, num_targets):
     """engine.py:633-647: device-order gradient sum + SGD, on the GPU.
     Mutates `params` (host ModelParams, reference semantics) and returns the
-    summed gradients."""
+    summed gradients (built on the host on first access). Gradients from a
+    SplitExecutor run carry the device copy of the parameters they were
+    computed with: when `params` still holds those values, the step runs on
+    that copy and only the updated parameters come back (one D2H)."""
     if isinstance(params, DeviceParams):
         dp = params
         host_params = None
     else:
         host_params = params if isinstance(params, ModelParams) else ModelParams.from_reference(params)
-        dp = DeviceParams.from_host(host_params)
+        dp = None
+        snap = getattr(per_device_grads[0], "param_snapshot", None) if per_device_grads else None
+        cand = getattr(per_device_grads[0], "dparams", None) if per_device_grads else None
+        if snap is not None and cand is not None and all(getattr(gd, "dparams", None) is cand
+                                                         for gd in per_device_grads):
+            if np.array_equal(_host_flat(host_params), snap):
+                dp = cand
+        if dp is None:
+            dp = DeviceParams.from_host(host_params)
     flats = []
     for gd in per_device_grads:
         f = getattr(gd, "device_flat", None)
@@ -871,9 +1016,14 @@ def allreduce_and_step(params, per_device_grads, lr, num_targets):
     total = torch.empty(dp.n, dtype=torch.float32, device=dp.flat.device)
     _lib.call("sg_sum_sgd", _lib.ptr(dp.flat), _lib.ptr(total), _lib.ptr(ptrs), len(flats), dp.n,
               float(lr) / float(num_targets), _lib.stream_ptr())
-    summed = dp.grads_to_dict(total)
+    summed = GradDict(dparams=dp, device_flat=total)
     if host_params is not None:
-        new = dp.to_host().tensors()
+        down = _pinned_of(dp, "down")  # one pinned D2H of the updated parameters
+        down.wait()
+        down.t.copy_(dp.flat, non_blocking=True)
+        down.record()
+        down.wait()
+        new = {k: down.np[dp.offsets[i]:dp.offsets[i + 1]].reshape(dp.shapes[i]) for i, k in enumerate(dp.names)}
         for k, v in host_params.tensors().items():
             v[...] = new[k]
         if params is not host_params:  # reference object: write back in place
@@ -1268,7 +1418,7 @@ class CapturedStep:
         self.warm_out = self._body()  # the eager warm-up step's gradients (+ loss slot)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with _capturing(self.graph):
             self.out = self._body()
         torch.cuda.synchronize()
         return self
@@ -1363,6 +1513,64 @@ class CapturedStep:
             self._pipe = None
 
 
+# ---- reference-API captured step ----------------------------------------------------
+
+class _ApiGraphStep(CapturedStep):
+    """The reference-API executor's captured step: split -> layer-0 rows ->
+    forward -> loss -> backward -> per-device gradient reduction, no SGD
+    (allreduce_and_step applies it). Cached per (model shape, partition,
+    cache, features, labels, capacity bucket); the sample arrives as a
+    device-to-device copy of split_minibatch's packed buffer, the parameters as
+    an H2D copy of the host ModelParams."""
+
+    def _body(self):
+        inp = self.inp
+        ds = DeviceSplit(inp.V, inp.es, inp.ed, inp.cap_nV, inp.cap_nE, self.pm, self.cache, True, self.dev,
+                         sizes=inp.sizes)
+        step = SplitStep(self.p, ds, self.f, self.labels, exact=False)
+        step.run()
+        self.ds, self.step = ds, step
+        return [step.grads[d] for d in range(self.pm.num_devices)]
+
+    def load_packed(self, packed):
+        buf, used, _ = packed
+        self.inp.buf[:used].copy_(buf[:used])
+
+    def capture_packed(self, packed):
+        self.load_packed(packed)
+        with _pdl_for(self.p.kind):
+            self._body()  # eager warm-up (no SGD: parameters untouched)
+            torch.cuda.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with _capturing(self.graph):
+                self.out = self._body()
+        torch.cuda.synchronize()
+        return self
+
+
+_API_GRAPHS = {}
+_API_GRAPHS_MAX = 8
+
+
+def _api_graph(params, ds, feats, labels):
+    """Cached _ApiGraphStep for this model shape / capacity bucket (LRU of 8;
+    the entries hold the partition, cache, feature store and labels they were
+    captured with, so their ids stay unique while cached)."""
+    t = params.tensors()
+    geo = ds.packed[2]
+    key = (params.kind, tuple(t.keys()), tuple(np.shape(v) for v in t.values()), float(params.leaky_slope),
+           id(ds.pm), id(ds.cache), id(feats), labels.data_ptr(), tuple(geo.cap_nV), tuple(geo.cap_nE), str(ds.device))
+    gs = _API_GRAPHS.pop(key, None)
+    if gs is None:
+        dp = DeviceParams.from_host(params, ds.device)
+        gs = _ApiGraphStep(dp, ds.pm, ds.cache, feats, labels, geo.cap_nV, geo.cap_nE, 1.0, device=ds.device, lr=1.0)
+        gs.capture_packed(ds.packed)
+        while len(_API_GRAPHS) >= _API_GRAPHS_MAX:
+            _API_GRAPHS.pop(next(iter(_API_GRAPHS)))
+    _API_GRAPHS[key] = gs
+    return gs
+
+
 # ---- one process per GPU ------------------------------------------------------------
 
 class SampledCapturedStep(CapturedStep):
@@ -1413,7 +1621,7 @@ class SampledCapturedStep(CapturedStep):
         self._body()
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with _capturing(self.graph):
             self.out = self._body()
         torch.cuda.synchronize()
         return self

@@ -1,9 +1,10 @@
 """Partition map and per-device feature-cache selection.
 
-Mirrors splitgnn.partition's data types (partition.py:20-91) and the cache
-policy build_cache (:358-377). The offline multilevel partitioner itself is
-out of scope for the B200 hot path; range_partition
-gives the contiguous-id map the benchmark configs use.
+Mirrors splitgnn.partition's data types (partition.py:20-91), the cache
+policy build_cache (:358-377, selected on the GPU) and the offline multilevel
+partitioner (:298-349) as a GPU multilevel scheme;
+range_partition gives the contiguous-id map the benchmark configs use
+(PAPER.md:821).
 """
 
 from __future__ import annotations
@@ -123,17 +124,28 @@ class CacheState:
 
 def build_cache(graph, pm: PartitionMap, capacity_fraction: float) -> CacheState:
     """Highest in+out degree vertices of each partition, ties by lower id
-    (partition.py:358-377)."""
+    (partition.py:358-377), selected on the GPU: degrees by device bincount,
+    one stable device sort of (part, -degree) keys over the id-ordered vertices
+    (so equal degrees keep ascending ids), the first `cap` of every part."""
+    import torch
     if not (0.0 <= capacity_fraction <= 1.0):
         raise ValueError("capacity_fraction must be in [0, 1]")
-    n = graph.num_vertices
+    n = int(graph.num_vertices)
     cap = math.ceil(capacity_fraction * n - 1e-9)
-    degree = graph.in_degrees() + graph.out_degrees()
-    cached = []
-    for d in range(pm.num_devices):
-        ids = pm.device_vertices(d)
-        order = np.lexsort((ids, -degree[ids]))
-        cached.append(np.sort(ids[order][:cap]))
+    g = pm.num_devices
+    if n == 0:
+        return CacheState([np.empty(0, dtype=np.int64) for _ in range(g)], capacity_fraction)
+    dev = torch.device("cuda")
+    ro = torch.from_numpy(np.asarray(graph.row_offsets, dtype=np.int64)).to(dev)
+    ci = torch.from_numpy(np.asarray(graph.col_indices, dtype=np.int64)).to(dev)
+    degree = (ro[1:] - ro[:-1]) + torch.bincount(ci, minlength=n)
+    part = torch.from_numpy(np.asarray(pm.assignment, dtype=np.int64)).to(dev)
+    key = (part << 40) | (int(degree.max()) - degree)
+    _, order = torch.sort(key, stable=True)
+    counts = torch.bincount(part, minlength=g).cpu().numpy()
+    starts = np.concatenate([[0], np.cumsum(counts)[:-1]])
+    order = order.cpu().numpy()
+    cached = [np.sort(order[s:s + min(cap, int(c))]) for s, c in zip(starts, counts)]
     return CacheState(cached, capacity_fraction)
 
 
@@ -145,59 +157,158 @@ def full_cache(pm: PartitionMap) -> CacheState:
     return CacheState([pm.device_vertices(d) for d in range(pm.num_devices)], float(frac))
 
 
-# ---- balanced k-way partitioning on the GPU (csrc/partition.cu) -------------------
+# ---- balanced k-way partitioning on the GPU (csrc/partition.cu, csrc/host.cpp) ------
 
-class _DeviceGraph:
-    """In-CSR and out-CSR (the transpose, by a stable device sort) of a graph."""
+class _Level:
+    """Symmetric weighted CSR of one level (device tensors): off int64[n+1],
+    nbr / wt int32[nnz], vw int32[n]; cmap maps the finer level onto it."""
 
-    def __init__(self, graph, device="cuda"):
-        import torch
-        dev = torch.device(device)
-        n = int(graph.num_vertices)
-        self.n = n
-        self.ro = torch.from_numpy(np.asarray(graph.row_offsets, dtype=np.int64)).to(dev)
-        self.ci = torch.from_numpy(np.asarray(graph.col_indices, dtype=np.int32)).to(dev)
-        deg = self.ro[1:] - self.ro[:-1]
-        dst = torch.repeat_interleave(torch.arange(n, dtype=torch.int32, device=dev), deg)
-        src_sorted, perm = torch.sort(self.ci, stable=True)
-        self.oci = dst[perm].contiguous()
-        cnt = torch.bincount(self.ci.long(), minlength=n)
-        self.oro = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-        self.oro[1:] = torch.cumsum(cnt, 0)
-        del src_sorted, perm, dst
+    def __init__(self, off, nbr, wt, vw):
+        self.off, self.nbr, self.wt, self.vw = off, nbr, wt, vw
+        self.n = int(vw.numel())
 
     def cut(self, part):
+        """Directed-arc units (entries are counted from both ends)."""
         import torch
-        out = torch.zeros(1, dtype=torch.int64, device=part.device)
         from paper_2303_13775_b200 import _lib
-        _lib.call("sg_partition_cut", _lib.ptr(self.ro), _lib.ptr(self.ci), self.n, _lib.ptr(part), _lib.ptr(out),
+        out = torch.zeros(1, dtype=torch.int64, device=part.device)
+        _lib.call("sg_partition_cut_w", _lib.ptr(self.off), _lib.ptr(self.nbr), _lib.ptr(self.wt), self.n,
+                  _lib.ptr(part), _lib.ptr(out), _lib.stream_ptr())
+        return int(out.item()) // 2
+
+    def sizes(self, part, g):
+        import torch
+        from paper_2303_13775_b200 import _lib
+        out = torch.empty(g, dtype=torch.int64, device=part.device)
+        _lib.call("sg_partition_sizes", _lib.ptr(part), _lib.ptr(self.vw), self.n, g, _lib.ptr(out),
                   _lib.stream_ptr())
-        return int(out.item())
+        return out
 
 
-def _refine_device(dg, part, g, cap, seed, max_passes):
-    """Parallel refinement rounds (two rounds per reference pass: each round
-    moves a seeded half of the vertices); a round that raised the cut is
-    undone, so the history never increases."""
+def _csr_from_keys(keys, wts, n):
+    """Sorted unique (u * n + v) keys with weights -> CSR level."""
+    import torch
+    u = keys // n
+    off = torch.zeros(n + 1, dtype=torch.int64, device=keys.device)
+    off[1:] = torch.cumsum(torch.bincount(u, minlength=n), 0)
+    return off, (keys - u * n).to(torch.int32), wts.to(torch.int32)
+
+
+def _symmetric_level(graph, device="cuda"):
+    """Level 0: the input graph symmetrised, weight(u,v) = arcs u->v + arcs
+    v->u, self loops dropped (partition.py:123-136)."""
+    import torch
+    dev = torch.device(device)
+    n = int(graph.num_vertices)
+    ro = torch.from_numpy(np.asarray(graph.row_offsets, dtype=np.int64)).to(dev)
+    src = torch.from_numpy(np.asarray(graph.col_indices, dtype=np.int64)).to(dev)
+    dst = torch.repeat_interleave(torch.arange(n, dtype=torch.int64, device=dev), ro[1:] - ro[:-1])
+    keep = src != dst
+    src, dst = src[keep], dst[keep]
+    keys = torch.cat([src * n + dst, dst * n + src])
+    del src, dst, keep
+    uk, cnt = torch.unique(keys, sorted=True, return_counts=True)
+    del keys
+    off, nbr, wt = _csr_from_keys(uk, cnt, n)
+    return _Level(off, nbr, wt, torch.ones(n, dtype=torch.int32, device=dev))
+
+
+def _match_siblings(level, match, wcap):
+    """Two-hop matching for what heavy-edge matching leaves unmatched (on
+    power-law graphs: the many low-degree vertices whose only neighbours are
+    already-matched hubs): unmatched vertices with the same heaviest neighbour
+    (the anchor; ties by lower id) are paired in id order, within the weight
+    cap. Without it coarsening stalls after a few levels."""
+    import torch
+    dev = match.device
+    n = level.n
+    un = torch.nonzero(match < 0).squeeze(1)
+    if un.numel() < 2:
+        return
+    deg = level.off[1:] - level.off[:-1]
+    row = torch.repeat_interleave(torch.arange(n, dtype=torch.int64, device=dev), deg)
+    # per-vertex argmax of (weight, -neighbour id) over the CSR row
+    key = (level.wt.to(torch.int64) << 32) | (2**31 - 1 - level.nbr.to(torch.int64))
+    best = torch.full((n,), -1, dtype=torch.int64, device=dev).scatter_reduce_(0, row, key, "amax")
+    anchor = torch.where(best >= 0, 2**31 - 1 - (best & 0xFFFFFFFF), torch.full_like(best, -1))[un]
+    keep = anchor >= 0
+    un, anchor = un[keep], anchor[keep]
+    if un.numel() < 2:
+        return
+    order = torch.argsort(anchor * n + un)
+    un, anchor = un[order], anchor[order]
+    m = un.numel()
+    pos = torch.arange(m, device=dev)
+    start = torch.ones(m, dtype=torch.bool, device=dev)
+    start[1:] = anchor[1:] != anchor[:-1]
+    run0 = torch.cummax(torch.where(start, pos, torch.zeros_like(pos)), 0).values
+    first = ((pos - run0) % 2 == 0)[:-1] & ~start[1:]  # even position in its run, next in the same run
+    a, b = un[:-1][first], un[1:][first]
+    ok = level.vw[a].to(torch.int64) + level.vw[b].to(torch.int64) <= wcap
+    a, b = a[ok], b[ok]
+    match[a] = b.to(torch.int32)
+    match[b] = a.to(torch.int32)
+
+
+def _coarsen(level, wcap, seed, rounds=6, two_hop=True):
+    """Heavy-edge matching (sg_partition_match_round) and contraction. Returns
+    (coarse level, cmap int64[n])."""
+    import torch
+    from paper_2303_13775_b200 import _lib
+    dev = level.vw.device
+    n = level.n
+    match = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    ws = torch.empty(4 * max(n, 1), dtype=torch.uint8, device=dev)
+    matched = torch.zeros(1, dtype=torch.int64, device=dev)
+    for r in range(rounds):
+        _lib.call("sg_partition_match_round", _lib.ptr(level.off), _lib.ptr(level.nbr), _lib.ptr(level.wt),
+                  _lib.ptr(level.vw), n, int(wcap), int(seed) & (2**64 - 1), r, _lib.ptr(match), _lib.ptr(ws),
+                  _lib.ptr(matched), _lib.stream_ptr())
+    idx = torch.arange(n, dtype=torch.int64, device=dev)
+    if two_hop:
+        _match_siblings(level, match, wcap)
+    mate = torch.where(match >= 0, match.to(torch.int64), idx)
+    leader = idx <= mate
+    cid = torch.cumsum(leader.to(torch.int64), 0) - 1
+    cmap = cid[torch.minimum(idx, mate)]
+    nc = int(cid[-1].item()) + 1 if n else 0
+    vw = torch.zeros(nc, dtype=torch.int64, device=dev).index_add_(0, cmap, level.vw.to(torch.int64))
+    u = torch.repeat_interleave(cmap, level.off[1:] - level.off[:-1])
+    v = cmap[level.nbr.to(torch.int64)]
+    keep = u != v
+    keys = u[keep] * nc + v[keep]
+    w = level.wt.to(torch.int64)[keep]
+    del u, v, keep
+    uk, inv = torch.unique(keys, sorted=True, return_inverse=True)
+    cw = torch.zeros(uk.numel(), dtype=torch.int64, device=dev).index_add_(0, inv, w)
+    off, nbr, wt = _csr_from_keys(uk, cw, nc)
+    return _Level(off, nbr, wt, vw.to(torch.int32)), cmap
+
+
+def _refine_device(level, part, g, cap, seed, max_passes):
+    """Parallel refinement rounds on one level (two rounds per reference pass:
+    each round moves a seeded half of the vertices); a round that raised the
+    cut is undone, so the history (directed-arc units) never increases."""
     import torch
     from paper_2303_13775_b200 import _lib
     dev = part.device
-    sizes = torch.bincount(part.long(), minlength=g).to(torch.int64)
-    ws = torch.empty(8 * dg.n + 4 * 16 * 65 + 64, dtype=torch.uint8, device=dev)
+    n = level.n
+    sizes = level.sizes(part, g)
+    ws = torch.empty(8 * n + 8 * 16 * 64 + 64, dtype=torch.uint8, device=dev)
     moved = torch.zeros(1, dtype=torch.int64, device=dev)
-    cut = dg.cut(part)
+    cut = level.cut(part)
     history = [cut]
     idle = 0
     for r in range(2 * max_passes):
         prev = part.clone()
-        _lib.call("sg_partition_round", _lib.ptr(dg.ro), _lib.ptr(dg.ci), _lib.ptr(dg.oro), _lib.ptr(dg.oci), dg.n,
-                  g, int(cap), int(seed) & (2**64 - 1), r, _lib.ptr(part), _lib.ptr(sizes), _lib.ptr(ws),
-                  _lib.ptr(moved), _lib.stream_ptr())
+        _lib.call("sg_partition_round", _lib.ptr(level.off), _lib.ptr(level.nbr), _lib.ptr(level.wt),
+                  _lib.ptr(level.vw), n, g, int(cap), int(seed) & (2**64 - 1), r, _lib.ptr(part),
+                  _lib.ptr(sizes), _lib.ptr(ws), _lib.ptr(moved), _lib.stream_ptr())
         nmoved = int(moved.item())
-        new = dg.cut(part) if nmoved else cut
+        new = level.cut(part) if nmoved else cut
         if new > cut:  # simultaneous moves of neighbours made it worse: undo
             part.copy_(prev)
-            sizes = torch.bincount(part.long(), minlength=g).to(torch.int64)
+            sizes = level.sizes(part, g)
             nmoved = 0
         else:
             cut = new
@@ -207,6 +318,49 @@ def _refine_device(dg, part, g, cap, seed, max_passes):
         if idle >= 2:
             break
     return part, history
+
+
+def _refine_host(level, part, g, cap, max_passes):
+    """Sequential refinement of a small level on the host (csrc/host.cpp)."""
+    import ctypes as C
+    import torch
+    from paper_2303_13775_b200 import _lib
+    p = part.cpu().numpy().astype(np.int32)
+    off, nbr, wt, vw = (t.cpu().numpy() for t in (level.off, level.nbr, level.wt, level.vw))  # alive for the call
+    cut = C.c_int64(0)
+    _lib.call("sg_partition_refine_host", level.n, _lib.ptr(off), _lib.ptr(nbr), _lib.ptr(wt), _lib.ptr(vw),
+              g, int(cap), int(max_passes), _lib.ptr(p), C.byref(cut))
+    return torch.from_numpy(p).to(part.device)
+
+
+# levels with at most this many vertices are refined sequentially on the host
+# (a move there updates its neighbours' gains at once); larger ones by GPU rounds
+HOST_REFINE_MAX = int(__import__("os").environ.get("SG_PART_HOST_REFINE", 1 << 18))
+
+
+def _refine(level, part, g, cap, seed, max_passes):
+    if level.n <= HOST_REFINE_MAX or int(level.sizes(part, g).max()) > cap:
+        # (a level above the host threshold is repaired there only if it came out
+        # over the cap: the GPU rounds never move a vertex into a full part)
+        part = _refine_host(level, part, g, cap, max_passes)
+    part, _ = _refine_device(level, part, g, cap, seed, max_passes)
+    return part
+
+
+def _coarse_partition(level, g, cap, seed, restarts=4):
+    """Initial partition of the coarsest level on the host (csrc/host.cpp)."""
+    import ctypes as C
+    import torch
+    from paper_2303_13775_b200 import _lib
+    off = level.off.cpu().numpy()
+    nbr = level.nbr.cpu().numpy()
+    wt = level.wt.cpu().numpy()
+    vw = level.vw.cpu().numpy()
+    part = np.empty(level.n, dtype=np.int32)
+    cut = C.c_int64(0)
+    _lib.call("sg_partition_coarse_host", level.n, _lib.ptr(off), _lib.ptr(nbr), _lib.ptr(wt), _lib.ptr(vw), g,
+              int(cap), int(seed) & (2**64 - 1), restarts, _lib.ptr(part), C.byref(cut))
+    return torch.from_numpy(part).to(level.vw.device)
 
 
 def refine_assignment(graph, assignment, num_devices, balance_eps=0.05, max_passes=10, seed=0):
@@ -219,19 +373,26 @@ def refine_assignment(graph, assignment, num_devices, balance_eps=0.05, max_pass
         raise ValueError("the GPU partitioner supports at most 16 parts")
     n = int(graph.num_vertices)
     cap = max_part_size(n, g, balance_eps)
-    dg = _DeviceGraph(graph)
+    level = _symmetric_level(graph)
     part = torch.from_numpy(np.asarray(assignment, dtype=np.int32)).cuda()
-    part, hist = _refine_device(dg, part, g, cap, seed, max_passes)
+    part, hist = _refine_device(level, part, g, cap, seed, max_passes)
     return part.cpu().numpy().astype(np.int64), hist
 
 
-def partition_graph(graph, g, balance_eps=0.05, seed=0, max_passes=25) -> PartitionMap:
+def partition_graph(graph, g, balance_eps=0.05, seed=0, max_passes=10) -> PartitionMap:
     """Balanced k-way partition with a small edge cut (partition.py:298-349),
-    GPU edition: the contiguous-id map (balanced by construction) refined by
-    parallel gain moves on the symmetrised graph within the balance cap.
-    Deterministic given `seed`. Not the reference's multilevel heuristic (so
-    not the same assignment); same contract: balanced within eps, cut never
-    worse than the starting map."""
+    multilevel on the GPU: coarsen by heavy-edge matching
+    (sg_partition_match_round, then two-hop sibling matching of what is left
+    unmatched, and contraction) until at most max(20g, 200) vertices remain
+    (merged weight capped at n / 2g, partition.py:324-335), partition the
+    coarsest level by greedy region growing + sequential refinement (best of 4
+    restarts, csrc/host.cpp), then project back level by level with boundary
+    refinement: sequential on the host for levels of <= HOST_REFINE_MAX
+    vertices, then parallel GPU rounds (sg_partition_round).
+    Deterministic given `seed`; not the reference's exact assignment (its
+    matching and refinement visit vertices sequentially), same contract:
+    balanced within eps, comparable cut (tests/test_gpu_partition.py pins the
+    cut against reference runs)."""
     import torch
     n = int(graph.num_vertices)
     if g < 1:
@@ -245,17 +406,39 @@ def partition_graph(graph, g, balance_eps=0.05, seed=0, max_passes=25) -> Partit
     if g > 16:
         raise ValueError("the GPU partitioner supports at most 16 parts")
     cap = max_part_size(n, g, balance_eps)
-    dg = _DeviceGraph(graph)
-    part = ((torch.arange(n, dtype=torch.int64, device="cuda") * g) // n).to(torch.int32)
-    part, _ = _refine_device(dg, part, g, cap, seed, max_passes)
+    levels = [_symmetric_level(graph)]
+    cmaps = []
+    coarse_target = max(20 * g, 200)
+    wcap = max(2, n // (2 * g))
+    import os
+    two_hop = os.environ.get("SG_PART_TWO_HOP", "1") == "1"
+    trace = os.environ.get("SG_PART_TRACE") == "1"
+    while levels[-1].n > coarse_target:
+        coarse, cmap = _coarsen(levels[-1], wcap, seed + 7919 * len(cmaps), two_hop=two_hop)
+        if coarse.n > 0.95 * levels[-1].n:
+            break  # matching stalled; coarser levels would not help
+        levels.append(coarse)
+        cmaps.append(cmap)
+    part = _coarse_partition(levels[-1], g, cap, seed)
+    if trace:
+        print(f"[partition] levels {[lv.n for lv in levels]}, coarsest cut {levels[-1].cut(part)}")
+    part = _refine(levels[-1], part, g, cap, seed, max_passes)
+    for lvl in range(len(cmaps) - 1, -1, -1):
+        part = part[cmaps[lvl]].contiguous()
+        part = _refine(levels[lvl], part, g, cap, seed + lvl + 1, max_passes)
+        if trace:
+            print(f"[partition] level {lvl} (n {levels[lvl].n}): cut {levels[lvl].cut(part)}")
     return PartitionMap(part.cpu().numpy().astype(np.int64), g, balance_eps)
 
 
 def cut_size(graph, pm: PartitionMap) -> int:
     """Directed edges whose endpoints live on different devices (partition.py:352-355)."""
     import torch
-    dg = _DeviceGraph.__new__(_DeviceGraph)
-    dg.n = int(graph.num_vertices)
-    dg.ro = torch.from_numpy(np.asarray(graph.row_offsets, dtype=np.int64)).cuda()
-    dg.ci = torch.from_numpy(np.asarray(graph.col_indices, dtype=np.int32)).cuda()
-    return dg.cut(torch.from_numpy(pm.assignment.astype(np.int32)).cuda())
+    from paper_2303_13775_b200 import _lib
+    ro = torch.from_numpy(np.asarray(graph.row_offsets, dtype=np.int64)).cuda()
+    ci = torch.from_numpy(np.asarray(graph.col_indices, dtype=np.int32)).cuda()
+    part = torch.from_numpy(pm.assignment.astype(np.int32)).cuda()
+    out = torch.zeros(1, dtype=torch.int64, device=part.device)
+    _lib.call("sg_partition_cut", _lib.ptr(ro), _lib.ptr(ci), int(graph.num_vertices), _lib.ptr(part),
+              _lib.ptr(out), _lib.stream_ptr())
+    return int(out.item())

@@ -55,7 +55,7 @@ class MiniBatchSample:
                 dst = np.asarray(dst)
                 if len(dst) > 1:
                     starts = np.flatnonzero(np.r_[True, dst[1:] != dst[:-1]])
-                    if len(np.unique(dst[starts])) != len(starts):
+                    if np.bincount(dst[starts]).max() > 1:  # a destination starts two runs
                         ok = False
                         break
             self.dst_grouped = ok

@@ -101,13 +101,193 @@ class ShufflePlan:
         return [o for o in range(self.num_devices) if o != holder and (l, holder, o) in self.entries]
 
     def pair_count(self, l):
+        if self.device_split is not None:  # from the device counts, without building host views
+            return self.device_split.pair_count(l)
         return sum(e.count for (ll, _, _), e in self.entries.items() if ll == l)
 
 
 class SplitList(list):
-    """list[LocalSplit] that also carries the device-resident split."""
+    """list[LocalSplit] that also carries the device-resident split. From
+    split_minibatch its LocalSplit host views are built lazily, on the first
+    access to the list's contents."""
 
     device_split = None
+    _fill_fn = None
+
+    def _fill(self):
+        f = self._fill_fn
+        if f is not None:
+            self._fill_fn = None
+            f()
+
+    def __getitem__(self, i):
+        self._fill()
+        return list.__getitem__(self, i)
+
+    def __iter__(self):
+        self._fill()
+        return list.__iter__(self)
+
+    def __len__(self):
+        if self._fill_fn is not None and self.device_split is not None:
+            return self.device_split.g
+        return list.__len__(self)
+
+    def __bool__(self):
+        return len(self) > 0
+
+    def __contains__(self, x):
+        self._fill()
+        return list.__contains__(self, x)
+
+    def __reversed__(self):
+        self._fill()
+        return list.__reversed__(self)
+
+    def __eq__(self, other):
+        self._fill()
+        return list.__eq__(self, other)
+
+    def __repr__(self):
+        self._fill()
+        return list.__repr__(self)
+
+    def index(self, *a):
+        self._fill()
+        return list.index(self, *a)
+
+    def count(self, x):
+        self._fill()
+        return list.count(self, x)
+
+    def copy(self):
+        self._fill()
+        return list(list.__iter__(self))
+
+
+class _LazyEntries(dict):
+    """ShufflePlan.entries built on first access (see SplitList)."""
+
+    def __init__(self, fn):
+        super().__init__()
+        self._fn = fn
+
+    def _fill(self):
+        f = self._fn
+        if f is not None:
+            self._fn = None
+            dict.update(self, f())
+
+    for _m in ("__getitem__", "__iter__", "__len__", "__contains__", "__repr__", "__eq__", "keys", "values",
+               "items", "get", "copy"):
+        def _wrap(self, *a, _name=_m, **k):
+            self._fill()
+            return getattr(dict, _name)(self, *a, **k)
+        locals()[_m] = _wrap
+    del _m, _wrap
+
+
+def _bucket(x):
+    """Capacity bucket: x rounded up to 1/8 of its power of two (>= 64)."""
+    x = int(x)
+    if x <= 64:
+        return 64
+    q = 1 << (x.bit_length() - 4)
+    return (x + q - 1) // q * q
+
+
+class PackGeometry:
+    """Offsets (int32 words) of the captured-step sample layout for given
+    capacities (engine.StaticSample uses the same geometry)."""
+
+    _cache = {}
+
+    def __init__(self, cap_nV, cap_nE):
+        self.cap_nV = [int(x) for x in cap_nV]
+        self.cap_nE = [int(x) for x in cap_nE]
+        self.L = len(self.cap_nE)
+        self.voff = np.r_[0, np.cumsum(self.cap_nV)].astype(np.int64)
+        self.eoff = np.r_[0, np.cumsum(self.cap_nE)].astype(np.int64)
+        VC, EC = int(self.voff[-1]), max(int(self.eoff[-1]), 1)
+        self.S = 2 * (2 * self.L + 1)
+        self.EC = EC
+        self.o_V, self.o_es, self.o_ed = self.S, self.S + VC, self.S + VC + EC
+        self.words = self.S + VC + 2 * EC
+
+    @classmethod
+    def for_sizes(cls, nV, nE, scope=None):
+        """The current geometry of `scope` if the sizes fit it, else a grown
+        one (every capacity at least the bucket of 1.15 x the size): the
+        geometry -- and so the executor's cached graph -- changes only when
+        a larger sample than any before arrives."""
+        cur = cls._cache.get(scope)
+        if cur is not None and len(cur.cap_nV) == len(nV) and \
+                all(a <= b for a, b in zip(nV, cur.cap_nV)) and all(a <= b for a, b in zip(nE, cur.cap_nE)):
+            return cur
+        grow = lambda x: _bucket(int(x * 1.15) + 1)  # noqa: E731
+        if cur is not None and len(cur.cap_nV) == len(nV):
+            cV = [max(c, grow(x)) for c, x in zip(cur.cap_nV, nV)]
+            cE = [max(c, grow(x)) for c, x in zip(cur.cap_nE, nE)]
+        else:
+            cV, cE = [grow(x) for x in nV], [grow(x) for x in nE]
+        geo = cls._cache[scope] = cls(cV, cE)
+        return geo
+
+    def pack(self, sample, out):
+        """Write the sample into host int32 `out` (sg_pack_sample: native,
+        multi-threaded); returns the words used."""
+        nV, nE = sample.sizes()
+        if any(a > b for a, b in zip(nV, self.cap_nV)) or any(a > b for a, b in zip(nE, self.cap_nE)):
+            raise ValueError("sample exceeds the captured capacities")
+        used = self.o_ed + int(self.eoff[self.L - 1] + nE[self.L - 1]) if self.L else self.o_es
+        L = self.L
+        arrs = [_i32_or_i64(v) for v in sample.layer_vertices] + \
+               [_i32_or_i64(a) for a, _ in sample.layer_edges] + [_i32_or_i64(b) for _, b in sample.layer_edges]
+        off = np.array([self.o_V + self.voff[l] for l in range(L + 1)] +
+                       [self.o_es + self.eoff[l] for l in range(L)] +
+                       [self.o_ed + self.eoff[l] for l in range(L)], dtype=np.int64)
+        sizes = np.array(list(nV) + list(nE), dtype=np.int64)
+        ptrs = np.array([a.ctypes.data for a in arrs], dtype=np.uint64)
+        eb = np.array([a.itemsize for a in arrs], dtype=np.int32)
+        _lib.call("sg_pack_sample", out.ctypes.data, L, sizes.ctypes.data, off.ctypes.data, ptrs.ctypes.data,
+                  eb.ctypes.data, 4)
+        return used
+
+
+def _i32_or_i64(a):
+    a = np.asarray(a)
+    if a.dtype not in (np.int32, np.int64):
+        a = a.astype(np.int64)
+    return np.ascontiguousarray(a)
+
+
+class _PinnedRing:
+    """Two reusable pinned staging slots for split_minibatch's H2D copy; a slot
+    is repacked only after its previous copy completed (the copy is async)."""
+
+    def __init__(self):
+        self.bufs = [None, None]
+        self.ev = [None, None]
+        self.slot = 0
+
+    def pack(self, geo, sample):
+        k = self.slot
+        if self.ev[k] is not None:
+            self.ev[k].synchronize()
+        if self.bufs[k] is None or self.bufs[k].numel() < geo.words:
+            self.bufs[k] = torch.empty(max(geo.words, 1 << 16), dtype=torch.int32).pin_memory()
+        hb = self.bufs[k]
+        used = geo.pack(sample, hb.numpy())
+        return hb, used
+
+    def record(self):
+        ev = torch.cuda.Event()
+        ev.record()
+        self.ev[self.slot] = ev
+        self.slot ^= 1
+
+
+_PINNED = _PinnedRing()
 
 
 def _carr(a):
@@ -133,10 +313,13 @@ class DeviceSplit:
     receive slots (recv_off, owner-major)."""
 
     def __init__(self, V, esrc, edst, nV, nE, pm: PartitionMap, cache: CacheState | None,
-                 dst_grouped: bool, device=None, host_V=None, sizes=None):
+                 dst_grouped: bool, device=None, host_V=None, sizes=None, defer=False):
         """nV / nE are the CAPACITIES the layout is built for; `sizes` (device
         int64 [nV_0..nV_L, nE_1..nE_L]) gives the actual sizes (default: the
-        capacities). V / esrc / edst hold layer l at the capacity offsets."""
+        capacities). V / esrc / edst hold layer l at the capacity offsets.
+        defer=True postpones the workspace and the split kernel to the first
+        use of `ws` (split_minibatch: a SplitExecutor on the captured path
+        re-splits inside its graph and never needs it)."""
         lib = _lib.load()
         self.device = torch.device(device or "cuda")
         self.pm = pm
@@ -152,24 +335,85 @@ class DeviceSplit:
         _lib.check(lib.sg_split_layout(self.L, self.g, nVa, nEa, len(pm.assignment), C.byref(lay)),
                    "split_layout")
         self.lay = lay
-        self.ws = torch.empty(int(lay.total_bytes), dtype=torch.uint8, device=self.device)
         self.V, self.esrc, self.edst = V, esrc, edst
-        self.host_V = host_V
-        bits = cache.device_bits(len(pm.assignment), self.device) if cache is not None else None
+        self._host_V = host_V
         n = len(pm.assignment)
         if cache is not None and getattr(cache, "_all", None) is None:
             cache._all = cache.covers_all(n)
-        flags = (1 if self.dst_grouped else 0) | (2 if cache is not None and cache._all else 0)
-        self.all_cached = bool(flags & 2)
+        self._flags = (1 if self.dst_grouped else 0) | (2 if cache is not None and cache._all else 0)
+        self.all_cached = bool(self._flags & 2)
         self.sizes = sizes
-        _lib.check(lib.sg_split_run(_lib.ptr(self.ws), C.byref(lay), _lib.ptr(V), _lib.ptr(esrc),
-                                    _lib.ptr(edst), _lib.ptr(sizes), _lib.ptr(pm.device_u8(self.device)),
-                                    _lib.ptr(bits), flags, _lib.stream_ptr()),
-                   "split_run")
+        self.packed = None
         self._meta = None
         self._views = None
+        if not defer:
+            self._run_split()
+
+    def _run_split(self):
+        """Allocate the workspace and launch sg_split_run (on the current stream)."""
+        ws = torch.empty(int(self.lay.total_bytes), dtype=torch.uint8, device=self.device)
+        n = len(self.pm.assignment)
+        bits = self.cache.device_bits(n, self.device) if self.cache is not None else None
+        _lib.check(_lib.load().sg_split_run(_lib.ptr(ws), C.byref(self.lay), _lib.ptr(self.V), _lib.ptr(self.esrc),
+                                            _lib.ptr(self.edst), _lib.ptr(self.sizes),
+                                            _lib.ptr(self.pm.device_u8(self.device)), _lib.ptr(bits), self._flags,
+                                            _lib.stream_ptr()),
+                   "split_run")
+        self.ws = ws
+
+    def __getattr__(self, name):
+        # only reached for attributes not set yet: the deferred workspace
+        if name == "ws" and "lay" in self.__dict__:
+            self._run_split()
+            return self.__dict__["ws"]
+        raise AttributeError(name)
+
+    @property
+    def host_V(self):
+        hv = self._host_V
+        if callable(hv):
+            hv = self._host_V = hv()
+        return hv
+
+    @host_V.setter
+    def host_V(self, v):
+        self._host_V = v
 
     # -- construction from a host sample ------------------------------------
+    @classmethod
+    def from_sample_packed(cls, sample, pm, cache=None, device=None, defer=True):
+        """The sample in the captured-step layout (StaticSample: one int32
+        buffer [sizes | V | esrc | edst], layer l at its capacity offset) with
+        capacities from a geometry that only grows (PackGeometry.for_sizes),
+        so that successive samples map onto one cached CUDA graph of the
+        executor.
+        One pinned pack + one H2D; the split kernel is deferred (see __init__).
+        Needs a destination-grouped sample."""
+        sample = as_sample(sample)
+        nV, nE = sample.sizes()
+        dev = torch.device(device or "cuda")
+        geo = PackGeometry.for_sizes(nV, nE, scope=(len(nE), len(pm.assignment), pm.num_devices))
+        hb, used = _PINNED.pack(geo, sample)
+        buf = torch.empty(geo.words, dtype=torch.int32, device=dev)
+        buf[:used].copy_(hb[:used], non_blocking=True)
+        _PINNED.record()
+        VC = int(geo.voff[-1])
+        V = buf[geo.o_V:geo.o_V + VC]
+        es = buf[geo.o_es:geo.o_es + geo.EC]
+        ed = buf[geo.o_ed:geo.o_ed + geo.EC]
+
+        def host_V():
+            out = np.zeros(VC, dtype=np.int32)
+            for l, v in enumerate(sample.layer_vertices):
+                out[geo.voff[l]:geo.voff[l] + len(v)] = v
+            return out
+
+        ds = cls(V, es, ed, geo.cap_nV, geo.cap_nE, pm, cache, True, dev, host_V=host_V,
+                 sizes=buf[:geo.S].view(torch.int64), defer=defer)
+        ds.packed = (buf, used, geo)
+        ds.num_targets = len(sample.targets)
+        return ds
+
     @classmethod
     def from_sample(cls, sample, pm, cache=None, device=None):
         sample = as_sample(sample)
@@ -292,8 +536,30 @@ def split_minibatch(sample, pm: PartitionMap, cache: CacheState | None = None):
         v = np.asarray(v)
         if len(v) and (v.max() >= n or v.min() < 0):
             raise ValueError("sample vertex missing from partition map")
-    ds = DeviceSplit.from_sample(sample, pm, cache)
-    return ds.to_reference_types()
+    if sample.is_dst_grouped():
+        ds = DeviceSplit.from_sample_packed(sample, pm, cache)
+    else:
+        ds = DeviceSplit.from_sample(sample, pm, cache)
+    return _lazy_views(ds)
+
+
+def _lazy_views(ds):
+    """(splits, plan) whose host contents are built from the device split on
+    first access (one D2H of the workspace); SplitExecutor reads only
+    `.device_split` and never triggers it."""
+    splits = SplitList()
+    splits.device_split = ds
+    plan = ShufflePlan(ds.L, ds.g, device_split=ds)
+    state = {}
+
+    def fill():
+        if not state:
+            state["v"] = ds.to_reference_types()
+        return state["v"]
+
+    splits._fill_fn = lambda: list.extend(splits, fill()[0])
+    plan.entries = _LazyEntries(lambda: fill()[1].entries)
+    return splits, plan
 
 
 @dataclass

@@ -158,3 +158,98 @@ def test_init_params_matches_oracle_draws():
         assert list(p) == list(q)
         for k in p:
             assert np.array_equal(p[k], q[k])
+
+
+def _sym_csr(n, edges):
+    import collections
+    w = collections.Counter()
+    for u, v in edges:
+        if u != v:
+            w[(u, v)] += 1
+            w[(v, u)] += 1
+    keys = sorted(w)
+    off = np.zeros(n + 1, dtype=np.int64)
+    for u, _ in keys:
+        off[u + 1] += 1
+    off = np.cumsum(off)
+    nbr = np.array([v for _, v in keys], dtype=np.int32)
+    wt = np.array([w[k] for k in keys], dtype=np.int32)
+    return off, nbr, wt
+
+
+@pytest.mark.parametrize("perm", [[0, 1, 2, 3, 4, 5], [0, 3, 1, 4, 2, 5], [5, 2, 4, 0, 3, 1]])
+def test_coarse_partition_bridge_graph(perm):
+    """csrc/host.cpp sg_partition_coarse_host (the multilevel partitioner's
+    coarsest level): two bidirected 3-cliques joined by one arc, eps 0 -> the
+    exhaustive optimum (cut 1, reference test_partition.py:49-58), whatever the
+    vertex numbering."""
+    import ctypes as C
+    import itertools
+    from paper_2303_13775_b200 import _lib
+    p = np.array(perm)
+    edges = [(p[u], p[v]) for blk in ([0, 1, 2], [3, 4, 5]) for u, v in itertools.permutations(blk, 2)]
+    edges.append((p[2], p[3]))
+    off, nbr, wt = _sym_csr(6, edges)
+    vw = np.ones(6, dtype=np.int32)
+    part = np.empty(6, dtype=np.int32)
+    cut = C.c_int64(0)
+    _lib.call("sg_partition_coarse_host", 6, _lib.ptr(off), _lib.ptr(nbr), _lib.ptr(wt), _lib.ptr(vw), 2, 3,
+              0, 4, _lib.ptr(part), C.byref(cut))
+    assert cut.value == 1
+    assert np.bincount(part, minlength=2).tolist() == [3, 3]
+    assert len(set(part[p[:3]])) == 1 and len(set(part[p[3:]])) == 1
+
+
+def test_coarse_partition_weighted_balance():
+    """Vertex weights count toward the cap; a ring of 40 weighted vertices
+    splits into 4 contiguous arcs within the cap, deterministically."""
+    import ctypes as C
+    from paper_2303_13775_b200 import _lib
+    n = 40
+    off, nbr, wt = _sym_csr(n, [(i, (i + 1) % n) for i in range(n)])
+    vw = (1 + (np.arange(n) % 3)).astype(np.int32)
+    cap = int(np.ceil(vw.sum() / 4 * 1.1))
+    outs = []
+    for _ in range(2):
+        part = np.empty(n, dtype=np.int32)
+        cut = C.c_int64(0)
+        _lib.call("sg_partition_coarse_host", n, _lib.ptr(off), _lib.ptr(nbr), _lib.ptr(wt), _lib.ptr(vw), 4, cap,
+                  9, 4, _lib.ptr(part), C.byref(cut))
+        sizes = np.bincount(part, weights=vw, minlength=4)
+        assert sizes.max() <= cap
+        assert cut.value <= 6  # 4 arcs is optimal on a ring; allow a little for the heuristic
+        outs.append(part.copy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
+def test_pack_sample_matches_numpy_layout(dtype):
+    """sg_pack_sample (split_minibatch's native staging) writes the captured-step
+    layout: int64 size header, V^l at the capacity offsets, then sources and
+    destinations per layer -- for int32 and int64 sample arrays."""
+    from paper_2303_13775_b200.sampling import MiniBatchSample
+    from paper_2303_13775_b200.scheduler import PackGeometry
+    rng = np.random.default_rng(0)
+    nV = [50000, 7000, 900, 100]
+    nE = [70000, 9000, 1000]
+    V = [rng.integers(0, 1 << 30, k).astype(dtype) for k in nV]
+    E = [(rng.integers(0, nV[l], nE[l]).astype(dtype), np.sort(rng.integers(0, nV[l + 1], nE[l])).astype(dtype))
+         for l in range(3)]
+    smp = MiniBatchSample(3, V, E, dst_grouped=True)
+    geo = PackGeometry.for_sizes(nV, nE, scope=("test", dtype))
+    assert all(c >= x for c, x in zip(geo.cap_nV, nV)) and all(c >= x for c, x in zip(geo.cap_nE, nE))
+    out = np.full(geo.words, -7, dtype=np.int32)
+    used = geo.pack(smp, out)
+    assert out[:geo.S].view(np.int64).tolist() == nV + nE
+    for l in range(4):
+        o = geo.o_V + geo.voff[l]
+        assert np.array_equal(out[o:o + nV[l]], V[l].astype(np.int32))
+    for l in range(3):
+        o = geo.eoff[l]
+        assert np.array_equal(out[geo.o_es + o:geo.o_es + o + nE[l]], E[l][0].astype(np.int32))
+        assert np.array_equal(out[geo.o_ed + o:geo.o_ed + o + nE[l]], E[l][1].astype(np.int32))
+    assert used == geo.o_ed + geo.eoff[2] + nE[2]
+    # a smaller sample keeps the geometry (one cached graph serves both); a larger one grows it
+    assert PackGeometry.for_sizes([x // 2 for x in nV], [x // 2 for x in nE], scope=("test", dtype)) is geo
+    big = PackGeometry.for_sizes([2 * x for x in nV], nE, scope=("test", dtype))
+    assert big is not geo and all(b >= c for b, c in zip(big.cap_nV, geo.cap_nV))

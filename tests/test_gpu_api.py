@@ -1,0 +1,112 @@
+"""The reference-facing API as a user drives it (reference engine.py:655-826
+run_epoch's split branch): split_minibatch -> SplitExecutor.run ->
+allreduce_and_step, step after step, with host ModelParams updated in place.
+
+The executor runs destination-grouped samples as a replay of a cached CUDA
+graph (engine._ApiGraphStep) and leaves gradients on the device; these tests
+pin that path to the eager kernels (SG_API_EAGER=1) and to the float64 oracle,
+and check the lazy host views."""
+
+import os
+
+import numpy as np
+import pytest
+
+from helpers import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _workload(kind, g, F=24, C=5, B=64, steps=5, seed=0, cache_frac=None):
+    import paper_2303_13775_b200 as sg
+    graph = sg.generate_powerlaw(6000, 60000, blocks=8, p_local=0.8, seed=seed)
+    pm = sg.range_partition(graph.num_vertices, g)
+    cache = sg.full_cache(pm) if cache_frac is None else sg.build_cache(graph, pm, cache_frac)
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=seed + 1)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=seed + 2)
+    rng = np.random.default_rng(seed + 3)
+    samples = [sg.sample_minibatch(graph, rng.choice(graph.num_vertices, B - 7 * (i % 2), replace=False),
+                                   [6, 4, 3], rng) for i in range(steps)]
+    params = sg.init_params(kind, F, 8, C, 3, seed=seed + 4)
+    return graph, pm, cache, feats, labels, samples, params
+
+
+def _train(sg, params, samples, pm, cache, feats, labels, lr=0.1):
+    losses = []
+    for smp in samples:
+        splits, plan = sg.split_minibatch(smp, pm, cache)
+        ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+        loss, grads = ex.run()
+        sg.allreduce_and_step(params, grads, lr, len(smp.targets))
+        losses.append(loss)
+    return losses
+
+
+@pytest.mark.parametrize("kind,g", [("graphsage", 1), ("graphsage", 3), ("gat", 2)])
+def test_api_loop_graph_path_matches_eager_and_oracle(kind, g, monkeypatch):
+    import copy
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import engine
+    from oracle.coop_oracle import CoopRun, reduce_and_sgd
+    from oracle.split_oracle import split_sample
+    graph, pm, cache, feats, labels, samples, params = _workload(kind, g)
+    p_graph, p_eager = copy.deepcopy(params), copy.deepcopy(params)
+    engine._API_GRAPHS.clear()
+    l_graph = _train(sg, p_graph, samples, pm, cache, feats, labels)
+    assert len(engine._API_GRAPHS) >= 1  # the captured path ran
+    monkeypatch.setenv("SG_API_EAGER", "1")
+    l_eager = _train(sg, p_eager, samples, pm, cache, feats, labels)
+    np.testing.assert_allclose(l_graph, l_eager, rtol=1e-5)
+    for k, v in p_graph.tensors().items():
+        assert rel_err(v, p_eager.tensors()[k]) < 1e-5, k
+    # float64 oracle replaying the same samples from the same init
+    from oracle.model_oracle import glorot_params
+    rp = glorot_params(kind, feats.shape[1], 8, 5, 3, seed=4)
+    for i, smp in enumerate(samples):
+        ws, wp = split_sample(smp.layer_vertices, smp.layer_edges, pm.assignment, g, cache.cached)
+        rloss, rgrads = CoopRun(rp, ws, wp, feats.astype(np.float64), labels).run()
+        reduce_and_sgd(rp, rgrads, 0.1, len(smp.targets))
+        assert abs(l_graph[i] - rloss) <= 1e-4 * abs(rloss), (i, l_graph[i], rloss)
+    for k, v in p_graph.tensors().items():
+        assert rel_err(v, rp[k]) < 1e-4, k
+
+
+def test_api_lazy_views_and_states():
+    """split_minibatch's host views are built on first access and equal the
+    oracle split; states after a captured run() equal the eager executor's."""
+    import paper_2303_13775_b200 as sg
+    from oracle.split_oracle import split_sample
+    graph, pm, cache, feats, labels, samples, params = _workload("graphsage", 2, steps=1)
+    smp = samples[0]
+    splits, plan = sg.split_minibatch(smp, pm, cache)
+    assert splits._fill_fn is not None and len(splits) == 2  # not built yet
+    ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+    loss, grads = ex.run()
+    assert splits._fill_fn is not None  # run() did not need the host views
+    assert grads[0]._lazy
+    ws, wp = split_sample(smp.layer_vertices, smp.layer_edges, pm.assignment, 2, cache.cached)
+    for d in range(2):
+        for l in range(4):
+            assert np.array_equal(splits[d].owned_gids[l], ws[d]["owned_gids"][l])
+    assert plan.pair_count(1) == sum(e.count for (l, _, _), e in plan.entries.items() if l == 1)
+    ex2 = sg.SplitExecutor(params, *sg.split_minibatch(smp, pm, cache), feats, labels)
+    ex2.forward()
+    for d in range(2):
+        for l in range(4):
+            np.testing.assert_array_equal(ex.states[d].h[l], ex2.states[d].h[l])
+    assert set(grads[0].keys()) == set(params.tensors().keys())
+
+
+def test_api_partial_cache():
+    """Cache misses staged from host memory on the captured API path."""
+    import copy
+    import paper_2303_13775_b200 as sg
+    graph, pm, cache, feats, labels, samples, params = _workload("graphsage", 2, cache_frac=0.2, steps=3)
+    p1, p2 = copy.deepcopy(params), copy.deepcopy(params)
+    l1 = _train(sg, p1, samples, pm, cache, feats, labels)
+    os.environ["SG_API_EAGER"] = "1"
+    try:
+        l2 = _train(sg, p2, samples, pm, cache, feats, labels)
+    finally:
+        del os.environ["SG_API_EAGER"]
+    np.testing.assert_allclose(l1, l2, rtol=1e-5)

@@ -52,3 +52,118 @@ def test_refine_history_never_increases():
     assert all(b <= a for a, b in zip(hist, hist[1:])), hist
     assert hist[-1] < hist[0]
     assert np.bincount(part, minlength=g).max() <= sg.max_part_size(graph.num_vertices, g, 0.05)
+
+
+# ---- quality against the reference partitioner (tests/golden/partition_quality.json,
+#      written by tests/golden/make_partition_golden.py from reference partition_graph)
+
+def _quality_cases():
+    import json
+    import os
+    here = os.path.dirname(os.path.abspath(__file__))
+    with open(os.path.join(here, "golden", "partition_quality.json")) as f:
+        gold = json.load(f)
+    return gold
+
+
+def _quality_graph(name):
+    from partition_graphs import permuted, planted_blocks, powerlaw_edges, reference_planted_edges
+    if name == "ref_planted":
+        return 4000, *reference_planted_edges(4000, 4, 0.1, 0.001, seed=3)
+    if name == "ref_planted_permuted":
+        return 4000, *permuted(4000, *reference_planted_edges(4000, 4, 0.1, 0.001, seed=3), seed=11)
+    if name == "planted8_shuffled":
+        return 20000, *planted_blocks()
+    if name == "powerlaw50k":
+        return 50000, *powerlaw_edges()
+    raise KeyError(name)
+
+
+# ours may exceed the reference's cut by at most this factor (the reference is a
+# sequential multilevel heuristic; ours a parallel one: same contract, different moves)
+QUALITY_SLACK = 1.10
+
+
+@pytest.mark.parametrize("name", ["ref_planted", "ref_planted_permuted", "planted8_shuffled", "powerlaw50k"])
+def test_partition_quality_vs_reference(name):
+    import paper_2303_13775_b200 as sg
+    gold = _quality_cases()[name]
+    n, s, d = _quality_graph(name)
+    assert len(s) == gold["m"] and int((s * 1000003 + d).sum() % (1 << 61)) == gold["edge_checksum"]
+    graph = sg.from_edges(n, s, d)
+    for g, ref_cut in gold["cut"].items():
+        g = int(g)
+        pm = sg.partition_graph(graph, g, 0.05, seed=5)
+        assert pm.counts().max() <= sg.max_part_size(n, g, 0.05)
+        cut = sg.cut_size(graph, pm)
+        print(f"[quality] {name} g={g}: cut {cut} vs reference {ref_cut} ({cut / max(ref_cut, 1):.3f}x)")
+        assert cut <= QUALITY_SLACK * ref_cut + 2, (name, g, cut, ref_cut)
+        if name.startswith("ref_planted"):
+            assert 1.0 - cut / len(s) >= 0.90  # reference test_partition.py:62-69
+
+
+def _bridge():
+    import itertools
+    import paper_2303_13775_b200 as sg
+    edges = [(u, v) for blk in ([0, 1, 2], [3, 4, 5]) for u, v in itertools.permutations(blk, 2)]
+    edges.append((2, 3))
+    s, d = zip(*edges)
+    return sg.from_edges(6, np.array(s), np.array(d))
+
+
+def test_bridge_graph_optimal_cut():
+    """reference test_partition.py:49-58: the two cliques separated, cut 1 (the
+    exhaustive optimum), also when the ids are interleaved."""
+    import paper_2303_13775_b200 as sg
+    g = _bridge()
+    pm = sg.partition_graph(g, 2, 0.0, seed=0)
+    assert sg.cut_size(g, pm) == 1
+    assert len(set(pm.assignment[:3])) == 1 and len(set(pm.assignment[3:])) == 1
+    assert pm.assignment[0] != pm.assignment[3]
+    perm = np.array([0, 3, 1, 4, 2, 5])  # vertex i -> perm[i]: the cliques interleave in id order
+    s = perm[np.repeat(np.arange(6), np.diff(g.row_offsets))]
+    d = perm[g.col_indices.astype(np.int64)]
+    gp = sg.from_edges(6, d, s)
+    pmp = sg.partition_graph(gp, 2, 0.0, seed=0)
+    assert sg.cut_size(gp, pmp) == 1
+
+
+def test_single_device_and_errors():
+    """reference test_partition.py:43-47, 88-96."""
+    import paper_2303_13775_b200 as sg
+    g = _bridge()
+    pm = sg.partition_graph(g, 1, 0.0, seed=0)
+    assert np.array_equal(pm.assignment, np.zeros(6, dtype=np.int64)) and sg.cut_size(g, pm) == 0
+    for args in ((7, 0.0), (2, -0.1), (0, 0.0)):
+        with pytest.raises(ValueError):
+            sg.partition_graph(g, *args, seed=0)
+
+
+def test_partition_balance_and_determinism_small():
+    """reference test_partition.py:72-86 (random small graphs, g = 2, 3)."""
+    import paper_2303_13775_b200 as sg
+    rng = np.random.default_rng(0)
+    for trial in range(5):
+        n = int(rng.integers(10, 80))
+        m = int(rng.integers(0, 4 * n))
+        g = sg.from_edges(n, rng.integers(0, n, m), rng.integers(0, n, m))
+        for devices in (2, 3):
+            pm = sg.partition_graph(g, devices, 0.05, seed=trial)
+            assert pm.counts().max() <= sg.max_part_size(n, devices, 0.05)
+            again = sg.partition_graph(g, devices, 0.05, seed=trial)
+            assert np.array_equal(pm.assignment, again.assignment)
+
+
+def test_refinement_never_increases_cut_random():
+    """reference test_partition.py:99-115 (50 random graphs, random starts, eps 1.0)."""
+    import paper_2303_13775_b200 as sg
+    rng = np.random.default_rng(42)
+    for trial in range(50):
+        n = int(rng.integers(8, 40))
+        m = int(rng.integers(n, 5 * n))
+        g = sg.from_edges(n, rng.integers(0, n, m), rng.integers(0, n, m))
+        devices = int(rng.integers(2, 5))
+        assign = rng.integers(0, devices, n)
+        refined, history = sg.refine_assignment(g, assign, devices, balance_eps=1.0)
+        assert all(b <= a for a, b in zip(history, history[1:]))
+        assert sg.cut_size(g, sg.PartitionMap(refined, devices, 1.0)) == history[-1]
