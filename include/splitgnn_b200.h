@@ -512,6 +512,19 @@ int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, const int64_t*
 int sg_partition_refine_host(int64_t n, const int64_t* off, const int32_t* nbr, const int32_t* wt,
                              const int32_t* vw, int32_t g, int64_t cap, int32_t max_passes, int32_t* part,
                              int64_t* cut_out);
+/* sg_gat_wgrad_dst: GAT layer-1 weight gradient in one destination-centric
+ * pass (engine.py:480-552 regrouped by destination: dW = sum_v A_v^T dn_v +
+ * SB (x) a_src + SC (x) a_dst, da_src = SB W, da_dst = SC W with
+ * A_v = sum_u alpha_uv h_u, SB = sum dpre_uv h_u, SC = sum_v dt_v h_self(v));
+ * replaces sg_gat_bwd_src + sg_gat_bwd_param at layer 1. D = 64, heads in
+ * {1, 2, 4}, w % 4 == 0, w <= 128. partial: nblocks slices of w*64 + 128
+ * floats [dW | da_src | da_dst]; sg_gat_wgrad_dst_blocks gives nblocks. */
+int32_t sg_gat_wgrad_dst_blocks(int64_t rows);
+int sg_gat_wgrad_dst(const void* split_ws, const SgSplitLayout* lay, int32_t d, int32_t w, int32_t heads,
+                     const float* h0, const int32_t* src_row, const int32_t* dperm, const float* alpha,
+                     const float* d_pre, const float* dnc, const float* dnc_recv, int32_t recv_stride,
+                     const float* dt_loc, const float* dt_recv, const float* W, const float* a_src,
+                     const float* a_dst, float* partial, int32_t nblocks, void* stream);
 /* sg_reduce_partials with the SGD step fused (single device, nothing to
  * all-reduce): jobs are 6 int64 per job {partials, nblocks, n, out, param,
  * n_sgd}; the first n_sgd summed columns g also update param: p -= scale*g

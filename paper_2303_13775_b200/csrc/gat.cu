@@ -1585,6 +1585,265 @@ __global__ void __launch_bounds__(256) k_gat_attn_partial(const SgMeta* __restri
     }                                                                                     \
   } while (0)
 
+// ---------------------------------------------------------------- layer-1 weight gradient, destination-centric
+// At layer 1 nothing needs d(loss)/d(h0), only dW, da_src, da_dst. Per source
+// row u the reference gradient is (engine.py:480-552)
+//   dz_u = sum_{e=(u->v)} alpha_e (.) dn_v + ds_u a_src + [u = self(v)] dt_v a_dst,
+//   ds_u = sum_e dpre_e,   dW = sum_u h_u^T dz_u,
+//   da_src = sum_u ds_u z_u,   da_dst = sum_v dt_v z_self(v),   z = h W.
+// All of it is linear in the edges, so it regroups by DESTINATION:
+//   dW^(h) = sum_v A_v^(h)T dn_v^(h) + SB^(h) (x) a_src^(h) + SC^(h) (x) a_dst^(h),
+//   A_v^(h) = sum_{u in N(v)} alpha_uv^(h) h_u,   SB^(h) = sum_v sum_u dpre_uv^(h) h_u,
+//   SC^(h) = sum_v dt_v^(h) h_self(v),   da_src^(h) = SB^(h) W^(h),  da_dst^(h) = SC^(h) W^(h).
+// One pass over each destination's in-edges (the forward's CSR-by-destination,
+// no sort by source), h rows gathered once per edge, no d_z / ds / dt_tot
+// round trip through HBM; replaces k_gat_bwd_src + the weight-gradient kernel
+// at layer 1. Warp per destination row (lanes own 4 columns of h), TM = 8 rows
+// per tile; per tile the A / B / h_self / dt / dn rows go to shared memory,
+// then dW (shared, 4x4 register blocks) += A^T dn and SB / SC += column sums.
+// Per-CTA partials in the k_gat_bwd_param layout [dW | da_src | da_dst].
+struct WdArgs {
+  int d, w, heads, stride, g;
+  int64_t eoff_li, rbase_li, pbase_l, voff_l;
+  const int32_t* rowbeg;
+  const int32_t* rowend;
+  const int32_t* lsrc;
+  const int32_t* dperm;
+  const int32_t* sendpos;
+  const int32_t* selfrow;
+  const int32_t* contrib;
+  const int32_t* src_row;
+  const float* h0;        // feature table [rows][w]
+  const float* alpha;     // [edge][head]
+  const float* d_pre;     // [edge][head]
+  const float* dnc;       // owned rows, stride D + H
+  const float* dnc_recv;  // pair layout, stride `stride`
+  const float* dt_loc;    // [row][head]
+  const float* dt_recv;   // receive layout, stride H
+  const float* W;         // [w][D]
+  const float* a_src;     // [D]
+  const float* a_dst;
+  float* partial;
+};
+
+constexpr int WD_D = 64;
+constexpr int WD_RPW = 2;            // destination rows per warp per tile
+constexpr int WD_TM = 8 * WD_RPW;    // rows per tile
+
+template <int H>
+__global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restrict__ meta, WdArgs a) {
+  SG_PDL_ENTRY();
+  constexpr int D = WD_D, DH = D / H, TM = WD_TM, RPW = WD_RPW;
+  extern __shared__ __align__(16) float sm[];
+  const int w = a.w, d = a.d;
+  const int HW = H * w;
+  float* dW_s = sm;                    // [w][D]
+  float* SB_s = dW_s + w * D;          // [H][w]
+  float* SC_s = SB_s + HW;             // [H][w]
+  float* A_s = SC_s + HW;              // [TM][H][w]
+  float* hs_s = A_s + TM * HW;         // [TM][w]
+  float* dn_s = hs_s + TM * w;         // [TM][D]
+  float* dt_s = dn_s + TM * D;         // [TM][H]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < w * D + 2 * HW; i += 256) sm[i] = 0.f;
+  const int l = 1;
+  const int n_own = meta->n_own[l][d];
+  const int R = n_own + meta->n_ref[l][d];
+  const int own0 = meta->own_off[l][d], ref0 = meta->ref_off[l][d];
+  const int prev0 = meta->own_off[l - 1][d];
+  const int64_t rb = a.rbase_li + own0 + ref0;
+  const int col = 4 * lane;
+  const bool colok = col < w;
+  const int nslots = (w / 4) * (D / 4);
+  const int ntiles = (R + TM - 1) / TM;
+  auto edge_x = [&](int j) -> int64_t { return a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j; };
+  auto ld_h = [&](int r) -> float4 {
+    return colok ? __ldg(reinterpret_cast<const float4*>(a.h0 + (int64_t)r * w + col))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto ld_e = [&](const float* base, int64_t x) -> float4 {  // the edge's H values (warp-uniform address)
+    if (H == 4) return __ldg(reinterpret_cast<const float4*>(base + x * 4));
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    t.x = base[x * H];
+    if (H > 1) t.y = base[x * H + 1];
+    return t;
+  };
+  // B = sum_e dpre_e h_u only enters through its total SB: this lane's running part
+  float4 B[H];
+#pragma unroll
+  for (int h = 0; h < H; ++h) B[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int q0 = tile * TM + wid * RPW;
+    // row bounds of this warp's RPW rows; the first row's index chain
+    int be = 0;
+    if (lane < 2 * RPW && q0 + (lane >> 1) < R)
+      be = (lane & 1) ? a.rowend[rb + q0 + (lane >> 1)] : a.rowbeg[rb + q0 + (lane >> 1)];
+    int b = __shfl_sync(0xffffffffu, be, 0), e = __shfl_sync(0xffffffffu, be, 1);
+    int xn = 0, hn = 0, un = 0;
+    if (q0 < R && lane < e - b) {
+      xn = (int)edge_x(b + lane);
+      un = prev0 + a.lsrc[xn];
+      hn = a.src_row ? a.src_row[un] : un;
+    }
+    __syncthreads();  // the previous tile's pass is done with the tile buffers
+    for (int i = 0; i < RPW; ++i) {
+      const int q = q0 + i;
+      const int rr = wid * RPW + i;  // tile row
+      float4 A[H];
+#pragma unroll
+      for (int h = 0; h < H; ++h) A[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 hs = make_float4(0.f, 0.f, 0.f, 0.f);
+      float dn_v = 0.f, dn_v2 = 0.f, dt_v = 0.f;
+      if (q < R) {  // warp-uniform
+        const int xc = xn, hc = hn, bc = b, ec = e;
+        // next row's bounds + first index hop, issued before this row's loads
+        int nb = 0, ne = 0;
+        const bool more = i + 1 < RPW && q + 1 < R;
+        if (more) {
+          nb = __shfl_sync(0xffffffffu, be, 2 * (i + 1));
+          ne = __shfl_sync(0xffffffffu, be, 2 * (i + 1) + 1);
+          if (lane < ne - nb) {
+            xn = (int)edge_x(nb + lane);
+            un = prev0 + a.lsrc[xn];
+          }
+        }
+        const bool own = q < n_own;
+        const float* dn_row = own ? a.dnc + (int64_t)(own0 + q) * (D + H)
+                                  : a.dnc_recv + (int64_t)a.sendpos[a.pbase_l + ref0 + (q - n_own)] * a.stride;
+        dn_v = dn_row[lane];
+        dn_v2 = dn_row[lane + 32];
+        if (own) {
+          const int64_t G = own0 + q;
+          int rs = prev0 + a.selfrow[a.voff_l + G];
+          if (a.src_row) rs = a.src_row[rs];
+          hs = ld_h(rs);
+          if (lane < H) {
+            dt_v = a.dt_loc[G * H + lane];
+            if (a.g > 1) {
+              const int* cb = a.contrib + (int64_t)a.g * a.voff_l + G * a.g;
+              for (int s2 = 0; s2 < a.g; ++s2) {
+                const int r2 = cb[s2];
+                if (r2 >= 0) dt_v += a.dt_recv[(int64_t)r2 * H + lane];
+              }
+            }
+          }
+        }
+        // one edge: A += alpha h_u, B += dpre h_u
+        auto edge = [&](const float4& v, int64_t x) {
+          const float4 al = ld_e(a.alpha, x), dp = ld_e(a.d_pre, x);
+          const float alh[4] = {al.x, al.y, al.z, al.w}, dph[4] = {dp.x, dp.y, dp.z, dp.w};
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            A[h].x = fmaf(alh[h], v.x, A[h].x); A[h].y = fmaf(alh[h], v.y, A[h].y);
+            A[h].z = fmaf(alh[h], v.z, A[h].z); A[h].w = fmaf(alh[h], v.w, A[h].w);
+            B[h].x = fmaf(dph[h], v.x, B[h].x); B[h].y = fmaf(dph[h], v.y, B[h].y);
+            B[h].z = fmaf(dph[h], v.z, B[h].z); B[h].w = fmaf(dph[h], v.w, B[h].w);
+          }
+        };
+        const int cnt0 = min(32, ec - bc);
+        for (int k0 = 0; k0 < cnt0; k0 += 4) {  // warp-uniform trip count
+          float4 v[4];
+          int xs[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int k = min(k0 + t, 31);
+            xs[t] = __shfl_sync(0xffffffffu, xc, k);
+            const int r = __shfl_sync(0xffffffffu, hc, k);
+            v[t] = (k0 + t < cnt0) ? ld_h(r) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (k0 + t < cnt0) edge(v[t], xs[t]);
+        }
+        // rows with more than 32 in-edges: the remaining edges, one at a time (rare)
+        for (int j = bc + 32; j < ec; ++j) {
+          const int64_t x = edge_x(j);
+          const int u = prev0 + a.lsrc[x];
+          edge(ld_h(a.src_row ? a.src_row[u] : u), x);
+        }
+        // second index hop of the next row, overlapping this row's tail
+        if (more) {
+          hn = (lane < ne - nb) ? (a.src_row ? a.src_row[un] : un) : 0;
+          b = nb;
+          e = ne;
+        }
+      }
+      if (colok) {
+#pragma unroll
+        for (int h = 0; h < H; ++h) *reinterpret_cast<float4*>(A_s + (rr * H + h) * w + col) = A[h];
+        *reinterpret_cast<float4*>(hs_s + rr * w + col) = hs;
+      }
+      dn_s[rr * D + lane] = dn_v;
+      dn_s[rr * D + lane + 32] = dn_v2;
+      if (lane < H) dt_s[rr * H + lane] = dt_v;
+    }
+    __syncthreads();
+    // dW += A^T dn (4x4 blocks: c-group cg of w, j-group jg of D; head of jg)
+    for (int s2 = tid; s2 < nslots; s2 += 256) {
+      const int cg = s2 / (D / 4), jg = s2 - cg * (D / 4);
+      const int hh = (4 * jg) / DH;
+      float acc[16];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 t4 = *reinterpret_cast<const float4*>(dW_s + (4 * cg + i) * D + 4 * jg);
+        acc[4 * i] = t4.x; acc[4 * i + 1] = t4.y; acc[4 * i + 2] = t4.z; acc[4 * i + 3] = t4.w;
+      }
+#pragma unroll
+      for (int r = 0; r < TM; ++r) {
+        const float4 a4 = *reinterpret_cast<const float4*>(A_s + (r * H + hh) * w + 4 * cg);
+        const float4 g4 = *reinterpret_cast<const float4*>(dn_s + r * D + 4 * jg);
+        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          acc[4 * i + 0] = fmaf(av[i], g4.x, acc[4 * i + 0]);
+          acc[4 * i + 1] = fmaf(av[i], g4.y, acc[4 * i + 1]);
+          acc[4 * i + 2] = fmaf(av[i], g4.z, acc[4 * i + 2]);
+          acc[4 * i + 3] = fmaf(av[i], g4.w, acc[4 * i + 3]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        *reinterpret_cast<float4*>(dW_s + (4 * cg + i) * D + 4 * jg) =
+            make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
+    }
+    // SC += dt-weighted column sums of h_self
+    for (int idx = tid; idx < HW; idx += 256) {
+      const int hh = idx / w, c = idx - hh * w;
+      float sc = SC_s[idx];
+#pragma unroll
+      for (int r = 0; r < TM; ++r) sc = fmaf(dt_s[r * H + hh], hs_s[r * w + c], sc);
+      SC_s[idx] = sc;
+    }
+  }
+  // SB = the warps' running B parts, summed in warp order (A_s is free now)
+  __syncthreads();
+  if (colok) {
+#pragma unroll
+    for (int h = 0; h < H; ++h) *reinterpret_cast<float4*>(A_s + (wid * H + h) * w + col) = B[h];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < HW; idx += 256) {
+    float sb = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) sb += A_s[ww * HW + idx];
+    SB_s[idx] = sb;
+  }
+  __syncthreads();
+  // dW^(h) += SB^(h) (x) a_src^(h) + SC^(h) (x) a_dst^(h); da = S W (per head)
+  float* out = a.partial + (int64_t)blockIdx.x * ((int64_t)w * D + 2 * D);
+  for (int idx = tid; idx < w * D; idx += 256) {
+    const int c = idx / D, j = idx - c * D, hh = j / DH;
+    out[idx] = dW_s[idx] + SB_s[hh * w + c] * a.a_src[j] + SC_s[hh * w + c] * a.a_dst[j];
+  }
+  if (tid < 2 * D) {
+    const int j = tid & (D - 1), hh = j / DH;
+    const float* S = (tid < D ? SB_s : SC_s) + hh * w;
+    float v = 0.f;
+    for (int c = 0; c < w; ++c) v = fmaf(S[c], a.W[c * D + j], v);
+    out[(int64_t)w * D + tid] = v;
+  }
+}
+
 }  // namespace
 
 #define SPLIT_PTRS                                                     \
@@ -1916,6 +2175,52 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
     ::sg::launch(k_gat_bwd_param<0>, nblocks, 256, smem, st, meta, a);
   }
   SG_CHECK_LAUNCH("k_gat_bwd_param");
+  return SG_OK;
+}
+
+
+// Layer-1 weight gradient of GAT in one destination-centric pass (see
+// k_gat_wgrad_dst): replaces sg_gat_bwd_src + sg_gat_bwd_param at layer 1
+// (engine.py:480-552, nothing needs d(loss)/d(features)). D = 64, heads in
+// {1, 2, 4}, w % 4 == 0 and w <= 128; partial holds nblocks slices of
+// w*64 + 128 floats ([dW | da_src | da_dst], the k_gat_bwd_param layout).
+extern "C" int32_t sg_gat_wgrad_dst_blocks(int64_t rows) {
+  return (int32_t)std::max<int64_t>(1, std::min<int64_t>((rows + WD_TM - 1) / WD_TM, 3 * kSMs));  // 3 CTAs / SM
+}
+
+extern "C" int sg_gat_wgrad_dst(const void* split_ws, const SgSplitLayout* lay, int32_t d, int32_t w, int32_t heads,
+                                const float* h0, const int32_t* src_row, const int32_t* dperm, const float* alpha,
+                                const float* d_pre, const float* dnc, const float* dnc_recv, int32_t recv_stride,
+                                const float* dt_loc, const float* dt_recv, const float* W, const float* a_src,
+                                const float* a_dst, float* partial, int32_t nblocks, void* stream) {
+  SG_REQUIRE(split_ws && lay && h0 && alpha && d_pre && dnc && dt_loc && W && a_src && a_dst && partial,
+             "gat_wgrad_dst: null argument");
+  SPLIT_PTRS
+  SG_REQUIRE(d >= 0 && d < y.g && y.L >= 1, "gat_wgrad_dst: bad device");
+  SG_REQUIRE(w % 4 == 0 && w >= 4 && w <= 128 && (heads == 1 || heads == 2 || heads == 4),
+             "gat_wgrad_dst: needs w % 4 == 0, w <= 128, heads in {1, 2, 4}, D = 64");
+  SG_REQUIRE(nblocks >= 1, "gat_wgrad_dst: nblocks >= 1");
+  WdArgs a;
+  memset(&a, 0, sizeof(a));
+  a.d = d; a.w = w; a.heads = heads; a.stride = recv_stride; a.g = y.g;
+  a.eoff_li = y.eoff[0]; a.rbase_li = y.rbase[0]; a.pbase_l = y.pbase[1]; a.voff_l = y.voff[1];
+  a.rowbeg = I32p(y.o_rowbeg); a.rowend = I32p(y.o_rowend); a.lsrc = I32p(y.o_lsrc); a.dperm = dperm;
+  a.sendpos = I32p(y.o_sendpos); a.selfrow = I32p(y.o_selfrow); a.contrib = I32p(y.o_contrib);
+  a.src_row = src_row; a.h0 = h0; a.alpha = alpha; a.d_pre = d_pre; a.dnc = dnc; a.dnc_recv = dnc_recv;
+  a.dt_loc = dt_loc; a.dt_recv = dt_recv; a.W = W; a.a_src = a_src; a.a_dst = a_dst; a.partial = partial;
+  const int HW = heads * w;
+  const size_t smem = sizeof(float) * ((size_t)w * WD_D + 2 * HW + (size_t)WD_TM * (HW + w + WD_D + heads));
+  SG_REQUIRE(smem <= 227 * 1024, "gat_wgrad_dst: shared memory");
+  cudaStream_t st = (cudaStream_t)stream;
+switch (heads) {
+    case 1: { const cudaError_t e1 = allow_max_smem<k_gat_wgrad_dst<1>>(); SG_CUDA(e1);
+              ::sg::launch(k_gat_wgrad_dst<1>, nblocks, 256, smem, st, meta, a); break; }
+    case 2: { const cudaError_t e2 = allow_max_smem<k_gat_wgrad_dst<2>>(); SG_CUDA(e2);
+              ::sg::launch(k_gat_wgrad_dst<2>, nblocks, 256, smem, st, meta, a); break; }
+    default: { const cudaError_t e4 = allow_max_smem<k_gat_wgrad_dst<4>>(); SG_CUDA(e4);
+               ::sg::launch(k_gat_wgrad_dst<4>, nblocks, 256, smem, st, meta, a); break; }
+  }
+  SG_CHECK_LAUNCH("k_gat_wgrad_dst");
   return SG_OK;
 }
 

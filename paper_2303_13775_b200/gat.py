@@ -46,6 +46,22 @@ def _from_owner(step, l, rows, width):
     return out
 
 
+def _wgrad_dst_ok(step):
+    """Layer 1 runs the destination-centric weight gradient (sg_gat_wgrad_dst):
+    D = 64, heads in {1, 2, 4}, w % 4 == 0, w <= 128; SG_GAT_WGRAD_DST=0 turns
+    it off (then k_gat_bwd_src + the weight-gradient kernel, as at every other layer)."""
+    import os
+    if os.environ.get("SG_GAT_WGRAD_DST", "1") != "1" or step.L < 1:
+        return False
+    w, dout = step.p.layer_dims(0)
+    return dout == 64 and step.p.heads_of(0) in (1, 2, 4) and w % 4 == 0 and w <= 128
+
+
+def _csr_lmin(step):
+    """Lowest layer whose backward needs the CSR by source row."""
+    return 2 if _wgrad_dst_ok(step) else 1
+
+
 def gat_forward(step):
     if getattr(step.f, "padded", False):
         raise ValueError("the GAT kernels read unpadded feature rows (FeatureStore pad_rows=False)")
@@ -55,7 +71,7 @@ def gat_forward(step):
     with step.phase("layer0"):
         step.layer0()
     dperm = step._dst_perm()
-    step._launch_src_csr_async(1)
+    step._launch_src_csr_async(_csr_lmin(step))
     dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
     nEtot = int(ds.lay.nEtot)
     step.h[0] = step.f.table
@@ -125,7 +141,7 @@ def gat_backward(step):
     dp_ptr = (lambda d: _lib.ptr(dperm[d][0])) if dperm is not None else (lambda d: None)
     nEtot = int(ds.lay.nEtot)
     with step.phase("src_csr_join"):
-        csr, kb = step._join_src_csr(1)
+        csr, kb = step._join_src_csr(_csr_lmin(step))
     d_h = step.d_h
     from paper_2303_13775_b200.engine import TSPMM_MIN_EDGES, _nblocks
     for l in range(step.L, 0, -1):
@@ -157,6 +173,21 @@ def gat_backward(step):
             step.transport.to_owner(ds, l, dt_send, dt_recv, H)
             if step.meta is not None:
                 step.wire_bytes += int(step.meta.npairs[l]) * 4 * H
+        if l == 1 and _wgrad_dst_ok(step):
+            # one destination-centric pass: dW, da_src, da_dst (no d_z / ds / dt_tot)
+            npart = w * dout + 2 * dout
+            with step.phase(f"bwd_param{l}"):
+                for d in step.devices:
+                    nb = int(_lib.load().sg_gat_wgrad_dst_blocks(step.n_rows(l, d)))
+                    part = _f32(nb * npart, device=step.dev)
+                    _lib.call("sg_gat_wgrad_dst", _lib.ptr(ds.ws), ds.lay, d, w, H, _lib.ptr(h_prev),
+                              _lib.ptr(src_row), dp_ptr(d), _lib.ptr(keep["alpha"]), _lib.ptr(d_pre),
+                              _lib.ptr(dnc), _lib.ptr(dnc_recv), DS, _lib.ptr(dt_loc), _lib.ptr(dt_recv),
+                              _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(part), nb, st)
+                    step.jobs.append((part, nb, npart, step.grads[d], p.offset(f"layer{l-1}.w")))
+                    step._partials.append(part)
+            d_h = None
+            continue
         d_z = _f32(nVp, dout, device=step.dev)
         dsb = _f32(nVp, *_hs(H), device=step.dev)
         dt_tot = _f32(nV, *_hs(H), device=step.dev)
@@ -167,7 +198,7 @@ def gat_backward(step):
                     nf = int(_lib.load().sg_tspmm_part_floats(ds.nE[l - 1], dout, H))
                     part = _f32(nf, device=step.dev)
                     _lib.call("sg_gat_bwd_src_lb", _lib.ptr(ds.ws), ds.lay, l, d, dout, H, _lib.ptr(keys),
-                              _lib.ptr(perm), _lib.ptr(beg), _lib.ptr(end), kb[l], 1, _lib.ptr(keep["alpha"]),
+                              _lib.ptr(perm), _lib.ptr(beg), _lib.ptr(end), kb[l], _csr_lmin(step), _lib.ptr(keep["alpha"]),
                               _lib.ptr(d_pre), _lib.ptr(dnc), _lib.ptr(dnc_recv), DS, _lib.ptr(dt_loc),
                               _lib.ptr(dt_recv), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(d_z), _lib.ptr(dsb),
                               _lib.ptr(dt_tot), _lib.ptr(part), ds.nE[l - 1], step.n_own(l - 1, d), st)

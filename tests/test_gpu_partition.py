@@ -167,3 +167,20 @@ def test_refinement_never_increases_cut_random():
         refined, history = sg.refine_assignment(g, assign, devices, balance_eps=1.0)
         assert all(b <= a for a, b in zip(history, history[1:]))
         assert sg.cut_size(g, sg.PartitionMap(refined, devices, 1.0)) == history[-1]
+
+
+@pytest.mark.parametrize("g,frac", [(1, 0.3), (2, 0.05), (4, 0.25), (3, 1.0), (8, 0.0)])
+def test_build_cache_gpu_matches_reference_policy(g, frac):
+    """build_cache on the GPU == reference partition.py:358-377 (oracle restatement:
+    highest in+out degree per partition, ties by lower id, ceil(frac*n) each),
+    on a graph with many degree ties, under a non-contiguous partition."""
+    import paper_2303_13775_b200 as sg
+    from oracle.workload import build_cache as ref_build_cache
+    graph, blk = _planted(n=6000, k=8, m=30000, seed=g)
+    assign = (blk % g) if g > 1 else np.zeros(graph.num_vertices, dtype=np.int64)
+    pm = sg.PartitionMap(np.asarray(assign, dtype=np.int64), g, 10.0)
+    got = sg.build_cache(graph, pm, frac)
+    want = ref_build_cache(np.asarray(graph.row_offsets), np.asarray(graph.col_indices), assign, g, frac)
+    assert len(got.cached) == g
+    for d in range(g):
+        assert np.array_equal(got.cached[d], want[d]), d

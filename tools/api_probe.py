@@ -54,6 +54,28 @@ for smp in samples[10:]:
 torch.cuda.synchronize()
 t = time.perf_counter() - t
 print(f"api loop: {1e3 * t / 20:.3f} ms/step; " + ", ".join(f"{k} {1e3 * v / 20:.3f}" for k, v in T.items()))
+# the same loop with a device synchronise after every call: wall time of each
+# call INCLUDING the GPU work it queued
+S = {"split+h2d": 0.0, "exec_init": 0.0, "replay": 0.0, "allreduce": 0.0}
+for smp in samples[10:]:
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    splits, plan = sg.split_minibatch(smp, pm, cache)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    loss, grads = ex.run()
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    sg.allreduce_and_step(params, grads, 0.1, len(smp.targets))
+    torch.cuda.synchronize()
+    t4 = time.perf_counter()
+    for k, a, b in (("split+h2d", t0, t1), ("exec_init", t1, t2), ("replay", t2, t3), ("allreduce", t3, t4)):
+        S[k] += b - a
+print("synchronised: " + ", ".join(f"{k} {1e3 * v / 20:.3f}" for k, v in S.items()) +
+      f" ms; packed words {splits.device_split.packed[1]}, geometry words {splits.device_split.packed[2].words}")
 pr = cProfile.Profile()
 pr.enable()
 for smp in samples[10:]:
