@@ -505,10 +505,12 @@ int sg_partition_coarse_host(int64_t n, const int64_t* off, const int32_t* nbr, 
 /* sg_pack_sample (HOST memory, CPU): a sample's arrays (V^0..V^L, E^l sources,
  * E^l destinations; each int32 or int64, elem_bytes 4 / 8) copied as int32 to
  * out + dst_off[i] (words), after an int64 header of the 2L+1 sizes
- * [nV_0..nV_L, nE_1..nE_L]; split over `threads` host threads (0 = all).
+ * [nV_0..nV_L, nE_1..nE_L]; split over `threads` host threads (0 = all),
+ * non-temporal stores (the buffer is read next by the H2D DMA, not a CPU).
+ * vrange (nullable) receives [min, max] over the vertex ids V^0..V^L.
  * split_minibatch's staging of the sample (scheduler.py:164). */
 int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, const int64_t* dst_off, const void* const* src,
-                   const int32_t* elem_bytes, int32_t threads);
+                   const int32_t* elem_bytes, int32_t threads, int64_t* vrange);
 int sg_partition_refine_host(int64_t n, const int64_t* off, const int32_t* nbr, const int32_t* wt,
                              const int32_t* vw, int32_t g, int64_t cap, int32_t max_passes, int32_t* part,
                              int64_t* cut_out);

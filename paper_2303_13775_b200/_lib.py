@@ -99,10 +99,10 @@ _SIGS = {
     "sg_partition_round": (i32, [vp, vp, vp, vp, i64, i32, i64, u64, i32, vp, vp, vp, vp, vp]),
     "sg_partition_coarse_host": (i32, [i64, vp, vp, vp, vp, i32, i64, u64, i32, vp, vp]),
     "sg_partition_refine_host": (i32, [i64, vp, vp, vp, vp, i32, i64, i32, vp, vp]),
-    "sg_pack_sample": (i32, [vp, i32, vp, vp, vp, vp, i32]),
+    "sg_pack_sample": (i32, [vp, i32, vp, vp, vp, vp, i32, vp]),
     "sg_gat_wgrad_dst_blocks": (i32, [i64]),
     "sg_gat_wgrad_dst": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp,
-                               i32, vp, vp, f32, vp]),
+                               i32, vp]),
     "sg_gpu_sampler_ws_bytes": (i64, [i64, i64, i64, i32]),
     "sg_gpu_sampler_ws_init": (i32, [vp, i64, i64, vp]),
     "sg_gpu_sample": (i32, [vp, vp, i64, vp, i64, vp, i32, u64, vp, i64, vp, vp, i64, i64, vp, vp, vp, vp, vp, vp,

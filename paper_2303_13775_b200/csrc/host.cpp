@@ -3,7 +3,10 @@
 // the thread count (all randomness is counter-based, rng.h).
 #include <stdint.h>
 
+#include <emmintrin.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -531,7 +534,8 @@ extern "C" int sg_partition_refine_host(int64_t n, const int64_t* off, const int
 // header of the sizes as int64 [nV_0..nV_L, nE_1..nE_L]. The copy is split
 // evenly over `threads` host threads (it is a few MB per C2 sample).
 extern "C" int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, const int64_t* dst_off,
-                              const void* const* src, const int32_t* elem_bytes, int32_t threads) {
+                              const void* const* src, const int32_t* elem_bytes, int32_t threads,
+                              int64_t* vrange) {
   if (!out || L < 1 || !sizes || !dst_off || !src || !elem_bytes) {
     sg::set_error("pack_sample: bad argument");
     return SG_ERR_ARG;
@@ -548,32 +552,74 @@ extern "C" int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, con
     start[i + 1] = start[i] + len[i];
   }
   const int64_t total = start[narr];
-  auto copy_range = [&](int64_t a, int64_t b) {  // global element range [a, b)
+  // non-temporal stores unless SG_PACK_NT=0: right after a cached multi-core
+  // write the pinned buffer's H2D copy measured ~7 GB/s against ~48 GB/s
+  static const bool nt = [] {
+    const char* e = std::getenv("SG_PACK_NT");
+    return !(e && e[0] == '0');
+  }();
+  std::vector<int64_t> vmin(64, INT64_MAX), vmax(64, INT64_MIN);  // per thread, over V^0..V^L
+  auto copy_range = [&](int64_t a, int64_t b, int tix) {  // global element range [a, b)
     int i = (int)(std::upper_bound(start.begin(), start.end(), a) - start.begin()) - 1;
     while (a < b && i < narr) {
       const int64_t e = std::min(b, start[i + 1]);
       if (e > a) {
         const int64_t o = a - start[i], k = e - a;
         int32_t* dst = out + dst_off[i] + o;
-        if (elem_bytes[i] == 4) {
-          std::memcpy(dst, (const int32_t*)src[i] + o, 4 * k);
+        if (i <= L) {  // vertex ids: also their range (split_minibatch's validation)
+          int64_t lo = vmin[tix], hi = vmax[tix];
+          for (int64_t j = 0; j < k; ++j) {
+            const int64_t v = elem_bytes[i] == 4 ? (int64_t)((const int32_t*)src[i])[o + j]
+                                                 : ((const int64_t*)src[i])[o + j];
+            lo = std::min(lo, v);
+            hi = std::max(hi, v);
+            if (nt) _mm_stream_si32(dst + j, (int32_t)v);
+            else dst[j] = (int32_t)v;
+          }
+          vmin[tix] = lo;
+          vmax[tix] = hi;
+        } else if (elem_bytes[i] == 4) {
+          const int32_t* s = (const int32_t*)src[i] + o;
+          if (nt) {  // streaming stores: the DMA engine reads the buffer next, not a CPU
+            int64_t j = 0;
+            for (; j < k && ((uintptr_t)(dst + j) & 15); ++j) _mm_stream_si32(dst + j, s[j]);
+            for (; j + 4 <= k; j += 4)
+              _mm_stream_si128((__m128i*)(dst + j), _mm_loadu_si128((const __m128i*)(s + j)));
+            for (; j < k; ++j) _mm_stream_si32(dst + j, s[j]);
+          } else {
+            std::memcpy(dst, s, 4 * k);
+          }
         } else {
           const int64_t* s = (const int64_t*)src[i] + o;
-          for (int64_t j = 0; j < k; ++j) dst[j] = (int32_t)s[j];
+          if (nt) {
+            for (int64_t j = 0; j < k; ++j) _mm_stream_si32(dst + j, (int32_t)s[j]);
+          } else {
+            for (int64_t j = 0; j < k; ++j) dst[j] = (int32_t)s[j];
+          }
         }
       }
       a = e;
       ++i;
     }
+    if (nt) _mm_sfence();
   };
+  static const int env_threads = [] {
+    const char* e = std::getenv("SG_PACK_THREADS");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env_threads > 0) threads = env_threads;
   const int T = std::max(1, std::min<int>(pick_threads(threads), (int)(total / (1 << 16)) + 1));
-  if (T == 1) {
-    copy_range(0, total);
-    return SG_OK;
+  const int TT = std::min(T, 64);
+  if (TT == 1) {
+    copy_range(0, total, 0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < TT; ++t) pool.emplace_back(copy_range, total * t / TT, total * (t + 1) / TT, t);
+    for (auto& th : pool) th.join();
   }
-  std::vector<std::thread> pool;
-  for (int t = 0; t < T; ++t)
-    pool.emplace_back(copy_range, total * t / T, total * (t + 1) / T);
-  for (auto& th : pool) th.join();
+  if (vrange) {
+    vrange[0] = *std::min_element(vmin.begin(), vmin.end());
+    vrange[1] = *std::max_element(vmax.begin(), vmax.end());
+  }
   return SG_OK;
 }

@@ -32,7 +32,7 @@ from paper_2303_13775_b200.metrics import EpochMetrics, IterationMetrics, accoun
 from paper_2303_13775_b200.models import DeviceParams, ModelParams, init_params
 from paper_2303_13775_b200.partition import CacheState, PartitionMap, full_cache
 from paper_2303_13775_b200.sampling import epoch_batches, sample_microbatches, sample_minibatch
-from paper_2303_13775_b200.scheduler import DeviceSplit, split_cost_packed, split_minibatch
+from paper_2303_13775_b200.scheduler import DeviceSplit, pinned_from, split_cost_packed, split_minibatch
 
 DEBUG_CHECK_FINITE = False
 NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions (measured best vs 592, 888)
@@ -724,7 +724,7 @@ class _PinnedFlat:
     last async copy (a buffer is rewritten only after that copy completed)."""
 
     def __init__(self, n):
-        self.t = torch.empty(n, dtype=torch.float32).pin_memory()
+        self.t = torch.empty(n, dtype=torch.float32, pin_memory=True)
         self.np = self.t.numpy()
         self.ev = None
 
@@ -1273,7 +1273,7 @@ class StaticSample:
         asynchronous: packing the next sample into a slot whose copy is still
         queued behind a running step would corrupt that step's input)."""
         if self.hbuf is None:
-            self.hbuf = [torch.zeros(self.words, dtype=torch.int32).pin_memory() for _ in range(2)]
+            self.hbuf = [torch.zeros(self.words, dtype=torch.int32, pin_memory=True) for _ in range(2)]
             self.hev = [None, None]
             self.slot = 0
         k = self.slot
@@ -1310,7 +1310,7 @@ class PinnedSample:
         self.compact = bool(compact) and all(
             len(b) < 2 or bool(np.all(np.diff(np.asarray(b)) >= 0)) for _, b in sample.layer_edges)
         if not self.compact:
-            self.buf = torch.from_numpy(host[:used].copy()).pin_memory()
+            self.buf = pinned_from(host[:used].copy())
             self.h2d_bytes = 4 * used
             return
         nV, nE = sample.sizes()
@@ -1324,7 +1324,7 @@ class PinnedSample:
             starts.append(st)
         st = np.concatenate(starts) if starts else np.zeros(0, np.int32)
         self.prefix_words = prefix
-        self.buf = torch.from_numpy(np.concatenate([host[:prefix], st])).pin_memory()
+        self.buf = pinned_from(np.concatenate([host[:prefix], st]))
         self.starts_off = 4 * prefix
         self.starts_bytes = 4 * len(st)
         self.h2d_bytes = 4 * prefix + self.starts_bytes
@@ -1588,7 +1588,7 @@ class SampledCapturedStep(CapturedStep):
         self.fanouts = [int(f) for f in fanouts]
         self.batch = int(batch)
         self.tgt = torch.zeros(self.batch + 1, dtype=torch.int64, device=self.dev)  # targets | seed
-        self.htgt = [torch.zeros(self.batch + 1, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self.htgt = [torch.zeros(self.batch + 1, dtype=torch.int64, pin_memory=True) for _ in range(2)]
         self.tev = [None, None]
         self.tslot = 0
 
@@ -1638,7 +1638,7 @@ class SampledCapturedStep(CapturedStep):
         """Pack [(targets, seed), ...] into pinned host buffers (untimed)."""
         out = []
         for t, sd in plan:
-            h = torch.zeros(self.batch + 1, dtype=torch.int64).pin_memory()
+            h = torch.zeros(self.batch + 1, dtype=torch.int64, pin_memory=True)
             a = h.numpy()
             a[:self.batch] = np.asarray(t, dtype=np.int64)
             a[self.batch] = np.int64(np.uint64(int(sd) & (2**64 - 1)).view(np.int64))
@@ -1651,7 +1651,7 @@ class SampledCapturedStep(CapturedStep):
         and an async D2H of the step's loss sum; one synchronisation at the
         end. Returns (loss sums, H2D bytes, D2H bytes)."""
         n = self.p.n
-        outs = torch.zeros(len(pinned), dtype=torch.float32).pin_memory()
+        outs = torch.zeros(len(pinned), dtype=torch.float32, pin_memory=True)
         for i, h in enumerate(pinned):
             self.tgt.copy_(h, non_blocking=True)
             self.graph.replay()

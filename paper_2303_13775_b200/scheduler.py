@@ -187,6 +187,17 @@ class _LazyEntries(dict):
     del _m, _wrap
 
 
+def pinned_from(a):
+    """A page-locked copy of host array `a` allocated pinned from the start
+    (torch.empty(..., pin_memory=True)): H2D from such buffers measured 48 GB/s
+    on B200 boxes against 22-28 GB/s from Tensor.pin_memory() copies
+    (tools/h2d_pinned_probe.py)."""
+    a = np.ascontiguousarray(a)
+    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+    t.numpy()[...] = a
+    return t
+
+
 def _bucket(x):
     """Capacity bucket: x rounded up to 1/8 of its power of two (>= 64)."""
     x = int(x)
@@ -249,8 +260,10 @@ class PackGeometry:
         sizes = np.array(list(nV) + list(nE), dtype=np.int64)
         ptrs = np.array([a.ctypes.data for a in arrs], dtype=np.uint64)
         eb = np.array([a.itemsize for a in arrs], dtype=np.int32)
+        vr = np.zeros(2, dtype=np.int64)
         _lib.call("sg_pack_sample", out.ctypes.data, L, sizes.ctypes.data, off.ctypes.data, ptrs.ctypes.data,
-                  eb.ctypes.data, 4)
+                  eb.ctypes.data, 4, vr.ctypes.data)
+        self.last_vrange = (int(vr[0]), int(vr[1]))
         return used
 
 
@@ -275,7 +288,7 @@ class _PinnedRing:
         if self.ev[k] is not None:
             self.ev[k].synchronize()
         if self.bufs[k] is None or self.bufs[k].numel() < geo.words:
-            self.bufs[k] = torch.empty(max(geo.words, 1 << 16), dtype=torch.int32).pin_memory()
+            self.bufs[k] = torch.empty(max(geo.words, 1 << 16), dtype=torch.int32, pin_memory=True)
         hb = self.bufs[k]
         used = geo.pack(sample, hb.numpy())
         return hb, used
@@ -394,6 +407,9 @@ class DeviceSplit:
         dev = torch.device(device or "cuda")
         geo = PackGeometry.for_sizes(nV, nE, scope=(len(nE), len(pm.assignment), pm.num_devices))
         hb, used = _PINNED.pack(geo, sample)
+        lo, hi = geo.last_vrange
+        if sum(nV) and (lo < 0 or hi >= len(pm.assignment)):  # checked while packing
+            raise ValueError("sample vertex missing from partition map")
         buf = torch.empty(geo.words, dtype=torch.int32, device=dev)
         buf[:used].copy_(hb[:used], non_blocking=True)
         _PINNED.record()
@@ -420,9 +436,9 @@ class DeviceSplit:
         nV, nE = sample.sizes()
         V, es, ed = sample.packed()
         dev = torch.device(device or "cuda")
-        Vt = torch.from_numpy(V).pin_memory().to(dev, non_blocking=True)
-        st = torch.from_numpy(es).pin_memory().to(dev, non_blocking=True)
-        dt = torch.from_numpy(ed).pin_memory().to(dev, non_blocking=True)
+        Vt = pinned_from(V).to(dev, non_blocking=True)
+        st = pinned_from(es).to(dev, non_blocking=True)
+        dt = pinned_from(ed).to(dev, non_blocking=True)
         return cls(Vt, st, dt, nV, nE, pm, cache, sample.is_dst_grouped(), dev, host_V=V)
 
     # -- device views -------------------------------------------------------
@@ -531,14 +547,14 @@ def split_minibatch(sample, pm: PartitionMap, cache: CacheState | None = None):
     host views; both carry `.device_split` for the executor. Raises ValueError
     for a sampled vertex outside the partition map (scheduler.py:175-178)."""
     sample = as_sample(sample)
-    n = len(pm.assignment)
-    for v in sample.layer_vertices:
-        v = np.asarray(v)
-        if len(v) and (v.max() >= n or v.min() < 0):
-            raise ValueError("sample vertex missing from partition map")
-    if sample.is_dst_grouped():
+    if sample.is_dst_grouped():  # the vertex range is checked while packing
         ds = DeviceSplit.from_sample_packed(sample, pm, cache)
     else:
+        n = len(pm.assignment)
+        for v in sample.layer_vertices:
+            v = np.asarray(v)
+            if len(v) and (v.max() >= n or v.min() < 0):
+                raise ValueError("sample vertex missing from partition map")
         ds = DeviceSplit.from_sample(sample, pm, cache)
     return _lazy_views(ds)
 

@@ -30,6 +30,20 @@ def test_library_exports_every_declared_symbol():
     assert not (set(syms) - set(_lib.EXPORTED)), sorted(set(syms) - set(_lib.EXPORTED))
 
 
+def test_ctypes_signatures_match_header_arity():
+    """Every ctypes binding in _lib._SIGS takes as many arguments as the header
+    declaration (a stale binding fails only at call time, on a GPU box)."""
+    from paper_2303_13775_b200 import _lib
+    text = open(os.path.join(ROOT, "include", "splitgnn_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    decl = {}
+    for m in re.finditer(r"\b(sg_[a-z0-9_]+)\s*\(([^;{]*?)\)\s*;", text, flags=re.S):
+        params = m.group(2).strip()
+        decl[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    bad = {k: (decl[k], len(args)) for k, (_, args) in _lib._SIGS.items() if k in decl and decl[k] != len(args)}
+    assert not bad, bad
+
+
 def test_struct_sizes_match_abi():
     from paper_2303_13775_b200 import _lib
     sizes = np.zeros(2, dtype=np.int64)
@@ -249,6 +263,8 @@ def test_pack_sample_matches_numpy_layout(dtype):
         assert np.array_equal(out[geo.o_es + o:geo.o_es + o + nE[l]], E[l][0].astype(np.int32))
         assert np.array_equal(out[geo.o_ed + o:geo.o_ed + o + nE[l]], E[l][1].astype(np.int32))
     assert used == geo.o_ed + geo.eoff[2] + nE[2]
+    allv = np.concatenate(V)
+    assert geo.last_vrange == (int(allv.min()), int(allv.max()))  # split_minibatch's range check
     # a smaller sample keeps the geometry (one cached graph serves both); a larger one grows it
     assert PackGeometry.for_sizes([x // 2 for x in nV], [x // 2 for x in nE], scope=("test", dtype)) is geo
     big = PackGeometry.for_sizes([2 * x for x in nV], nE, scope=("test", dtype))

@@ -76,6 +76,46 @@ for smp in samples[10:]:
         S[k] += b - a
 print("synchronised: " + ", ".join(f"{k} {1e3 * v / 20:.3f}" for k, v in S.items()) +
       f" ms; packed words {splits.device_split.packed[1]}, geometry words {splits.device_split.packed[2].words}")
+# pieces of split_minibatch: native pack into the pinned slot; the H2D copy alone
+from paper_2303_13775_b200.scheduler import _PINNED, PackGeometry  # noqa: E402
+geo = splits.device_split.packed[2]
+dst = torch.empty(geo.words, dtype=torch.int32, device="cuda")
+tp = th = 0.0
+for smp in samples[10:]:
+    t0 = time.perf_counter()
+    hb, used = _PINNED.pack(geo, smp)
+    t1 = time.perf_counter()
+    dst[:used].copy_(hb[:used], non_blocking=True)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    tp += t1 - t0
+    th += t2 - t1
+print(f"pack {1e3 * tp / 20:.3f} ms, H2D {1e3 * th / 20:.3f} ms for {4 * used / 1e6:.2f} MB "
+      f"({4 * used / (th / 20) / 1e9:.1f} GB/s)")
+
+
+def h2d_only(buf, k=20):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(k):
+        dst[:used].copy_(buf[:used], non_blocking=True)
+        torch.cuda.synchronize()
+    return 1e3 * (time.perf_counter() - t0) / k
+
+
+print(f"H2D only, ring slot: {h2d_only(hb):.3f} ms")
+fresh = torch.empty(geo.words, dtype=torch.int32, pin_memory=True)
+fresh.numpy()[:used] = hb.numpy()[:used]
+print(f"H2D only, fresh pinned buffer: {h2d_only(fresh):.3f} ms")
+print(f"H2D only, ring slot again: {h2d_only(hb):.3f} ms; slot is_pinned {hb.is_pinned()} "
+      f"data_ptr {hb.data_ptr():#x} numel {hb.numel()}")
+d2 = torch.empty(geo.words, dtype=torch.int32, device="cuda")
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(20):
+    d2[:used].copy_(hb[:used], non_blocking=True)
+    torch.cuda.synchronize()
+print(f"H2D only into a fresh device buffer: {1e3 * (time.perf_counter() - t0) / 20:.3f} ms")
 pr = cProfile.Profile()
 pr.enable()
 for smp in samples[10:]:
