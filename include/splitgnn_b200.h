@@ -332,6 +332,13 @@ int sg_gat_agg(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_
                const float* t_recv, const int32_t* dperm, float* pre_e, float* loc_m,
                float* loc_s, float* loc_U, float* sendbuf, int32_t send_stride,
                int64_t max_rows, void* stream);
+/* sg_gat_agg_fused: one device only -- sg_gat_agg with the owner combine
+ * (num = U / den, h, md) and the per-edge alpha (engine.py:380-400) folded
+ * into the aggregation epilogue (no holder partials to merge). */
+int sg_gat_agg_fused(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t dout, int32_t heads,
+                     float slope, const float* z, const float* s, const float* t, const int32_t* dperm, float* pre_e,
+                     int32_t final_layer, float* md, float* num, float* h, float* alpha, int64_t max_rows,
+                     void* stream);
 int sg_gat_combine(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                    int32_t dout, int32_t heads, const float* loc_m, const float* loc_s,
                    const float* loc_U, const float* recv, int32_t recv_stride,

@@ -57,6 +57,8 @@ struct V4<4> {
                        __shfl_xor_sync(m, v.z, o, w), __shfl_xor_sync(m, v.w, o, w));
   }
   __device__ static void add(T& a, T b) { a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w; }
+  __device__ static T div(T x, float s) { return make_float4(x.x / s, x.y / s, x.z / s, x.w / s); }
+  __device__ static T relu(T x) { return make_float4(sg_relu(x.x), sg_relu(x.y), sg_relu(x.z), sg_relu(x.w)); }
 };
 template <>
 struct V4<1> {
@@ -71,6 +73,8 @@ struct V4<1> {
   __device__ static float dot(T x, T y) { return x * y; }
   __device__ static T shfl_xor(unsigned m, T v, int o, int w) { return __shfl_xor_sync(m, v, o, w); }
   __device__ static void add(T& a, T b) { a += b; }
+  __device__ static T div(T x, float s) { return x / s; }
+  __device__ static T relu(T x) { return sg_relu(x); }
 };
 
 // ---------------------------------------------------------------- projection
@@ -681,6 +685,12 @@ struct AggArgs {
   float* loc_s;
   float* loc_U;         // [row][D]
   float* sendbuf;       // [U (D) | m (H) | s (H)]
+  // one device (no holders to combine): the owner combine and alpha folded in
+  int fuse, final_;
+  float* md;     // [m (H) | den (H)] per owned row
+  float* num;    // [row][D]
+  float* h;      // [row][D]
+  float* alpha;  // [edge][head]
 };
 
 // Team of RL = LPR*EG lanes per destination row; LPR lanes span D (VEC each),
@@ -743,6 +753,26 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
       ssum = ssum * f1 + s2 * f2;
       U = V::axpby(f1, U, f2, U2);
       m = mm;
+    }
+    if (a.fuse) {  // warp-uniform; every row is owned (g == 1)
+      const int64_t G = own0 + q;
+      if (eg == 0 && colok) {  // k_gat_combine with no senders: num = U / den
+        const T nv = V::div(U, ssum);
+        V::st(a.num + G * dout + col, nv);
+        V::st(a.h + G * dout + col, a.final_ ? nv : V::relu(nv));
+        if (head_lead) {
+          a.md[G * 2 * H + hl] = m;
+          a.md[G * 2 * H + H + hl] = ssum;
+        }
+      }
+      // k_gat_alpha over this row's edges (each edge group its own edges again)
+      for (int j = b + eg; j < e; j += EG) {
+        const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
+        const int u = prev0 + a.lsrc[x];
+        const float pre = a.s[(int64_t)u * H + hl] + tq;
+        if (head_lead && colok) a.alpha[x * H + hl] = expf(leaky(pre, a.slope) - m) / ssum;
+      }
+      continue;
     }
     if (eg != 0) continue;
     if (own) {
@@ -875,6 +905,45 @@ __global__ void k_gat_bwd_rows(const SgMeta* __restrict__ meta, BRowsArgs a) {
       c = fmaf(dn, nv, c);
     }
     a.dnc[G * st + dout + hh] = c;
+  }
+}
+
+// k_gat_bwd_rows with float4 lanes: LPH = d_head / 4 consecutive threads per
+// head of a row (power of two, <= 32), c reduced by an xor tree inside the
+// group; coalesced float4 loads of d_h / num (the scalar kernel walked d_head
+// contiguous floats per thread: 16 us for C3 layer 1 -> a few us).
+template <int LPH>
+__global__ void k_gat_bwd_rows4(const SgMeta* __restrict__ meta, BRowsArgs a) {
+  SG_PDL_ENTRY();
+  const int l = a.l, d = a.d, dout = a.dout, H = a.heads, st = dout + H, q4 = dout / 4;
+  const int n = meta->n_own[l][d];
+  const int own0 = meta->own_off[l][d];
+  const int64_t tot = (int64_t)n * q4;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k0 = t0 - (t0 % 32); k0 < tot; k0 += step) {  // warp-uniform trip count
+    const int64_t k = k0 + (threadIdx.x & 31);
+    const bool ok = k < tot;
+    const int64_t q = ok ? k / q4 : 0;
+    const int c4 = ok ? (int)(k - q * q4) : 0;
+    const int64_t G = own0 + q;
+    float4 nv = make_float4(0.f, 0.f, 0.f, 0.f), dn = nv;
+    if (ok) {
+      nv = *reinterpret_cast<const float4*>(a.num + G * dout + 4 * c4);
+      dn = *reinterpret_cast<const float4*>(a.d_h + G * dout + 4 * c4);
+      if (!a.final_) {
+        if (!(nv.x > 0.f)) dn.x = 0.f;
+        if (!(nv.y > 0.f)) dn.y = 0.f;
+        if (!(nv.z > 0.f)) dn.z = 0.f;
+        if (!(nv.w > 0.f)) dn.w = 0.f;
+      }
+      float* o = a.dnc + G * st + 4 * c4;  // stride D + H: not 16 B aligned
+      o[0] = dn.x; o[1] = dn.y; o[2] = dn.z; o[3] = dn.w;
+    }
+    float c = fmaf(dn.x, nv.x, fmaf(dn.y, nv.y, fmaf(dn.z, nv.z, dn.w * nv.w)));
+#pragma unroll
+    for (int o2 = 1; o2 < LPH; o2 <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o2);
+    if (ok && c4 % LPH == 0) a.dnc[G * st + dout + c4 / LPH] = c;
   }
 }
 
@@ -1989,6 +2058,31 @@ extern "C" int sg_gat_agg(const void* split_ws, const SgSplitLayout* lay, int32_
   return SG_OK;
 }
 
+// sg_gat_agg with the owner combine and alpha folded in (one device: every
+// row is owned, no holder partials): writes md, num, h and alpha directly.
+extern "C" int sg_gat_agg_fused(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t dout,
+                                int32_t heads, float slope, const float* z, const float* s, const float* t,
+                                const int32_t* dperm, float* pre_e, int32_t final_layer, float* md, float* num,
+                                float* h, float* alpha, int64_t max_rows, void* stream) {
+  SG_REQUIRE(split_ws && lay && z && s && t && pre_e && md && num && h && alpha, "gat_agg_fused: null argument");
+  SPLIT_PTRS
+  SG_REQUIRE(y.g == 1 && l >= 1 && l <= y.L, "gat_agg_fused: one device only (no holders to combine)");
+  GAT_HEADS_CHECK(dout, heads);
+  if (max_rows <= 0) return SG_OK;
+  AggArgs a;
+  memset(&a, 0, sizeof(a));
+  a.l = l; a.d = 0; a.dout = dout; a.heads = heads; a.stride = 0; a.slope = slope;
+  a.eoff_li = y.eoff[l - 1]; a.rbase_li = y.rbase[l - 1]; a.pbase_l = y.pbase[l];
+  a.rowbeg = I32p(y.o_rowbeg); a.rowend = I32p(y.o_rowend); a.lsrc = I32p(y.o_lsrc);
+  a.dperm = dperm; a.sendpos = I32p(y.o_sendpos);
+  a.z = z; a.s = s; a.t = t; a.pre_e = pre_e;
+  a.fuse = 1; a.final_ = final_layer; a.md = md; a.num = num; a.h = h; a.alpha = alpha;
+  cudaStream_t st = (cudaStream_t)stream;
+  GAT_TEAM_DISPATCH(k_gat_agg, dout, heads, max_rows, st, meta, a);
+  SG_CHECK_LAUNCH("k_gat_agg(fused)");
+  return SG_OK;
+}
+
 extern "C" int sg_gat_combine(const void* split_ws, const SgSplitLayout* lay, int32_t l, int32_t d,
                               int32_t dout, int32_t heads, const float* loc_m, const float* loc_s,
                               const float* loc_U, const float* recv, int32_t recv_stride,
@@ -2035,6 +2129,21 @@ extern "C" int sg_gat_bwd_rows(const void* split_ws, const SgSplitLayout* lay, i
   GAT_HEADS_CHECK(dout, heads);
   if (max_rows <= 0) return SG_OK;
   BRowsArgs a{l, d, dout, heads, final_layer, d_h, num, dnc};
+  const int dh = dout / heads;
+  if (dh % 4 == 0 && dh <= 128 && ((dh / 4) & (dh / 4 - 1)) == 0) {
+    const int grid = clamp_grid(div_up(max_rows * (dout / 4), 256), kSMs * 8);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (dh / 4) {
+      case 1: ::sg::launch(k_gat_bwd_rows4<1>, grid, 256, 0, st, meta, a); break;
+      case 2: ::sg::launch(k_gat_bwd_rows4<2>, grid, 256, 0, st, meta, a); break;
+      case 4: ::sg::launch(k_gat_bwd_rows4<4>, grid, 256, 0, st, meta, a); break;
+      case 8: ::sg::launch(k_gat_bwd_rows4<8>, grid, 256, 0, st, meta, a); break;
+      case 16: ::sg::launch(k_gat_bwd_rows4<16>, grid, 256, 0, st, meta, a); break;
+      default: ::sg::launch(k_gat_bwd_rows4<32>, grid, 256, 0, st, meta, a); break;
+    }
+    SG_CHECK_LAUNCH("k_gat_bwd_rows4");
+    return SG_OK;
+  }
   ::sg::launch(k_gat_bwd_rows, clamp_grid(div_up(max_rows * heads, 256), kSMs * 4), 256, 0, (cudaStream_t)stream, meta, a);
   SG_CHECK_LAUNCH("k_gat_bwd_rows");
   return SG_OK;

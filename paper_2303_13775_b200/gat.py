@@ -99,6 +99,21 @@ def gat_forward(step):
         send = _f32(P, SW, device=step.dev)
         recv = step._xbuf(P, SW)
         pre_e = _f32(nEtot, *_hs(H), device=step.dev)
+        if step.g == 1:
+            # one device: the owner combine and alpha ride on the aggregation epilogue
+            md = _f32(nV, 2 * H, device=step.dev)
+            num = _f32(nV, dout, device=step.dev)
+            h = _f32(nV, dout, device=step.dev)
+            alpha = _f32(nEtot, *_hs(H), device=step.dev)
+            with step.phase(f"agg{l}"):
+                step._ev(f"agg{l}_start")
+                _lib.call("sg_gat_agg_fused", _lib.ptr(ds.ws), ds.lay, l, dout, H, slope, _lib.ptr(z), _lib.ptr(s),
+                          _lib.ptr(t), dp_ptr(0), _lib.ptr(pre_e), final, _lib.ptr(md), _lib.ptr(num), _lib.ptr(h),
+                          _lib.ptr(alpha), step.n_rows(l, 0), st)
+                step._ev(f"agg{l}_end")
+            step.h[l] = h
+            step.keep[l] = dict(z=z, s=s, num=num, md=md, alpha=alpha, pre_e=pre_e)
+            continue
         loc_m = _f32(nV, *_hs(H), device=step.dev)
         loc_s = _f32(nV, *_hs(H), device=step.dev)
         loc_U = _f32(nV, dout, device=step.dev)
