@@ -1377,9 +1377,9 @@ __global__ void __launch_bounds__(256, 2) k_gat_wgrad_mma(const SgMeta* __restri
                                                                    : (16 * MB + 8 + 31) / 32 * 32 - 8;
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, H = a.heads, dh = D / H, w4 = w / 4;
-  const int wt = w + 1;
+  const int wt = w;  // W^T rows, float4-aligned (w % 4 == 0 on this path)
   const int stage_f = QTR * WP + QTR * DZP + QTR * D + 2 * QTR * H;
-  float* Wt_s = smem;                                      // [D][w+1] (d_prev only)
+  float* Wt_s = smem;                                      // [D][w] (d_prev only)
   float* stg = Wt_s + (a.d_prev ? D * wt : 0);             // 2 x stage
   int* idx_s = reinterpret_cast<int*>(stg + 2 * stage_f);  // [2][2][QTR]: h row, dt row
   if (a.d_prev)
@@ -1502,15 +1502,20 @@ __global__ void __launch_bounds__(256, 2) k_gat_wgrad_mma(const SgMeta* __restri
         ad = fmaf(z_s[rr * D + j], dt_s[rr * H + hh], ad);
       }
     }
-    if (a.d_prev) {
+    if (a.d_prev) {  // d_prev = d_z W^T: 4 columns per thread (one LDS.128 of W^T per j)
       const int nrow = min(QTR, n - tile * QTR);
-      for (int i = threadIdx.x; i < nrow * w; i += blockDim.x) {
-        const int rr = i / w, c = i - rr * w;
-        float sacc = 0.f;
+      for (int i = threadIdx.x; i < nrow * w4; i += blockDim.x) {
+        const int rr = i / w4, cg = i - rr * w4;
+        float4 sacc = make_float4(0.f, 0.f, 0.f, 0.f);
         const float* dzr = dz_s + rr * DZP;
 #pragma unroll 8
-        for (int j = 0; j < D; ++j) sacc = fmaf(dzr[j], Wt_s[j * wt + c], sacc);
-        a.d_prev[(int64_t)(own0 + tile * QTR + rr) * w + c] = sacc;
+        for (int j = 0; j < D; ++j) {
+          const float g = dzr[j];
+          const float4 wv = *reinterpret_cast<const float4*>(Wt_s + j * wt + 4 * cg);
+          sacc.x = fmaf(g, wv.x, sacc.x); sacc.y = fmaf(g, wv.y, sacc.y);
+          sacc.z = fmaf(g, wv.z, sacc.z); sacc.w = fmaf(g, wv.w, sacc.w);
+        }
+        *reinterpret_cast<float4*>(a.d_prev + (int64_t)(own0 + tile * QTR + rr) * w + 4 * cg) = sacc;
       }
     }
   }
@@ -1541,7 +1546,7 @@ int launch_wgrad_mma(const SgMeta* meta, const BParamArgs& a, int nblocks, cudaS
   constexpr int WP = ((16 * MB + 8 + 31) / 32 * 32 - 8) < 16 * MB ? (16 * MB + 8 + 31) / 32 * 32 + 24
                                                                    : (16 * MB + 8 + 31) / 32 * 32 - 8;
   const size_t stage_f = (size_t)QTR * WP + (size_t)QTR * (D + 8) + (size_t)QTR * D + 2 * (size_t)QTR * a.heads;
-  const size_t smem = sizeof(float) * ((a.d_prev ? (size_t)D * (a.w + 1) : 0) + 2 * stage_f) + sizeof(int) * 4 * QTR;
+  const size_t smem = sizeof(float) * ((a.d_prev ? (size_t)D * a.w : 0) + 2 * stage_f) + sizeof(int) * 4 * QTR;
   if (smem > 227 * 1024) {
     set_error("gat_bwd_param: width too large for the MMA path");
     return SG_ERR_ARG;
