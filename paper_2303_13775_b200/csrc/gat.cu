@@ -724,22 +724,42 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
     const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
     float m = -INFINITY, ssum = 0.f;
     T U = V::zero();
-    for (int j = b + eg; j < e; j += EG) {
-      const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
-      const int u = prev0 + a.lsrc[x];
-      const float pre = a.s[(int64_t)u * H + hl] + tq;
-      const float ev = leaky(pre, a.slope);
-      if (head_lead && colok) a.pre_e[x * H + hl] = pre;
-      const T zu = colok ? V::ld(a.z + (int64_t)u * dout + col) : V::zero();
-      if (ev > m) {
-        const float sc = expf(m - ev);  // 0 on the first edge (m = -inf)
-        ssum = fmaf(ssum, sc, 1.f);
-        U = V::axpby(1.f, zu, sc, U);
-        m = ev;
-      } else {
-        const float wv = expf(ev - m);
-        ssum += wv;
-        V::fma_(U, wv, zu);
+    // four edges' loads in flight per edge group, applied in edge order
+    for (int j0 = b + eg; j0 < e; j0 += 4 * EG) {
+      int64_t xs[4];
+      int us[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = j0 + t * EG;
+        xs[t] = j < e ? (a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j) : 0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) us[t] = j0 + t * EG < e ? prev0 + a.lsrc[xs[t]] : 0;
+      float pres[4];
+      T zs[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const bool ok = j0 + t * EG < e;
+        pres[t] = ok ? a.s[(int64_t)us[t] * H + hl] + tq : 0.f;
+        zs[t] = (ok && colok) ? V::ld(a.z + (int64_t)us[t] * dout + col) : V::zero();
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (j0 + t * EG >= e) break;
+        const float pre = pres[t];
+        const float ev = leaky(pre, a.slope);
+        if (head_lead && colok) a.pre_e[xs[t] * H + hl] = pre;
+        const T zu = zs[t];
+        if (ev > m) {
+          const float sc = expf(m - ev);  // 0 on the first edge (m = -inf)
+          ssum = fmaf(ssum, sc, 1.f);
+          U = V::axpby(1.f, zu, sc, U);
+          m = ev;
+        } else {
+          const float wv = expf(ev - m);
+          ssum += wv;
+          V::fma_(U, wv, zu);
+        }
       }
     }
 #pragma unroll
@@ -766,12 +786,22 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
         }
       }
       // k_gat_alpha over this row's edges (each edge group its own edges again)
-      for (int j = b + eg; j < e; j += EG) {
-        const int64_t x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
-        const int u = prev0 + a.lsrc[x];
-        const float pre = a.s[(int64_t)u * H + hl] + tq;
-        if (head_lead && colok) a.alpha[x * H + hl] = expf(leaky(pre, a.slope) - m) / ssum;
-      }
+      if (head_lead && colok)
+        for (int j0 = b + eg; j0 < e; j0 += 4 * EG) {
+          int64_t xs[4];
+          float ss[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int j = j0 + t * EG;
+            xs[t] = j < e ? (a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j) : 0;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            ss[t] = j0 + t * EG < e ? a.s[(int64_t)(prev0 + a.lsrc[xs[t]]) * H + hl] : 0.f;
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (j0 + t * EG < e) a.alpha[xs[t] * H + hl] = expf(leaky(ss[t] + tq, a.slope) - m) / ssum;
+        }
       continue;
     }
     if (eg != 0) continue;
@@ -997,23 +1027,40 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ 
     const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
     float dt = 0.f;
     const int rounds = (e - b + EG - 1) / EG;
-    for (int kk = 0; kk < rounds; ++kk) {
-      const int j = b + kk * EG + eg;
-      const bool ok = j < e;
-      int64_t x = 0;
-      float part = 0.f;
-      if (ok) {
-        x = a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j;
-        const int u = prev0 + a.lsrc[x];
-        if (colok) part = V::dot(dn, V::ld(a.z + (int64_t)u * dout + col));
+    // four rounds' loads in flight (the index chain and the z / alpha / pre_e
+    // reads of round k no longer wait for round k-1); rounds still applied in order
+    for (int k0 = 0; k0 < rounds; k0 += 4) {
+      int64_t xs[4];
+      int us[4];
+      bool oks[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int j = b + (k0 + t) * EG + eg;
+        oks[t] = k0 + t < rounds && j < e;
+        xs[t] = oks[t] ? (a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j) : 0;
       }
-      // d_alpha = d_num . z_u per head: reduce over the LH lanes of the head
-      for (int o = 1; o < LH; o <<= 1) part += __shfl_xor_sync(tmask, part, o, RL);
-      if (ok) {
-        const float de = a.alpha[x * H + hl] * (part - c);
-        const float dp = de * (a.pre_e[x * H + hl] > 0.f ? 1.f : a.slope);
-        if (head_lead && colok) a.d_pre[x * H + hl] = dp;
-        dt += dp;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) us[t] = oks[t] ? prev0 + a.lsrc[xs[t]] : 0;
+      T zs[4];
+      float als[4], prs[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        zs[t] = (oks[t] && colok) ? V::ld(a.z + (int64_t)us[t] * dout + col) : V::zero();
+        als[t] = oks[t] ? a.alpha[xs[t] * H + hl] : 0.f;
+        prs[t] = oks[t] ? a.pre_e[xs[t] * H + hl] : 0.f;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (k0 + t >= rounds) break;  // team-uniform
+        float part = (oks[t] && colok) ? V::dot(dn, zs[t]) : 0.f;
+        // d_alpha = d_num . z_u per head: reduce over the LH lanes of the head
+        for (int o = 1; o < LH; o <<= 1) part += __shfl_xor_sync(tmask, part, o, RL);
+        if (oks[t]) {
+          const float de = als[t] * (part - c);
+          const float dp = de * (prs[t] > 0.f ? 1.f : a.slope);
+          if (head_lead && colok) a.d_pre[xs[t] * H + hl] = dp;
+          dt += dp;
+        }
       }
     }
 #pragma unroll
@@ -1701,13 +1748,20 @@ struct WdArgs {
 };
 
 constexpr int WD_D = 64;
-constexpr int WD_RPW = 2;            // destination rows per warp per tile
-constexpr int WD_TM = 8 * WD_RPW;    // rows per tile
+// destination rows per warp per tile: 2 (16-row tiles, 3 CTAs / SM) by default,
+// SG_WD_RPW=4 (32-row tiles, 2 CTAs / SM)
+static int wd_rpw() {
+  static const int r = [] {
+    const char* e = std::getenv("SG_WD_RPW");
+    return (e && std::atoi(e) == 4) ? 4 : 2;
+  }();
+  return r;
+}
 
-template <int H>
-__global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restrict__ meta, WdArgs a) {
+template <int H, int RPW>
+__global__ void __launch_bounds__(256, RPW >= 4 ? 2 : 3) k_gat_wgrad_dst(const SgMeta* __restrict__ meta, WdArgs a) {
   SG_PDL_ENTRY();
-  constexpr int D = WD_D, DH = D / H, TM = WD_TM, RPW = WD_RPW;
+  constexpr int D = WD_D, DH = D / H, TM = 8 * RPW;
   extern __shared__ __align__(16) float sm[];
   const int w = a.w, d = a.d;
   const int HW = H * w;
@@ -2299,7 +2353,8 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
 // {1, 2, 4}, w % 4 == 0 and w <= 128; partial holds nblocks slices of
 // w*64 + 128 floats ([dW | da_src | da_dst], the k_gat_bwd_param layout).
 extern "C" int32_t sg_gat_wgrad_dst_blocks(int64_t rows) {
-  return (int32_t)std::max<int64_t>(1, std::min<int64_t>((rows + WD_TM - 1) / WD_TM, 3 * kSMs));  // 3 CTAs / SM
+  const int tm = 8 * wd_rpw();
+  return (int32_t)std::max<int64_t>(1, std::min<int64_t>((rows + tm - 1) / tm, (wd_rpw() >= 4 ? 2 : 3) * kSMs));
 }
 
 extern "C" int sg_gat_wgrad_dst(const void* split_ws, const SgSplitLayout* lay, int32_t d, int32_t w, int32_t heads,
@@ -2323,17 +2378,22 @@ extern "C" int sg_gat_wgrad_dst(const void* split_ws, const SgSplitLayout* lay, 
   a.src_row = src_row; a.h0 = h0; a.alpha = alpha; a.d_pre = d_pre; a.dnc = dnc; a.dnc_recv = dnc_recv;
   a.dt_loc = dt_loc; a.dt_recv = dt_recv; a.W = W; a.a_src = a_src; a.a_dst = a_dst; a.partial = partial;
   const int HW = heads * w;
-  const size_t smem = sizeof(float) * ((size_t)w * WD_D + 2 * HW + (size_t)WD_TM * (HW + w + WD_D + heads));
+  const size_t smem = sizeof(float) * ((size_t)w * WD_D + 2 * HW + (size_t)(8 * wd_rpw()) * (HW + w + WD_D + heads));
   SG_REQUIRE(smem <= 227 * 1024, "gat_wgrad_dst: shared memory");
   cudaStream_t st = (cudaStream_t)stream;
-switch (heads) {
-    case 1: { const cudaError_t e1 = allow_max_smem<k_gat_wgrad_dst<1>>(); SG_CUDA(e1);
-              ::sg::launch(k_gat_wgrad_dst<1>, nblocks, 256, smem, st, meta, a); break; }
-    case 2: { const cudaError_t e2 = allow_max_smem<k_gat_wgrad_dst<2>>(); SG_CUDA(e2);
-              ::sg::launch(k_gat_wgrad_dst<2>, nblocks, 256, smem, st, meta, a); break; }
-    default: { const cudaError_t e4 = allow_max_smem<k_gat_wgrad_dst<4>>(); SG_CUDA(e4);
-               ::sg::launch(k_gat_wgrad_dst<4>, nblocks, 256, smem, st, meta, a); break; }
+#define WD_GO(HH, RR)                                                                   \
+  do {                                                                                  \
+    const cudaError_t e_ = allow_max_smem<k_gat_wgrad_dst<HH, RR>>();                   \
+    SG_CUDA(e_);                                                                        \
+    ::sg::launch(k_gat_wgrad_dst<HH, RR>, nblocks, 256, smem, st, meta, a);             \
+  } while (0)
+  const bool r4 = wd_rpw() == 4;
+  switch (heads) {
+    case 1: if (r4) WD_GO(1, 4); else WD_GO(1, 2); break;
+    case 2: if (r4) WD_GO(2, 4); else WD_GO(2, 2); break;
+    default: if (r4) WD_GO(4, 4); else WD_GO(4, 2); break;
   }
+#undef WD_GO
   SG_CHECK_LAUNCH("k_gat_wgrad_dst");
   return SG_OK;
 }
