@@ -1748,20 +1748,13 @@ struct WdArgs {
 };
 
 constexpr int WD_D = 64;
-// destination rows per warp per tile: 2 (16-row tiles, 3 CTAs / SM) by default,
-// SG_WD_RPW=4 (32-row tiles, 2 CTAs / SM)
-static int wd_rpw() {
-  static const int r = [] {
-    const char* e = std::getenv("SG_WD_RPW");
-    return (e && std::atoi(e) == 4) ? 4 : 2;
-  }();
-  return r;
-}
+constexpr int WD_RPW = 2;          // destination rows per warp per tile (measured: 4 -> 0.479 vs 0.456 ms C3)
+constexpr int WD_TM = 8 * WD_RPW;  // rows per tile: 16 (65 KB shared, 3 CTAs / SM)
 
-template <int H, int RPW>
-__global__ void __launch_bounds__(256, RPW >= 4 ? 2 : 3) k_gat_wgrad_dst(const SgMeta* __restrict__ meta, WdArgs a) {
+template <int H>
+__global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restrict__ meta, WdArgs a) {
   SG_PDL_ENTRY();
-  constexpr int D = WD_D, DH = D / H, TM = 8 * RPW;
+  constexpr int D = WD_D, DH = D / H, TM = WD_TM, RPW = WD_RPW;
   extern __shared__ __align__(16) float sm[];
   const int w = a.w, d = a.d;
   const int HW = H * w;
@@ -2353,8 +2346,7 @@ extern "C" int sg_gat_bwd_param(const void* split_ws, const SgSplitLayout* lay, 
 // {1, 2, 4}, w % 4 == 0 and w <= 128; partial holds nblocks slices of
 // w*64 + 128 floats ([dW | da_src | da_dst], the k_gat_bwd_param layout).
 extern "C" int32_t sg_gat_wgrad_dst_blocks(int64_t rows) {
-  const int tm = 8 * wd_rpw();
-  return (int32_t)std::max<int64_t>(1, std::min<int64_t>((rows + tm - 1) / tm, (wd_rpw() >= 4 ? 2 : 3) * kSMs));
+  return (int32_t)std::max<int64_t>(1, std::min<int64_t>((rows + WD_TM - 1) / WD_TM, 3 * kSMs));  // 3 CTAs / SM
 }
 
 extern "C" int sg_gat_wgrad_dst(const void* split_ws, const SgSplitLayout* lay, int32_t d, int32_t w, int32_t heads,
@@ -2378,22 +2370,17 @@ extern "C" int sg_gat_wgrad_dst(const void* split_ws, const SgSplitLayout* lay, 
   a.src_row = src_row; a.h0 = h0; a.alpha = alpha; a.d_pre = d_pre; a.dnc = dnc; a.dnc_recv = dnc_recv;
   a.dt_loc = dt_loc; a.dt_recv = dt_recv; a.W = W; a.a_src = a_src; a.a_dst = a_dst; a.partial = partial;
   const int HW = heads * w;
-  const size_t smem = sizeof(float) * ((size_t)w * WD_D + 2 * HW + (size_t)(8 * wd_rpw()) * (HW + w + WD_D + heads));
+  const size_t smem = sizeof(float) * ((size_t)w * WD_D + 2 * HW + (size_t)WD_TM * (HW + w + WD_D + heads));
   SG_REQUIRE(smem <= 227 * 1024, "gat_wgrad_dst: shared memory");
   cudaStream_t st = (cudaStream_t)stream;
-#define WD_GO(HH, RR)                                                                   \
-  do {                                                                                  \
-    const cudaError_t e_ = allow_max_smem<k_gat_wgrad_dst<HH, RR>>();                   \
-    SG_CUDA(e_);                                                                        \
-    ::sg::launch(k_gat_wgrad_dst<HH, RR>, nblocks, 256, smem, st, meta, a);             \
-  } while (0)
-  const bool r4 = wd_rpw() == 4;
-  switch (heads) {
-    case 1: if (r4) WD_GO(1, 4); else WD_GO(1, 2); break;
-    case 2: if (r4) WD_GO(2, 4); else WD_GO(2, 2); break;
-    default: if (r4) WD_GO(4, 4); else WD_GO(4, 2); break;
+switch (heads) {
+    case 1: { const cudaError_t e1 = allow_max_smem<k_gat_wgrad_dst<1>>(); SG_CUDA(e1);
+              ::sg::launch(k_gat_wgrad_dst<1>, nblocks, 256, smem, st, meta, a); break; }
+    case 2: { const cudaError_t e2 = allow_max_smem<k_gat_wgrad_dst<2>>(); SG_CUDA(e2);
+              ::sg::launch(k_gat_wgrad_dst<2>, nblocks, 256, smem, st, meta, a); break; }
+    default: { const cudaError_t e4 = allow_max_smem<k_gat_wgrad_dst<4>>(); SG_CUDA(e4);
+               ::sg::launch(k_gat_wgrad_dst<4>, nblocks, 256, smem, st, meta, a); break; }
   }
-#undef WD_GO
   SG_CHECK_LAUNCH("k_gat_wgrad_dst");
   return SG_OK;
 }
