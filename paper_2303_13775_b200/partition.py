@@ -388,7 +388,9 @@ def partition_graph(graph, g, balance_eps=0.05, seed=0, max_passes=10) -> Partit
     coarsest level by greedy region growing + sequential refinement (best of 4
     restarts, csrc/host.cpp), then project back level by level with boundary
     refinement: sequential on the host for levels of <= HOST_REFINE_MAX
-    vertices, then parallel GPU rounds (sg_partition_round).
+    vertices, then parallel GPU rounds (sg_partition_round). The contiguous-id
+    map, refined the same way on the input graph, is kept instead when its cut
+    is lower.
     Deterministic given `seed`; not the reference's exact assignment (its
     matching and refinement visit vertices sequentially), same contract:
     balanced within eps, comparable cut (tests/test_gpu_partition.py pins the
@@ -428,6 +430,16 @@ def partition_graph(graph, g, balance_eps=0.05, seed=0, max_passes=10) -> Partit
         part = _refine(levels[lvl], part, g, cap, seed + lvl + 1, max_passes)
         if trace:
             print(f"[partition] level {lvl} (n {levels[lvl].n}): cut {levels[lvl].cut(part)}")
+    # one more candidate: the contiguous-id map refined on the input graph (ids
+    # often carry locality -- the benchmark generators plant their blocks by id
+    # range); the lower cut wins, ties to the multilevel result
+    base = levels[0]
+    alt = ((torch.arange(n, dtype=torch.int64, device=part.device) * g) // n).to(torch.int32)
+    alt = _refine(base, alt, g, cap, seed + 104729, max_passes)
+    if int(base.sizes(alt, g).max()) <= cap and base.cut(alt) < base.cut(part):
+        part = alt
+        if trace:
+            print(f"[partition] contiguous map refined: cut {base.cut(part)} (kept)")
     return PartitionMap(part.cpu().numpy().astype(np.int64), g, balance_eps)
 
 
