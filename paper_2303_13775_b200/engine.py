@@ -53,27 +53,11 @@ def _capturing(graph):
     gc.collect()
     gc.disable()
     try:
-        with torch.cuda.graph(graph, stream=_capture_stream(), capture_error_mode="thread_local"):
+        with torch.cuda.graph(graph, capture_error_mode="thread_local"):
             yield
     finally:
         if was:
             gc.enable()
-
-
-_CAP_STREAMS = {}
-
-
-def _capture_stream():
-    """Capture on a high-priority stream (SG_CAPTURE_PRIORITY=0: torch's default
-    capture stream): the step's critical-path kernels then win SM slots over the
-    side stream's CSR-by-source sort that overlaps the layer-1 forward."""
-    if os.environ.get("SG_CAPTURE_PRIORITY", "1") != "1":
-        return None
-    dev = torch.cuda.current_device()
-    s = _CAP_STREAMS.get(dev)
-    if s is None:
-        s = _CAP_STREAMS[dev] = torch.cuda.Stream(device=dev, priority=-100)  # clamped to the highest
-    return s
 
 
 def _nblocks(rows, tile=32):
