@@ -116,7 +116,7 @@ class SplitStep:
     def _ev(self, name):
         if self.events is None:
             return None
-        if self.ev_mode == "agg" and not name.startswith(("agg1", "roof1")):
+        if self.ev_mode == "agg" and not name.startswith(("agg1", "roof1", "wgd1")):
             return None
         try:  # external=True: a real event-record node when captured in a CUDA graph
             e = torch.cuda.Event(enable_timing=True, external=True)

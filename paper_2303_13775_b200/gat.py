@@ -192,6 +192,7 @@ def gat_backward(step):
             # one destination-centric pass: dW, da_src, da_dst (no d_z / ds / dt_tot)
             npart = w * dout + 2 * dout
             with step.phase(f"bwd_param{l}"):
+                step._ev("wgd1_start")
                 for d in step.devices:
                     nb = int(_lib.load().sg_gat_wgrad_dst_blocks(step.n_rows(l, d)))
                     part = _f32(nb * npart, device=step.dev)
@@ -201,6 +202,7 @@ def gat_backward(step):
                               _lib.ptr(W), _lib.ptr(a_s), _lib.ptr(a_d), _lib.ptr(part), nb, st)
                     step.jobs.append((part, nb, npart, step.grads[d], p.offset(f"layer{l-1}.w")))
                     step._partials.append(part)
+                step._ev("wgd1_end")
             d_h = None
             continue
         d_z = _f32(nVp, dout, device=step.dev)
