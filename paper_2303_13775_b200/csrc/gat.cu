@@ -1850,6 +1850,26 @@ __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restri
           }
         }
         // one edge: A += alpha h_u, B += dpre h_u
+        // alpha / d_pre of the row's first 32 edges, one edge per lane (coalesced),
+        // handed to every lane by shuffles as the edges are applied
+        const float4 al_l = lane < ec - bc ? ld_e(a.alpha, xc) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 dp_l = lane < ec - bc ? ld_e(a.d_pre, xc) : make_float4(0.f, 0.f, 0.f, 0.f);
+        auto edge_k = [&](const float4& v, int k) {  // edge k < 32 of the row (k warp-uniform)
+          float alh[4], dph[4];
+          alh[0] = __shfl_sync(0xffffffffu, al_l.x, k); dph[0] = __shfl_sync(0xffffffffu, dp_l.x, k);
+          if (H > 1) { alh[1] = __shfl_sync(0xffffffffu, al_l.y, k); dph[1] = __shfl_sync(0xffffffffu, dp_l.y, k); }
+          if (H > 2) {
+            alh[2] = __shfl_sync(0xffffffffu, al_l.z, k); dph[2] = __shfl_sync(0xffffffffu, dp_l.z, k);
+            alh[3] = __shfl_sync(0xffffffffu, al_l.w, k); dph[3] = __shfl_sync(0xffffffffu, dp_l.w, k);
+          }
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            A[h].x = fmaf(alh[h], v.x, A[h].x); A[h].y = fmaf(alh[h], v.y, A[h].y);
+            A[h].z = fmaf(alh[h], v.z, A[h].z); A[h].w = fmaf(alh[h], v.w, A[h].w);
+            B[h].x = fmaf(dph[h], v.x, B[h].x); B[h].y = fmaf(dph[h], v.y, B[h].y);
+            B[h].z = fmaf(dph[h], v.z, B[h].z); B[h].w = fmaf(dph[h], v.w, B[h].w);
+          }
+        };
         auto edge = [&](const float4& v, int64_t x) {
           const float4 al = ld_e(a.alpha, x), dp = ld_e(a.d_pre, x);
           const float alh[4] = {al.x, al.y, al.z, al.w}, dph[4] = {dp.x, dp.y, dp.z, dp.w};
@@ -1864,17 +1884,15 @@ __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restri
         const int cnt0 = min(32, ec - bc);
         for (int k0 = 0; k0 < cnt0; k0 += 4) {  // warp-uniform trip count
           float4 v[4];
-          int xs[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int k = min(k0 + t, 31);
-            xs[t] = __shfl_sync(0xffffffffu, xc, k);
             const int r = __shfl_sync(0xffffffffu, hc, k);
             v[t] = (k0 + t < cnt0) ? ld_h(r) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            if (k0 + t < cnt0) edge(v[t], xs[t]);
+            if (k0 + t < cnt0) edge_k(v[t], k0 + t);
         }
         // rows with more than 32 in-edges: the remaining edges, one at a time (rare)
         for (int j = bc + 32; j < ec; ++j) {
