@@ -785,22 +785,22 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
           a.md[G * 2 * H + H + hl] = ssum;
         }
       }
-      // k_gat_alpha over this row's edges (each edge group its own edges again)
+      // k_gat_alpha over this row's edges: each edge group re-reads the pre_e its
+      // head lead wrote in the first pass (one hop instead of lsrc -> s)
       if (head_lead && colok)
         for (int j0 = b + eg; j0 < e; j0 += 4 * EG) {
           int64_t xs[4];
-          float ss[4];
+          float pr[4];
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
             const int j = j0 + t * EG;
             xs[t] = j < e ? (a.dperm ? (int64_t)a.dperm[j] : a.eoff_li + j) : 0;
           }
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
-            ss[t] = j0 + t * EG < e ? a.s[(int64_t)(prev0 + a.lsrc[xs[t]]) * H + hl] : 0.f;
+          for (int t = 0; t < 4; ++t) pr[t] = j0 + t * EG < e ? a.pre_e[xs[t] * H + hl] : 0.f;
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            if (j0 + t * EG < e) a.alpha[xs[t] * H + hl] = expf(leaky(ss[t] + tq, a.slope) - m) / ssum;
+            if (j0 + t * EG < e) a.alpha[xs[t] * H + hl] = expf(leaky(pr[t], a.slope) - m) / ssum;
         }
       continue;
     }
