@@ -717,21 +717,11 @@ __global__ void __launch_bounds__(256) k_gat_agg(const SgMeta* __restrict__ meta
   const bool colok = col < dout;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  // each row's bounds are fetched one row ahead (software-pipelined rows)
-  int b_n = 0, e_n = 0;
-  if (gw * RPW + team < R) {
-    b_n = a.rowbeg[rb + gw * RPW + team];
-    e_n = a.rowend[rb + gw * RPW + team];
-  }
   for (int64_t q = gw * RPW + team; q < R; q += nw * RPW) {
     const bool own = q < n_own;
-    const int b = b_n, e = e_n;
-    if (q + nw * RPW < R) {
-      b_n = a.rowbeg[rb + q + nw * RPW];
-      e_n = a.rowend[rb + q + nw * RPW];
-    }
     const int slot = own ? 0 : a.sendpos[a.pbase_l + ref0 + (q - n_own)];
     const float tq = own ? a.t[(int64_t)(own0 + q) * H + hl] : a.t_recv[(int64_t)slot * H + hl];
+    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
     float m = -INFINITY, ssum = 0.f;
     T U = V::zero();
     // four edges' loads in flight per edge group, applied in edge order
@@ -1028,22 +1018,13 @@ __global__ void __launch_bounds__(256) k_gat_bwd_dst(const SgMeta* __restrict__ 
   const bool colok = col < dout;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int b_n = 0, e_n = 0;  // bounds fetched one row ahead
-  if (gw * RPW + team < R) {
-    b_n = a.rowbeg[rb + gw * RPW + team];
-    e_n = a.rowend[rb + gw * RPW + team];
-  }
   for (int64_t q = gw * RPW + team; q < R; q += nw * RPW) {
     const bool own = q < n_own;
-    const int b = b_n, e = e_n;
-    if (q + nw * RPW < R) {
-      b_n = a.rowbeg[rb + q + nw * RPW];
-      e_n = a.rowend[rb + q + nw * RPW];
-    }
     const int slot = own ? 0 : a.sendpos[a.pbase_l + ref0 + (q - n_own)];
     const float* dn_row = own ? a.dnc + (int64_t)(own0 + q) * (dout + H) : a.dnc_recv + (int64_t)slot * a.stride;
     const T dn = colok ? V::ld_any(dn_row + col) : V::zero();  // stride D+H: not 16B aligned
     const float c = dn_row[dout + hl];
+    const int b = a.rowbeg[rb + q], e = a.rowend[rb + q];
     float dt = 0.f;
     const int rounds = (e - b + EG - 1) / EG;
     // four rounds' loads in flight (the index chain and the z / alpha / pre_e
@@ -1812,34 +1793,19 @@ __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restri
   float4 B[H];
 #pragma unroll
   for (int h = 0; h < H; ++h) B[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-  // row bounds of a warp's RPW rows, and the first row's index chain, of the
-  // NEXT tile are fetched during this tile's shared-memory pass (one hop
-  // before it, one after it), not between the tile barrier and the loads
-  auto bounds = [&](int qq) {
-    int v = 0;
-    if (lane < 2 * RPW && qq + (lane >> 1) < R)
-      v = (lane & 1) ? a.rowend[rb + qq + (lane >> 1)] : a.rowbeg[rb + qq + (lane >> 1)];
-    return v;
-  };
-  auto first_hop = [&](int qq, int bb, int ee, int& x, int& u) {
-    x = 0;
-    u = 0;
-    if (qq < R && lane < ee - bb) {
-      x = (int)edge_x(bb + lane);
-      u = prev0 + a.lsrc[x];
-    }
-  };
-  int be_n = bounds(blockIdx.x * TM + wid * RPW);
-  int xn_n, un_n;
-  first_hop(blockIdx.x * TM + wid * RPW, __shfl_sync(0xffffffffu, be_n, 0), __shfl_sync(0xffffffffu, be_n, 1), xn_n,
-            un_n);
-  int hn_n = a.src_row ? a.src_row[un_n] : un_n;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int q0 = tile * TM + wid * RPW;
-    const int q0n = q0 + gridDim.x * TM;  // this warp's rows in its next tile
-    int be = be_n;
+    // row bounds of this warp's RPW rows; the first row's index chain
+    int be = 0;
+    if (lane < 2 * RPW && q0 + (lane >> 1) < R)
+      be = (lane & 1) ? a.rowend[rb + q0 + (lane >> 1)] : a.rowbeg[rb + q0 + (lane >> 1)];
     int b = __shfl_sync(0xffffffffu, be, 0), e = __shfl_sync(0xffffffffu, be, 1);
-    int xn = xn_n, hn = hn_n, un = un_n;
+    int xn = 0, hn = 0, un = 0;
+    if (q0 < R && lane < e - b) {
+      xn = (int)edge_x(b + lane);
+      un = prev0 + a.lsrc[xn];
+      hn = a.src_row ? a.src_row[un] : un;
+    }
     __syncthreads();  // the previous tile's pass is done with the tile buffers
     for (int i = 0; i < RPW; ++i) {
       const int q = q0 + i;
@@ -1951,7 +1917,6 @@ __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restri
       if (lane < H) dt_s[rr * H + lane] = dt_v;
     }
     __syncthreads();
-    be_n = bounds(q0n);  // next tile: hop 1
     // dW += A^T dn (4x4 blocks: c-group cg of w, j-group jg of D; head of jg)
     for (int s2 = tid; s2 < nslots; s2 += 256) {
       const int cg = s2 / (D / 4), jg = s2 - cg * (D / 4);
@@ -1980,7 +1945,6 @@ __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restri
         *reinterpret_cast<float4*>(dW_s + (4 * cg + i) * D + 4 * jg) =
             make_float4(acc[4 * i], acc[4 * i + 1], acc[4 * i + 2], acc[4 * i + 3]);
     }
-    first_hop(q0n, __shfl_sync(0xffffffffu, be_n, 0), __shfl_sync(0xffffffffu, be_n, 1), xn_n, un_n);  // hop 2
     // SC += dt-weighted column sums of h_self
     for (int idx = tid; idx < HW; idx += 256) {
       const int hh = idx / w, c = idx - hh * w;
@@ -1989,7 +1953,6 @@ __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restri
       for (int r = 0; r < TM; ++r) sc = fmaf(dt_s[r * H + hh], hs_s[r * w + c], sc);
       SC_s[idx] = sc;
     }
-    hn_n = a.src_row ? a.src_row[un_n] : un_n;  // next tile: hop 3
   }
   // SB = the warps' running B parts, summed in warp order (A_s is free now)
   __syncthreads();

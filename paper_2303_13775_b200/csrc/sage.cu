@@ -436,31 +436,15 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
     int r = prev0 + a.lsrc[a.eoff_li + j];
     return a.src_row ? a.src_row[r] : r;
   };
-  const bool comb = a.sums != nullptr;
-  // The first row's index chain (row bounds -> lsrc -> src_row) of a tile is
-  // fetched during the PREVIOUS tile: one hop before its GEMM, one after it,
-  // one after its output stores (cross-tile software pipelining; the three
-  // dependent hops used to stand between every tile's barrier and its loads).
-  auto bounds = [&](int qq) {  // lanes < 2 RPW: rowbeg / rowend of rows qq ..
-    int v = 0;
-    if (!comb && lane < 2 * RPW && qq + (lane >> 1) < n)
-      v = (lane & 1) ? a.rowend[rb + qq + (lane >> 1)] : a.rowbeg[rb + qq + (lane >> 1)];
-    return v;
-  };
-  int be_n = bounds(blockIdx.x * TM + wid * RPW);
-  int lsrc_n = 0;
-  {
-    const int b0 = __shfl_sync(0xffffffffu, be_n, 0), e0 = __shfl_sync(0xffffffffu, be_n, 1);
-    if (!comb && blockIdx.x * TM + wid * RPW < n && lane < e0 - b0) lsrc_n = prev0 + a.lsrc[a.eoff_li + b0 + lane];
-  }
-  int rnext_n = a.src_row ? a.src_row[lsrc_n] : lsrc_n;  // lanes without an edge read row 0 (unused)
   for (int r0 = blockIdx.x * TM; r0 < n; r0 += gridDim.x * TM) {
     // ---- aggregation: warp wid owns tile rows [wid*RPW, wid*RPW + RPW)
     const int q0 = r0 + wid * RPW;
-    int be = be_n;
+    const bool comb = a.sums != nullptr;
+    int be = 0;
+    if (!comb && lane < 2 * RPW && q0 + (lane >> 1) < n)
+      be = (lane & 1) ? a.rowend[rb + q0 + (lane >> 1)] : a.rowbeg[rb + q0 + (lane >> 1)];
     int b = __shfl_sync(0xffffffffu, be, 0), e = __shfl_sync(0xffffffffu, be, 1);
-    int rnext = (!comb && q0 < n && lane < e - b) ? rnext_n : 0;
-    const int q0n = q0 + gridDim.x * TM;  // this warp's first row of its next tile
+    int rnext = (!comb && q0 < n && lane < e - b) ? edge_row(b + lane) : 0;
     __syncthreads();  // previous tile's GEMM done with A_s
     for (int i = 0; i < RPW; ++i) {
       const int q = q0 + i;
@@ -547,7 +531,6 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
       }
       if (lane == 0) a.counts[G] = cntf;
     }
-    be_n = bounds(q0n);  // next tile: hop 1, in the shadow of this tile's GEMM
     __syncthreads();
     // ---- dense transform from smem (rows past n hold garbage: never stored)
     float acc2[4][4];
@@ -573,10 +556,6 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
         }
       }
     }
-    {  // next tile: hop 2 (its row bounds have landed during the GEMM)
-      const int bn = __shfl_sync(0xffffffffu, be_n, 0), en = __shfl_sync(0xffffffffu, be_n, 1);
-      lsrc_n = (!comb && q0n < n && lane < en - bn) ? prev0 + a.lsrc[a.eoff_li + bn + lane] : 0;
-    }
     __syncthreads();
     float* red = A_s;  // [NS][TM][dout]
 #pragma unroll
@@ -592,8 +571,6 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
       for (int s2 = 0; s2 < NS; ++s2) v += red[(s2 * TM + r) * dout + j];
       a.h[(int64_t)(own0 + r0 + r) * dout + j] = a.final_ ? v : sg_relu(v);
     }
-    // next tile: hop 3
-    rnext_n = (!comb && q0n < n) ? (a.src_row ? a.src_row[lsrc_n] : lsrc_n) : 0;
   }
 }
 
