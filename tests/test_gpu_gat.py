@@ -159,3 +159,30 @@ def test_gat_tcgen05_projection_shapes(F, H):
     assert_grads_close(grads[0], rgrads, TOL, "tc")
     for l in range(1, 3):
         assert rel_err(ex.states[0].h[l], rh[l][splits[0].owned_pos[l]]) < TOL, l
+
+
+@pytest.mark.parametrize("H,dh,g", [(1, 64, 1), (2, 32, 3), (4, 16, 2), (4, 16, 1)])
+def test_gat_wgrad_dst_matches_source_path(H, dh, g, monkeypatch):
+    """The destination-centric layer-1 weight gradient (sg_gat_wgrad_dst,
+    heads 1 / 2 / 4, with holders' dt combined at g > 1) against the
+    source-row path it replaces (k_gat_bwd_src + the weight-gradient kernel,
+    SG_GAT_WGRAD_DST=0): same loss, every gradient within fp32 roundoff."""
+    import paper_2303_13775_b200 as sg
+    from helpers import assert_grads_close
+    graph, pm, sample, cache = random_partition_case(400 + H * 10 + g, n=6000, m=70000, g=g, batch=128,
+                                                     fanouts=(7, 5), cache_frac=0.5)
+    F, C = 24, 5
+    feats = sg.synthetic_features(graph.num_vertices, F, seed=3)
+    labels = sg.synthetic_labels(graph.num_vertices, C, seed=4)
+    params = sg.init_params("gat", F, dh, C, 2, seed=5, heads=H)
+    out = {}
+    monkeypatch.setenv("SG_API_EAGER", "1")  # the flag is read per step, not per cached graph
+    for flag in ("1", "0"):
+        monkeypatch.setenv("SG_GAT_WGRAD_DST", flag)
+        splits, plan = sg.split_minibatch(sample, pm, cache)
+        ex = sg.SplitExecutor(params, splits, plan, feats, labels)
+        loss, grads = ex.run()
+        tot = {k: sum(np.asarray(gd[k], dtype=np.float64) for gd in grads) for k in grads[0]}
+        out[flag] = (loss, tot)
+    assert abs(out["1"][0] - out["0"][0]) <= 1e-6 * abs(out["0"][0])
+    assert_grads_close(out["1"][1], out["0"][1], 1e-5)
