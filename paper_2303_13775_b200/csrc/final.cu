@@ -53,7 +53,8 @@ struct FinalArgs {
 };
 
 __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ meta, FinalArgs a) {
-  SG_PDL_ENTRY();
+  // weights staged and accumulators zeroed before the PDL wait (nothing here
+  // is written by the preceding kernel; parameters change only at step end)
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, C = a.C, K = 2 * w, cp = C + 1;
   const int nwd = w * dout, nwc = dout * C;
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
   for (int i = tid; i < dout; i += 256) bs[i] = a.bias[i];
   for (int i = tid; i < ncls; i += 256) acc_c[i] = 0.f;
   for (int i = tid; i < nlay; i += 256) acc_l[i] = 0.f;
+  SG_PDL_ENTRY();
   const int l = a.L, d = a.d;
   const int n = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];

@@ -405,7 +405,8 @@ int launch_linear_q(const SgMeta* meta, const LinArgs& a, int64_t max_rows, cuda
 // operands); then the same register-tiled FP32 GEMM as k_sage_linear.
 template <int NQ, int UN, int RPW, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restrict__ meta, FusedArgs a) {
-  SG_PDL_ENTRY();
+  // the weight staging below runs before the PDL wait (parameters are not
+  // written by the preceding kernel; see k_sage_wgrad)
   constexpr int TM = 8 * RPW;  // rows per tile (RPW per warp)
   constexpr int NT = (TM / 4) * NQ;
   constexpr int NS = 256 / NT;
@@ -419,6 +420,7 @@ __global__ void __launch_bounds__(256, MINB) k_sage_layer(const SgMeta* __restri
     reinterpret_cast<float4*>(W_s)[i] = reinterpret_cast<const float4*>(a.ws)[i];
     reinterpret_cast<float4*>(W_s)[w * dout / 4 + i] = reinterpret_cast<const float4*>(a.wn)[i];
   }
+  SG_PDL_ENTRY();
   const int n = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];
   const int prev0 = meta->own_off[l - 1][d];
@@ -1007,7 +1009,9 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 
 template <int NQ>
 __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict__ meta, BwdArgs a) {
-  SG_PDL_ENTRY();
+  // prologue before the PDL wait: barrier init and the weight staging read
+  // nothing the preceding kernel writes (parameters change only in the step's
+  // last kernel, and a graph replay / eager step never overlaps the previous one)
   constexpr int TR = 32;
   extern __shared__ __align__(16) float smem[];
   const int w = a.w, dout = a.dout, K = 2 * w, wst = dout + 4;
@@ -1032,6 +1036,7 @@ __global__ void __launch_bounds__(256, 2) k_sage_wgrad(const SgMeta* __restrict_
       ws_s[c * wst + j] = a.ws[i];
       wn_s[c * wst + j] = a.wn[i];
     }
+  SG_PDL_ENTRY();
   const int n = meta->n_own[a.l][a.d];
   const int own0 = meta->own_off[a.l][a.d];
   const int ncg = K / 4, nslots = ncg * NQ, dq = dout / 4;
