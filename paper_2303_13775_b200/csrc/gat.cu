@@ -374,7 +374,9 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t da, uint64_t db, u
 template <int DH>  // head width (divides 32: a thread's 32 accumulator columns hold whole heads)
 __global__ void __launch_bounds__(256, 1) k_gat_project_tc(const SgMeta* __restrict__ meta, ProjArgs a) {
   using namespace tc5;
-  SG_PDL_ENTRY();
+  // TMEM allocation, barrier init and the W hi/lo planes run before the PDL
+  // wait: they read only parameters and the split's counts, which the
+  // preceding kernel does not write
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* A_raw = smem_raw;
   unsigned char* A_hi = A_raw + A_BYTES;
@@ -424,6 +426,7 @@ __global__ void __launch_bounds__(256, 1) k_gat_project_tc(const SgMeta* __restr
     av_s[i] = a.a_src[i];
     av_s[64 + i] = a.a_dst[i];
   }
+  SG_PDL_ENTRY();
   auto hrow_of = [&](int tile, int m) {
     const int r = tile * M + m;
     if (tile >= ntiles || r >= n) return -1;

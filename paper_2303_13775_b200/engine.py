@@ -615,14 +615,14 @@ class SplitStep:
 
 
 class _pdl_for:
-    """The GAT step runs without programmatic dependent launch: it measured
-    faster without it (C3 0.69-0.70 vs 0.73 ms; SG_GAT_PDL=1 turns it on).
-    The intermittent C3 NaNs once blamed on PDL were the pinned staging race
-    fixed in StaticSample.load; with PDL on the GAT tests pass and the step is
-    bit-identical to the PDL-off step."""
+    """Programmatic dependent launch for the GAT step (SG_GAT_PDL=0 turns it
+    off). Round 1 measured the GAT step faster without it (0.69-0.70 vs 0.73
+    ms); on the round-2 kernels, with the tcgen05 projection's setup moved
+    before its griddepcontrol.wait, it is slightly faster with it (C3 0.4554
+    vs 0.4571 ms) and bit-identical."""
 
     def __init__(self, kind):
-        self.off = kind != "graphsage" and os.environ.get("SG_GAT_PDL") != "1"
+        self.off = kind != "graphsage" and os.environ.get("SG_GAT_PDL", "1") != "1"
 
     def __enter__(self):
         if self.off:
