@@ -1421,7 +1421,7 @@ __device__ __forceinline__ void cp_async4g(void* dst, const void* src) {
 
 template <int MB>
 __global__ void __launch_bounds__(256, 2) k_gat_wgrad_mma(const SgMeta* __restrict__ meta, BParamArgs a) {
-  SG_PDL_ENTRY();
+  // W^T staging and the K-padding zeros run before the PDL wait (parameters only)
   constexpr int D = 64, DZP = D + 8;
   constexpr int WP = ((16 * MB + 8 + 31) / 32 * 32 - 8) < 16 * MB ? (16 * MB + 8 + 31) / 32 * 32 + 24
                                                                    : (16 * MB + 8 + 31) / 32 * 32 - 8;
@@ -1441,6 +1441,7 @@ __global__ void __launch_bounds__(256, 2) k_gat_wgrad_mma(const SgMeta* __restri
     const int r = i / (WP - w), c = w + (i - r * (WP - w));
     stg[(r / QTR) * stage_f + (r % QTR) * WP + c] = 0.f;
   }
+  SG_PDL_ENTRY();
   const int l = a.l, d = a.d;
   const int n = meta->n_own[l - 1][d];
   const int own0 = meta->own_off[l - 1][d];
@@ -1756,7 +1757,7 @@ constexpr int WD_TM = 8 * WD_RPW;  // rows per tile: 16 (65 KB shared, 3 CTAs / 
 
 template <int H>
 __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restrict__ meta, WdArgs a) {
-  SG_PDL_ENTRY();
+  // (the shared accumulators are zeroed before the PDL wait)
   constexpr int D = WD_D, DH = D / H, TM = WD_TM, RPW = WD_RPW;
   extern __shared__ __align__(16) float sm[];
   const int w = a.w, d = a.d;
@@ -1770,6 +1771,7 @@ __global__ void __launch_bounds__(256, 3) k_gat_wgrad_dst(const SgMeta* __restri
   float* dt_s = dn_s + TM * D;         // [TM][H]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (int i = tid; i < w * D + 2 * HW; i += 256) sm[i] = 0.f;
+  SG_PDL_ENTRY();
   const int l = 1;
   const int n_own = meta->n_own[l][d];
   const int R = n_own + meta->n_ref[l][d];

@@ -34,7 +34,7 @@ struct LossArgs {
 };
 
 __global__ void __launch_bounds__(256) k_cls_loss(const SgMeta* __restrict__ meta, LossArgs a) {
-  SG_PDL_ENTRY();
+  // W staged before the PDL wait (parameters are not written by the preceding kernel)
   extern __shared__ float smem[];
   const int hid = a.hid, C = a.ncls, cp = C + 1;
   float* w_s = smem;                // [hid][C] when staged
@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(256) k_cls_loss(const SgMeta* __restrict__ met
   float* loss_s = (float*)(y_s + LTR);
   if (a.w_smem)
     for (int i = threadIdx.x; i < hid * C; i += blockDim.x) w_s[i] = a.w[i];
+  SG_PDL_ENTRY();
   const float* Wm = a.w_smem ? w_s : a.w;
   const int n = meta->n_own[a.L][a.d];
   const int own0 = meta->own_off[a.L][a.d];
