@@ -85,7 +85,6 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
   for (int i = tid; i < dout; i += 256) bs[i] = a.bias[i];
   for (int i = tid; i < ncls; i += 256) acc_c[i] = 0.f;
   for (int i = tid; i < nlay; i += 256) acc_l[i] = 0.f;
-  SG_PDL_ENTRY();
   const int l = a.L, d = a.d;
   const int n = meta->n_own[l][d];
   const int own0 = meta->own_off[l][d];
@@ -97,7 +96,24 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
   const int EG = 32 / LPR;
   const int eg = lane / LPR, lr = lane - eg * LPR;
   const int ntiles = (n + FTR - 1) / FTR;
+  // also before the wait: the first tile's row bounds, this edge group's first
+  // source index and the row's label -- all from the split / sample, which the
+  // preceding kernel (the layer below, l >= 2) does not write. For l == 1 the
+  // predecessor may be the split itself: no prefetch.
+  const bool pre = l >= 2 && !a.sums;
+  int b_pre = 0, e_pre = 0, rr_pre = -1, y_pre = -1;
+  if (pre && blockIdx.x < ntiles) {
+    const int q = blockIdx.x * FTR + warp;
+    if (q < n) {
+      b_pre = a.rowbeg[rb + q];
+      e_pre = a.rowend[rb + q];
+      if (b_pre + eg < e_pre) rr_pre = prev0 + a.lsrc[a.eoff_li + b_pre + eg];
+      if (lane == 0) y_pre = a.labels[a.V[a.voff_l + a.grouped[a.voff_l + own0 + q]]];
+    }
+  }
+  SG_PDL_ENTRY();
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const bool first_tile = pre && tile == (int)blockIdx.x;
     const int r0 = tile * FTR;
     const int rows = min(FTR, n - r0);
     __syncthreads();  // previous tile done with the smem rows
@@ -106,7 +122,8 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
       const int r = warp;
       if (r < rows) {
         const int q = r0 + r;
-        const int b = a.sums ? 0 : a.rowbeg[rb + q], e = a.sums ? 0 : a.rowend[rb + q];
+        const int b = a.sums ? 0 : (first_tile ? b_pre : a.rowbeg[rb + q]);
+        const int e = a.sums ? 0 : (first_tile ? e_pre : a.rowend[rb + q]);
         const int64_t G = own0 + q;
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         const bool colok = lr < w4;
@@ -128,7 +145,7 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
           cntf = N;
         } else {
           for (int j = b + eg; j < e; j += EG) {
-            int rr = prev0 + a.lsrc[a.eoff_li + j];
+            int rr = (first_tile && j == b + eg) ? rr_pre : prev0 + a.lsrc[a.eoff_li + j];
             if (a.src_row) rr = a.src_row[rr];
             if (colok) {
               const float4 v = __ldg(reinterpret_cast<const float4*>(a.h_prev + (int64_t)rr * w + 4 * lr));
@@ -157,8 +174,12 @@ __global__ void __launch_bounds__(256) k_sage_final(const SgMeta* __restrict__ m
           }
         }
         if (lane == 0) {
-          const int p = a.grouped[a.voff_l + own0 + q];
-          ys[r] = a.labels[a.V[a.voff_l + p]];
+          if (first_tile) {
+            ys[r] = y_pre;
+          } else {
+            const int p = a.grouped[a.voff_l + own0 + q];
+            ys[r] = a.labels[a.V[a.voff_l + p]];
+          }
         }
       } else {
         for (int k = lane; k < K; k += 32) A_s[r * K + k] = 0.f;
