@@ -625,6 +625,15 @@ void* sg_pipe_create2(int64_t bytes, int64_t extra);
 int sg_pipe_stage_compact(void* h, int32_t slot, const void* host_prefix, int64_t prefix_bytes,
                           const void* host_starts, int64_t starts_bytes, int32_t L, const int64_t* edge_off,
                           int64_t o_ed, int64_t full_bytes, void* dev_dst, void* stream);
+/* Direct staging for one captured graph per slot: the H2D (and, with run
+ * starts, the ed rebuild) lands straight in the slot graph's input buffer on
+ * the copy stream, which waits for the previous graph on that slot
+ * (sg_pipe_release, recorded after queueing it); no device-to-device copy on
+ * the step's critical path. starts_bytes == 0: full layout in host_prefix. */
+int sg_pipe_stage_direct(void* h, int32_t slot, const void* host_prefix, int64_t prefix_bytes,
+                         const void* host_starts, int64_t starts_bytes, int32_t L, const int64_t* edge_off,
+                         int64_t o_ed, void* dev_dst, void* stream);
+int sg_pipe_release(void* h, int32_t slot, void* stream);
 void sg_pipe_destroy(void* h);
 int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,
                   void* stream);

@@ -100,12 +100,12 @@ struct ExpandGeo {
   int L;
 };
 
-__global__ void __launch_bounds__(256) k_pipe_expand(int32_t* __restrict__ stage, ExpandGeo geo) {
+__global__ void __launch_bounds__(256) k_pipe_expand(int32_t* __restrict__ stage, const int32_t* __restrict__ starts,
+                                                     ExpandGeo geo) {
   const int64_t* sizes = reinterpret_cast<const int64_t*>(stage);  // [nV (L+1) | nE (L)]
   int64_t off[SG_MAXL + 1];
   off[0] = 0;
   for (int l = 1; l <= geo.L; ++l) off[l] = off[l - 1] + sizes[l];
-  const int32_t* starts = stage + geo.starts_off;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < off[geo.L];
        x += (int64_t)gridDim.x * blockDim.x) {
     int l = 1;
@@ -145,13 +145,59 @@ extern "C" int sg_pipe_stage_compact(void* h, int32_t slot, const void* host_pre
   geo.o_ed = o_ed;
   geo.starts_off = p->bytes / 4;
   if (starts_bytes > 0) {
-    k_pipe_expand<<<clamp_grid(div_up(starts_bytes / 4, 256), kSMs), 256, 0, p->copy>>>((int32_t*)stage, geo);
+    k_pipe_expand<<<clamp_grid(div_up(starts_bytes / 4, 256), kSMs), 256, 0, p->copy>>>(
+        (int32_t*)stage, (const int32_t*)stage + geo.starts_off, geo);
     SG_CHECK_LAUNCH("k_pipe_expand");
   }
   SG_CUDA(cudaEventRecord(p->h2d[slot], p->copy));
   SG_CUDA(cudaStreamWaitEvent(st, p->h2d[slot], 0));
   SG_CUDA(cudaMemcpyAsync(dev_dst, stage, (size_t)full_bytes, cudaMemcpyDeviceToDevice, st));
   SG_CUDA(cudaEventRecord(p->used[slot], st));
+  return SG_OK;
+}
+
+// Direct staging (one captured graph per slot, each reading its own input
+// buffer): the H2D lands straight in the graph's input buffer `dev_dst` on the
+// copy stream -- no device-to-device copy on the step's critical path. The
+// copy into slot s waits for the graph that last read slot s (sg_pipe_release).
+// host_starts / starts_bytes: the compact form (run starts into the slot's
+// scratch, ed rebuilt into dev_dst by k_pipe_expand); starts_bytes == 0: the
+// full layout in host_prefix.
+extern "C" int sg_pipe_stage_direct(void* h, int32_t slot, const void* host_prefix, int64_t prefix_bytes,
+                                    const void* host_starts, int64_t starts_bytes, int32_t L,
+                                    const int64_t* edge_off, int64_t o_ed, void* dev_dst, void* stream) {
+  Pipe* p = (Pipe*)h;
+  SG_REQUIRE(p && (slot == 0 || slot == 1), "pipe_stage_direct: bad handle/slot");
+  SG_REQUIRE(prefix_bytes >= 0 && prefix_bytes <= p->bytes && starts_bytes >= 0 && starts_bytes <= p->extra,
+             "pipe_stage_direct: bytes exceed the staging slot");
+  SG_REQUIRE(host_prefix && dev_dst && (starts_bytes == 0 || (host_starts && edge_off && L >= 1 && L <= SG_MAXL)),
+             "pipe_stage_direct: null buffer / bad geometry");
+  cudaStream_t st = (cudaStream_t)stream;
+  SG_CUDA(cudaStreamWaitEvent(p->copy, p->used[slot], 0));
+  SG_CUDA(cudaMemcpyAsync(dev_dst, host_prefix, (size_t)prefix_bytes, cudaMemcpyHostToDevice, p->copy));
+  if (starts_bytes > 0) {
+    char* scratch = (char*)p->stage[slot] + p->bytes;
+    SG_CUDA(cudaMemcpyAsync(scratch, host_starts, (size_t)starts_bytes, cudaMemcpyHostToDevice, p->copy));
+    ExpandGeo geo;
+    memset(&geo, 0, sizeof(geo));
+    geo.L = L;
+    for (int l = 0; l < L; ++l) geo.eoff[l] = edge_off[l];
+    geo.o_ed = o_ed;
+    k_pipe_expand<<<clamp_grid(div_up(starts_bytes / 4, 256), kSMs), 256, 0, p->copy>>>(
+        (int32_t*)dev_dst, (const int32_t*)scratch, geo);
+    SG_CHECK_LAUNCH("k_pipe_expand");
+  }
+  SG_CUDA(cudaEventRecord(p->h2d[slot], p->copy));
+  SG_CUDA(cudaStreamWaitEvent(st, p->h2d[slot], 0));
+  return SG_OK;
+}
+
+// After the graph that reads slot `slot` is queued on `stream`: the slot's next
+// H2D may begin once that graph has run.
+extern "C" int sg_pipe_release(void* h, int32_t slot, void* stream) {
+  Pipe* p = (Pipe*)h;
+  SG_REQUIRE(p && (slot == 0 || slot == 1), "pipe_release: bad handle/slot");
+  SG_CUDA(cudaEventRecord(p->used[slot], (cudaStream_t)stream));
   return SG_OK;
 }
 

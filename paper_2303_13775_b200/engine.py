@@ -42,6 +42,12 @@ NB_PARTIAL = 2 * 148  # max blocks of the deterministic partial reductions (meas
 TSPMM_MIN_EDGES = int(os.environ.get("SG_TSPMM_MIN_EDGES", "65536"))  # load-balanced transposed SpMM from this many edges
 
 
+def _pipe_direct():
+    """run_pipelined with one captured graph per staging slot (SG_PIPE_DIRECT=0:
+    one graph and a device-to-device copy of each staged sample)."""
+    return os.environ.get("SG_PIPE_DIRECT", "1") == "1"
+
+
 @contextlib.contextmanager
 def _capturing(graph):
     """CUDA-graph capture that other threads' CUDA calls cannot invalidate
@@ -1443,7 +1449,31 @@ class CapturedStep:
         for ps in pinned:
             scratch[:ps.buf.numel()].copy_(ps.buf, non_blocking=True)
         torch.cuda.synchronize(self.dev)
+        if _pipe_direct() and self._twin_ok:
+            self._twin()  # captured here, outside any timed loop
         return pinned
+
+    _twin_ok = True  # RankCapturedStep: one graph (its exchange rounds share the transport's buffers)
+
+    def _twin(self):
+        """A second capture of the same step reading its own input buffer:
+        run_pipelined alternates the two graphs so that each sample's H2D lands
+        directly in the input of the graph that will read it (no device-to-
+        device copy between graphs). Capturing runs no kernels, so the
+        parameters are untouched; the step state of the first graph (ds, step,
+        the per-phase events) is restored afterwards."""
+        tw = getattr(self, "_tw", None)
+        if tw is None:
+            keep = (self.inp, self.graph, self.out, getattr(self, "ds", None), getattr(self, "step", None))
+            self.inp = StaticSample(keep[0].cap_nV, keep[0].cap_nE, self.dev)
+            self.inp.buf.copy_(keep[0].buf)
+            g1 = torch.cuda.CUDAGraph()
+            with _capturing(g1):
+                out1 = self._body()
+            torch.cuda.synchronize()
+            tw = self._tw = (self.inp, g1, out1)
+            self.inp, self.graph, self.out, self.ds, self.step = keep
+        return tw
 
     def run_pipelined(self, pinned):
         """Train on a sequence of PinnedSamples end to end: per step an async
@@ -1470,9 +1500,41 @@ class CapturedStep:
         pending = None
         pc = time.perf_counter
         t_stage = t_replay = t_wait = 0.0
+        direct = _pipe_direct() and self._twin_ok
+        if direct:
+            tw = self._twin()
+            inps, graphs, outs = (self.inp, tw[0]), (self.graph, tw[1]), (self.out, tw[2])
         for i, ps in enumerate(pinned):
             b = i & 1
             t0 = pc()
+            if direct:
+                base = ps.buf.data_ptr()
+                if ps.compact:
+                    _lib.check(lib.sg_pipe_stage_direct(h, b, base, ps.starts_off, base + ps.starts_off,
+                                                        ps.starts_bytes, self.inp.L, self._pipe_eoff.ctypes.data,
+                                                        self.inp.o_ed, _lib.ptr(inps[b].buf), st),
+                               "sg_pipe_stage_direct")
+                else:
+                    _lib.check(lib.sg_pipe_stage_direct(h, b, base, ps.h2d_bytes, None, 0, self.inp.L,
+                                                        self._pipe_eoff.ctypes.data, self.inp.o_ed,
+                                                        _lib.ptr(inps[b].buf), st), "sg_pipe_stage_direct")
+                t1 = pc()
+                graphs[b].replay()
+                t2 = pc()
+                _lib.check(lib.sg_pipe_release(h, b, st), "sg_pipe_release")
+                _lib.check(lib.sg_pipe_finish(h, b, outs[b].data_ptr() + 4 * self.p.n, st), "sg_pipe_finish")
+                h2d += ps.h2d_bytes
+                d2h += 4
+                t3 = pc()
+                if pending is not None:
+                    _lib.check(lib.sg_pipe_wait(h, pending[0], ctypes.byref(out)), "sg_pipe_wait")
+                    losses.append(out.value / pending[1])
+                t4 = pc()
+                t_stage += t3 - t2 + t1 - t0
+                t_replay += t2 - t1
+                t_wait += t4 - t3
+                pending = (b, ps.num_targets)
+                continue
             if ps.compact:
                 base = ps.buf.data_ptr()
                 _lib.check(lib.sg_pipe_stage_compact(h, b, base, ps.starts_off, base + ps.starts_off, ps.starts_bytes,
@@ -1703,6 +1765,8 @@ class RankCapturedStep(CapturedStep):
     CUDA graph: replicated split -> rank-local forward/backward whose exchange
     rounds run over the PeerTransport's mapped buffers -> peer all-reduce +
     SGD. Sizes are read on the device; nothing returns to the host."""
+
+    _twin_ok = False
 
     def __init__(self, dparams, pm, cache, feats, labels_dev, cap_nV, cap_nE, lr_scale, rank, transport,
                  device="cuda", record_events=False, lr=None):
