@@ -634,6 +634,7 @@ int sg_pipe_stage_direct(void* h, int32_t slot, const void* host_prefix, int64_t
                          const void* host_starts, int64_t starts_bytes, int32_t L, const int64_t* edge_off,
                          int64_t o_ed, void* dev_dst, void* stream);
 int sg_pipe_release(void* h, int32_t slot, void* stream);
+void* sg_pipe_copy_stream(void* h);
 void sg_pipe_destroy(void* h);
 int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,
                   void* stream);

@@ -72,6 +72,10 @@ extern "C" void* sg_pipe_create(int64_t bytes) { return sg_pipe_create2((bytes +
 
 extern "C" void sg_pipe_destroy(void* h) { pipe_free((Pipe*)h); }
 
+// The pipe's copy stream (host-to-device copies; with direct staging also the
+// next sample's split graph runs there).
+extern "C" void* sg_pipe_copy_stream(void* h) { return h ? (void*)((Pipe*)h)->copy : nullptr; }
+
 extern "C" int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,
                              void* stream) {
   Pipe* p = (Pipe*)h;

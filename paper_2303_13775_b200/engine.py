@@ -1390,10 +1390,16 @@ class CapturedStep:
                 except TypeError:
                     ev.append(torch.cuda.Event(enable_timing=True))
             ev[0].record()
-        ds = DeviceSplit(inp.V, inp.es, inp.ed, inp.cap_nV, inp.cap_nE, self.pm, self.cache, True,
-                         self.dev, sizes=inp.sizes)
+        ds = self._split(inp)
         if ev:
             ev[1].record()
+        return self._after_split(ds, ev)
+
+    def _split(self, inp):
+        return DeviceSplit(inp.V, inp.es, inp.ed, inp.cap_nV, inp.cap_nE, self.pm, self.cache, True, self.dev,
+                           sizes=inp.sizes)
+
+    def _after_split(self, ds, ev=()):
         step = SplitStep(self.p, ds, self.f, self.labels, exact=False, record_events=self.record_events)
         if ev:
             step.events["ph:split:s"] = [ev[0]]
@@ -1456,22 +1462,32 @@ class CapturedStep:
     _twin_ok = True  # RankCapturedStep: one graph (its exchange rounds share the transport's buffers)
 
     def _twin(self):
-        """A second capture of the same step reading its own input buffer:
-        run_pipelined alternates the two graphs so that each sample's H2D lands
-        directly in the input of the graph that will read it (no device-to-
-        device copy between graphs). Capturing runs no kernels, so the
-        parameters are untouched; the step state of the first graph (ds, step,
-        the per-phase events) is restored afterwards."""
+        """Two staging slots for run_pipelined, each with its own input buffer
+        and its step captured as TWO graphs: the split (which reads only the
+        sample) and the rest. Each sample's H2D lands directly in its slot's
+        input, and its split runs on the copy stream right after it, while the
+        previous step is still computing; the main stream then runs only the
+        rest (no device-to-device copy, and the split off the critical path).
+        Capturing runs no kernels, so the parameters are untouched; the state of
+        the single-graph capture (ds, step, the per-phase events) is restored
+        afterwards."""
         tw = getattr(self, "_tw", None)
         if tw is None:
             keep = (self.inp, self.graph, self.out, getattr(self, "ds", None), getattr(self, "step", None))
-            self.inp = StaticSample(keep[0].cap_nV, keep[0].cap_nE, self.dev)
-            self.inp.buf.copy_(keep[0].buf)
-            g1 = torch.cuda.CUDAGraph()
-            with _capturing(g1):
-                out1 = self._body()
-            torch.cuda.synchronize()
-            tw = self._tw = (self.inp, g1, out1)
+            tw = []
+            for slot in range(2):
+                inp = keep[0] if slot == 0 else StaticSample(keep[0].cap_nV, keep[0].cap_nE, self.dev)
+                if slot:
+                    inp.buf.copy_(keep[0].buf)
+                self.inp = inp
+                gs, gm = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                with _capturing(gs):
+                    ds = self._split(inp)
+                with _capturing(gm):
+                    out = self._after_split(ds)
+                torch.cuda.synchronize()
+                tw.append((inp, gs, gm, out, ds))
+            self._tw = tw
             self.inp, self.graph, self.out, self.ds, self.step = keep
         return tw
 
@@ -1503,26 +1519,33 @@ class CapturedStep:
         direct = _pipe_direct() and self._twin_ok
         if direct:
             tw = self._twin()
-            inps, graphs, outs = (self.inp, tw[0]), (self.graph, tw[1]), (self.out, tw[2])
+            copy_st = torch.cuda.ExternalStream(lib.sg_pipe_copy_stream(h), device=self.dev)
+            split_done = [torch.cuda.Event(), torch.cuda.Event()]
+            main_st = torch.cuda.current_stream()
         for i, ps in enumerate(pinned):
             b = i & 1
             t0 = pc()
             if direct:
+                inp_b, gsplit, gmain, out_b, _ = tw[b]
                 base = ps.buf.data_ptr()
                 if ps.compact:
                     _lib.check(lib.sg_pipe_stage_direct(h, b, base, ps.starts_off, base + ps.starts_off,
                                                         ps.starts_bytes, self.inp.L, self._pipe_eoff.ctypes.data,
-                                                        self.inp.o_ed, _lib.ptr(inps[b].buf), st),
+                                                        self.inp.o_ed, _lib.ptr(inp_b.buf), st),
                                "sg_pipe_stage_direct")
                 else:
                     _lib.check(lib.sg_pipe_stage_direct(h, b, base, ps.h2d_bytes, None, 0, self.inp.L,
                                                         self._pipe_eoff.ctypes.data, self.inp.o_ed,
-                                                        _lib.ptr(inps[b].buf), st), "sg_pipe_stage_direct")
+                                                        _lib.ptr(inp_b.buf), st), "sg_pipe_stage_direct")
+                with torch.cuda.stream(copy_st):  # the split, behind the sample's H2D on the copy stream
+                    gsplit.replay()
+                    split_done[b].record(copy_st)
+                main_st.wait_event(split_done[b])
                 t1 = pc()
-                graphs[b].replay()
+                gmain.replay()
                 t2 = pc()
                 _lib.check(lib.sg_pipe_release(h, b, st), "sg_pipe_release")
-                _lib.check(lib.sg_pipe_finish(h, b, outs[b].data_ptr() + 4 * self.p.n, st), "sg_pipe_finish")
+                _lib.check(lib.sg_pipe_finish(h, b, out_b.data_ptr() + 4 * self.p.n, st), "sg_pipe_finish")
                 h2d += ps.h2d_bytes
                 d2h += 4
                 t3 = pc()
