@@ -634,6 +634,14 @@ int sg_pipe_stage_direct(void* h, int32_t slot, const void* host_prefix, int64_t
                          const void* host_starts, int64_t starts_bytes, int32_t L, const int64_t* edge_off,
                          int64_t o_ed, void* dev_dst, void* stream);
 int sg_pipe_release(void* h, int32_t slot, void* stream);
+/* split_minibatch for a sample whose arrays the native sampler wrote into one
+ * pinned buffer [int64 header of the 2L+1 sizes | V^0..V^L | E^l sources |
+ * E^l destinations] (scheduler.py:164 entry; replaces sg_pack_sample's host
+ * copy): after one H2D of that buffer to `src`, copy its nseg segments
+ * (word offsets src_off -> dst_off, len words) into the capacity layout
+ * `dst` on the device. nseg <= 3*SG_MAXL+2. */
+int sg_relayout_sample(const int32_t* src, int32_t* dst, int32_t nseg, const int64_t* src_off,
+                       const int64_t* dst_off, const int64_t* len, void* stream);
 void* sg_pipe_copy_stream(void* h);
 void sg_pipe_destroy(void* h);
 int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,

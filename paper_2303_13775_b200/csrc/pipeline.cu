@@ -8,6 +8,7 @@
 //   copy stream : wait used[s] -> H2D host -> stage[s] -> record h2d[s]
 //   main stream : wait h2d[s] -> D2D stage[s] -> graph inputs -> record used[s]
 //                 -> graph replay -> D2H loss -> record done[s]
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -219,6 +220,48 @@ extern "C" int sg_pipe_wait(void* h, int32_t slot, float* loss_out) {
   SG_REQUIRE(p && (slot == 0 || slot == 1) && loss_out, "pipe_wait: bad handle/slot/pointer");
   SG_CUDA(cudaEventSynchronize(p->done[slot]));
   *loss_out = p->loss_h[slot];
+  return SG_OK;
+}
+
+// split_minibatch's direct path (a sampler-pinned sample, no host pack): the
+// sample's contiguous [header | V | es | ed] arrived with one H2D; its 3L+2
+// segments are moved to their word offsets in the capacity layout (one kernel,
+// blockIdx.y = segment).
+namespace {
+constexpr int kMaxSeg = 3 * SG_MAXL + 2;
+struct Segs {
+  int32_t n;
+  int64_t src[kMaxSeg], dst[kMaxSeg], len[kMaxSeg];
+};
+__global__ void k_relayout(const int32_t* __restrict__ src, int32_t* __restrict__ dst, Segs s) {
+  const int seg = blockIdx.y;
+  const int64_t len = s.len[seg];
+  const int32_t* a = src + s.src[seg];
+  int32_t* b = dst + s.dst[seg];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+}  // namespace
+
+extern "C" int sg_relayout_sample(const int32_t* src, int32_t* dst, int32_t nseg, const int64_t* src_off,
+                                  const int64_t* dst_off, const int64_t* len, void* stream) {
+  SG_REQUIRE(src && dst && src_off && dst_off && len && nseg >= 0 && nseg <= kMaxSeg,
+             "relayout_sample: bad argument");
+  Segs s;
+  memset(&s, 0, sizeof(s));
+  s.n = nseg;
+  int64_t mx = 0;
+  for (int i = 0; i < nseg; ++i) {
+    SG_REQUIRE(src_off[i] >= 0 && dst_off[i] >= 0 && len[i] >= 0, "relayout_sample: negative offset/length");
+    s.src[i] = src_off[i];
+    s.dst[i] = dst_off[i];
+    s.len[i] = len[i];
+    mx = std::max(mx, len[i]);
+  }
+  if (nseg == 0 || mx == 0) return SG_OK;
+  dim3 grid(clamp_grid(div_up(mx, 4 * 256), kSMs), nseg);
+  k_relayout<<<grid, 256, 0, (cudaStream_t)stream>>>(src, dst, s);
+  SG_CHECK_LAUNCH("k_relayout");
   return SG_OK;
 }
 

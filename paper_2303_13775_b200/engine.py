@@ -696,17 +696,19 @@ class GradDict(dict):
     allreduce_and_step never pays the D2H)."""
 
     device_flat = None
+    host_flat = None
     dparams = None
 
-    def __init__(self, data=None, dparams=None, device_flat=None):
+    def __init__(self, data=None, dparams=None, device_flat=None, host_flat=None):
         super().__init__(data or {})
-        self.dparams, self.device_flat = dparams, device_flat
-        self._lazy = data is None and device_flat is not None
+        self.dparams, self.device_flat, self.host_flat = dparams, device_flat, host_flat
+        self._lazy = data is None and (device_flat is not None or host_flat is not None)
 
     def _fill(self):
         if self._lazy:
             self._lazy = False
-            dict.update(self, self.dparams.grads_to_dict(self.device_flat))
+            src = torch.from_numpy(self.host_flat) if self.host_flat is not None else self.device_flat
+            dict.update(self, self.dparams.grads_to_dict(src))
 
     for _m in ("__getitem__", "__iter__", "__len__", "__contains__", "__repr__", "__eq__", "keys", "values",
                "items", "get", "copy"):
@@ -743,11 +745,11 @@ class _PinnedFlat:
         self.ev.record()
 
 
-def _pinned_of(dp, which):
+def _pinned_of(dp, which, shape=None):
     key = "_pin_" + which
     pf = getattr(dp, key, None)
     if pf is None:
-        pf = _PinnedFlat(dp.n)
+        pf = _PinnedFlat(dp.n if shape is None else shape)
         setattr(dp, key, pf)
     return pf
 
@@ -837,7 +839,7 @@ class SplitExecutor:
         self._meter()
         loss = float(self.step.loss_sum_dev().item())
         out = [GradDict(dparams=self.dparams, device_flat=self.step.grads[d]) for d in range(self.g)]
-        self._loss_slots = [f[self.dparams.n] for f in (gd.device_flat for gd in out)]
+        self._loss_slots = [float(gd.device_flat[self.dparams.n].item()) for gd in out]
         return loss, out
 
     def _run_graph(self):
@@ -852,16 +854,28 @@ class SplitExecutor:
         gs.load_packed(self.ds.packed)
         gs.replay()
         n = gs.p.n
-        flats = [o.clone() for o in gs.out]  # the graph's buffers are reused by the next replay
+        # every device's flat gradient (+ loss slot) comes back in one pinned
+        # D2H: the loss needs a host sync anyway, and allreduce_and_step then
+        # applies the device-order sum + SGD to the host parameters directly
+        g = len(gs.out)
+        dn = _pinned_of(gs.p, f"grads{g}", (g, n + 1))
+        dn.wait()
+        for d, f in enumerate(gs.out):
+            dn.t[d].copy_(f[:n + 1], non_blocking=True)
+        dn.record()
+        dn.wait()
+        hg = dn.np.copy()  # the graph's buffers (and this slot) are reused by the next run
         self._meter()
         out = []
-        for f in flats:
-            gd = GradDict(dparams=gs.p, device_flat=f)
+        for d in range(g):
+            gd = GradDict(dparams=gs.p, host_flat=hg[d])
             gd.param_snapshot = host
             out.append(gd)
-        self._loss_slots = [f[n] for f in flats]
-        loss = float((flats[0][n] if len(flats) == 1 else torch.stack(self._loss_slots).sum()).item())
-        return loss, out
+        self._loss_slots = [float(hg[d, n]) for d in range(g)]
+        loss = hg[0, n]
+        for d in range(1, g):
+            loss = np.float32(loss + hg[d, n])
+        return float(loss), out
 
     @property
     def states(self):
@@ -884,7 +898,7 @@ class SplitExecutor:
             self._states = _materialise_states(self)
             slots = getattr(self, "_loss_slots", None)
             for d, st in enumerate(self._states):
-                st.loss_sum = float(slots[d].item()) if slots is not None else 0.0
+                st.loss_sum = float(slots[d]) if slots is not None else 0.0
         return self._states
 
 
@@ -1004,6 +1018,11 @@ def allreduce_and_step(params, per_device_grads, lr, num_targets):
         host_params = params if isinstance(params, ModelParams) else ModelParams.from_reference(params)
         dp = None
         snap = getattr(per_device_grads[0], "param_snapshot", None) if per_device_grads else None
+        hfl = [getattr(gd, "host_flat", None) for gd in per_device_grads]
+        if snap is not None and hfl and all(h is not None for h in hfl):
+            cur = _host_flat(host_params)
+            if np.array_equal(cur, snap):
+                return _host_sum_sgd(params, host_params, per_device_grads, hfl, cur, lr, num_targets)
         cand = getattr(per_device_grads[0], "dparams", None) if per_device_grads else None
         if snap is not None and cand is not None and all(getattr(gd, "dparams", None) is cand
                                                          for gd in per_device_grads):
@@ -1035,6 +1054,27 @@ def allreduce_and_step(params, per_device_grads, lr, num_targets):
         if params is not host_params:  # reference object: write back in place
             _write_back_reference(params, new)
     return summed
+
+
+def _host_sum_sgd(params, host_params, per_device_grads, hfl, cur, lr, num_targets):
+    """allreduce_and_step for gradients a captured SplitExecutor run already
+    brought to the host (with the loss, in one D2H): the device-order fp32 sum
+    and p -= lr/num_targets * g of sg_sum_sgd (a fused multiply-add: the exact
+    product of two fp32 values is formed in float64, then rounded once more),
+    on the host parameters that the run used."""
+    dp = per_device_grads[0].dparams
+    n = dp.n
+    total = np.array(hfl[0][:n], dtype=np.float32)
+    for h in hfl[1:]:
+        total += h[:n]
+    scale = np.float64(np.float32(float(lr) / float(num_targets)))
+    newf = (cur.astype(np.float64) - scale * total.astype(np.float64)).astype(np.float32)
+    new = {k: newf[dp.offsets[i]:dp.offsets[i + 1]].reshape(dp.shapes[i]) for i, k in enumerate(dp.names)}
+    for k, v in host_params.tensors().items():
+        v[...] = new[k]
+    if params is not host_params:  # reference object: write back in place
+        _write_back_reference(params, new)
+    return GradDict(dparams=dp, host_flat=total)
 
 
 def _write_back_reference(params, new):

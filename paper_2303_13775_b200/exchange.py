@@ -11,6 +11,9 @@ message per peer), over NVLink/NVSwitch.
 
 from __future__ import annotations
 
+import atexit
+import weakref
+
 from paper_2303_13775_b200 import _lib
 
 
@@ -89,6 +92,18 @@ class NcclTransport:
                   [c * stride for c in send_rows], [c * stride for c in recv_rows])
 
 
+_LIVE = weakref.WeakSet()
+
+
+@atexit.register
+def _close_live_transports():
+    for tp in list(_LIVE):
+        try:
+            tp.close()
+        except Exception:
+            pass
+
+
 class PeerTransport:
     """One rank per GPU, exchanges over peer memory (csrc/peer.cu): every
     round's buffer of every rank is mapped into its peers with CUDA IPC
@@ -124,6 +139,20 @@ class PeerTransport:
         self._nbuf = 0
         self._nx = 0
         self._grad = None
+        _LIVE.add(self)
+
+    def close(self):
+        """Synchronise and unmap the peers' buffers while CUDA is still up (also
+        run at interpreter exit, before torch's own teardown: dropping IPC
+        mappings during that teardown could crash the process on exit)."""
+        import torch
+        if self._keep:
+            torch.cuda.synchronize(self.dev)
+        self._bufs.clear()
+        self._grad = None
+        self._keep.clear()
+        self.peer_flags = None
+        _LIVE.discard(self)
 
     # -- CUDA IPC mapping -----------------------------------------------------
     def _share(self, t):

@@ -23,6 +23,7 @@ class MiniBatchSample:
     layer_vertices: list
     layer_edges: list
     dst_grouped: bool | None = field(default=None, compare=False)
+    pinned: object = field(default=None, compare=False, repr=False)
 
     @property
     def targets(self):
@@ -101,6 +102,64 @@ class MiniBatchSample:
             assert np.isin(diag, key).all(), "missing self-edge"
 
 
+@dataclass
+class PinnedArrays:
+    """A native-sampler sample's arrays as one page-locked int32 buffer
+    [int64 header of the sizes (S words) | V^0..V^L (VS) | E^l sources (ES) |
+    E^l destinations (ES)]; the sample's arrays are views of it. vbound: every
+    vertex id is < vbound (the sampled graph's vertex count)."""
+
+    tensor: object
+    base: int
+    S: int
+    VS: int
+    ES: int
+    vbound: int
+
+    def intact(self, sample) -> bool:
+        """The sample's arrays are still the views into this buffer (a caller
+        that replaced one gets the packing path instead)."""
+        off = self.base + 4 * self.S
+        for v in sample.layer_vertices:
+            if not (isinstance(v, np.ndarray) and v.dtype == np.int32 and v.ctypes.data == off):
+                return False
+            off += 4 * len(v)
+        if off != self.base + 4 * (self.S + self.VS):
+            return False
+        for k in (0, 1):
+            for e in sample.layer_edges:
+                a = e[k]
+                if not (isinstance(a, np.ndarray) and a.dtype == np.int32 and a.ctypes.data == off):
+                    return False
+                off += 4 * len(a)
+        return off == self.base + 4 * (self.S + self.VS + 2 * self.ES)
+
+
+_CUDA = None
+
+
+def _cuda_present():
+    global _CUDA
+    if _CUDA is None:
+        import os
+        try:
+            import torch
+            _CUDA = bool(torch.cuda.is_available()) and os.environ.get("SG_SAMPLE_PINNED", "1") != "0"
+        except Exception:
+            _CUDA = False
+    return _CUDA
+
+
+def _pinned_int32(n):
+    """Page-locked int32 host tensor from torch's caching host allocator (a
+    freed sample's buffer is reused; an async copy from it is tracked)."""
+    import torch
+    try:
+        return torch.empty(max(int(n), 1), dtype=torch.int32, pin_memory=True)
+    except RuntimeError:
+        return None
+
+
 def as_sample(obj) -> MiniBatchSample:
     """Accept a reference splitgnn MiniBatchSample (duck-typed) or ours."""
     if isinstance(obj, MiniBatchSample):
@@ -111,9 +170,13 @@ def as_sample(obj) -> MiniBatchSample:
 class NativeSampler:
     """Reusable native sampler bound to one graph (keeps O(n) scratch)."""
 
-    def __init__(self, graph, threads=0):
+    def __init__(self, graph, threads=0, pinned=None):
+        """pinned: write samples into page-locked host memory (default: when
+        a GPU is present, SG_SAMPLE_PINNED=0 disables) so that split_minibatch
+        DMAs them without a host copy."""
         self.graph = graph
         self.threads = int(threads)
+        self.pinned = _cuda_present() if pinned is None else bool(pinned)
         self._h = _lib.load().sg_sampler_create(int(graph.num_vertices),
                                                 _lib.ptr(graph.row_offsets),
                                                 _lib.ptr(graph.col_indices))
@@ -136,16 +199,27 @@ class NativeSampler:
         _lib.check(lib.sg_sampler_run(self._h, _lib.ptr(targets), len(targets), _lib.ptr(fan), L,
                                       int(seed) & (2**64 - 1), self.threads, _lib.ptr(nV),
                                       _lib.ptr(nE)), "sample_minibatch")
-        V = np.empty(int(nV.sum()), dtype=np.int32)
-        es = np.empty(int(nE[:L].sum()), dtype=np.int32)
-        ed = np.empty(int(nE[:L].sum()), dtype=np.int32)
+        VS, ES = int(nV.sum()), int(nE[:L].sum())
+        S = 2 * (2 * L + 1)  # int64 header of the sizes, as in the capacity layout
+        pin = _pinned_int32(S + VS + 2 * ES) if self.pinned else None
+        if pin is not None:
+            # one DMA-ready buffer [header | V | es | ed]: split_minibatch sends
+            # it to the device as is (no host pack)
+            buf = pin.numpy()
+            buf[:S].view(np.int64)[:] = np.r_[nV, nE[:L]]
+        else:
+            buf = np.empty(S + VS + 2 * ES, dtype=np.int32)
+        V, es, ed = buf[S:S + VS], buf[S + VS:S + VS + ES], buf[S + VS + ES:]
         _lib.check(lib.sg_sampler_fetch(self._h, _lib.ptr(V), _lib.ptr(es), _lib.ptr(ed)),
                    "sampler_fetch")
         vo = np.r_[0, np.cumsum(nV)]
         eo = np.r_[0, np.cumsum(nE[:L])]
         lv = [V[vo[l]:vo[l + 1]] for l in range(L + 1)]
         le = [(es[eo[l]:eo[l + 1]], ed[eo[l]:eo[l + 1]]) for l in range(L)]
-        return MiniBatchSample(L, lv, le, dst_grouped=True)
+        smp = MiniBatchSample(L, lv, le, dst_grouped=True)
+        if pin is not None:
+            smp.pinned = PinnedArrays(pin, buf.ctypes.data, S, VS, ES, int(self.graph.num_vertices))
+        return smp
 
 
 _SAMPLERS = {}

@@ -10,6 +10,7 @@ No part of this module computes a split on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -266,6 +267,34 @@ class PackGeometry:
         self.last_vrange = (int(vr[0]), int(vr[1]))
         return used
 
+    def relayout_from_pinned(self, sample, pin, buf):
+        """A native-sampler sample already in one pinned buffer (PinnedArrays):
+        one H2D of it (torch's copy, so the caching host allocator tracks the
+        buffer until the DMA ends) and one kernel moving its segments to this
+        layout's offsets in `buf` (sg_relayout_sample). Returns the words used."""
+        import torch
+        nV, nE = sample.sizes()
+        if any(a > b for a, b in zip(nV, self.cap_nV)) or any(a > b for a, b in zip(nE, self.cap_nE)):
+            raise ValueError("sample exceeds the captured capacities")
+        L = self.L
+        n = pin.S + pin.VS + 2 * pin.ES
+        stage = torch.empty(n, dtype=torch.int32, device=buf.device)
+        stage.copy_(pin.tensor[:n], non_blocking=True)
+        vo = np.r_[0, np.cumsum(nV)]
+        eo = np.r_[0, np.cumsum(nE)]
+        so = [0] + [pin.S + vo[l] for l in range(L + 1)] + [pin.S + pin.VS + eo[l] for l in range(L)] + \
+             [pin.S + pin.VS + pin.ES + eo[l] for l in range(L)]
+        do = [0] + [self.o_V + self.voff[l] for l in range(L + 1)] + [self.o_es + self.eoff[l] for l in range(L)] + \
+             [self.o_ed + self.eoff[l] for l in range(L)]
+        ln = [pin.S] + list(nV) + list(nE) + list(nE)
+        so, do, ln = (np.asarray(x, dtype=np.int64) for x in (so, do, ln))
+        _lib.call("sg_relayout_sample", _lib.ptr(stage), _lib.ptr(buf), len(ln), so.ctypes.data, do.ctypes.data,
+                  ln.ctypes.data, _lib.stream_ptr())
+        return self.o_ed + int(self.eoff[L - 1] + nE[L - 1]) if L else self.o_es
+
+
+_DIRECT = os.environ.get("SG_SAMPLE_DIRECT", "1") != "0"
+
 
 def _i32_or_i64(a):
     a = np.asarray(a)
@@ -406,13 +435,18 @@ class DeviceSplit:
         nV, nE = sample.sizes()
         dev = torch.device(device or "cuda")
         geo = PackGeometry.for_sizes(nV, nE, scope=(len(nE), len(pm.assignment), pm.num_devices))
-        hb, used = _PINNED.pack(geo, sample)
-        lo, hi = geo.last_vrange
-        if sum(nV) and (lo < 0 or hi >= len(pm.assignment)):  # checked while packing
-            raise ValueError("sample vertex missing from partition map")
         buf = torch.empty(geo.words, dtype=torch.int32, device=dev)
-        buf[:used].copy_(hb[:used], non_blocking=True)
-        _PINNED.record()
+        pin = getattr(sample, "pinned", None)
+        if (pin is not None and pin.vbound <= len(pm.assignment) and _DIRECT
+                and pin.tensor.device.type == "cpu" and pin.intact(sample)):
+            used = geo.relayout_from_pinned(sample, pin, buf)
+        else:
+            hb, used = _PINNED.pack(geo, sample)
+            lo, hi = geo.last_vrange
+            if sum(nV) and (lo < 0 or hi >= len(pm.assignment)):  # checked while packing
+                raise ValueError("sample vertex missing from partition map")
+            buf[:used].copy_(hb[:used], non_blocking=True)
+            _PINNED.record()
         VC = int(geo.voff[-1])
         V = buf[geo.o_V:geo.o_V + VC]
         es = buf[geo.o_es:geo.o_es + geo.EC]

@@ -110,3 +110,51 @@ def test_api_partial_cache():
     finally:
         del os.environ["SG_API_EAGER"]
     np.testing.assert_allclose(l1, l2, rtol=1e-5)
+
+
+def test_split_from_pinned_sample_matches_packed(monkeypatch):
+    """A native-sampler sample lives in one pinned buffer and reaches the
+    device with one H2D + sg_relayout_sample (no host pack): the device layout,
+    the split's host views and the plan equal those of the packing path; a
+    sample whose arrays were replaced falls back to packing."""
+    import torch
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import scheduler
+    graph, pm, cache, feats, labels, samples, params = _workload("graphsage", 3, cache_frac=0.3)
+    smp = samples[1]
+    assert smp.pinned is not None and smp.pinned.intact(smp)
+
+    def layout(splits):
+        buf, used, geo = splits.device_split.packed
+        h = buf[:used].cpu().numpy()
+        nV, nE = smp.sizes()
+        segs = [h[:geo.S]] + [h[geo.o_V + geo.voff[l]:][:nV[l]] for l in range(geo.L + 1)] + \
+               [h[geo.o_es + geo.eoff[l]:][:nE[l]] for l in range(geo.L)] + \
+               [h[geo.o_ed + geo.eoff[l]:][:nE[l]] for l in range(geo.L)]
+        return np.concatenate(segs)
+
+    s1, p1 = sg.split_minibatch(smp, pm, cache)
+    monkeypatch.setattr(scheduler, "_DIRECT", False)
+    s2, p2 = sg.split_minibatch(smp, pm, cache)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(layout(s1), layout(s2))
+    for a, b in zip(s1, s2):
+        for l in range(len(a.owned_gids)):
+            np.testing.assert_array_equal(a.owned_gids[l], b.owned_gids[l])
+            np.testing.assert_array_equal(a.ref_gids[l], b.ref_gids[l])
+        np.testing.assert_array_equal(a.load_gids, b.load_gids)
+    assert sorted(p1.entries.keys()) == sorted(p2.entries.keys())
+    for k in p1.entries.keys():
+        for f in ("gids", "holder_idx", "owner_idx"):
+            np.testing.assert_array_equal(getattr(p1.entries[k], f), getattr(p2.entries[k], f))
+    monkeypatch.setattr(scheduler, "_DIRECT", True)
+    # an array replaced by the caller: the pinned buffer no longer describes the sample
+    other = sg.MiniBatchSample(smp.num_layers, [v.copy() for v in smp.layer_vertices], list(smp.layer_edges),
+                               dst_grouped=True, pinned=smp.pinned)
+    assert not other.pinned.intact(other)
+    s3, _ = sg.split_minibatch(other, pm, cache)
+    np.testing.assert_array_equal(layout(s3), layout(s2))
+    # vertices beyond the partition map still raise (packing path checks them)
+    small = sg.range_partition(graph.num_vertices // 2, 3)
+    with pytest.raises(ValueError, match="missing from partition map"):
+        sg.split_minibatch(smp, small)

@@ -68,6 +68,9 @@ def _worker(rank, world, port, kind, captured, q, partial=False):
         tp.check()
         q.put((rank, losses, flat.cpu().numpy()))
         dist.barrier()
+        if hasattr(tp, "close"):
+            tp.close()   # unmap the peers' buffers before teardown
+        dist.barrier()
     finally:
         dist.destroy_process_group()
 

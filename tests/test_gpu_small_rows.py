@@ -199,6 +199,9 @@ def _scatter_worker(rank, world, port, kind, q):
         torch.cuda.synchronize()
         q.put((rank, out))
         dist.barrier()
+        if hasattr(tp, "close"):
+            tp.close()   # unmap the peers' buffers before teardown
+        dist.barrier()
     finally:
         dist.destroy_process_group()
 
