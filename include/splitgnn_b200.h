@@ -642,6 +642,14 @@ int sg_pipe_release(void* h, int32_t slot, void* stream);
  * `dst` on the device. nseg <= 3*SG_MAXL+2. */
 int sg_relayout_sample(const int32_t* src, int32_t* dst, int32_t nseg, const int64_t* src_off,
                        const int64_t* dst_off, const int64_t* len, void* stream);
+/* One cudaMemcpyAsync (cudaMemcpyDefault: pinned host / device pointers under
+ * UVA) on `stream`: SplitExecutor.run's parameter upload (engine.py:95-117
+ * executor inputs), sample load and gradient read-back. */
+int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* sg_relayout_sample preceded by the H2D of the page-locked host buffer
+ * (`words` int32) into the device staging buffer `stage`, both on `stream`. */
+int sg_h2d_relayout_sample(const int32_t* host_src, int64_t words, int32_t* stage, int32_t* dst, int32_t nseg,
+                           const int64_t* src_off, const int64_t* dst_off, const int64_t* len, void* stream);
 void* sg_pipe_copy_stream(void* h);
 void sg_pipe_destroy(void* h);
 int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,

@@ -265,4 +265,24 @@ extern "C" int sg_relayout_sample(const int32_t* src, int32_t* dst, int32_t nseg
   return SG_OK;
 }
 
+// One async copy in any direction (UVA: pinned host <-> device, device <->
+// device) on `stream`: the executor's parameter upload, sample load and
+// gradient read-back, without a framework dispatch per copy.
+extern "C" int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+  SG_REQUIRE(bytes >= 0 && (bytes == 0 || (dst && src)), "copy_async: bad argument");
+  if (bytes > 0) SG_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  return SG_OK;
+}
+
+// The same with the H2D in front: host_src (page-locked, `words` int32) ->
+// stage (device) on `stream`, then the relayout stage -> dst. One host call.
+extern "C" int sg_h2d_relayout_sample(const int32_t* host_src, int64_t words, int32_t* stage, int32_t* dst,
+                                      int32_t nseg, const int64_t* src_off, const int64_t* dst_off,
+                                      const int64_t* len, void* stream) {
+  SG_REQUIRE(host_src && stage && words >= 0, "h2d_relayout_sample: bad argument");
+  if (words > 0)
+    SG_CUDA(cudaMemcpyAsync(stage, host_src, (size_t)words * 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return sg_relayout_sample(stage, dst, nseg, src_off, dst_off, len, stream);
+}
+
 }  // namespace sg

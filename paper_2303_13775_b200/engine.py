@@ -846,12 +846,14 @@ class SplitExecutor:
         gs = self.graph
         host = _host_flat(self.params)
         self._snapshot = host
+        st = _lib.stream_ptr()
         up = _pinned_of(gs.p, "up")
         up.wait()
         up.np[:] = host
-        gs.p.flat.copy_(up.t, non_blocking=True)
+        _lib.call("sg_copy_async", _lib.ptr(gs.p.flat), _lib.ptr(up.t), 4 * gs.p.n, st)
         up.record()
-        gs.load_packed(self.ds.packed)
+        buf, used, _ = self.ds.packed  # the sample into the graph's input buffer
+        _lib.call("sg_copy_async", _lib.ptr(gs.inp.buf), _lib.ptr(buf), 4 * int(used), st)
         gs.replay()
         n = gs.p.n
         # every device's flat gradient (+ loss slot) comes back in one pinned
@@ -861,7 +863,7 @@ class SplitExecutor:
         dn = _pinned_of(gs.p, f"grads{g}", (g, n + 1))
         dn.wait()
         for d, f in enumerate(gs.out):
-            dn.t[d].copy_(f[:n + 1], non_blocking=True)
+            _lib.call("sg_copy_async", _lib.ptr(dn.t) + 4 * d * (n + 1), _lib.ptr(f), 4 * (n + 1), st)
         dn.record()
         dn.wait()
         hg = dn.np.copy()  # the graph's buffers (and this slot) are reused by the next run
@@ -1067,13 +1069,19 @@ def _host_sum_sgd(params, host_params, per_device_grads, hfl, cur, lr, num_targe
     total = np.array(hfl[0][:n], dtype=np.float32)
     for h in hfl[1:]:
         total += h[:n]
-    scale = np.float64(np.float32(float(lr) / float(num_targets)))
+    scale = float(np.float32(float(lr) / float(num_targets)))
     newf = (cur.astype(np.float64) - scale * total.astype(np.float64)).astype(np.float32)
-    new = {k: newf[dp.offsets[i]:dp.offsets[i + 1]].reshape(dp.shapes[i]) for i, k in enumerate(dp.names)}
-    for k, v in host_params.tensors().items():
-        v[...] = new[k]
+    off = dp.offsets
+    t = host_params.tensors()
+    if list(t.keys()) == list(dp.names):
+        for i, v in enumerate(t.values()):
+            v[...] = newf[off[i]:off[i + 1]].reshape(v.shape)
+    else:
+        for i, k in enumerate(dp.names):
+            t[k][...] = newf[off[i]:off[i + 1]].reshape(dp.shapes[i])
     if params is not host_params:  # reference object: write back in place
-        _write_back_reference(params, new)
+        _write_back_reference(params, {k: newf[off[i]:off[i + 1]].reshape(dp.shapes[i])
+                                       for i, k in enumerate(dp.names)})
     return GradDict(dparams=dp, host_flat=total)
 
 

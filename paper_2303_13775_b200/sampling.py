@@ -115,24 +115,25 @@ class PinnedArrays:
     VS: int
     ES: int
     vbound: int
+    views: tuple = ()  # the sampler's array objects: V^0..V^L, then (src, dst) per layer
 
     def intact(self, sample) -> bool:
-        """The sample's arrays are still the views into this buffer (a caller
-        that replaced one gets the packing path instead)."""
-        off = self.base + 4 * self.S
-        for v in sample.layer_vertices:
-            if not (isinstance(v, np.ndarray) and v.dtype == np.int32 and v.ctypes.data == off):
-                return False
-            off += 4 * len(v)
-        if off != self.base + 4 * (self.S + self.VS):
+        """The sample still holds the sampler's own array objects (views into
+        this buffer; in-place edits travel with the buffer). A caller that
+        replaced one gets the packing path instead."""
+        lv, le = sample.layer_vertices, sample.layer_edges
+        L = len(le)
+        w = self.views
+        if len(lv) != L + 1 or len(w) != 2 * L + 1:
             return False
-        for k in (0, 1):
-            for e in sample.layer_edges:
-                a = e[k]
-                if not (isinstance(a, np.ndarray) and a.dtype == np.int32 and a.ctypes.data == off):
-                    return False
-                off += 4 * len(a)
-        return off == self.base + 4 * (self.S + self.VS + 2 * self.ES)
+        for l in range(L + 1):
+            if lv[l] is not w[l]:
+                return False
+        for l in range(L):
+            e = le[l]
+            if e[0] is not w[L + 1 + l][0] or e[1] is not w[L + 1 + l][1]:
+                return False
+        return True
 
 
 _CUDA = None
@@ -218,7 +219,8 @@ class NativeSampler:
         le = [(es[eo[l]:eo[l + 1]], ed[eo[l]:eo[l + 1]]) for l in range(L)]
         smp = MiniBatchSample(L, lv, le, dst_grouped=True)
         if pin is not None:
-            smp.pinned = PinnedArrays(pin, buf.ctypes.data, S, VS, ES, int(self.graph.num_vertices))
+            smp.pinned = PinnedArrays(pin, buf.ctypes.data, S, VS, ES, int(self.graph.num_vertices),
+                                      tuple(lv) + tuple(le))
         return smp
 
 

@@ -223,6 +223,9 @@ class PackGeometry:
         VC, EC = int(self.voff[-1]), max(int(self.eoff[-1]), 1)
         self.S = 2 * (2 * self.L + 1)
         self.EC = EC
+        self._voff_l = [int(x) for x in self.voff]
+        self._eoff_l = [int(x) for x in self.eoff]
+        self._seg = None
         self.o_V, self.o_es, self.o_ed = self.S, self.S + VC, self.S + VC + EC
         self.words = self.S + VC + 2 * EC
 
@@ -269,30 +272,75 @@ class PackGeometry:
 
     def relayout_from_pinned(self, sample, pin, buf):
         """A native-sampler sample already in one pinned buffer (PinnedArrays):
-        one H2D of it (torch's copy, so the caching host allocator tracks the
-        buffer until the DMA ends) and one kernel moving its segments to this
-        layout's offsets in `buf` (sg_relayout_sample). Returns the words used."""
-        import torch
+        one H2D of it into a device staging buffer and one kernel moving its
+        segments to this layout's offsets in `buf` (sg_h2d_relayout_sample,
+        one host call). The pinned buffer stays referenced until an event
+        after its DMA has completed (_InFlight). Returns the words used."""
         nV, nE = sample.sizes()
-        if any(a > b for a, b in zip(nV, self.cap_nV)) or any(a > b for a, b in zip(nE, self.cap_nE)):
-            raise ValueError("sample exceeds the captured capacities")
+        cV, cE = self.cap_nV, self.cap_nE
         L = self.L
-        n = pin.S + pin.VS + 2 * pin.ES
-        stage = torch.empty(n, dtype=torch.int32, device=buf.device)
-        stage.copy_(pin.tensor[:n], non_blocking=True)
-        vo = np.r_[0, np.cumsum(nV)]
-        eo = np.r_[0, np.cumsum(nE)]
-        so = [0] + [pin.S + vo[l] for l in range(L + 1)] + [pin.S + pin.VS + eo[l] for l in range(L)] + \
-             [pin.S + pin.VS + pin.ES + eo[l] for l in range(L)]
-        do = [0] + [self.o_V + self.voff[l] for l in range(L + 1)] + [self.o_es + self.eoff[l] for l in range(L)] + \
-             [self.o_ed + self.eoff[l] for l in range(L)]
-        ln = [pin.S] + list(nV) + list(nE) + list(nE)
-        so, do, ln = (np.asarray(x, dtype=np.int64) for x in (so, do, ln))
-        _lib.call("sg_relayout_sample", _lib.ptr(stage), _lib.ptr(buf), len(ln), so.ctypes.data, do.ctypes.data,
-                  ln.ctypes.data, _lib.stream_ptr())
-        return self.o_ed + int(self.eoff[L - 1] + nE[L - 1]) if L else self.o_es
+        if any(nV[l] > cV[l] for l in range(L + 1)) or any(nE[l] > cE[l] for l in range(L)):
+            raise ValueError("sample exceeds the captured capacities")
+        S, VS, ES = pin.S, pin.VS, pin.ES
+        n = S + VS + 2 * ES
+        seg = self._seg
+        if seg is None:
+            seg = self._seg = np.zeros((3, 3 * L + 2), dtype=np.int64)
+        so, do, ln = seg[0], seg[1], seg[2]
+        voff, eoff = self._voff_l, self._eoff_l
+        so[0], do[0], ln[0] = 0, 0, S
+        a = S
+        for l in range(L + 1):
+            so[1 + l], do[1 + l], ln[1 + l] = a, self.o_V + voff[l], nV[l]
+            a += nV[l]
+        b = S + VS + ES
+        for l in range(L):
+            k = 2 + L + l
+            so[k], do[k], ln[k] = a, self.o_es + eoff[l], nE[l]
+            so[k + L], do[k + L], ln[k + L] = b, self.o_ed + eoff[l], nE[l]
+            a += nE[l]
+            b += nE[l]
+        stage = _STAGE.get(n, buf.device)
+        _lib.call("sg_h2d_relayout_sample", pin.base, n, _lib.ptr(stage), _lib.ptr(buf), 3 * L + 2,
+                  so.ctypes.data, do.ctypes.data, ln.ctypes.data, _lib.stream_ptr())
+        _INFLIGHT.hold(pin.tensor)
+        return self.o_ed + eoff[L - 1] + nE[L - 1] if L else self.o_es
 
 
+class _Stage:
+    """Device staging buffer of the direct path, reused across calls (its uses
+    are ordered on the current stream)."""
+
+    def __init__(self):
+        self.t = None
+
+    def get(self, n, device):
+        if self.t is None or self.t.numel() < n or self.t.device != device:
+            self.t = torch.empty(max(int(n * 1.25), 1 << 16), dtype=torch.int32, device=device)
+        return self.t
+
+
+class _InFlight:
+    """Pinned sample buffers whose H2D may still be running: each is kept
+    alive until an event recorded after its copy has completed (the caller
+    may drop the sample right after split_minibatch)."""
+
+    def __init__(self):
+        self.q = []
+
+    def hold(self, t):
+        ev = torch.cuda.Event()
+        ev.record()
+        self.q.append((ev, t))
+        while self.q and (len(self.q) > 64 or self.q[0][0].query()):
+            if len(self.q) > 64:
+                self.q[0][0].synchronize()
+            self.q.pop(0)
+
+
+_STAGE = _Stage()
+_INFLIGHT = _InFlight()
+_LAYOUTS = {}
 _DIRECT = os.environ.get("SG_SAMPLE_DIRECT", "1") != "0"
 
 
@@ -371,11 +419,17 @@ class DeviceSplit:
         self.nV = [int(x) for x in nV]
         self.nE = [int(x) for x in nE]
         self.dst_grouped = bool(dst_grouped)
-        lay = _lib.SgSplitLayout()
-        nVa = (C.c_int64 * (self.L + 1))(*self.nV)
-        nEa = (C.c_int64 * max(self.L, 1))(*(self.nE or [0]))
-        _lib.check(lib.sg_split_layout(self.L, self.g, nVa, nEa, len(pm.assignment), C.byref(lay)),
-                   "split_layout")
+        key = (self.L, self.g, tuple(self.nV), tuple(self.nE), len(pm.assignment))
+        lay = _LAYOUTS.get(key)  # read-only once built: shared by splits of one geometry
+        if lay is None:
+            lay = _lib.SgSplitLayout()
+            nVa = (C.c_int64 * (self.L + 1))(*self.nV)
+            nEa = (C.c_int64 * max(self.L, 1))(*(self.nE or [0]))
+            _lib.check(lib.sg_split_layout(self.L, self.g, nVa, nEa, len(pm.assignment), C.byref(lay)),
+                       "split_layout")
+            if len(_LAYOUTS) > 256:
+                _LAYOUTS.clear()
+            _LAYOUTS[key] = lay
         self.lay = lay
         self.V, self.esrc, self.edst = V, esrc, edst
         self._host_V = host_V
@@ -437,8 +491,7 @@ class DeviceSplit:
         geo = PackGeometry.for_sizes(nV, nE, scope=(len(nE), len(pm.assignment), pm.num_devices))
         buf = torch.empty(geo.words, dtype=torch.int32, device=dev)
         pin = getattr(sample, "pinned", None)
-        if (pin is not None and pin.vbound <= len(pm.assignment) and _DIRECT
-                and pin.tensor.device.type == "cpu" and pin.intact(sample)):
+        if pin is not None and pin.vbound <= len(pm.assignment) and _DIRECT and pin.intact(sample):
             used = geo.relayout_from_pinned(sample, pin, buf)
         else:
             hb, used = _PINNED.pack(geo, sample)
