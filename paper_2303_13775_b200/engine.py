@@ -755,8 +755,8 @@ def _pinned_of(dp, which, shape=None):
 
 
 def _host_flat(params):
-    t = params.tensors()
-    return np.concatenate([np.asarray(v, dtype=np.float32).reshape(-1) for v in t.values()])
+    return np.concatenate([np.ravel(v) for v in params.tensors().values()], dtype=np.float32,
+                          casting="same_kind")
 
 
 class SplitExecutor:

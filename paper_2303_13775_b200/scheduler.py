@@ -493,7 +493,9 @@ class DeviceSplit:
         pin = getattr(sample, "pinned", None)
         if pin is not None and pin.vbound <= len(pm.assignment) and _DIRECT and pin.intact(sample):
             used = geo.relayout_from_pinned(sample, pin, buf)
+            h2d = 4 * (pin.S + pin.VS + 2 * pin.ES)
         else:
+            h2d = None
             hb, used = _PINNED.pack(geo, sample)
             lo, hi = geo.last_vrange
             if sum(nV) and (lo < 0 or hi >= len(pm.assignment)):  # checked while packing
@@ -514,6 +516,7 @@ class DeviceSplit:
         ds = cls(V, es, ed, geo.cap_nV, geo.cap_nE, pm, cache, True, dev, host_V=host_V,
                  sizes=buf[:geo.S].view(torch.int64), defer=defer)
         ds.packed = (buf, used, geo)
+        ds.h2d_bytes = h2d if h2d is not None else 4 * used  # what crossed PCIe for this sample
         ds.num_targets = len(sample.targets)
         return ds
 
