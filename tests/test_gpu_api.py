@@ -158,3 +158,32 @@ def test_split_from_pinned_sample_matches_packed(monkeypatch):
     small = sg.range_partition(graph.num_vertices // 2, 3)
     with pytest.raises(ValueError, match="missing from partition map"):
         sg.split_minibatch(smp, small)
+
+
+@pytest.mark.parametrize("g", [1, 3])
+def test_host_sgd_matches_device_sgd(g):
+    """allreduce_and_step on gradients a captured run brought to the host (the
+    host SGD) equals the device kernel (sg_sum_sgd: device-order fp32 sum,
+    fused multiply-add) on the same gradients: at most 1 ulp apart, almost
+    always equal."""
+    import copy
+    import torch
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import engine
+    graph, pm, cache, feats, labels, samples, params = _workload("graphsage", g)
+    p_host, p_dev = copy.deepcopy(params), copy.deepcopy(params)
+    splits, plan = sg.split_minibatch(samples[0], pm, cache)
+    ex = sg.SplitExecutor(p_host, splits, plan, feats, labels)
+    _, grads = ex.run()
+    assert ex.graph is not None and all(gd.host_flat is not None for gd in grads)
+    dev_grads = [engine.GradDict(dparams=gd.dparams, device_flat=torch.from_numpy(gd.host_flat).cuda())
+                 for gd in grads]
+    nt = len(samples[0].targets)
+    s_host = sg.allreduce_and_step(p_host, grads, 0.37, nt)
+    s_dev = sg.allreduce_and_step(p_dev, dev_grads, 0.37, nt)
+    for k in s_host.keys():
+        np.testing.assert_array_equal(s_host[k], s_dev[k])  # the device-order sum, bit-exact
+    a = engine._host_flat(p_host)
+    b = engine._host_flat(p_dev)
+    ulp = np.abs(a.view(np.int32).astype(np.int64) - b.view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1 and np.count_nonzero(ulp) <= max(1, a.size // 1000), (ulp.max(), np.count_nonzero(ulp))
