@@ -518,6 +518,21 @@ int sg_partition_coarse_host(int64_t n, const int64_t* off, const int32_t* nbr, 
  * split_minibatch's staging of the sample (scheduler.py:164). */
 int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, const int64_t* dst_off, const void* const* src,
                    const int32_t* elem_bytes, int32_t threads, int64_t* vrange);
+/* sg_host_params_gather (HOST memory, CPU): SplitExecutor.run's parameter
+ * snapshot (engine.py:95-117): k contiguous arrays (elem_bytes 8 = fp64,
+ * 4 = fp32) flattened to fp32 in order into out. */
+int sg_host_params_gather(int32_t k, const void* const* ptrs, const int64_t* sizes, const int32_t* elem_bytes,
+                          float* out);
+/* sg_host_sum_sgd (HOST memory, CPU): allreduce_and_step (engine.py:633-647,
+ * models.py:95-99) for gradients already on the host. If the k parameter
+ * arrays still equal `snapshot` (nullable: skip the check): total_out = the g
+ * flat fp32 gradients (n each) summed in device order, and every parameter
+ * p <- fp32(p - scale * total), the product exact and rounded once (the device
+ * kernel's fused multiply-add), written back in the array's element type;
+ * *applied = 1. Otherwise nothing is written and *applied = 0. */
+int sg_host_sum_sgd(int32_t k, void* const* ptrs, const int64_t* sizes, const int32_t* elem_bytes,
+                    const float* snapshot, const float* const* grads, int32_t g, int64_t n, float scale,
+                    float* total_out, int32_t* applied);
 int sg_partition_refine_host(int64_t n, const int64_t* off, const int32_t* nbr, const int32_t* wt,
                              const int32_t* vw, int32_t g, int64_t cap, int32_t max_passes, int32_t* part,
                              int64_t* cut_out);

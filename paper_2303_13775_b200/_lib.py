@@ -100,6 +100,8 @@ _SIGS = {
     "sg_partition_coarse_host": (i32, [i64, vp, vp, vp, vp, i32, i64, u64, i32, vp, vp]),
     "sg_partition_refine_host": (i32, [i64, vp, vp, vp, vp, i32, i64, i32, vp, vp]),
     "sg_pack_sample": (i32, [vp, i32, vp, vp, vp, vp, i32, vp]),
+    "sg_host_params_gather": (i32, [i32, vp, vp, vp, vp]),
+    "sg_host_sum_sgd": (i32, [i32, vp, vp, vp, vp, vp, i32, i64, f32, vp, vp]),
     "sg_gat_wgrad_dst_blocks": (i32, [i64]),
     "sg_gat_agg_fused": (i32, [vp, P(SgSplitLayout), i32, i32, i32, f32, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, i64,
                                vp]),

@@ -623,3 +623,88 @@ extern "C" int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, con
   }
   return SG_OK;
 }
+
+// SplitExecutor.run / allreduce_and_step on host ModelParams (engine.py:95-117,
+// 633-647): the k parameter arrays (contiguous, fp64 or fp32: elem_bytes 8 / 4)
+// flattened to fp32 in order -- the upload snapshot.
+extern "C" int sg_host_params_gather(int32_t k, const void* const* ptrs, const int64_t* sizes,
+                                     const int32_t* elem_bytes, float* out) {
+  if (k < 0 || (k > 0 && (!ptrs || !sizes || !elem_bytes || !out))) {
+    sg::set_error("host_params_gather: bad argument");
+    return SG_ERR_ARG;
+  }
+  for (int32_t i = 0; i < k; ++i) {
+    const int64_t m = sizes[i];
+    if (elem_bytes[i] == 8) {
+      const double* s = (const double*)ptrs[i];
+      for (int64_t j = 0; j < m; ++j) out[j] = (float)s[j];
+    } else if (elem_bytes[i] == 4) {
+      std::memcpy(out, ptrs[i], 4 * m);
+    } else {
+      sg::set_error("host_params_gather: element size must be 4 or 8");
+      return SG_ERR_ARG;
+    }
+    out += m;
+  }
+  return SG_OK;
+}
+
+// allreduce_and_step's host side for gradients already on the host: when the
+// parameters still equal `snapshot` (the values the step ran with),
+// total = the g flat gradients summed in device order (fp32), and every
+// parameter p <- fp32(p - scale * total) with the product formed exactly (in
+// fp64) and rounded once, as the device kernel's fused multiply-add; written
+// back into the arrays in their own element type. *applied = 0 (nothing
+// written) when the parameters changed since the snapshot.
+extern "C" int sg_host_sum_sgd(int32_t k, void* const* ptrs, const int64_t* sizes, const int32_t* elem_bytes,
+                               const float* snapshot, const float* const* grads, int32_t g, int64_t n,
+                               float scale, float* total_out, int32_t* applied) {
+  if (k < 0 || g < 1 || n < 0 || !grads || !total_out || !applied || (k > 0 && (!ptrs || !sizes || !elem_bytes))) {
+    sg::set_error("host_sum_sgd: bad argument");
+    return SG_ERR_ARG;
+  }
+  int64_t tot = 0;
+  for (int32_t i = 0; i < k; ++i) tot += sizes[i];
+  if (tot != n) {
+    sg::set_error("host_sum_sgd: parameter sizes do not add up to n");
+    return SG_ERR_ARG;
+  }
+  *applied = 0;
+  if (snapshot) {  // unchanged since the run?
+    int64_t o = 0;
+    for (int32_t i = 0; i < k; ++i) {
+      const int64_t m = sizes[i];
+      if (elem_bytes[i] == 8) {
+        const double* s = (const double*)ptrs[i];
+        for (int64_t j = 0; j < m; ++j)
+          if ((float)s[j] != snapshot[o + j] && !(std::isnan((float)s[j]) && std::isnan(snapshot[o + j])))
+            return SG_OK;
+      } else {
+        const float* s = (const float*)ptrs[i];
+        for (int64_t j = 0; j < m; ++j)
+          if (s[j] != snapshot[o + j] && !(std::isnan(s[j]) && std::isnan(snapshot[o + j]))) return SG_OK;
+      }
+      o += m;
+    }
+  }
+  for (int64_t j = 0; j < n; ++j) {
+    float t = grads[0][j];
+    for (int32_t d = 1; d < g; ++d) t += grads[d][j];
+    total_out[j] = t;
+  }
+  const double sc = (double)scale;
+  int64_t o = 0;
+  for (int32_t i = 0; i < k; ++i) {
+    const int64_t m = sizes[i];
+    if (elem_bytes[i] == 8) {
+      double* s = (double*)ptrs[i];
+      for (int64_t j = 0; j < m; ++j) s[j] = (double)(float)((double)(float)s[j] - sc * (double)total_out[o + j]);
+    } else {
+      float* s = (float*)ptrs[i];
+      for (int64_t j = 0; j < m; ++j) s[j] = (float)((double)s[j] - sc * (double)total_out[o + j]);
+    }
+    o += m;
+  }
+  *applied = 1;
+  return SG_OK;
+}

@@ -754,7 +754,64 @@ def _pinned_of(dp, which, shape=None):
     return pf
 
 
+class _ParamTable:
+    """Pointers / sizes / element sizes of a host ModelParams' arrays for the
+    native host helpers (sg_host_params_gather, sg_host_sum_sgd), kept on the
+    ModelParams and rebuilt when one of its arrays is replaced."""
+
+    __slots__ = ("arrs", "ptrs", "sizes", "eb", "n", "k", "a_ptrs", "a_sizes", "a_eb", "applied", "a_applied")
+
+    def __init__(self, arrs):
+        self.arrs = arrs
+        self.k = len(arrs)
+        self.ptrs = np.array([a.ctypes.data for a in arrs], dtype=np.uint64)
+        self.sizes = np.array([a.size for a in arrs], dtype=np.int64)
+        self.eb = np.array([a.itemsize for a in arrs], dtype=np.int32)
+        self.n = int(self.sizes.sum())
+        self.applied = np.zeros(1, dtype=np.int32)
+        # addresses as ints: a numpy .ctypes.data costs ~1 us per access
+        self.a_ptrs, self.a_sizes, self.a_eb, self.a_applied = (
+            x.ctypes.data for x in (self.ptrs, self.sizes, self.eb, self.applied))
+
+
+def _param_arrays(params):
+    """params.tensors().values() in the same order, without building the names."""
+    out = []
+    if params.kind == "graphsage":
+        for l in params.layers:
+            out += (l.w_self, l.w_neigh, l.bias)
+    else:
+        for l in params.layers:
+            out += (l.w, l.a_src, l.a_dst)
+    out += (params.w_cls, params.b_cls)
+    return out
+
+
+def _param_table(params):
+    """The native pointer table of `params` (host ModelParams), or None when an
+    array is not a C-contiguous fp32 / fp64 ndarray (numpy paths then)."""
+    arrs = _param_arrays(params)
+    tab = getattr(params, "_sg_table", None)
+    if tab is not None and len(tab.arrs) == len(arrs) and all(a is b for a, b in zip(tab.arrs, arrs)):
+        return tab
+    for a in arrs:
+        if not (isinstance(a, np.ndarray) and a.dtype in (np.float32, np.float64) and a.flags.c_contiguous
+                and a.flags.writeable):
+            return None
+    tab = _ParamTable(arrs)
+    try:
+        params._sg_table = tab
+    except AttributeError:
+        pass
+    return tab
+
+
 def _host_flat(params):
+    tab = _param_table(params) if isinstance(params, ModelParams) else None
+    if tab is not None:
+        out = np.empty(tab.n, dtype=np.float32)
+        _lib.call("sg_host_params_gather", tab.k, tab.a_ptrs, tab.a_sizes, tab.a_eb, out.ctypes.data)
+        return out
     return np.concatenate([np.ravel(v) for v in params.tensors().values()], dtype=np.float32,
                           casting="same_kind")
 
@@ -1022,9 +1079,20 @@ def allreduce_and_step(params, per_device_grads, lr, num_targets):
         snap = getattr(per_device_grads[0], "param_snapshot", None) if per_device_grads else None
         hfl = [getattr(gd, "host_flat", None) for gd in per_device_grads]
         if snap is not None and hfl and all(h is not None for h in hfl):
-            cur = _host_flat(host_params)
-            if np.array_equal(cur, snap):
-                return _host_sum_sgd(params, host_params, per_device_grads, hfl, cur, lr, num_targets)
+            tab = _param_table(host_params) if params is host_params else None
+            if tab is not None:  # one native call: unchanged-check, device-order sum, SGD, write-back
+                dpr = per_device_grads[0].dparams
+                if tab.n == dpr.n and all(h.dtype == np.float32 and h.flags.c_contiguous for h in hfl):
+                    total = np.empty(dpr.n, dtype=np.float32)
+                    gp = (ctypes.c_void_p * len(hfl))(*[h.ctypes.data for h in hfl])
+                    _lib.call("sg_host_sum_sgd", tab.k, tab.a_ptrs, tab.a_sizes, tab.a_eb, snap.ctypes.data, gp,
+                              len(hfl), dpr.n, float(lr) / float(num_targets), total.ctypes.data, tab.a_applied)
+                    if tab.applied[0]:
+                        return GradDict(dparams=dpr, host_flat=total)
+            else:
+                cur = _host_flat(host_params)
+                if np.array_equal(cur, snap):
+                    return _host_sum_sgd(params, host_params, per_device_grads, hfl, cur, lr, num_targets)
         cand = getattr(per_device_grads[0], "dparams", None) if per_device_grads else None
         if snap is not None and cand is not None and all(getattr(gd, "dparams", None) is cand
                                                          for gd in per_device_grads):

@@ -226,6 +226,7 @@ class PackGeometry:
         self._voff_l = [int(x) for x in self.voff]
         self._eoff_l = [int(x) for x in self.eoff]
         self._seg = None
+        self._seg_ptrs = None
         self.o_V, self.o_es, self.o_ed = self.S, self.S + VC, self.S + VC + EC
         self.words = self.S + VC + 2 * EC
 
@@ -270,22 +271,20 @@ class PackGeometry:
         self.last_vrange = (int(vr[0]), int(vr[1]))
         return used
 
-    def relayout_from_pinned(self, sample, pin, buf):
-        """A native-sampler sample already in one pinned buffer (PinnedArrays):
-        one H2D of it into a device staging buffer and one kernel moving its
-        segments to this layout's offsets in `buf` (sg_h2d_relayout_sample,
-        one host call). The pinned buffer stays referenced until an event
-        after its DMA has completed (_InFlight). Returns the words used."""
+    def relayout_from_stage(self, sample, pin, stage, buf):
+        """A native-sampler sample (PinnedArrays) already sent to the device
+        staging buffer by _h2d_pinned: one kernel moves its segments to this
+        layout's offsets in `buf` (sg_relayout_sample). Returns the words used."""
         nV, nE = sample.sizes()
         cV, cE = self.cap_nV, self.cap_nE
         L = self.L
         if any(nV[l] > cV[l] for l in range(L + 1)) or any(nE[l] > cE[l] for l in range(L)):
             raise ValueError("sample exceeds the captured capacities")
         S, VS, ES = pin.S, pin.VS, pin.ES
-        n = S + VS + 2 * ES
         seg = self._seg
         if seg is None:
             seg = self._seg = np.zeros((3, 3 * L + 2), dtype=np.int64)
+            self._seg_ptrs = tuple(seg[i].ctypes.data for i in range(3))
         so, do, ln = seg[0], seg[1], seg[2]
         voff, eoff = self._voff_l, self._eoff_l
         so[0], do[0], ln[0] = 0, 0, S
@@ -300,11 +299,20 @@ class PackGeometry:
             so[k + L], do[k + L], ln[k + L] = b, self.o_ed + eoff[l], nE[l]
             a += nE[l]
             b += nE[l]
-        stage = _STAGE.get(n, buf.device)
-        _lib.call("sg_h2d_relayout_sample", pin.base, n, _lib.ptr(stage), _lib.ptr(buf), 3 * L + 2,
-                  so.ctypes.data, do.ctypes.data, ln.ctypes.data, _lib.stream_ptr())
-        _INFLIGHT.hold(pin.tensor)
+        _lib.call("sg_relayout_sample", stage.data_ptr(), buf.data_ptr(), 3 * L + 2, *self._seg_ptrs,
+                  _lib.stream_ptr())
         return self.o_ed + eoff[L - 1] + nE[L - 1] if L else self.o_es
+
+
+def _h2d_pinned(pin, device):
+    """One H2D of a native-sampler sample's pinned buffer into the reused
+    device staging buffer (current stream); the pinned buffer stays referenced
+    until an event after the copy has completed (_InFlight)."""
+    n = pin.S + pin.VS + 2 * pin.ES
+    stage = _STAGE.get(n, device)
+    _lib.call("sg_copy_async", stage.data_ptr(), pin.base, 4 * n, _lib.stream_ptr())
+    _INFLIGHT.hold(pin.tensor)
+    return stage
 
 
 class _Stage:
@@ -315,6 +323,8 @@ class _Stage:
         self.t = None
 
     def get(self, n, device):
+        if device.type == "cuda" and device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
         if self.t is None or self.t.numel() < n or self.t.device != device:
             self.t = torch.empty(max(int(n * 1.25), 1 << 16), dtype=torch.int32, device=device)
         return self.t
@@ -486,13 +496,16 @@ class DeviceSplit:
         One pinned pack + one H2D; the split kernel is deferred (see __init__).
         Needs a destination-grouped sample."""
         sample = as_sample(sample)
-        nV, nE = sample.sizes()
         dev = torch.device(device or "cuda")
+        pin = getattr(sample, "pinned", None)
+        stage = None
+        if pin is not None and pin.vbound <= len(pm.assignment) and _DIRECT and pin.intact(sample):
+            stage = _h2d_pinned(pin, dev)  # first: the host work below overlaps the DMA
+        nV, nE = sample.sizes()
         geo = PackGeometry.for_sizes(nV, nE, scope=(len(nE), len(pm.assignment), pm.num_devices))
         buf = torch.empty(geo.words, dtype=torch.int32, device=dev)
-        pin = getattr(sample, "pinned", None)
-        if pin is not None and pin.vbound <= len(pm.assignment) and _DIRECT and pin.intact(sample):
-            used = geo.relayout_from_pinned(sample, pin, buf)
+        if stage is not None:
+            used = geo.relayout_from_stage(sample, pin, stage, buf)
             h2d = 4 * (pin.S + pin.VS + 2 * pin.ES)
         else:
             h2d = None

@@ -37,15 +37,17 @@ def tick(k, t0):
 def split(smp):
     t = time.perf_counter()
     smp = sg.sampling.as_sample(smp)
+    ok = smp.pinned.intact(smp)
+    t = tick("intact", t)
+    stage = scheduler._h2d_pinned(smp.pinned, torch.device("cuda"))
+    t = tick("h2d", t)
     nV, nE = smp.sizes()
     geo = PackGeometry.for_sizes(nV, nE, scope=(len(nE), len(pm.assignment), pm.num_devices))
     t = tick("geometry", t)
     buf = torch.empty(geo.words, dtype=torch.int32, device="cuda")
     t = tick("empty", t)
-    ok = smp.pinned.intact(smp)
-    t = tick("intact", t)
-    used = geo.relayout_from_pinned(smp, smp.pinned, buf)
-    t = tick("h2d+relayout", t)
+    used = geo.relayout_from_stage(smp, smp.pinned, stage, buf)
+    t = tick("relayout", t)
     VC = int(geo.voff[-1])
     ds = DeviceSplit(buf[geo.o_V:geo.o_V + VC], buf[geo.o_es:geo.o_es + geo.EC], buf[geo.o_ed:geo.o_ed + geo.EC],
                      geo.cap_nV, geo.cap_nE, pm, cache, True, torch.device("cuda"), host_V=None,
