@@ -269,3 +269,49 @@ def test_pack_sample_matches_numpy_layout(dtype):
     assert PackGeometry.for_sizes([x // 2 for x in nV], [x // 2 for x in nE], scope=("test", dtype)) is geo
     big = PackGeometry.for_sizes([2 * x for x in nV], nE, scope=("test", dtype))
     assert big is not geo and all(b >= c for b, c in zip(big.cap_nV, geo.cap_nV))
+
+
+@pytest.mark.parametrize("g", [1, 3])
+def test_host_sum_sgd_matches_fma_formula(g):
+    """allreduce_and_step's host side (sg_host_params_gather + sg_host_sum_sgd,
+    engine.py:633-647): the snapshot is the fp32 flattening, the sum runs in
+    device order in fp32, and p <- fp32(p - scale * total) with the product
+    exact (fp64) -- bit-exact against that formula in numpy, for fp64 and fp32
+    parameter arrays; nothing is written when the parameters changed."""
+    import copy
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import engine
+    params = sg.init_params("graphsage", 20, 8, 5, 2, seed=1)
+    params.w_cls = params.w_cls.astype(np.float32)  # mixed element types
+    tab = engine._param_table(params)
+    assert tab is not None
+    snap = engine._host_flat(params)
+    np.testing.assert_array_equal(snap, np.concatenate([np.ravel(v) for v in params.tensors().values()])
+                                  .astype(np.float32))
+    rng = np.random.default_rng(0)
+    grads = [rng.standard_normal(tab.n + 1).astype(np.float32) for _ in range(g)]
+    total = np.empty(tab.n, np.float32)
+    gp = (C.c_void_p * g)(*[h.ctypes.data for h in grads])
+    scale = float(np.float32(0.37 / 64))
+    before = copy.deepcopy(params)
+    from paper_2303_13775_b200 import _lib
+    _lib.call("sg_host_sum_sgd", tab.k, tab.a_ptrs, tab.a_sizes, tab.a_eb, snap.ctypes.data, gp, g, tab.n,
+              scale, total.ctypes.data, tab.a_applied)
+    assert tab.applied[0] == 1
+    want_t = grads[0][:tab.n].copy()
+    for h in grads[1:]:
+        want_t += h[:tab.n]
+    np.testing.assert_array_equal(total, want_t)
+    want = (snap.astype(np.float64) - scale * want_t.astype(np.float64)).astype(np.float32)
+    np.testing.assert_array_equal(engine._host_flat(params), want)
+    for (k, a), b in zip(params.tensors().items(), before.tensors().values()):
+        assert a.dtype == b.dtype, k
+    # parameters changed since the snapshot: untouched, applied = 0
+    cur = engine._host_flat(params)
+    _lib.call("sg_host_sum_sgd", tab.k, tab.a_ptrs, tab.a_sizes, tab.a_eb, snap.ctypes.data, gp, g, tab.n,
+              scale, total.ctypes.data, tab.a_applied)
+    assert tab.applied[0] == 0
+    np.testing.assert_array_equal(engine._host_flat(params), cur)
+    # a replaced array rebuilds the table
+    params.b_cls = params.b_cls.copy()
+    assert engine._param_table(params) is not tab
