@@ -117,6 +117,11 @@ class PinnedArrays:
     vbound: int
     views: tuple = ()  # the sampler's array objects: V^0..V^L, then (src, dst) per layer
 
+    def __reduce__(self):
+        # the page-locked buffer and its address belong to this process: a
+        # pickled (e.g. sent to another process) sample is packed instead
+        return (_no_pinned, ())
+
     def intact(self, sample) -> bool:
         """The sample still holds the sampler's own array objects (views into
         this buffer; in-place edits travel with the buffer). A caller that
@@ -124,7 +129,7 @@ class PinnedArrays:
         lv, le = sample.layer_vertices, sample.layer_edges
         L = len(le)
         w = self.views
-        if len(lv) != L + 1 or len(w) != 2 * L + 1:
+        if len(lv) != L + 1 or len(w) != 2 * L + 1 or self.tensor.data_ptr() != self.base:
             return False
         for l in range(L + 1):
             if lv[l] is not w[l]:
@@ -134,6 +139,10 @@ class PinnedArrays:
             if e[0] is not w[L + 1 + l][0] or e[1] is not w[L + 1 + l][1]:
                 return False
         return True
+
+
+def _no_pinned():
+    return None
 
 
 _CUDA = None

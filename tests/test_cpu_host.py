@@ -315,3 +315,19 @@ def test_host_sum_sgd_matches_fma_formula(g):
     # a replaced array rebuilds the table
     params.b_cls = params.b_cls.copy()
     assert engine._param_table(params) is not tab
+
+
+def test_pinned_sample_does_not_survive_pickling():
+    """A sample's page-locked buffer (PinnedArrays) is process-local: pickling
+    the sample drops it, so split_minibatch packs the unpickled copy instead
+    of DMAing from a stale address."""
+    import pickle
+    from paper_2303_13775_b200.sampling import MiniBatchSample, PinnedArrays
+    buf = np.zeros(64, dtype=np.int32)
+    lv = [buf[2:6], buf[6:8]]
+    le = [(buf[8:10], buf[10:12])]
+    smp = MiniBatchSample(1, lv, le, dst_grouped=True,
+                          pinned=PinnedArrays(None, buf.ctypes.data, 2, 6, 2, 100, tuple(lv) + tuple(le)))
+    back = pickle.loads(pickle.dumps(smp))
+    assert back.pinned is None
+    np.testing.assert_array_equal(back.layer_vertices[0], lv[0])
