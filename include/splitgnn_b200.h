@@ -661,6 +661,11 @@ int sg_relayout_sample(const int32_t* src, int32_t* dst, int32_t nseg, const int
  * UVA) on `stream`: SplitExecutor.run's parameter upload (engine.py:95-117
  * executor inputs), sample load and gradient read-back. */
 int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* sg_relayout_sample with the segments derived on the device from the sample's
+ * own int64 sizes header (src[0 .. S) words, S = 2(2L+1)): geo = [L, S, o_V,
+ * o_es, o_ed, voff[0..L+1], eoff[0..L]] (host int64, the capacity layout;
+ * lengths clamped to it); max_len bounds the longest segment (grid size). */
+int sg_relayout_sample_hdr(const int32_t* src, int32_t* dst, const int64_t* geo, int64_t max_len, void* stream);
 /* sg_relayout_sample preceded by the H2D of the page-locked host buffer
  * (`words` int32) into the device staging buffer `stage`, both on `stream`. */
 int sg_h2d_relayout_sample(const int32_t* host_src, int64_t words, int32_t* stage, int32_t* dst, int32_t nseg,

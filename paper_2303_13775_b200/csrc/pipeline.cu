@@ -274,6 +274,62 @@ extern "C" int sg_copy_async(void* dst, const void* src, int64_t bytes, void* st
   return SG_OK;
 }
 
+// Header-driven form: the segments are derived on the device from the int64
+// sizes header the sample carries (stage[0 .. S)), so the host passes only the
+// capacity geometry (cached per geometry): geo = [L, S, o_V, o_es, o_ed,
+// voff[0..L+1], eoff[0..L]] (int64, host memory, read at launch). Lengths are
+// clamped to the capacities.
+namespace {
+struct RelGeo {
+  int32_t L;
+  int64_t S, o_V, o_es, o_ed, voff[SG_MAXL + 2], eoff[SG_MAXL + 1];
+};
+__global__ void k_relayout_hdr(const int32_t* __restrict__ src, int32_t* __restrict__ dst, RelGeo g) {
+  const int seg = blockIdx.y, L = g.L;
+  const int64_t* sz = reinterpret_cast<const int64_t*>(src);  // [nV_0..nV_L, nE_1..nE_L]
+  int64_t VS = 0, ES = 0;
+  for (int l = 0; l <= L; ++l) VS += sz[l];
+  for (int l = 0; l < L; ++l) ES += sz[L + 1 + l];
+  int64_t so, dof, len;
+  if (seg == 0) {
+    so = 0; dof = 0; len = g.S;
+  } else if (seg <= L + 1) {  // V^l
+    const int l = seg - 1;
+    so = g.S;
+    for (int k = 0; k < l; ++k) so += sz[k];
+    dof = g.o_V + g.voff[l];
+    len = min(sz[l], g.voff[l + 1] - g.voff[l]);
+  } else {  // E^l sources (seg < 2L+2), then destinations
+    const bool d = seg >= 2 * L + 2;
+    const int l = seg - (d ? 2 * L + 2 : L + 2);
+    so = g.S + VS + (d ? ES : 0);
+    for (int k = 0; k < l; ++k) so += sz[L + 1 + k];
+    dof = (d ? g.o_ed : g.o_es) + g.eoff[l];
+    len = min(sz[L + 1 + l], g.eoff[l + 1] - g.eoff[l]);
+  }
+  const int32_t* a = src + so;
+  int32_t* b = dst + dof;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+}  // namespace
+
+extern "C" int sg_relayout_sample_hdr(const int32_t* src, int32_t* dst, const int64_t* geo, int64_t max_len,
+                                      void* stream) {
+  SG_REQUIRE(src && dst && geo && geo[0] >= 1 && geo[0] <= SG_MAXL && geo[1] == 2 * (2 * geo[0] + 1),
+             "relayout_sample_hdr: bad argument");
+  RelGeo g;
+  memset(&g, 0, sizeof(g));
+  g.L = (int32_t)geo[0];
+  g.S = geo[1]; g.o_V = geo[2]; g.o_es = geo[3]; g.o_ed = geo[4];
+  for (int l = 0; l <= g.L + 1; ++l) g.voff[l] = geo[5 + l];
+  for (int l = 0; l <= g.L; ++l) g.eoff[l] = geo[5 + g.L + 2 + l];
+  dim3 grid(clamp_grid(div_up(std::max<int64_t>(max_len, 1), 4 * 256), kSMs), 3 * g.L + 2);
+  k_relayout_hdr<<<grid, 256, 0, (cudaStream_t)stream>>>(src, dst, g);
+  SG_CHECK_LAUNCH("k_relayout_hdr");
+  return SG_OK;
+}
+
 // The same with the H2D in front: host_src (page-locked, `words` int32) ->
 // stage (device) on `stream`, then the relayout stage -> dst. One host call.
 extern "C" int sg_h2d_relayout_sample(const int32_t* host_src, int64_t words, int32_t* stage, int32_t* dst,

@@ -225,8 +225,7 @@ class PackGeometry:
         self.EC = EC
         self._voff_l = [int(x) for x in self.voff]
         self._eoff_l = [int(x) for x in self.eoff]
-        self._seg = None
-        self._seg_ptrs = None
+        self._relgeo = None
         self.o_V, self.o_es, self.o_ed = self.S, self.S + VC, self.S + VC + EC
         self.words = self.S + VC + 2 * EC
 
@@ -271,37 +270,21 @@ class PackGeometry:
         self.last_vrange = (int(vr[0]), int(vr[1]))
         return used
 
-    def relayout_from_stage(self, sample, pin, stage, buf):
+    def relayout_from_stage(self, sample, pin, stage, buf, nE):
         """A native-sampler sample (PinnedArrays) already sent to the device
         staging buffer by _h2d_pinned: one kernel moves its segments to this
-        layout's offsets in `buf` (sg_relayout_sample). Returns the words used."""
-        nV, nE = sample.sizes()
-        cV, cE = self.cap_nV, self.cap_nE
+        layout's offsets in `buf`, deriving them from the sample's own sizes
+        header on the device (sg_relayout_sample_hdr; the capacity geometry is
+        a cached host array). Returns the words used."""
+        g = self._relgeo
+        if g is None:
+            L = self.L
+            arr = np.array([L, self.S, self.o_V, self.o_es, self.o_ed] + self._voff_l + self._eoff_l,
+                           dtype=np.int64)
+            g = self._relgeo = (arr, arr.ctypes.data, max(self.cap_nV + self.cap_nE + [self.S]))
+        _lib.call("sg_relayout_sample_hdr", stage.data_ptr(), buf.data_ptr(), g[1], g[2], _lib.stream_ptr())
         L = self.L
-        if any(nV[l] > cV[l] for l in range(L + 1)) or any(nE[l] > cE[l] for l in range(L)):
-            raise ValueError("sample exceeds the captured capacities")
-        S, VS, ES = pin.S, pin.VS, pin.ES
-        seg = self._seg
-        if seg is None:
-            seg = self._seg = np.zeros((3, 3 * L + 2), dtype=np.int64)
-            self._seg_ptrs = tuple(seg[i].ctypes.data for i in range(3))
-        so, do, ln = seg[0], seg[1], seg[2]
-        voff, eoff = self._voff_l, self._eoff_l
-        so[0], do[0], ln[0] = 0, 0, S
-        a = S
-        for l in range(L + 1):
-            so[1 + l], do[1 + l], ln[1 + l] = a, self.o_V + voff[l], nV[l]
-            a += nV[l]
-        b = S + VS + ES
-        for l in range(L):
-            k = 2 + L + l
-            so[k], do[k], ln[k] = a, self.o_es + eoff[l], nE[l]
-            so[k + L], do[k + L], ln[k + L] = b, self.o_ed + eoff[l], nE[l]
-            a += nE[l]
-            b += nE[l]
-        _lib.call("sg_relayout_sample", stage.data_ptr(), buf.data_ptr(), 3 * L + 2, *self._seg_ptrs,
-                  _lib.stream_ptr())
-        return self.o_ed + eoff[L - 1] + nE[L - 1] if L else self.o_es
+        return self.o_ed + self._eoff_l[L - 1] + nE[L - 1] if L else self.o_es
 
 
 def _h2d_pinned(pin, device):
@@ -337,15 +320,16 @@ class _InFlight:
 
     def __init__(self):
         self.q = []
+        self.free = []  # completed events, recorded again (no creation per call)
 
     def hold(self, t):
-        ev = torch.cuda.Event()
+        ev = self.free.pop() if self.free else torch.cuda.Event()
         ev.record()
         self.q.append((ev, t))
         while self.q and (len(self.q) > 64 or self.q[0][0].query()):
             if len(self.q) > 64:
                 self.q[0][0].synchronize()
-            self.q.pop(0)
+            self.free.append(self.q.pop(0)[0])
 
 
 _STAGE = _Stage()
@@ -504,8 +488,8 @@ class DeviceSplit:
         nV, nE = sample.sizes()
         geo = PackGeometry.for_sizes(nV, nE, scope=(len(nE), len(pm.assignment), pm.num_devices))
         buf = torch.empty(geo.words, dtype=torch.int32, device=dev)
-        if stage is not None:
-            used = geo.relayout_from_stage(sample, pin, stage, buf)
+        if stage is not None:  # the geometry fits the sizes (for_sizes)
+            used = geo.relayout_from_stage(sample, pin, stage, buf, nE)
             h2d = 4 * (pin.S + pin.VS + 2 * pin.ES)
         else:
             h2d = None

@@ -46,7 +46,7 @@ def split(smp):
     t = tick("geometry", t)
     buf = torch.empty(geo.words, dtype=torch.int32, device="cuda")
     t = tick("empty", t)
-    used = geo.relayout_from_stage(smp, smp.pinned, stage, buf)
+    used = geo.relayout_from_stage(smp, smp.pinned, stage, buf, nE)
     t = tick("relayout", t)
     VC = int(geo.voff[-1])
     ds = DeviceSplit(buf[geo.o_V:geo.o_V + VC], buf[geo.o_es:geo.o_es + geo.EC], buf[geo.o_ed:geo.o_ed + geo.EC],
