@@ -194,8 +194,11 @@ class NativeSampler:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            _lib.load().sg_sampler_destroy(h)
             self._h = None
+            try:
+                _lib.load().sg_sampler_destroy(h)
+            except TypeError:  # interpreter shutdown: module globals already cleared
+                pass
 
     def sample(self, targets, fanouts, seed) -> MiniBatchSample:
         lib = _lib.load()
