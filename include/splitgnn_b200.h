@@ -518,6 +518,12 @@ int sg_partition_coarse_host(int64_t n, const int64_t* off, const int32_t* nbr, 
  * split_minibatch's staging of the sample (scheduler.py:164). */
 int sg_pack_sample(int32_t* out, int32_t L, const int64_t* sizes, const int64_t* dst_off, const void* const* src,
                    const int32_t* elem_bytes, int32_t threads, int64_t* vrange);
+/* sg_sampler_fetch_starts (HOST memory, CPU): sg_sampler_fetch plus the
+ * per-destination run starts of every layer (layers 1..L back to back, |V^l|
+ * ints each) -- the compact form split_minibatch sends instead of the
+ * destination lists (sampling.py:118-177 output, edges grouped per
+ * destination in ascending order). */
+int sg_sampler_fetch_starts(void* h, int32_t* V, int32_t* esrc, int32_t* edst, int32_t* starts);
 /* sg_host_params_gather (HOST memory, CPU): SplitExecutor.run's parameter
  * snapshot (engine.py:95-117): k contiguous arrays (elem_bytes 8 = fp64,
  * 4 = fp32) flattened to fp32 in order into out. */
@@ -666,6 +672,13 @@ int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
  * o_es, o_ed, voff[0..L+1], eoff[0..L]] (host int64, the capacity layout;
  * lengths clamped to it); max_len bounds the longest segment (grid size). */
 int sg_relayout_sample_hdr(const int32_t* src, int32_t* dst, const int64_t* geo, int64_t max_len, void* stream);
+/* Compact form of sg_relayout_sample_hdr: src = [header | V^0..V^L | E^l
+ * sources | per-destination run starts of layers 1..L (|V^l| ints each, first
+ * edge of each destination, ascending)]; the E^l destination lists are
+ * rebuilt from the starts into the capacity layout (the sampler's edge order:
+ * one run per destination). */
+int sg_relayout_sample_compact(const int32_t* src, int32_t* dst, const int64_t* geo, int64_t max_len,
+                               void* stream);
 /* sg_relayout_sample preceded by the H2D of the page-locked host buffer
  * (`words` int32) into the device staging buffer `stage`, both on `stream`. */
 int sg_h2d_relayout_sample(const int32_t* host_src, int64_t words, int32_t* stage, int32_t* dst, int32_t nseg,

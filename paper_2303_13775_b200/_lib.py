@@ -166,6 +166,7 @@ _SIGS = {
     "sg_sampler_destroy": (None, [vp]),
     "sg_sampler_run": (i32, [vp, vp, i64, vp, i32, u64, i32, vp, vp]),
     "sg_sampler_fetch": (i32, [vp, vp, vp, vp]),
+    "sg_sampler_fetch_starts": (i32, [vp, vp, vp, vp, vp]),
     "sg_tspmm_part_floats": (i64, [i64, i32, i32]),
     "sg_sage_scatter_bwd_lb": (i32, [vp, P(SgSplitLayout), i32, i32, i32, vp, vp, vp, i32, vp, vp, vp, vp, i64, i32, vp,
                                      i64, vp, i64, vp]),
@@ -180,6 +181,7 @@ _SIGS = {
     "sg_pipe_stage_direct": (i32, [vp, i32, vp, i64, vp, i64, i32, vp, i64, vp, vp]),
     "sg_relayout_sample": (i32, [vp, vp, i32, vp, vp, vp, vp]),
     "sg_relayout_sample_hdr": (i32, [vp, vp, vp, i64, vp]),
+    "sg_relayout_sample_compact": (i32, [vp, vp, vp, i64, vp]),
     "sg_copy_async": (i32, [vp, vp, i64, vp]),
     "sg_h2d_relayout_sample": (i32, [vp, i64, vp, vp, i32, vp, vp, vp, vp]),
     "sg_pipe_release": (i32, [vp, i32, vp]),

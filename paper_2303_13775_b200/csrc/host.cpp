@@ -305,6 +305,40 @@ extern "C" int sg_sampler_run(void* h, const int64_t* targets, int64_t n_targets
   return SG_OK;
 }
 
+// sg_sampler_fetch plus the per-destination run starts of every layer
+// (starts: layer 1..L back to back, |V^l| ints each; starts[i] = first edge of
+// destination i in E^l -- the sampler emits each destination's edges as one
+// run, destinations ascending, the self edge first, so every run is non-empty).
+extern "C" int sg_sampler_fetch_starts(void* h, int32_t* V, int32_t* esrc, int32_t* edst, int32_t* starts) {
+  Sampler& S = *(Sampler*)h;
+  int64_t o = 0;
+  for (auto& lv : S.layers) {
+    std::memcpy(V + o, lv.data(), lv.size() * 4);
+    o += (int64_t)lv.size();
+  }
+  o = 0;
+  int64_t so = 0;
+  for (size_t l = 0; l < S.es.size(); ++l) {
+    const int64_t m = (int64_t)S.es[l].size();
+    std::memcpy(esrc + o, S.es[l].data(), m * 4);
+    const int32_t* d = S.ed[l].data();
+    int32_t* out = edst + o;
+    int32_t* st = starts + so;
+    int32_t prev = -1;
+    for (int64_t j = 0; j < m; ++j) {
+      const int32_t v = d[j];
+      out[j] = v;
+      if (v != prev) {
+        st[v] = (int32_t)j;
+        prev = v;
+      }
+    }
+    o += m;
+    so += (int64_t)S.layers[l + 1].size();
+  }
+  return SG_OK;
+}
+
 extern "C" int sg_sampler_fetch(void* h, int32_t* V, int32_t* esrc, int32_t* edst) {
   Sampler& S = *(Sampler*)h;
   int64_t o = 0;

@@ -314,6 +314,67 @@ __global__ void k_relayout_hdr(const int32_t* __restrict__ src, int32_t* __restr
 }
 }  // namespace
 
+// Compact form: src = [header | V | es | per-destination run starts of layers
+// 1..L (|V^l| each)]; the destination lists are rebuilt from the starts into
+// the capacity layout (blocks y >= 2L+2: one thread per destination writes its
+// run), the other segments copied as in k_relayout_hdr.
+__global__ void k_relayout_compact(const int32_t* __restrict__ src, int32_t* __restrict__ dst, RelGeo g) {
+  const int seg = blockIdx.y, L = g.L;
+  const int64_t* sz = reinterpret_cast<const int64_t*>(src);
+  int64_t VS = 0, ES = 0;
+  for (int l = 0; l <= L; ++l) VS += sz[l];
+  for (int l = 0; l < L; ++l) ES += sz[L + 1 + l];
+  if (seg < 2 * L + 2) {
+    int64_t so, dof, len;
+    if (seg == 0) {
+      so = 0; dof = 0; len = g.S;
+    } else if (seg <= L + 1) {
+      const int l = seg - 1;
+      so = g.S;
+      for (int k = 0; k < l; ++k) so += sz[k];
+      dof = g.o_V + g.voff[l];
+      len = min(sz[l], g.voff[l + 1] - g.voff[l]);
+    } else {
+      const int l = seg - (L + 2);
+      so = g.S + VS;
+      for (int k = 0; k < l; ++k) so += sz[L + 1 + k];
+      dof = g.o_es + g.eoff[l];
+      len = min(sz[L + 1 + l], g.eoff[l + 1] - g.eoff[l]);
+    }
+    const int32_t* a = src + so;
+    int32_t* b = dst + dof;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
+      b[i] = a[i];
+    return;
+  }
+  const int l = seg - (2 * L + 2);  // E^(l+1): destinations are V^(l+1) positions
+  int64_t so = g.S + VS + ES;
+  for (int k = 0; k < l; ++k) so += sz[k + 1];
+  const int64_t nd = sz[l + 1], ne = min(sz[L + 1 + l], g.eoff[l + 1] - g.eoff[l]);
+  const int32_t* st = src + so;
+  int32_t* ed = dst + g.o_ed + g.eoff[l];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = st[i], e = i + 1 < nd ? (int64_t)st[i + 1] : ne;
+    for (int64_t k = max(b, (int64_t)0); k < min(e, ne); ++k) ed[k] = (int32_t)i;
+  }
+}
+
+extern "C" int sg_relayout_sample_compact(const int32_t* src, int32_t* dst, const int64_t* geo, int64_t max_len,
+                                          void* stream) {
+  SG_REQUIRE(src && dst && geo && geo[0] >= 1 && geo[0] <= SG_MAXL && geo[1] == 2 * (2 * geo[0] + 1),
+             "relayout_sample_compact: bad argument");
+  RelGeo g;
+  memset(&g, 0, sizeof(g));
+  g.L = (int32_t)geo[0];
+  g.S = geo[1]; g.o_V = geo[2]; g.o_es = geo[3]; g.o_ed = geo[4];
+  for (int l = 0; l <= g.L + 1; ++l) g.voff[l] = geo[5 + l];
+  for (int l = 0; l <= g.L; ++l) g.eoff[l] = geo[5 + g.L + 2 + l];
+  dim3 grid(clamp_grid(div_up(std::max<int64_t>(max_len, 1), 4 * 256), kSMs), 3 * g.L + 2);
+  k_relayout_compact<<<grid, 256, 0, (cudaStream_t)stream>>>(src, dst, g);
+  SG_CHECK_LAUNCH("k_relayout_compact");
+  return SG_OK;
+}
+
 extern "C" int sg_relayout_sample_hdr(const int32_t* src, int32_t* dst, const int64_t* geo, int64_t max_len,
                                       void* stream) {
   SG_REQUIRE(src && dst && geo && geo[0] >= 1 && geo[0] <= SG_MAXL && geo[1] == 2 * (2 * geo[0] + 1),

@@ -116,6 +116,13 @@ class PinnedArrays:
     ES: int
     vbound: int
     views: tuple = ()  # the sampler's array objects: V^0..V^L, then (src, dst) per layer
+    RS: int = 0  # run starts after es (compact form; the dst lists are read-only views)
+
+    @property
+    def dma_words(self):
+        """Words split_minibatch sends: [header | V | es | starts] in the
+        compact form, else [header | V | es | ed]."""
+        return self.S + self.VS + self.ES + (self.RS if self.RS else self.ES)
 
     def __reduce__(self):
         # the page-locked buffer and its address belong to this process: a
@@ -137,6 +144,8 @@ class PinnedArrays:
         for l in range(L):
             e = le[l]
             if e[0] is not w[L + 1 + l][0] or e[1] is not w[L + 1 + l][1]:
+                return False
+            if self.RS and e[1].flags.writeable:  # made writable again: may have been edited
                 return False
         return True
 
@@ -213,26 +222,35 @@ class NativeSampler:
                                       int(seed) & (2**64 - 1), self.threads, _lib.ptr(nV),
                                       _lib.ptr(nE)), "sample_minibatch")
         VS, ES = int(nV.sum()), int(nE[:L].sum())
+        RS = VS - int(nV[0])  # one run start per destination of layers 1..L
         S = 2 * (2 * L + 1)  # int64 header of the sizes, as in the capacity layout
-        pin = _pinned_int32(S + VS + 2 * ES) if self.pinned else None
+        pin = _pinned_int32(S + VS + 2 * ES + RS) if self.pinned else None
         if pin is not None:
-            # one DMA-ready buffer [header | V | es | ed]: split_minibatch sends
-            # it to the device as is (no host pack)
+            # one DMA-ready buffer [header | V | es | run starts | ed]:
+            # split_minibatch sends the prefix before ed as is (no host pack)
+            # and the device rebuilds the destination lists from the starts
             buf = pin.numpy()
             buf[:S].view(np.int64)[:] = np.r_[nV, nE[:L]]
+            V, es = buf[S:S + VS], buf[S + VS:S + VS + ES]
+            starts, ed = buf[S + VS + ES:S + VS + ES + RS], buf[S + VS + ES + RS:]
+            _lib.check(lib.sg_sampler_fetch_starts(self._h, _lib.ptr(V), _lib.ptr(es), _lib.ptr(ed),
+                                                   _lib.ptr(starts)), "sampler_fetch")
         else:
-            buf = np.empty(S + VS + 2 * ES, dtype=np.int32)
-        V, es, ed = buf[S:S + VS], buf[S + VS:S + VS + ES], buf[S + VS + ES:]
-        _lib.check(lib.sg_sampler_fetch(self._h, _lib.ptr(V), _lib.ptr(es), _lib.ptr(ed)),
-                   "sampler_fetch")
+            buf = np.empty(VS + 2 * ES, dtype=np.int32)
+            V, es, ed = buf[:VS], buf[VS:VS + ES], buf[VS + ES:]
+            _lib.check(lib.sg_sampler_fetch(self._h, _lib.ptr(V), _lib.ptr(es), _lib.ptr(ed)),
+                       "sampler_fetch")
         vo = np.r_[0, np.cumsum(nV)]
         eo = np.r_[0, np.cumsum(nE[:L])]
         lv = [V[vo[l]:vo[l + 1]] for l in range(L + 1)]
         le = [(es[eo[l]:eo[l + 1]], ed[eo[l]:eo[l + 1]]) for l in range(L)]
+        if pin is not None:
+            for _, d in le:  # the device rebuilds these from the starts: no in-place edits
+                d.flags.writeable = False
         smp = MiniBatchSample(L, lv, le, dst_grouped=True)
         if pin is not None:
             smp.pinned = PinnedArrays(pin, buf.ctypes.data, S, VS, ES, int(self.graph.num_vertices),
-                                      tuple(lv) + tuple(le))
+                                      tuple(lv) + tuple(le), RS)
         return smp
 
 

@@ -275,14 +275,17 @@ class PackGeometry:
         staging buffer by _h2d_pinned: one kernel moves its segments to this
         layout's offsets in `buf`, deriving them from the sample's own sizes
         header on the device (sg_relayout_sample_hdr; the capacity geometry is
-        a cached host array). Returns the words used."""
+        a cached host array); in the compact form the destination lists are
+        rebuilt from the run starts (sg_relayout_sample_compact). Returns the
+        words used."""
         g = self._relgeo
         if g is None:
             L = self.L
             arr = np.array([L, self.S, self.o_V, self.o_es, self.o_ed] + self._voff_l + self._eoff_l,
                            dtype=np.int64)
             g = self._relgeo = (arr, arr.ctypes.data, max(self.cap_nV + self.cap_nE + [self.S]))
-        _lib.call("sg_relayout_sample_hdr", stage.data_ptr(), buf.data_ptr(), g[1], g[2], _lib.stream_ptr())
+        _lib.call("sg_relayout_sample_compact" if pin.RS else "sg_relayout_sample_hdr", stage.data_ptr(),
+                  buf.data_ptr(), g[1], g[2], _lib.stream_ptr())
         L = self.L
         return self.o_ed + self._eoff_l[L - 1] + nE[L - 1] if L else self.o_es
 
@@ -291,7 +294,7 @@ def _h2d_pinned(pin, device):
     """One H2D of a native-sampler sample's pinned buffer into the reused
     device staging buffer (current stream); the pinned buffer stays referenced
     until an event after the copy has completed (_InFlight)."""
-    n = pin.S + pin.VS + 2 * pin.ES
+    n = pin.dma_words
     stage = _STAGE.get(n, device)
     _lib.call("sg_copy_async", stage.data_ptr(), pin.base, 4 * n, _lib.stream_ptr())
     _INFLIGHT.hold(pin.tensor)
@@ -490,7 +493,7 @@ class DeviceSplit:
         buf = torch.empty(geo.words, dtype=torch.int32, device=dev)
         if stage is not None:  # the geometry fits the sizes (for_sizes)
             used = geo.relayout_from_stage(sample, pin, stage, buf, nE)
-            h2d = 4 * (pin.S + pin.VS + 2 * pin.ES)
+            h2d = 4 * pin.dma_words
         else:
             h2d = None
             hb, used = _PINNED.pack(geo, sample)

@@ -331,3 +331,30 @@ def test_pinned_sample_does_not_survive_pickling():
     back = pickle.loads(pickle.dumps(smp))
     assert back.pinned is None
     np.testing.assert_array_equal(back.layer_vertices[0], lv[0])
+
+
+def test_sampler_fetch_starts_are_run_starts():
+    """sg_sampler_fetch_starts (the compact form split_minibatch DMAs): the
+    same V / es / ed as sg_sampler_fetch, and per layer one start per
+    destination = the first index of its run in the ascending destination list."""
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import _lib
+    g = _graph()
+    smp = sg.NativeSampler(g, threads=4, pinned=False)
+    ref = smp.sample(np.arange(0, 20000, 41), [6, 4, 3], seed=5)
+    nV, nE = ref.sizes()
+    V = np.empty(sum(nV), np.int32)
+    es = np.empty(sum(nE), np.int32)
+    ed = np.empty(sum(nE), np.int32)
+    st = np.full(sum(nV[1:]), -1, np.int32)
+    _lib.check(_lib.load().sg_sampler_fetch_starts(smp._h, V.ctypes.data, es.ctypes.data, ed.ctypes.data,
+                                                   st.ctypes.data))
+    np.testing.assert_array_equal(V, np.concatenate(ref.layer_vertices))
+    np.testing.assert_array_equal(es, np.concatenate([a for a, _ in ref.layer_edges]))
+    np.testing.assert_array_equal(ed, np.concatenate([b for _, b in ref.layer_edges]))
+    o = 0
+    for l in range(1, len(nV)):
+        d = ref.layer_edges[l - 1][1]
+        assert np.all(np.diff(d) >= 0)
+        np.testing.assert_array_equal(st[o:o + nV[l]], np.searchsorted(d, np.arange(nV[l]), side="left"))
+        o += nV[l]

@@ -123,6 +123,11 @@ def test_split_from_pinned_sample_matches_packed(monkeypatch):
     graph, pm, cache, feats, labels, samples, params = _workload("graphsage", 3, cache_frac=0.3)
     smp = samples[1]
     assert smp.pinned is not None and smp.pinned.intact(smp)
+    # compact form: only [header | V | es | run starts] crosses PCIe; the
+    # destination lists are rebuilt on the device, so they are read-only here
+    assert smp.pinned.RS > 0 and smp.pinned.dma_words < smp.pinned.S + smp.pinned.VS + 2 * smp.pinned.ES
+    with pytest.raises(ValueError):
+        smp.layer_edges[0][1][0] = 0
 
     def layout(splits):
         buf, used, geo = splits.device_split.packed
@@ -152,6 +157,12 @@ def test_split_from_pinned_sample_matches_packed(monkeypatch):
     other = sg.MiniBatchSample(smp.num_layers, [v.copy() for v in smp.layer_vertices], list(smp.layer_edges),
                                dst_grouped=True, pinned=smp.pinned)
     assert not other.pinned.intact(other)
+    # a destination list made writable again (and so possibly edited) is packed too
+    d = smp.layer_edges[1][1]
+    d.flags.writeable = True
+    assert not smp.pinned.intact(smp)
+    d.flags.writeable = False
+    assert smp.pinned.intact(smp)
     s3, _ = sg.split_minibatch(other, pm, cache)
     np.testing.assert_array_equal(layout(s3), layout(s2))
     # vertices beyond the partition map still raise (packing path checks them)
