@@ -655,19 +655,15 @@ int sg_pipe_stage_direct(void* h, int32_t slot, const void* host_prefix, int64_t
                          const void* host_starts, int64_t starts_bytes, int32_t L, const int64_t* edge_off,
                          int64_t o_ed, void* dev_dst, void* stream);
 int sg_pipe_release(void* h, int32_t slot, void* stream);
-/* split_minibatch for a sample whose arrays the native sampler wrote into one
- * pinned buffer [int64 header of the 2L+1 sizes | V^0..V^L | E^l sources |
- * E^l destinations] (scheduler.py:164 entry; replaces sg_pack_sample's host
- * copy): after one H2D of that buffer to `src`, copy its nseg segments
- * (word offsets src_off -> dst_off, len words) into the capacity layout
- * `dst` on the device. nseg <= 3*SG_MAXL+2. */
-int sg_relayout_sample(const int32_t* src, int32_t* dst, int32_t nseg, const int64_t* src_off,
-                       const int64_t* dst_off, const int64_t* len, void* stream);
 /* One cudaMemcpyAsync (cudaMemcpyDefault: pinned host / device pointers under
  * UVA) on `stream`: SplitExecutor.run's parameter upload (engine.py:95-117
  * executor inputs), sample load and gradient read-back. */
 int sg_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
-/* sg_relayout_sample with the segments derived on the device from the sample's
+/* split_minibatch for a sample the native sampler wrote into one pinned
+ * buffer [int64 header of the 2L+1 sizes | V^0..V^L | E^l sources | E^l
+ * destinations] (scheduler.py:164 entry; replaces sg_pack_sample's host copy):
+ * after one H2D of it to `src`, its 3L+2 segments are copied into the capacity
+ * layout `dst`, the segment bounds derived on the device from the sample's
  * own int64 sizes header (src[0 .. S) words, S = 2(2L+1)): geo = [L, S, o_V,
  * o_es, o_ed, voff[0..L+1], eoff[0..L]] (host int64, the capacity layout;
  * lengths clamped to it); max_len bounds the longest segment (grid size). */
@@ -679,10 +675,6 @@ int sg_relayout_sample_hdr(const int32_t* src, int32_t* dst, const int64_t* geo,
  * one run per destination). */
 int sg_relayout_sample_compact(const int32_t* src, int32_t* dst, const int64_t* geo, int64_t max_len,
                                void* stream);
-/* sg_relayout_sample preceded by the H2D of the page-locked host buffer
- * (`words` int32) into the device staging buffer `stage`, both on `stream`. */
-int sg_h2d_relayout_sample(const int32_t* host_src, int64_t words, int32_t* stage, int32_t* dst, int32_t nseg,
-                           const int64_t* src_off, const int64_t* dst_off, const int64_t* len, void* stream);
 void* sg_pipe_copy_stream(void* h);
 void sg_pipe_destroy(void* h);
 int sg_pipe_stage(void* h, int32_t slot, const void* host_src, int64_t bytes, void* dev_dst,

@@ -179,11 +179,9 @@ _SIGS = {
     "sg_pipe_stage": (i32, [vp, i32, vp, i64, vp, vp]),
     "sg_pipe_finish": (i32, [vp, i32, vp, vp]),
     "sg_pipe_stage_direct": (i32, [vp, i32, vp, i64, vp, i64, i32, vp, i64, vp, vp]),
-    "sg_relayout_sample": (i32, [vp, vp, i32, vp, vp, vp, vp]),
     "sg_relayout_sample_hdr": (i32, [vp, vp, vp, i64, vp]),
     "sg_relayout_sample_compact": (i32, [vp, vp, vp, i64, vp]),
     "sg_copy_async": (i32, [vp, vp, i64, vp]),
-    "sg_h2d_relayout_sample": (i32, [vp, i64, vp, vp, i32, vp, vp, vp, vp]),
     "sg_pipe_release": (i32, [vp, i32, vp]),
     "sg_pipe_copy_stream": (vp, [vp]),
     "sg_pipe_wait": (i32, [vp, i32, vp]),

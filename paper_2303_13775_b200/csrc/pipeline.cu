@@ -223,48 +223,6 @@ extern "C" int sg_pipe_wait(void* h, int32_t slot, float* loss_out) {
   return SG_OK;
 }
 
-// split_minibatch's direct path (a sampler-pinned sample, no host pack): the
-// sample's contiguous [header | V | es | ed] arrived with one H2D; its 3L+2
-// segments are moved to their word offsets in the capacity layout (one kernel,
-// blockIdx.y = segment).
-namespace {
-constexpr int kMaxSeg = 3 * SG_MAXL + 2;
-struct Segs {
-  int32_t n;
-  int64_t src[kMaxSeg], dst[kMaxSeg], len[kMaxSeg];
-};
-__global__ void k_relayout(const int32_t* __restrict__ src, int32_t* __restrict__ dst, Segs s) {
-  const int seg = blockIdx.y;
-  const int64_t len = s.len[seg];
-  const int32_t* a = src + s.src[seg];
-  int32_t* b = dst + s.dst[seg];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (int64_t)gridDim.x * blockDim.x)
-    b[i] = a[i];
-}
-}  // namespace
-
-extern "C" int sg_relayout_sample(const int32_t* src, int32_t* dst, int32_t nseg, const int64_t* src_off,
-                                  const int64_t* dst_off, const int64_t* len, void* stream) {
-  SG_REQUIRE(src && dst && src_off && dst_off && len && nseg >= 0 && nseg <= kMaxSeg,
-             "relayout_sample: bad argument");
-  Segs s;
-  memset(&s, 0, sizeof(s));
-  s.n = nseg;
-  int64_t mx = 0;
-  for (int i = 0; i < nseg; ++i) {
-    SG_REQUIRE(src_off[i] >= 0 && dst_off[i] >= 0 && len[i] >= 0, "relayout_sample: negative offset/length");
-    s.src[i] = src_off[i];
-    s.dst[i] = dst_off[i];
-    s.len[i] = len[i];
-    mx = std::max(mx, len[i]);
-  }
-  if (nseg == 0 || mx == 0) return SG_OK;
-  dim3 grid(clamp_grid(div_up(mx, 4 * 256), kSMs), nseg);
-  k_relayout<<<grid, 256, 0, (cudaStream_t)stream>>>(src, dst, s);
-  SG_CHECK_LAUNCH("k_relayout");
-  return SG_OK;
-}
-
 // One async copy in any direction (UVA: pinned host <-> device, device <->
 // device) on `stream`: the executor's parameter upload, sample load and
 // gradient read-back, without a framework dispatch per copy.
@@ -274,7 +232,10 @@ extern "C" int sg_copy_async(void* dst, const void* src, int64_t bytes, void* st
   return SG_OK;
 }
 
-// Header-driven form: the segments are derived on the device from the int64
+// split_minibatch's direct path (a native-sampler sample in one pinned
+// buffer, no host pack): after one H2D of [header | V | es | ed], its 3L+2
+// segments are moved to their word offsets in the capacity layout (one kernel,
+// blockIdx.y = segment). The segments are derived on the device from the int64
 // sizes header the sample carries (stage[0 .. S)), so the host passes only the
 // capacity geometry (cached per geometry): geo = [L, S, o_V, o_es, o_ed,
 // voff[0..L+1], eoff[0..L]] (int64, host memory, read at launch). Lengths are
@@ -391,15 +352,5 @@ extern "C" int sg_relayout_sample_hdr(const int32_t* src, int32_t* dst, const in
   return SG_OK;
 }
 
-// The same with the H2D in front: host_src (page-locked, `words` int32) ->
-// stage (device) on `stream`, then the relayout stage -> dst. One host call.
-extern "C" int sg_h2d_relayout_sample(const int32_t* host_src, int64_t words, int32_t* stage, int32_t* dst,
-                                      int32_t nseg, const int64_t* src_off, const int64_t* dst_off,
-                                      const int64_t* len, void* stream) {
-  SG_REQUIRE(host_src && stage && words >= 0, "h2d_relayout_sample: bad argument");
-  if (words > 0)
-    SG_CUDA(cudaMemcpyAsync(stage, host_src, (size_t)words * 4, cudaMemcpyHostToDevice, (cudaStream_t)stream));
-  return sg_relayout_sample(stage, dst, nseg, src_off, dst_off, len, stream);
-}
 
 }  // namespace sg
