@@ -198,3 +198,54 @@ def test_host_sgd_matches_device_sgd(g):
     b = engine._host_flat(p_dev)
     ulp = np.abs(a.view(np.int32).astype(np.int64) - b.view(np.int32).astype(np.int64))
     assert ulp.max() <= 1 and np.count_nonzero(ulp) <= max(1, a.size // 1000), (ulp.max(), np.count_nonzero(ulp))
+
+
+def test_split_from_pinned_full_form_matches_packed(monkeypatch):
+    """The non-compact pinned form ([header | V | es | ed], no run starts:
+    sg_relayout_sample_hdr) gives the same device layout as packing."""
+    import torch
+    import paper_2303_13775_b200 as sg
+    from paper_2303_13775_b200 import scheduler
+    from paper_2303_13775_b200.sampling import PinnedArrays
+    graph, pm, cache, feats, labels, samples, params = _workload("graphsage", 2)
+    src = samples[2]
+    nV, nE = src.sizes()
+    L = len(nE)
+    S, VS, ES = 2 * (2 * L + 1), sum(nV), sum(nE)
+    t = torch.empty(S + VS + 2 * ES, dtype=torch.int32, pin_memory=True)
+    buf = t.numpy()
+    buf[:S].view(np.int64)[:] = nV + nE
+    o = S
+    lv = []
+    for v in src.layer_vertices:
+        buf[o:o + len(v)] = v
+        lv.append(buf[o:o + len(v)])
+        o += len(v)
+    es, ed = [], []
+    for a, _ in src.layer_edges:
+        buf[o:o + len(a)] = a
+        es.append(buf[o:o + len(a)])
+        o += len(a)
+    for _, b in src.layer_edges:
+        buf[o:o + len(b)] = b
+        ed.append(buf[o:o + len(b)])
+        o += len(b)
+    le = list(zip(es, ed))
+    smp = sg.MiniBatchSample(L, lv, le, dst_grouped=True)
+    smp.pinned = PinnedArrays(t, buf.ctypes.data, S, VS, ES, graph.num_vertices, tuple(lv) + tuple(le))
+    assert smp.pinned.intact(smp) and smp.pinned.RS == 0
+    s1, _ = sg.split_minibatch(smp, pm, cache)
+    monkeypatch.setattr(scheduler, "_DIRECT", False)
+    s2, _ = sg.split_minibatch(smp, pm, cache)
+    torch.cuda.synchronize()
+    b1, u1, geo = s1.device_split.packed
+    b2, u2, _ = s2.device_split.packed
+    assert u1 == u2 and s1.device_split.h2d_bytes == 4 * (S + VS + 2 * ES)
+    h1, h2 = b1[:u1].cpu().numpy(), b2[:u2].cpu().numpy()
+    for a, n in [(0, geo.S)] + [(geo.o_V + geo.voff[l], nV[l]) for l in range(L + 1)] + \
+            [(geo.o_es + geo.eoff[l], nE[l]) for l in range(L)] + [(geo.o_ed + geo.eoff[l], nE[l]) for l in range(L)]:
+        np.testing.assert_array_equal(h1[a:a + n], h2[a:a + n])
+    for a, b in zip(s1, s2):
+        np.testing.assert_array_equal(a.load_gids, b.load_gids)
+        for l in range(len(a.owned_gids)):
+            np.testing.assert_array_equal(a.owned_gids[l], b.owned_gids[l])
