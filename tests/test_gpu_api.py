@@ -114,7 +114,7 @@ def test_api_partial_cache():
 
 def test_split_from_pinned_sample_matches_packed(monkeypatch):
     """A native-sampler sample lives in one pinned buffer and reaches the
-    device with one H2D + sg_relayout_sample (no host pack): the device layout,
+    device with one H2D + sg_relayout_sample_compact (no host pack): the device layout,
     the split's host views and the plan equal those of the packing path; a
     sample whose arrays were replaced falls back to packing."""
     import torch
