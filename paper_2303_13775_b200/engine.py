@@ -1064,12 +1064,14 @@ def scatter_shuffle_forward(splits, plan, l, owned_rows, runner=None, record=Non
 
 
 def allreduce_and_step(params, per_device_grads, lr, num_targets):
-    """engine.py:633-647: device-order gradient sum + SGD, on the GPU.
+    """engine.py:633-647: device-order gradient sum + SGD.
     Mutates `params` (host ModelParams, reference semantics) and returns the
-    summed gradients (built on the host on first access). Gradients from a
-    SplitExecutor run carry the device copy of the parameters they were
-    computed with: when `params` still holds those values, the step runs on
-    that copy and only the updated parameters come back (one D2H)."""
+    summed gradients (reference dicts built on first access). Gradients from a
+    captured SplitExecutor run are already on the host (one D2H with the
+    loss): when `params` still holds the values the run used, one native call
+    sums them and applies the step in place (sg_host_sum_sgd, the device
+    kernel's arithmetic). Otherwise the sum + SGD run on the GPU
+    (sg_sum_sgd) and the updated parameters come back with one D2H."""
     if isinstance(params, DeviceParams):
         dp = params
         host_params = None
