@@ -822,9 +822,9 @@ class SplitExecutor:
 
     Samples from split_minibatch (destination-grouped, i.e. every sampler's
     output) run as a replay of a cached CUDA graph of the whole step (split
-    included; SG_API_EAGER=1 forces the eager kernels); gradients stay on the
-    device until a caller reads them, and allreduce_and_step applies the SGD
-    step on the device copy of the parameters."""
+    included; SG_API_EAGER=1 forces the eager kernels); the per-device
+    gradients and the loss return in one pinned D2H, and allreduce_and_step
+    applies the device-order sum + SGD to the host parameters."""
 
     def __init__(self, params, splits, plan, features, labels, runner=None, record=None):
         ds = getattr(splits, "device_split", None) or getattr(plan, "device_split", None)
