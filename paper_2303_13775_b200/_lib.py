@@ -240,10 +240,22 @@ def ptr(t):
     return t.data_ptr()
 
 
+_RAW_STREAM = None
+
+
 def stream_ptr(stream=None):
-    import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    """cudaStream_t of `stream` or of torch's current stream on the current
+    device (read through torch's raw-stream query: building a Stream object
+    costs ~3 us per call, and the hot paths call this several times a step)."""
+    global _RAW_STREAM
+    if stream is not None:
+        return stream.cuda_stream
+    if _RAW_STREAM is None:
+        import torch
+        raw, dev = getattr(torch._C, "_cuda_getCurrentRawStream", None), getattr(torch._C, "_cuda_getDevice", None)
+        _RAW_STREAM = (lambda: raw(dev())) if raw is not None and dev is not None else \
+            (lambda: torch.cuda.current_stream().cuda_stream)
+    return _RAW_STREAM()
 
 
 def launch_count():

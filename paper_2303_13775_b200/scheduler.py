@@ -309,8 +309,11 @@ class _Stage:
         self.t = None
 
     def get(self, n, device):
-        if device.type == "cuda" and device.index is None:
-            device = torch.device("cuda", torch.cuda.current_device())
+        idx = device.index if device.index is not None else torch._C._cuda_getDevice()
+        t = self.t
+        if t is not None and t.numel() >= n and t.device.index == idx:
+            return t
+        device = torch.device("cuda", idx)
         if self.t is None or self.t.numel() < n or self.t.device != device:
             self.t = torch.empty(max(int(n * 1.25), 1 << 16), dtype=torch.int32, device=device)
         return self.t
