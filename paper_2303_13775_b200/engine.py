@@ -842,8 +842,7 @@ class SplitExecutor:
         self.g = ds.g
         self.L = params.num_layers
         F = int(np.asarray(features).shape[1]) if not isinstance(features, FeatureStore) else 0
-        t = params.tensors()
-        hid = int(np.shape(t["layer0.w_self" if params.kind == "graphsage" else "layer0.w"])[1]) if self.L else 0
+        hid = int(np.shape(_param_arrays(params)[0])[1]) if self.L else 0  # layer0.w_self / layer0.w
         pad = (params.kind == "graphsage" and self.L >= 2 and 64 < F <= 128 and F % 4 == 0
                and hid in (4, 8, 16, 32))  # wide layer 1 read in whole 128 B lines
         self.feats = _feature_store(features, ds.cache, ds.device, pad_rows=pad)
@@ -1759,10 +1758,11 @@ def _api_graph(params, ds, feats, labels):
     """Cached _ApiGraphStep for this model shape / capacity bucket (LRU of 8;
     the entries hold the partition, cache, feature store and labels they were
     captured with, so their ids stay unique while cached)."""
-    t = params.tensors()
     geo = ds.packed[2]
-    key = (params.kind, tuple(t.keys()), tuple(np.shape(v) for v in t.values()), float(params.leaky_slope),
-           id(ds.pm), id(ds.cache), id(feats), labels.data_ptr(), tuple(geo.cap_nV), tuple(geo.cap_nE), str(ds.device))
+    # parameter names follow from (kind, layer count); shapes from the arrays
+    key = (params.kind, len(params.layers), tuple(np.shape(v) for v in _param_arrays(params)),
+           float(params.leaky_slope), id(ds.pm), id(ds.cache), id(feats), labels.data_ptr(), tuple(geo.cap_nV),
+           tuple(geo.cap_nE), ds.device)
     gs = _API_GRAPHS.pop(key, None)
     if gs is None:
         dp = DeviceParams.from_host(params, ds.device)

@@ -403,7 +403,7 @@ class DeviceSplit:
     receive slots (recv_off, owner-major)."""
 
     def __init__(self, V, esrc, edst, nV, nE, pm: PartitionMap, cache: CacheState | None,
-                 dst_grouped: bool, device=None, host_V=None, sizes=None, defer=False):
+                 dst_grouped: bool, device=None, host_V=None, sizes=None, defer=False, views=None):
         """nV / nE are the CAPACITIES the layout is built for; `sizes` (device
         int64 [nV_0..nV_L, nE_1..nE_L]) gives the actual sizes (default: the
         capacities). V / esrc / edst hold layer l at the capacity offsets.
@@ -431,14 +431,17 @@ class DeviceSplit:
                 _LAYOUTS.clear()
             _LAYOUTS[key] = lay
         self.lay = lay
-        self.V, self.esrc, self.edst = V, esrc, edst
+        if views is None:
+            self.V, self.esrc, self.edst = V, esrc, edst
+            self.sizes = sizes
+        else:  # (V, esrc, edst, sizes) built on first access (__getattr__)
+            self._views_fn = views
         self._host_V = host_V
         n = len(pm.assignment)
         if cache is not None and getattr(cache, "_all", None) is None:
             cache._all = cache.covers_all(n)
         self._flags = (1 if self.dst_grouped else 0) | (2 if cache is not None and cache._all else 0)
         self.all_cached = bool(self._flags & 2)
-        self.sizes = sizes
         self.packed = None
         self._meta = None
         self._views = None
@@ -458,10 +461,15 @@ class DeviceSplit:
         self.ws = ws
 
     def __getattr__(self, name):
-        # only reached for attributes not set yet: the deferred workspace
-        if name == "ws" and "lay" in self.__dict__:
+        # only reached for attributes not set yet: the deferred sample views
+        # and workspace
+        d = self.__dict__
+        if name in ("V", "esrc", "edst", "sizes") and "_views_fn" in d:
+            d["V"], d["esrc"], d["edst"], d["sizes"] = d.pop("_views_fn")()
+            return d[name]
+        if name == "ws" and "lay" in d:
             self._run_split()
-            return self.__dict__["ws"]
+            return d["ws"]
         raise AttributeError(name)
 
     @property
@@ -506,9 +514,10 @@ class DeviceSplit:
             buf[:used].copy_(hb[:used], non_blocking=True)
             _PINNED.record()
         VC = int(geo.voff[-1])
-        V = buf[geo.o_V:geo.o_V + VC]
-        es = buf[geo.o_es:geo.o_es + geo.EC]
-        ed = buf[geo.o_ed:geo.o_ed + geo.EC]
+
+        def views():  # built on first use: the captured executor path reads only `packed`
+            return (buf[geo.o_V:geo.o_V + VC], buf[geo.o_es:geo.o_es + geo.EC], buf[geo.o_ed:geo.o_ed + geo.EC],
+                    buf[:geo.S].view(torch.int64))
 
         def host_V():
             out = np.zeros(VC, dtype=np.int32)
@@ -516,8 +525,8 @@ class DeviceSplit:
                 out[geo.voff[l]:geo.voff[l] + len(v)] = v
             return out
 
-        ds = cls(V, es, ed, geo.cap_nV, geo.cap_nE, pm, cache, True, dev, host_V=host_V,
-                 sizes=buf[:geo.S].view(torch.int64), defer=defer)
+        ds = cls(None, None, None, geo.cap_nV, geo.cap_nE, pm, cache, True, dev, host_V=host_V, defer=defer,
+                 views=views)
         ds.packed = (buf, used, geo)
         ds.h2d_bytes = h2d if h2d is not None else 4 * used  # what crossed PCIe for this sample
         ds.num_targets = len(sample.targets)
