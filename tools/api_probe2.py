@@ -49,9 +49,9 @@ def split(smp):
     used = geo.relayout_from_stage(smp, smp.pinned, stage, buf, nE)
     t = tick("relayout", t)
     VC = int(geo.voff[-1])
-    ds = DeviceSplit(buf[geo.o_V:geo.o_V + VC], buf[geo.o_es:geo.o_es + geo.EC], buf[geo.o_ed:geo.o_ed + geo.EC],
-                     geo.cap_nV, geo.cap_nE, pm, cache, True, torch.device("cuda"), host_V=None,
-                     sizes=buf[:geo.S].view(torch.int64), defer=True)
+    ds = DeviceSplit(None, None, None, geo.cap_nV, geo.cap_nE, pm, cache, True, torch.device("cuda"), host_V=None,
+                     defer=True, views=lambda: (buf[geo.o_V:geo.o_V + VC], buf[geo.o_es:geo.o_es + geo.EC],
+                                                buf[geo.o_ed:geo.o_ed + geo.EC], buf[:geo.S].view(torch.int64)))
     ds.packed = (buf, used, geo)
     ds.num_targets = len(smp.targets)
     t = tick("DeviceSplit", t)
