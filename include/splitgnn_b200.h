@@ -531,7 +531,8 @@ int sg_host_params_gather(int32_t k, const void* const* ptrs, const int64_t* siz
                           float* out);
 /* sg_host_sum_sgd (HOST memory, CPU): allreduce_and_step (engine.py:633-647,
  * models.py:95-99) for gradients already on the host. If the k parameter
- * arrays still equal `snapshot` (nullable: skip the check): total_out = the g
+ * arrays, rounded to fp32, still equal `snapshot` bit for bit (nullable: skip
+ * the check): total_out = the g
  * flat fp32 gradients (n each) summed in device order, and every parameter
  * p <- fp32(p - scale * total), the product exact and rounded once (the device
  * kernel's fused multiply-add), written back in the array's element type;

@@ -704,20 +704,24 @@ extern "C" int sg_host_sum_sgd(int32_t k, void* const* ptrs, const int64_t* size
     return SG_ERR_ARG;
   }
   *applied = 0;
-  if (snapshot) {  // unchanged since the run?
+  if (snapshot) {  // unchanged since the run? (bit compare, branch-free: vectorised)
+    auto bits = [](float x) {
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      return u;
+    };
     int64_t o = 0;
     for (int32_t i = 0; i < k; ++i) {
       const int64_t m = sizes[i];
+      uint32_t diff = 0;
       if (elem_bytes[i] == 8) {
         const double* s = (const double*)ptrs[i];
-        for (int64_t j = 0; j < m; ++j)
-          if ((float)s[j] != snapshot[o + j] && !(std::isnan((float)s[j]) && std::isnan(snapshot[o + j])))
-            return SG_OK;
+        for (int64_t j = 0; j < m; ++j) diff |= bits((float)s[j]) ^ bits(snapshot[o + j]);
       } else {
         const float* s = (const float*)ptrs[i];
-        for (int64_t j = 0; j < m; ++j)
-          if (s[j] != snapshot[o + j] && !(std::isnan(s[j]) && std::isnan(snapshot[o + j]))) return SG_OK;
+        for (int64_t j = 0; j < m; ++j) diff |= bits(s[j]) ^ bits(snapshot[o + j]);
       }
+      if (diff) return SG_OK;
       o += m;
     }
   }
