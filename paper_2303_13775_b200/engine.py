@@ -741,7 +741,10 @@ class _PinnedFlat:
             self.ev.synchronize()
 
     def record(self):
-        self.ev = torch.cuda.Event()
+        # one event per buffer, re-recorded: every rewrite of the buffer waits
+        # for the latest copy first, so only the latest record matters
+        if self.ev is None:
+            self.ev = torch.cuda.Event()
         self.ev.record()
 
 
