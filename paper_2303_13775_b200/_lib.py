@@ -258,5 +258,20 @@ def stream_ptr(stream=None):
     return _RAW_STREAM()
 
 
+_STREAM_OBJ = [None, None]  # ((device, raw cudaStream_t), torch Stream)
+
+
+def current_stream():
+    """torch's current Stream object, reused while the current device and its
+    raw current stream are unchanged (torch.cuda.current_stream() builds a new
+    object per call, ~3 us; Event.record() without a stream calls it)."""
+    import torch
+    key = (torch._C._cuda_getDevice(), stream_ptr())
+    if _STREAM_OBJ[0] != key or _STREAM_OBJ[1] is None:
+        _STREAM_OBJ[1] = torch.cuda.current_stream()
+        _STREAM_OBJ[0] = key
+    return _STREAM_OBJ[1]
+
+
 def launch_count():
     return int(load().sg_launch_count())

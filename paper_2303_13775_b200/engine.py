@@ -745,7 +745,7 @@ class _PinnedFlat:
         # for the latest copy first, so only the latest record matters
         if self.ev is None:
             self.ev = torch.cuda.Event()
-        self.ev.record()
+        self.ev.record(_lib.current_stream())
 
 
 def _pinned_of(dp, which, shape=None):

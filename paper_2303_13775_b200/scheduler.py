@@ -330,7 +330,7 @@ class _InFlight:
 
     def hold(self, t):
         ev = self.free.pop() if self.free else torch.cuda.Event()
-        ev.record()
+        ev.record(_lib.current_stream())
         self.q.append((ev, t))
         while self.q and (len(self.q) > 64 or self.q[0][0].query()):
             if len(self.q) > 64:
